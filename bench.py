@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Moshpit averaging-round benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+                    [--config C2] [--kernel auto|register|bulk] [--no-e2e] [--no-cpu]
+
+Metric: peer-vector GB/s averaged per Moshpit round = N_peers * D * 4 B /
+t_round (BASELINE.json).  One *step* = one Moshpit round (host draws ->
+kernel 1 group formation -> kernel 2 segmented group mean, in place) over the
+resident fp32 peer state.  Default workload = configs[1] (C2: 1024 peers on a
+32x32 grid, D = 2^22 fp32, 1% per-round peer failure), which fits one B200
+(17.2 GB); the state is 136x the 126 MB L2, so no L2 flush is needed between
+rounds.  Synthetic, counter-initialised data.
+
+Multi-GPU (torchrun, one rank per GPU): coordinate-sharded weak scaling --
+every rank owns the full C2 peer set over its own D-slab (coordinates are
+independent; no data-path collective), host draws identical on
+every rank.  value = sum over ranks / max-over-ranks time.
+
+--impl reference: the unmodified reference run_moshpit (oracle/_ref, compiled
+from the reference headers) on bounded column slices of the same workload on
+all host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (M, d, N, D, p, rounds-of-the-config)
+    "C1": (16, 2, 256, 1 << 20, 0.0, 2),
+    "C2": (32, 2, 1024, 1 << 22, 0.01, 10),
+    "C3slab": (16, 3, 4096, 1 << 22, 0.0, 3),
+    "C5slab": (8, 4, 4096, 1 << 22, 0.0, 4),
+}
+PROTOCOL_SEED = 7
+INIT_SEED = 0x5EED
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(kernel_name, cfg_name):
+    """dram bytes per launch of the top kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            s = json.load(f)
+        ent = s["kernels"][kernel_name][cfg_name]
+        return ent["dram_bytes_per_launch"], ent
+    except Exception:  # noqa: BLE001
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline: unmodified run_moshpit on column slices
+# ---------------------------------------------------------------------------
+def cpu_reference(cfg_name, budget_s, threads=None):
+    from oracle.oracle import REF_SO, Checker
+    M, d, N, D, p, R = CONFIGS[cfg_name]
+    threads = threads or len(os.sched_getaffinity(0))
+    kind = "reference"
+    if os.path.exists(REF_SO):
+        chk = Checker("ref")
+    else:
+        chk = None
+        kind = "port"
+    width = 64
+    if chk is None:  # the C restatement, single-threaded, as the port baseline
+        from oracle.oracle import Checker as Ck
+        o = Ck("oracle")
+        import numpy as np
+        x = o.init_state(INIT_SEED, N, width, dtype=np.float64)
+        t0 = time.perf_counter()
+        o.run_moshpit(M, d, x, p, PROTOCOL_SEED, R)
+        run_s = time.perf_counter() - t0
+        return dict(kind="port", cores=1, run_s=run_s, cols=width, rounds=R, N=N, D=D,
+                    sample=f"oracle port, 1 thread, {width} of {D} columns, {R} rounds")
+    # calibrate on one slice per thread
+    run_s, _, _ = chk.slice_bench(M, d, N, width, threads, 0, INIT_SEED, PROTOCOL_SEED, p, R,
+                                  threads)
+    per_slice_batch = max(run_s, 1e-3)
+    batches = max(1, int(budget_s / per_slice_batch))
+    slices = threads * batches
+    run_s, init_s, _ = chk.slice_bench(M, d, N, width, slices, 0, INIT_SEED, PROTOCOL_SEED, p, R,
+                                       threads)
+    cols = slices * width
+    return dict(kind=kind, cores=threads, run_s=run_s, init_s=init_s, cols=cols, rounds=R, N=N,
+                D=D, sample=(f"unmodified run_moshpit (incl. record_round) on {slices} column "
+                             f"slices x {width} = {cols} of D={D} coordinates, {R} rounds, "
+                             f"{threads} threads; cost linear in D (coordinates independent)"))
+
+
+def cpu_value(res):
+    gbs = res["N"] * res["cols"] * 4 * res["rounds"] / res["run_s"] / 1e9
+    ms_round_full = res["run_s"] / res["rounds"] * (res["D"] / res["cols"]) * 1e3
+    return gbs, ms_round_full
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cfg = args.config
+    M, d, N, D, p, R = CONFIGS[cfg]
+    per_step = float(os.environ.get("MOSHPIT_REF_STEP_S", "4"))
+    vals, mss = [], []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference(cfg, per_step)
+        g, ms = cpu_value(res)
+        if i >= args.warmup:
+            vals.append(g)
+            mss.append(ms)
+    value = sum(vals) / len(vals)
+    line = {
+        "impl": "reference", "metric": "peer-vector GB/s averaged per Moshpit round",
+        "value": round(value, 6), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sum(mss) / len(mss), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
+        "config": workload_config(cfg, args),
+        "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, args):
+    M, d, N, D, p, R = CONFIGS[cfg]
+    return {"workload": f"{cfg}: Moshpit All-Reduce round, {N} peers on {M}^{d} grid, "
+                        f"D={D} fp32 per peer, p_fail={p}; step = one round",
+            "peers": N, "grid": f"{M}^{d}", "dim": D, "p_round": p, "protocol_seed": PROTOCOL_SEED,
+            "l2": "state >> 126 MB L2 (no flush needed)", "kernel": args.kernel}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_mine(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_03239_b200 as mb
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        log(f"--gpus {args.gpus} requested without torchrun; running 1 rank")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = args.config
+    M, d, N, D, p, Rcfg = CONFIGS[cfg]
+    kernel = {"auto": 0, "register": 1, "bulk": 2}[args.kernel]
+    stream = torch.cuda.current_stream()
+
+    x = torch.empty((N, D), dtype=torch.float32, device="cuda")
+    # each rank owns its own D-slab of the (D * world)-coordinate problem
+    mb.fill_synthetic(x, INIT_SEED, col0=rank * D)
+    eng = mb.Engine(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
+                    device=local, kernel=kernel)
+    for _ in range(args.warmup):
+        eng.round(x)
+    torch.cuda.synchronize()
+    r0, rows0 = eng.stats()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    eng.set_timing(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        eng.round(x)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    k_ms, k_launches = eng.kernel_time()
+    eng.set_timing(False)
+    r1, rows1 = eng.stats()
+    active_rows = rows1 - rows0
+
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = tt.item()
+
+    state_bytes = N * D * 4
+    value = world * state_bytes * args.steps / (t_max / 1e3) / 1e9
+    alg_bytes = 2 * 4 * D * active_rows  # kernel 2 reads+writes every active row once
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+    peak, peak_src = peaks()
+    traffic, traffic_ent = load_traffic("group_mean_register", cfg)
+    launches_per_step = 2  # kernel 1 (group formation) + kernel 2 (group mean)
+
+    del x
+    torch.cuda.empty_cache()
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = measure_e2e(mb, cfg)
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        try:
+            res = cpu_reference(cfg, float(os.environ.get("MOSHPIT_CPU_BUDGET_S", "15")))
+            g, _ = cpu_value(res)
+            cpu = {"value": round(g, 6), "unit": "GB/s", "cores": res["cores"],
+                   "kind": res["kind"], "sample": res["sample"]}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
+            "config": dict(workload_config(cfg, args),
+                           parallelism=(f"coordinate-sharded x{world} (each rank: all {N} peers "
+                                        f"x its own D-slab; no exchange)") if world > 1
+                           else "single GPU"),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None,
+                         "traffic": traffic, "kernel": "group_mean_register (kernel 2)",
+                         "algorithmic_bytes": "2 * 4 B * D * rows in non-voided groups",
+                         "avg_launch_ms": round(k_ms / max(k_launches, 1), 4),
+                         "launches": k_launches, "active_rows_timed": active_rows,
+                         "peak_source": peak_src},
+            "kernel2_share_of_step": round(k_ms / t_ms, 4) if t_ms > 0 else None,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+    return 0
+
+
+def measure_e2e(mb, cfg):
+    """The reference-facing call (run_moshpit through the C ABI) with HOST
+    buffers: H2D of the initial state, R rounds + TrialReport diagnostics,
+    D2H of the final vectors, all inside the timed region."""
+    import numpy as np
+    import torch
+    M, d, N, D, p, R = CONFIGS[cfg]
+    host = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
+    xh = host.numpy()
+    # fill the pinned buffer from the device init (same synthetic data)
+    for i0 in range(0, N, 64):
+        blk = torch.empty((min(64, N - i0), D), dtype=torch.float32, device="cuda")
+        mb.fill_synthetic(blk, INIT_SEED)
+        host[i0:i0 + blk.shape[0]].copy_(blk)  # row ids restart per block: fine for timing
+    torch.cuda.synchronize()
+    import ctypes as C
+    from paper_2103_03239_b200 import _capi
+    lib = _capi.lib()
+    dist_ = np.zeros(R)
+    drift = np.zeros(R)
+    act = np.zeros(R, dtype=np.uint32)
+    init_d, cost = C.c_double(0), C.c_double(0)
+    ptr = xh.ctypes.data_as(C.c_void_p)
+    t0 = time.perf_counter()
+    _capi.check(lib.moshpit_run_moshpit(_capi.F32, M, d, R, ptr, N, D, p, PROTOCOL_SEED, R,
+                                        _capi.DIAG_FAST, C.byref(init_d),
+                                        dist_.ctypes.data_as(C.c_void_p),
+                                        drift.ctypes.data_as(C.c_void_p),
+                                        act.ctypes.data_as(C.c_void_p), C.byref(cost), ptr))
+    t = time.perf_counter() - t0
+    bytes_ = N * D * 4
+    return {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
+            "call": f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, pinned",
+            "seconds": round(t, 4), "final_distortion": float(dist_[-1])}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup < 3 is not allowed by the timing rules; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_mine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

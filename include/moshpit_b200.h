@@ -1,0 +1,186 @@
+/*
+ * moshpit_b200.h -- C ABI of the B200-native Moshpit averaging engine.
+ *
+ * The reference (arXiv 2103.03239 "moshpit-lab", proj/include/moshpit/) is a
+ * header-only C++20 library with no FFI: its drop-in boundary is the header
+ * API.  Each entry point below replaces one reference function (cited
+ * file:line, relative to proj/include/moshpit/); the C++ header
+ * include/moshpit_b200/moshpit.hpp re-exposes them under the reference's own
+ * namespaces, signatures and exception types, and INTEGRATION.md shows the
+ * bindings (C++ header swap, Python ctypes) a maintainer would add.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / CUDA types in signatures
+ *    (CUDA streams travel as `void*` = cudaStream_t, device buffers as void*);
+ *  - every function returns MOSHPIT_OK (0) or a negative status whose class
+ *    maps 1:1 onto the reference's exception types; moshpit_last_error()
+ *    returns the message (thread-local);
+ *  - reentrant: no global mutable state besides the thread-local message;
+ *    one moshpit_engine per calling thread;
+ *  - compute entry points run on the GPU (sm_100a kernels).  There is no CPU
+ *    fallback: without a usable device they return MOSHPIT_ERR_CUDA.
+ *    Pure-host helpers (rng, key arithmetic) are marked [host].
+ */
+#ifndef MOSHPIT_B200_H
+#define MOSHPIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOSHPIT_OK 0
+#define MOSHPIT_ERR_INVALID_ARGUMENT (-1) /* std::invalid_argument */
+#define MOSHPIT_ERR_OUT_OF_RANGE (-2)     /* std::out_of_range */
+#define MOSHPIT_ERR_RUNTIME (-3)          /* std::runtime_error */
+#define MOSHPIT_ERR_CUDA (-4)             /* device / driver failure */
+
+#define MOSHPIT_F32 0 /* peer state in float (performance path) */
+#define MOSHPIT_F64 1 /* peer state in double (bit parity with the reference) */
+
+/* TrialReport diagnostics (protocols.hpp:68-84 record_round). */
+#define MOSHPIT_DIAG_NONE 0  /* skip: the averaging round alone */
+#define MOSHPIT_DIAG_FAST 1  /* fixed-order blocked fp64 sums (tolerance) */
+#define MOSHPIT_DIAG_EXACT 2 /* the reference's summation order (bit parity) */
+
+/* Group-mean kernel variants. */
+#define MOSHPIT_KERNEL_AUTO 0
+#define MOSHPIT_KERNEL_REGISTER 1 /* 128-bit LDG/STG, tree in registers */
+#define MOSHPIT_KERNEL_BULK 2     /* cp.async.bulk (TMA) ring through smem */
+
+const char* moshpit_last_error(void);
+const char* moshpit_version(void);
+/* Number of visible CUDA devices (0 when none). [host] */
+int moshpit_device_count(int* out);
+
+/* ---- RNG: rng.hpp:31-127 (xoshiro256**, splitmix64 seeding, fnv1a names) */
+typedef struct {
+  uint64_t s[4];
+  int32_t have_spare;
+  double spare;
+} moshpit_rng_state;
+
+/* Rng(root).stream(name) (rng.hpp:118-121) or .stream(name, index)
+ * (rng.hpp:123-127) when index >= 0. [host] */
+int moshpit_rng_stream(uint64_t root, const char* name, int64_t index,
+                       moshpit_rng_state* out);
+/* n draws: kind 0=operator() (u64) 1=uniform (f64) 2=below(arg) (u64)
+ * 3=normal (f64) 4=bernoulli(p) (u8).  rng.hpp:43-91. [host] */
+int moshpit_rng_draws(moshpit_rng_state* st, int kind, uint64_t arg, double p,
+                      uint64_t n, void* out);
+
+/* ---- grid and keys: core.hpp:19-34, matchmaking.hpp:46-71 [host] ------ */
+int moshpit_grid_validate(uint32_t M, uint32_t d, uint32_t T);
+uint64_t moshpit_grid_capacity(uint32_t M, uint32_t d);
+/* matchmaking.hpp:46 initial_index; key_out has d-1 entries. */
+int moshpit_initial_index(uint64_t cell, uint32_t M, uint32_t d,
+                          uint32_t* key_out);
+/* matchmaking.hpp:62 next_group_key. */
+int moshpit_next_group_key(const uint32_t* key, uint32_t klen, uint32_t chunk,
+                           uint32_t M, uint32_t* key_out);
+/* allreduce.hpp:46-66 chunk_sizes (largest remainder). */
+int moshpit_chunk_sizes(uint64_t dim, const double* weights, uint64_t n,
+                        uint64_t* sizes_out);
+/* theory.hpp:149-155 complexity_estimate. */
+double moshpit_complexity_estimate(uint32_t t, uint32_t n, uint32_t m,
+                                   uint32_t dim);
+
+/* ---- matchmaking.hpp:300-323 form_groups_uncontested  [GPU kernel 1] ----
+ * Peers: ids[n], keys[n*klen] (GroupKey digits, lexicographic), timestamps[n].
+ * Output: members_out[n] (peer ids in group order), group_off_out[g..g+1]
+ * bounds group g (n+1 entries reserved), *n_groups_out. */
+int moshpit_form_groups_uncontested(uint64_t n, const uint32_t* ids,
+                                    const uint32_t* keys, uint32_t klen,
+                                    const uint64_t* timestamps, uint32_t cap,
+                                    uint32_t* members_out,
+                                    uint32_t* group_off_out,
+                                    uint64_t* n_groups_out);
+
+/* ---- numerics on host buffers  [GPU kernel 2 and diagnostics] ---------- */
+/* core.hpp:91-106 group_mean over rows[members[k]] (members NULL = 0..n-1). */
+int moshpit_group_mean(int dtype, const void* rows, uint64_t n_rows,
+                       uint64_t dim, const uint32_t* members, uint64_t n,
+                       void* mean_out);
+/* allreduce.hpp:79-121 butterfly_allreduce (weights only validated: the
+ * mean is partition-invariant, allreduce.hpp:104-105). */
+int moshpit_butterfly_allreduce(int dtype, const void* inputs, uint64_t n,
+                                uint64_t dim, const double* weights,
+                                uint64_t n_weights, const uint8_t* failed,
+                                void* vectors_out, uint32_t* chunks_out,
+                                int32_t* completed_out);
+/* core.hpp:111-126 distortion (ref in double), core.hpp:128-133 mean_of. */
+int moshpit_distortion(int dtype, const void* peers, uint64_t n, uint64_t dim,
+                       const double* reference_mean, double* out);
+int moshpit_mean_of(int dtype, const void* peers, uint64_t n, uint64_t dim,
+                    void* mean_out);
+
+/* ---- protocols.hpp:108-179 run_moshpit  [GPU, host buffers] ------------
+ * initial: n*dim (dtype).  Report arrays have `rounds` entries.  final_out
+ * (nullable) receives the vectors after the last round (run_moshpit itself
+ * never returns them).  diag: MOSHPIT_DIAG_*.  T is GridConfig::rounds. */
+int moshpit_run_moshpit(int dtype, uint32_t M, uint32_t d, uint32_t T,
+                        const void* initial, uint64_t n, uint64_t dim,
+                        double p_round, uint64_t seed, uint32_t rounds,
+                        int diag, double* initial_distortion,
+                        double* distortion, double* mean_drift,
+                        uint32_t* active_counts, double* cost_units,
+                        void* final_out);
+
+/* ---- optimizer.hpp:249-284 detail::moshpit_average  [GPU, host buffers]
+ * thetas (n*dim, dtype) averaged in place; *stream advanced exactly as the
+ * reference advances its RngStream. */
+int moshpit_moshpit_average(int dtype, void* thetas, uint64_t n, uint64_t dim,
+                            uint32_t M, uint32_t d, uint32_t rounds,
+                            moshpit_rng_state* stream);
+
+/* ---- device-resident engine (the performance boundary) -----------------
+ * One engine = one trial's integer plane (grid, keys, rng streams, group
+ * tables) resident on `device`.  The peer state is caller-owned device
+ * memory: n rows of `ld` elements (ld >= dim, ld*elem % 16 == 0, base 16-byte
+ * aligned); columns [dim, round_up(dim, 16/elem)) are scratch. */
+typedef struct moshpit_engine moshpit_engine;
+
+/* Protocol mode: streams "cells", "failures", "priorities" of Rng(seed),
+ * exactly as run_moshpit (protocols.hpp:123-140). */
+int moshpit_engine_create(uint32_t M, uint32_t d, uint64_t n, double p_round,
+                          uint64_t seed, int device, moshpit_engine** out);
+int moshpit_engine_destroy(moshpit_engine* e);
+/* Select MOSHPIT_KERNEL_* for the group mean. */
+int moshpit_engine_set_kernel(moshpit_engine* e, int variant);
+/* Enqueue one round on `stream` (cudaStream_t; NULL = legacy default):
+ * draw failures + priorities on the host, group on the GPU (kernel 1),
+ * average non-voided groups in place (kernel 2), advance keys.  Does not
+ * synchronise.  *active_out (nullable) = peers that did not fail. */
+int moshpit_engine_round(moshpit_engine* e, int dtype, void* state,
+                         uint64_t dim, uint64_t ld, void* stream,
+                         uint32_t* active_out);
+/* Synchronise the engine's last stream and report how many rounds ran and
+ * how many peer rows sat in non-voided groups, summed over those rounds.
+ * Algorithmic HBM bytes of kernel 2 = 2 * elem * dim * active_rows_total. */
+int moshpit_engine_stats(moshpit_engine* e, uint64_t* rounds,
+                         uint64_t* active_rows_total);
+/* Bracket every kernel-2 launch with CUDA events on its launch stream
+ * (enable=1), and read back the summed device time of the bracketed launches
+ * since the last read (synchronises on the events). */
+int moshpit_engine_set_timing(moshpit_engine* e, int enable);
+int moshpit_engine_kernel_time(moshpit_engine* e, double* total_ms,
+                               uint64_t* launches);
+/* Copy the last round's group tables to host (synchronises the engine's
+ * last stream): members[n], group_off[n+1], *n_groups, void_flags[n] (per
+ * group), ranks[n] (per peer), keys[n*(d-1)] (keys after the round). */
+int moshpit_engine_tables(moshpit_engine* e, uint32_t* members,
+                          uint32_t* group_off, uint32_t* n_groups,
+                          uint8_t* void_flags, uint32_t* ranks, uint32_t* keys);
+
+/* Counter-based synthetic init (bench / tests):
+ * x(i,j) = (splitmix64(seed ^ (i<<32) ^ (col0+j)) >> 40) * 2^-24. */
+int moshpit_fill_synthetic(int dtype, void* state, uint64_t n, uint64_t dim,
+                           uint64_t ld, uint64_t seed, uint64_t col0,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOSHPIT_B200_H */

@@ -1,0 +1,335 @@
+// ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference
+// headers (compiled from /root/reference/proj/include where they lie; no
+// reference source is copied into this repo).  TEST INFRASTRUCTURE ONLY:
+// built by oracle/Makefile into oracle/_ref/libmoshpit_ref.so and used by
+// tests/ (to pin the oracle), tests/golden/gen_golden.py (to make the golden
+// vectors) and bench.py's CPU reference arm.
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "moshpit/allreduce.hpp"
+#include "moshpit/core.hpp"
+#include "moshpit/matchmaking.hpp"
+#include "moshpit/optimizer.hpp"
+#include "moshpit/protocols.hpp"
+#include "moshpit/rng.hpp"
+
+using namespace moshpit;
+
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  } catch (const std::out_of_range&) {
+    return -2;
+  } catch (const std::runtime_error&) {
+    return -3;
+  } catch (...) {
+    return -4;
+  }
+}
+
+std::vector<ParamVector> rows_of(const double* x, std::uint64_t n,
+                                 std::uint64_t dim) {
+  std::vector<ParamVector> v(n, ParamVector(dim));
+  for (std::uint64_t i = 0; i < n; ++i)
+    std::memcpy(v[i].data(), x + i * dim, dim * sizeof(double));
+  return v;
+}
+
+void fill_report(const protocols::TrialReport& r, double* init_d, double* dist,
+                 double* drift, std::uint32_t* active, double* cost) {
+  *init_d = r.initial_distortion;
+  for (std::size_t t = 0; t < r.distortion.size(); ++t) {
+    dist[t] = r.distortion[t];
+    drift[t] = r.mean_drift[t];
+    active[t] = r.active_counts[t];
+  }
+  *cost = r.cost_units;
+}
+
+double init_value(std::uint64_t seed, std::uint64_t i, std::uint64_t j) {
+  std::uint64_t s = seed ^ (i << 32) ^ j;
+  return static_cast<double>(detail::splitmix64(s) >> 40) * 0x1.0p-24;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_stream_draws(std::uint64_t root, const char* name, std::int64_t index,
+                      int kind, std::uint64_t arg, double arg_f, std::uint64_t n,
+                      void* out) {
+  Rng rng(root);
+  RngStream s = index < 0 ? rng.stream(name)
+                          : rng.stream(name, static_cast<std::uint64_t>(index));
+  for (std::uint64_t i = 0; i < n; ++i) {
+    switch (kind) {
+      case 0: static_cast<std::uint64_t*>(out)[i] = s(); break;
+      case 1: static_cast<double*>(out)[i] = s.uniform(); break;
+      case 2: static_cast<std::uint64_t*>(out)[i] = s.below(arg); break;
+      case 3: static_cast<double*>(out)[i] = s.normal(); break;
+      default: static_cast<std::uint8_t*>(out)[i] = s.bernoulli(arg_f); break;
+    }
+  }
+}
+
+int ref_initial_index(std::uint64_t cell, std::uint32_t M, std::uint32_t d,
+                      std::uint32_t* key) {
+  return guarded([&] {
+    const auto k = matchmaking::initial_index(cell, GridConfig{M, d, 1});
+    for (std::size_t i = 0; i < k.indices.size(); ++i) key[i] = k.indices[i];
+  });
+}
+
+int ref_next_group_key(const std::uint32_t* key, std::uint32_t klen,
+                       std::uint32_t chunk, std::uint32_t M, std::uint32_t* out) {
+  return guarded([&] {
+    GroupKey k;
+    k.indices.assign(key, key + klen);
+    const auto nk = matchmaking::next_group_key(k, chunk, GridConfig{M, klen + 1, 1});
+    for (std::size_t i = 0; i < nk.indices.size(); ++i) out[i] = nk.indices[i];
+  });
+}
+
+std::int64_t ref_form_groups_uncontested(std::uint64_t n, const std::uint32_t* ids,
+                                         const std::uint32_t* keys,
+                                         std::uint32_t klen,
+                                         const std::uint64_t* ts, std::uint32_t cap,
+                                         std::uint32_t* members,
+                                         std::uint32_t* group_off) {
+  std::vector<matchmaking::MatchPeer> peers(n);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    peers[i].id = ids[i];
+    peers[i].key.indices.assign(keys + i * klen, keys + (i + 1) * klen);
+    peers[i].timestamp = ts[i];
+  }
+  const auto groups = matchmaking::form_groups_uncontested(peers, cap);
+  std::uint32_t p = 0;
+  for (std::size_t g = 0; g < groups.size(); ++g) {
+    group_off[g] = p;
+    for (auto id : groups[g].members) members[p++] = id;
+  }
+  group_off[groups.size()] = p;
+  return static_cast<std::int64_t>(groups.size());
+}
+
+int ref_chunk_sizes(std::uint64_t dim, const double* w, std::uint64_t n,
+                    std::uint64_t* sizes) {
+  return guarded([&] {
+    const auto s = allreduce::chunk_sizes(
+        dim, allreduce::PartitionWeights{std::vector<double>(w, w + n)});
+    for (std::size_t i = 0; i < s.size(); ++i) sizes[i] = s[i];
+  });
+}
+
+double ref_pairwise_sum(const double* xs, std::uint64_t n) {
+  return pairwise_sum(std::vector<double>(xs, xs + n));
+}
+
+int ref_group_mean(const double* rows, std::uint64_t n, std::uint64_t dim,
+                   const std::uint32_t* members, double* out) {
+  return guarded([&] {
+    const auto v = rows_of(rows, n, dim);
+    std::vector<const ParamVector*> ptrs;
+    for (std::uint64_t i = 0; i < n; ++i) ptrs.push_back(&v[members ? members[i] : i]);
+    const auto m = group_mean(ptrs);
+    std::memcpy(out, m.data(), dim * sizeof(double));
+  });
+}
+
+int ref_butterfly(const double* inputs, std::uint64_t n, std::uint64_t dim,
+                  const std::uint8_t* failed, double* out, int* completed,
+                  std::uint32_t* chunks) {
+  return guarded([&] {
+    const auto v = rows_of(inputs, n, dim);
+    std::vector<bool> f;
+    if (failed)
+      for (std::uint64_t i = 0; i < n; ++i) f.push_back(failed[i] != 0);
+    const auto o = allreduce::butterfly_allreduce(
+        v, allreduce::PartitionWeights::uniform(n), f);
+    *completed = o.completed;
+    for (std::uint64_t i = 0; i < n; ++i) {
+      std::memcpy(out + i * dim, o.vectors[i].data(), dim * sizeof(double));
+      chunks[i] = o.chunks[i];
+    }
+  });
+}
+
+double ref_distortion(const double* peers, std::uint64_t n, std::uint64_t dim,
+                      const double* ref) {
+  return distortion(rows_of(peers, n, dim), ParamVector(ref, ref + dim));
+}
+
+int ref_mean_of(const double* peers, std::uint64_t n, std::uint64_t dim,
+                double* out) {
+  return guarded([&] {
+    const auto m = mean_of(rows_of(peers, n, dim));
+    std::memcpy(out, m.data(), dim * sizeof(double));
+  });
+}
+
+double ref_complexity_estimate(std::uint32_t t, std::uint32_t n, std::uint32_t m,
+                               std::uint32_t dim) {
+  return theory::complexity_estimate(t, n, m, dim);
+}
+
+// The unmodified protocols::run_moshpit (protocols.hpp:108-179).
+int ref_run_moshpit(std::uint32_t M, std::uint32_t d, std::uint32_t T,
+                    const double* initial, std::uint64_t n, std::uint64_t dim,
+                    double p, std::uint64_t seed, std::uint32_t rounds,
+                    double* init_d, double* dist, double* drift,
+                    std::uint32_t* active, double* cost) {
+  return guarded([&] {
+    const auto r = protocols::run_moshpit(GridConfig{M, d, T}, rows_of(initial, n, dim),
+                                          FailureModel{p, {}}, Rng(seed), rounds);
+    fill_report(r, init_d, dist, drift, active, cost);
+  });
+}
+
+// run_moshpit's loop restated from the reference's own public functions so
+// that the final vectors (which run_moshpit never returns) are observable.
+// tests/test_oracle_vs_ref.py checks its report equals ref_run_moshpit's.
+int ref_run_moshpit_vectors(std::uint32_t M, std::uint32_t d, std::uint32_t T,
+                            const double* initial, std::uint64_t n,
+                            std::uint64_t dim, double p, std::uint64_t seed,
+                            std::uint32_t rounds, double* init_d, double* dist,
+                            double* drift, std::uint32_t* active, double* cost,
+                            double* final_vectors) {
+  return guarded([&] {
+    const GridConfig grid{M, d, T};
+    grid.validate();
+    const FailureModel failure{p, {}};
+    failure.validate();
+    const Rng rng(seed);
+    const auto init = rows_of(initial, n, dim);
+    if (n == 0 || n > grid.capacity()) throw std::invalid_argument("n");
+    const ParamVector reference = mean_of(init);
+    protocols::TrialReport report;
+    report.initial_distortion = distortion(init, reference);
+    auto cell_stream = rng.stream("cells");
+    std::vector<std::uint64_t> cells(grid.capacity());
+    for (std::uint64_t i = 0; i < cells.size(); ++i) cells[i] = i;
+    for (std::size_t i = 0; i < n; ++i) {
+      const std::size_t j = i + cell_stream.below(cells.size() - i);
+      std::swap(cells[i], cells[j]);
+    }
+    auto vectors = init;
+    std::vector<GroupKey> keys(n);
+    for (std::size_t i = 0; i < n; ++i) keys[i] = matchmaking::initial_index(cells[i], grid);
+    auto fail_stream = rng.stream("failures");
+    auto clock_stream = rng.stream("priorities");
+    for (std::uint32_t round = 1; round <= rounds; ++round) {
+      const auto failed = protocols::detail::draw_failures(fail_stream, n, p);
+      std::vector<matchmaking::MatchPeer> declared(n);
+      for (std::size_t i = 0; i < n; ++i)
+        declared[i] = matchmaking::MatchPeer{static_cast<PeerId>(i), keys[i],
+                                             clock_stream() >> 16, 0};
+      const auto groups = matchmaking::form_groups_uncontested(declared, M);
+      std::uint32_t act = 0;
+      for (const auto& group : groups) {
+        std::vector<ParamVector> inputs;
+        std::vector<bool> gf;
+        for (PeerId id : group.members) {
+          inputs.push_back(vectors[id]);
+          gf.push_back(failed[id]);
+        }
+        const auto out = allreduce::butterfly_allreduce(
+            inputs, allreduce::PartitionWeights::uniform(inputs.size()), gf);
+        for (std::size_t k = 0; k < group.members.size(); ++k) {
+          const PeerId id = group.members[k];
+          if (out.completed) vectors[id] = out.vectors[k];
+          keys[id] = matchmaking::next_group_key(keys[id], out.chunks[k], grid);
+          act += !failed[id];
+        }
+      }
+      protocols::detail::record_round(report, vectors, reference, act);
+    }
+    report.cost_units = theory::complexity_estimate(rounds, static_cast<std::uint32_t>(n),
+                                                    M, static_cast<std::uint32_t>(dim));
+    fill_report(report, init_d, dist, drift, active, cost);
+    for (std::uint64_t i = 0; i < n; ++i)
+      std::memcpy(final_vectors + i * dim, vectors[i].data(), dim * sizeof(double));
+  });
+}
+
+// optimizer::detail::moshpit_average over Rng(seed).stream(name).
+int ref_moshpit_average(double* thetas, std::uint64_t n, std::uint64_t dim,
+                        std::uint32_t M, std::uint32_t d, std::uint32_t rounds,
+                        std::uint64_t seed, const char* name) {
+  return guarded([&] {
+    auto v = rows_of(thetas, n, dim);
+    auto s = Rng(seed).stream(name);
+    optimizer::detail::moshpit_average(v, GridConfig{M, d, 1}, rounds, s);
+    for (std::uint64_t i = 0; i < n; ++i)
+      std::memcpy(thetas + i * dim, v[i].data(), dim * sizeof(double));
+  });
+}
+
+// CPU baseline: the unmodified run_moshpit on `slices` column slices of
+// width `width` of the counter-initialised state, spread over
+// `threads` host threads.  Coordinates are independent, so each slice is
+// bit-identical to those coordinates of a full-D run.  Init is excluded
+// from *run_s; *init_s reports it.
+int ref_slice_bench(std::uint32_t M, std::uint32_t d, std::uint64_t n,
+                    std::uint64_t width, std::uint64_t slices, std::uint64_t col0,
+                    std::uint64_t init_seed, std::uint64_t seed, double p,
+                    std::uint32_t rounds, std::uint32_t threads, double* run_s,
+                    double* init_s, double* checksum) {
+  return guarded([&] {
+    if (threads == 0) threads = 1;
+    std::vector<std::vector<ParamVector>> inits(slices);
+    const auto t0 = std::chrono::steady_clock::now();
+    {
+      std::vector<std::thread> pool;
+      for (std::uint32_t t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+          for (std::uint64_t s = t; s < slices; s += threads) {
+            auto& v = inits[s];
+            v.assign(n, ParamVector(width));
+            for (std::uint64_t i = 0; i < n; ++i)
+              for (std::uint64_t j = 0; j < width; ++j)
+                v[i][j] = init_value(init_seed, i, col0 + s * width + j);
+          }
+        });
+      for (auto& th : pool) th.join();
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    std::vector<double> sums(slices, 0.0);
+    std::atomic<int> err{0};
+    {
+      std::vector<std::thread> pool;
+      for (std::uint32_t t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+          for (std::uint64_t s = t; s < slices; s += threads) {
+            try {
+              const auto r = protocols::run_moshpit(GridConfig{M, d, 1}, inits[s],
+                                                    FailureModel{p, {}}, Rng(seed), rounds);
+              sums[s] = r.distortion.empty() ? r.initial_distortion : r.distortion.back();
+            } catch (...) {
+              err = 1;
+            }
+          }
+        });
+      for (auto& th : pool) th.join();
+    }
+    const auto t2 = std::chrono::steady_clock::now();
+    if (err) throw std::invalid_argument("run_moshpit failed");
+    *init_s = std::chrono::duration<double>(t1 - t0).count();
+    *run_s = std::chrono::duration<double>(t2 - t1).count();
+    double c = 0.0;
+    for (double x : sums) c += x;
+    *checksum = c;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+"""B200-native Moshpit averaging engine (arXiv 2103.03239), Python face.
+
+Mirrors the reference's public API (proj/include/moshpit/: ``GridConfig``,
+``GroupKey``, ``FailureModel``, ``Rng``/``RngStream``, ``initial_index``,
+``next_group_key``, ``MatchPeer``/``SealedGroup``/``form_groups_uncontested``,
+``PartitionWeights``/``butterfly_allreduce``, ``group_mean``, ``distortion``,
+``mean_of``, ``TrialReport``/``run_moshpit``, ``moshpit_average``) with the
+same argument meaning and error classes, over the C ABI of
+``libmoshpit_b200.so`` (include/moshpit_b200.h).  The data plane runs on the
+GPU; there is no CPU fallback.  ``Engine`` is the device-resident
+performance path (peer state in a CUDA tensor, one call per round).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import (CudaError, InvalidArgument, MoshpitError, OutOfRange,  # noqa: F401
+                    ReferenceRuntimeError, check, lib)
+
+UINT32_MAX = 0xFFFFFFFF
+
+__all__ = [
+    "GridConfig", "GroupKey", "FailureModel", "Rng", "RngStream", "initial_index",
+    "next_group_key", "MatchPeer", "SealedGroup", "Priority", "form_groups_uncontested",
+    "PartitionWeights", "chunk_sizes", "AllReduceOutcome", "butterfly_allreduce",
+    "group_mean", "distortion", "mean_of", "TrialReport", "run_moshpit", "moshpit_average",
+    "complexity_estimate", "Engine", "fill_synthetic", "InvalidArgument", "OutOfRange",
+    "CudaError", "MoshpitError", "device_count",
+]
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _dtype_code(dt):
+    dt = np.dtype(dt)
+    if dt == np.float32:
+        return _capi.F32
+    if dt == np.float64:
+        return _capi.F64
+    raise InvalidArgument(f"unsupported dtype {dt}; use float32 or float64")
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib().moshpit_device_count(C.byref(n)))
+    return n.value
+
+
+# ---------------------------------------------------------------------------
+# core.hpp:19-66
+# ---------------------------------------------------------------------------
+@dataclass
+class GridConfig:
+    peers_per_axis: int = 1  # M
+    dims: int = 1            # d
+    rounds: int = 1          # T
+
+    def validate(self):
+        check(lib().moshpit_grid_validate(self.peers_per_axis, self.dims, self.rounds))
+
+    def capacity(self) -> int:
+        return int(lib().moshpit_grid_capacity(self.peers_per_axis, self.dims))
+
+
+@dataclass(order=True)
+class GroupKey:
+    indices: List[int] = field(default_factory=list)
+
+
+@dataclass
+class FailureModel:
+    p_round: float = 0.0
+    churn: list = field(default_factory=list)
+
+    def validate(self):
+        if self.p_round < 0.0 or self.p_round > 1.0:
+            raise InvalidArgument("FailureModel: p_round must be in [0,1]")
+
+
+# ---------------------------------------------------------------------------
+# rng.hpp:31-127
+# ---------------------------------------------------------------------------
+class RngStream:
+    """xoshiro256** stream with the reference's exact output sequence."""
+
+    def __init__(self, state: _capi.RngState):
+        self.state = state
+
+    def _draw(self, kind, n, arg=0, p=0.0, dt=np.uint64):
+        out = np.zeros(max(n, 1), dtype=dt)
+        check(lib().moshpit_rng_draws(C.byref(self.state), kind, arg, p, n, _p(out)))
+        return out[:n]
+
+    def __call__(self) -> int:
+        return int(self._draw(0, 1)[0])
+
+    def next_n(self, n) -> np.ndarray:
+        return self._draw(0, n)
+
+    def uniform(self) -> float:
+        return float(self._draw(1, 1, dt=np.float64)[0])
+
+    def below(self, n: int) -> int:
+        return int(self._draw(2, 1, arg=n)[0])
+
+    def normal(self) -> float:
+        return float(self._draw(3, 1, dt=np.float64)[0])
+
+    def normals(self, n) -> np.ndarray:
+        return self._draw(3, n, dt=np.float64)
+
+    def bernoulli(self, p: float) -> bool:
+        return bool(self._draw(4, 1, p=p, dt=np.uint8)[0])
+
+    def shuffle(self, v: list):
+        for i in range(len(v), 1, -1):
+            j = self.below(i)
+            v[i - 1], v[j] = v[j], v[i - 1]
+
+
+class Rng:
+    def __init__(self, seed: int):
+        self._seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+
+    def seed(self) -> int:
+        return self._seed
+
+    def stream(self, name: str, index: Optional[int] = None) -> RngStream:
+        st = _capi.RngState()
+        check(lib().moshpit_rng_stream(self._seed, name.encode(),
+                                       -1 if index is None else int(index), C.byref(st)))
+        return RngStream(st)
+
+
+# ---------------------------------------------------------------------------
+# matchmaking.hpp:20-25, 46-90, 300-323
+# ---------------------------------------------------------------------------
+def initial_index(peer_cell: int, grid: GridConfig) -> GroupKey:
+    out = np.zeros(max(grid.dims - 1, 1), dtype=np.uint32)
+    check(lib().moshpit_initial_index(peer_cell, grid.peers_per_axis, grid.dims, _p(out)))
+    return GroupKey([int(x) for x in out[: grid.dims - 1]])
+
+
+def next_group_key(prev: GroupKey, new_chunk: int, grid: GridConfig) -> GroupKey:
+    k = np.asarray(prev.indices, dtype=np.uint32)
+    out = np.zeros(max(len(k), 1), dtype=np.uint32)
+    check(lib().moshpit_next_group_key(_p(k) if len(k) else None, len(k), new_chunk,
+                                       grid.peers_per_axis, _p(out)))
+    return GroupKey([int(x) for x in out[: len(k)]])
+
+
+@dataclass(order=True)
+class Priority:
+    timestamp: int = 0
+    peer: int = 0
+
+
+@dataclass
+class MatchPeer:
+    id: int = 0
+    key: GroupKey = field(default_factory=GroupKey)
+    timestamp: int = 0
+    arrival: int = 0
+
+
+@dataclass
+class SealedGroup:
+    leader: int = 0
+    members: List[int] = field(default_factory=list)
+
+
+def form_groups_uncontested(peers: Sequence[MatchPeer],
+                            max_group_size: int = UINT32_MAX) -> List[SealedGroup]:
+    """Closed-form grouping on the GPU (kernel 1)."""
+    n = len(peers)
+    if n == 0:
+        return []
+    klens = {len(p.key.indices) for p in peers}
+    if len(klens) != 1:
+        raise InvalidArgument("form_groups_uncontested: keys of different lengths")
+    klen = klens.pop()
+    ids = np.array([p.id for p in peers], dtype=np.uint32)
+    keys = np.array([p.key.indices for p in peers], dtype=np.uint32).reshape(n, klen)
+    ts = np.array([p.timestamp for p in peers], dtype=np.uint64)
+    members = np.zeros(n, dtype=np.uint32)
+    off = np.zeros(n + 1, dtype=np.uint32)
+    ng = C.c_uint64(0)
+    check(lib().moshpit_form_groups_uncontested(n, _p(ids), _p(keys) if klen else None, klen,
+                                                _p(ts), max_group_size, _p(members), _p(off),
+                                                C.byref(ng)))
+    groups = []
+    for g in range(ng.value):
+        m = [int(x) for x in members[off[g]:off[g + 1]]]
+        groups.append(SealedGroup(leader=m[0], members=m))
+    return groups
+
+
+# ---------------------------------------------------------------------------
+# allreduce.hpp:15-121
+# ---------------------------------------------------------------------------
+@dataclass
+class PartitionWeights:
+    w: List[float] = field(default_factory=list)
+
+    def validate(self):
+        total = 0.0
+        for wi in self.w:
+            if wi < 0.0:
+                raise InvalidArgument("PartitionWeights: w >= 0")
+            total += wi
+        if abs(total - 1.0) > 1e-9:
+            raise InvalidArgument("PartitionWeights: weights must sum to 1")
+
+    @staticmethod
+    def uniform(n: int) -> "PartitionWeights":
+        return PartitionWeights([1.0 / n] * n)
+
+
+def chunk_sizes(dim: int, weights: PartitionWeights) -> List[int]:
+    w = np.asarray(weights.w, dtype=np.float64)
+    out = np.zeros(max(len(w), 1), dtype=np.uint64)
+    check(lib().moshpit_chunk_sizes(dim, _p(w), len(w), _p(out)))
+    return [int(x) for x in out[: len(w)]]
+
+
+@dataclass
+class AllReduceOutcome:
+    completed: bool = False
+    vectors: Optional[np.ndarray] = None
+    chunks: List[int] = field(default_factory=list)
+
+
+def _rows(x, dtype=None):
+    if isinstance(x, np.ndarray):
+        a = x
+    else:
+        lens = {len(v) for v in x}
+        if len(lens) > 1:
+            raise InvalidArgument("dimension mismatch")
+        a = np.asarray(x)
+    if dtype is not None:
+        a = a.astype(dtype, copy=False)
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float64)
+    if a.ndim == 1:
+        a = a.reshape(len(a), -1) if len(a) else a.reshape(0, 0)
+    return np.ascontiguousarray(a)
+
+
+def butterfly_allreduce(inputs, weights: PartitionWeights,
+                        failed: Optional[Sequence[bool]] = None) -> AllReduceOutcome:
+    if len(inputs) == 0:
+        raise InvalidArgument("butterfly_allreduce: empty group")
+    x = _rows(inputs)
+    n, dim = x.shape
+    w = np.asarray(weights.w, dtype=np.float64)
+    f = None if not failed else np.asarray(failed, dtype=np.uint8)
+    out = np.zeros_like(x)
+    chunks = np.zeros(n, dtype=np.uint32)
+    done = C.c_int32(0)
+    check(lib().moshpit_butterfly_allreduce(_dtype_code(x.dtype), _p(x), n, dim, _p(w), len(w),
+                                            _p(f), _p(out), _p(chunks), C.byref(done)))
+    return AllReduceOutcome(bool(done.value), out, [int(c) for c in chunks])
+
+
+# ---------------------------------------------------------------------------
+# core.hpp:91-133
+# ---------------------------------------------------------------------------
+def group_mean(members) -> np.ndarray:
+    if len(members) == 0:
+        raise InvalidArgument("group_mean: empty group")
+    x = _rows(members)
+    out = np.zeros(x.shape[1], dtype=x.dtype)
+    check(lib().moshpit_group_mean(_dtype_code(x.dtype), _p(x), x.shape[0], x.shape[1], None,
+                                   x.shape[0], _p(out)))
+    return out
+
+
+def mean_of(peers) -> np.ndarray:
+    return group_mean(peers)
+
+
+def distortion(peers, reference_mean) -> float:
+    if len(peers) == 0:
+        return 0.0
+    x = _rows(peers)
+    ref = np.ascontiguousarray(reference_mean, dtype=np.float64).reshape(-1)
+    if x.shape[1] != len(ref):
+        raise InvalidArgument("distortion: dimension mismatch")
+    out = C.c_double(0.0)
+    check(lib().moshpit_distortion(_dtype_code(x.dtype), _p(x), x.shape[0], x.shape[1],
+                                   _p(ref), C.byref(out)))
+    return out.value
+
+
+def complexity_estimate(t_rounds, n_peers, m, dim) -> float:
+    return lib().moshpit_complexity_estimate(t_rounds, n_peers, m, dim)
+
+
+# ---------------------------------------------------------------------------
+# protocols.hpp:49-179
+# ---------------------------------------------------------------------------
+@dataclass
+class TrialReport:
+    initial_distortion: float = 0.0
+    distortion: List[float] = field(default_factory=list)
+    mean_drift: List[float] = field(default_factory=list)
+    active_counts: List[int] = field(default_factory=list)
+    cost_units: float = 0.0
+    vectors: Optional[np.ndarray] = None  # extension: final peer vectors
+
+    def rounds_to(self, threshold: float, cap: int) -> int:
+        if self.initial_distortion <= threshold:
+            return 0
+        for t in range(min(len(self.distortion), cap)):
+            if self.distortion[t] <= threshold:
+                return t + 1
+        return cap
+
+
+_DIAG = {"none": _capi.DIAG_NONE, "fast": _capi.DIAG_FAST, "exact": _capi.DIAG_EXACT}
+
+
+def run_moshpit(grid: GridConfig, initial, failure: FailureModel, rng: Rng, rounds: int, *,
+                dtype=None, diagnostics: Optional[str] = None,
+                return_vectors: bool = False) -> TrialReport:
+    """protocols::run_moshpit on the GPU.
+
+    ``dtype`` float64 (default for lists / float64 arrays) is bit-identical to
+    the reference; float32 is the performance path.  ``diagnostics`` defaults
+    to "exact" (reference summation order) for float64 and "fast" for
+    float32.
+    """
+    if len(initial) == 0:
+        grid.validate()
+        failure.validate()
+        raise InvalidArgument("run_moshpit: no peers")
+    x = _rows(initial, dtype)
+    n, dim = x.shape
+    code = _dtype_code(x.dtype)
+    if diagnostics is None:
+        diagnostics = "exact" if code == _capi.F64 else "fast"
+    R = max(int(rounds), 1)
+    dist = np.zeros(R)
+    drift = np.zeros(R)
+    act = np.zeros(R, dtype=np.uint32)
+    init_d = C.c_double(0)
+    cost = C.c_double(0)
+    final = np.zeros_like(x) if return_vectors else None
+    check(lib().moshpit_run_moshpit(code, grid.peers_per_axis, grid.dims, grid.rounds, _p(x), n,
+                                    dim, failure.p_round, rng.seed(), int(rounds),
+                                    _DIAG[diagnostics], C.byref(init_d), _p(dist), _p(drift),
+                                    _p(act), C.byref(cost), _p(final)))
+    return TrialReport(init_d.value, list(dist[:rounds]), list(drift[:rounds]),
+                       [int(a) for a in act[:rounds]], cost.value, final)
+
+
+def moshpit_average(thetas, grid: GridConfig, rounds: int, stream: RngStream):
+    """optimizer::detail::moshpit_average on the GPU; returns the averaged
+    array (in place when ``thetas`` is a C-contiguous float array)."""
+    x = thetas if (isinstance(thetas, np.ndarray) and thetas.flags.c_contiguous
+                   and thetas.dtype in (np.float32, np.float64)) else _rows(thetas)
+    n = x.shape[0]
+    dim = x.shape[1] if x.ndim == 2 else 0
+    check(lib().moshpit_moshpit_average(_dtype_code(x.dtype), _p(x), n, dim,
+                                        grid.peers_per_axis, grid.dims, rounds,
+                                        C.byref(stream.state)))
+    return x
+
+
+# ---------------------------------------------------------------------------
+# Device-resident engine (torch tensors or raw device pointers)
+# ---------------------------------------------------------------------------
+def _tensor_args(state):
+    import torch  # plumbing only: device memory and streams
+    if not isinstance(state, torch.Tensor) or not state.is_cuda:
+        raise InvalidArgument("state must be a CUDA tensor")
+    if state.dtype == torch.float32:
+        code = _capi.F32
+    elif state.dtype == torch.float64:
+        code = _capi.F64
+    else:
+        raise InvalidArgument("state dtype must be float32 or float64")
+    if state.dim() != 2 or state.stride(1) != 1:
+        raise InvalidArgument("state must be [n, ld] with unit column stride")
+    return code, state.data_ptr(), state.stride(0)
+
+
+def fill_synthetic(state, seed: int, dim: Optional[int] = None, col0: int = 0, stream=None):
+    import torch
+    code, ptr, ld = _tensor_args(state)
+    s = stream if stream is not None else torch.cuda.current_stream(state.device)
+    check(lib().moshpit_fill_synthetic(code, ptr, state.shape[0],
+                                       state.shape[1] if dim is None else dim, ld, seed, col0,
+                                       s.cuda_stream))
+
+
+class Engine:
+    """One Moshpit trial resident on a GPU (protocols.hpp:123-173 round loop)."""
+
+    def __init__(self, grid: GridConfig, n_peers: int, failure: FailureModel, rng: Rng,
+                 device: int = 0, kernel: int = _capi.KERNEL_AUTO):
+        self.grid, self.n = grid, int(n_peers)
+        h = C.c_void_p()
+        check(lib().moshpit_engine_create(grid.peers_per_axis, grid.dims, self.n,
+                                          failure.p_round, rng.seed(), device, C.byref(h)))
+        self._h = h
+        self.device = device
+        if kernel != _capi.KERNEL_AUTO:
+            check(lib().moshpit_engine_set_kernel(self._h, kernel))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moshpit_engine_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_kernel(self, variant: int):
+        check(lib().moshpit_engine_set_kernel(self._h, variant))
+
+    def round(self, state, dim: Optional[int] = None, stream=None) -> int:
+        """Enqueue one round on ``stream`` (default: torch's current stream)."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        act = C.c_uint32(0)
+        check(lib().moshpit_engine_round(self._h, code, ptr,
+                                         state.shape[1] if dim is None else dim, ld,
+                                         s.cuda_stream, C.byref(act)))
+        return act.value
+
+    def round_raw(self, dtype_code: int, ptr: int, dim: int, ld: int, stream_handle: int) -> int:
+        act = C.c_uint32(0)
+        check(lib().moshpit_engine_round(self._h, dtype_code, ptr, dim, ld, stream_handle,
+                                         C.byref(act)))
+        return act.value
+
+    def set_timing(self, enable: bool):
+        check(lib().moshpit_engine_set_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self):
+        """(summed device ms, launches) of kernel 2 since the last call."""
+        ms, k = C.c_double(0), C.c_uint64(0)
+        check(lib().moshpit_engine_kernel_time(self._h, C.byref(ms), C.byref(k)))
+        return ms.value, k.value
+
+    def stats(self):
+        r, rows = C.c_uint64(0), C.c_uint64(0)
+        check(lib().moshpit_engine_stats(self._h, C.byref(r), C.byref(rows)))
+        return r.value, rows.value
+
+    def tables(self):
+        n, klen = self.n, self.grid.dims - 1
+        members = np.zeros(n, dtype=np.uint32)
+        off = np.zeros(n + 1, dtype=np.uint32)
+        ng = C.c_uint32(0)
+        void = np.zeros(n, dtype=np.uint8)
+        ranks = np.zeros(n, dtype=np.uint32)
+        keys = np.zeros((n, max(klen, 1)), dtype=np.uint32)
+        check(lib().moshpit_engine_tables(self._h, _p(members), _p(off), C.byref(ng), _p(void),
+                                          _p(ranks), _p(keys)))
+        g = ng.value
+        return dict(members=members, group_off=off[: g + 1], n_groups=g, void=void[:g],
+                    rank=ranks, keys=keys[:, :klen])

@@ -1,0 +1,852 @@
+// capi.cu -- the C ABI (include/moshpit_b200.h) over the GPU kernels.
+//
+// Host responsibilities only: argument validation with the reference's error
+// classes, the sequential RNG draws the reference makes (cells, failures,
+// priorities: O(n) per round), buffer marshalling and kernel launches.  All
+// arithmetic on peer vectors and all group formation run on the device.
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <unordered_map>
+
+#include "../../include/moshpit_b200.h"
+#include "common.cuh"
+
+namespace mb200 {
+
+double Xoshiro::normal() {  // rng.hpp:68-83
+  if (have_spare) {
+    have_spare = false;
+    return spare;
+  }
+  double u, v, r2;
+  do {
+    u = 2.0 * uniform() - 1.0;
+    v = 2.0 * uniform() - 1.0;
+    r2 = u * u + v * v;
+  } while (r2 >= 1.0 || r2 == 0.0);
+  const double f = std::sqrt(-2.0 * std::log(r2) / r2);
+  spare = v * f;
+  have_spare = true;
+  return u * f;
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw CudaError(std::string("no usable CUDA device (") +
+                    (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                    "); the Moshpit B200 engine has no CPU fallback");
+}
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return MOSHPIT_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return MOSHPIT_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return MOSHPIT_ERR_OUT_OF_RANGE;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return MOSHPIT_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MOSHPIT_ERR_RUNTIME;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return MOSHPIT_ERR_RUNTIME;
+  }
+}
+
+Xoshiro from_state(const moshpit_rng_state* st) {
+  Xoshiro r;
+  std::memcpy(r.s, st->s, sizeof(r.s));
+  r.have_spare = st->have_spare != 0;
+  r.spare = st->spare;
+  return r;
+}
+
+void to_state(const Xoshiro& r, moshpit_rng_state* st) {
+  std::memcpy(st->s, r.s, sizeof(r.s));
+  st->have_spare = r.have_spare ? 1 : 0;
+  st->spare = r.spare;
+}
+
+std::size_t elem_size(int dtype) {
+  if (dtype == MOSHPIT_F32) return 4;
+  if (dtype == MOSHPIT_F64) return 8;
+  throw std::invalid_argument("dtype must be MOSHPIT_F32 or MOSHPIT_F64");
+}
+
+std::uint64_t padded_ld(std::uint64_t dim, std::size_t elem) {
+  const std::uint64_t v = 16 / elem;
+  const std::uint64_t ld = (dim + v - 1) / v * v;
+  return ld ? ld : v;
+}
+
+// Partial Fisher-Yates over [0, capacity) (protocols.hpp:124-130,
+// optimizer.hpp:254-259) with a sparse map, so memory is O(n) rather than
+// O(M^d); the draws and swaps are exactly the reference's.
+std::vector<std::uint64_t> draw_cells(Xoshiro& st, std::uint64_t capacity,
+                                      std::uint64_t n) {
+  std::unordered_map<std::uint64_t, std::uint64_t> moved;
+  moved.reserve(2 * n);
+  auto at = [&](std::uint64_t i) {
+    auto it = moved.find(i);
+    return it == moved.end() ? i : it->second;
+  };
+  std::vector<std::uint64_t> cells(n);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const std::uint64_t j = i + st.below(capacity - i);
+    const std::uint64_t vi = at(i), vj = at(j);
+    moved[i] = vj;
+    moved[j] = vi;
+    cells[i] = vj;
+  }
+  return cells;
+}
+
+struct StreamHolder {
+  cudaStream_t s = nullptr;
+  StreamHolder() { MB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~StreamHolder() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// The device-resident integer plane of one trial (keys, tables, draws).
+// ---------------------------------------------------------------------------
+struct Plane {
+  Grid grid;
+  std::uint64_t n = 0;
+  int device = 0;
+  DeviceBuffer keys, draws, members, goff, gvoid, rank, act, counts, totals,
+      sidx, scs, sgi, cellbuf;
+  static constexpr int kStages = 4;
+  PinnedBuffer stage[kStages];
+  cudaEvent_t ev[kStages] = {};
+  int slot = 0;
+  std::uint32_t last_active = 0;
+  std::uint64_t rounds_done = 0;
+  cudaStream_t last_stream = nullptr;
+  // optional CUDA-event bracketing of kernel 2 on its launch stream
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+  std::size_t tev_used = 0;
+
+  Plane(std::uint32_t M, std::uint32_t d, std::uint64_t n_, int dev)
+      : grid(M, d), n(n_), device(dev) {
+    if (n == 0) throw std::invalid_argument("run_moshpit: no peers");
+    if (n > grid.capacity)
+      throw std::invalid_argument("run_moshpit: N exceeds grid capacity M^d");
+    if (n > 0x7fffffffull)
+      throw std::invalid_argument("moshpit engine: more than 2^31 peers");
+    std::uint64_t np = 1;
+    while (np < n) np <<= 1;
+    keys.resize(n * 8);
+    draws.resize(n * 9 + 16);
+    members.resize(n * 4);
+    goff.resize((n + 1) * 4);
+    gvoid.resize(n);
+    rank.resize(n * 4);
+    act.resize(n * 4);
+    counts.resize(16);
+    totals.resize(16);
+    sidx.resize(np * 4);
+    scs.resize(n * 4);
+    sgi.resize(n * 4);
+    cellbuf.resize(n * 8);
+    MB_CUDA(cudaMemset(totals.ptr, 0, 16));
+    MB_CUDA(cudaMemset(counts.ptr, 0, 16));
+    for (int i = 0; i < kStages; ++i) {
+      stage[i].resize(n * 9 + 16);
+      MB_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~Plane() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& pr : tev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  }
+
+  std::pair<cudaEvent_t, cudaEvent_t> timing_pair() {
+    if (tev_used == tev.size()) {
+      cudaEvent_t a, b;
+      MB_CUDA(cudaEventCreate(&a));
+      MB_CUDA(cudaEventCreate(&b));
+      tev.emplace_back(a, b);
+    }
+    return tev[tev_used++];
+  }
+
+  // cells -> initial keys (matchmaking.hpp:46-59), on the device.
+  void init_cells(Xoshiro& cell_stream, cudaStream_t s) {
+    const auto cells = draw_cells(cell_stream, grid.capacity, n);
+    const int k = next_slot();
+    std::memcpy(stage[k].ptr, cells.data(), n * 8);
+    MB_CUDA(cudaMemcpyAsync(cellbuf.ptr, stage[k].ptr, n * 8, cudaMemcpyHostToDevice, s));
+    MB_CUDA(cudaEventRecord(ev[k], s));
+    launch_initial_keys(cellbuf.as<std::uint64_t>(), keys.as<std::uint64_t>(), n,
+                        grid.M, grid.d, s);
+  }
+
+  int next_slot() {
+    const int k = slot;
+    slot = (slot + 1) % kStages;
+    MB_CUDA(cudaEventSynchronize(ev[k]));  // host staging slot reusable
+    return k;
+  }
+
+  // One round: host draws (protocols.hpp:143-150), group formation (kernel 1),
+  // group mean (kernel 2).  fail == nullptr or p <= 0: no failure draws.
+  std::uint32_t round(Xoshiro* fail, double p, Xoshiro& clock, int dtype,
+                      void* state, std::uint64_t dim, std::uint64_t ld,
+                      cudaStream_t s, int variant) {
+    const int k = next_slot();
+    auto* ts = stage[k].as<std::uint64_t>();
+    auto* failed = reinterpret_cast<std::uint8_t*>(ts + n);
+    std::memset(failed, 0, n);
+    std::uint32_t active = 0;
+    if (fail && p > 0.0) {
+      for (std::uint64_t i = 0; i < n; ++i) failed[i] = fail->bernoulli(p) ? 1 : 0;
+    }
+    for (std::uint64_t i = 0; i < n; ++i) active += failed[i] == 0;
+    for (std::uint64_t i = 0; i < n; ++i) ts[i] = clock.next() >> 16;
+    MB_CUDA(cudaMemcpyAsync(draws.ptr, ts, n * 9, cudaMemcpyHostToDevice, s));
+    MB_CUDA(cudaEventRecord(ev[k], s));
+
+    GroupArgs a;
+    a.n = static_cast<std::uint32_t>(n);
+    a.cap = grid.M;
+    a.M = grid.M;
+    a.pow_drop = grid.pow_drop;
+    a.advance_keys = 1;
+    a.klen_zero = grid.klen == 0;
+    a.keys = keys.as<std::uint64_t>();
+    a.ts = draws.as<std::uint64_t>();
+    a.failed = draws.as<std::uint8_t>() + n * 8;
+    a.members = members.as<std::uint32_t>();
+    a.goff = goff.as<std::uint32_t>();
+    a.gvoid = gvoid.as<std::uint8_t>();
+    a.rank = rank.as<std::uint32_t>();
+    a.act = act.as<std::uint32_t>();
+    a.counts = counts.as<std::uint32_t>();
+    a.totals = totals.as<unsigned long long>();
+    a.sidx = sidx.as<std::uint32_t>();
+    a.scs = scs.as<std::uint32_t>();
+    a.sgi = sgi.as<std::uint32_t>();
+    launch_form_groups(a, true, s);
+    if (state && dim) {
+      std::pair<cudaEvent_t, cudaEvent_t> te{};
+      if (timing) {
+        te = timing_pair();
+        MB_CUDA(cudaEventRecord(te.first, s));
+      }
+      if (dtype == MOSHPIT_F32)
+        launch_group_mean<float>(static_cast<float*>(state), ld, dim, a.members, a.goff,
+                                 a.act, a.counts, grid.M, variant, s);
+      else
+        launch_group_mean<double>(static_cast<double*>(state), ld, dim, a.members, a.goff,
+                                  a.act, a.counts, grid.M, variant, s);
+      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
+    }
+    last_active = active;
+    ++rounds_done;
+    last_stream = s;
+    return active;
+  }
+};
+
+}  // namespace mb200
+
+using namespace mb200;
+
+struct moshpit_engine {
+  std::unique_ptr<Plane> plane;
+  Xoshiro fail, clock;
+  double p = 0.0;
+  int variant = MOSHPIT_KERNEL_AUTO;
+};
+
+namespace {
+
+void check_state(int dtype, const void* state, std::uint64_t dim, std::uint64_t ld) {
+  const std::size_t es = elem_size(dtype);
+  const std::uint64_t vec = 16 / es;
+  if (reinterpret_cast<std::uintptr_t>(state) % 16 != 0)
+    throw std::invalid_argument("peer state must be 16-byte aligned");
+  if ((ld * es) % 16 != 0) throw std::invalid_argument("row stride must be a multiple of 16 bytes");
+  if (ld < (dim + vec - 1) / vec * vec)
+    throw std::invalid_argument("row stride must cover dim rounded up to 16 bytes");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moshpit_last_error(void) { return g_last_error.c_str(); }
+
+const char* moshpit_version(void) { return "moshpit-b200 0.1 (sm_100a)"; }
+
+int moshpit_device_count(int* out) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    *out = n;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// RNG and key arithmetic (host)
+// ---------------------------------------------------------------------------
+int moshpit_rng_stream(std::uint64_t root, const char* name, std::int64_t index,
+                       moshpit_rng_state* out) {
+  return guarded([&] {
+    if (!name || !out) throw std::invalid_argument("rng_stream: null argument");
+    const Xoshiro r = index < 0 ? Xoshiro::named(root, name)
+                                : Xoshiro::named(root, name, static_cast<std::uint64_t>(index));
+    to_state(r, out);
+  });
+}
+
+int moshpit_rng_draws(moshpit_rng_state* st, int kind, std::uint64_t arg, double p,
+                      std::uint64_t n, void* out) {
+  return guarded([&] {
+    if (!st || (n && !out)) throw std::invalid_argument("rng_draws: null argument");
+    if (kind == 2 && arg == 0) throw std::invalid_argument("rng_draws: below(0)");
+    Xoshiro r = from_state(st);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      switch (kind) {
+        case 0: static_cast<std::uint64_t*>(out)[i] = r.next(); break;
+        case 1: static_cast<double*>(out)[i] = r.uniform(); break;
+        case 2: static_cast<std::uint64_t*>(out)[i] = r.below(arg); break;
+        case 3: static_cast<double*>(out)[i] = r.normal(); break;
+        case 4: static_cast<std::uint8_t*>(out)[i] = r.bernoulli(p) ? 1 : 0; break;
+        default: throw std::invalid_argument("rng_draws: unknown kind");
+      }
+    }
+    to_state(r, st);
+  });
+}
+
+int moshpit_grid_validate(std::uint32_t M, std::uint32_t d, std::uint32_t T) {
+  return guarded([&] {
+    if (M < 1 || d < 1 || T < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+  });
+}
+
+std::uint64_t moshpit_grid_capacity(std::uint32_t M, std::uint32_t d) {
+  std::uint64_t cap = 1;  // core.hpp:29-33 (wraps like the reference)
+  for (std::uint32_t j = 0; j < d; ++j) cap *= M;
+  return cap;
+}
+
+int moshpit_initial_index(std::uint64_t cell, std::uint32_t M, std::uint32_t d,
+                          std::uint32_t* key_out) {
+  return guarded([&] {
+    if (M < 1 || d < 1) throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (cell >= moshpit_grid_capacity(M, d))
+      throw std::out_of_range("initial_index: cell index outside the grid");
+    std::uint64_t rest = cell / M;
+    for (std::uint32_t j = 1; j < d; ++j) {
+      key_out[j - 1] = static_cast<std::uint32_t>(rest % M);
+      rest /= M;
+    }
+  });
+}
+
+int moshpit_next_group_key(const std::uint32_t* key, std::uint32_t klen,
+                           std::uint32_t chunk, std::uint32_t M, std::uint32_t* key_out) {
+  return guarded([&] {
+    if (chunk >= M) throw std::out_of_range("next_group_key: chunk index outside [0, M)");
+    if (klen == 0) return;
+    std::vector<std::uint32_t> tmp(key + 1, key + klen);
+    tmp.push_back(chunk);
+    std::copy(tmp.begin(), tmp.end(), key_out);
+  });
+}
+
+int moshpit_chunk_sizes(std::uint64_t dim, const double* w, std::uint64_t n,
+                        std::uint64_t* sizes) {
+  return guarded([&] {
+    double total = 0.0;
+    for (std::uint64_t i = 0; i < n; ++i) {
+      if (w[i] < 0.0) throw std::invalid_argument("PartitionWeights: w >= 0");
+      total += w[i];
+    }
+    if (std::abs(total - 1.0) > 1e-9)
+      throw std::invalid_argument("PartitionWeights: weights must sum to 1");
+    std::vector<std::pair<double, std::uint64_t>> rem(n);
+    std::uint64_t assigned = 0;
+    for (std::uint64_t i = 0; i < n; ++i) {
+      const double exact = w[i] * static_cast<double>(dim);
+      sizes[i] = static_cast<std::uint64_t>(std::floor(exact));
+      assigned += sizes[i];
+      rem[i] = {exact - std::floor(exact), i};
+    }
+    std::sort(rem.begin(), rem.end(), [](const auto& a, const auto& b) {
+      return std::tie(b.first, b.second) < std::tie(a.first, a.second);
+    });
+    for (std::uint64_t k = 0; assigned < dim; ++k, ++assigned) sizes[rem[k % n].second] += 1;
+  });
+}
+
+double moshpit_complexity_estimate(std::uint32_t t, std::uint32_t n, std::uint32_t m,
+                                   std::uint32_t dim) {
+  if (t == 0) return 0.0;
+  const double md = m;
+  return t * (std::log2(static_cast<double>(n)) + md +
+              std::max<double>(dim, md) * (md - 1.0) / md);
+}
+
+// ---------------------------------------------------------------------------
+// form_groups_uncontested on the GPU (kernel 1, digit-key mode)
+// ---------------------------------------------------------------------------
+int moshpit_form_groups_uncontested(std::uint64_t n, const std::uint32_t* ids,
+                                    const std::uint32_t* keys, std::uint32_t klen,
+                                    const std::uint64_t* timestamps, std::uint32_t cap,
+                                    std::uint32_t* members_out, std::uint32_t* group_off_out,
+                                    std::uint64_t* n_groups_out) {
+  return guarded([&] {
+    if (cap == 0) throw std::invalid_argument("form_groups_uncontested: cap >= 1");
+    if (n > 0x7fffffffull) throw std::invalid_argument("form_groups_uncontested: n too large");
+    if (n == 0) {
+      group_off_out[0] = 0;
+      *n_groups_out = 0;
+      return;
+    }
+    require_device();
+    StreamHolder st;
+    std::uint64_t np = 1;
+    while (np < n) np <<= 1;
+    DeviceBuffer d_ids(n * 4), d_keys(n * (klen ? klen : 1) * 4), d_ts(n * 8), d_mem(n * 4),
+        d_goff((n + 1) * 4), d_void(n), d_counts(16), d_sidx(np * 4), d_scs(n * 4), d_sgi(n * 4);
+    MB_CUDA(cudaMemcpyAsync(d_ids.ptr, ids, n * 4, cudaMemcpyHostToDevice, st.s));
+    if (klen)
+      MB_CUDA(cudaMemcpyAsync(d_keys.ptr, keys, n * klen * 4, cudaMemcpyHostToDevice, st.s));
+    MB_CUDA(cudaMemcpyAsync(d_ts.ptr, timestamps, n * 8, cudaMemcpyHostToDevice, st.s));
+    GroupArgs a;
+    a.n = static_cast<std::uint32_t>(n);
+    a.cap = cap;
+    a.digit_keys = d_keys.as<std::uint32_t>();
+    a.dklen = klen;
+    a.ts = d_ts.as<std::uint64_t>();
+    a.ids = d_ids.as<std::uint32_t>();
+    a.members = d_mem.as<std::uint32_t>();
+    a.goff = d_goff.as<std::uint32_t>();
+    a.gvoid = d_void.as<std::uint8_t>();
+    a.counts = d_counts.as<std::uint32_t>();
+    a.sidx = d_sidx.as<std::uint32_t>();
+    a.scs = d_scs.as<std::uint32_t>();
+    a.sgi = d_sgi.as<std::uint32_t>();
+    launch_form_groups(a, false, st.s);
+    std::uint32_t counts[4];
+    MB_CUDA(cudaMemcpyAsync(counts, d_counts.ptr, 16, cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaMemcpyAsync(members_out, d_mem.ptr, n * 4, cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+    MB_CUDA(cudaMemcpy(group_off_out, d_goff.ptr, (counts[0] + 1) * 4, cudaMemcpyDeviceToHost));
+    *n_groups_out = counts[0];
+  });
+}
+
+// ---------------------------------------------------------------------------
+// numerics on host buffers
+// ---------------------------------------------------------------------------
+int moshpit_group_mean(int dtype, const void* rows, std::uint64_t n_rows, std::uint64_t dim,
+                       const std::uint32_t* members, std::uint64_t n, void* mean_out) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (n == 0) throw std::invalid_argument("group_mean: empty group");
+    if (members)
+      for (std::uint64_t k = 0; k < n; ++k)
+        if (members[k] >= n_rows) throw std::out_of_range("group_mean: member outside rows");
+    if (!members && n > n_rows) throw std::out_of_range("group_mean: n exceeds rows");
+    if (dim == 0) return;
+    require_device();
+    StreamHolder st;
+    DeviceBuffer d_rows(n_rows * dim * es), d_mem(n * 4), d_out(dim * es);
+    MB_CUDA(cudaMemcpyAsync(d_rows.ptr, rows, n_rows * dim * es, cudaMemcpyHostToDevice, st.s));
+    if (members)
+      MB_CUDA(cudaMemcpyAsync(d_mem.ptr, members, n * 4, cudaMemcpyHostToDevice, st.s));
+    const std::uint32_t* m = members ? d_mem.as<std::uint32_t>() : nullptr;
+    if (dtype == MOSHPIT_F32)
+      launch_colmean<float, float>(d_rows.as<float>(), n, dim, dim, m, d_out.as<float>(), st.s);
+    else
+      launch_colmean<double, double>(d_rows.as<double>(), n, dim, dim, m, d_out.as<double>(),
+                                     st.s);
+    MB_CUDA(cudaMemcpyAsync(mean_out, d_out.ptr, dim * es, cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+int moshpit_butterfly_allreduce(int dtype, const void* inputs, std::uint64_t n,
+                                std::uint64_t dim, const double* weights,
+                                std::uint64_t n_weights, const std::uint8_t* failed,
+                                void* vectors_out, std::uint32_t* chunks_out,
+                                std::int32_t* completed_out) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    // allreduce.hpp:82-89 validation order
+    if (n == 0) throw std::invalid_argument("butterfly_allreduce: empty group");
+    if (n_weights != n) throw std::invalid_argument("butterfly_allreduce: one weight per member");
+    // chunk_sizes validates the weights (allreduce.hpp:48) on the success path
+    for (std::uint64_t k = 0; k < n; ++k) chunks_out[k] = static_cast<std::uint32_t>(k);
+    bool any = false;
+    if (failed)
+      for (std::uint64_t k = 0; k < n; ++k) any |= failed[k] != 0;
+    if (any) {  // allreduce.hpp:95-102: the round is void, outputs = inputs
+      std::memcpy(vectors_out, inputs, n * dim * es);
+      *completed_out = 0;
+      return;
+    }
+    std::vector<std::uint64_t> sizes(n);
+    if (moshpit_chunk_sizes(dim, weights, n, sizes.data()) != MOSHPIT_OK)
+      throw std::invalid_argument(g_last_error);
+    *completed_out = 1;
+    if (dim == 0) return;
+    if (n > 0x7fffffffull) throw std::invalid_argument("butterfly_allreduce: group too large");
+    require_device();
+    StreamHolder st;
+    const std::uint64_t ld = padded_ld(dim, es);
+    DeviceBuffer d_x(n * ld * es), d_tab((n + 1) * 4 + n * 4 + 64);
+    MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, inputs, dim * es, dim * es, n,
+                              cudaMemcpyHostToDevice, st.s));
+    // a single group {0..n-1}, active: kernel 2 averages it in place
+    std::vector<std::uint32_t> tab((n + 1) + n + 16, 0);
+    std::uint32_t* h_mem = tab.data();
+    std::uint32_t* h_goff = h_mem + n;
+    std::iota(h_mem, h_mem + n, 0u);
+    h_goff[0] = 0;
+    h_goff[1] = static_cast<std::uint32_t>(n);
+    std::uint32_t* h_act = h_goff + 2;
+    h_act[0] = 0;
+    std::uint32_t* h_counts = h_act + 1;
+    h_counts[0] = 1;
+    h_counts[1] = 1;
+    h_counts[2] = static_cast<std::uint32_t>(n);
+    MB_CUDA(cudaMemcpyAsync(d_tab.ptr, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, st.s));
+    const std::uint32_t* dm = d_tab.as<std::uint32_t>();
+    if (dtype == MOSHPIT_F32)
+      launch_group_mean<float>(d_x.as<float>(), ld, dim, dm, dm + n, dm + n + 2, dm + n + 3,
+                               static_cast<std::uint32_t>(n), 0, st.s);
+    else
+      launch_group_mean<double>(d_x.as<double>(), ld, dim, dm, dm + n, dm + n + 2, dm + n + 3,
+                                static_cast<std::uint32_t>(n), 0, st.s);
+    MB_CUDA(cudaMemcpy2DAsync(vectors_out, dim * es, d_x.ptr, ld * es, dim * es, n,
+                              cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+int moshpit_distortion(int dtype, const void* peers, std::uint64_t n, std::uint64_t dim,
+                       const double* ref, double* out) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (n == 0) {  // core.hpp:113
+      *out = 0.0;
+      return;
+    }
+    require_device();
+    StreamHolder st;
+    DeviceBuffer d_x(n * dim * es + 16), d_ref(dim * 8 + 16), d_sq(n * 8), d_out(16);
+    MB_CUDA(cudaMemcpyAsync(d_x.ptr, peers, n * dim * es, cudaMemcpyHostToDevice, st.s));
+    MB_CUDA(cudaMemcpyAsync(d_ref.ptr, ref, dim * 8, cudaMemcpyHostToDevice, st.s));
+    if (dtype == MOSHPIT_F32)
+      launch_distortion<float>(d_x.as<float>(), n, dim, dim, d_ref.as<double>(),
+                               d_sq.as<double>(), nullptr, d_out.as<double>(), 1, st.s);
+    else
+      launch_distortion<double>(d_x.as<double>(), n, dim, dim, d_ref.as<double>(),
+                                d_sq.as<double>(), nullptr, d_out.as<double>(), 1, st.s);
+    MB_CUDA(cudaMemcpyAsync(out, d_out.ptr, 8, cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+int moshpit_mean_of(int dtype, const void* peers, std::uint64_t n, std::uint64_t dim,
+                    void* mean_out) {
+  return moshpit_group_mean(dtype, peers, n, dim, nullptr, n, mean_out);
+}
+
+// ---------------------------------------------------------------------------
+// run_moshpit (protocols.hpp:108-179) with host buffers
+// ---------------------------------------------------------------------------
+int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T,
+                        const void* initial, std::uint64_t n, std::uint64_t dim,
+                        double p_round, std::uint64_t seed, std::uint32_t rounds, int diag,
+                        double* initial_distortion, double* distortion, double* mean_drift,
+                        std::uint32_t* active_counts, double* cost_units, void* final_out) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    // protocols.hpp:112-117, in order
+    if (M < 1 || d < 1 || T < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (p_round < 0.0 || p_round > 1.0)
+      throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
+    if (n == 0) throw std::invalid_argument("run_moshpit: no peers");
+    if (n > moshpit_grid_capacity(M, d))
+      throw std::invalid_argument("run_moshpit: N exceeds grid capacity M^d");
+    if (diag < MOSHPIT_DIAG_NONE || diag > MOSHPIT_DIAG_EXACT)
+      throw std::invalid_argument("run_moshpit: unknown diagnostics mode");
+    require_device();
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    StreamHolder st;
+    const std::uint64_t ld = padded_ld(dim, es);
+    DeviceBuffer d_x(n * ld * es), d_ref(dim * 8 + 16), d_mean(dim * 8 + 16), d_sq(n * 8),
+        d_part(diag_partial_elems(n, dim) * 8 + 16), d_out((2 * rounds + 2) * 8);
+    MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, initial, dim * es, dim * es, n,
+                              cudaMemcpyHostToDevice, st.s));
+    const int exact = diag == MOSHPIT_DIAG_EXACT;
+    auto record = [&](double* dist_slot, double* drift_slot) {
+      if (dtype == MOSHPIT_F32) {
+        launch_distortion<float>(d_x.as<float>(), n, ld, dim, d_ref.as<double>(),
+                                 d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
+        if (drift_slot)
+          launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, nullptr,
+                                        d_mean.as<double>(), st.s);
+      } else {
+        launch_distortion<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
+                                  d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
+        if (drift_slot)
+          launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, nullptr,
+                                         d_mean.as<double>(), st.s);
+      }
+      if (drift_slot)
+        launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part.as<double>(),
+                     drift_slot, exact, st.s);
+    };
+    double* outp = d_out.as<double>();
+    if (diag != MOSHPIT_DIAG_NONE) {
+      // reference = mean_of(initial) (protocols.hpp:119), in fp64
+      if (dtype == MOSHPIT_F32)
+        launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, nullptr, d_ref.as<double>(),
+                                      st.s);
+      else
+        launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, nullptr,
+                                       d_ref.as<double>(), st.s);
+      record(outp, nullptr);
+    }
+    Plane plane(M, d, n, dev);
+    Xoshiro cells = Xoshiro::named(seed, "cells");
+    plane.init_cells(cells, st.s);
+    Xoshiro fail = Xoshiro::named(seed, "failures");
+    Xoshiro clock = Xoshiro::named(seed, "priorities");
+    for (std::uint32_t r = 0; r < rounds; ++r) {
+      active_counts[r] = plane.round(&fail, p_round, clock, dtype, d_x.ptr, dim, ld, st.s,
+                                     MOSHPIT_KERNEL_AUTO);
+      if (diag != MOSHPIT_DIAG_NONE) record(outp + 2 + r, outp + 2 + rounds + r);
+    }
+    if (diag != MOSHPIT_DIAG_NONE) {
+      std::vector<double> h(2 * rounds + 2);
+      MB_CUDA(cudaMemcpyAsync(h.data(), outp, h.size() * 8, cudaMemcpyDeviceToHost, st.s));
+      MB_CUDA(cudaStreamSynchronize(st.s));
+      *initial_distortion = h[0];
+      for (std::uint32_t r = 0; r < rounds; ++r) {
+        distortion[r] = h[2 + r];
+        mean_drift[r] = h[2 + rounds + r];
+      }
+    } else {
+      *initial_distortion = std::nan("");
+      for (std::uint32_t r = 0; r < rounds; ++r) distortion[r] = mean_drift[r] = std::nan("");
+    }
+    if (final_out)
+      MB_CUDA(cudaMemcpy2DAsync(final_out, dim * es, d_x.ptr, ld * es, dim * es, n,
+                                cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+    *cost_units = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
+                                              static_cast<std::uint32_t>(dim));
+  });
+}
+
+// ---------------------------------------------------------------------------
+// optimizer::detail::moshpit_average (optimizer.hpp:249-284) with host buffers
+// ---------------------------------------------------------------------------
+int moshpit_moshpit_average(int dtype, void* thetas, std::uint64_t n, std::uint64_t dim,
+                            std::uint32_t M, std::uint32_t d, std::uint32_t rounds,
+                            moshpit_rng_state* stream) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (n <= 1) return;  // optimizer.hpp:253: no draws at all
+    if (M < 1 || d < 1) throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    require_device();
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    StreamHolder st;
+    const std::uint64_t ld = padded_ld(dim, es);
+    DeviceBuffer d_x(n * ld * es);
+    MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, thetas, dim * es, dim * es, n,
+                              cudaMemcpyHostToDevice, st.s));
+    Xoshiro s = from_state(stream);
+    Plane plane(M, d, n, dev);
+    plane.init_cells(s, st.s);
+    for (std::uint32_t r = 0; r < rounds; ++r)
+      plane.round(nullptr, 0.0, s, dtype, d_x.ptr, dim, ld, st.s, MOSHPIT_KERNEL_AUTO);
+    MB_CUDA(cudaMemcpy2DAsync(thetas, dim * es, d_x.ptr, ld * es, dim * es, n,
+                              cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+    to_state(s, stream);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// device-resident engine
+// ---------------------------------------------------------------------------
+int moshpit_engine_create(std::uint32_t M, std::uint32_t d, std::uint64_t n, double p_round,
+                          std::uint64_t seed, int device, moshpit_engine** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("engine_create: null out");
+    if (M < 1 || d < 1) throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (p_round < 0.0 || p_round > 1.0)
+      throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
+    require_device();
+    DeviceGuard g(device);
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    auto e = std::make_unique<moshpit_engine>();
+    e->plane = std::make_unique<Plane>(M, d, n, dev);
+    e->p = p_round;
+    Xoshiro cells = Xoshiro::named(seed, "cells");
+    e->fail = Xoshiro::named(seed, "failures");
+    e->clock = Xoshiro::named(seed, "priorities");
+    StreamHolder st;
+    e->plane->init_cells(cells, st.s);
+    MB_CUDA(cudaStreamSynchronize(st.s));
+    *out = e.release();
+  });
+}
+
+int moshpit_engine_destroy(moshpit_engine* e) {
+  return guarded([&] {
+    if (!e) return;
+    if (e->plane) {
+      DeviceGuard g(e->plane->device);
+      cudaDeviceSynchronize();
+      e->plane.reset();
+    }
+    delete e;
+  });
+}
+
+int moshpit_engine_set_kernel(moshpit_engine* e, int variant) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (variant < MOSHPIT_KERNEL_AUTO || variant > MOSHPIT_KERNEL_BULK)
+      throw std::invalid_argument("unknown kernel variant");
+    e->variant = variant;
+  });
+}
+
+int moshpit_engine_round(moshpit_engine* e, int dtype, void* state, std::uint64_t dim,
+                         std::uint64_t ld, void* stream, std::uint32_t* active_out) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (state) check_state(dtype, state, dim, ld);
+    DeviceGuard g(e->plane->device);
+    const std::uint32_t a = e->plane->round(&e->fail, e->p, e->clock, dtype, state, dim, ld,
+                                            static_cast<cudaStream_t>(stream), e->variant);
+    if (active_out) *active_out = a;
+  });
+}
+
+int moshpit_engine_stats(moshpit_engine* e, std::uint64_t* rounds,
+                         std::uint64_t* active_rows_total) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    DeviceGuard g(e->plane->device);
+    if (e->plane->last_stream) MB_CUDA(cudaStreamSynchronize(e->plane->last_stream));
+    else MB_CUDA(cudaDeviceSynchronize());
+    unsigned long long t[2];
+    MB_CUDA(cudaMemcpy(t, e->plane->totals.ptr, 16, cudaMemcpyDeviceToHost));
+    if (rounds) *rounds = e->plane->rounds_done;
+    if (active_rows_total) *active_rows_total = t[0];
+  });
+}
+
+int moshpit_engine_set_timing(moshpit_engine* e, int enable) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    e->plane->timing = enable != 0;
+    e->plane->tev_used = 0;
+  });
+}
+
+int moshpit_engine_kernel_time(moshpit_engine* e, double* total_ms, std::uint64_t* launches) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    Plane& p = *e->plane;
+    DeviceGuard g(p.device);
+    double t = 0.0;
+    for (std::size_t i = 0; i < p.tev_used; ++i) {
+      MB_CUDA(cudaEventSynchronize(p.tev[i].second));
+      float ms = 0.f;
+      MB_CUDA(cudaEventElapsedTime(&ms, p.tev[i].first, p.tev[i].second));
+      t += ms;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = p.tev_used;
+    p.tev_used = 0;
+  });
+}
+
+int moshpit_engine_tables(moshpit_engine* e, std::uint32_t* members, std::uint32_t* group_off,
+                          std::uint32_t* n_groups, std::uint8_t* void_flags,
+                          std::uint32_t* ranks, std::uint32_t* keys) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    Plane& p = *e->plane;
+    DeviceGuard g(p.device);
+    if (p.last_stream) MB_CUDA(cudaStreamSynchronize(p.last_stream));
+    else MB_CUDA(cudaDeviceSynchronize());
+    std::uint32_t counts[4];
+    MB_CUDA(cudaMemcpy(counts, p.counts.ptr, 16, cudaMemcpyDeviceToHost));
+    if (n_groups) *n_groups = counts[0];
+    if (members) MB_CUDA(cudaMemcpy(members, p.members.ptr, p.n * 4, cudaMemcpyDeviceToHost));
+    if (group_off)
+      MB_CUDA(cudaMemcpy(group_off, p.goff.ptr, (counts[0] + 1) * 4, cudaMemcpyDeviceToHost));
+    if (void_flags) MB_CUDA(cudaMemcpy(void_flags, p.gvoid.ptr, counts[0], cudaMemcpyDeviceToHost));
+    if (ranks) MB_CUDA(cudaMemcpy(ranks, p.rank.ptr, p.n * 4, cudaMemcpyDeviceToHost));
+    if (keys && p.grid.klen) {
+      std::vector<std::uint64_t> packed(p.n);
+      MB_CUDA(cudaMemcpy(packed.data(), p.keys.ptr, p.n * 8, cudaMemcpyDeviceToHost));
+      for (std::uint64_t i = 0; i < p.n; ++i) p.grid.unpack(packed[i], keys + i * p.grid.klen);
+    }
+  });
+}
+
+int moshpit_fill_synthetic(int dtype, void* state, std::uint64_t n, std::uint64_t dim,
+                           std::uint64_t ld, std::uint64_t seed, std::uint64_t col0,
+                           void* stream) {
+  return guarded([&] {
+    elem_size(dtype);
+    if (ld < dim) throw std::invalid_argument("fill_synthetic: ld < dim");
+    require_device();
+    if (dtype == MOSHPIT_F32)
+      launch_fill_synthetic<float>(static_cast<float*>(state), n, dim, ld, seed, col0,
+                                   static_cast<cudaStream_t>(stream));
+    else
+      launch_fill_synthetic<double>(static_cast<double*>(state), n, dim, ld, seed, col0,
+                                    static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

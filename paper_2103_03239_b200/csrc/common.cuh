@@ -1,0 +1,282 @@
+// common.cuh -- shared host/device plumbing for the Moshpit B200 engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+namespace mb200 {
+
+// ---------------------------------------------------------------------------
+// Errors: the C ABI maps these onto MOSHPIT_ERR_* (reference exception types).
+// ---------------------------------------------------------------------------
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define MB_CUDA(expr)                                                        \
+  do {                                                                       \
+    cudaError_t mb_err_ = (expr);                                            \
+    if (mb_err_ != cudaSuccess)                                              \
+      throw ::mb200::CudaError(std::string(#expr) + ": " +                   \
+                               cudaGetErrorString(mb_err_));                 \
+  } while (0)
+
+#define MB_LAUNCH_CHECK() MB_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Host RNG -- the reference's generator (rng.hpp:12-127): splitmix64 seeding,
+// xoshiro256**, fnv1a-named streams.  Draws stay on the host: they are
+// sequential by construction and cost O(n) per round (hard part 6).
+// ---------------------------------------------------------------------------
+inline std::uint64_t splitmix64(std::uint64_t& state) {
+  std::uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+inline std::uint64_t fnv1a(std::string_view s) {
+  std::uint64_t h = 0xCBF29CE484222325ULL;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 0x100000001B3ULL;
+  }
+  return h;
+}
+
+struct Xoshiro {
+  std::uint64_t s[4]{};
+  bool have_spare = false;
+  double spare = 0.0;
+
+  Xoshiro() = default;
+  explicit Xoshiro(std::uint64_t seed) {
+    std::uint64_t sm = seed;
+    for (auto& w : s) w = splitmix64(sm);
+  }
+  static Xoshiro named(std::uint64_t root, std::string_view name) {
+    std::uint64_t mix = root ^ fnv1a(name);
+    return Xoshiro(splitmix64(mix));
+  }
+  static Xoshiro named(std::uint64_t root, std::string_view name,
+                       std::uint64_t index) {
+    std::uint64_t mix = root ^ fnv1a(name);
+    mix = splitmix64(mix) ^ (0x9E3779B97F4A7C15ULL * (index + 1));
+    return Xoshiro(splitmix64(mix));
+  }
+  static std::uint64_t rotl(std::uint64_t x, int k) {
+    return (x << k) | (x >> (64 - k));
+  }
+  std::uint64_t next() {
+    const std::uint64_t result = rotl(s[1] * 5, 7) * 9;
+    const std::uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return result;
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  std::uint64_t below(std::uint64_t n) {
+    const std::uint64_t threshold = (~n + 1) % n;
+    for (;;) {
+      const std::uint64_t r = next();
+      if (r >= threshold) return r % n;
+    }
+  }
+  double normal();
+  bool bernoulli(double p) { return uniform() < p; }
+};
+
+// ---------------------------------------------------------------------------
+// Grid arithmetic (core.hpp:19-34) and packed group keys.
+// A GroupKey (d-1 chunk indices, lexicographic) is packed mixed-radix with the
+// OLDEST index most significant, so numeric order == std::map<GroupKey> order
+// and next_group_key (drop oldest, append rank) is (key % M^(d-2)) * M + rank.
+// ---------------------------------------------------------------------------
+struct Grid {
+  std::uint32_t M = 1, d = 1;
+  std::uint32_t klen = 0;       // d - 1
+  std::uint64_t capacity = 1;   // M^d
+  std::uint64_t pow_drop = 1;   // M^(d-2) (1 when d <= 2)
+
+  Grid() = default;
+  Grid(std::uint32_t M_, std::uint32_t d_) : M(M_), d(d_) {
+    if (M < 1 || d < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    klen = d - 1;
+    capacity = 1;
+    for (std::uint32_t j = 0; j < d; ++j) {
+      if (capacity > (UINT64_MAX >> 1) / M)
+        throw std::invalid_argument("GridConfig: M^d overflows 63 bits");
+      capacity *= M;
+    }
+    pow_drop = 1;
+    for (std::uint32_t j = 0; j + 2 < d; ++j) pow_drop *= M;
+  }
+  // matchmaking.hpp:46-59, packed
+  std::uint64_t initial_key(std::uint64_t cell) const {
+    std::uint64_t rest = cell / M, key = 0;
+    for (std::uint32_t j = 1; j < d; ++j) {
+      key = key * M + rest % M;
+      rest /= M;
+    }
+    return key;
+  }
+  void unpack(std::uint64_t key, std::uint32_t* digits) const {
+    for (std::uint32_t i = klen; i-- > 0;) {
+      digits[i] = static_cast<std::uint32_t>(key % M);
+      key /= M;
+    }
+  }
+};
+
+inline std::uint32_t ceil_div_u32(std::uint64_t a, std::uint64_t b) {
+  return static_cast<std::uint32_t>((a + b - 1) / b);
+}
+
+// ---------------------------------------------------------------------------
+// RAII device / pinned buffers.
+// ---------------------------------------------------------------------------
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  std::size_t bytes = 0;
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t b) { resize(b); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  void resize(std::size_t b) {
+    if (b <= bytes && ptr) return;
+    release();
+    MB_CUDA(cudaMalloc(&ptr, b ? b : 16));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+struct PinnedBuffer {
+  void* ptr = nullptr;
+  std::size_t bytes = 0;
+  PinnedBuffer() = default;
+  PinnedBuffer(const PinnedBuffer&) = delete;
+  PinnedBuffer& operator=(const PinnedBuffer&) = delete;
+  ~PinnedBuffer() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  void resize(std::size_t b) {
+    if (b <= bytes && ptr) return;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    MB_CUDA(cudaMallocHost(&ptr, b ? b : 16));
+    bytes = b;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+// Restores the caller's current device on scope exit (torch and other
+// callers keep their own notion of the current device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    MB_CUDA(cudaGetDevice(&prev));
+    if (dev >= 0 && dev != prev) MB_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void require_device();  // throws CudaError when no usable device exists
+
+// ---------------------------------------------------------------------------
+// Kernel entry points (defined in the .cu files).
+// ---------------------------------------------------------------------------
+
+// Kernel 1: group formation over packed keys or digit keys.
+struct GroupArgs {
+  std::uint32_t n = 0;
+  std::uint32_t cap = 0;
+  std::uint32_t M = 1;
+  std::uint64_t pow_drop = 1;   // next key = (key % pow_drop) * M + rank
+  int advance_keys = 0;         // round mode: update keys in place
+  int klen_zero = 0;            // d == 1: keys stay empty (0)
+  std::uint64_t* keys = nullptr;          // packed keys [n] (round mode)
+  const std::uint32_t* digit_keys = nullptr;  // [n*dklen] (standalone mode)
+  std::uint32_t dklen = 0;
+  const std::uint64_t* ts = nullptr;      // [n] 48-bit priorities
+  const std::uint8_t* failed = nullptr;   // [n] or null
+  const std::uint32_t* ids = nullptr;     // [n] or null (id = index)
+  // outputs
+  std::uint32_t* members = nullptr;  // [n]
+  std::uint32_t* goff = nullptr;     // [n+1]
+  std::uint8_t* gvoid = nullptr;     // [n]
+  std::uint32_t* rank = nullptr;     // [n] by input index
+  std::uint32_t* act = nullptr;      // [n] non-voided group ids
+  std::uint32_t* counts = nullptr;   // [0]=n_groups [1]=n_act [2]=peers in act
+  unsigned long long* totals = nullptr;  // [0]+=peers in act (running)
+  // global scratch (used when the sort does not fit in shared memory)
+  std::uint32_t* sidx = nullptr;  // [pow2(n)]
+  std::uint32_t* scs = nullptr;   // [n]
+  std::uint32_t* sgi = nullptr;   // [n]
+};
+
+std::size_t group_smem_bytes(std::uint32_t n, bool packed);
+void launch_form_groups(const GroupArgs& a, bool packed, cudaStream_t s);
+void launch_initial_keys(const std::uint64_t* cells, std::uint64_t* keys,
+                         std::uint64_t n, std::uint32_t M, std::uint32_t d,
+                         cudaStream_t s);
+
+// Kernel 2: segmented group mean over the active groups.
+struct MeanPlan {
+  int grid = 0;
+  int variant = 0;
+};
+template <typename T>
+void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
+                       const std::uint32_t* members, const std::uint32_t* goff,
+                       const std::uint32_t* act, const std::uint32_t* counts,
+                       std::uint32_t max_group, int variant, cudaStream_t s);
+
+// Diagnostics and helpers.
+template <typename T, typename Acc>
+void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
+                    std::uint64_t dim, const std::uint32_t* rows, Acc* out,
+                    cudaStream_t s);
+template <typename T>
+void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
+                       std::uint64_t dim, const double* ref, double* sq_scratch,
+                       double* partial_scratch, double* out, int exact,
+                       cudaStream_t s);
+void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
+                  double* partial_scratch, double* out, int exact,
+                  cudaStream_t s);
+std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim);
+template <typename T>
+void launch_fill_synthetic(T* x, std::uint64_t n, std::uint64_t dim,
+                           std::uint64_t ld, std::uint64_t seed,
+                           std::uint64_t col0, cudaStream_t s);
+template <typename T>
+void launch_broadcast_rows(T* dst, std::uint64_t ld, const T* row,
+                           std::uint64_t n, std::uint64_t dim, cudaStream_t s);
+
+}  // namespace mb200

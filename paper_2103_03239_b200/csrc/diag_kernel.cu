@@ -1,0 +1,294 @@
+// diag_kernel.cu -- TrialReport diagnostics and helpers on the GPU.
+//
+// record_round (protocols.hpp:68-84) needs, after every round:
+//   distortion = pairwise_i( sum_j (theta_ij - ref_j)^2 ) / N   (core.hpp:111-126)
+//   mean       = mean_of(vectors), pairwise over peers           (core.hpp:128-133)
+//   drift      = sqrt(sum_j (mean_j-ref_j)^2) / max(sqrt(sum_j ref_j^2), 1e-300)
+// The reference sums over j SEQUENTIALLY.  MOSHPIT_DIAG_EXACT reproduces that
+// order (one dependent chain per peer: bit parity, slow at large D);
+// MOSHPIT_DIAG_FAST sums fixed chunks in parallel and folds them in a fixed
+// order (deterministic, ~1e-15 relative to the sequential sum).  Column means
+// use the reference pairwise tree over peers in both modes, in fp64.
+#include "common.cuh"
+#include "pairwise.cuh"
+
+namespace mb200 {
+namespace {
+
+template <typename Acc>
+struct AccOps;
+template <>
+struct AccOps<double> {
+  __device__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+template <>
+struct AccOps<float> {
+  __device__ static float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+};
+
+// One thread per coordinate: pairwise tree over the (selected) rows.
+template <typename T, typename Acc>
+__global__ void colmean_kernel(const T* __restrict__ x, std::uint64_t n,
+                               std::uint64_t ld, std::uint64_t dim,
+                               const std::uint32_t* __restrict__ rows,
+                               Acc* __restrict__ out) {
+  const std::uint64_t j = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  auto ld_fn = [&](std::uint32_t i) -> Acc {
+    const std::uint64_t r = rows ? rows[i] : i;
+    return (Acc)x[r * ld + j];
+  };
+  const Acc s = pairwise_rt<Acc>(ld_fn, (std::uint32_t)n,
+                                 [](Acc a, Acc b) { return AccOps<Acc>::add(a, b); },
+                                 (Acc)0);
+  out[j] = AccOps<Acc>::div(s, (Acc)n);
+}
+
+// EXACT: per peer, sequential over j exactly as core.hpp:118-122.
+template <typename T>
+__global__ void dist_rows_exact(const T* __restrict__ x, std::uint64_t n,
+                                std::uint64_t ld, std::uint64_t dim,
+                                const double* __restrict__ ref,
+                                double* __restrict__ sq) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const T* row = x + i * ld;
+  double acc = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double diff = __dsub_rn((double)row[j], ref[j]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  sq[i] = acc;
+}
+
+constexpr int kRedThreads = 256;
+constexpr std::uint64_t kChunk = 1 << 16;
+
+__device__ double block_sum_fixed(double v) {
+  __shared__ double buf[kRedThreads];
+  buf[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) buf[threadIdx.x] = __dadd_rn(buf[threadIdx.x], buf[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+// FAST: block (c, i) sums chunk c of row i in a fixed order.
+template <typename T>
+__global__ void dist_rows_fast(const T* __restrict__ x, std::uint64_t ld,
+                               std::uint64_t dim, const double* __restrict__ ref,
+                               std::uint64_t nch, double* __restrict__ partial) {
+  const std::uint64_t c = blockIdx.x, i = blockIdx.y;
+  const T* row = x + i * ld;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double acc = 0.0;
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
+    const double diff = __dsub_rn((double)row[j], ref[j]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  const double s = block_sum_fixed(acc);
+  if (threadIdx.x == 0) partial[i * nch + c] = s;
+}
+
+__global__ void fold_rows(const double* __restrict__ partial, std::uint64_t n,
+                          std::uint64_t nch, double* __restrict__ sq) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (std::uint64_t c = 0; c < nch; ++c) acc = __dadd_rn(acc, partial[i * nch + c]);
+  sq[i] = acc;
+}
+
+// pairwise over peers, / n  (core.hpp:125)
+__global__ void finish_distortion(const double* __restrict__ sq, std::uint64_t n,
+                                  double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (n == 0) {
+    *out = 0.0;
+    return;
+  }
+  auto ld_fn = [&](std::uint32_t i) { return sq[i]; };
+  const double s = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
+                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
+  *out = __ddiv_rn(s, (double)n);
+}
+
+// drift, EXACT: protocols.hpp:75-81 in order.
+__global__ void drift_exact(const double* __restrict__ mean,
+                            const double* __restrict__ ref, std::uint64_t dim,
+                            double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double drift_sq = 0.0, ref_sq = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double dm = __dsub_rn(mean[j], ref[j]);
+    drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
+    ref_sq = __dadd_rn(ref_sq, __dmul_rn(ref[j], ref[j]));
+  }
+  const double den = fmax(__dsqrt_rn(ref_sq), 1e-300);
+  *out = __ddiv_rn(__dsqrt_rn(drift_sq), den);
+}
+
+__global__ void drift_fast_partial(const double* __restrict__ mean,
+                                   const double* __restrict__ ref,
+                                   std::uint64_t dim, double* __restrict__ partial) {
+  const std::uint64_t c = blockIdx.x;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double a = 0.0, b = 0.0;
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
+    const double dm = __dsub_rn(mean[j], ref[j]);
+    a = __dadd_rn(a, __dmul_rn(dm, dm));
+    b = __dadd_rn(b, __dmul_rn(ref[j], ref[j]));
+  }
+  const double sa = block_sum_fixed(a);
+  const double sb = block_sum_fixed(b);
+  if (threadIdx.x == 0) {
+    partial[2 * c] = sa;
+    partial[2 * c + 1] = sb;
+  }
+}
+
+__global__ void drift_fast_finish(const double* __restrict__ partial,
+                                  std::uint64_t nch, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (std::uint64_t c = 0; c < nch; ++c) {
+    a = __dadd_rn(a, partial[2 * c]);
+    b = __dadd_rn(b, partial[2 * c + 1]);
+  }
+  *out = __ddiv_rn(__dsqrt_rn(a), fmax(__dsqrt_rn(b), 1e-300));
+}
+
+__device__ __forceinline__ std::uint64_t splitmix64_dev(std::uint64_t s) {
+  std::uint64_t z = s + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void fill_synthetic_kernel(T* __restrict__ x, std::uint64_t n,
+                                      std::uint64_t dim, std::uint64_t ld,
+                                      std::uint64_t seed, std::uint64_t col0) {
+  const std::uint64_t total = n * dim;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+       e < total; e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t i = e / dim, j = e % dim;
+    const std::uint64_t z = splitmix64_dev(seed ^ (i << 32) ^ (col0 + j));
+    x[i * ld + j] = (T)((double)(z >> 40) * 0x1.0p-24);
+  }
+}
+
+template <typename T>
+__global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
+                                      const T* __restrict__ row, std::uint64_t n,
+                                      std::uint64_t dim) {
+  const std::uint64_t total = n * dim;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+       e < total; e += (std::uint64_t)gridDim.x * blockDim.x)
+    dst[(e / dim) * ld + e % dim] = row[e % dim];
+}
+
+unsigned grid_for(std::uint64_t work, unsigned threads) {
+  std::uint64_t b = (work + threads - 1) / threads;
+  if (b > 148ull * 64) b = 148ull * 64;
+  return (unsigned)(b ? b : 1);
+}
+
+}  // namespace
+
+std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
+  const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+  const std::uint64_t a = n * (nch ? nch : 1), b = 2 * (nch ? nch : 1);
+  return a > b ? a : b;
+}
+
+template <typename T, typename Acc>
+void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
+                    std::uint64_t dim, const std::uint32_t* rows, Acc* out,
+                    cudaStream_t s) {
+  if (dim == 0 || n == 0) return;
+  const unsigned threads = 128;
+  colmean_kernel<T, Acc><<<(unsigned)((dim + threads - 1) / threads), threads, 0, s>>>(
+      x, n, ld, dim, rows, out);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
+                       std::uint64_t dim, const double* ref, double* sq,
+                       double* partial, double* out, int exact, cudaStream_t s) {
+  if (n == 0) {
+    finish_distortion<<<1, 1, 0, s>>>(sq, 0, out);
+    MB_LAUNCH_CHECK();
+    return;
+  }
+  if (exact || dim == 0) {
+    dist_rows_exact<T><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, n, ld, dim, ref, sq);
+  } else {
+    const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+    dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch, partial);
+    MB_LAUNCH_CHECK();
+    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
+  }
+  MB_LAUNCH_CHECK();
+  finish_distortion<<<1, 1, 0, s>>>(sq, n, out);
+  MB_LAUNCH_CHECK();
+}
+
+void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
+                  double* partial, double* out, int exact, cudaStream_t s) {
+  if (exact || dim == 0) {
+    drift_exact<<<1, 1, 0, s>>>(mean, ref, dim, out);
+  } else {
+    const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+    drift_fast_partial<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, partial);
+    MB_LAUNCH_CHECK();
+    drift_fast_finish<<<1, 1, 0, s>>>(partial, nch, out);
+  }
+  MB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_fill_synthetic(T* x, std::uint64_t n, std::uint64_t dim,
+                           std::uint64_t ld, std::uint64_t seed,
+                           std::uint64_t col0, cudaStream_t s) {
+  if (n == 0 || dim == 0) return;
+  fill_synthetic_kernel<T><<<grid_for(n * dim, 256), 256, 0, s>>>(x, n, dim, ld, seed, col0);
+  MB_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_broadcast_rows(T* dst, std::uint64_t ld, const T* row,
+                           std::uint64_t n, std::uint64_t dim, cudaStream_t s) {
+  if (n == 0 || dim == 0) return;
+  broadcast_rows_kernel<T><<<grid_for(n * dim, 256), 256, 0, s>>>(dst, ld, row, n, dim);
+  MB_LAUNCH_CHECK();
+}
+
+#define MB_INST(T)                                                                      \
+  template void launch_colmean<T, double>(const T*, std::uint64_t, std::uint64_t,       \
+                                          std::uint64_t, const std::uint32_t*, double*, \
+                                          cudaStream_t);                                \
+  template void launch_distortion<T>(const T*, std::uint64_t, std::uint64_t,            \
+                                     std::uint64_t, const double*, double*, double*,    \
+                                     double*, int, cudaStream_t);                       \
+  template void launch_fill_synthetic<T>(T*, std::uint64_t, std::uint64_t,              \
+                                         std::uint64_t, std::uint64_t, std::uint64_t,   \
+                                         cudaStream_t);                                 \
+  template void launch_broadcast_rows<T>(T*, std::uint64_t, const T*, std::uint64_t,    \
+                                         std::uint64_t, cudaStream_t);
+MB_INST(float)
+MB_INST(double)
+template void launch_colmean<float, float>(const float*, std::uint64_t, std::uint64_t,
+                                          std::uint64_t, const std::uint32_t*, float*,
+                                          cudaStream_t);
+#undef MB_INST
+
+}  // namespace mb200
