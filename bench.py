@@ -312,7 +312,10 @@ def run_mine(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
-                         "traffic": traffic, "kernel": "group_mean_register (kernel 2)",
+                         "traffic": traffic,
+                         "traffic_over_algorithmic": (traffic_ent or {}).get("traffic_over_algorithmic"),
+                         "traffic_source": "profiles/ncu_summary.json (ncu --set full, one launch)",
+                         "kernel": "group_mean_register (kernel 2)",
                          "algorithmic_bytes": "2 * 4 B * D * rows in non-voided groups",
                          "avg_launch_ms": round(k_ms / max(k_launches, 1), 4),
                          "launches": k_launches, "active_rows_timed": active_rows,

@@ -1,0 +1,48 @@
+"""The reference's own test cases, compiled against the drop-in C++ header
+(include/moshpit_b200/moshpit.hpp) and run on the GPU; plus a golden
+TrialReport compared bit-for-bit with the unmodified reference's."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+
+
+def build_dropin():
+    lib = os.path.join(ROOT, "paper_2103_03239_b200")
+    cmd = ["g++", "-std=c++20", "-O2", SRC, "-I", os.path.join(ROOT, "include"), "-L", lib,
+           "-lmoshpit_b200", f"-Wl,-rpath,{lib}", "-o", BIN]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    return BIN
+
+
+def test_dropin_header_compiles_and_links(mb):
+    mb.lib()
+    build_dropin()
+    assert os.path.exists(BIN)
+
+
+@pytest.mark.gpu
+def test_reference_cases_through_dropin_header(mb, golden):
+    if not os.path.exists(BIN):
+        build_dropin()
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    lines = r.stdout.strip().splitlines()
+    assert lines[-1].startswith("PASS=") and lines[-1].endswith("FAIL=0")
+    kv = [ln.split("=", 1) for ln in lines[:-1]]
+    case = [c for c in golden["run_moshpit"]
+            if (c["M"], c["d"], c["n"], c["dim"], c["p"], c["seed"], c["rounds"]) ==
+            (32, 2, 1024, 4, 0.01, 7, 10)][0]
+    assert kv[0] == ["initial_distortion", case["initial_distortion"]]
+    dist = [v for k, v in kv if k == "distortion"]
+    drift = [v for k, v in kv if k == "mean_drift"]
+    act = [int(v) for k, v in kv if k == "active"]
+    assert dist == case["distortion"]
+    assert drift == case["mean_drift"]
+    assert act == case["active_counts"]
+    assert [v for k, v in kv if k == "cost_units"] == [case["cost_units"]]
