@@ -129,6 +129,9 @@ def load_traffic(kernel_name, cfg_name):
 # ---------------------------------------------------------------------------
 # CPU reference arm / baseline: unmodified run_moshpit on column slices
 # ---------------------------------------------------------------------------
+_CALIB = {}
+
+
 def cpu_reference(cfg_name, budget_s, threads=None):
     from oracle.oracle import REF_SO, Checker
     M, d, N, D, p, R = CONFIGS[cfg_name]
@@ -150,10 +153,13 @@ def cpu_reference(cfg_name, budget_s, threads=None):
         run_s = time.perf_counter() - t0
         return dict(kind="port", cores=1, run_s=run_s, cols=width, rounds=R, N=N, D=D,
                     sample=f"oracle port, 1 thread, {width} of {D} columns, {R} rounds")
-    # calibrate on one slice per thread
-    run_s, _, _ = chk.slice_bench(M, d, N, width, threads, 0, INIT_SEED, PROTOCOL_SEED, p, R,
-                                  threads)
-    per_slice_batch = max(run_s, 1e-3)
+    # calibrate once: one slice per thread
+    key = (cfg_name, threads)
+    if key not in _CALIB:
+        run_s, _, _ = chk.slice_bench(M, d, N, width, threads, 0, INIT_SEED, PROTOCOL_SEED, p, R,
+                                      threads)
+        _CALIB[key] = max(run_s, 1e-3)
+    per_slice_batch = _CALIB[key]
     batches = max(1, int(budget_s / per_slice_batch))
     slices = threads * batches
     run_s, init_s, _ = chk.slice_bench(M, d, N, width, slices, 0, INIT_SEED, PROTOCOL_SEED, p, R,
@@ -177,8 +183,9 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     cfg = args.config
-    M, d, N, D, p, R = CONFIGS[cfg]
-    per_step = float(os.environ.get("MOSHPIT_REF_STEP_S", "4"))
+    # each step = one bounded sample; the whole run stays within ~2-3 minutes
+    total = float(os.environ.get("MOSHPIT_REF_TOTAL_S", "120"))
+    per_step = max(0.25, min(10.0, total / (args.steps + args.warmup)))
     vals, mss = [], []
     res = None
     for i in range(args.warmup + args.steps):

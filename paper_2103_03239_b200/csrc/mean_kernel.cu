@@ -18,6 +18,8 @@
 // tree is register-local, so no cross-lane shuffles are needed and the fp32
 // result is bit-identical to the fp32 restatement of the reference, and the
 // fp64 instantiation bit-identical to the reference itself.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mb200 {
@@ -159,6 +161,169 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk (TMA) variant: one producer warp streams every member-row tile of an
+// item into a shared-memory ring with cp.async.bulk (global -> shared, mbarrier
+// complete_tx, L2 evict-first), consumer warps evaluate the same register tree
+// from shared memory and store the mean with 128-bit streaming stores.  One
+// CTA per SM; the ring keeps `stages` items (up to ~190 KB) of loads in flight.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ std::uint64_t evict_first_policy() {
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes,
+                                         std::uint64_t* bar, std::uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+constexpr int kBulkTileVec = 128;  // 16-byte vectors per row tile (2 KB)
+constexpr int kBulkConsumerWarps = kBulkTileVec / 32;
+constexpr int kBulkThreads = kBulkTileVec + 32;
+constexpr int kBulkMaxRows = 32;
+
+struct BulkHdr {
+  std::uint32_t ids[kBulkMaxRows];
+  std::uint32_t n;
+  std::uint32_t nv;
+  std::uint64_t col;
+};
+
+template <int N, typename V>
+__device__ __forceinline__ void mean_fixed_smem(const V* in, V* base, std::uint64_t ld_vec,
+                                                std::uint64_t col, const std::uint32_t* ids) {
+  V x[32];
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = in[k * kBulkTileVec];
+  const V m = vdiv(tree<N, 0>(x), (std::uint32_t)N);
+#pragma unroll
+  for (int k = 0; k < N; ++k) vstore(base + (std::uint64_t)ids[k] * ld_vec + col, m);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    group_mean_bulk(MeanArgs<T> a, int stages, int srows) {
+  using V = typename V16<T>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  V* data = reinterpret_cast<V*>(smem);
+  BulkHdr* hdr = reinterpret_cast<BulkHdr*>(data + (std::size_t)stages * srows * kBulkTileVec);
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(hdr + stages);
+  std::uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumerWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const std::uint32_t n_act = a.counts[1];
+  const std::uint64_t n_items = (std::uint64_t)n_act * a.n_tiles;
+  V* base = reinterpret_cast<V*>(a.state);
+  int s = 0;
+  std::uint32_t ph = 0;
+  if (warp == kBulkConsumerWarps) {
+    // Producer warp: lane k owns member row k of the current group (ids
+    // cached in registers across the items of one group) and issues its own
+    // bulk copy; lane 0 arms the stage's full barrier first.
+    const std::uint64_t pol = evict_first_policy();
+    std::uint32_t cached = 0xffffffffu, n = 0, my_id = 0;
+    for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const std::uint32_t g = a.act[w / a.n_tiles];
+      if (g != cached) {
+        const std::uint32_t beg = a.goff[g];
+        n = a.goff[g + 1] - beg;
+        my_id = (std::uint32_t)lane < n ? a.members[beg + lane] : 0u;
+        cached = g;
+      }
+      const std::uint64_t col = (w % a.n_tiles) * kBulkTileVec;
+      const std::uint64_t left = a.nvec - col;
+      const std::uint32_t nv = left < (std::uint64_t)kBulkTileVec ? (std::uint32_t)left
+                                                                  : (std::uint32_t)kBulkTileVec;
+      if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
+      __syncwarp();
+      BulkHdr& h = hdr[s];
+      if ((std::uint32_t)lane < n) h.ids[lane] = my_id;
+      if (lane == 0) {
+        h.n = n;
+        h.nv = nv;
+        h.col = col;
+        mbar_arrive_expect_tx(&full[s], n * nv * 16u);
+      }
+      __syncwarp();
+      if ((std::uint32_t)lane < n)
+        bulk_g2s(data + ((std::size_t)s * srows + lane) * kBulkTileVec,
+                 base + (std::uint64_t)my_id * a.ld_vec + col, nv * 16u, &full[s], pol);
+      if (++s == stages) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    return;
+  }
+  const int t = threadIdx.x;  // consumer: one 16-byte column of the tile
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    mbar_wait(&full[s], ph);
+    const BulkHdr& h = hdr[s];
+    const std::uint32_t n = h.n;
+    if ((std::uint32_t)t < h.nv) {
+      const V* in = data + (std::size_t)s * srows * kBulkTileVec + t;
+      const std::uint64_t col = h.col + t;
+      switch (n) {
+#define MB_BCASE(N) \
+  case N:           \
+    mean_fixed_smem<N, V>(in, base, a.ld_vec, col, h.ids); \
+    break;
+        MB_BCASE(1) MB_BCASE(2) MB_BCASE(3) MB_BCASE(4) MB_BCASE(5) MB_BCASE(6) MB_BCASE(7)
+        MB_BCASE(8) MB_BCASE(9) MB_BCASE(10) MB_BCASE(11) MB_BCASE(12) MB_BCASE(13)
+        MB_BCASE(14) MB_BCASE(15) MB_BCASE(16) MB_BCASE(17) MB_BCASE(18) MB_BCASE(19)
+        MB_BCASE(20) MB_BCASE(21) MB_BCASE(22) MB_BCASE(23) MB_BCASE(24) MB_BCASE(25)
+        MB_BCASE(26) MB_BCASE(27) MB_BCASE(28) MB_BCASE(29) MB_BCASE(30) MB_BCASE(31)
+        MB_BCASE(32)
+#undef MB_BCASE
+        default: break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+}
+
 struct GridCache {
   int dev = -1;
   int grid[2] = {0, 0};
@@ -184,6 +349,14 @@ int mean_grid() {
   return cache.grid[slot];
 }
 
+bool bulk_default() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOSHPIT_KERNEL");
+    return e && std::string(e) == "bulk";
+  }();
+  return on;
+}
+
 }  // namespace
 
 template <typename T>
@@ -191,8 +364,6 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
                        const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint32_t* act, const std::uint32_t* counts,
                        std::uint32_t max_group, int variant, cudaStream_t s) {
-  (void)variant;
-  (void)max_group;
   if (dim == 0) return;
   constexpr int kVec = V16<T>::kN;
   MeanArgs<T> a;
@@ -204,7 +375,32 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
   a.goff = goff;
   a.act = act;
   a.counts = counts;
-  group_mean_register<T><<<mean_grid<T>(), kThreads, 0, s>>>(a);
+  const bool bulk_ok = max_group <= (std::uint32_t)kBulkMaxRows;
+  if (variant == 2 || (variant == 0 && bulk_ok && bulk_default())) {
+    if (!bulk_ok) throw std::invalid_argument("bulk kernel: groups larger than 32 members");
+    const std::uint32_t srows = max_group;
+    const std::size_t row_bytes = (std::size_t)kBulkTileVec * 16;
+    const std::size_t budget = 200 * 1024;
+    int stages = (int)(budget / (srows * row_bytes + sizeof(BulkHdr) + 16));
+    if (stages > 8) stages = 8;
+    if (stages < 2) stages = 2;
+    const std::size_t smem = (std::size_t)stages * (srows * row_bytes + sizeof(BulkHdr) + 16) + 128;
+    static thread_local int configured_dev[2] = {-1, -1};
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    const int slot = sizeof(T) == 4 ? 0 : 1;
+    if (configured_dev[slot] != dev) {
+      MB_CUDA(cudaFuncSetAttribute(group_mean_bulk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+      configured_dev[slot] = dev;
+    }
+    int sms = 0;
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    a.n_tiles = (a.nvec + kBulkTileVec - 1) / kBulkTileVec;
+    group_mean_bulk<T><<<sms, kBulkThreads, smem, s>>>(a, stages, (int)srows);
+  } else {
+    group_mean_register<T><<<mean_grid<T>(), kThreads, 0, s>>>(a);
+  }
   MB_LAUNCH_CHECK();
 }
 

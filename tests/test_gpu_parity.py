@@ -265,17 +265,35 @@ def test_moshpit_average_gpu_matches_golden(mb, oracle, golden):
 # ---------------------------------------------------------------------------
 # Device-resident engine: padded strides, both precisions, both kernels
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("dim,ldpad", [(1, 0), (3, 4), (5, 0), (64, 8), (1027, 4)])
+@pytest.mark.parametrize("dim,ldpad", [(1, 0), (3, 4), (5, 0), (64, 8), (1027, 4), (4099, 0)])
 @pytest.mark.parametrize("f64", [False, True])
-def test_engine_padded_rows_match_oracle(mb, oracle, torch, dim, ldpad, f64):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_engine_padded_rows_match_oracle(mb, oracle, torch, dim, ldpad, f64, kernel):
     M, d, n, p, R = 16, 2, 256, 0.05, 4
     dt = torch.float64 if f64 else torch.float32
     vec = 2 if f64 else 4
     ld = (dim + vec - 1) // vec * vec + ldpad
-    x, _, _ = engine_run(mb, torch, M, d, n, dim, p, 7, R, dtype=dt, ld=ld)
+    x, _, _ = engine_run(mb, torch, M, d, n, dim, p, 7, R, dtype=dt, ld=ld, kernel=kernel)
     init = oracle.init_state(INIT_SEED, n, dim, dtype=np.float64 if f64 else np.float32)
     _, want = oracle.run_moshpit(M, d, init, p, 7, R)
     assert bits_equal(x[:, :dim].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("M,d,n,p,R", [(32, 2, 1024, 0.01, 10), (8, 4, 4096, 0.02, 4),
+                                       (16, 3, 4096, 0.0, 3), (32, 2, 700, 0.05, 6),
+                                       (5, 3, 125, 0.1, 5)])
+def test_bulk_kernel_equals_register_kernel(mb, torch, M, d, n, p, R):
+    """Kernel-2 variants (register tree vs cp.async.bulk ring): bit-identical."""
+    dim = 70001
+    a, _, sa = engine_run(mb, torch, M, d, n, dim, p, 7, R, kernel=1)
+    b, _, sb = engine_run(mb, torch, M, d, n, dim, p, 7, R, kernel=2)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    assert sa == sb
+
+
+def test_bulk_kernel_rejects_groups_over_32(mb, torch):
+    with pytest.raises(mb.InvalidArgument):
+        engine_run(mb, torch, 64, 2, 200, 8, 0.0, 7, 1, kernel=2)
 
 
 def _slice_check(mb, oracle, x, M, d, n, p, seed, R, cols):
