@@ -174,6 +174,38 @@ int moshpit_engine_tables(moshpit_engine* e, uint32_t* members,
                           uint32_t* group_off, uint32_t* n_groups,
                           uint8_t* void_flags, uint32_t* ranks, uint32_t* keys);
 
+/* ---- peer-sharded multi-GPU rounds ---------------------------
+ * One rank per GPU (or, with emulate=1, all `world` ranks as separate pools
+ * on the current device -- a 1-GPU test harness for the same data plane).
+ * Peers sit cell-major with grid digit d-1 split across ranks; rounds on axes
+ * 0..d-2 are GPU-local, the axis-(d-1) round runs one fused kernel that reads
+ * and writes member rows in peer HBM over NVLink.  Requires a full grid
+ * (N == M^d), world | M, M <= 32.  Every rank makes the same host draws and
+ * computes the same tables (no metadata exchange). */
+typedef struct moshpit_shard moshpit_shard;
+int moshpit_shard_create(int dtype, uint32_t M, uint32_t d, uint64_t n,
+                         double p_round, uint64_t seed, uint64_t dim,
+                         int32_t rank, int32_t world, int32_t emulate,
+                         int32_t device, moshpit_shard** out);
+int moshpit_shard_destroy(moshpit_shard* s);
+/* 128 bytes: cudaIpcMemHandle_t of this rank's row pool and barrier flags. */
+int moshpit_shard_ipc_handles(moshpit_shard* s, void* out128);
+/* world*128 bytes gathered in rank order; maps every peer's pool/flags. */
+int moshpit_shard_open_peers(moshpit_shard* s, const void* all_handles);
+/* Synthetic init of the resident peers' rows (x(peer, j), as fill_synthetic). */
+int moshpit_shard_fill_synthetic(moshpit_shard* s, uint64_t seed, void* stream);
+/* Enqueue one round (all ranks must call it the same number of times). */
+int moshpit_shard_round(moshpit_shard* s, void* stream, uint32_t* active_out,
+                        int32_t* crossed_out);
+/* Resident peers' vectors -> out[n*dim] by peer id, mask[p]=1 where written. */
+int moshpit_shard_read(moshpit_shard* s, void* out, uint8_t* mask);
+int moshpit_shard_set_timing(moshpit_shard* s, int32_t enable);
+int moshpit_shard_kernel_time(moshpit_shard* s, double* local_ms,
+                              uint64_t* local_n, double* cross_ms,
+                              uint64_t* cross_n);
+int moshpit_shard_pool(moshpit_shard* s, int32_t k, void** ptr, uint64_t* rows,
+                       uint64_t* ld);
+
 /* Counter-based synthetic init (bench / tests):
  * x(i,j) = (splitmix64(seed ^ (i<<32) ^ (col0+j)) >> 40) * 2^-24. */
 int moshpit_fill_synthetic(int dtype, void* state, uint64_t n, uint64_t dim,

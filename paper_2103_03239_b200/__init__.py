@@ -30,7 +30,7 @@ __all__ = [
     "PartitionWeights", "chunk_sizes", "AllReduceOutcome", "butterfly_allreduce",
     "group_mean", "distortion", "mean_of", "TrialReport", "run_moshpit", "moshpit_average",
     "complexity_estimate", "Engine", "fill_synthetic", "InvalidArgument", "OutOfRange",
-    "CudaError", "MoshpitError", "device_count",
+    "CudaError", "MoshpitError", "device_count", "Shard",
 ]
 
 
@@ -476,3 +476,92 @@ class Engine:
         g = ng.value
         return dict(members=members, group_off=off[: g + 1], n_groups=g, void=void[:g],
                     rank=ranks, keys=keys[:, :klen])
+
+
+# ---------------------------------------------------------------------------
+# Peer-sharded multi-GPU engine
+# ---------------------------------------------------------------------------
+def exchange_handles(mine: bytes, world: int, group=None) -> List[bytes]:
+    """All-gather one fixed-size handle blob per rank, in rank order."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) != world:
+        raise InvalidArgument("process group size differs from the shard's world")
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    if any(len(h) != len(mine) for h in allh):
+        raise InvalidArgument("ranks disagree on the handle size")
+    return allh
+
+
+class Shard:
+    """One rank of a peer-sharded Moshpit trial (or, ``emulate=True``, all
+    ``world`` ranks as separate pools on one GPU).
+
+    Real multi-process use (one process per GPU, torch.distributed for the
+    one-time handle exchange only)::
+
+        sh = Shard(grid, n, failure, rng, dim, rank=r, world=w, device=local)
+        sh.connect(process_group)        # all_gather of CUDA IPC handles
+        sh.fill_synthetic(seed)
+        for _ in range(rounds): sh.round()
+    """
+
+    def __init__(self, grid: GridConfig, n_peers: int, failure: FailureModel, rng: Rng,
+                 dim: int, rank: int = 0, world: int = 1, emulate: bool = False,
+                 device: int = 0, dtype=np.float32):
+        self.grid, self.n, self.dim = grid, int(n_peers), int(dim)
+        self.rank, self.world, self.emulate = rank, world, emulate
+        self.dtype = np.dtype(dtype)
+        h = C.c_void_p()
+        check(lib().moshpit_shard_create(_dtype_code(self.dtype), grid.peers_per_axis, grid.dims,
+                                         self.n, failure.p_round, rng.seed(), self.dim, rank,
+                                         world, 1 if emulate else 0, device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moshpit_shard_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def ipc_handles(self) -> bytes:
+        buf = (C.c_char * 128)()
+        check(lib().moshpit_shard_ipc_handles(self._h, buf))
+        return bytes(buf)
+
+    def open_peers(self, handles: Sequence[bytes]):
+        blob = b"".join(handles)
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        check(lib().moshpit_shard_open_peers(self._h, buf))
+
+    def connect(self, group=None):
+        """Exchange CUDA IPC handles over torch.distributed (plumbing only)."""
+        self.open_peers(exchange_handles(self.ipc_handles(), self.world, group))
+
+    def fill_synthetic(self, seed: int, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        check(lib().moshpit_shard_fill_synthetic(self._h, seed, s.cuda_stream))
+
+    def round(self, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        act, crossed = C.c_uint32(0), C.c_int32(0)
+        check(lib().moshpit_shard_round(self._h, s.cuda_stream, C.byref(act), C.byref(crossed)))
+        return act.value, bool(crossed.value)
+
+    def read(self):
+        out = np.zeros((self.n, self.dim), dtype=self.dtype)
+        mask = np.zeros(self.n, dtype=np.uint8)
+        check(lib().moshpit_shard_read(self._h, _p(out), _p(mask)))
+        return out, mask.astype(bool)
+
+    def set_timing(self, enable: bool):
+        check(lib().moshpit_shard_set_timing(self._h, 1 if enable else 0))
+
+    def kernel_time(self):
+        lm, ln, cm, cn = C.c_double(0), C.c_uint64(0), C.c_double(0), C.c_uint64(0)
+        check(lib().moshpit_shard_kernel_time(self._h, C.byref(lm), C.byref(ln), C.byref(cm),
+                                              C.byref(cn)))
+        return lm.value, ln.value, cm.value, cn.value

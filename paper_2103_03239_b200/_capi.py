@@ -78,6 +78,17 @@ PROTOTYPES = {
     "moshpit_engine_set_timing": (C.c_int, [vp, C.c_int]),
     "moshpit_engine_kernel_time": (C.c_int, [vp, P(dbl), P(u64)]),
     "moshpit_engine_tables": (C.c_int, [vp, vp, vp, P(u32), vp, vp, vp]),
+    "moshpit_shard_create": (C.c_int, [C.c_int, u32, u32, u64, dbl, u64, u64, i32, i32, i32,
+                                       i32, P(vp)]),
+    "moshpit_shard_destroy": (C.c_int, [vp]),
+    "moshpit_shard_ipc_handles": (C.c_int, [vp, vp]),
+    "moshpit_shard_open_peers": (C.c_int, [vp, vp]),
+    "moshpit_shard_fill_synthetic": (C.c_int, [vp, u64, vp]),
+    "moshpit_shard_round": (C.c_int, [vp, vp, P(u32), P(i32)]),
+    "moshpit_shard_read": (C.c_int, [vp, vp, vp]),
+    "moshpit_shard_set_timing": (C.c_int, [vp, i32]),
+    "moshpit_shard_kernel_time": (C.c_int, [vp, P(dbl), P(u64), P(dbl), P(u64)]),
+    "moshpit_shard_pool": (C.c_int, [vp, i32, P(vp), P(u64), P(u64)]),
     "moshpit_fill_synthetic": (C.c_int, [C.c_int, vp, u64, u64, u64, u64, u64, vp]),
 }
 

@@ -13,8 +13,11 @@
 
 #include "../../include/moshpit_b200.h"
 #include "common.cuh"
+#include "plane.cuh"
 
 namespace mb200 {
+
+thread_local std::string g_last_error;
 
 double Xoshiro::normal() {  // rng.hpp:68-83
   if (have_spare) {
@@ -44,32 +47,6 @@ void require_device() {
 
 namespace {
 
-thread_local std::string g_last_error;
-
-template <typename F>
-int guarded(F&& f) {
-  try {
-    f();
-    g_last_error.clear();
-    return MOSHPIT_OK;
-  } catch (const std::invalid_argument& e) {
-    g_last_error = e.what();
-    return MOSHPIT_ERR_INVALID_ARGUMENT;
-  } catch (const std::out_of_range& e) {
-    g_last_error = e.what();
-    return MOSHPIT_ERR_OUT_OF_RANGE;
-  } catch (const CudaError& e) {
-    g_last_error = e.what();
-    return MOSHPIT_ERR_CUDA;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return MOSHPIT_ERR_RUNTIME;
-  } catch (...) {
-    g_last_error = "unknown error";
-    return MOSHPIT_ERR_RUNTIME;
-  }
-}
-
 Xoshiro from_state(const moshpit_rng_state* st) {
   Xoshiro r;
   std::memcpy(r.s, st->s, sizeof(r.s));
@@ -84,196 +61,7 @@ void to_state(const Xoshiro& r, moshpit_rng_state* st) {
   st->spare = r.spare;
 }
 
-std::size_t elem_size(int dtype) {
-  if (dtype == MOSHPIT_F32) return 4;
-  if (dtype == MOSHPIT_F64) return 8;
-  throw std::invalid_argument("dtype must be MOSHPIT_F32 or MOSHPIT_F64");
-}
-
-std::uint64_t padded_ld(std::uint64_t dim, std::size_t elem) {
-  const std::uint64_t v = 16 / elem;
-  const std::uint64_t ld = (dim + v - 1) / v * v;
-  return ld ? ld : v;
-}
-
-// Partial Fisher-Yates over [0, capacity) (protocols.hpp:124-130,
-// optimizer.hpp:254-259) with a sparse map, so memory is O(n) rather than
-// O(M^d); the draws and swaps are exactly the reference's.
-std::vector<std::uint64_t> draw_cells(Xoshiro& st, std::uint64_t capacity,
-                                      std::uint64_t n) {
-  std::unordered_map<std::uint64_t, std::uint64_t> moved;
-  moved.reserve(2 * n);
-  auto at = [&](std::uint64_t i) {
-    auto it = moved.find(i);
-    return it == moved.end() ? i : it->second;
-  };
-  std::vector<std::uint64_t> cells(n);
-  for (std::uint64_t i = 0; i < n; ++i) {
-    const std::uint64_t j = i + st.below(capacity - i);
-    const std::uint64_t vi = at(i), vj = at(j);
-    moved[i] = vj;
-    moved[j] = vi;
-    cells[i] = vj;
-  }
-  return cells;
-}
-
-struct StreamHolder {
-  cudaStream_t s = nullptr;
-  StreamHolder() { MB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
-  ~StreamHolder() {
-    if (s) cudaStreamDestroy(s);
-  }
-};
-
 }  // namespace
-
-// ---------------------------------------------------------------------------
-// The device-resident integer plane of one trial (keys, tables, draws).
-// ---------------------------------------------------------------------------
-struct Plane {
-  Grid grid;
-  std::uint64_t n = 0;
-  int device = 0;
-  DeviceBuffer keys, draws, members, goff, gvoid, rank, act, counts, totals,
-      sidx, scs, sgi, cellbuf;
-  static constexpr int kStages = 4;
-  PinnedBuffer stage[kStages];
-  cudaEvent_t ev[kStages] = {};
-  int slot = 0;
-  std::uint32_t last_active = 0;
-  std::uint64_t rounds_done = 0;
-  cudaStream_t last_stream = nullptr;
-  // optional CUDA-event bracketing of kernel 2 on its launch stream
-  bool timing = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
-  std::size_t tev_used = 0;
-
-  Plane(std::uint32_t M, std::uint32_t d, std::uint64_t n_, int dev)
-      : grid(M, d), n(n_), device(dev) {
-    if (n == 0) throw std::invalid_argument("run_moshpit: no peers");
-    if (n > grid.capacity)
-      throw std::invalid_argument("run_moshpit: N exceeds grid capacity M^d");
-    if (n > 0x7fffffffull)
-      throw std::invalid_argument("moshpit engine: more than 2^31 peers");
-    std::uint64_t np = 1;
-    while (np < n) np <<= 1;
-    keys.resize(n * 8);
-    draws.resize(n * 9 + 16);
-    members.resize(n * 4);
-    goff.resize((n + 1) * 4);
-    gvoid.resize(n);
-    rank.resize(n * 4);
-    act.resize(n * 4);
-    counts.resize(16);
-    totals.resize(16);
-    sidx.resize(np * 4);
-    scs.resize(n * 4);
-    sgi.resize(n * 4);
-    cellbuf.resize(n * 8);
-    MB_CUDA(cudaMemset(totals.ptr, 0, 16));
-    MB_CUDA(cudaMemset(counts.ptr, 0, 16));
-    for (int i = 0; i < kStages; ++i) {
-      stage[i].resize(n * 9 + 16);
-      MB_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-    }
-  }
-  ~Plane() {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
-    for (auto& pr : tev) {
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
-    }
-  }
-
-  std::pair<cudaEvent_t, cudaEvent_t> timing_pair() {
-    if (tev_used == tev.size()) {
-      cudaEvent_t a, b;
-      MB_CUDA(cudaEventCreate(&a));
-      MB_CUDA(cudaEventCreate(&b));
-      tev.emplace_back(a, b);
-    }
-    return tev[tev_used++];
-  }
-
-  // cells -> initial keys (matchmaking.hpp:46-59), on the device.
-  void init_cells(Xoshiro& cell_stream, cudaStream_t s) {
-    const auto cells = draw_cells(cell_stream, grid.capacity, n);
-    const int k = next_slot();
-    std::memcpy(stage[k].ptr, cells.data(), n * 8);
-    MB_CUDA(cudaMemcpyAsync(cellbuf.ptr, stage[k].ptr, n * 8, cudaMemcpyHostToDevice, s));
-    MB_CUDA(cudaEventRecord(ev[k], s));
-    launch_initial_keys(cellbuf.as<std::uint64_t>(), keys.as<std::uint64_t>(), n,
-                        grid.M, grid.d, s);
-  }
-
-  int next_slot() {
-    const int k = slot;
-    slot = (slot + 1) % kStages;
-    MB_CUDA(cudaEventSynchronize(ev[k]));  // host staging slot reusable
-    return k;
-  }
-
-  // One round: host draws (protocols.hpp:143-150), group formation (kernel 1),
-  // group mean (kernel 2).  fail == nullptr or p <= 0: no failure draws.
-  std::uint32_t round(Xoshiro* fail, double p, Xoshiro& clock, int dtype,
-                      void* state, std::uint64_t dim, std::uint64_t ld,
-                      cudaStream_t s, int variant) {
-    const int k = next_slot();
-    auto* ts = stage[k].as<std::uint64_t>();
-    auto* failed = reinterpret_cast<std::uint8_t*>(ts + n);
-    std::memset(failed, 0, n);
-    std::uint32_t active = 0;
-    if (fail && p > 0.0) {
-      for (std::uint64_t i = 0; i < n; ++i) failed[i] = fail->bernoulli(p) ? 1 : 0;
-    }
-    for (std::uint64_t i = 0; i < n; ++i) active += failed[i] == 0;
-    for (std::uint64_t i = 0; i < n; ++i) ts[i] = clock.next() >> 16;
-    MB_CUDA(cudaMemcpyAsync(draws.ptr, ts, n * 9, cudaMemcpyHostToDevice, s));
-    MB_CUDA(cudaEventRecord(ev[k], s));
-
-    GroupArgs a;
-    a.n = static_cast<std::uint32_t>(n);
-    a.cap = grid.M;
-    a.M = grid.M;
-    a.pow_drop = grid.pow_drop;
-    a.advance_keys = 1;
-    a.klen_zero = grid.klen == 0;
-    a.keys = keys.as<std::uint64_t>();
-    a.ts = draws.as<std::uint64_t>();
-    a.failed = draws.as<std::uint8_t>() + n * 8;
-    a.members = members.as<std::uint32_t>();
-    a.goff = goff.as<std::uint32_t>();
-    a.gvoid = gvoid.as<std::uint8_t>();
-    a.rank = rank.as<std::uint32_t>();
-    a.act = act.as<std::uint32_t>();
-    a.counts = counts.as<std::uint32_t>();
-    a.totals = totals.as<unsigned long long>();
-    a.sidx = sidx.as<std::uint32_t>();
-    a.scs = scs.as<std::uint32_t>();
-    a.sgi = sgi.as<std::uint32_t>();
-    launch_form_groups(a, true, s);
-    if (state && dim) {
-      std::pair<cudaEvent_t, cudaEvent_t> te{};
-      if (timing) {
-        te = timing_pair();
-        MB_CUDA(cudaEventRecord(te.first, s));
-      }
-      if (dtype == MOSHPIT_F32)
-        launch_group_mean<float>(static_cast<float*>(state), ld, dim, a.members, a.goff,
-                                 a.act, a.counts, grid.M, variant, s);
-      else
-        launch_group_mean<double>(static_cast<double*>(state), ld, dim, a.members, a.goff,
-                                  a.act, a.counts, grid.M, variant, s);
-      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
-    }
-    last_active = active;
-    ++rounds_done;
-    last_stream = s;
-    return active;
-  }
-};
 
 }  // namespace mb200
 

@@ -1,0 +1,768 @@
+// shard.cu -- peer-sharded multi-GPU Moshpit rounds (north-star
+// layout).
+//
+// Placement.  Peers sit cell-major: global row = current grid cell, GPU =
+// row / R with R = M^d / G, i.e. the most significant grid digit x_{d-1} is
+// split across the G GPUs.  Keys evolve by shift-append of ranks
+// (matchmaking.hpp:62-71); relabelling the active coordinate to the member's
+// rank after every round makes round t a set of grid lines along axis
+// (t-1) mod d, so rounds on axes 0..d-2 are GPU-local and only
+// axis d-1 crosses GPUs.  Locally, a peer's row is an indirection (loc[p]):
+// voided groups keep their rows and nothing moves.
+//
+// Cross round (axis d-1).  The tree order spans GPUs, so no partial sums can
+// be shipped: GPU g owns coordinate chunk g of every group and evaluates the
+// reference tree over the members' raw chunk-g vectors, loading remote rows
+// straight from peer HBM over NVLink (CUDA IPC mappings) and storing the mean
+// into every member row, remote ones included -- one fused kernel, the
+// transfer overlapped with the arithmetic tile by tile.  Members of a
+// non-voided group whose rank moves them to another GPU inherit, on that GPU,
+// the row of a member that left it (same group), so the mean lands in place
+// and only voided groups move data (staged pull, then write).
+//
+// The integer plane (draws, kernel 1, placement) is replicated on every rank:
+// every rank computes identical tables, so no metadata is exchanged.  Ranks
+// synchronise with a P2P flag barrier kernel (no host round-trip).  Emulation
+// mode runs all G "virtual GPUs" as separate pools on one device (tests).
+#include <algorithm>
+#include <memory>
+
+#include "plane.cuh"
+
+namespace mb200 {
+namespace {
+
+constexpr int kMaxWorld = 8;
+
+struct PlaceArgs {
+  std::uint32_t n = 0, world = 1, Mg = 1;
+  std::uint64_t R = 0;
+  int cross = 0;
+  const std::uint32_t* members = nullptr;
+  const std::uint32_t* goff = nullptr;
+  const std::uint32_t* counts = nullptr;
+  const std::uint8_t* gvoid = nullptr;
+  std::uint32_t* loc = nullptr;         // [n] global row per peer (in/out)
+  std::uint32_t* rows_local = nullptr;  // [n] local row per member position
+  std::uint32_t* act_local = nullptr;   // [world][n]
+  std::uint32_t* cnt_local = nullptr;   // [world][4]: [1] n_act, [2] rows
+  std::uint32_t* src_row = nullptr;     // [n] by position (cross)
+  std::uint32_t* dst_row = nullptr;     // [n] by position (cross)
+  std::uint32_t* act_cross = nullptr;   // [n]
+  std::uint32_t* cnt_cross = nullptr;   // [4]: [1] n_act, [2] rows
+  std::uint32_t* moves = nullptr;       // [world][R][2] (src, dst), grouped by dst GPU
+  std::uint32_t* n_moves = nullptr;     // [world]
+  std::uint32_t* err = nullptr;         // [1]
+};
+
+// Replicated bookkeeping for one round (one CTA, one thread per group).
+__global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
+  const std::uint32_t ng = a.counts[0];
+  if (threadIdx.x < a.world * 4) a.cnt_local[threadIdx.x] = 0;
+  if (threadIdx.x < 4) a.cnt_cross[threadIdx.x] = 0;
+  if (threadIdx.x < a.world) a.n_moves[threadIdx.x] = 0;
+  __syncthreads();
+  for (std::uint32_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    const std::uint32_t b = a.goff[g], e = a.goff[g + 1];
+    const bool voided = a.gvoid[g] != 0;
+    if (!a.cross) {
+      const std::uint32_t owner = (std::uint32_t)(a.loc[a.members[b]] / a.R);
+      for (std::uint32_t pos = b; pos < e; ++pos) {
+        const std::uint32_t r = a.loc[a.members[pos]];
+        if (r / a.R != owner) atomicOr(a.err, 1u);  // a local round must be GPU-local
+        a.rows_local[pos] = (std::uint32_t)(r % a.R);
+      }
+      if (!voided) {
+        const std::uint32_t k = atomicAdd(&a.cnt_local[owner * 4 + 1], 1u);
+        a.act_local[owner * a.n + k] = g;
+        atomicAdd(&a.cnt_local[owner * 4 + 2], e - b);
+      }
+      continue;
+    }
+    // cross round: stayers keep their row; arrivals on GPU h take, in
+    // position order, the rows of this group's members leaving h.
+    for (std::uint32_t pos = b; pos < e; ++pos) {
+      const std::uint32_t src = a.loc[a.members[pos]];
+      const std::uint32_t og = (std::uint32_t)(src / a.R), nw = (pos - b) / a.Mg;
+      a.src_row[pos] = src;
+      a.dst_row[pos] = og == nw ? src : 0xffffffffu;
+    }
+    for (std::uint32_t h = 0; h < a.world; ++h) {
+      std::uint32_t li = b;
+      for (std::uint32_t pos = b; pos < e; ++pos) {
+        const std::uint32_t og = (std::uint32_t)(a.src_row[pos] / a.R), nw = (pos - b) / a.Mg;
+        if (nw != h || og == h) continue;  // not an arrival on h
+        while (li < e && !((std::uint32_t)(a.src_row[li] / a.R) == h && (li - b) / a.Mg != h)) ++li;
+        if (li == e) {
+          atomicOr(a.err, 2u);  // unbalanced line: sharded mode needs a full grid
+          break;
+        }
+        a.dst_row[pos] = a.src_row[li++];
+      }
+    }
+    for (std::uint32_t pos = b; pos < e; ++pos) {
+      a.loc[a.members[pos]] = a.dst_row[pos];
+      if (voided && a.dst_row[pos] != a.src_row[pos]) {
+        const std::uint32_t h = (std::uint32_t)(a.dst_row[pos] / a.R);
+        const std::uint32_t k = atomicAdd(&a.n_moves[h], 1u);
+        a.moves[((std::uint64_t)h * a.R + k) * 2] = a.src_row[pos];
+        a.moves[((std::uint64_t)h * a.R + k) * 2 + 1] = a.dst_row[pos];
+      }
+    }
+    if (!voided) {
+      const std::uint32_t k = atomicAdd(&a.cnt_cross[1], 1u);
+      a.act_cross[k] = g;
+      atomicAdd(&a.cnt_cross[2], e - b);
+    }
+  }
+}
+
+__global__ void init_loc_kernel(const std::uint64_t* cells, std::uint32_t* loc, std::uint64_t n) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) loc[i] = (std::uint32_t)cells[i];
+}
+
+template <typename T>
+struct V16s;
+template <>
+struct V16s<float> {
+  using type = float4;
+};
+template <>
+struct V16s<double> {
+  using type = double2;
+};
+__device__ __forceinline__ float4 sadd(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ double2 sadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float4 sdiv(float4 a, std::uint32_t n) {
+  const float f = (float)n;
+  return make_float4(__fdiv_rn(a.x, f), __fdiv_rn(a.y, f), __fdiv_rn(a.z, f), __fdiv_rn(a.w, f));
+}
+__device__ __forceinline__ double2 sdiv(double2 a, std::uint32_t n) {
+  const double f = (double)n;
+  return make_double2(__ddiv_rn(a.x, f), __ddiv_rn(a.y, f));
+}
+__device__ __forceinline__ float4 szero(float4*) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ double2 szero(double2*) { return make_double2(0.0, 0.0); }
+
+template <int N, int B, typename V>
+__device__ __forceinline__ V stree(const V (&x)[32]) {
+  if constexpr (N <= 8) {
+    V s = szero((V*)nullptr);
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = sadd(s, x[B + i]);
+    return s;
+  } else {
+    constexpr int H = N / 2;
+    return sadd(stree<H, B>(x), stree<N - H, B + H>(x));
+  }
+}
+
+constexpr int kCrossThreads = 128;
+
+template <typename T>
+struct CrossArgs {
+  T* pools[kMaxWorld];
+  std::uint64_t ld_vec = 0, R = 0;
+  std::uint64_t c0 = 0, c1 = 0, n_tiles = 0;
+  const std::uint32_t* goff = nullptr;
+  const std::uint32_t* src_row = nullptr;
+  const std::uint32_t* dst_row = nullptr;
+  const std::uint32_t* act = nullptr;
+  const std::uint32_t* cnt = nullptr;
+};
+
+template <int N, typename V>
+__device__ __forceinline__ void cross_fixed(V* const* src, V* const* dst, std::uint64_t col) {
+  V x[32];
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = __ldcs(src[k] + col);
+  const V m = sdiv(stree<N, 0>(x), (std::uint32_t)N);
+#pragma unroll
+  for (int k = 0; k < N; ++k) __stcs(dst[k] + col, m);
+}
+
+// Fused cross-GPU round: this GPU's coordinate chunk of every active group,
+// member rows read from (and the mean written to) local or peer HBM.
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<T> a) {
+  using V = typename V16s<T>::type;
+  __shared__ V* s_src[32];
+  __shared__ V* s_dst[32];
+  const std::uint32_t n_act = a.cnt[1];
+  const std::uint64_t n_items = (std::uint64_t)n_act * a.n_tiles;
+  std::uint32_t cached = 0xffffffffu, cnt = 0;
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t g = a.act[w / a.n_tiles];
+    if (g != cached) {
+      __syncthreads();
+      const std::uint32_t beg = a.goff[g];
+      cnt = a.goff[g + 1] - beg;
+      if (threadIdx.x < cnt) {
+        const std::uint32_t s = a.src_row[beg + threadIdx.x], d = a.dst_row[beg + threadIdx.x];
+        s_src[threadIdx.x] = reinterpret_cast<V*>(a.pools[s / a.R]) + (s % a.R) * a.ld_vec;
+        s_dst[threadIdx.x] = reinterpret_cast<V*>(a.pools[d / a.R]) + (d % a.R) * a.ld_vec;
+      }
+      cached = g;
+      __syncthreads();
+    }
+    const std::uint64_t col = a.c0 + (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    if (col >= a.c1) continue;
+    switch (cnt) {
+#define MB_XCASE(N)                       \
+  case N:                                 \
+    cross_fixed<N, V>(s_src, s_dst, col); \
+    break;
+      MB_XCASE(1) MB_XCASE(2) MB_XCASE(3) MB_XCASE(4) MB_XCASE(5) MB_XCASE(6) MB_XCASE(7)
+      MB_XCASE(8) MB_XCASE(9) MB_XCASE(10) MB_XCASE(11) MB_XCASE(12) MB_XCASE(13)
+      MB_XCASE(14) MB_XCASE(15) MB_XCASE(16) MB_XCASE(17) MB_XCASE(18) MB_XCASE(19)
+      MB_XCASE(20) MB_XCASE(21) MB_XCASE(22) MB_XCASE(23) MB_XCASE(24) MB_XCASE(25)
+      MB_XCASE(26) MB_XCASE(27) MB_XCASE(28) MB_XCASE(29) MB_XCASE(30) MB_XCASE(31)
+      MB_XCASE(32)
+#undef MB_XCASE
+      default: break;
+    }
+  }
+}
+
+// Voided cross groups: rows whose owner GPU changes are pulled into staging
+// (phase 0), then written to their new rows after a barrier (phase 1).
+template <typename T>
+__global__ void move_rows_kernel(T* const* pools, const std::uint32_t* moves,
+                                 const std::uint32_t* n_moves, std::uint32_t me, std::uint64_t R,
+                                 std::uint64_t ld_vec, std::uint64_t nvec, T* staging, int phase) {
+  using V = typename V16s<T>::type;
+  const std::uint32_t cnt = n_moves[me];
+  const std::uint64_t total = (std::uint64_t)cnt * nvec;
+  V* st = reinterpret_cast<V*>(staging);
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t k = e / nvec, c = e % nvec;
+    const std::uint32_t* mv = moves + ((std::uint64_t)me * R + k) * 2;
+    if (phase == 0) {
+      const std::uint32_t s = mv[0];
+      const V* src = reinterpret_cast<const V*>(pools[s / R]) + (s % R) * ld_vec;
+      st[k * ld_vec + c] = src[c];
+    } else {
+      const std::uint32_t d = mv[1];
+      V* dst = reinterpret_cast<V*>(pools[d / R]) + (d % R) * ld_vec;
+      dst[c] = st[k * ld_vec + c];
+    }
+  }
+}
+
+// P2P flag barrier: each rank publishes `epoch` into every peer's flag slot,
+// then waits for all peers' slots to reach it.  Bounded spin -> __trap()
+// (an error, never a hang).
+__global__ void peer_barrier_kernel(unsigned long long* my_flags, unsigned long long* const* peer_flags,
+                                    std::uint32_t me, std::uint32_t world, unsigned long long epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (std::uint32_t h = 0; h < world; ++h) {
+    if (h == me) continue;
+    unsigned long long* f = peer_flags[h] + me;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+  }
+  const long long t0 = clock64();
+  for (std::uint32_t h = 0; h < world; ++h) {
+    if (h == me) continue;
+    unsigned long long v = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + h) : "memory");
+      if (v >= epoch) break;
+      if (clock64() - t0 > 40000000000ll) __trap();  // ~20 s at 1.96 GHz
+    }
+  }
+  __threadfence_system();
+}
+
+template <typename T>
+__global__ void shard_fill_kernel(T* pool, const std::uint32_t* loc, std::uint64_t n,
+                                  std::uint64_t dim, std::uint64_t ld, std::uint64_t R,
+                                  std::uint32_t me, std::uint64_t seed) {
+  const std::uint64_t total = n * dim;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t p = e / dim, j = e % dim;
+    const std::uint32_t r = loc[p];
+    if (r / R != me) continue;
+    std::uint64_t z = (seed ^ (p << 32) ^ j) + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z = z ^ (z >> 31);
+    pool[(r % R) * ld + j] = (T)((double)(z >> 40) * 0x1.0p-24);
+  }
+}
+
+// Copy resident peers' rows to/from a by-id buffer (device) on this GPU.
+template <typename T>
+__global__ void shard_gather_kernel(const T* pool, const std::uint32_t* loc, std::uint64_t n,
+                                    std::uint64_t dim, std::uint64_t ld, std::uint64_t R,
+                                    std::uint32_t me, T* out, std::uint8_t* mask, int to_pool) {
+  const std::uint64_t total = n * dim;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t p = e / dim, j = e % dim;
+    const std::uint32_t r = loc[p];
+    const bool mine = r / R == me;
+    if (j == 0 && mask) mask[p] = mine ? 1 : 0;
+    if (!mine) continue;
+    if (to_pool)
+      const_cast<T*>(pool)[(r % R) * ld + j] = out[p * dim + j];
+    else
+      out[p * dim + j] = pool[(r % R) * ld + j];
+  }
+}
+
+unsigned grid_cap(std::uint64_t work) {
+  std::uint64_t b = (work + 255) / 256;
+  if (b > 148ull * 32) b = 148ull * 32;
+  return (unsigned)(b ? b : 1);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct Shard {
+  std::unique_ptr<Plane> plane;
+  Xoshiro fail, clock;
+  double p = 0.0;
+  int dtype = MOSHPIT_F32;
+  std::size_t es = 4;
+  std::uint64_t dim = 0, ld = 0, R = 0;
+  std::uint32_t world = 1, me = 0, Mg = 1, M = 1, d = 1;
+  int device = 0;
+  bool emulate = false;
+  std::uint32_t round_no = 0;
+  unsigned long long epoch = 0;
+  // replicated bookkeeping
+  DeviceBuffer loc, rows_local, act_local, cnt_local, src_row, dst_row, act_cross, cnt_cross,
+      moves, n_moves, err, pool_tab, flag_tab;
+  // pools: [world] in emulation, [1] (mine) otherwise
+  std::vector<std::unique_ptr<DeviceBuffer>> own_pools;
+  std::vector<std::unique_ptr<DeviceBuffer>> staging;
+  void* pools[kMaxWorld] = {};
+  DeviceBuffer flags;  // [world] u64 (real mode)
+  unsigned long long* peer_flags[kMaxWorld] = {};
+  std::vector<void*> opened;  // IPC mappings to close
+  // timing of the data-plane kernels (CUDA events on the launch stream)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_local, tev_cross;
+  std::size_t used_local = 0, used_cross = 0;
+
+  ~Shard() {
+    for (void* q : opened) cudaIpcCloseMemHandle(q);
+    for (auto* v : {&tev_local, &tev_cross})
+      for (auto& pr : *v) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+  }
+
+  std::pair<cudaEvent_t, cudaEvent_t> tpair(bool cross) {
+    auto& v = cross ? tev_cross : tev_local;
+    auto& u = cross ? used_cross : used_local;
+    if (u == v.size()) {
+      cudaEvent_t a, b;
+      MB_CUDA(cudaEventCreate(&a));
+      MB_CUDA(cudaEventCreate(&b));
+      v.emplace_back(a, b);
+    }
+    return v[u++];
+  }
+
+  std::uint64_t nvec() const { return (dim + (16 / es) - 1) / (16 / es); }
+  std::uint32_t n() const { return (std::uint32_t)plane->n; }
+
+  void barrier(cudaStream_t s) {
+    if (emulate || world == 1) return;
+    ++epoch;
+    peer_barrier_kernel<<<1, 32, 0, s>>>(flags.as<unsigned long long>(),
+                                        flag_tab.as<unsigned long long* const>(), me, world,
+                                        epoch);
+    MB_LAUNCH_CHECK();
+  }
+
+  template <typename T>
+  void cross_launch(std::uint32_t r, cudaStream_t s) {
+    CrossArgs<T> a;
+    for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
+    a.ld_vec = ld * es / 16;
+    a.R = R;
+    const std::uint64_t nv = nvec();
+    a.c0 = nv * r / world;
+    a.c1 = nv * (r + 1) / world;
+    a.n_tiles = (a.c1 - a.c0 + kCrossThreads - 1) / kCrossThreads;
+    a.goff = plane->goff.as<std::uint32_t>();
+    a.src_row = src_row.as<std::uint32_t>();
+    a.dst_row = dst_row.as<std::uint32_t>();
+    a.act = act_cross.as<std::uint32_t>();
+    a.cnt = cnt_cross.as<std::uint32_t>();
+    int per = 0, sms = 0;
+    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_mean_kernel<T>,
+                                                          kCrossThreads, 0));
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (a.n_tiles) cross_mean_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+
+  template <typename T>
+  void moves_launch(std::uint32_t r, int phase, cudaStream_t s) {
+    if (p <= 0.0) return;  // no voided groups without failures
+    auto& st = staging[emulate ? r : 0];
+    if (!st) {
+      st = std::make_unique<DeviceBuffer>(R * ld * es);
+    }
+    move_rows_kernel<T><<<grid_cap(R * nvec()), 256, 0, s>>>(
+        pool_tab.as<T* const>(), moves.as<std::uint32_t>(), n_moves.as<std::uint32_t>(), r, R,
+        ld * es / 16, nvec(), st->as<T>(), phase);
+    MB_LAUNCH_CHECK();
+  }
+
+  // One round on every rank: identical host draws and kernel 1, replicated
+  // placement, then this rank's data plane (all virtual ranks in emulation).
+  std::uint32_t round(cudaStream_t s, int* crossed) {
+    const std::uint32_t axis = d ? round_no % d : 0;
+    const int cross = (world > 1 && axis == d - 1) ? 1 : 0;
+    ++round_no;
+    const std::uint32_t active = plane->round(&fail, p, clock, dtype, nullptr, 0, 0, s, 0);
+    PlaceArgs a;
+    a.n = n();
+    a.world = world;
+    a.Mg = Mg;
+    a.R = R;
+    a.cross = cross || world == 1;
+    if (world == 1) a.cross = 0;
+    a.members = plane->members.as<std::uint32_t>();
+    a.goff = plane->goff.as<std::uint32_t>();
+    a.counts = plane->counts.as<std::uint32_t>();
+    a.gvoid = plane->gvoid.as<std::uint8_t>();
+    a.loc = loc.as<std::uint32_t>();
+    a.rows_local = rows_local.as<std::uint32_t>();
+    a.act_local = act_local.as<std::uint32_t>();
+    a.cnt_local = cnt_local.as<std::uint32_t>();
+    a.src_row = src_row.as<std::uint32_t>();
+    a.dst_row = dst_row.as<std::uint32_t>();
+    a.act_cross = act_cross.as<std::uint32_t>();
+    a.cnt_cross = cnt_cross.as<std::uint32_t>();
+    a.moves = moves.as<std::uint32_t>();
+    a.n_moves = n_moves.as<std::uint32_t>();
+    a.err = err.as<std::uint32_t>();
+    place_kernel<<<1, 1024, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+    const std::uint32_t nranks = emulate ? world : 1;
+    if (!a.cross) {
+      std::pair<cudaEvent_t, cudaEvent_t> te{};
+      if (timing) {
+        te = tpair(false);
+        MB_CUDA(cudaEventRecord(te.first, s));
+      }
+      for (std::uint32_t k = 0; k < nranks; ++k) {
+        const std::uint32_t r = emulate ? k : me;
+        const std::uint32_t* rows = rows_local.as<std::uint32_t>();
+        const std::uint32_t* act = act_local.as<std::uint32_t>() + (std::uint64_t)r * n();
+        const std::uint32_t* cnt = cnt_local.as<std::uint32_t>() + r * 4;
+        if (dtype == MOSHPIT_F32)
+          launch_group_mean<float>(static_cast<float*>(pools[r]), ld, dim, rows, a.goff, act,
+                                   cnt, M, 0, s);
+        else
+          launch_group_mean<double>(static_cast<double*>(pools[r]), ld, dim, rows, a.goff, act,
+                                    cnt, M, 0, s);
+      }
+      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
+    } else {
+      barrier(s);  // peers finished writing the rows we are about to read
+      std::pair<cudaEvent_t, cudaEvent_t> te{};
+      if (timing) {
+        te = tpair(true);
+        MB_CUDA(cudaEventRecord(te.first, s));
+      }
+      for (std::uint32_t k = 0; k < nranks; ++k) {
+        const std::uint32_t r = emulate ? k : me;
+        if (dtype == MOSHPIT_F32) {
+          cross_launch<float>(r, s);
+          moves_launch<float>(r, 0, s);
+        } else {
+          cross_launch<double>(r, s);
+          moves_launch<double>(r, 0, s);
+        }
+      }
+      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
+      barrier(s);  // every remote read/write of our rows is done
+      for (std::uint32_t k = 0; k < nranks; ++k) {
+        const std::uint32_t r = emulate ? k : me;
+        if (dtype == MOSHPIT_F32)
+          moves_launch<float>(r, 1, s);
+        else
+          moves_launch<double>(r, 1, s);
+      }
+    }
+    if (crossed) *crossed = a.cross;
+    return active;
+  }
+};
+
+}  // namespace mb200
+
+using namespace mb200;
+
+struct moshpit_shard {
+  std::unique_ptr<Shard> s;
+};
+
+extern "C" {
+
+int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint64_t n,
+                         double p_round, std::uint64_t seed, std::uint64_t dim,
+                         std::int32_t rank, std::int32_t world, std::int32_t emulate,
+                         std::int32_t device, moshpit_shard** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("shard_create: null out");
+    const std::size_t es = elem_size(dtype);
+    if (M < 1 || d < 1) throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (p_round < 0.0 || p_round > 1.0)
+      throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
+    if (world < 1 || world > kMaxWorld) throw std::invalid_argument("shard: world in [1, 8]");
+    if (rank < 0 || rank >= world) throw std::invalid_argument("shard: rank outside [0, world)");
+    if (M % (std::uint32_t)world != 0)
+      throw std::invalid_argument("shard: the GPU count must divide M (split of grid digit d-1)");
+    if (M > 32) throw std::invalid_argument("shard: groups larger than 32 are not sharded");
+    const std::uint64_t cap = moshpit_grid_capacity(M, d);
+    if (n != cap)
+      throw std::invalid_argument("shard: peer sharding needs a full grid (N == M^d)");
+    if (cap > 0xffffffffull) throw std::invalid_argument("shard: grid larger than 2^32 cells");
+    require_device();
+    DeviceGuard g(device);
+    auto sh = std::make_unique<Shard>();
+    Shard& S = *sh;
+    MB_CUDA(cudaGetDevice(&S.device));
+    S.dtype = dtype;
+    S.es = es;
+    S.dim = dim;
+    S.ld = padded_ld(dim, es);
+    S.world = (std::uint32_t)world;
+    S.me = (std::uint32_t)rank;
+    S.emulate = emulate != 0;
+    S.M = M;
+    S.d = d;
+    S.Mg = M / (std::uint32_t)world;
+    S.R = cap / (std::uint64_t)world;
+    S.p = p_round;
+    S.plane = std::make_unique<Plane>(M, d, n, S.device);
+    Xoshiro cells = Xoshiro::named(seed, "cells");
+    S.fail = Xoshiro::named(seed, "failures");
+    S.clock = Xoshiro::named(seed, "priorities");
+    StreamHolder st;
+    S.plane->init_cells(cells, st.s);
+    S.loc.resize(n * 4);
+    init_loc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st.s>>>(
+        S.plane->cellbuf.as<std::uint64_t>(), S.loc.as<std::uint32_t>(), n);
+    MB_LAUNCH_CHECK();
+    S.rows_local.resize(n * 4);
+    S.act_local.resize((std::uint64_t)world * n * 4);
+    S.cnt_local.resize((std::uint64_t)world * 16 + 16);
+    S.src_row.resize(n * 4);
+    S.dst_row.resize(n * 4);
+    S.act_cross.resize(n * 4);
+    S.cnt_cross.resize(16);
+    S.moves.resize((std::uint64_t)world * S.R * 8);
+    S.n_moves.resize(world * 4 + 16);
+    S.err.resize(16);
+    MB_CUDA(cudaMemsetAsync(S.err.ptr, 0, 16, st.s));
+    const std::uint32_t npools = S.emulate ? S.world : 1;
+    for (std::uint32_t k = 0; k < npools; ++k) {
+      S.own_pools.push_back(std::make_unique<DeviceBuffer>(S.R * S.ld * es));
+      MB_CUDA(cudaMemsetAsync(S.own_pools.back()->ptr, 0, S.R * S.ld * es, st.s));
+    }
+    S.staging.resize(npools);
+    if (S.emulate)
+      for (std::uint32_t k = 0; k < S.world; ++k) S.pools[k] = S.own_pools[k]->ptr;
+    else
+      S.pools[S.me] = S.own_pools[0]->ptr;
+    S.flags.resize(kMaxWorld * 8);
+    MB_CUDA(cudaMemsetAsync(S.flags.ptr, 0, kMaxWorld * 8, st.s));
+    S.pool_tab.resize(kMaxWorld * 8);
+    S.flag_tab.resize(kMaxWorld * 8);
+    MB_CUDA(cudaMemcpyAsync(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice,
+                            st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+    *out = new moshpit_shard{std::move(sh)};
+  });
+}
+
+int moshpit_shard_destroy(moshpit_shard* h) {
+  return guarded([&] {
+    if (!h) return;
+    if (h->s) {
+      DeviceGuard g(h->s->device);
+      cudaDeviceSynchronize();
+      h->s.reset();
+    }
+    delete h;
+  });
+}
+
+// cudaIpcMemHandle_t of [pool, flags] (2 * 64 bytes) for the peers.
+int moshpit_shard_ipc_handles(moshpit_shard* h, void* out128) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    if (S.emulate) throw std::invalid_argument("shard: emulation mode has no IPC handles");
+    DeviceGuard g(S.device);
+    cudaIpcMemHandle_t a, b;
+    MB_CUDA(cudaIpcGetMemHandle(&a, S.own_pools[0]->ptr));
+    MB_CUDA(cudaIpcGetMemHandle(&b, S.flags.ptr));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    std::memcpy(out128, &a, 64);
+    std::memcpy(static_cast<char*>(out128) + 64, &b, 64);
+  });
+}
+
+// all: world * 128 bytes, rank-ordered handles from moshpit_shard_ipc_handles.
+int moshpit_shard_open_peers(moshpit_shard* h, const void* all) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    if (S.emulate) return;
+    DeviceGuard g(S.device);
+    for (std::uint32_t r = 0; r < S.world; ++r) {
+      if (r == S.me) {
+        S.peer_flags[r] = S.flags.as<unsigned long long>();
+        continue;
+      }
+      cudaIpcMemHandle_t a, b;
+      std::memcpy(&a, static_cast<const char*>(all) + r * 128, 64);
+      std::memcpy(&b, static_cast<const char*>(all) + r * 128 + 64, 64);
+      void* pa = nullptr;
+      void* pb = nullptr;
+      MB_CUDA(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess));
+      S.opened.push_back(pa);
+      MB_CUDA(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess));
+      S.opened.push_back(pb);
+      S.pools[r] = pa;
+      S.peer_flags[r] = static_cast<unsigned long long*>(pb);
+    }
+    MB_CUDA(cudaMemcpy(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice));
+    MB_CUDA(cudaMemcpy(S.flag_tab.ptr, S.peer_flags, sizeof(S.peer_flags),
+                       cudaMemcpyHostToDevice));
+  });
+}
+
+int moshpit_shard_fill_synthetic(moshpit_shard* h, std::uint64_t seed, void* stream) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const std::uint32_t npools = S.emulate ? S.world : 1;
+    for (std::uint32_t k = 0; k < npools; ++k) {
+      const std::uint32_t r = S.emulate ? k : S.me;
+      if (S.dtype == MOSHPIT_F32)
+        shard_fill_kernel<float><<<grid_cap(S.plane->n * S.dim), 256, 0, s>>>(
+            static_cast<float*>(S.pools[r]), S.loc.as<std::uint32_t>(), S.plane->n, S.dim, S.ld,
+            S.R, r, seed);
+      else
+        shard_fill_kernel<double><<<grid_cap(S.plane->n * S.dim), 256, 0, s>>>(
+            static_cast<double*>(S.pools[r]), S.loc.as<std::uint32_t>(), S.plane->n, S.dim, S.ld,
+            S.R, r, seed);
+      MB_LAUNCH_CHECK();
+    }
+  });
+}
+
+int moshpit_shard_round(moshpit_shard* h, void* stream, std::uint32_t* active_out,
+                        std::int32_t* crossed_out) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    int crossed = 0;
+    const std::uint32_t a = S.round(static_cast<cudaStream_t>(stream), &crossed);
+    if (active_out) *active_out = a;
+    if (crossed_out) *crossed_out = crossed;
+  });
+}
+
+// Copy the vectors of the peers resident on this rank (all, in emulation)
+// to host out[n*dim] by peer id; mask[p] = 1 where written.  Synchronises.
+int moshpit_shard_read(moshpit_shard* h, void* out, std::uint8_t* mask) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    StreamHolder st;
+    const std::uint64_t n = S.plane->n;
+    if (S.plane->last_stream) MB_CUDA(cudaStreamSynchronize(S.plane->last_stream));
+    MB_CUDA(cudaDeviceSynchronize());
+    DeviceBuffer buf(n * S.dim * S.es + 16), m(n + 16), acc(n + 16);
+    MB_CUDA(cudaMemsetAsync(acc.ptr, 0, n, st.s));
+    std::vector<std::uint8_t> hm(n), tot(n, 0);
+    const std::uint32_t npools = S.emulate ? S.world : 1;
+    for (std::uint32_t k = 0; k < npools; ++k) {
+      const std::uint32_t r = S.emulate ? k : S.me;
+      if (S.dtype == MOSHPIT_F32)
+        shard_gather_kernel<float><<<grid_cap(n * S.dim), 256, 0, st.s>>>(
+            static_cast<float*>(S.pools[r]), S.loc.as<std::uint32_t>(), n, S.dim, S.ld, S.R, r,
+            buf.as<float>(), m.as<std::uint8_t>(), 0);
+      else
+        shard_gather_kernel<double><<<grid_cap(n * S.dim), 256, 0, st.s>>>(
+            static_cast<double*>(S.pools[r]), S.loc.as<std::uint32_t>(), n, S.dim, S.ld, S.R, r,
+            buf.as<double>(), m.as<std::uint8_t>(), 0);
+      MB_LAUNCH_CHECK();
+      MB_CUDA(cudaMemcpyAsync(hm.data(), m.ptr, n, cudaMemcpyDeviceToHost, st.s));
+      MB_CUDA(cudaStreamSynchronize(st.s));
+      for (std::uint64_t i = 0; i < n; ++i) tot[i] |= hm[i];
+    }
+    MB_CUDA(cudaMemcpy(out, buf.ptr, n * S.dim * S.es, cudaMemcpyDeviceToHost));
+    if (mask) std::memcpy(mask, tot.data(), n);
+    std::uint32_t e = 0;
+    MB_CUDA(cudaMemcpy(&e, S.err.ptr, 4, cudaMemcpyDeviceToHost));
+    if (e) throw std::runtime_error("shard: placement invariant violated (code " +
+                                    std::to_string(e) + ")");
+  });
+}
+
+// Bracket the local-round and cross-round data-plane kernels with CUDA events.
+int moshpit_shard_set_timing(moshpit_shard* h, std::int32_t enable) {
+  return guarded([&] {
+    h->s->timing = enable != 0;
+    h->s->used_local = h->s->used_cross = 0;
+  });
+}
+
+int moshpit_shard_kernel_time(moshpit_shard* h, double* local_ms, std::uint64_t* local_n,
+                              double* cross_ms, std::uint64_t* cross_n) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    auto sum = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, std::size_t used) {
+      double t = 0;
+      for (std::size_t i = 0; i < used; ++i) {
+        MB_CUDA(cudaEventSynchronize(v[i].second));
+        float ms = 0;
+        MB_CUDA(cudaEventElapsedTime(&ms, v[i].first, v[i].second));
+        t += ms;
+      }
+      return t;
+    };
+    *local_ms = sum(S.tev_local, S.used_local);
+    *local_n = S.used_local;
+    *cross_ms = sum(S.tev_cross, S.used_cross);
+    *cross_n = S.used_cross;
+    S.used_local = S.used_cross = 0;
+  });
+}
+
+// Device pointer / rows / stride of this rank's local pool (emulation: pool k).
+int moshpit_shard_pool(moshpit_shard* h, std::int32_t k, void** ptr, std::uint64_t* rows,
+                       std::uint64_t* ld) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    *ptr = S.pools[r];
+    *rows = S.R;
+    *ld = S.ld;
+  });
+}
+
+}  // extern "C"
