@@ -40,7 +40,11 @@ CONFIGS = {
     "C2": (32, 2, 1024, 1 << 22, 0.01, 10),
     "C3slab": (16, 3, 4096, 1 << 22, 0.0, 3),
     "C5slab": (8, 4, 4096, 1 << 22, 0.0, 4),
+    # C5 as written (8192 peers on 8^4) is rejected by the reference
+    # (protocols.hpp:116-117); C5v is the closest valid config.
+    "C5v": (8, 4, 4096, 18_000_000, 0.0, 4),
 }
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 PROTOCOL_SEED = 7
 INIT_SEED = 0x5EED
 
@@ -237,6 +241,18 @@ def run_mine(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.mode == "peer":
+        res = run_peer(mb, torch, dist, args.config, args.steps, args.warmup, rank, world, local)
+        if rank == 0:
+            line = dict(res, n_gpus=world, warmup=args.warmup, higher_is_better=True,
+                        vs_baseline=None, dtype="f32", data="synthetic",
+                        config={"workload": res["workload"], "parallelism": f"peer-sharded x{world}"})
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
     cfg = args.config
     M, d, N, D, p, Rcfg = CONFIGS[cfg]
     kernel = {"auto": 0, "register": 1, "bulk": 2}[args.kernel]
@@ -291,6 +307,15 @@ def run_mine(args):
     del x
     torch.cuda.empty_cache()
 
+    peer = None
+    if world > 1 and not args.no_peer:
+        pcfg = "C5v" if 8 % world == 0 and world >= 4 else "C2"
+        try:
+            peer = run_peer(mb, torch, dist, pcfg, max(8, min(args.steps, 40)), 4, rank, world,
+                            local)
+        except Exception as exc:  # noqa: BLE001
+            peer = {"error": str(exc)}
+
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(mb, cfg)
@@ -332,6 +357,7 @@ def run_mine(args):
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "peer_sharded": peer,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -339,6 +365,81 @@ def run_mine(args):
         dist.destroy_process_group()
     eng.close()
     return 0
+
+
+def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
+    """Peer-sharded rounds: peers split by grid digit d-1, rounds on
+    axes 0..d-2 local, the axis d-1 round one fused NVLink kernel.  Returns
+    the whole-problem metric (strong scaling) and the combined roofline."""
+    M, d, N, D, p, Rcfg = CONFIGS[cfg]
+    sh = mb.Shard(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED), D,
+                  rank=rank, world=world, device=local)
+    if world > 1:
+        sh.connect()
+    sh.fill_synthetic(INIT_SEED)
+    for _ in range(warmup):
+        sh.round()
+    torch.cuda.synchronize()
+    c0 = sh.stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sh.set_timing(True)
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        sh.round()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    lms, ln, cms, cn = sh.kernel_time()
+    c1 = sh.stats()
+    sh.set_timing(False)
+    cross_rounds, cross_groups, local_rows = (c1[0] - c0[0], c1[1] - c0[1], c1[2] - c0[2])
+    es, Mg = 4, M // world
+    # minimal (algorithmic) bytes, busiest GPU: every resident row read and
+    # written once per round; in a cross round each GPU must receive the raw
+    # chunk of every remote member (no pre-reduction: the tree spans GPUs) and
+    # one copy of each foreign mean chunk (SURVEY 8d).
+    hbm_local = 2 * es * D * local_rows
+    hbm_cross = 2 * es * D * Mg * cross_groups
+    nvl_cross = cross_groups * es * (D / world) * ((M - Mg) + (world - 1)) if world > 1 else 0
+    peak, _ = peaks()
+    t_roof_local = hbm_local / (peak * 1e9) * 1e3
+    t_roof_cross = max(hbm_cross / (peak * 1e9), nvl_cross / (NVLINK_GBS * 1e9)) * 1e3
+    vals = torch.tensor([t_ms, lms, cms, t_roof_local, t_roof_cross], dtype=torch.float64,
+                        device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_max, lmax, cmax, trl, trc = vals.tolist()
+    sh.close()
+    torch.cuda.empty_cache()
+    value = N * D * es * steps / (t_max / 1e3) / 1e9
+    return {
+        "workload": f"{cfg}: {N} peers on {M}^{d}, D={D} fp32, p_fail={p}, peer-sharded over "
+                    f"{world} GPU(s) (grid digit d-1 split; axes 0..d-2 local)",
+        "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),
+        "unit": "GB/s", "scaling": "strong", "steps": steps, "ms_per_step": round(t_max / steps, 4),
+        "rounds_local": ln, "rounds_cross": cross_rounds,
+        "gpu_launches": ln * 3 + cross_rounds * (6 + (2 if p > 0 else 0)),
+        "local_kernel_ms": round(lmax, 3), "cross_kernel_ms": round(cmax, 3),
+        "roofline": {
+            "bound": "hbm (local rounds) + nvlink (cross rounds)",
+            "local": {"achieved": round(hbm_local / (lmax / 1e3) / 1e9, 1) if lmax else None,
+                      "peak": peak, "unit": "GB/s",
+                      "frac": round(trl / lmax, 4) if lmax else None},
+            "cross": {"nvlink_ingress_gb_per_gpu": round(nvl_cross / 1e9, 3),
+                      "achieved_nvlink": round(nvl_cross / (cmax / 1e3) / 1e9, 1) if cmax else None,
+                      "peak_nvlink": NVLINK_GBS, "unit": "GB/s",
+                      "frac": round(trc / cmax, 4) if cmax else None},
+            "combined_frac": round((trl + trc) / (lmax + cmax), 4) if (lmax + cmax) else None,
+            "note": "t_roof = max(HBM bytes / hbm_gbs, NVLink ingress / 770 GB/s) per round, "
+                    "busiest GPU, minimal bytes (raw remote member chunks + one copy of each "
+                    "foreign mean chunk); t_measured = data-plane kernels incl. the local "
+                    "fan-out; frac = sum t_roof / sum t_measured",
+        },
+    }
 
 
 def measure_e2e(mb, cfg):
@@ -388,6 +489,11 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="skip the peer-sharded (NVLink) measurement attached at N>1")
+    ap.add_argument("--mode", default="coord", choices=["coord", "peer"],
+                    help="coord: coordinate-sharded weak scaling (default); "
+                         "peer: peer-sharded strong scaling with cross-GPU rounds")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")

@@ -203,6 +203,12 @@ int moshpit_shard_set_timing(moshpit_shard* s, int32_t enable);
 int moshpit_shard_kernel_time(moshpit_shard* s, double* local_ms,
                               uint64_t* local_n, double* cross_ms,
                               uint64_t* cross_n);
+/* Cumulative counters (synchronises): cross rounds run, non-voided groups
+ * summed over cross rounds, rows in non-voided local groups on rank k (own
+ * rank in real mode) -- the algorithmic-byte accounting of the bench. */
+int moshpit_shard_stats(moshpit_shard* s, int32_t k, uint64_t* cross_rounds,
+                        uint64_t* cross_active_groups,
+                        uint64_t* local_active_rows);
 int moshpit_shard_pool(moshpit_shard* s, int32_t k, void** ptr, uint64_t* rows,
                        uint64_t* ld);
 

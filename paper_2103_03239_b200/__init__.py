@@ -560,6 +560,12 @@ class Shard:
     def set_timing(self, enable: bool):
         check(lib().moshpit_shard_set_timing(self._h, 1 if enable else 0))
 
+    def stats(self, k: int = 0):
+        """(cross rounds, active groups over cross rounds, local active rows)."""
+        a, b, c = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        check(lib().moshpit_shard_stats(self._h, k, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
     def kernel_time(self):
         lm, ln, cm, cn = C.c_double(0), C.c_uint64(0), C.c_double(0), C.c_uint64(0)
         check(lib().moshpit_shard_kernel_time(self._h, C.byref(lm), C.byref(ln), C.byref(cm),

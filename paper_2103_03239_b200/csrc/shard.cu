@@ -53,6 +53,8 @@ struct PlaceArgs {
   std::uint32_t* moves = nullptr;       // [world][R][2] (src, dst), grouped by dst GPU
   std::uint32_t* n_moves = nullptr;     // [world]
   std::uint32_t* err = nullptr;         // [1]
+  unsigned long long* totals = nullptr; // [0] cross active groups, [1] cross rounds,
+                                        // [2+h] local active rows on GPU h
 };
 
 // Replicated bookkeeping for one round (one CTA, one thread per group).
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
   if (threadIdx.x < a.world * 4) a.cnt_local[threadIdx.x] = 0;
   if (threadIdx.x < 4) a.cnt_cross[threadIdx.x] = 0;
   if (threadIdx.x < a.world) a.n_moves[threadIdx.x] = 0;
+  if (threadIdx.x == 0 && a.cross) a.totals[1] += 1;
   __syncthreads();
   for (std::uint32_t g = threadIdx.x; g < ng; g += blockDim.x) {
     const std::uint32_t b = a.goff[g], e = a.goff[g + 1];
@@ -76,6 +79,7 @@ __global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
         const std::uint32_t k = atomicAdd(&a.cnt_local[owner * 4 + 1], 1u);
         a.act_local[owner * a.n + k] = g;
         atomicAdd(&a.cnt_local[owner * 4 + 2], e - b);
+        atomicAdd(&a.totals[2 + owner], (unsigned long long)(e - b));
       }
       continue;
     }
@@ -113,6 +117,7 @@ __global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
       const std::uint32_t k = atomicAdd(&a.cnt_cross[1], 1u);
       a.act_cross[k] = g;
       atomicAdd(&a.cnt_cross[2], e - b);
+      atomicAdd(&a.totals[0], 1ull);
     }
   }
 }
@@ -170,6 +175,7 @@ struct CrossArgs {
   T* pools[kMaxWorld];
   std::uint64_t ld_vec = 0, R = 0;
   std::uint64_t c0 = 0, c1 = 0, n_tiles = 0;
+  std::uint32_t me = 0;
   const std::uint32_t* goff = nullptr;
   const std::uint32_t* src_row = nullptr;
   const std::uint32_t* dst_row = nullptr;
@@ -184,7 +190,8 @@ __device__ __forceinline__ void cross_fixed(V* const* src, V* const* dst, std::u
   for (int k = 0; k < N; ++k) x[k] = __ldcs(src[k] + col);
   const V m = sdiv(stree<N, 0>(x), (std::uint32_t)N);
 #pragma unroll
-  for (int k = 0; k < N; ++k) __stcs(dst[k] + col, m);
+  for (int k = 0; k < N; ++k)
+    if (dst[k]) __stcs(dst[k] + col, m);
 }
 
 // Fused cross-GPU round: this GPU's coordinate chunk of every active group,
@@ -205,8 +212,19 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
       cnt = a.goff[g + 1] - beg;
       if (threadIdx.x < cnt) {
         const std::uint32_t s = a.src_row[beg + threadIdx.x], d = a.dst_row[beg + threadIdx.x];
+        const std::uint32_t dg = (std::uint32_t)(d / a.R);
+        // A remote GPU receives ONE copy of this chunk's mean, in its first
+        // member row (in group order); it broadcasts locally after the
+        // barrier (shard_bcast_kernel).  Local member rows get it directly.
+        bool store = dg == a.me;
+        if (!store) {
+          store = true;
+          for (std::uint32_t j = 0; j < threadIdx.x; ++j)
+            if ((std::uint32_t)(a.dst_row[beg + j] / a.R) == dg) store = false;
+        }
         s_src[threadIdx.x] = reinterpret_cast<V*>(a.pools[s / a.R]) + (s % a.R) * a.ld_vec;
-        s_dst[threadIdx.x] = reinterpret_cast<V*>(a.pools[d / a.R]) + (d % a.R) * a.ld_vec;
+        s_dst[threadIdx.x] =
+            store ? reinterpret_cast<V*>(a.pools[dg]) + (d % a.R) * a.ld_vec : nullptr;
       }
       cached = g;
       __syncthreads();
@@ -227,6 +245,44 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
 #undef MB_XCASE
       default: break;
     }
+  }
+}
+
+// After the cross round's barrier: copy the foreign chunks (written by their
+// owner GPUs into this GPU's first member row of each active group) into the
+// group's other member rows on this GPU.  Local HBM only.
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads)
+    shard_bcast_kernel(T* pool, std::uint64_t ld_vec, std::uint64_t R, std::uint32_t me,
+                       std::uint64_t own0, std::uint64_t own1, std::uint64_t nvec,
+                       std::uint64_t n_tiles, const std::uint32_t* goff,
+                       const std::uint32_t* dst_row, const std::uint32_t* act,
+                       const std::uint32_t* cnt_cross) {
+  using V = typename V16s<T>::type;
+  __shared__ V* s_rows[32];
+  __shared__ std::uint32_t s_n;
+  const std::uint64_t n_items = (std::uint64_t)cnt_cross[1] * n_tiles;
+  std::uint32_t cached = 0xffffffffu;
+  V* base = reinterpret_cast<V*>(pool);
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t g = act[w / n_tiles];
+    if (g != cached) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        std::uint32_t k = 0;
+        for (std::uint32_t pos = goff[g]; pos < goff[g + 1]; ++pos) {
+          const std::uint32_t d = dst_row[pos];
+          if ((std::uint32_t)(d / R) == me) s_rows[k++] = base + (d % R) * ld_vec;
+        }
+        s_n = k;
+      }
+      cached = g;
+      __syncthreads();
+    }
+    const std::uint64_t col = (w % n_tiles) * kCrossThreads + threadIdx.x;
+    if (col >= nvec || (col >= own0 && col < own1) || s_n < 2) continue;
+    const V v = __ldcs(s_rows[0] + col);
+    for (std::uint32_t k = 1; k < s_n; ++k) __stcs(s_rows[k] + col, v);
   }
 }
 
@@ -342,7 +398,7 @@ struct Shard {
   unsigned long long epoch = 0;
   // replicated bookkeeping
   DeviceBuffer loc, rows_local, act_local, cnt_local, src_row, dst_row, act_cross, cnt_cross,
-      moves, n_moves, err, pool_tab, flag_tab;
+      moves, n_moves, err, pool_tab, flag_tab, totals;
   // pools: [world] in emulation, [1] (mine) otherwise
   std::vector<std::unique_ptr<DeviceBuffer>> own_pools;
   std::vector<std::unique_ptr<DeviceBuffer>> staging;
@@ -398,6 +454,7 @@ struct Shard {
     a.c0 = nv * r / world;
     a.c1 = nv * (r + 1) / world;
     a.n_tiles = (a.c1 - a.c0 + kCrossThreads - 1) / kCrossThreads;
+    a.me = r;
     a.goff = plane->goff.as<std::uint32_t>();
     a.src_row = src_row.as<std::uint32_t>();
     a.dst_row = dst_row.as<std::uint32_t>();
@@ -408,6 +465,20 @@ struct Shard {
                                                           kCrossThreads, 0));
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     if (a.n_tiles) cross_mean_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+
+  template <typename T>
+  void bcast_launch(std::uint32_t r, cudaStream_t s) {
+    if (Mg < 2) return;  // one member per GPU: nothing to fan out
+    const std::uint64_t nv = nvec();
+    const std::uint64_t n_tiles = (nv + kCrossThreads - 1) / kCrossThreads;
+    int sms = 0;
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    shard_bcast_kernel<T><<<sms * 4, kCrossThreads, 0, s>>>(
+        static_cast<T*>(pools[r]), ld * es / 16, R, r, nv * r / world, nv * (r + 1) / world, nv,
+        n_tiles, plane->goff.as<std::uint32_t>(), dst_row.as<std::uint32_t>(),
+        act_cross.as<std::uint32_t>(), cnt_cross.as<std::uint32_t>());
     MB_LAUNCH_CHECK();
   }
 
@@ -453,6 +524,7 @@ struct Shard {
     a.moves = moves.as<std::uint32_t>();
     a.n_moves = n_moves.as<std::uint32_t>();
     a.err = err.as<std::uint32_t>();
+    a.totals = totals.as<unsigned long long>();
     place_kernel<<<1, 1024, 0, s>>>(a);
     MB_LAUNCH_CHECK();
     const std::uint32_t nranks = emulate ? world : 1;
@@ -494,13 +566,22 @@ struct Shard {
       }
       if (timing) MB_CUDA(cudaEventRecord(te.second, s));
       barrier(s);  // every remote read/write of our rows is done
+      std::pair<cudaEvent_t, cudaEvent_t> tb{};
+      if (timing) {
+        tb = tpair(true);
+        MB_CUDA(cudaEventRecord(tb.first, s));
+      }
       for (std::uint32_t k = 0; k < nranks; ++k) {
         const std::uint32_t r = emulate ? k : me;
-        if (dtype == MOSHPIT_F32)
+        if (dtype == MOSHPIT_F32) {
+          bcast_launch<float>(r, s);
           moves_launch<float>(r, 1, s);
-        else
+        } else {
+          bcast_launch<double>(r, s);
           moves_launch<double>(r, 1, s);
+        }
       }
+      if (timing) MB_CUDA(cudaEventRecord(tb.second, s));
     }
     if (crossed) *crossed = a.cross;
     return active;
@@ -574,6 +655,8 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     S.n_moves.resize(world * 4 + 16);
     S.err.resize(16);
     MB_CUDA(cudaMemsetAsync(S.err.ptr, 0, 16, st.s));
+    S.totals.resize(8 * (kMaxWorld + 2));
+    MB_CUDA(cudaMemsetAsync(S.totals.ptr, 0, 8 * (kMaxWorld + 2), st.s));
     const std::uint32_t npools = S.emulate ? S.world : 1;
     for (std::uint32_t k = 0; k < npools; ++k) {
       S.own_pools.push_back(std::make_unique<DeviceBuffer>(S.R * S.ld * es));
@@ -750,6 +833,24 @@ int moshpit_shard_kernel_time(moshpit_shard* h, double* local_ms, std::uint64_t*
     *cross_ms = sum(S.tev_cross, S.used_cross);
     *cross_n = S.used_cross;
     S.used_local = S.used_cross = 0;
+  });
+}
+
+// Cumulative counters (synchronises): cross rounds, active groups summed over
+// cross rounds, and rows in non-voided local groups on rank `k` (this rank's
+// own index in real mode).
+int moshpit_shard_stats(moshpit_shard* h, std::int32_t k, std::uint64_t* cross_rounds,
+                        std::uint64_t* cross_active_groups, std::uint64_t* local_active_rows) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    MB_CUDA(cudaDeviceSynchronize());
+    unsigned long long t[kMaxWorld + 2];
+    MB_CUDA(cudaMemcpy(t, S.totals.ptr, sizeof(t), cudaMemcpyDeviceToHost));
+    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    *cross_rounds = t[1];
+    *cross_active_groups = t[0];
+    *local_active_rows = t[2 + r];
   });
 }
 
