@@ -135,6 +135,31 @@ int moshpit_moshpit_average(int dtype, void* thetas, uint64_t n, uint64_t dim,
                             uint32_t M, uint32_t d, uint32_t rounds,
                             moshpit_rng_state* stream);
 
+/* ---- optimizer.hpp:231-242 local_step, Quadratic objective  [GPU] --------
+ * Quadratic(dim, L, mu, target) (optimizer.hpp:31-72); the noise is drawn
+ * from *noise exactly as the reference draws it; theta (host, dtype) is
+ * updated in place.  runtime_error on a non-finite gradient. */
+int moshpit_local_step_quadratic(int dtype, void* theta, uint64_t dim, double L,
+                                 double mu, const double* target, double gamma,
+                                 double sigma, moshpit_rng_state* noise);
+
+/* ---- optimizer.hpp:297-439 run_moshpit_sgd, Quadratic objective [GPU] ----
+ * Schedule: n_events MembershipEvent{ev_step[e], ev_delta[e]}.  diag:
+ * MOSHPIT_DIAG_EXACT (reference summation order) or MOSHPIT_DIAG_FAST.
+ * noise_mode 0: the reference's "noise" stream (host draws, bit-exact);
+ * 1: device Philox4x32-10 normals (statistical parity, the fast path).
+ * Outputs: f_gap, grad_norm_sq, f_gap_weighted, dispersion [steps];
+ * final_mean [dim]; diag6 = {delta_aq_hat, sigma_hat, delta_pv1_hat,
+ * delta_pv2_hat, n_min, n_final}; final_thetas (nullable, n_final*dim). */
+int moshpit_run_moshpit_sgd_quadratic(
+    int dtype, uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers,
+    uint64_t dim, double L, double mu, const double* target,
+    const double* theta0, double gamma, uint32_t tau, uint32_t steps,
+    double sigma, uint32_t inner_rounds, uint64_t seed, const uint32_t* ev_step,
+    const int32_t* ev_delta, uint64_t n_events, int diag, int noise_mode,
+    double* f_gap, double* grad_norm_sq, double* f_gap_weighted,
+    double* dispersion, double* final_mean, double* diag6, void* final_thetas);
+
 /* ---- device-resident engine (the performance boundary) -----------------
  * One engine = one trial's integer plane (grid, keys, rng streams, group
  * tables) resident on `device`.  The peer state is caller-owned device

@@ -108,7 +108,15 @@ int orc_moshpit_trace(uint32_t M, uint32_t d, uint64_t n, double p,
                             double* cost_units, R* final_vectors);             \
   int orc_moshpit_average_##SFX(R* thetas, uint64_t n, uint64_t dim,           \
                                 uint32_t M, uint32_t d, uint32_t rounds,       \
-                                orc_rng* stream);
+                                orc_rng* stream);                               \
+  int orc_sgd_quadratic_##SFX(                                                 \
+      uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers, uint64_t dim,      \
+      double L, double mu, const double* target, const double* theta0,         \
+      double gamma, uint32_t tau, uint32_t steps, double sigma,                \
+      uint32_t inner_rounds, uint64_t seed, const uint32_t* ev_step,           \
+      const int32_t* ev_delta, uint64_t n_events, double* f_gap,               \
+      double* grad_norm_sq, double* f_gap_weighted, double* dispersion,        \
+      double* final_mean, double* diag6, R* final_thetas);
 
 ORC_DECLARE_REAL(double, f64)
 ORC_DECLARE_REAL(float, f32)

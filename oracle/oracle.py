@@ -80,6 +80,10 @@ class Checker:
             f("moshpit_trace", C.c_int,
               [u32, u32, u64, dbl, u64, u32, vp, vp, vp, vp, vp, vp, vp, vp])
             f("init_value", dbl, [u64, u64, u64])
+            for sfx in ("f64", "f32"):
+                f(f"sgd_quadratic_{sfx}", C.c_int,
+                  [u32, u32, u32, u32, u64, dbl, dbl, vp, vp, dbl, u32, u32, dbl, u32, u64, vp,
+                   vp, u64, vp, vp, vp, vp, vp, vp, vp])
             f("rng_stream", None, [vp, u64, cstr])
         else:
             f("pairwise_sum", dbl, [vp, u64])
@@ -92,6 +96,10 @@ class Checker:
             f("run_moshpit_vectors", C.c_int,
               [u32, u32, u32, vp, u64, u64, dbl, u64, u32, vp, vp, vp, vp, vp, vp])
             f("moshpit_average", C.c_int, [vp, u64, u64, u32, u32, u32, u64, cstr])
+            f("sgd_quadratic", C.c_int,
+              [u32, u32, u32, u32, u64, dbl, dbl, vp, vp, dbl, u32, u32, dbl, u32, u64, vp,
+               vp, u64, vp, vp, vp, vp, vp, vp])
+            f("local_step_quadratic", C.c_int, [vp, u64, dbl, dbl, vp, dbl, dbl, u64, cstr])
             f("slice_bench", C.c_int,
               [u32, u32, u64, u64, u64, u64, u64, u64, dbl, u32, u32, vp, vp, vp])
 
@@ -229,6 +237,43 @@ class Checker:
             _check(getattr(self, "_moshpit_average" + self._sfx(x.dtype))(
                 _p(x), n, dim, M, d, rounds, C.byref(st)), "moshpit_average")
         return x
+
+    def sgd_quadratic(self, M, d, n_peers, dim, L, mu, target, theta0, gamma, tau, steps, sigma,
+                      seed, inner_rounds=0, schedule=(), T=1, dtype=np.float64):
+        """run_moshpit_sgd(Quadratic(dim, L, mu, target)); returns a dict."""
+        tgt = np.ascontiguousarray(target, dtype=np.float64)
+        th0 = np.ascontiguousarray(theta0, dtype=np.float64)
+        evs = np.array([e[0] for e in schedule], dtype=np.uint32)
+        evd = np.array([e[1] for e in schedule], dtype=np.int32)
+        K = max(steps, 1)
+        out = {k: np.zeros(K) for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion")}
+        fm = np.zeros(max(dim, 1))
+        diag = np.zeros(6)
+        n_max = n_peers + sum(max(e[1], 0) for e in schedule)
+        args = [M, d, T, n_peers, dim, L, mu, _p(tgt), _p(th0), gamma, tau, steps, sigma,
+                inner_rounds, seed, _p(evs) if len(evs) else None, _p(evd) if len(evd) else None,
+                len(evs), _p(out["f_gap"]), _p(out["grad_norm_sq"]), _p(out["f_gap_weighted"]),
+                _p(out["dispersion"]), _p(fm), _p(diag)]
+        fin = None
+        if self.kind == "ref":
+            _check(self._sgd_quadratic(*args), "sgd_quadratic")
+        else:
+            fin = np.zeros((n_max, max(dim, 1)), dtype=dtype)
+            _check(getattr(self, "_sgd_quadratic" + self._sfx(dtype))(*args, _p(fin)),
+                   "sgd_quadratic")
+            fin = fin[: int(diag[5]), :dim]
+        res = {k: v[:steps] for k, v in out.items()}
+        res.update(final_mean=fm[:dim], delta_aq_hat=diag[0], sigma_hat=diag[1],
+                   delta_pv1_hat=diag[2], delta_pv2_hat=diag[3], n_min=int(diag[4]),
+                   final_thetas=fin)
+        return res
+
+    def local_step_quadratic(self, theta, L, mu, target, gamma, sigma, seed, name):
+        th = np.ascontiguousarray(theta, dtype=np.float64).copy()
+        tgt = np.ascontiguousarray(target, dtype=np.float64)
+        _check(self._local_step_quadratic(_p(th), len(th), L, mu, _p(tgt), gamma, sigma, seed,
+                                          name.encode()), "local_step")
+        return th
 
     # ---- oracle-only ------------------------------------------------------------
     def trace(self, M, d, n, p, seed, rounds):

@@ -275,6 +275,58 @@ int ref_moshpit_average(double* thetas, std::uint64_t n, std::uint64_t dim,
   });
 }
 
+// optimizer::run_moshpit_sgd with the Quadratic objective (optimizer.hpp:297).
+int ref_sgd_quadratic(std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
+                      std::uint64_t dim, double L, double mu, const double* target,
+                      const double* theta0, double gamma, std::uint32_t tau,
+                      std::uint32_t steps, double sigma, std::uint32_t inner_rounds,
+                      std::uint64_t seed, const std::uint32_t* ev_step,
+                      const std::int32_t* ev_delta, std::uint64_t n_events, double* f_gap,
+                      double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
+                      double* final_mean, double* diag6) {
+  return guarded([&] {
+    const optimizer::Quadratic quad(dim, L, mu, ParamVector(target, target + dim));
+    optimizer::OptimizerConfig cfg;
+    cfg.gamma = gamma;
+    cfg.tau = tau;
+    cfg.steps = steps;
+    cfg.grid = GridConfig{M, d, T};
+    cfg.sigma = sigma;
+    cfg.n_peers = n_peers;
+    cfg.inner_rounds = inner_rounds;
+    std::vector<optimizer::MembershipEvent> sched;
+    for (std::uint64_t e = 0; e < n_events; ++e) sched.push_back({ev_step[e], ev_delta[e]});
+    const auto r = optimizer::run_moshpit_sgd(cfg, quad, ParamVector(theta0, theta0 + dim), sched,
+                                              Rng(seed));
+    for (std::size_t k = 0; k < r.f_gap.size(); ++k) {
+      f_gap[k] = r.f_gap[k];
+      grad_norm_sq[k] = r.grad_norm_sq[k];
+      f_gap_weighted[k] = r.f_gap_weighted[k];
+      dispersion[k] = r.diagnostics.dispersion[k];
+    }
+    for (std::size_t j = 0; j < r.final_mean.size(); ++j) final_mean[j] = r.final_mean[j];
+    diag6[0] = r.diagnostics.delta_aq_hat;
+    diag6[1] = r.diagnostics.sigma_hat;
+    diag6[2] = r.diagnostics.delta_pv1_hat;
+    diag6[3] = r.diagnostics.delta_pv2_hat;
+    diag6[4] = r.diagnostics.n_min;
+    diag6[5] = 0;
+  });
+}
+
+// optimizer::local_step with the Quadratic objective over Rng(seed).stream(name).
+int ref_local_step_quadratic(double* theta, std::uint64_t dim, double L, double mu,
+                             const double* target, double gamma, double sigma,
+                             std::uint64_t seed, const char* name) {
+  return guarded([&] {
+    const optimizer::Quadratic quad(dim, L, mu, ParamVector(target, target + dim));
+    ParamVector th(theta, theta + dim);
+    auto s = Rng(seed).stream(name);
+    optimizer::local_step(th, quad, gamma, sigma, s);
+    std::memcpy(theta, th.data(), dim * sizeof(double));
+  });
+}
+
 // CPU baseline: the unmodified run_moshpit on `slices` column slices of
 // width `width` of the counter-initialised state, spread over
 // `threads` host threads.  Coordinates are independent, so each slice is

@@ -30,7 +30,8 @@ __all__ = [
     "PartitionWeights", "chunk_sizes", "AllReduceOutcome", "butterfly_allreduce",
     "group_mean", "distortion", "mean_of", "TrialReport", "run_moshpit", "moshpit_average",
     "complexity_estimate", "Engine", "fill_synthetic", "InvalidArgument", "OutOfRange",
-    "CudaError", "MoshpitError", "device_count", "Shard",
+    "CudaError", "MoshpitError", "device_count", "Shard", "Quadratic", "OptimizerConfig",
+    "MembershipEvent", "SgdResult", "AssumptionDiagnostics", "local_step", "run_moshpit_sgd",
 ]
 
 
@@ -373,6 +374,130 @@ def moshpit_average(thetas, grid: GridConfig, rounds: int, stream: RngStream):
                                         grid.peers_per_axis, grid.dims, rounds,
                                         C.byref(stream.state)))
     return x
+
+
+# ---------------------------------------------------------------------------
+# optimizer.hpp:31-72, 186-227, 231-242, 297-439 (Quadratic objective)
+# ---------------------------------------------------------------------------
+class Quadratic:
+    """Axis-aligned quadratic with curvature interpolated mu -> L."""
+
+    def __init__(self, dim: int, l: float, mu: float, target):
+        if l < mu or mu < 0.0:
+            raise InvalidArgument("Quadratic: need L >= mu >= 0")
+        t = np.ascontiguousarray(target, dtype=np.float64).reshape(-1)
+        if len(t) != dim:
+            raise InvalidArgument("Quadratic: target dimension mismatch")
+        self._dim, self.l, self.mu, self.target = int(dim), float(l), float(mu), t
+
+    def dim(self):
+        return self._dim
+
+    def smoothness(self):
+        return self.l
+
+    def strong_convexity(self):
+        return self.mu
+
+    def optimum_value(self):
+        return 0.0
+
+    def optimum(self):
+        return self.target
+
+
+@dataclass
+class OptimizerConfig:
+    gamma: float = 0.1
+    tau: int = 1
+    steps: int = 100
+    grid: GridConfig = field(default_factory=GridConfig)
+    sigma: float = 0.0
+    n_peers: int = 1
+    inner_rounds: int = 0
+
+    def validate(self):
+        if self.gamma <= 0.0:
+            raise InvalidArgument("OptimizerConfig: gamma > 0")
+        if self.tau < 1:
+            raise InvalidArgument("OptimizerConfig: tau >= 1")
+        if self.sigma < 0.0:
+            raise InvalidArgument("OptimizerConfig: sigma >= 0")
+        self.grid.validate()
+        if self.n_peers < 1 or self.n_peers > self.grid.capacity():
+            raise InvalidArgument("OptimizerConfig: 1 <= N <= M^d")
+
+
+@dataclass
+class MembershipEvent:
+    step: int = 0
+    delta: int = 0
+
+
+@dataclass
+class AssumptionDiagnostics:
+    dispersion: List[float] = field(default_factory=list)
+    delta_aq_hat: float = 0.0
+    sigma_hat: float = 0.0
+    delta_pv1_hat: float = 0.0
+    delta_pv2_hat: float = 0.0
+    n_min: int = 0
+
+
+@dataclass
+class SgdResult:
+    f_gap: List[float] = field(default_factory=list)
+    grad_norm_sq: List[float] = field(default_factory=list)
+    f_gap_weighted: List[float] = field(default_factory=list)
+    final_mean: Optional[np.ndarray] = None
+    diagnostics: AssumptionDiagnostics = field(default_factory=AssumptionDiagnostics)
+    final_thetas: Optional[np.ndarray] = None  # extension
+
+
+def local_step(theta: np.ndarray, objective: Quadratic, gamma: float, sigma: float,
+               noise: RngStream) -> np.ndarray:
+    """optimizer::local_step on the GPU (in place for float arrays)."""
+    x = theta if (isinstance(theta, np.ndarray) and theta.dtype in (np.float32, np.float64)
+                  and theta.flags.c_contiguous) else np.ascontiguousarray(theta, np.float64)
+    check(lib().moshpit_local_step_quadratic(_dtype_code(x.dtype), _p(x), len(x), objective.l,
+                                             objective.mu, _p(objective.target), gamma, sigma,
+                                             C.byref(noise.state)))
+    return x
+
+
+def run_moshpit_sgd(config: OptimizerConfig, objective: Quadratic, theta0,
+                    schedule: Sequence[MembershipEvent], rng: Rng, *, dtype=np.float64,
+                    diagnostics: str = "exact", noise: str = "reference",
+                    return_thetas: bool = False) -> SgdResult:
+    """optimizer::run_moshpit_sgd on the GPU.  float64 + diagnostics="exact" +
+    noise="reference" is bit-identical to the reference; noise="device" uses
+    Philox normals on the GPU (statistical parity, no O(N*D) host draws)."""
+    th0 = np.ascontiguousarray(theta0, dtype=np.float64).reshape(-1)
+    if len(th0) != objective.dim():
+        config.validate()
+        raise InvalidArgument("run_moshpit_sgd: theta0 dimension mismatch")
+    K = max(config.steps, 1)
+    out = {k: np.zeros(K) for k in ("f_gap", "g", "fw", "disp")}
+    dim = objective.dim()
+    fm = np.zeros(max(dim, 1))
+    d6 = np.zeros(6)
+    evs = np.array([e.step for e in schedule], dtype=np.uint32)
+    evd = np.array([e.delta for e in schedule], dtype=np.int32)
+    n_max = config.n_peers + sum(max(e.delta, 0) for e in schedule)
+    fin = np.zeros((n_max, max(dim, 1)), dtype=dtype) if return_thetas else None
+    check(lib().moshpit_run_moshpit_sgd_quadratic(
+        _dtype_code(dtype), config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
+        config.n_peers, dim, objective.l, objective.mu, _p(objective.target), _p(th0),
+        config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds, rng.seed(),
+        _p(evs) if len(evs) else None, _p(evd) if len(evd) else None, len(evs),
+        _DIAG[diagnostics], {"reference": 0, "device": 1}[noise], _p(out["f_gap"]),
+        _p(out["g"]), _p(out["fw"]), _p(out["disp"]), _p(fm), _p(d6), _p(fin)))
+    n_fin = int(d6[5])
+    diag = AssumptionDiagnostics(list(out["disp"][:config.steps]), d6[0], d6[1], d6[2], d6[3],
+                                 int(d6[4]))
+    return SgdResult(list(out["f_gap"][:config.steps]), list(out["g"][:config.steps]),
+                     list(out["fw"][:config.steps]), fm[:dim], diag,
+                     None if fin is None else fin[:n_fin, :dim])
 
 
 # ---------------------------------------------------------------------------

@@ -70,6 +70,12 @@ PROTOTYPES = {
     "moshpit_run_moshpit": (C.c_int, [C.c_int, u32, u32, u32, vp, u64, u64, dbl, u64, u32,
                                       C.c_int, P(dbl), vp, vp, vp, P(dbl), vp]),
     "moshpit_moshpit_average": (C.c_int, [C.c_int, vp, u64, u64, u32, u32, u32, P(RngState)]),
+    "moshpit_local_step_quadratic": (C.c_int, [C.c_int, vp, u64, dbl, dbl, vp, dbl, dbl,
+                                               P(RngState)]),
+    "moshpit_run_moshpit_sgd_quadratic": (C.c_int, [C.c_int, u32, u32, u32, u32, u64, dbl, dbl,
+                                                    vp, vp, dbl, u32, u32, dbl, u32, u64, vp, vp,
+                                                    u64, C.c_int, C.c_int, vp, vp, vp, vp, vp,
+                                                    vp, vp]),
     "moshpit_engine_create": (C.c_int, [u32, u32, u64, dbl, u64, C.c_int, P(vp)]),
     "moshpit_engine_destroy": (C.c_int, [vp]),
     "moshpit_engine_set_kernel": (C.c_int, [vp, C.c_int]),

@@ -1,0 +1,578 @@
+// sgd.cu -- Moshpit SGD on the Quadratic objective (SURVEY 8a rows a17/a18,
+// 8f rank 1): optimizer::local_step (optimizer.hpp:231-242) and
+// optimizer::run_moshpit_sgd (optimizer.hpp:297-439) on the GPU.
+//
+// Per step: membership events (leavers truncate, joiners copy a donor row:
+// device memcpy), the local step theta <- theta - gamma*(c*(theta - t) + noise)
+// as one elementwise kernel (no FMA: the reference rounds the product and the
+// difference separately), the averaging pass (kernels 1 + 2 on the shared
+// "averaging" stream, cells redrawn each sync exactly as
+// optimizer.hpp:254-268), and the diagnostics as fp64 device reductions
+// (EXACT: the reference's sequential order; FAST: fixed-order blocks).
+// Noise: the reference's own sequential polar stream drawn on the host
+// (bit-exact; O(N*D) host draws per step) or a counter-based Philox4x32-10
+// normal on the device (statistical parity; the performance path).
+#include <cmath>
+#include <memory>
+
+#include "plane.cuh"
+
+namespace mb200 {
+namespace {
+
+template <typename T>
+struct SOps;
+template <>
+struct SOps<float> {
+  __device__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+  __device__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ static float add(float a, float b) { return __fadd_rn(a, b); }
+};
+template <>
+struct SOps<double> {
+  __device__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ static double add(double a, double b) { return __dadd_rn(a, b); }
+};
+
+// Philox4x32-10 (Salmon et al. 2011), counter = (step, peer, j/4, 0).
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const std::uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+__device__ __forceinline__ void box_muller(std::uint32_t a, std::uint32_t b, double& z0,
+                                           double& z1) {
+  const double u1 = ((double)a + 1.0) * 0x1.0p-32;  // (0, 1]
+  const double u2 = (double)b * 0x1.0p-32;
+  const double r = sqrt(-2.0 * log(u1));
+  double s, c;
+  sincospi(2.0 * u2, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
+constexpr int kStepThreads = 256;
+
+// theta <- theta - gamma * (c * (theta - t) + nj)   (optimizer.hpp:356-373)
+template <typename T>
+__global__ void __launch_bounds__(kStepThreads)
+    sgd_step_kernel(T* __restrict__ x, std::uint64_t n, std::uint64_t dim, std::uint64_t ld,
+                    const T* __restrict__ curv, const T* __restrict__ tgt, T gamma,
+                    const T* __restrict__ noise, double coord_std, int philox_mode,
+                    std::uint64_t seed, std::uint64_t step, std::uint32_t* nonfinite,
+                    double* noise_partial) {
+  using O = SOps<T>;
+  __shared__ double red[kStepThreads];
+  double nsq = 0.0;
+  const std::uint64_t quads = (dim + 3) / 4;
+  const std::uint64_t total = n * quads;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t i = e / quads, q = e % quads;
+    double z[4] = {0, 0, 0, 0};
+    if (philox_mode) {
+      const uint4 r = philox(make_uint4((std::uint32_t)step, (std::uint32_t)i, (std::uint32_t)q,
+                                        (std::uint32_t)(q >> 32)),
+                             make_uint2((std::uint32_t)seed, (std::uint32_t)(seed >> 32)));
+      box_muller(r.x, r.y, z[0], z[1]);
+      box_muller(r.z, r.w, z[2], z[3]);
+    }
+    for (int u = 0; u < 4; ++u) {
+      const std::uint64_t j = q * 4 + u;
+      if (j >= dim) break;
+      T* p = x + i * ld + j;
+      T g = O::mul(curv[j], O::sub(*p, tgt[j]));
+      if (noise) {
+        g = O::add(g, noise[i * dim + j]);
+      } else if (philox_mode) {
+        const double nj = coord_std * z[u];
+        nsq += nj * nj;
+        g = O::add(g, (T)nj);
+      }
+      if (!isfinite((double)g)) atomicOr(nonfinite, 1u);
+      *p = O::sub(*p, O::mul(gamma, g));
+    }
+  }
+  if (philox_mode) {
+    red[threadIdx.x] = nsq;
+    __syncthreads();
+    for (int s = kStepThreads / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) noise_partial[blockIdx.x] = red[0];
+  }
+}
+
+// Sequential D-vector diagnostics (EXACT, one thread, optimizer.hpp:386-418):
+// out[0] pv inner product, [1] f(mean), [2] |grad f(mean)|^2, [3] f(weighted);
+// wsum[j] += w_k * mean[j] in place.
+__global__ void sgd_vec_exact(const double* __restrict__ mean, const double* __restrict__ hat,
+                              const double* __restrict__ c, const double* __restrict__ t,
+                              double* __restrict__ wsum, double w_k, double weight_total,
+                              std::uint64_t dim, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double ip = 0.0, f = 0.0, gn = 0.0, fw = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double mj = mean[j];
+    ip = __dadd_rn(ip, __dmul_rn(__dsub_rn(mj, hat[j]), __dadd_rn(mj, hat[j])));
+    const double dd = __dsub_rn(mj, t[j]);
+    f = __dadd_rn(f, __dmul_rn(__dmul_rn(__dmul_rn(0.5, c[j]), dd), dd));
+    const double g = __dmul_rn(c[j], dd);
+    gn = __dadd_rn(gn, __dmul_rn(g, g));
+    const double ws = __dadd_rn(wsum[j], __dmul_rn(w_k, mj));
+    wsum[j] = ws;
+    const double wd = __dsub_rn(__ddiv_rn(ws, weight_total), t[j]);
+    fw = __dadd_rn(fw, __dmul_rn(__dmul_rn(__dmul_rn(0.5, c[j]), wd), wd));
+  }
+  out[0] = ip;
+  out[1] = f;
+  out[2] = gn;
+  out[3] = fw;
+}
+
+constexpr int kRed = 256;
+constexpr std::uint64_t kChunk = 1 << 16;
+
+__device__ double blk_sum(double v, double* buf) {
+  buf[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kRed / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) buf[threadIdx.x] = __dadd_rn(buf[threadIdx.x], buf[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double r = buf[0];
+  __syncthreads();
+  return r;
+}
+
+// FAST variant: fixed-order chunk partials, folded by sgd_vec_fold.
+__global__ void sgd_vec_fast(const double* __restrict__ mean, const double* __restrict__ hat,
+                             const double* __restrict__ c, const double* __restrict__ t,
+                             double* __restrict__ wsum, double w_k, double weight_total,
+                             std::uint64_t dim, double* __restrict__ partial) {
+  __shared__ double buf[kRed];
+  const std::uint64_t lo = blockIdx.x * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double a[4] = {0, 0, 0, 0};
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRed) {
+    const double mj = mean[j];
+    a[0] = __dadd_rn(a[0], __dmul_rn(__dsub_rn(mj, hat[j]), __dadd_rn(mj, hat[j])));
+    const double dd = __dsub_rn(mj, t[j]);
+    a[1] = __dadd_rn(a[1], __dmul_rn(__dmul_rn(__dmul_rn(0.5, c[j]), dd), dd));
+    const double g = __dmul_rn(c[j], dd);
+    a[2] = __dadd_rn(a[2], __dmul_rn(g, g));
+    const double ws = __dadd_rn(wsum[j], __dmul_rn(w_k, mj));
+    wsum[j] = ws;
+    const double wd = __dsub_rn(__ddiv_rn(ws, weight_total), t[j]);
+    a[3] = __dadd_rn(a[3], __dmul_rn(__dmul_rn(__dmul_rn(0.5, c[j]), wd), wd));
+  }
+  for (int q = 0; q < 4; ++q) {
+    const double s = blk_sum(a[q], buf);
+    if (threadIdx.x == 0) partial[blockIdx.x * 4 + q] = s;
+  }
+}
+
+__global__ void sgd_vec_fold(const double* __restrict__ partial, std::uint64_t nch,
+                             double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s[4] = {0, 0, 0, 0};
+  for (std::uint64_t c = 0; c < nch; ++c)
+    for (int q = 0; q < 4; ++q) s[q] = __dadd_rn(s[q], partial[c * 4 + q]);
+  for (int q = 0; q < 4; ++q) out[q] = s[q];
+}
+
+// V_k = sum_i sum_j (theta_ij - mean_j)^2 / n, EXACT: one running sum over
+// (i, j) in row-major order (optimizer.hpp:394-401).
+template <typename T>
+__global__ void dispersion_exact(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                                 std::uint64_t dim, const double* __restrict__ mean,
+                                 double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double v = 0.0;
+  for (std::uint64_t i = 0; i < n; ++i)
+    for (std::uint64_t j = 0; j < dim; ++j) {
+      const double dd = __dsub_rn((double)x[i * ld + j], mean[j]);
+      v = __dadd_rn(v, __dmul_rn(dd, dd));
+    }
+  *out = __ddiv_rn(v, (double)n);
+}
+
+// FAST: block (chunk, row) partials, then one fold in (row, chunk) order.
+template <typename T>
+__global__ void dispersion_fast(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                                const double* __restrict__ mean, std::uint64_t nch,
+                                double* __restrict__ partial) {
+  __shared__ double buf[kRed];
+  const std::uint64_t c = blockIdx.x, i = blockIdx.y;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double a = 0.0;
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRed) {
+    const double dd = __dsub_rn((double)x[i * ld + j], mean[j]);
+    a = __dadd_rn(a, __dmul_rn(dd, dd));
+  }
+  const double s = blk_sum(a, buf);
+  if (threadIdx.x == 0) partial[i * nch + c] = s;
+}
+
+__global__ void fold_all(const double* __restrict__ partial, std::uint64_t count, double div,
+                         double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (std::uint64_t k = 0; k < count; ++k) s = __dadd_rn(s, partial[k]);
+  *out = __ddiv_rn(s, div);
+}
+
+template <typename T>
+__global__ void cast_kernel(const double* __restrict__ in, T* __restrict__ out,
+                            std::uint64_t n) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (T)in[i];
+}
+
+template <typename T>
+__global__ void broadcast_theta0(T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                                 std::uint64_t dim, const double* __restrict__ th0) {
+  const std::uint64_t total = n * dim;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x)
+    x[(e / dim) * ld + e % dim] = (T)th0[e % dim];
+}
+
+unsigned grid_for(std::uint64_t work, unsigned threads) {
+  std::uint64_t b = (work + threads - 1) / threads;
+  if (b > 148ull * 16) b = 148ull * 16;
+  return (unsigned)(b ? b : 1);
+}
+
+}  // namespace
+
+// optimizer.hpp:39-44
+std::vector<double> quad_curvature(std::uint64_t dim, double L, double mu) {
+  std::vector<double> c(dim ? dim : 1);
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double t = dim > 1 ? static_cast<double>(j) / static_cast<double>(dim - 1) : 0.0;
+    c[j] = mu + (L - mu) * t;
+  }
+  if (dim == 1) c[0] = L;
+  return c;
+}
+
+struct SgdRun {
+  int dtype;
+  std::size_t es;
+  std::uint64_t dim, ld;
+  cudaStream_t s;
+  DeviceBuffer c64, t64, cT, tT, noise_dev, flag, npart, hat, mean, wsum, vpart, vout, dpart;
+  double noise_sq_host = 0.0;
+
+  template <typename T>
+  void step(void* x, std::uint64_t n, double gamma, double coord_std, int philox,
+            std::uint64_t seed, std::uint64_t k, const T* noise_host_rows) {
+    const T* nz = nullptr;
+    if (noise_host_rows) {
+      noise_dev.resize(n * dim * sizeof(T) + 16);
+      MB_CUDA(cudaMemcpyAsync(noise_dev.ptr, noise_host_rows, n * dim * sizeof(T),
+                              cudaMemcpyHostToDevice, s));
+      nz = noise_dev.as<T>();
+    }
+    const unsigned grid = grid_for(n * ((dim + 3) / 4), kStepThreads);
+    sgd_step_kernel<T><<<grid, kStepThreads, 0, s>>>(
+        static_cast<T*>(x), n, dim, ld, cT.as<T>(), tT.as<T>(), (T)gamma, nz, coord_std,
+        philox, seed, k, flag.as<std::uint32_t>(), npart.as<double>() + k * 148 * 16);
+    MB_LAUNCH_CHECK();
+  }
+};
+
+}  // namespace mb200
+
+using namespace mb200;
+
+extern "C" {
+
+// optimizer.hpp:231-242 local_step with Quadratic(dim, L, mu, target); the
+// noise is drawn from *noise (the caller's RngStream), as the reference does.
+int moshpit_local_step_quadratic(int dtype, void* theta, std::uint64_t dim, double L, double mu,
+                                 const double* target, double gamma, double sigma,
+                                 moshpit_rng_state* noise) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (L < mu || mu < 0.0) throw std::invalid_argument("Quadratic: need L >= mu >= 0");
+    if (dim == 0) return;
+    require_device();
+    Xoshiro st;
+    std::memcpy(st.s, noise->s, sizeof(st.s));
+    st.have_spare = noise->have_spare != 0;
+    st.spare = noise->spare;
+    const double coord_std = sigma > 0.0 ? sigma / std::sqrt(static_cast<double>(dim)) : 0.0;
+    std::vector<double> nz;
+    if (coord_std > 0.0) {
+      nz.resize(dim);
+      for (auto& v : nz) v = coord_std * st.normal();
+    }
+    StreamHolder h;
+    SgdRun r{dtype, es, dim, dim, h.s};
+    const auto c = quad_curvature(dim, L, mu);
+    r.cT.resize(dim * es);
+    r.tT.resize(dim * es);
+    r.flag.resize(16);
+    r.npart.resize(148 * 16 * 8 + 16);
+    DeviceBuffer x(dim * es + 16), tmp(dim * 8 + 16);
+    MB_CUDA(cudaMemsetAsync(r.flag.ptr, 0, 16, h.s));
+    MB_CUDA(cudaMemcpyAsync(x.ptr, theta, dim * es, cudaMemcpyHostToDevice, h.s));
+    DeviceBuffer c64(dim * 8), t64(dim * 8);
+    MB_CUDA(cudaMemcpyAsync(c64.ptr, c.data(), dim * 8, cudaMemcpyHostToDevice, h.s));
+    MB_CUDA(cudaMemcpyAsync(t64.ptr, target, dim * 8, cudaMemcpyHostToDevice, h.s));
+    const unsigned b = (unsigned)((dim + 255) / 256);
+    if (dtype == MOSHPIT_F32) {
+      cast_kernel<float><<<b, 256, 0, h.s>>>(c64.as<double>(), r.cT.as<float>(), dim);
+      cast_kernel<float><<<b, 256, 0, h.s>>>(t64.as<double>(), r.tT.as<float>(), dim);
+      std::vector<float> nzf(nz.begin(), nz.end());
+      r.step<float>(x.ptr, 1, gamma, coord_std, 0, 0, 0, nz.empty() ? nullptr : nzf.data());
+      MB_CUDA(cudaStreamSynchronize(h.s));
+    } else {
+      cast_kernel<double><<<b, 256, 0, h.s>>>(c64.as<double>(), r.cT.as<double>(), dim);
+      cast_kernel<double><<<b, 256, 0, h.s>>>(t64.as<double>(), r.tT.as<double>(), dim);
+      r.step<double>(x.ptr, 1, gamma, coord_std, 0, 0, 0, nz.empty() ? nullptr : nz.data());
+      MB_CUDA(cudaStreamSynchronize(h.s));
+    }
+    std::uint32_t bad = 0;
+    MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
+    if (bad) throw std::runtime_error("local_step: non-finite gradient");
+    MB_CUDA(cudaMemcpy(theta, x.ptr, dim * es, cudaMemcpyDeviceToHost));
+    std::memcpy(noise->s, st.s, sizeof(st.s));
+    noise->have_spare = st.have_spare ? 1 : 0;
+    noise->spare = st.spare;
+  });
+}
+
+// optimizer.hpp:297-439 run_moshpit_sgd with Quadratic(dim, L, mu, target).
+// noise_mode 0: the reference "noise" stream (host draws, bit-exact);
+// noise_mode 1: device Philox normals (statistical parity).
+// diag: MOSHPIT_DIAG_EXACT or MOSHPIT_DIAG_FAST.  diag6 = {delta_aq_hat,
+// sigma_hat, delta_pv1_hat, delta_pv2_hat, n_min, n_final}.
+int moshpit_run_moshpit_sgd_quadratic(
+    int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
+    std::uint64_t dim, double L, double mu, const double* target, const double* theta0,
+    double gamma, std::uint32_t tau, std::uint32_t steps, double sigma,
+    std::uint32_t inner_rounds, std::uint64_t seed, const std::uint32_t* ev_step,
+    const std::int32_t* ev_delta, std::uint64_t n_events, int diag, int noise_mode,
+    double* f_gap, double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
+    double* final_mean, double* diag6, void* final_thetas) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (L < mu || mu < 0.0) throw std::invalid_argument("Quadratic: need L >= mu >= 0");
+    // OptimizerConfig::validate (optimizer.hpp:195-202)
+    if (gamma <= 0.0) throw std::invalid_argument("OptimizerConfig: gamma > 0");
+    if (tau < 1) throw std::invalid_argument("OptimizerConfig: tau >= 1");
+    if (sigma < 0.0) throw std::invalid_argument("OptimizerConfig: sigma >= 0");
+    if (M < 1 || d < 1 || T < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    const std::uint64_t cap = moshpit_grid_capacity(M, d);
+    if (n_peers < 1 || n_peers > cap) throw std::invalid_argument("OptimizerConfig: 1 <= N <= M^d");
+    for (std::uint64_t e = 0; e < n_events; ++e)
+      if (ev_delta[e] < 0 && static_cast<std::uint32_t>(-ev_delta[e]) >= n_peers)
+        throw std::invalid_argument("run_moshpit_sgd: schedule kills everyone");
+    if (diag != MOSHPIT_DIAG_EXACT && diag != MOSHPIT_DIAG_FAST)
+      throw std::invalid_argument("run_moshpit_sgd: diagnostics must be EXACT or FAST");
+    if (noise_mode != 0 && noise_mode != 1)
+      throw std::invalid_argument("run_moshpit_sgd: noise_mode must be 0 or 1");
+    require_device();
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    const std::uint32_t inner = inner_rounds == 0 ? d : inner_rounds;
+    std::uint64_t n_max = n_peers;
+    for (std::uint64_t e = 0; e < n_events; ++e)
+      if (ev_delta[e] > 0) n_max += static_cast<std::uint64_t>(ev_delta[e]);
+    StreamHolder h;
+    SgdRun r{dtype, es, dim, padded_ld(dim, es), h.s};
+    const std::uint64_t D = dim ? dim : 1;
+    DeviceBuffer x(n_max * r.ld * es + 16), th0(D * 8);
+    r.c64.resize(D * 8);
+    r.t64.resize(D * 8);
+    r.cT.resize(D * es);
+    r.tT.resize(D * es);
+    r.flag.resize(16);
+    r.npart.resize((std::uint64_t)(steps + 1) * 148 * 16 * 8 + 16);
+    r.hat.resize(D * 8);
+    r.mean.resize(D * 8);
+    r.wsum.resize(D * 8);
+    const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+    r.vpart.resize((nch + 1) * 4 * 8 + 64);
+    r.dpart.resize(n_max * (nch + 1) * 8 + 16);
+    DeviceBuffer out((std::uint64_t)(steps + 1) * 8 * 8);
+    MB_CUDA(cudaMemsetAsync(r.flag.ptr, 0, 16, h.s));
+    MB_CUDA(cudaMemsetAsync(r.wsum.ptr, 0, D * 8, h.s));
+    MB_CUDA(cudaMemsetAsync(r.npart.ptr, 0, r.npart.bytes, h.s));
+    const auto c = quad_curvature(dim, L, mu);
+    MB_CUDA(cudaMemcpyAsync(r.c64.ptr, c.data(), dim * 8, cudaMemcpyHostToDevice, h.s));
+    MB_CUDA(cudaMemcpyAsync(r.t64.ptr, target, dim * 8, cudaMemcpyHostToDevice, h.s));
+    MB_CUDA(cudaMemcpyAsync(th0.ptr, theta0, dim * 8, cudaMemcpyHostToDevice, h.s));
+    const unsigned b = (unsigned)((D + 255) / 256);
+    if (dtype == MOSHPIT_F32) {
+      cast_kernel<float><<<b, 256, 0, h.s>>>(r.c64.as<double>(), r.cT.as<float>(), dim);
+      cast_kernel<float><<<b, 256, 0, h.s>>>(r.t64.as<double>(), r.tT.as<float>(), dim);
+      broadcast_theta0<float><<<grid_for(n_peers * D, 256), 256, 0, h.s>>>(
+          x.as<float>(), n_peers, r.ld, dim, th0.as<double>());
+    } else {
+      cast_kernel<double><<<b, 256, 0, h.s>>>(r.c64.as<double>(), r.cT.as<double>(), dim);
+      cast_kernel<double><<<b, 256, 0, h.s>>>(r.t64.as<double>(), r.tT.as<double>(), dim);
+      broadcast_theta0<double><<<grid_for(n_peers * D, 256), 256, 0, h.s>>>(
+          x.as<double>(), n_peers, r.ld, dim, th0.as<double>());
+    }
+    MB_LAUNCH_CHECK();
+
+    Xoshiro noise = Xoshiro::named(seed, "noise");
+    Xoshiro avg = Xoshiro::named(seed, "averaging");
+    Xoshiro join = Xoshiro::named(seed, "join");
+    std::unique_ptr<Plane> plane;
+    std::uint64_t n = n_peers;
+    std::uint32_t n_min = n_peers;
+    double noise_sq_sum = 0.0, weight_total = 0.0, w_k = 1.0;
+    std::uint64_t noise_count = 0;
+    const double w_growth = mu > 0.0 ? 1.0 / (1.0 - gamma * mu) : 1.0;
+    const double coord_std = sigma > 0.0 ? sigma / std::sqrt(static_cast<double>(dim)) : 0.0;
+    const int exact = diag == MOSHPIT_DIAG_EXACT;
+    std::vector<double> nz64;
+    std::vector<float> nz32;
+    PinnedBuffer nz_pin;
+    std::vector<double> wt_hist(steps);
+    for (std::uint32_t k = 0; k < steps; ++k) {
+      for (std::uint64_t e = 0; e < n_events; ++e) {  // optimizer.hpp:337-350
+        if (ev_step[e] != k) continue;
+        if (ev_delta[e] < 0) {
+          const std::uint64_t leave = static_cast<std::uint64_t>(-ev_delta[e]);
+          if (leave >= n) throw std::runtime_error("run_moshpit_sgd: all peers vanished");
+          n -= leave;
+        } else {
+          for (std::int32_t q = 0; q < ev_delta[e]; ++q) {
+            const std::uint64_t donor = join.below(n);
+            MB_CUDA(cudaMemcpyAsync(static_cast<char*>(x.ptr) + n * r.ld * es,
+                                    static_cast<char*>(x.ptr) + donor * r.ld * es, r.ld * es,
+                                    cudaMemcpyDeviceToDevice, h.s));
+            ++n;
+          }
+        }
+      }
+      n_min = std::min<std::uint32_t>(n_min, static_cast<std::uint32_t>(n));
+      // local step (optimizer.hpp:356-375)
+      const void* host_noise = nullptr;
+      if (coord_std > 0.0 && noise_mode == 0) {
+        nz_pin.resize(n * dim * es + 16);
+        MB_CUDA(cudaStreamSynchronize(h.s));  // the pinned buffer is reused per step
+        for (std::uint64_t i = 0; i < n * dim; ++i) {
+          const double nj = coord_std * noise.normal();
+          noise_sq_sum += nj * nj;
+          if (dtype == MOSHPIT_F32)
+            nz_pin.as<float>()[i] = static_cast<float>(nj);
+          else
+            nz_pin.as<double>()[i] = nj;
+        }
+        host_noise = nz_pin.ptr;
+      }
+      noise_count += n;
+      const int philox = (coord_std > 0.0 && noise_mode == 1) ? 1 : 0;
+      if (dtype == MOSHPIT_F32) {
+        r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                      static_cast<const float*>(host_noise));
+        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.hat.as<double>(),
+                                      h.s);
+      } else {
+        r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                       static_cast<const double*>(host_noise));
+        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
+                                       r.hat.as<double>(), h.s);
+      }
+      // averaging pass (optimizer.hpp:379-381, 249-284)
+      if ((k + 1) % tau == 0 && n > 1) {
+        if (n > cap) throw std::invalid_argument("moshpit_average: N exceeds grid capacity M^d");
+        if (!plane || plane->n != n) plane = std::make_unique<Plane>(M, d, n, dev);
+        plane->init_cells(avg, h.s);
+        for (std::uint32_t q = 0; q < inner; ++q)
+          plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
+      }
+      double* o = out.as<double>() + (std::uint64_t)k * 8;
+      if (dtype == MOSHPIT_F32)
+        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
+                                      h.s);
+      else
+        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
+                                       r.mean.as<double>(), h.s);
+      w_k *= w_growth;
+      weight_total += w_k;
+      wt_hist[k] = weight_total;
+      if (exact) {
+        sgd_vec_exact<<<1, 1, 0, h.s>>>(r.mean.as<double>(), r.hat.as<double>(),
+                                        r.c64.as<double>(), r.t64.as<double>(),
+                                        r.wsum.as<double>(), w_k, weight_total, dim, o);
+        if (dtype == MOSHPIT_F32)
+          dispersion_exact<float><<<1, 1, 0, h.s>>>(x.as<float>(), n, r.ld, dim,
+                                                    r.mean.as<double>(), o + 4);
+        else
+          dispersion_exact<double><<<1, 1, 0, h.s>>>(x.as<double>(), n, r.ld, dim,
+                                                     r.mean.as<double>(), o + 4);
+      } else {
+        const std::uint64_t ch = nch ? nch : 1;
+        sgd_vec_fast<<<(unsigned)ch, kRed, 0, h.s>>>(r.mean.as<double>(), r.hat.as<double>(),
+                                                    r.c64.as<double>(), r.t64.as<double>(),
+                                                    r.wsum.as<double>(), w_k, weight_total, dim,
+                                                    r.vpart.as<double>());
+        sgd_vec_fold<<<1, 1, 0, h.s>>>(r.vpart.as<double>(), ch, o);
+        if (dtype == MOSHPIT_F32)
+          dispersion_fast<float><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+              x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+        else
+          dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+              x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+        fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, o + 4);
+      }
+      MB_LAUNCH_CHECK();
+    }
+    std::vector<double> hout((std::uint64_t)steps * 8 + 8);
+    MB_CUDA(cudaMemcpyAsync(hout.data(), out.ptr, (std::uint64_t)steps * 64, cudaMemcpyDeviceToHost,
+                            h.s));
+    std::vector<double> hnp;
+    if (noise_mode == 1 && coord_std > 0.0) {
+      hnp.resize((std::uint64_t)steps * 148 * 16);
+      MB_CUDA(cudaMemcpyAsync(hnp.data(), r.npart.ptr, hnp.size() * 8, cudaMemcpyDeviceToHost, h.s));
+    }
+    if (final_mean)
+      MB_CUDA(cudaMemcpyAsync(final_mean, r.mean.ptr, dim * 8, cudaMemcpyDeviceToHost, h.s));
+    if (final_thetas)
+      MB_CUDA(cudaMemcpy2DAsync(final_thetas, dim * es, x.ptr, r.ld * es, dim * es, n,
+                                cudaMemcpyDeviceToHost, h.s));
+    MB_CUDA(cudaStreamSynchronize(h.s));
+    std::uint32_t bad = 0;
+    MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
+    if (bad) throw std::runtime_error("run_moshpit_sgd: non-finite gradient");
+    for (double v : hnp) noise_sq_sum += v;
+    double pv_max = 0.0;
+    for (std::uint32_t k = 0; k < steps; ++k) {
+      const double* o = hout.data() + (std::uint64_t)k * 8;
+      pv_max = std::max(pv_max, o[0]);
+      f_gap[k] = o[1] - 0.0;
+      grad_norm_sq[k] = o[2];
+      f_gap_weighted[k] = o[3] - 0.0;
+      dispersion[k] = o[4];
+    }
+    double v_sync_max = 0.0;
+    for (std::uint32_t k = tau - 1; k < steps; k += tau) v_sync_max = std::max(v_sync_max, dispersion[k]);
+    diag6[0] = std::sqrt(v_sync_max) / gamma;
+    diag6[1] = noise_count > 0 && sigma > 0.0
+                   ? std::sqrt(noise_sq_sum / static_cast<double>(noise_count))
+                   : 0.0;
+    diag6[2] = 0.0;
+    diag6[3] = std::sqrt(std::max(0.0, pv_max)) / gamma;
+    diag6[4] = n_min;
+    diag6[5] = static_cast<double>(n);
+  });
+}
+
+}  // extern "C"

@@ -120,6 +120,37 @@ def main():
     out["moshpit_average"].append(dict(M=4, d=3, rounds=3, seed=8, name="averaging", n=60, dim=2,
                                        out=hxa(r.moshpit_average(x, 4, 3, 3, 8))))
 
+    sgd = []
+    for (M, d, n, dim, L, mu, gamma, tau, K, sigma, sched, seed) in [
+            (4, 2, 9, 4, 5.0, 0.5, 0.05, 1, 60, 0.0, (), 500),
+            (4, 2, 12, 3, 10.0, 1.0, 0.02, 4, 40, 1.0, (), 8000),
+            (8, 2, 16, 2, 4.0, 1.0, 0.05, 1, 30, 1.0, (), 9000),
+            (4, 2, 8, 2, 2.0, 1.0, 0.1, 2, 20, 0.5, ((5, -3), (12, 2)), 777),
+            (32, 2, 1024, 8, 1.0, 0.1, 0.1, 1, 6, 1.0, (), 7)]:
+        tgt = r.stream_draws(seed, "objective", dim, "normal")
+        th0 = np.zeros(dim)
+        res = r.sgd_quadratic(M, d, n, dim, L, mu, tgt, th0, gamma, tau, K, sigma, seed,
+                              schedule=sched)
+        sgd.append(dict(M=M, d=d, n=n, dim=dim, L=L, mu=mu, gamma=gamma, tau=tau, steps=K,
+                        sigma=sigma, schedule=[list(e) for e in sched], seed=seed,
+                        target=hxa(tgt), f_gap=hxa(res["f_gap"]),
+                        grad_norm_sq=hxa(res["grad_norm_sq"]),
+                        f_gap_weighted=hxa(res["f_gap_weighted"]),
+                        dispersion=hxa(res["dispersion"]), final_mean=hxa(res["final_mean"]),
+                        delta_aq_hat=hx(res["delta_aq_hat"]), sigma_hat=hx(res["sigma_hat"]),
+                        delta_pv2_hat=hx(res["delta_pv2_hat"]), n_min=res["n_min"]))
+    out["sgd_quadratic"] = sgd
+    th = np.array([0.0, 0.0])
+    out["local_step"] = [dict(dim=2, L=2.0, mu=2.0, target=[1.0, 1.0], gamma=0.25, sigma=0.0,
+                              seed=23, name="n", theta=[0.0, 0.0],
+                              out=hxa(r.local_step_quadratic(th, 2.0, 2.0, [1.0, 1.0], 0.25, 0.0,
+                                                             23, "n"))),
+                         dict(dim=5, L=3.0, mu=0.5, target=[0.1, -0.2, 0.3, 0.4, -0.5], gamma=0.1,
+                              sigma=2.0, seed=4, name="noise", theta=[1.0, 2.0, 3.0, 4.0, 5.0],
+                              out=hxa(r.local_step_quadratic(np.arange(1.0, 6.0), 3.0, 0.5,
+                                                             [0.1, -0.2, 0.3, 0.4, -0.5], 0.1,
+                                                             2.0, 4, "noise")))]
+
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0, separators=(",", ":"))

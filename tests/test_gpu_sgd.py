@@ -1,0 +1,164 @@
+"""GPU Moshpit SGD (optimizer.hpp:231-242, 297-439, Quadratic objective).
+
+Bars: fp64 + reference noise stream + EXACT diagnostics -> bit-identical to
+the reference (golden vectors and oracle/_ref); fp32 -> bit-identical to the
+fp32 restatement; FAST diagnostics within 1e-12 relative; device (Philox)
+noise -> the reference's own statistical properties (test_optimizer.cpp)."""
+import numpy as np
+import pytest
+
+from tests._util import bits_equal, unhex, unhexa
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_device(mb):
+    if mb.device_count() == 0:
+        pytest.fail("no CUDA device visible")
+
+
+def _cfg(mb, c):
+    cfg = mb.OptimizerConfig(gamma=c["gamma"], tau=c["tau"], steps=c["steps"],
+                             grid=mb.GridConfig(c["M"], c["d"], 1), sigma=c["sigma"],
+                             n_peers=c["n"])
+    quad = mb.Quadratic(c["dim"], c["L"], c["mu"], unhexa(c["target"]))
+    sched = [mb.MembershipEvent(s, dd) for s, dd in c["schedule"]]
+    return cfg, quad, sched
+
+
+def test_sgd_f64_bit_exact_vs_golden(mb, golden):
+    for c in golden["sgd_quadratic"]:
+        cfg, quad, sched = _cfg(mb, c)
+        r = mb.run_moshpit_sgd(cfg, quad, np.zeros(c["dim"]), sched, mb.Rng(c["seed"]))
+        assert bits_equal(np.array(r.f_gap), unhexa(c["f_gap"])), c["seed"]
+        assert bits_equal(np.array(r.grad_norm_sq), unhexa(c["grad_norm_sq"]))
+        assert bits_equal(np.array(r.f_gap_weighted), unhexa(c["f_gap_weighted"]))
+        assert bits_equal(np.array(r.diagnostics.dispersion), unhexa(c["dispersion"]))
+        assert bits_equal(r.final_mean, unhexa(c["final_mean"]))
+        assert r.diagnostics.delta_aq_hat == unhex(c["delta_aq_hat"])
+        assert r.diagnostics.sigma_hat == unhex(c["sigma_hat"])
+        assert r.diagnostics.delta_pv2_hat == unhex(c["delta_pv2_hat"])
+        assert r.diagnostics.n_min == c["n_min"]
+
+
+def test_local_step_matches_golden(mb, golden):
+    for c in golden["local_step"]:
+        th = np.array(c["theta"], dtype=np.float64)
+        quad = mb.Quadratic(c["dim"], c["L"], c["mu"], c["target"])
+        s = mb.Rng(c["seed"]).stream(c["name"])
+        mb.local_step(th, quad, c["gamma"], c["sigma"], s)
+        assert bits_equal(th, unhexa(c["out"]))
+    # test_optimizer.cpp:60-69
+    th = np.zeros(2)
+    mb.local_step(th, mb.Quadratic(2, 2.0, 2.0, [1.0, 1.0]), 0.25, 0.0, mb.Rng(23).stream("n"))
+    assert th.tolist() == [0.5, 0.5]
+
+
+@pytest.mark.parametrize("sigma,tau,sched", [(0.0, 1, ()), (1.0, 3, ()),
+                                             (0.5, 2, ((5, -3), (12, 2)))])
+def test_sgd_f32_bit_exact_vs_oracle(mb, oracle, sigma, tau, sched):
+    dim, n = 37, 12
+    tgt = oracle.stream_draws(11, "objective", dim, "normal")
+    res = oracle.sgd_quadratic(4, 2, n, dim, 2.0, 0.5, tgt, np.zeros(dim), 0.05, tau, 20, sigma,
+                               99, schedule=sched, dtype=np.float32)
+    cfg = mb.OptimizerConfig(gamma=0.05, tau=tau, steps=20, grid=mb.GridConfig(4, 2, 1),
+                             sigma=sigma, n_peers=n)
+    r = mb.run_moshpit_sgd(cfg, mb.Quadratic(dim, 2.0, 0.5, tgt), np.zeros(dim),
+                           [mb.MembershipEvent(*e) for e in sched], mb.Rng(99), dtype=np.float32,
+                           return_thetas=True)
+    assert bits_equal(r.final_thetas, res["final_thetas"])
+    assert bits_equal(np.array(r.f_gap), res["f_gap"])
+    assert bits_equal(np.array(r.diagnostics.dispersion), res["dispersion"])
+    fast = mb.run_moshpit_sgd(cfg, mb.Quadratic(dim, 2.0, 0.5, tgt), np.zeros(dim),
+                              [mb.MembershipEvent(*e) for e in sched], mb.Rng(99),
+                              dtype=np.float32, diagnostics="fast")
+    np.testing.assert_allclose(fast.f_gap, res["f_gap"], rtol=1e-12)
+    np.testing.assert_allclose(fast.diagnostics.dispersion, res["dispersion"], rtol=1e-12,
+                               atol=1e-300)
+
+
+def test_sgd_validation_matches_reference(mb):
+    quad = mb.Quadratic(2, 2.0, 1.0, [1.0, 1.0])
+    cfg = mb.OptimizerConfig(gamma=0.1, tau=2, steps=20, grid=mb.GridConfig(4, 2, 1), sigma=0.5,
+                             n_peers=8)
+    r = mb.run_moshpit_sgd(cfg, quad, np.zeros(2), [mb.MembershipEvent(5, -3),
+                                                    mb.MembershipEvent(12, 2)], mb.Rng(777))
+    assert r.diagnostics.n_min == 5 and len(r.f_gap) == 20   # test_optimizer.cpp:160-176
+    with pytest.raises(ValueError):                            # :177-180
+        mb.run_moshpit_sgd(cfg, quad, np.zeros(2), [mb.MembershipEvent(3, -8)], mb.Rng(1))
+    with pytest.raises(ValueError):
+        mb.Quadratic(2, 1.0, 2.0, [0.0, 0.0])
+    bad = mb.OptimizerConfig(gamma=0.0, grid=mb.GridConfig(2, 2, 1), n_peers=4)
+    with pytest.raises(ValueError):
+        mb.run_moshpit_sgd(bad, quad, np.zeros(2), [], mb.Rng(1))
+    with pytest.raises(mb.ReferenceRuntimeError):  # non-finite gradient
+        huge = mb.Quadratic(2, 1e308, 1e308, [0.0, 0.0])
+        c2 = mb.OptimizerConfig(gamma=1e10, steps=3, grid=mb.GridConfig(2, 2, 1), n_peers=4)
+        mb.run_moshpit_sgd(c2, huge, np.full(2, 1e300), [], mb.Rng(1))
+
+
+def test_tau1_sigma0_equals_gradient_descent(mb):
+    # test_optimizer.cpp:71-98
+    s = mb.Rng(24).stream("target")
+    quad = mb.Quadratic(4, 5.0, 0.5, s.normals(4))
+    cfg = mb.OptimizerConfig(gamma=0.05, tau=1, steps=60, grid=mb.GridConfig(4, 2, 1),
+                             sigma=0.0, n_peers=9)
+    r = mb.run_moshpit_sgd(cfg, quad, np.full(4, 2.0), [], mb.Rng(500), noise="device")
+    c = np.array([0.5 + 4.5 * j / 3 for j in range(4)])
+    th = np.full(4, 2.0)
+    for k in range(60):
+        th = th - 0.05 * (c * (th - quad.target))
+        f = float(np.sum(0.5 * c * (th - quad.target) ** 2))
+        assert abs(r.f_gap[k] - f) <= 1e-12
+        assert r.diagnostics.dispersion[k] <= 1e-24
+    assert np.allclose(r.final_mean, th, atol=1e-12)
+
+
+def test_device_noise_statistics(mb):
+    """Philox noise: sigma_hat ~ sigma, and the reference's V_k bound
+    (test_optimizer.cpp:100-130) and N-doubling property (:132-158)."""
+    cfg = mb.OptimizerConfig(gamma=0.02, tau=4, steps=80, grid=mb.GridConfig(4, 2, 1), sigma=1.0,
+                             n_peers=12)
+    quad = mb.Quadratic(3, 10.0, 1.0, np.ones(3))
+    n_seeds = 60
+    mean_vk = np.zeros(80)
+    worst_aq, sigma_hat = 0.0, 0.0
+    for s in range(n_seeds):
+        r = mb.run_moshpit_sgd(cfg, quad, np.zeros(3), [], mb.Rng(8000 + s), noise="device",
+                               diagnostics="fast")
+        mean_vk += np.array(r.diagnostics.dispersion) / n_seeds
+        worst_aq = max(worst_aq, r.diagnostics.delta_aq_hat)
+        sigma_hat += r.diagnostics.sigma_hat / n_seeds
+    assert abs(sigma_hat - 1.0) < 0.1
+    bound = 2 * 0.02 ** 2 * (4 * worst_aq ** 2 + 3 * sigma_hat ** 2)
+    assert (mean_vk <= 1.5 * bound).all()
+
+    def steady(n_peers):
+        c = mb.OptimizerConfig(gamma=0.05, tau=1, steps=200, grid=mb.GridConfig(8, 2, 1),
+                               sigma=1.0, n_peers=n_peers)
+        q = mb.Quadratic(2, 4.0, 1.0, np.full(2, 0.5))
+        acc = 0.0
+        for s in range(30):
+            r = mb.run_moshpit_sgd(c, q, np.zeros(2), [], mb.Rng(9000 + s), noise="device",
+                                   diagnostics="fast")
+            acc += float(np.mean(r.f_gap[150:]))
+        return acc / 30
+    assert steady(16) < steady(8)
+
+
+@pytest.mark.slow
+def test_c4_shaped_run_device_noise(mb):
+    """C4: 1024 peers on 32x32, Quadratic(D=2^16, L=1, mu=0.1), gamma=0.1,
+    tau=1, sigma=1, device noise, FAST diagnostics: converges and stays
+    consistent (dispersion after exact 2-round averaging ~ fp rounding)."""
+    D = 1 << 16
+    s = mb.Rng(7).stream("objective")
+    quad = mb.Quadratic(D, 1.0, 0.1, s.normals(D))
+    cfg = mb.OptimizerConfig(gamma=0.1, tau=1, steps=20, grid=mb.GridConfig(32, 2, 1), sigma=1.0,
+                             n_peers=1024)
+    r = mb.run_moshpit_sgd(cfg, quad, np.zeros(D), [], mb.Rng(7), noise="device",
+                           diagnostics="fast", dtype=np.float32)
+    assert r.f_gap[-1] < 0.5 * r.f_gap[0]
+    assert max(r.diagnostics.dispersion) < 1e-9  # full grid, tau=1: exact average each step
+    assert abs(r.diagnostics.sigma_hat - 1.0) < 0.01

@@ -129,3 +129,32 @@ def test_oracle_trace_is_consistent(oracle):
         assert off[0] == 0 and off[-1] == 1024
         assert np.all(np.diff(off) == 32)  # full grid: every group exactly M
         assert sorted(t["members"][r].tolist()) == list(range(1024))
+
+
+def _sgd_case(c):
+    from tests._util import unhexa as U
+    return dict(M=c["M"], d=c["d"], n_peers=c["n"], dim=c["dim"], L=c["L"], mu=c["mu"],
+                target=U(c["target"]), theta0=np.zeros(c["dim"]), gamma=c["gamma"], tau=c["tau"],
+                steps=c["steps"], sigma=c["sigma"], seed=c["seed"],
+                schedule=[tuple(e) for e in c["schedule"]])
+
+
+def test_sgd_oracle_matches_golden(oracle, golden):
+    for c in golden["sgd_quadratic"]:
+        res = oracle.sgd_quadratic(**_sgd_case(c))
+        for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion", "final_mean"):
+            assert bits_equal(res[k], unhexa(c[k])), k
+        assert res["delta_aq_hat"] == unhex(c["delta_aq_hat"])
+        assert res["sigma_hat"] == unhex(c["sigma_hat"])
+        assert res["delta_pv2_hat"] == unhex(c["delta_pv2_hat"])
+        assert res["n_min"] == c["n_min"]
+
+
+def test_sgd_oracle_equals_reference_with_schedule(oracle, ref):
+    tgt = ref.stream_draws(24, "target", 3, "normal")
+    kw = dict(M=4, d=2, n_peers=12, dim=3, L=10.0, mu=1.0, target=tgt, theta0=np.zeros(3),
+              gamma=0.02, tau=3, steps=30, sigma=0.7, seed=31, schedule=((4, -5), (9, 6)))
+    a, b = oracle.sgd_quadratic(**kw), ref.sgd_quadratic(**kw)
+    for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion", "final_mean"):
+        assert bits_equal(a[k], b[k]), k
+    assert a["sigma_hat"] == b["sigma_hat"] and a["n_min"] == b["n_min"] == 7
