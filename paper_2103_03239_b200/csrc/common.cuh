@@ -246,16 +246,29 @@ void launch_initial_keys(const std::uint64_t* cells, std::uint64_t* keys,
                          std::uint64_t n, std::uint32_t M, std::uint32_t d,
                          cudaStream_t s);
 
-// Kernel 2: segmented group mean over the active groups.
-struct MeanPlan {
-  int grid = 0;
-  int variant = 0;
+// Kernel 3 prologue: the local SGD step (optimizer.hpp:356-373) applied to
+// each member vector as kernel 2 loads it (row index == peer id).
+template <typename T>
+struct StepPrologue {
+  const T* curv = nullptr;  // [ld] curvature (padded with zeros)
+  const T* tgt = nullptr;   // [ld] target
+  T gamma = 0;
+  double coord_std = 0.0;
+  int philox = 0;           // device noise (0: sigma == 0)
+  std::uint64_t seed = 0, step_no = 0, dim = 0;
+  std::uint32_t* nonfinite = nullptr;
+  double* noise_partial = nullptr;  // [gridDim] sum of nj^2 per CTA
 };
+
+// Kernel 2: segmented group mean over the active groups (with the kernel-3
+// step fused into the loads when `step` is non-null).
 template <typename T>
 void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
                        const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint32_t* act, const std::uint32_t* counts,
-                       std::uint32_t max_group, int variant, cudaStream_t s);
+                       std::uint32_t max_group, int variant, cudaStream_t s,
+                       const StepPrologue<T>* step = nullptr);
+int group_mean_grid_size(bool f64, bool step);
 
 // Diagnostics and helpers.
 template <typename T, typename Acc>

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace mb200 {
 namespace {
@@ -91,6 +92,7 @@ constexpr int kMaxSmemIds = 1024;
 
 template <typename T>
 struct MeanArgs {
+  StepPrologue<T> step;     // kernel 3: local SGD step fused into the loads
   T* state;
   std::uint64_t ld_vec;     // row stride in 16-byte vectors
   std::uint64_t nvec;       // vectors per row to process
@@ -101,21 +103,73 @@ struct MeanArgs {
   const std::uint32_t* counts;  // [1] = number of active groups
 };
 
-template <int N, typename V>
+// Kernel 3 prologue (optimizer.hpp:356-373): g = c*(theta-t) [+ nj]; the
+// non-finite check is on g; theta' = theta - gamma*g.  Same rounding and the
+// same Philox noise per (step, peer, coordinate) as the standalone step kernel
+// (sgd.cu), so fused == unfused bit for bit.
+__device__ __forceinline__ float sgd_grad(float x, float c, float t, double nj, bool noisy) {
+  float g = __fmul_rn(c, __fsub_rn(x, t));
+  return noisy ? __fadd_rn(g, (float)nj) : g;
+}
+__device__ __forceinline__ double sgd_grad(double x, double c, double t, double nj, bool noisy) {
+  double g = __dmul_rn(c, __dsub_rn(x, t));
+  return noisy ? __dadd_rn(g, nj) : g;
+}
+__device__ __forceinline__ float sgd_update(float x, float gm, float g) {
+  return __fsub_rn(x, __fmul_rn(gm, g));
+}
+__device__ __forceinline__ double sgd_update(double x, double gm, double g) {
+  return __dsub_rn(x, __dmul_rn(gm, g));
+}
+
+template <typename T, typename V>
+__device__ __forceinline__ V apply_step(const StepPrologue<T>& sp, V v, std::uint32_t peer,
+                                        std::uint64_t col, double& nsq, bool& bad) {
+  constexpr int kV = sizeof(V) / sizeof(T);
+  const V c = reinterpret_cast<const V*>(sp.curv)[col];
+  const V t = reinterpret_cast<const V*>(sp.tgt)[col];
+  T* pv = reinterpret_cast<T*>(&v);
+  const T* pc = reinterpret_cast<const T*>(&c);
+  const T* pt = reinterpret_cast<const T*>(&t);
+  const std::uint64_t j0 = col * kV;
+  double z[4] = {0, 0, 0, 0};
+  const bool noisy = sp.philox != 0;
+  if (noisy) philox_normals4(sp.seed, sp.step_no, peer, j0 / 4, z);
+#pragma unroll
+  for (int u = 0; u < kV; ++u) {
+    const std::uint64_t j = j0 + u;
+    if (j >= sp.dim) break;
+    const double nj = noisy ? sp.coord_std * z[j % 4] : 0.0;
+    if (noisy) nsq += nj * nj;
+    const T g = sgd_grad(pv[u], pc[u], pt[u], nj, noisy);
+    bad |= !isfinite((double)g);
+    pv[u] = sgd_update(pv[u], sp.gamma, g);
+  }
+  return v;
+}
+
+template <int N, bool STEP, typename T, typename V>
 __device__ __forceinline__ void mean_fixed(V* base, std::uint64_t ld_vec,
                                            std::uint64_t col,
-                                           const std::uint32_t* ids) {
+                                           const std::uint32_t* ids,
+                                           const StepPrologue<T>& sp, double& nsq, bool& bad) {
   V x[32];
 #pragma unroll
   for (int k = 0; k < N; ++k) x[k] = vload(base + (std::uint64_t)ids[k] * ld_vec + col);
+  if constexpr (STEP) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = apply_step(sp, x[k], ids[k], col, nsq, bad);
+  }
   const V m = vdiv(tree<N, 0>(x), (std::uint32_t)N);
 #pragma unroll
   for (int k = 0; k < N; ++k) vstore(base + (std::uint64_t)ids[k] * ld_vec + col, m);
 }
 
-template <typename T>
+template <typename T, bool STEP>
 __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a) {
   using V = typename V16<T>::type;
+  double nsq = 0.0;
+  bool bad = false;
   __shared__ std::uint32_t sids[kMaxSmemIds];
   const std::uint32_t n_act = a.counts[1];
   const std::uint64_t n_items = (std::uint64_t)n_act * a.n_tiles;
@@ -138,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
     switch (cnt) {
 #define MB_CASE(N) \
   case N:          \
-    mean_fixed<N, V>(base, a.ld_vec, col, sids); \
+    mean_fixed<N, STEP, T, V>(base, a.ld_vec, col, sids, a.step, nsq, bad); \
     break;
       MB_CASE(1) MB_CASE(2) MB_CASE(3) MB_CASE(4) MB_CASE(5) MB_CASE(6) MB_CASE(7)
       MB_CASE(8) MB_CASE(9) MB_CASE(10) MB_CASE(11) MB_CASE(12) MB_CASE(13)
@@ -150,7 +204,9 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
       default: {
         const std::uint32_t* ids = cnt <= kMaxSmemIds ? sids : a.members + beg;
         auto ld = [&](std::uint32_t k) {
-          return vload(base + (std::uint64_t)ids[k] * a.ld_vec + col);
+          V v = vload(base + (std::uint64_t)ids[k] * a.ld_vec + col);
+          if constexpr (STEP) v = apply_step(a.step, v, ids[k], col, nsq, bad);
+          return v;
         };
         const V m = vdiv(pairwise_rt<V>(ld, cnt, [](V x, V y) { return vadd(x, y); },
                                            vzero((V*)nullptr)), cnt);
@@ -158,6 +214,17 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
           vstore(base + (std::uint64_t)ids[k] * a.ld_vec + col, m);
       }
     }
+  }
+  if constexpr (STEP) {
+    __shared__ double red[kThreads];
+    red[threadIdx.x] = nsq;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && a.step.noise_partial) a.step.noise_partial[blockIdx.x] = red[0];
+    if (bad) atomicOr(a.step.nonfinite, 1u);
   }
 }
 
@@ -326,24 +393,24 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
 struct GridCache {
   int dev = -1;
-  int grid[2] = {0, 0};
+  int grid[4] = {0, 0, 0, 0};
 };
 
-template <typename T>
+template <typename T, bool STEP>
 int mean_grid() {
   static thread_local GridCache cache;
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
-  const int slot = sizeof(T) == 4 ? 0 : 1;
+  const int slot = (sizeof(T) == 4 ? 0 : 1) + (STEP ? 2 : 0);
   if (cache.dev != dev) {
     cache.dev = dev;
-    cache.grid[0] = cache.grid[1] = 0;
+    cache.grid[0] = cache.grid[1] = cache.grid[2] = cache.grid[3] = 0;
   }
   if (!cache.grid[slot]) {
     int sms = 0, per = 0;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per, group_mean_register<T>, kThreads, 0));
+        &per, group_mean_register<T, STEP>, kThreads, 0));
     cache.grid[slot] = sms * (per > 0 ? per : 1);
   }
   return cache.grid[slot];
@@ -363,7 +430,8 @@ template <typename T>
 void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
                        const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint32_t* act, const std::uint32_t* counts,
-                       std::uint32_t max_group, int variant, cudaStream_t s) {
+                       std::uint32_t max_group, int variant, cudaStream_t s,
+                       const StepPrologue<T>* step) {
   if (dim == 0) return;
   constexpr int kVec = V16<T>::kN;
   MeanArgs<T> a;
@@ -375,6 +443,12 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
   a.goff = goff;
   a.act = act;
   a.counts = counts;
+  if (step) {
+    a.step = *step;
+    group_mean_register<T, true><<<mean_grid<T, true>(), kThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+    return;
+  }
   const bool bulk_ok = max_group <= (std::uint32_t)kBulkMaxRows;
   if (variant == 2 || (variant == 0 && bulk_ok && bulk_default())) {
     if (!bulk_ok) throw std::invalid_argument("bulk kernel: groups larger than 32 members");
@@ -399,7 +473,7 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     a.n_tiles = (a.nvec + kBulkTileVec - 1) / kBulkTileVec;
     group_mean_bulk<T><<<sms, kBulkThreads, smem, s>>>(a, stages, (int)srows);
   } else {
-    group_mean_register<T><<<mean_grid<T>(), kThreads, 0, s>>>(a);
+    group_mean_register<T, false><<<mean_grid<T, false>(), kThreads, 0, s>>>(a);
   }
   MB_LAUNCH_CHECK();
 }
@@ -407,10 +481,17 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
 template void launch_group_mean<float>(float*, std::uint64_t, std::uint64_t,
                                        const std::uint32_t*, const std::uint32_t*,
                                        const std::uint32_t*, const std::uint32_t*,
-                                       std::uint32_t, int, cudaStream_t);
+                                       std::uint32_t, int, cudaStream_t,
+                                       const StepPrologue<float>*);
 template void launch_group_mean<double>(double*, std::uint64_t, std::uint64_t,
                                         const std::uint32_t*, const std::uint32_t*,
                                         const std::uint32_t*, const std::uint32_t*,
-                                        std::uint32_t, int, cudaStream_t);
+                                        std::uint32_t, int, cudaStream_t,
+                                        const StepPrologue<double>*);
+
+int group_mean_grid_size(bool f64, bool step) {
+  if (f64) return step ? mean_grid<double, true>() : mean_grid<double, false>();
+  return step ? mean_grid<float, true>() : mean_grid<float, false>();
+}
 
 }  // namespace mb200

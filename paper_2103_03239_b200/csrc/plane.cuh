@@ -175,7 +175,9 @@ struct Plane {
   // group mean (kernel 2).  fail == nullptr or p <= 0: no failure draws.
   std::uint32_t round(Xoshiro* fail, double p, Xoshiro& clock, int dtype,
                       void* state, std::uint64_t dim, std::uint64_t ld,
-                      cudaStream_t s, int variant) {
+                      cudaStream_t s, int variant,
+                      const StepPrologue<float>* step_f = nullptr,
+                      const StepPrologue<double>* step_d = nullptr) {
     const int k = next_slot();
     auto* ts = stage[k].as<std::uint64_t>();
     auto* failed = reinterpret_cast<std::uint8_t*>(ts + n);
@@ -218,10 +220,10 @@ struct Plane {
       }
       if (dtype == MOSHPIT_F32)
         launch_group_mean<float>(static_cast<float*>(state), ld, dim, a.members, a.goff,
-                                 a.act, a.counts, grid.M, variant, s);
+                                 a.act, a.counts, grid.M, variant, s, step_f);
       else
         launch_group_mean<double>(static_cast<double*>(state), ld, dim, a.members, a.goff,
-                                  a.act, a.counts, grid.M, variant, s);
+                                  a.act, a.counts, grid.M, variant, s, step_d);
       if (timing) MB_CUDA(cudaEventRecord(te.second, s));
     }
     last_active = active;

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <memory>
 
+#include "philox.cuh"
 #include "plane.cuh"
 
 namespace mb200 {
@@ -35,30 +36,6 @@ struct SOps<double> {
   __device__ static double add(double a, double b) { return __dadd_rn(a, b); }
 };
 
-// Philox4x32-10 (Salmon et al. 2011), counter = (step, peer, j/4, 0).
-__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const std::uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
-}
-
-__device__ __forceinline__ void box_muller(std::uint32_t a, std::uint32_t b, double& z0,
-                                           double& z1) {
-  const double u1 = ((double)a + 1.0) * 0x1.0p-32;  // (0, 1]
-  const double u2 = (double)b * 0x1.0p-32;
-  const double r = sqrt(-2.0 * log(u1));
-  double s, c;
-  sincospi(2.0 * u2, &s, &c);
-  z0 = r * c;
-  z1 = r * s;
-}
-
 constexpr int kStepThreads = 256;
 
 // theta <- theta - gamma * (c * (theta - t) + nj)   (optimizer.hpp:356-373)
@@ -78,13 +55,7 @@ __global__ void __launch_bounds__(kStepThreads)
        e += (std::uint64_t)gridDim.x * blockDim.x) {
     const std::uint64_t i = e / quads, q = e % quads;
     double z[4] = {0, 0, 0, 0};
-    if (philox_mode) {
-      const uint4 r = philox(make_uint4((std::uint32_t)step, (std::uint32_t)i, (std::uint32_t)q,
-                                        (std::uint32_t)(q >> 32)),
-                             make_uint2((std::uint32_t)seed, (std::uint32_t)(seed >> 32)));
-      box_muller(r.x, r.y, z[0], z[1]);
-      box_muller(r.z, r.w, z[2], z[3]);
-    }
+    if (philox_mode) philox_normals4(seed, step, i, q, z);
     for (int u = 0; u < 4; ++u) {
       const std::uint64_t j = q * 4 + u;
       if (j >= dim) break;
@@ -380,8 +351,8 @@ int moshpit_run_moshpit_sgd_quadratic(
     for (std::uint64_t e = 0; e < n_events; ++e)
       if (ev_delta[e] < 0 && static_cast<std::uint32_t>(-ev_delta[e]) >= n_peers)
         throw std::invalid_argument("run_moshpit_sgd: schedule kills everyone");
-    if (diag != MOSHPIT_DIAG_EXACT && diag != MOSHPIT_DIAG_FAST)
-      throw std::invalid_argument("run_moshpit_sgd: diagnostics must be EXACT or FAST");
+    if (diag < MOSHPIT_DIAG_NONE || diag > MOSHPIT_DIAG_EXACT)
+      throw std::invalid_argument("run_moshpit_sgd: unknown diagnostics mode");
     if (noise_mode != 0 && noise_mode != 1)
       throw std::invalid_argument("run_moshpit_sgd: noise_mode must be 0 or 1");
     require_device();
@@ -440,6 +411,18 @@ int moshpit_run_moshpit_sgd_quadratic(
     const double w_growth = mu > 0.0 ? 1.0 / (1.0 - gamma * mu) : 1.0;
     const double coord_std = sigma > 0.0 ? sigma / std::sqrt(static_cast<double>(dim)) : 0.0;
     const int exact = diag == MOSHPIT_DIAG_EXACT;
+    // DIAG_NONE: kernel 3 -- the local step rides in the first averaging
+    // round's loads (one read + one write of the state for step + round 1).
+    const bool fused = diag == MOSHPIT_DIAG_NONE && !(coord_std > 0.0 && noise_mode == 0);
+    DeviceBuffer cpad, tpad;
+    if (fused) {  // curvature / target padded to the row stride (zeros)
+      cpad.resize(r.ld * es + 16);
+      tpad.resize(r.ld * es + 16);
+      MB_CUDA(cudaMemsetAsync(cpad.ptr, 0, r.ld * es, h.s));
+      MB_CUDA(cudaMemsetAsync(tpad.ptr, 0, r.ld * es, h.s));
+      MB_CUDA(cudaMemcpyAsync(cpad.ptr, r.cT.ptr, dim * es, cudaMemcpyDeviceToDevice, h.s));
+      MB_CUDA(cudaMemcpyAsync(tpad.ptr, r.tT.ptr, dim * es, cudaMemcpyDeviceToDevice, h.s));
+    }
     std::vector<double> nz64;
     std::vector<float> nz32;
     PinnedBuffer nz_pin;
@@ -479,6 +462,34 @@ int moshpit_run_moshpit_sgd_quadratic(
       }
       noise_count += n;
       const int philox = (coord_std > 0.0 && noise_mode == 1) ? 1 : 0;
+      const bool sync = (k + 1) % tau == 0 && n > 1;
+      if (fused) {
+        if (sync) {
+          if (n > cap) throw std::invalid_argument("moshpit_average: N exceeds grid capacity M^d");
+          if (!plane || plane->n != n) plane = std::make_unique<Plane>(M, d, n, dev);
+          plane->init_cells(avg, h.s);
+          StepPrologue<float> sf;
+          StepPrologue<double> sd;
+          double* np_slot = r.npart.as<double>() + (std::uint64_t)k * 148 * 16;
+          if (dtype == MOSHPIT_F32) {
+            sf = StepPrologue<float>{cpad.as<float>(), tpad.as<float>(), (float)gamma, coord_std,
+                                     philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
+            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO, &sf);
+          } else {
+            sd = StepPrologue<double>{cpad.as<double>(), tpad.as<double>(), gamma, coord_std,
+                                      philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
+            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO,
+                         nullptr, &sd);
+          }
+          for (std::uint32_t q = 1; q < inner; ++q)
+            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
+        } else if (dtype == MOSHPIT_F32) {
+          r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k, nullptr);
+        } else {
+          r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k, nullptr);
+        }
+        continue;
+      }
       if (dtype == MOSHPIT_F32) {
         r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
                       static_cast<const float*>(host_noise));
@@ -535,6 +546,18 @@ int moshpit_run_moshpit_sgd_quadratic(
       }
       MB_LAUNCH_CHECK();
     }
+    if (fused) {
+      if (dtype == MOSHPIT_F32)
+        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
+                                      h.s);
+      else
+        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
+                                       r.mean.as<double>(), h.s);
+      const double nan = std::nan("");
+      std::vector<double> fill((std::uint64_t)steps * 8 + 8, nan);
+      MB_CUDA(cudaMemcpyAsync(out.ptr, fill.data(), (std::uint64_t)steps * 64,
+                              cudaMemcpyHostToDevice, h.s));
+    }
     std::vector<double> hout((std::uint64_t)steps * 8 + 8);
     MB_CUDA(cudaMemcpyAsync(hout.data(), out.ptr, (std::uint64_t)steps * 64, cudaMemcpyDeviceToHost,
                             h.s));
@@ -553,8 +576,8 @@ int moshpit_run_moshpit_sgd_quadratic(
     MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
     if (bad) throw std::runtime_error("run_moshpit_sgd: non-finite gradient");
     for (double v : hnp) noise_sq_sum += v;
-    double pv_max = 0.0;
-    for (std::uint32_t k = 0; k < steps; ++k) {
+    double pv_max = fused ? std::nan("") : 0.0;
+    for (std::uint32_t k = 0; k < steps && !fused; ++k) {
       const double* o = hout.data() + (std::uint64_t)k * 8;
       pv_max = std::max(pv_max, o[0]);
       f_gap[k] = o[1] - 0.0;
@@ -562,8 +585,12 @@ int moshpit_run_moshpit_sgd_quadratic(
       f_gap_weighted[k] = o[3] - 0.0;
       dispersion[k] = o[4];
     }
-    double v_sync_max = 0.0;
-    for (std::uint32_t k = tau - 1; k < steps; k += tau) v_sync_max = std::max(v_sync_max, dispersion[k]);
+    if (fused)
+      for (std::uint32_t k = 0; k < steps; ++k)
+        f_gap[k] = grad_norm_sq[k] = f_gap_weighted[k] = dispersion[k] = std::nan("");
+    double v_sync_max = fused ? std::nan("") : 0.0;
+    for (std::uint32_t k = tau - 1; k < steps && !fused; k += tau)
+      v_sync_max = std::max(v_sync_max, dispersion[k]);
     diag6[0] = std::sqrt(v_sync_max) / gamma;
     diag6[1] = noise_count > 0 && sigma > 0.0
                    ? std::sqrt(noise_sq_sum / static_cast<double>(noise_count))

@@ -162,3 +162,26 @@ def test_c4_shaped_run_device_noise(mb):
     assert r.f_gap[-1] < 0.5 * r.f_gap[0]
     assert max(r.diagnostics.dispersion) < 1e-9  # full grid, tau=1: exact average each step
     assert abs(r.diagnostics.sigma_hat - 1.0) < 0.01
+
+
+@pytest.mark.parametrize("f64", [False, True])
+@pytest.mark.parametrize("sigma,tau,M,d,n", [(0.0, 1, 4, 2, 16), (1.0, 1, 8, 2, 64),
+                                             (0.7, 3, 4, 3, 50), (1.0, 1, 40, 2, 1600)])
+def test_fused_kernel3_equals_unfused(mb, f64, sigma, tau, M, d, n):
+    """Kernel 3 (local step fused into averaging round 1) == step kernel +
+    averaging, bit for bit, with the same device noise."""
+    dim = 45
+    tgt = mb.Rng(3).stream("objective").normals(dim)
+    cfg = mb.OptimizerConfig(gamma=0.05, tau=tau, steps=12, grid=mb.GridConfig(M, d, 1),
+                             sigma=sigma, n_peers=n)
+    quad = mb.Quadratic(dim, 2.0, 0.2, tgt)
+    dt = np.float64 if f64 else np.float32
+    a = mb.run_moshpit_sgd(cfg, quad, np.zeros(dim), [], mb.Rng(5), dtype=dt, noise="device",
+                           diagnostics="none", return_thetas=True)
+    b = mb.run_moshpit_sgd(cfg, quad, np.zeros(dim), [], mb.Rng(5), dtype=dt, noise="device",
+                           diagnostics="fast", return_thetas=True)
+    assert bits_equal(a.final_thetas, b.final_thetas)
+    assert bits_equal(a.final_mean, b.final_mean)
+    assert np.isnan(a.f_gap).all()
+    if sigma > 0:
+        assert abs(a.diagnostics.sigma_hat - b.diagnostics.sigma_hat) <= 1e-9 * b.diagnostics.sigma_hat
