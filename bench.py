@@ -319,6 +319,12 @@ def run_mine(args):
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(mb, cfg)
+    sgd = None
+    if rank == 0 and world == 1 and not args.no_sgd:
+        try:
+            sgd = measure_sgd_c4(mb)
+        except Exception as exc:  # noqa: BLE001
+            sgd = {"error": str(exc)}
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         try:
@@ -358,6 +364,7 @@ def run_mine(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "peer_sharded": peer,
+            "sgd_c4": sgd,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -442,6 +449,35 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     }
 
 
+def measure_sgd_c4(mb, steps=20, sigma=1.0):
+    """C4 (configs[3]): Moshpit SGD, 1024 peers on 32x32, Quadratic(D=2^20,
+    L=1, mu=0.1, target ~ N(0,1)), gamma=0.1, tau=1, inner=d=2, fp32,
+    device Philox noise, kernel 3 (local step fused into averaging round 1).
+    Device time of the step loop (CUDA events inside the C ABI call)."""
+    import numpy as np
+    D, N = 1 << 20, 1024
+    tgt = mb.Rng(PROTOCOL_SEED).stream("objective").normals(D)
+    quad = mb.Quadratic(D, 1.0, 0.1, tgt)
+    cfg = mb.OptimizerConfig(gamma=0.1, tau=1, steps=steps, grid=mb.GridConfig(32, 2, 1),
+                             sigma=sigma, n_peers=N)
+    best = None
+    for _ in range(2):
+        r = mb.run_moshpit_sgd(cfg, quad, np.zeros(D), [], mb.Rng(PROTOCOL_SEED),
+                               dtype=np.float32, diagnostics="none", noise="device")
+        best = r.loop_ms if best is None else min(best, r.loop_ms)
+    ms = best / steps
+    alg = 2 * 2 * N * D * 4  # two averaging rounds, each one read + one write of the state
+    peak, _ = peaks()
+    return {"workload": f"C4: Moshpit SGD, 1024 peers on 32x32, Quadratic D=2^20, tau=1, "
+                        f"inner=2, sigma={sigma} (device noise), fp32, kernel 3 fused step",
+            "ms_per_sgd_step": round(ms, 4),
+            "peer_vector_gbs": round(N * D * 4 / (ms / 1e3) / 1e9, 1),
+            "algorithmic_bytes_per_step": alg,
+            "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+            "timing": f"CUDA events around the {steps}-step loop (best of 2), incl. host draws",
+            "final_sigma_hat": round(r.diagnostics.sigma_hat, 6)}
+
+
 def measure_e2e(mb, cfg):
     """The reference-facing call (run_moshpit through the C ABI) with HOST
     buffers: H2D of the initial state, R rounds + TrialReport diagnostics,
@@ -473,10 +509,20 @@ def measure_e2e(mb, cfg):
                                         act.ctypes.data_as(C.c_void_p), C.byref(cost), ptr))
     t = time.perf_counter() - t0
     bytes_ = N * D * 4
+    # PCIe reference point: one plain pinned H2D copy of the same state
+    dev = torch.empty((N, D), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    dev.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_gbs = bytes_ / (time.perf_counter() - t1) / 1e9
+    del dev
     return {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
             "call": f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, pinned",
-            "seconds": round(t, 4), "final_distortion": float(dist_[-1])}
+            "seconds": round(t, 4), "final_distortion": float(dist_[-1]),
+            "pipeline": "D-slabs of 256 MB: H2D(s+1) || 10 rounds + diagnostics(s) || D2H(s-1)",
+            "pcie_h2d_gbs_plain_copy": round(h2d_gbs, 1)}
 
 
 def main():
@@ -489,6 +535,7 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sgd", action="store_true", help="skip the C4 Moshpit-SGD measurement")
     ap.add_argument("--no-peer", action="store_true",
                     help="skip the peer-sharded (NVLink) measurement attached at N>1")
     ap.add_argument("--mode", default="coord", choices=["coord", "peer"],

@@ -150,7 +150,9 @@ int moshpit_local_step_quadratic(int dtype, void* theta, uint64_t dim, double L,
  * 1: device Philox4x32-10 normals (statistical parity, the fast path).
  * Outputs: f_gap, grad_norm_sq, f_gap_weighted, dispersion [steps];
  * final_mean [dim]; diag6 = {delta_aq_hat, sigma_hat, delta_pv1_hat,
- * delta_pv2_hat, n_min, n_final}; final_thetas (nullable, n_final*dim). */
+ * delta_pv2_hat, n_min, n_final}; final_thetas (nullable, n_final*dim).
+ * MOSHPIT_DIAG_NONE runs kernel 3 (the step fused into averaging round 1)
+ * and reports NaN diagnostics. */
 int moshpit_run_moshpit_sgd_quadratic(
     int dtype, uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers,
     uint64_t dim, double L, double mu, const double* target,
@@ -158,7 +160,10 @@ int moshpit_run_moshpit_sgd_quadratic(
     double sigma, uint32_t inner_rounds, uint64_t seed, const uint32_t* ev_step,
     const int32_t* ev_delta, uint64_t n_events, int diag, int noise_mode,
     double* f_gap, double* grad_norm_sq, double* f_gap_weighted,
-    double* dispersion, double* final_mean, double* diag6, void* final_thetas);
+    double* dispersion, double* final_mean, double* diag6, void* final_thetas,
+    double* loop_ms);
+/* loop_ms (nullable): device time of the step loop (CUDA events on the call's
+ * stream; excludes setup and the final copies). */
 
 /* ---- device-resident engine (the performance boundary) -----------------
  * One engine = one trial's integer plane (grid, keys, rng streams, group

@@ -452,6 +452,7 @@ class SgdResult:
     final_mean: Optional[np.ndarray] = None
     diagnostics: AssumptionDiagnostics = field(default_factory=AssumptionDiagnostics)
     final_thetas: Optional[np.ndarray] = None  # extension
+    loop_ms: float = 0.0  # extension: device time of the step loop
 
 
 def local_step(theta: np.ndarray, objective: Quadratic, gamma: float, sigma: float,
@@ -485,19 +486,21 @@ def run_moshpit_sgd(config: OptimizerConfig, objective: Quadratic, theta0,
     evd = np.array([e.delta for e in schedule], dtype=np.int32)
     n_max = config.n_peers + sum(max(e.delta, 0) for e in schedule)
     fin = np.zeros((n_max, max(dim, 1)), dtype=dtype) if return_thetas else None
+    loop_ms = C.c_double(0.0)
     check(lib().moshpit_run_moshpit_sgd_quadratic(
         _dtype_code(dtype), config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
         config.n_peers, dim, objective.l, objective.mu, _p(objective.target), _p(th0),
         config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds, rng.seed(),
         _p(evs) if len(evs) else None, _p(evd) if len(evd) else None, len(evs),
         _DIAG[diagnostics], {"reference": 0, "device": 1}[noise], _p(out["f_gap"]),
-        _p(out["g"]), _p(out["fw"]), _p(out["disp"]), _p(fm), _p(d6), _p(fin)))
+        _p(out["g"]), _p(out["fw"]), _p(out["disp"]), _p(fm), _p(d6), _p(fin),
+        C.byref(loop_ms)))
     n_fin = int(d6[5])
     diag = AssumptionDiagnostics(list(out["disp"][:config.steps]), d6[0], d6[1], d6[2], d6[3],
                                  int(d6[4]))
     return SgdResult(list(out["f_gap"][:config.steps]), list(out["g"][:config.steps]),
                      list(out["fw"][:config.steps]), fm[:dim], diag,
-                     None if fin is None else fin[:n_fin, :dim])
+                     None if fin is None else fin[:n_fin, :dim], loop_ms.value)
 
 
 # ---------------------------------------------------------------------------

@@ -75,7 +75,7 @@ PROTOTYPES = {
     "moshpit_run_moshpit_sgd_quadratic": (C.c_int, [C.c_int, u32, u32, u32, u32, u64, dbl, dbl,
                                                     vp, vp, dbl, u32, u32, dbl, u32, u64, vp, vp,
                                                     u64, C.c_int, C.c_int, vp, vp, vp, vp, vp,
-                                                    vp, vp]),
+                                                    vp, vp, P(dbl)]),
     "moshpit_engine_create": (C.c_int, [u32, u32, u64, dbl, u64, C.c_int, P(vp)]),
     "moshpit_engine_destroy": (C.c_int, [vp]),
     "moshpit_engine_set_kernel": (C.c_int, [vp, C.c_int]),

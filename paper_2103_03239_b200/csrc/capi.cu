@@ -398,6 +398,23 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     require_device();
     int dev = 0;
     MB_CUDA(cudaGetDevice(&dev));
+    // Large states stream through the GPU in D-slabs (stream_run.cu): H2D,
+    // rounds and D2H overlap; results are identical to the resident path.
+    const std::uint64_t W = stream_slab_cols(n, es, dim);
+    if (dim > W) {
+      if (dtype == MOSHPIT_F32)
+        run_moshpit_streamed<float>(M, d, static_cast<const float*>(initial), n, dim, p_round,
+                                    seed, rounds, diag, initial_distortion, distortion,
+                                    mean_drift, active_counts, static_cast<float*>(final_out), W);
+      else
+        run_moshpit_streamed<double>(M, d, static_cast<const double*>(initial), n, dim, p_round,
+                                     seed, rounds, diag, initial_distortion, distortion,
+                                     mean_drift, active_counts, static_cast<double*>(final_out),
+                                     W);
+      *cost_units = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
+                                                static_cast<std::uint32_t>(dim));
+      return;
+    }
     StreamHolder st;
     const std::uint64_t ld = padded_ld(dim, es);
     DeviceBuffer d_x(n * ld * es), d_ref(dim * 8 + 16), d_mean(dim * 8 + 16), d_sq(n * 8),

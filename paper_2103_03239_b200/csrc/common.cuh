@@ -284,6 +284,19 @@ void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
                   double* partial_scratch, double* out, int exact,
                   cudaStream_t s);
 std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim);
+std::uint64_t diag_chunk();
+// Slab-streamed diagnostics: j-sums that continue across D-slabs (EXACT:
+// per-peer / scalar running accumulators; FAST: chunk partials at global
+// chunk offset c0), then one finishing pass.
+template <typename T>
+void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                      const double* ref, int exact, double* acc, double* partial,
+                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s);
+void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim, int exact,
+                       double* acc2, double* partial, std::uint64_t c0, cudaStream_t s);
+void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, double* acc,
+                        double* row_partial, double* acc2, double* drift_partial,
+                        double* dist_out, double* drift_out, cudaStream_t s);
 template <typename T>
 void launch_fill_synthetic(T* x, std::uint64_t n, std::uint64_t dim,
                            std::uint64_t ld, std::uint64_t seed,

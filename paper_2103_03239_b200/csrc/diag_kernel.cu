@@ -194,6 +194,84 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
     dst[(e / dim) * ld + e % dim] = row[e % dim];
 }
 
+// ---- slab-streamed variants: the j-sums continue across D-slabs --------
+template <typename T>
+__global__ void dist_rows_exact_acc(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                                    std::uint64_t dim, const double* __restrict__ ref,
+                                    double* __restrict__ acc) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const T* row = x + i * ld;
+  double a = acc[i];
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double diff = __dsub_rn((double)row[j], ref[j]);
+    a = __dadd_rn(a, __dmul_rn(diff, diff));
+  }
+  acc[i] = a;
+}
+
+template <typename T>
+__global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                                   const double* __restrict__ ref, std::uint64_t nch_total,
+                                   std::uint64_t c0, double* __restrict__ partial) {
+  const std::uint64_t c = blockIdx.x, i = blockIdx.y;
+  const T* row = x + i * ld;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double acc = 0.0;
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
+    const double diff = __dsub_rn((double)row[j], ref[j]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  const double s = block_sum_fixed(acc);
+  if (threadIdx.x == 0) partial[i * nch_total + c0 + c] = s;
+}
+
+__global__ void finish_distortion_from_acc(const double* __restrict__ acc, std::uint64_t n,
+                                           double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto ld_fn = [&](std::uint32_t i) { return acc[i]; };
+  const double s = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
+                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
+  *out = __ddiv_rn(s, (double)n);
+}
+
+__global__ void drift_exact_acc(const double* __restrict__ mean, const double* __restrict__ ref,
+                                std::uint64_t dim, double* __restrict__ acc2) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double drift_sq = acc2[0], ref_sq = acc2[1];
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double dm = __dsub_rn(mean[j], ref[j]);
+    drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
+    ref_sq = __dadd_rn(ref_sq, __dmul_rn(ref[j], ref[j]));
+  }
+  acc2[0] = drift_sq;
+  acc2[1] = ref_sq;
+}
+
+__global__ void drift_fast_partial_off(const double* __restrict__ mean,
+                                       const double* __restrict__ ref, std::uint64_t dim,
+                                       std::uint64_t c0, double* __restrict__ partial) {
+  const std::uint64_t c = blockIdx.x;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  double a = 0.0, b = 0.0;
+  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
+    const double dm = __dsub_rn(mean[j], ref[j]);
+    a = __dadd_rn(a, __dmul_rn(dm, dm));
+    b = __dadd_rn(b, __dmul_rn(ref[j], ref[j]));
+  }
+  const double sa = block_sum_fixed(a);
+  const double sb = block_sum_fixed(b);
+  if (threadIdx.x == 0) {
+    partial[2 * (c0 + c)] = sa;
+    partial[2 * (c0 + c) + 1] = sb;
+  }
+}
+
+__global__ void drift_finish_acc(const double* __restrict__ acc2, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *out = __ddiv_rn(__dsqrt_rn(acc2[0]), fmax(__dsqrt_rn(acc2[1]), 1e-300));
+}
+
 unsigned grid_for(std::uint64_t work, unsigned threads) {
   std::uint64_t b = (work + threads - 1) / threads;
   if (b > 148ull * 64) b = 148ull * 64;
@@ -201,6 +279,61 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 }
 
 }  // namespace
+
+std::uint64_t diag_chunk() { return kChunk; }
+
+template <typename T>
+void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                      const double* ref, int exact, double* acc, double* partial,
+                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s) {
+  if (n == 0 || dim == 0) return;
+  if (exact) {
+    dist_rows_exact_acc<T><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, n, ld, dim, ref, acc);
+  } else {
+    const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+    dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch_total, c0, partial);
+  }
+  MB_LAUNCH_CHECK();
+}
+
+void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim, int exact,
+                       double* acc2, double* partial, std::uint64_t c0, cudaStream_t s) {
+  if (dim == 0) return;
+  if (exact) {
+    drift_exact_acc<<<1, 1, 0, s>>>(mean, ref, dim, acc2);
+  } else {
+    const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+    drift_fast_partial_off<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, c0, partial);
+  }
+  MB_LAUNCH_CHECK();
+}
+
+// Final reductions of the slab-streamed diagnostics.
+void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, double* acc,
+                        double* row_partial, double* acc2, double* drift_partial,
+                        double* dist_out, double* drift_out, cudaStream_t s) {
+  if (!exact) {
+    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(row_partial, n, nch_total, acc);
+    MB_LAUNCH_CHECK();
+  }
+  finish_distortion_from_acc<<<1, 1, 0, s>>>(acc, n, dist_out);
+  MB_LAUNCH_CHECK();
+  if (drift_out) {
+    if (exact)
+      drift_finish_acc<<<1, 1, 0, s>>>(acc2, drift_out);
+    else
+      drift_fast_finish<<<1, 1, 0, s>>>(drift_partial, nch_total, drift_out);
+    MB_LAUNCH_CHECK();
+  }
+}
+
+template void launch_dist_slab<float>(const float*, std::uint64_t, std::uint64_t, std::uint64_t,
+                                      const double*, int, double*, double*, std::uint64_t,
+                                      std::uint64_t, cudaStream_t);
+template void launch_dist_slab<double>(const double*, std::uint64_t, std::uint64_t,
+                                       std::uint64_t, const double*, int, double*, double*,
+                                       std::uint64_t, std::uint64_t, cudaStream_t);
 
 std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
   const std::uint64_t nch = (dim + kChunk - 1) / kChunk;

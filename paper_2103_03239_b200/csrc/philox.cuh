@@ -19,7 +19,8 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-// Four standard normals for (step, peer, quad) via Box-Muller in fp64.
+// Four standard normals for (step, peer, quad) via Box-Muller in fp32 (full-
+// rate SFU math; the device-noise path promises statistical parity only).
 __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_t step,
                                                 std::uint64_t peer, std::uint64_t quad,
                                                 double z[4]) {
@@ -30,13 +31,14 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
   const std::uint32_t a[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const double u1 = ((double)a[2 * h] + 1.0) * 0x1.0p-32;  // (0, 1]
-    const double u2 = (double)a[2 * h + 1] * 0x1.0p-32;
-    const double rr = sqrt(-2.0 * log(u1));
-    double s, c;
-    sincospi(2.0 * u2, &s, &c);
-    z[2 * h] = rr * c;
-    z[2 * h + 1] = rr * s;
+    // u1 in (0, 1]: top 24 bits + 1 ulp, exact in fp32
+    const float u1 = (float)((a[2 * h] >> 8) + 1u) * 0x1.0p-24f;
+    const float u2 = (float)(a[2 * h + 1] >> 8) * 0x1.0p-24f;
+    const float rr = sqrtf(-2.0f * logf(u1));
+    float s, c;
+    sincospif(2.0f * u2, &s, &c);
+    z[2 * h] = (double)(rr * c);
+    z[2 * h + 1] = (double)(rr * s);
   }
 }
 

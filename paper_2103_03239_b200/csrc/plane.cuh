@@ -234,4 +234,12 @@ struct Plane {
 };
 
 
+// Slab-pipelined run_moshpit over host buffers (stream_run.cu).
+std::uint64_t stream_slab_cols(std::uint64_t n, std::size_t es, std::uint64_t dim);
+template <typename T>
+void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, std::uint64_t n,
+                          std::uint64_t dim, double p, std::uint64_t seed, std::uint32_t rounds,
+                          int diag, double* init_dist, double* dist, double* drift,
+                          std::uint32_t* active, T* final_out, std::uint64_t W);
+
 }  // namespace mb200

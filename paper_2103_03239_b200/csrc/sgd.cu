@@ -336,7 +336,7 @@ int moshpit_run_moshpit_sgd_quadratic(
     std::uint32_t inner_rounds, std::uint64_t seed, const std::uint32_t* ev_step,
     const std::int32_t* ev_delta, std::uint64_t n_events, int diag, int noise_mode,
     double* f_gap, double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
-    double* final_mean, double* diag6, void* final_thetas) {
+    double* final_mean, double* diag6, void* final_thetas, double* loop_ms) {
   return guarded([&] {
     const std::size_t es = elem_size(dtype);
     if (L < mu || mu < 0.0) throw std::invalid_argument("Quadratic: need L >= mu >= 0");
@@ -427,6 +427,12 @@ int moshpit_run_moshpit_sgd_quadratic(
     std::vector<float> nz32;
     PinnedBuffer nz_pin;
     std::vector<double> wt_hist(steps);
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (loop_ms) {
+      MB_CUDA(cudaEventCreate(&ev0));
+      MB_CUDA(cudaEventCreate(&ev1));
+      MB_CUDA(cudaEventRecord(ev0, h.s));
+    }
     for (std::uint32_t k = 0; k < steps; ++k) {
       for (std::uint64_t e = 0; e < n_events; ++e) {  // optimizer.hpp:337-350
         if (ev_step[e] != k) continue;
@@ -546,6 +552,7 @@ int moshpit_run_moshpit_sgd_quadratic(
       }
       MB_LAUNCH_CHECK();
     }
+    if (loop_ms) MB_CUDA(cudaEventRecord(ev1, h.s));
     if (fused) {
       if (dtype == MOSHPIT_F32)
         launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
@@ -572,6 +579,13 @@ int moshpit_run_moshpit_sgd_quadratic(
       MB_CUDA(cudaMemcpy2DAsync(final_thetas, dim * es, x.ptr, r.ld * es, dim * es, n,
                                 cudaMemcpyDeviceToHost, h.s));
     MB_CUDA(cudaStreamSynchronize(h.s));
+    if (loop_ms) {
+      float ms = 0.f;
+      MB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+      *loop_ms = ms;
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+    }
     std::uint32_t bad = 0;
     MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
     if (bad) throw std::runtime_error("run_moshpit_sgd: non-finite gradient");

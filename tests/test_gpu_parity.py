@@ -390,3 +390,28 @@ def test_native_library_is_loaded_in_process(mb):
     import os
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libmoshpit_b200.so" in maps
+
+
+@pytest.mark.parametrize("f64,diag", [(False, "fast"), (False, "exact"), (True, "exact"),
+                                      (False, "none")])
+def test_streamed_run_moshpit_equals_resident(mb, oracle, monkeypatch, f64, diag):
+    """run_moshpit on host buffers streams D-slabs (H2D || rounds || D2H)
+    once the state exceeds the slab budget; vectors and TrialReport must be
+    bit-identical to the resident path (coordinates independent)."""
+    n, dim, R = 256, 200_003, 4
+    dt = np.float64 if f64 else np.float32
+    x = oracle.init_state(INIT_SEED, n, dim, dtype=dt)
+    grid, fm = mb.GridConfig(16, 2, 1), mb.FailureModel(0.05)
+    monkeypatch.setenv("MOSHPIT_SLAB_BYTES", "1")  # 64 Ki-column slabs -> 4 slabs, ring reused
+    a = mb.run_moshpit(grid, x, fm, mb.Rng(7), R, diagnostics=diag, return_vectors=True)
+    monkeypatch.setenv("MOSHPIT_SLAB_BYTES", str(1 << 40))  # resident
+    b = mb.run_moshpit(grid, x, fm, mb.Rng(7), R, diagnostics=diag, return_vectors=True)
+    assert bits_equal(a.vectors, b.vectors)
+    for k in ("distortion", "mean_drift"):
+        assert bits_equal(np.array(getattr(a, k)), np.array(getattr(b, k))), k
+    assert bits_equal(np.array([a.initial_distortion]), np.array([b.initial_distortion]))
+    assert a.active_counts == b.active_counts
+    if not f64:
+        init = oracle.init_state(INIT_SEED, n, 64, col0=131_000, dtype=dt)
+        _, want = oracle.run_moshpit(16, 2, init, 0.05, 7, R)
+        assert bits_equal(np.ascontiguousarray(a.vectors[:, 131_000:131_064]), want)
