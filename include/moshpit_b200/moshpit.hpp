@@ -17,7 +17,10 @@
 //                          butterfly_allreduce
 //   theory.hpp:149-155     complexity_estimate
 //   protocols.hpp:49-179   TrialReport, run_moshpit
+//   optimizer.hpp:19-242   Objective, Quadratic, OptimizerConfig, MembershipEvent,
+//                          AssumptionDiagnostics, SgdResult, local_step
 //   optimizer.hpp:249-284  detail::moshpit_average
+//   optimizer.hpp:297-439  run_moshpit_sgd (Quadratic objective)
 #pragma once
 
 #include <cmath>
@@ -390,6 +393,160 @@ inline TrialReport run_moshpit(const GridConfig& grid, const std::vector<ParamVe
 }
 
 }  // namespace protocols
+
+// ---- optimizer.hpp:19-242, 297-439 ---------------------------------------------
+namespace optimizer {
+
+class Objective {
+ public:
+  virtual ~Objective() = default;
+  virtual double value(const ParamVector& theta) const = 0;
+  virtual ParamVector gradient(const ParamVector& theta) const = 0;
+  virtual std::size_t dim() const = 0;
+  virtual double smoothness() const = 0;
+  virtual double strong_convexity() const = 0;
+  virtual double optimum_value() const { return 0.0; }
+};
+
+// optimizer.hpp:31-72.  value()/gradient() are the objective's own host
+// utilities; the optimizer loop (local_step, run_moshpit_sgd) runs on the GPU.
+class Quadratic final : public Objective {
+ public:
+  Quadratic(std::size_t dim, double l, double mu, ParamVector target)
+      : target_(std::move(target)), l_(l), mu_(mu) {
+    if (l < mu || mu < 0.0) throw std::invalid_argument("Quadratic: need L >= mu >= 0");
+    if (target_.size() != dim) throw std::invalid_argument("Quadratic: target dimension mismatch");
+    curvature_.resize(dim);
+    for (std::size_t j = 0; j < dim; ++j) {
+      const double t = dim > 1 ? static_cast<double>(j) / (dim - 1) : 0.0;
+      curvature_[j] = mu + (l - mu) * t;
+    }
+    if (dim == 1) curvature_[0] = l;
+  }
+  double value(const ParamVector& theta) const override {
+    double f = 0.0;
+    for (std::size_t j = 0; j < theta.size(); ++j) {
+      const double d = theta[j] - target_[j];
+      f += 0.5 * curvature_[j] * d * d;
+    }
+    return f;
+  }
+  ParamVector gradient(const ParamVector& theta) const override {
+    ParamVector g(theta.size());
+    for (std::size_t j = 0; j < theta.size(); ++j) g[j] = curvature_[j] * (theta[j] - target_[j]);
+    return g;
+  }
+  std::size_t dim() const override { return target_.size(); }
+  double smoothness() const override { return l_; }
+  double strong_convexity() const override { return mu_; }
+  const ParamVector& optimum() const { return target_; }
+
+ private:
+  ParamVector target_;
+  std::vector<double> curvature_;
+  double l_, mu_;
+};
+
+struct OptimizerConfig {
+  double gamma = 0.1;
+  std::uint32_t tau = 1;
+  std::uint32_t steps = 100;
+  GridConfig grid;
+  double sigma = 0.0;
+  std::uint32_t n_peers = 1;
+  std::uint32_t inner_rounds = 0;
+
+  void validate() const {
+    if (gamma <= 0.0) throw std::invalid_argument("OptimizerConfig: gamma > 0");
+    if (tau < 1) throw std::invalid_argument("OptimizerConfig: tau >= 1");
+    if (sigma < 0.0) throw std::invalid_argument("OptimizerConfig: sigma >= 0");
+    grid.validate();
+    if (n_peers < 1 || n_peers > grid.capacity())
+      throw std::invalid_argument("OptimizerConfig: 1 <= N <= M^d");
+  }
+};
+
+struct MembershipEvent {
+  std::uint32_t step = 0;
+  std::int32_t delta = 0;
+};
+
+struct AssumptionDiagnostics {
+  std::vector<double> dispersion;
+  double delta_aq_hat = 0.0;
+  double sigma_hat = 0.0;
+  double delta_pv1_hat = 0.0;
+  double delta_pv2_hat = 0.0;
+  std::uint32_t n_min = 0;
+};
+
+struct SgdResult {
+  std::vector<double> f_gap;
+  std::vector<double> grad_norm_sq;
+  std::vector<double> f_gap_weighted;
+  ParamVector final_mean;
+  AssumptionDiagnostics diagnostics;
+};
+
+namespace b200_detail {
+inline const Quadratic& as_quadratic(const Objective& o) {
+  const auto* q = dynamic_cast<const Quadratic*>(&o);
+  if (!q) throw std::invalid_argument("B200 optimizer path: only the Quadratic objective");
+  return *q;
+}
+inline double quad_l(const Quadratic& q) { return q.smoothness(); }
+inline double quad_mu(const Quadratic& q) { return q.strong_convexity(); }
+}  // namespace b200_detail
+
+// GPU, noise from the caller's stream (optimizer.hpp:231-242).
+inline void local_step(ParamVector& theta, const Objective& objective, double gamma, double sigma,
+                       RngStream& noise) {
+  const Quadratic& q = b200_detail::as_quadratic(objective);
+  b200::check(moshpit_local_step_quadratic(MOSHPIT_F64, theta.data(), theta.size(), q.smoothness(),
+                                           q.strong_convexity(), q.optimum().data(), gamma, sigma,
+                                           &noise.state()));
+}
+
+// GPU, fp64, the reference's noise stream and diagnostic order: the
+// SgdResult is bit-identical to the reference's (tests/test_cpp_dropin.py).
+inline SgdResult run_moshpit_sgd(const OptimizerConfig& config, const Objective& objective,
+                                 const ParamVector& theta0,
+                                 const std::vector<MembershipEvent>& schedule, const Rng& rng) {
+  config.validate();
+  if (theta0.size() != objective.dim())
+    throw std::invalid_argument("run_moshpit_sgd: theta0 dimension mismatch");
+  const Quadratic& q = b200_detail::as_quadratic(objective);
+  std::vector<std::uint32_t> st;
+  std::vector<std::int32_t> dl;
+  for (const auto& e : schedule) {
+    st.push_back(e.step);
+    dl.push_back(e.delta);
+  }
+  SgdResult r;
+  const std::uint32_t K = config.steps;
+  r.f_gap.resize(K);
+  r.grad_norm_sq.resize(K);
+  r.f_gap_weighted.resize(K);
+  r.diagnostics.dispersion.resize(K);
+  r.final_mean.resize(theta0.size());
+  double d6[6] = {0, 0, 0, 0, 0, 0};
+  b200::check(moshpit_run_moshpit_sgd_quadratic(
+      MOSHPIT_F64, config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
+      config.n_peers, theta0.size(), q.smoothness(), q.strong_convexity(), q.optimum().data(),
+      theta0.data(), config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds,
+      rng.seed(), st.empty() ? nullptr : st.data(), dl.empty() ? nullptr : dl.data(), st.size(),
+      MOSHPIT_DIAG_EXACT, 0, r.f_gap.data(), r.grad_norm_sq.data(), r.f_gap_weighted.data(),
+      r.diagnostics.dispersion.data(), r.final_mean.data(), d6, nullptr, nullptr));
+  r.diagnostics.delta_aq_hat = d6[0];
+  r.diagnostics.sigma_hat = d6[1];
+  r.diagnostics.delta_pv1_hat = d6[2];
+  r.diagnostics.delta_pv2_hat = d6[3];
+  r.diagnostics.n_min = static_cast<std::uint32_t>(d6[4]);
+  if (K == 0) r.final_mean.clear();
+  return r;
+}
+
+}  // namespace optimizer
 
 // ---- optimizer.hpp:249-284 ----------------------------------------------------
 namespace optimizer::detail {

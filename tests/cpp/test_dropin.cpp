@@ -199,6 +199,53 @@ int main() {
     for (const auto& t : thetas)
       for (std::size_t j = 0; j < 3; ++j) CHECK(std::abs(t[j] - m0[j]) <= 1e-15);
   }
+  // test_optimizer.cpp:60-98, 160-193 through the drop-in (GPU)
+  {
+    const optimizer::Quadratic quad(2, 2.0, 2.0, ParamVector{1.0, 1.0});
+    ParamVector theta{0.0, 0.0};
+    Rng rng(23);
+    auto noise = rng.stream("n");
+    optimizer::local_step(theta, quad, 0.25, 0.0, noise);
+    CHECK(std::abs(theta[0] - 0.5) < 1e-12);
+    CHECK(std::abs(theta[1] - 0.5) < 1e-12);
+
+    Rng r24(24);
+    auto st = r24.stream("target");
+    const optimizer::Quadratic q4(4, 5.0, 0.5, st.normals(4));
+    optimizer::OptimizerConfig cfg;
+    cfg.gamma = 0.05;
+    cfg.tau = 1;
+    cfg.steps = 60;
+    cfg.grid = GridConfig{4, 2, 1};
+    cfg.n_peers = 9;
+    const ParamVector theta0(4, 2.0);
+    const auto res = optimizer::run_moshpit_sgd(cfg, q4, theta0, {}, Rng(500));
+    ParamVector th = theta0;
+    for (std::uint32_t k = 0; k < cfg.steps; ++k) {
+      const auto g = q4.gradient(th);
+      for (std::size_t j = 0; j < th.size(); ++j) th[j] -= cfg.gamma * g[j];
+      CHECK(std::abs(res.f_gap[k] - q4.value(th)) <= 1e-12);
+      CHECK(res.diagnostics.dispersion[k] <= 1e-24);
+    }
+    const optimizer::Quadratic q2(2, 2.0, 1.0, ParamVector(2, 1.0));
+    optimizer::OptimizerConfig c2;
+    c2.gamma = 0.1;
+    c2.tau = 2;
+    c2.steps = 20;
+    c2.sigma = 0.5;
+    c2.grid = GridConfig{4, 2, 1};
+    c2.n_peers = 8;
+    const auto rm = optimizer::run_moshpit_sgd(c2, q2, ParamVector(2, 0.0), {{5, -3}, {12, +2}},
+                                               Rng(777));
+    CHECK(rm.diagnostics.n_min == 5);
+    CHECK(rm.f_gap.size() == c2.steps);
+    CHECK_THROWS_AS(optimizer::run_moshpit_sgd(c2, q2, ParamVector(2, 0.0), {{3, -8}}, Rng(1)),
+                    std::invalid_argument);
+    optimizer::OptimizerConfig bad;
+    bad.grid = GridConfig{2, 2, 1};
+    bad.n_peers = 5;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  }
   // golden case: counter init, C2-shaped (32x32, p=0.01, 10 rounds), dim 4
   {
     const std::size_t n = 1024, dim = 4;
