@@ -107,9 +107,9 @@ struct MeanArgs {
 // non-finite check is on g; theta' = theta - gamma*g.  Same rounding and the
 // same Philox noise per (step, peer, coordinate) as the standalone step kernel
 // (sgd.cu), so fused == unfused bit for bit.
-__device__ __forceinline__ float sgd_grad(float x, float c, float t, double nj, bool noisy) {
+__device__ __forceinline__ float sgd_grad(float x, float c, float t, float nj, bool noisy) {
   float g = __fmul_rn(c, __fsub_rn(x, t));
-  return noisy ? __fadd_rn(g, (float)nj) : g;
+  return noisy ? __fadd_rn(g, nj) : g;
 }
 __device__ __forceinline__ double sgd_grad(double x, double c, double t, double nj, bool noisy) {
   double g = __dmul_rn(c, __dsub_rn(x, t));
@@ -124,25 +124,24 @@ __device__ __forceinline__ double sgd_update(double x, double gm, double g) {
 
 template <typename T, typename V>
 __device__ __forceinline__ V apply_step(const StepPrologue<T>& sp, V v, std::uint32_t peer,
-                                        std::uint64_t col, double& nsq, bool& bad) {
+                                        std::uint64_t col, const V& c, const V& t, double& nsq,
+                                        bool& bad) {
   constexpr int kV = sizeof(V) / sizeof(T);
-  const V c = reinterpret_cast<const V*>(sp.curv)[col];
-  const V t = reinterpret_cast<const V*>(sp.tgt)[col];
   T* pv = reinterpret_cast<T*>(&v);
   const T* pc = reinterpret_cast<const T*>(&c);
   const T* pt = reinterpret_cast<const T*>(&t);
   const std::uint64_t j0 = col * kV;
-  double z[4] = {0, 0, 0, 0};
+  float z[4] = {0, 0, 0, 0};
   const bool noisy = sp.philox != 0;
   if (noisy) philox_normals4(sp.seed, sp.step_no, peer, j0 / 4, z);
 #pragma unroll
   for (int u = 0; u < kV; ++u) {
     const std::uint64_t j = j0 + u;
     if (j >= sp.dim) break;
-    const double nj = noisy ? sp.coord_std * z[j % 4] : 0.0;
-    if (noisy) nsq += nj * nj;
+    const T nj = noisy ? noise_component(z[j % 4], sp.coord_std, (T*)nullptr) : T(0);
+    if (noisy) nsq += (double)nj * (double)nj;
     const T g = sgd_grad(pv[u], pc[u], pt[u], nj, noisy);
-    bad |= !isfinite((double)g);
+    bad |= !isfinite(g);
     pv[u] = sgd_update(pv[u], sp.gamma, g);
   }
   return v;
@@ -157,8 +156,11 @@ __device__ __forceinline__ void mean_fixed(V* base, std::uint64_t ld_vec,
 #pragma unroll
   for (int k = 0; k < N; ++k) x[k] = vload(base + (std::uint64_t)ids[k] * ld_vec + col);
   if constexpr (STEP) {
+    // curvature / target of this column: loaded once per item, not per member
+    const V c = __ldg(reinterpret_cast<const V*>(sp.curv) + col);
+    const V t = __ldg(reinterpret_cast<const V*>(sp.tgt) + col);
 #pragma unroll
-    for (int k = 0; k < N; ++k) x[k] = apply_step(sp, x[k], ids[k], col, nsq, bad);
+    for (int k = 0; k < N; ++k) x[k] = apply_step(sp, x[k], ids[k], col, c, t, nsq, bad);
   }
   const V m = vdiv(tree<N, 0>(x), (std::uint32_t)N);
 #pragma unroll
@@ -205,7 +207,10 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
         const std::uint32_t* ids = cnt <= kMaxSmemIds ? sids : a.members + beg;
         auto ld = [&](std::uint32_t k) {
           V v = vload(base + (std::uint64_t)ids[k] * a.ld_vec + col);
-          if constexpr (STEP) v = apply_step(a.step, v, ids[k], col, nsq, bad);
+          if constexpr (STEP)
+            v = apply_step(a.step, v, ids[k], col,
+                           __ldg(reinterpret_cast<const V*>(a.step.curv) + col),
+                           __ldg(reinterpret_cast<const V*>(a.step.tgt) + col), nsq, bad);
           return v;
         };
         const V m = vdiv(pairwise_rt<V>(ld, cnt, [](V x, V y) { return vadd(x, y); },

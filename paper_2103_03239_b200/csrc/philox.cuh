@@ -19,11 +19,12 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
-// Four standard normals for (step, peer, quad) via Box-Muller in fp32 (full-
-// rate SFU math; the device-noise path promises statistical parity only).
+// Four standard normals for (step, peer, quad): Box-Muller on SFU intrinsics
+// (the device-noise path promises statistical parity only, and this keeps the
+// fused step + averaging kernel memory-bound).
 __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_t step,
                                                 std::uint64_t peer, std::uint64_t quad,
-                                                double z[4]) {
+                                                float z[4]) {
   const uint4 r = philox4x32_10(
       make_uint4((std::uint32_t)step, (std::uint32_t)peer, (std::uint32_t)quad,
                  (std::uint32_t)(quad >> 32)),
@@ -31,15 +32,23 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
   const std::uint32_t a[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    // u1 in (0, 1]: top 24 bits + 1 ulp, exact in fp32
-    const float u1 = (float)((a[2 * h] >> 8) + 1u) * 0x1.0p-24f;
-    const float u2 = (float)(a[2 * h + 1] >> 8) * 0x1.0p-24f;
-    const float rr = sqrtf(-2.0f * logf(u1));
+    const float u1 = (float)((a[2 * h] >> 8) + 1u) * 0x1.0p-24f;  // (0, 1]
+    const float u2 = (float)(a[2 * h + 1] >> 8) * 0x1.0p-24f;     // [0, 1)
+    const float rr = __fsqrt_rn(-2.0f * __logf(u1));
     float s, c;
-    sincospif(2.0f * u2, &s, &c);
-    z[2 * h] = (double)(rr * c);
-    z[2 * h + 1] = (double)(rr * s);
+    __sincosf(6.283185307179586f * u2, &s, &c);
+    z[2 * h] = rr * c;
+    z[2 * h + 1] = rr * s;
   }
+}
+
+// One noise component n_j = coord_std * z in the state's precision; both the
+// standalone step kernel and the fused kernel 3 use it (bit-identical noise).
+__device__ __forceinline__ float noise_component(float z, double coord_std, float*) {
+  return __fmul_rn((float)coord_std, z);
+}
+__device__ __forceinline__ double noise_component(float z, double coord_std, double*) {
+  return __dmul_rn(coord_std, (double)z);
 }
 
 }  // namespace mb200

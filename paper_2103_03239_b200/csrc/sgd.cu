@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kStepThreads)
   for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (std::uint64_t)gridDim.x * blockDim.x) {
     const std::uint64_t i = e / quads, q = e % quads;
-    double z[4] = {0, 0, 0, 0};
+    float z[4] = {0, 0, 0, 0};
     if (philox_mode) philox_normals4(seed, step, i, q, z);
     for (int u = 0; u < 4; ++u) {
       const std::uint64_t j = q * 4 + u;
@@ -64,11 +64,11 @@ __global__ void __launch_bounds__(kStepThreads)
       if (noise) {
         g = O::add(g, noise[i * dim + j]);
       } else if (philox_mode) {
-        const double nj = coord_std * z[u];
-        nsq += nj * nj;
-        g = O::add(g, (T)nj);
+        const T nj = noise_component(z[u], coord_std, (T*)nullptr);
+        nsq += (double)nj * (double)nj;
+        g = O::add(g, nj);
       }
-      if (!isfinite((double)g)) atomicOr(nonfinite, 1u);
+      if (!isfinite(g)) atomicOr(nonfinite, 1u);
       *p = O::sub(*p, O::mul(gamma, g));
     }
   }
