@@ -58,12 +58,13 @@ __device__ __forceinline__ double2 vdiv(double2 a, std::uint32_t n) {
   return make_double2(__ddiv_rn(a.x, f), __ddiv_rn(a.y, f));
 }
 
-// Streaming 128-bit accesses: every row tile is touched once per round, so
-// keep it out of L1 and mark it evict-first in L2.
-__device__ __forceinline__ float4 vload(const float4* p) { return __ldcs(p); }
-__device__ __forceinline__ double2 vload(const double2* p) { return __ldcs(p); }
-__device__ __forceinline__ void vstore(float4* p, float4 v) { __stcs(p, v); }
-__device__ __forceinline__ void vstore(double2* p, double2 v) { __stcs(p, v); }
+// Plain 128-bit LDG/STG.  Measured on B200 (profiles/k2_variants.cu): with one
+// CTA per SM the default cache policy beats the streaming (.cs) and .nc hints
+// by ~2-5 % on this access pattern.
+__device__ __forceinline__ float4 vload(const float4* p) { return *p; }
+__device__ __forceinline__ double2 vload(const double2* p) { return *p; }
+__device__ __forceinline__ void vstore(float4* p, float4 v) { *p = v; }
+__device__ __forceinline__ void vstore(double2* p, double2 v) { *p = v; }
 
 // core.hpp:72-81 over x[B .. B+N) with compile-time shape.
 template <int N, int B, typename V>
@@ -478,7 +479,19 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     a.n_tiles = (a.nvec + kBulkTileVec - 1) / kBulkTileVec;
     group_mean_bulk<T><<<sms, kBulkThreads, smem, s>>>(a, stages, (int)srows);
   } else {
-    group_mean_register<T, false><<<mean_grid<T, false>(), kThreads, 0, s>>>(a);
+    // Fewer concurrent row streams keep DRAM pages open: measured on B200
+    // (profiles/r01/k2_grid_sweep.txt) two 128-thread CTAs per SM are best for
+    // groups of 16-32 members (0.95-0.96 of the copy peak vs 0.91-0.92 at full
+    // occupancy); groups of <= 8 need full occupancy for bytes in flight.
+    int sms = 0, dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int occ = mean_grid<T, false>() / (sms ? sms : 1);
+    int per = max_group > 8 ? 2 : occ;
+    if (const char* e = std::getenv("MOSHPIT_K2_CTAS_PER_SM")) per = std::atoi(e);
+    if (per < 1) per = 1;
+    if (per > occ) per = occ;
+    group_mean_register<T, false><<<sms * per, kThreads, 0, s>>>(a);
   }
   MB_LAUNCH_CHECK();
 }
