@@ -501,13 +501,20 @@ def measure_e2e(mb, cfg):
     act = np.zeros(R, dtype=np.uint32)
     init_d, cost = C.c_double(0), C.c_double(0)
     ptr = xh.ctypes.data_as(C.c_void_p)
-    t0 = time.perf_counter()
-    _capi.check(lib.moshpit_run_moshpit(_capi.F32, M, d, R, ptr, N, D, p, PROTOCOL_SEED, R,
-                                        _capi.DIAG_FAST, C.byref(init_d),
-                                        dist_.ctypes.data_as(C.c_void_p),
-                                        drift.ctypes.data_as(C.c_void_p),
-                                        act.ctypes.data_as(C.c_void_p), C.byref(cost), ptr))
-    t = time.perf_counter() - t0
+
+    def call():
+        _capi.check(lib.moshpit_run_moshpit(_capi.F32, M, d, R, ptr, N, D, p, PROTOCOL_SEED, R,
+                                            _capi.DIAG_FAST, C.byref(init_d),
+                                            dist_.ctypes.data_as(C.c_void_p),
+                                            drift.ctypes.data_as(C.c_void_p),
+                                            act.ctypes.data_as(C.c_void_p), C.byref(cost), ptr))
+    call()  # warm-up: kernel module loading + workspace allocation (untimed)
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    t = sorted(times)[1]  # median of 3
     bytes_ = N * D * 4
     # PCIe reference point: one plain pinned H2D copy of the same state
     dev = torch.empty((N, D), dtype=torch.float32, device="cuda")
@@ -520,7 +527,9 @@ def measure_e2e(mb, cfg):
     return {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
             "call": f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, pinned",
-            "seconds": round(t, 4), "final_distortion": float(dist_[-1]),
+            "seconds": round(t, 4), "seconds_each": [round(x, 4) for x in times],
+            "timing": "host wall clock per call, 1 warm-up + median of 3",
+            "final_distortion": float(dist_[-1]),
             "pipeline": "D-slabs of 256 MB: H2D(s+1) || 10 rounds + diagnostics(s) || D2H(s-1)",
             "pcie_h2d_gbs_plain_copy": round(h2d_gbs, 1)}
 

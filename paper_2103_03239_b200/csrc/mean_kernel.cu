@@ -18,6 +18,7 @@
 // tree is register-local, so no cross-lane shuffles are needed and the fp32
 // result is bit-identical to the fp32 restatement of the reference, and the
 // fp64 instantiation bit-identical to the reference itself.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -491,7 +492,29 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     if (const char* e = std::getenv("MOSHPIT_K2_CTAS_PER_SM")) per = std::atoi(e);
     if (per < 1) per = 1;
     if (per > occ) per = occ;
-    group_mean_register<T, false><<<sms * per, kThreads, 0, s>>>(a);
+    // Pin residency to exactly `per` CTAs per SM: reserve enough dynamic shared
+    // memory that a (per+1)-th CTA cannot fit, so the grid of sms*per CTAs is
+    // spread evenly instead of stacking up to the register limit on some SMs.
+    std::size_t pin = 0;
+    if (per < occ) {
+      int smem_sm = 0;
+      MB_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+      pin = (std::size_t)smem_sm / (per + 1) + 1024;
+      static thread_local int set_dev[2] = {-1, -1};
+      const int slot = sizeof(T) == 4 ? 0 : 1;
+      if (set_dev[slot] != dev) {
+        MB_CUDA(cudaFuncSetAttribute(group_mean_register<T, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        set_dev[slot] = dev;
+      }
+    }
+    if (std::getenv("MOSHPIT_DEBUG")) {
+      static thread_local int once = 0;
+      if (!once++)
+        fprintf(stderr, "[moshpit] kernel2 max_group=%u occ=%d per=%d pin=%zu grid=%d\n",
+                max_group, occ, per, pin, sms * per);
+    }
+    group_mean_register<T, false><<<sms * per, kThreads, pin, s>>>(a);
   }
   MB_LAUNCH_CHECK();
 }

@@ -30,6 +30,37 @@ std::uint64_t stream_slab_cols(std::uint64_t n, std::size_t es, std::uint64_t di
   return w;
 }
 
+namespace {
+
+// Grow-only per-thread workspace: repeated host-buffer calls (the harness
+// runs many trials per thread) reuse the slab ring, tables, diagnostics
+// buffers, streams and -- for the same (M, d, n) -- the integer plane, instead
+// of paying cudaMalloc/cudaFree/cudaMallocHost on every call.
+struct StreamWorkspace {
+  int dev = -1;
+  std::unique_ptr<DeviceBuffer> ring[3];
+  DeviceBuffer t_mem, t_goff, t_act, t_cnt, ref, mean_s, acc, acc2, rpart, dpart, out;
+  std::unique_ptr<Plane> plane;
+  std::uint32_t pM = 0, pd = 0;
+  std::uint64_t pn = 0;
+  std::unique_ptr<StreamHolder> s_in, s_cmp, s_out;
+};
+thread_local std::unique_ptr<StreamWorkspace> tl_ws;
+
+StreamWorkspace& workspace(int dev) {
+  if (!tl_ws || tl_ws->dev != dev) {
+    tl_ws = std::make_unique<StreamWorkspace>();
+    tl_ws->dev = dev;
+    for (auto& r : tl_ws->ring) r = std::make_unique<DeviceBuffer>();
+    tl_ws->s_in = std::make_unique<StreamHolder>();
+    tl_ws->s_cmp = std::make_unique<StreamHolder>();
+    tl_ws->s_out = std::make_unique<StreamHolder>();
+  }
+  return *tl_ws;
+}
+
+}  // namespace
+
 template <typename T>
 void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, std::uint64_t n,
                           std::uint64_t dim, double p, std::uint64_t seed, std::uint32_t rounds,
@@ -38,16 +69,27 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
   const std::size_t es = sizeof(T);
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
-  StreamHolder s_in, s_cmp, s_out;
+  StreamWorkspace& ws = workspace(dev);
+  StreamHolder &s_in = *ws.s_in, &s_cmp = *ws.s_cmp, &s_out = *ws.s_out;
   const std::uint64_t R = rounds;
   // 1. the integer plane of every round (identical for all slabs)
-  Plane plane(M, d, n, dev);
+  if (!ws.plane || ws.pM != M || ws.pd != d || ws.pn != n) {
+    ws.plane.reset();
+    ws.plane = std::make_unique<Plane>(M, d, n, dev);
+    ws.pM = M;
+    ws.pd = d;
+    ws.pn = n;
+  }
+  Plane& plane = *ws.plane;
   Xoshiro cells = Xoshiro::named(seed, "cells");
   plane.init_cells(cells, s_cmp.s);
   Xoshiro fail = Xoshiro::named(seed, "failures");
   Xoshiro clock = Xoshiro::named(seed, "priorities");
-  DeviceBuffer t_mem(R * n * 4 + 16), t_goff(R * (n + 1) * 4 + 16), t_act(R * n * 4 + 16),
-      t_cnt(R * 16 + 16);
+  DeviceBuffer &t_mem = ws.t_mem, &t_goff = ws.t_goff, &t_act = ws.t_act, &t_cnt = ws.t_cnt;
+  t_mem.resize(R * n * 4 + 16);
+  t_goff.resize(R * (n + 1) * 4 + 16);
+  t_act.resize(R * n * 4 + 16);
+  t_cnt.resize(R * 16 + 16);
   for (std::uint64_t r = 0; r < R; ++r) {
     active[r] = plane.round(&fail, p, clock, 0, nullptr, 0, 0, s_cmp.s, 0);
     MB_CUDA(cudaMemcpyAsync(t_mem.as<std::uint32_t>() + r * n, plane.members.ptr, n * 4,
@@ -66,9 +108,10 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
   const int exact = diag == MOSHPIT_DIAG_EXACT;
   const bool dg = diag != MOSHPIT_DIAG_NONE;
   constexpr int kRing = 3;
-  std::unique_ptr<DeviceBuffer> buf[kRing];
-  for (auto& b : buf) b = std::make_unique<DeviceBuffer>(n * W * es + 16);
-  DeviceBuffer ref, mean_s, acc, acc2, rpart, dpart, out;
+  std::unique_ptr<DeviceBuffer>* buf = ws.ring;
+  for (int k = 0; k < kRing; ++k) buf[k]->resize(n * W * es + 16);
+  DeviceBuffer &ref = ws.ref, &mean_s = ws.mean_s, &acc = ws.acc, &acc2 = ws.acc2,
+               &rpart = ws.rpart, &dpart = ws.dpart, &out = ws.out;
   if (dg) {
     ref.resize(dim * 8 + 16);
     mean_s.resize(W * 8 + 16);
@@ -79,8 +122,8 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
       dpart.resize((R + 1) * 2 * nch * 8 + 16);
     }
     out.resize((2 * R + 2) * 8);
-    MB_CUDA(cudaMemsetAsync(acc.ptr, 0, acc.bytes, s_cmp.s));
-    MB_CUDA(cudaMemsetAsync(acc2.ptr, 0, acc2.bytes, s_cmp.s));
+    MB_CUDA(cudaMemsetAsync(acc.ptr, 0, (R + 1) * n * 8, s_cmp.s));
+    MB_CUDA(cudaMemsetAsync(acc2.ptr, 0, (R + 1) * 16 + 16, s_cmp.s));
   }
   cudaEvent_t ev_in[kRing], ev_cmp[kRing], ev_out[kRing];
   for (int k = 0; k < kRing; ++k) {
