@@ -429,7 +429,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
         "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),
         "unit": "GB/s", "scaling": "strong", "steps": steps, "ms_per_step": round(t_max / steps, 4),
         "rounds_local": ln, "rounds_cross": cross_rounds,
-        "gpu_launches": ln * 3 + cross_rounds * (6 + (2 if p > 0 else 0)),
+        "gpu_launches": ln * 3 + cross_rounds * (7 + (2 if p > 0 else 0)),
         "local_kernel_ms": round(lmax, 3), "cross_kernel_ms": round(cmax, 3),
         "roofline": {
             "bound": "hbm (local rounds) + nvlink (cross rounds)",
@@ -443,8 +443,9 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
             "combined_frac": round((trl + trc) / (lmax + cmax), 4) if (lmax + cmax) else None,
             "note": "t_roof = max(HBM bytes / hbm_gbs, NVLink ingress / 770 GB/s) per round, "
                     "busiest GPU, minimal bytes (raw remote member chunks + one copy of each "
-                    "foreign mean chunk); t_measured = data-plane kernels incl. the local "
-                    "fan-out; frac = sum t_roof / sum t_measured",
+                    "foreign mean chunk, all NVLink traffic as pulls); t_measured = data-plane "
+                    "kernels (phase A chunk means + phase B pulls); frac = sum t_roof / sum "
+                    "t_measured",
         },
     }
 

@@ -175,7 +175,7 @@ struct CrossArgs {
   T* pools[kMaxWorld];
   std::uint64_t ld_vec = 0, R = 0;
   std::uint64_t c0 = 0, c1 = 0, n_tiles = 0;
-  std::uint32_t me = 0;
+  std::uint32_t me = 0, world = 1;
   const std::uint32_t* goff = nullptr;
   const std::uint32_t* src_row = nullptr;
   const std::uint32_t* dst_row = nullptr;
@@ -213,15 +213,11 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
       if (threadIdx.x < cnt) {
         const std::uint32_t s = a.src_row[beg + threadIdx.x], d = a.dst_row[beg + threadIdx.x];
         const std::uint32_t dg = (std::uint32_t)(d / a.R);
-        // A remote GPU receives ONE copy of this chunk's mean, in its first
-        // member row (in group order); it broadcasts locally after the
-        // barrier (shard_bcast_kernel).  Local member rows get it directly.
-        bool store = dg == a.me;
-        if (!store) {
-          store = true;
-          for (std::uint32_t j = 0; j < threadIdx.x; ++j)
-            if ((std::uint32_t)(a.dst_row[beg + j] / a.R) == dg) store = false;
-        }
+        // Pull-only NVLink traffic: the mean of this GPU's chunk goes to its
+        // LOCAL member rows only; other GPUs pull it in phase B
+        // (shard_pull_kernel).  Mixing remote loads and remote stores in one
+        // kernel costs ~2x NVLink throughput (profiles/r01/p2p_probe.txt).
+        const bool store = dg == a.me;
         s_src[threadIdx.x] = reinterpret_cast<V*>(a.pools[s / a.R]) + (s % a.R) * a.ld_vec;
         s_dst[threadIdx.x] =
             store ? reinterpret_cast<V*>(a.pools[dg]) + (d % a.R) * a.ld_vec : nullptr;
@@ -248,41 +244,48 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
   }
 }
 
-// After the cross round's barrier: copy the foreign chunks (written by their
-// owner GPUs into this GPU's first member row of each active group) into the
-// group's other member rows on this GPU.  Local HBM only.
+// Phase B of the cross round (after a barrier): for every active group, pull
+// each foreign coordinate chunk c once from GPU c's first member row of the
+// group (in group order) -- a remote READ -- and write it into this GPU's
+// member rows of the group (local writes).  Every GPU derives the same rows
+// from the replicated tables, so no metadata travels.
 template <typename T>
 __global__ void __launch_bounds__(kCrossThreads)
-    shard_bcast_kernel(T* pool, std::uint64_t ld_vec, std::uint64_t R, std::uint32_t me,
-                       std::uint64_t own0, std::uint64_t own1, std::uint64_t nvec,
-                       std::uint64_t n_tiles, const std::uint32_t* goff,
-                       const std::uint32_t* dst_row, const std::uint32_t* act,
-                       const std::uint32_t* cnt_cross) {
+    shard_pull_kernel(CrossArgs<T> a, std::uint64_t nvec) {
   using V = typename V16s<T>::type;
   __shared__ V* s_rows[32];
+  __shared__ const V* s_rep[kMaxWorld];
   __shared__ std::uint32_t s_n;
-  const std::uint64_t n_items = (std::uint64_t)cnt_cross[1] * n_tiles;
+  const std::uint32_t world = a.world;
+  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
   std::uint32_t cached = 0xffffffffu;
-  V* base = reinterpret_cast<V*>(pool);
   for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const std::uint32_t g = act[w / n_tiles];
+    const std::uint32_t g = a.act[w / a.n_tiles];
     if (g != cached) {
       __syncthreads();
       if (threadIdx.x == 0) {
         std::uint32_t k = 0;
-        for (std::uint32_t pos = goff[g]; pos < goff[g + 1]; ++pos) {
-          const std::uint32_t d = dst_row[pos];
-          if ((std::uint32_t)(d / R) == me) s_rows[k++] = base + (d % R) * ld_vec;
+        for (std::uint32_t h = 0; h < world; ++h) s_rep[h] = nullptr;
+        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
+          const std::uint32_t d = a.dst_row[pos];
+          const std::uint32_t h = (std::uint32_t)(d / a.R);
+          V* row = reinterpret_cast<V*>(a.pools[h]) + (d % a.R) * a.ld_vec;
+          if (!s_rep[h]) s_rep[h] = row;
+          if (h == a.me) s_rows[k++] = row;
         }
         s_n = k;
       }
       cached = g;
       __syncthreads();
     }
-    const std::uint64_t col = (w % n_tiles) * kCrossThreads + threadIdx.x;
-    if (col >= nvec || (col >= own0 && col < own1) || s_n < 2) continue;
-    const V v = __ldcs(s_rows[0] + col);
-    for (std::uint32_t k = 1; k < s_n; ++k) __stcs(s_rows[k] + col, v);
+    const std::uint64_t col = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    if (col >= nvec || (col >= a.c0 && col < a.c1)) continue;
+    // owner of this column: chunk c covers [nvec*c/world, nvec*(c+1)/world)
+    std::uint32_t c = (std::uint32_t)((col * world) / nvec);
+    while (c + 1 < world && (nvec * (c + 1)) / world <= col) ++c;
+    while (c > 0 && (nvec * c) / world > col) --c;
+    const V v = *(s_rep[c] + col);
+    for (std::uint32_t k = 0; k < s_n; ++k) s_rows[k][col] = v;
   }
 }
 
@@ -455,6 +458,7 @@ struct Shard {
     a.c1 = nv * (r + 1) / world;
     a.n_tiles = (a.c1 - a.c0 + kCrossThreads - 1) / kCrossThreads;
     a.me = r;
+    a.world = world;
     a.goff = plane->goff.as<std::uint32_t>();
     a.src_row = src_row.as<std::uint32_t>();
     a.dst_row = dst_row.as<std::uint32_t>();
@@ -469,16 +473,25 @@ struct Shard {
   }
 
   template <typename T>
-  void bcast_launch(std::uint32_t r, cudaStream_t s) {
-    if (Mg < 2) return;  // one member per GPU: nothing to fan out
+  void pull_launch(std::uint32_t r, cudaStream_t s) {
+    if (world < 2) return;
+    CrossArgs<T> a;
+    for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
+    a.ld_vec = ld * es / 16;
+    a.R = R;
     const std::uint64_t nv = nvec();
-    const std::uint64_t n_tiles = (nv + kCrossThreads - 1) / kCrossThreads;
+    a.c0 = nv * r / world;
+    a.c1 = nv * (r + 1) / world;
+    a.n_tiles = (nv + kCrossThreads - 1) / kCrossThreads;
+    a.me = r;
+    a.world = world;
+    a.goff = plane->goff.as<std::uint32_t>();
+    a.dst_row = dst_row.as<std::uint32_t>();
+    a.act = act_cross.as<std::uint32_t>();
+    a.cnt = cnt_cross.as<std::uint32_t>();
     int sms = 0;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    shard_bcast_kernel<T><<<sms * 4, kCrossThreads, 0, s>>>(
-        static_cast<T*>(pools[r]), ld * es / 16, R, r, nv * r / world, nv * (r + 1) / world, nv,
-        n_tiles, plane->goff.as<std::uint32_t>(), dst_row.as<std::uint32_t>(),
-        act_cross.as<std::uint32_t>(), cnt_cross.as<std::uint32_t>());
+    shard_pull_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a, nv);
     MB_LAUNCH_CHECK();
   }
 
@@ -565,7 +578,7 @@ struct Shard {
         }
       }
       if (timing) MB_CUDA(cudaEventRecord(te.second, s));
-      barrier(s);  // every remote read/write of our rows is done
+      barrier(s);  // every chunk mean is in its owner's rows; raw reads are done
       std::pair<cudaEvent_t, cudaEvent_t> tb{};
       if (timing) {
         tb = tpair(true);
@@ -574,14 +587,15 @@ struct Shard {
       for (std::uint32_t k = 0; k < nranks; ++k) {
         const std::uint32_t r = emulate ? k : me;
         if (dtype == MOSHPIT_F32) {
-          bcast_launch<float>(r, s);
+          pull_launch<float>(r, s);
           moves_launch<float>(r, 1, s);
         } else {
-          bcast_launch<double>(r, s);
+          pull_launch<double>(r, s);
           moves_launch<double>(r, 1, s);
         }
       }
       if (timing) MB_CUDA(cudaEventRecord(tb.second, s));
+      barrier(s);  // peers finished pulling from our rows before we touch them again
     }
     if (crossed) *crossed = a.cross;
     return active;
