@@ -415,3 +415,23 @@ def test_streamed_run_moshpit_equals_resident(mb, oracle, monkeypatch, f64, diag
         init = oracle.init_state(INIT_SEED, n, 64, col0=131_000, dtype=dt)
         _, want = oracle.run_moshpit(16, 2, init, 0.05, 7, R)
         assert bits_equal(np.ascontiguousarray(a.vectors[:, 131_000:131_064]), want)
+
+
+def test_concurrent_callers_are_independent(mb, oracle):
+    """harness::run_experiment calls run_moshpit from many threads at once
+    (harness.hpp:240-248): concurrent calls through the C ABI (ctypes releases
+    the GIL) must equal the sequential results bit for bit."""
+    import concurrent.futures as cf
+    cases = [(16, 2, 256, 0.05, 6, 33), (32, 2, 1024, 0.01, 4, 17), (8, 3, 512, 0.0, 3, 9),
+             (5, 2, 25, 0.2, 10, 4)] * 3
+    def run(c):
+        M, d, n, p, R, dim = c
+        x = oracle.init_state(INIT_SEED + n, n, dim, dtype=np.float64)
+        r = mb.run_moshpit(mb.GridConfig(M, d, 1), x, mb.FailureModel(p), mb.Rng(n), R,
+                           return_vectors=True)
+        return r.vectors, np.array(r.distortion)
+    seq = [run(c) for c in cases]
+    with cf.ThreadPoolExecutor(max_workers=6) as ex:
+        par = list(ex.map(run, cases))
+    for (va, da), (vb, db) in zip(seq, par):
+        assert bits_equal(va, vb) and bits_equal(da, db)
