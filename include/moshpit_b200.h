@@ -128,6 +128,23 @@ int moshpit_run_moshpit(int dtype, uint32_t M, uint32_t d, uint32_t T,
                         uint32_t* active_counts, double* cost_units,
                         void* final_out);
 
+/* ---- trial-batched run_moshpit (harness.hpp:157-280 sweeps)  [GPU] ------
+ * `trials` independent protocols::run_moshpit calls in one batch: trial t
+ * uses initial + t*n*dim and Rng(seeds[t]); reports are [trials] and
+ * [trials][rounds]; diagnostics in the reference order unless DIAG_NONE.
+ * n <= 8192, trials <= 65535. */
+int moshpit_run_moshpit_batch(int dtype, uint32_t M, uint32_t d, uint32_t T,
+                              uint32_t trials, const void* initial, uint64_t n,
+                              uint64_t dim, double p_round, const uint64_t* seeds,
+                              uint32_t rounds, int diag, double* initial_distortion,
+                              double* distortion, double* mean_drift,
+                              uint32_t* active_counts, double* cost_units,
+                              void* final_out);
+/* harness.hpp:145-155 trial_rng: root seed of trial `seed_index` of a sweep
+ * cell (protocol name as protocols::to_string). [host] */
+uint64_t moshpit_trial_seed(uint64_t seed_base, const char* protocol, uint32_t n,
+                            double p, uint32_t seed_index);
+
 /* ---- optimizer.hpp:249-284 detail::moshpit_average  [GPU, host buffers]
  * thetas (n*dim, dtype) averaged in place; *stream advanced exactly as the
  * reference advances its RngStream. */

@@ -311,3 +311,33 @@ class Checker:
                                  threads, C.byref(run_s), C.byref(init_s), C.byref(chk)),
                "slice_bench")
         return run_s.value, init_s.value, chk.value
+
+
+REF_HARNESS_SO = os.path.join(HERE, "_ref", "libmoshpit_ref_harness.so")
+
+
+class RefHarness:
+    """The unmodified reference harness (trial_rng, run_trial) -- test only."""
+
+    def __init__(self):
+        if not os.path.exists(REF_HARNESS_SO):
+            raise FileNotFoundError(REF_HARNESS_SO)
+        self.lib = C.CDLL(REF_HARNESS_SO)
+        self.lib.refh_trial_seed.restype = u64
+        self.lib.refh_trial_seed.argtypes = [u64, u32, dbl, u32]
+        self.lib.refh_run_trial.restype = C.c_int
+        self.lib.refh_run_trial.argtypes = [u64, u32, dbl, u32, u32, u32, u32, C.c_int, u32, vp,
+                                            vp, vp, vp]
+
+    def trial_seed(self, seed_base, n, p, seed_index):
+        return int(self.lib.refh_trial_seed(seed_base, n, p, seed_index))
+
+    def run_trial(self, seed_base, n, p, seed_index, M, d, dim, init="uniform", round_cap=50):
+        init_d = C.c_double(0)
+        dist, drift = np.zeros(round_cap), np.zeros(round_cap)
+        act = np.zeros(round_cap, dtype=np.uint32)
+        _check(self.lib.refh_run_trial(seed_base, n, p, seed_index, M, d, dim,
+                                       1 if init == "normal" else 0, round_cap, C.byref(init_d),
+                                       _p(dist), _p(drift), _p(act)), "run_trial")
+        return dict(initial_distortion=init_d.value, distortion=dist, mean_drift=drift,
+                    active_counts=act)

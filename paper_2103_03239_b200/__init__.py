@@ -32,6 +32,7 @@ __all__ = [
     "complexity_estimate", "Engine", "fill_synthetic", "InvalidArgument", "OutOfRange",
     "CudaError", "MoshpitError", "device_count", "Shard", "Quadratic", "OptimizerConfig",
     "MembershipEvent", "SgdResult", "AssumptionDiagnostics", "local_step", "run_moshpit_sgd",
+    "run_moshpit_batch", "trial_seed",
 ]
 
 
@@ -361,6 +362,43 @@ def run_moshpit(grid: GridConfig, initial, failure: FailureModel, rng: Rng, roun
                                     _p(act), C.byref(cost), _p(final)))
     return TrialReport(init_d.value, list(dist[:rounds]), list(drift[:rounds]),
                        [int(a) for a in act[:rounds]], cost.value, final)
+
+
+def trial_seed(seed_base: int, protocol: str, n: int, p: float, seed_index: int) -> int:
+    """harness::trial_rng (harness.hpp:145-155) root seed."""
+    return int(lib().moshpit_trial_seed(seed_base, protocol.encode(), n, p, seed_index))
+
+
+def run_moshpit_batch(grid: GridConfig, initial, failure: FailureModel, seeds: Sequence[int],
+                      rounds: int, *, diagnostics: str = "exact",
+                      return_vectors: bool = False) -> List[TrialReport]:
+    """Trial-batched protocols::run_moshpit: ``initial`` is [trials, n, dim];
+    trial t runs with Rng(seeds[t]).  Equal, report by report, to calling
+    run_moshpit per trial -- but one launch per kernel per round for all."""
+    x = np.ascontiguousarray(initial)
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    T, n, dim = x.shape
+    sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+    if len(sd) != T:
+        raise InvalidArgument("run_moshpit_batch: one seed per trial")
+    R = max(rounds, 1)
+    init_d = np.zeros(max(T, 1))
+    dist = np.zeros((max(T, 1), R))
+    drift = np.zeros((max(T, 1), R))
+    act = np.zeros((max(T, 1), R), dtype=np.uint32)
+    cost = np.zeros(max(T, 1))
+    fin = np.zeros_like(x) if return_vectors else None
+    check(lib().moshpit_run_moshpit_batch(_dtype_code(x.dtype), grid.peers_per_axis, grid.dims,
+                                          grid.rounds, T, _p(x), n, dim, failure.p_round, _p(sd),
+                                          rounds, _DIAG[diagnostics], _p(init_d), _p(dist),
+                                          _p(drift), _p(act), _p(cost), _p(fin)))
+    out = []
+    for t in range(T):
+        out.append(TrialReport(float(init_d[t]), list(dist[t, :rounds]), list(drift[t, :rounds]),
+                               [int(a) for a in act[t, :rounds]], float(cost[t]),
+                               None if fin is None else fin[t]))
+    return out
 
 
 def moshpit_average(thetas, grid: GridConfig, rounds: int, stream: RngStream):

@@ -69,6 +69,9 @@ PROTOTYPES = {
     "moshpit_mean_of": (C.c_int, [C.c_int, vp, u64, u64, vp]),
     "moshpit_run_moshpit": (C.c_int, [C.c_int, u32, u32, u32, vp, u64, u64, dbl, u64, u32,
                                       C.c_int, P(dbl), vp, vp, vp, P(dbl), vp]),
+    "moshpit_run_moshpit_batch": (C.c_int, [C.c_int, u32, u32, u32, u32, vp, u64, u64, dbl, vp,
+                                            u32, C.c_int, vp, vp, vp, vp, vp, vp]),
+    "moshpit_trial_seed": (u64, [u64, C.c_char_p, u32, dbl, u32]),
     "moshpit_moshpit_average": (C.c_int, [C.c_int, vp, u64, u64, u32, u32, u32, P(RngState)]),
     "moshpit_local_step_quadratic": (C.c_int, [C.c_int, vp, u64, dbl, dbl, vp, dbl, dbl,
                                                P(RngState)]),

@@ -1,0 +1,277 @@
+// batch.cu -- trial-batched run_moshpit: T independent
+// trials, each exactly protocols::run_moshpit (protocols.hpp:108-179) with its
+// own Rng(seed_t), executed together -- one kernel-1 launch (one CTA per
+// trial), one kernel-2 launch (gridDim.y = trial) and one launch per
+// diagnostic per round for the whole batch.  This is the shape of
+// harness::run_experiment's sweeps (harness.hpp:195-280: thousands of small
+// trials, dim 1 for Table 3), where per-trial launches would be pure overhead.
+// The sequential xoshiro draws of different trials are independent, so the
+// host draws them in parallel threads.
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "pairwise.cuh"
+#include "plane.cuh"
+
+namespace mb200 {
+namespace {
+
+// colmean per trial (blockIdx.y): pairwise over the trial's n rows, fp64.
+template <typename T>
+__global__ void colmean_b(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                          std::uint64_t dim, double* __restrict__ out) {
+  const std::uint64_t j = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  const T* xt = x + (std::uint64_t)blockIdx.y * n * ld;
+  auto ld_fn = [&](std::uint32_t i) -> double { return (double)xt[(std::uint64_t)i * ld + j]; };
+  const double s = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
+                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
+  out[(std::uint64_t)blockIdx.y * dim + j] = __ddiv_rn(s, (double)n);
+}
+
+// per row (all trials): sequential over j (core.hpp:118-122)
+template <typename T>
+__global__ void dist_rows_b(const T* __restrict__ x, std::uint64_t n, std::uint64_t rows,
+                            std::uint64_t ld, std::uint64_t dim, const double* __restrict__ ref,
+                            double* __restrict__ sq) {
+  const std::uint64_t r = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const T* row = x + r * ld;
+  const double* rf = ref + (r / n) * dim;
+  double acc = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double diff = __dsub_rn((double)row[j], rf[j]);
+    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+  }
+  sq[r] = acc;
+}
+
+// per trial: pairwise over its n row sums, / n  (core.hpp:125)
+__global__ void finish_b(const double* __restrict__ sq, std::uint64_t n, std::uint64_t trials,
+                         double* __restrict__ out, std::uint64_t out_stride) {
+  const std::uint64_t t = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (t >= trials) return;
+  const double* s = sq + t * n;
+  auto ld_fn = [&](std::uint32_t i) { return s[i]; };
+  const double v = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
+                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
+  out[t * out_stride] = __ddiv_rn(v, (double)n);
+}
+
+// per trial: drift (protocols.hpp:75-81) in j order
+__global__ void drift_b(const double* __restrict__ mean, const double* __restrict__ ref,
+                        std::uint64_t dim, std::uint64_t trials, double* __restrict__ out,
+                        std::uint64_t out_stride) {
+  const std::uint64_t t = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (t >= trials) return;
+  const double* m = mean + t * dim;
+  const double* r = ref + t * dim;
+  double drift_sq = 0.0, ref_sq = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    const double dm = __dsub_rn(m[j], r[j]);
+    drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
+    ref_sq = __dadd_rn(ref_sq, __dmul_rn(r[j], r[j]));
+  }
+  out[t * out_stride] = __ddiv_rn(__dsqrt_rn(drift_sq), fmax(__dsqrt_rn(ref_sq), 1e-300));
+}
+
+template <typename F>
+void parallel_for(std::uint64_t count, F&& f) {
+  unsigned th = std::max(1u, std::thread::hardware_concurrency());
+  if (count < 4 || th == 1) {
+    for (std::uint64_t i = 0; i < count; ++i) f(i);
+    return;
+  }
+  th = (unsigned)std::min<std::uint64_t>(th, count);
+  std::vector<std::thread> pool;
+  for (unsigned k = 0; k < th; ++k)
+    pool.emplace_back([&, k] {
+      for (std::uint64_t i = k; i < count; i += th) f(i);
+    });
+  for (auto& t : pool) t.join();
+}
+
+template <typename T>
+void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* initial,
+               std::uint64_t n, std::uint64_t dim, double p, const std::uint64_t* seeds,
+               std::uint32_t rounds, int diag, double* init_dist, double* dist, double* drift,
+               std::uint32_t* active, T* final_out) {
+  const std::size_t es = sizeof(T);
+  const Grid grid(M, d);
+  StreamHolder st;
+  const std::uint64_t ld = padded_ld(dim, es), rows = (std::uint64_t)trials * n;
+  std::uint64_t np = 1;
+  while (np < n) np <<= 1;
+  DeviceBuffer x(rows * ld * es + 16), keys(rows * 8), cellb(rows * 8), draws(rows * 9 + 16),
+      members(rows * 4), goff((std::uint64_t)trials * (n + 1) * 4), gvoid(rows), act(rows * 4),
+      counts((std::uint64_t)trials * 16), sidx((std::uint64_t)trials * np * 4), scs(rows * 4),
+      sgi(rows * 4);
+  MB_CUDA(cudaMemcpy2DAsync(x.ptr, ld * es, initial, dim * es, dim * es, rows,
+                            cudaMemcpyHostToDevice, st.s));
+  // host: cells of every trial (protocols.hpp:124-130), in parallel
+  PinnedBuffer hcells, hdraw[2];
+  hcells.resize(rows * 8);
+  std::vector<Xoshiro> fail(trials), clock(trials);
+  parallel_for(trials, [&](std::uint64_t t) {
+    Xoshiro cs = Xoshiro::named(seeds[t], "cells");
+    const auto c = draw_cells(cs, grid.capacity, n);
+    std::memcpy(hcells.as<std::uint64_t>() + t * n, c.data(), n * 8);
+    fail[t] = Xoshiro::named(seeds[t], "failures");
+    clock[t] = Xoshiro::named(seeds[t], "priorities");
+  });
+  MB_CUDA(cudaMemcpyAsync(cellb.ptr, hcells.ptr, rows * 8, cudaMemcpyHostToDevice, st.s));
+  launch_initial_keys(cellb.as<std::uint64_t>(), keys.as<std::uint64_t>(), rows, M, d, st.s);
+  const bool dg = diag != MOSHPIT_DIAG_NONE;
+  DeviceBuffer ref, mean, sq, out;
+  const unsigned cb = 128;
+  const dim3 cgrid((unsigned)((dim + cb - 1) / cb), trials);
+  if (dg) {
+    ref.resize((std::uint64_t)trials * dim * 8 + 16);
+    mean.resize((std::uint64_t)trials * dim * 8 + 16);
+    sq.resize(rows * 8 + 16);
+    out.resize((std::uint64_t)trials * (2 * rounds + 1) * 8 + 16);
+    if (dim) colmean_b<T><<<cgrid, cb, 0, st.s>>>(x.as<T>(), n, ld, dim, ref.as<double>());
+    dist_rows_b<T><<<(unsigned)((rows + 127) / 128), 128, 0, st.s>>>(x.as<T>(), n, rows, ld, dim,
+                                                                     ref.as<double>(),
+                                                                     sq.as<double>());
+    finish_b<<<(trials + 127) / 128, 128, 0, st.s>>>(sq.as<double>(), n, trials,
+                                                     out.as<double>(), 2 * rounds + 1);
+    MB_LAUNCH_CHECK();
+  }
+  cudaEvent_t ev[2];
+  for (auto& e : ev) MB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  std::vector<std::uint32_t> act_h((std::uint64_t)trials * rounds);
+  for (std::uint32_t r = 0; r < rounds; ++r) {
+    PinnedBuffer& hd = hdraw[r & 1];
+    if (r >= 2) MB_CUDA(cudaEventSynchronize(ev[r & 1]));
+    hd.resize(rows * 9 + 16);
+    auto* ts = hd.as<std::uint64_t>();
+    auto* failed = reinterpret_cast<std::uint8_t*>(ts + rows);
+    parallel_for(trials, [&](std::uint64_t t) {  // protocols.hpp:143-150, per trial
+      std::uint8_t* f = failed + t * n;
+      std::memset(f, 0, n);
+      std::uint32_t a = 0;
+      if (p > 0.0)
+        for (std::uint64_t i = 0; i < n; ++i) f[i] = fail[t].bernoulli(p) ? 1 : 0;
+      for (std::uint64_t i = 0; i < n; ++i) a += f[i] == 0;
+      for (std::uint64_t i = 0; i < n; ++i) ts[t * n + i] = clock[t].next() >> 16;
+      act_h[t * rounds + r] = a;
+    });
+    MB_CUDA(cudaMemcpyAsync(draws.ptr, hd.ptr, rows * 9, cudaMemcpyHostToDevice, st.s));
+    MB_CUDA(cudaEventRecord(ev[r & 1], st.s));
+    GroupArgs a;
+    a.n = static_cast<std::uint32_t>(n);
+    a.cap = M;
+    a.M = M;
+    a.pow_drop = grid.pow_drop;
+    a.advance_keys = 1;
+    a.klen_zero = grid.klen == 0;
+    a.keys = keys.as<std::uint64_t>();
+    a.ts = draws.as<std::uint64_t>();
+    a.failed = draws.as<std::uint8_t>() + rows * 8;
+    a.members = members.as<std::uint32_t>();
+    a.goff = goff.as<std::uint32_t>();
+    a.gvoid = gvoid.as<std::uint8_t>();
+    a.act = act.as<std::uint32_t>();
+    a.counts = counts.as<std::uint32_t>();
+    a.sidx = sidx.as<std::uint32_t>();
+    a.scs = scs.as<std::uint32_t>();
+    a.sgi = sgi.as<std::uint32_t>();
+    a.batch = trials;
+    launch_form_groups(a, true, st.s);
+    launch_group_mean_batch<T>(x.as<T>(), n * ld, ld, dim, (std::uint32_t)n, trials, a.members,
+                               a.goff, a.act, a.counts, st.s);
+    if (dg) {
+      dist_rows_b<T><<<(unsigned)((rows + 127) / 128), 128, 0, st.s>>>(
+          x.as<T>(), n, rows, ld, dim, ref.as<double>(), sq.as<double>());
+      finish_b<<<(trials + 127) / 128, 128, 0, st.s>>>(sq.as<double>(), n, trials,
+                                                       out.as<double>() + 1 + r, 2 * rounds + 1);
+      if (dim) colmean_b<T><<<cgrid, cb, 0, st.s>>>(x.as<T>(), n, ld, dim, mean.as<double>());
+      drift_b<<<(trials + 127) / 128, 128, 0, st.s>>>(mean.as<double>(), ref.as<double>(), dim,
+                                                      trials, out.as<double>() + 1 + rounds + r,
+                                                      2 * rounds + 1);
+      MB_LAUNCH_CHECK();
+    }
+  }
+  std::vector<double> h;
+  if (dg) {
+    h.resize((std::uint64_t)trials * (2 * rounds + 1));
+    MB_CUDA(cudaMemcpyAsync(h.data(), out.ptr, h.size() * 8, cudaMemcpyDeviceToHost, st.s));
+  }
+  if (final_out)
+    MB_CUDA(cudaMemcpy2DAsync(final_out, dim * es, x.ptr, ld * es, dim * es, rows,
+                              cudaMemcpyDeviceToHost, st.s));
+  MB_CUDA(cudaStreamSynchronize(st.s));
+  for (auto& e : ev) cudaEventDestroy(e);
+  const double nan = std::nan("");
+  for (std::uint64_t t = 0; t < trials; ++t) {
+    const std::uint64_t o = t * (2 * rounds + 1);
+    init_dist[t] = dg ? h[o] : nan;
+    for (std::uint32_t r = 0; r < rounds; ++r) {
+      dist[t * rounds + r] = dg ? h[o + 1 + r] : nan;
+      drift[t * rounds + r] = dg ? h[o + 1 + rounds + r] : nan;
+      active[t * rounds + r] = act_h[t * rounds + r];
+    }
+  }
+}
+
+}  // namespace
+}  // namespace mb200
+
+using namespace mb200;
+
+extern "C" {
+
+// Trial-batched protocols::run_moshpit: trial t uses initial + t*n*dim and
+// Rng(seeds[t]); report arrays are [trials] / [trials][rounds].  Diagnostics
+// are computed in the reference order (EXACT) unless diag == NONE.
+int moshpit_run_moshpit_batch(int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T,
+                              std::uint32_t trials, const void* initial, std::uint64_t n,
+                              std::uint64_t dim, double p_round, const std::uint64_t* seeds,
+                              std::uint32_t rounds, int diag, double* initial_distortion,
+                              double* distortion, double* mean_drift,
+                              std::uint32_t* active_counts, double* cost_units,
+                              void* final_out) {
+  return guarded([&] {
+    elem_size(dtype);
+    if (M < 1 || d < 1 || T < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (p_round < 0.0 || p_round > 1.0)
+      throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
+    if (n == 0) throw std::invalid_argument("run_moshpit: no peers");
+    if (n > moshpit_grid_capacity(M, d))
+      throw std::invalid_argument("run_moshpit: N exceeds grid capacity M^d");
+    if (n > 8192) throw std::invalid_argument("run_moshpit_batch: at most 8192 peers per trial");
+    if (diag < MOSHPIT_DIAG_NONE || diag > MOSHPIT_DIAG_EXACT)
+      throw std::invalid_argument("run_moshpit: unknown diagnostics mode");
+    if (trials > 65535) throw std::invalid_argument("run_moshpit_batch: at most 65535 trials");
+    if (trials == 0) return;
+    require_device();
+    if (dtype == MOSHPIT_F32)
+      run_batch<float>(M, d, trials, static_cast<const float*>(initial), n, dim, p_round, seeds,
+                       rounds, diag, initial_distortion, distortion, mean_drift, active_counts,
+                       static_cast<float*>(final_out));
+    else
+      run_batch<double>(M, d, trials, static_cast<const double*>(initial), n, dim, p_round,
+                        seeds, rounds, diag, initial_distortion, distortion, mean_drift,
+                        active_counts, static_cast<double*>(final_out));
+    const double c = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
+                                                 static_cast<std::uint32_t>(dim));
+    for (std::uint32_t t = 0; t < trials; ++t) cost_units[t] = c;
+  });
+}
+
+// harness.hpp:145-155 trial_rng: the per-trial root seed of a sweep cell.
+std::uint64_t moshpit_trial_seed(std::uint64_t seed_base, const char* protocol,
+                                 std::uint32_t n, double p, std::uint32_t seed_index) {
+  std::uint64_t p_bits;
+  std::memcpy(&p_bits, &p, sizeof(p));
+  std::uint64_t mix = seed_base ^ fnv1a(protocol);
+  mix = splitmix64(mix) ^ n;
+  mix = splitmix64(mix) ^ p_bits;
+  mix = splitmix64(mix) ^ seed_index;
+  return splitmix64(mix);
+}
+
+}  // extern "C"

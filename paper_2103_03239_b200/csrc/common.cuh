@@ -238,10 +238,22 @@ struct GroupArgs {
   std::uint32_t* sidx = nullptr;  // [pow2(n)]
   std::uint32_t* scs = nullptr;   // [n]
   std::uint32_t* sgi = nullptr;   // [n]
+  // trial batching (moshpit_run_moshpit_batch): CTA b works on trial b; every
+  // per-peer array above is [batch][n] (goff [batch][n+1], counts [batch][4],
+  // sidx [batch][pow2(n)]).  0 = a single trial.
+  std::uint32_t batch = 0;
 };
 
 std::size_t group_smem_bytes(std::uint32_t n, bool packed);
 void launch_form_groups(const GroupArgs& a, bool packed, cudaStream_t s);
+// Batched kernel 2: trial t (= gridDim.y) reads state + t*state_stride and its
+// own tables at members/act + t*n, goff + t*(n+1), counts + t*4.
+template <typename T>
+void launch_group_mean_batch(T* state, std::uint64_t state_stride, std::uint64_t ld,
+                             std::uint64_t dim, std::uint32_t n, std::uint32_t trials,
+                             const std::uint32_t* members, const std::uint32_t* goff,
+                             const std::uint32_t* act, const std::uint32_t* counts,
+                             cudaStream_t s);
 void launch_initial_keys(const std::uint64_t* cells, std::uint64_t* keys,
                          std::uint64_t n, std::uint32_t M, std::uint32_t d,
                          cudaStream_t s);

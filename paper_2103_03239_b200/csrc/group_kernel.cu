@@ -92,6 +92,25 @@ template <class View>
 __global__ void __launch_bounds__(kThreads, 1)
     form_groups_kernel(GroupArgs a, View view, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (a.batch) {  // CTA b handles trial b of a batch
+    const std::uint64_t t = blockIdx.x, n = a.n;
+    std::uint64_t np = 1;
+    while (np < n) np <<= 1;
+    a.keys += t * n;
+    a.ts += t * n;
+    if (a.failed) a.failed += t * n;
+    a.members += t * n;
+    a.goff += t * (n + 1);
+    a.gvoid += t * n;
+    if (a.rank) a.rank += t * n;
+    if (a.act) a.act += t * n;
+    if (a.counts) a.counts += t * 4;
+    a.totals = nullptr;
+    a.sidx += t * np;
+    a.scs += t * n;
+    a.sgi += t * n;
+    if constexpr (std::is_same_v<View, PackedView>) view.key = a.keys;
+  }
   const std::uint32_t n = a.n;
   const std::uint32_t np = pow2_ceil(n);
   const std::uint32_t tid = threadIdx.x;
@@ -271,7 +290,7 @@ void launch_form_groups(const GroupArgs& a, bool packed, cudaStream_t s) {
     if (dyn > 48 * 1024)
       MB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)dyn));
-    k<<<1, kThreads, dyn, s>>>(a, PackedView{a.keys}, use_smem);
+    k<<<a.batch ? a.batch : 1, kThreads, dyn, s>>>(a, PackedView{a.keys}, use_smem);
   } else {
     auto* k = form_groups_kernel<DigitView>;
     if (dyn > 48 * 1024)

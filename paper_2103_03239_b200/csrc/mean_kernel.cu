@@ -103,6 +103,8 @@ struct MeanArgs {
   const std::uint32_t* goff;
   const std::uint32_t* act;
   const std::uint32_t* counts;  // [1] = number of active groups
+  std::uint64_t batch_state_stride;  // trial batching: state elements per trial
+  std::uint32_t batch_n;             // peers per trial (0: no batching)
 };
 
 // Kernel 3 prologue (optimizer.hpp:356-373): g = c*(theta-t) [+ nj]; the
@@ -174,6 +176,14 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
   using V = typename V16<T>::type;
   double nsq = 0.0;
   bool bad = false;
+  if (a.batch_n) {  // trial = blockIdx.y
+    const std::uint64_t t = blockIdx.y, n = a.batch_n;
+    a.state += t * a.batch_state_stride;
+    a.members += t * n;
+    a.goff += t * (n + 1);
+    a.act += t * n;
+    a.counts += t * 4;
+  }
   __shared__ std::uint32_t sids[kMaxSmemIds];
   const std::uint32_t n_act = a.counts[1];
   const std::uint64_t n_items = (std::uint64_t)n_act * a.n_tiles;
@@ -450,6 +460,8 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
   a.goff = goff;
   a.act = act;
   a.counts = counts;
+  a.batch_state_stride = 0;
+  a.batch_n = 0;
   if (step) {
     a.step = *step;
     group_mean_register<T, true><<<mean_grid<T, true>(), kThreads, 0, s>>>(a);
@@ -518,6 +530,57 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
   }
   MB_LAUNCH_CHECK();
 }
+
+template <typename T>
+void launch_group_mean_batch(T* state, std::uint64_t state_stride, std::uint64_t ld,
+                             std::uint64_t dim, std::uint32_t n, std::uint32_t trials,
+                             const std::uint32_t* members, const std::uint32_t* goff,
+                             const std::uint32_t* act, const std::uint32_t* counts,
+                             cudaStream_t s) {
+  if (dim == 0 || trials == 0) return;
+  constexpr int kVec = V16<T>::kN;
+  MeanArgs<T> a;
+  a.state = state;
+  a.ld_vec = ld / kVec;
+  a.nvec = (dim + kVec - 1) / kVec;
+  a.n_tiles = (a.nvec + kThreads - 1) / kThreads;
+  a.members = members;
+  a.goff = goff;
+  a.act = act;
+  a.counts = counts;
+  a.batch_state_stride = state_stride;
+  a.batch_n = n;
+  // per trial: at most n groups x n_tiles items; spread ~2 waves of CTAs
+  int sms = 0, dev = 0;
+  MB_CUDA(cudaGetDevice(&dev));
+  MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  std::uint64_t gx = ((std::uint64_t)sms * 2 + trials - 1) / trials;
+  const std::uint64_t items = (std::uint64_t)n * a.n_tiles;
+  if (gx > items) gx = items;
+  if (gx < 1) gx = 1;
+  for (std::uint32_t t0 = 0; t0 < trials; t0 += 65535) {
+    const std::uint32_t tb = trials - t0 < 65535 ? trials - t0 : 65535;
+    MeanArgs<T> b = a;
+    b.state += (std::uint64_t)t0 * state_stride;
+    b.members += (std::uint64_t)t0 * n;
+    b.goff += (std::uint64_t)t0 * (n + 1);
+    b.act += (std::uint64_t)t0 * n;
+    b.counts += (std::uint64_t)t0 * 4;
+    group_mean_register<T, false><<<dim3((unsigned)gx, tb), kThreads, 0, s>>>(b);
+    MB_LAUNCH_CHECK();
+  }
+}
+
+template void launch_group_mean_batch<float>(float*, std::uint64_t, std::uint64_t,
+                                             std::uint64_t, std::uint32_t, std::uint32_t,
+                                             const std::uint32_t*, const std::uint32_t*,
+                                             const std::uint32_t*, const std::uint32_t*,
+                                             cudaStream_t);
+template void launch_group_mean_batch<double>(double*, std::uint64_t, std::uint64_t,
+                                              std::uint64_t, std::uint32_t, std::uint32_t,
+                                              const std::uint32_t*, const std::uint32_t*,
+                                              const std::uint32_t*, const std::uint32_t*,
+                                              cudaStream_t);
 
 template void launch_group_mean<float>(float*, std::uint64_t, std::uint64_t,
                                        const std::uint32_t*, const std::uint32_t*,

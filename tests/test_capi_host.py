@@ -177,3 +177,13 @@ def test_compute_without_device_fails_loudly(mb):
         mb.group_mean([[1.0, 2.0], [3.0, 6.0]])
     with pytest.raises(mb.CudaError):
         mb.run_moshpit(mb.GridConfig(3, 2, 1), np.ones((9, 2)), mb.FailureModel(), mb.Rng(1), 2)
+
+
+def test_trial_seed_matches_reference_harness(mb):
+    from oracle.oracle import REF_HARNESS_SO, RefHarness
+    if not os.path.exists(REF_HARNESS_SO):
+        pytest.skip("reference harness shim not built")
+    h = RefHarness()
+    for n, p, k in [(1024, 0.0, 0), (768, 0.005, 17), (512, 0.01, 99), (900, 1e-3, 3)]:
+        assert mb.trial_seed(0, "moshpit", n, p, k) == h.trial_seed(0, n, p, k)
+        assert mb.trial_seed(12345, "moshpit", n, p, k) == h.trial_seed(12345, n, p, k)
