@@ -103,24 +103,25 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
   const std::uint64_t ld = padded_ld(dim, es), rows = (std::uint64_t)trials * n;
   std::uint64_t np = 1;
   while (np < n) np <<= 1;
-  DeviceBuffer x(rows * ld * es + 16), keys(rows * 8), cellb(rows * 8), draws(rows * 9 + 16),
+  DeviceBuffer x(rows * ld * es + 16), keys(rows * 8), cellb(rows * 8),
       members(rows * 4), goff((std::uint64_t)trials * (n + 1) * 4), gvoid(rows), act(rows * 4),
       counts((std::uint64_t)trials * 16), sidx((std::uint64_t)trials * np * 4), scs(rows * 4),
       sgi(rows * 4);
   MB_CUDA(cudaMemcpy2DAsync(x.ptr, ld * es, initial, dim * es, dim * es, rows,
                             cudaMemcpyHostToDevice, st.s));
   // host: cells of every trial (protocols.hpp:124-130), in parallel
-  PinnedBuffer hcells, hdraw[2];
-  hcells.resize(rows * 8);
+  // one-shot staging: pageable memory (a cudaMallocHost per call costs more
+  // than the copy it would speed up, and serialises concurrent callers)
+  std::vector<std::uint64_t> hcells(rows);
   std::vector<Xoshiro> fail(trials), clock(trials);
   parallel_for(trials, [&](std::uint64_t t) {
     Xoshiro cs = Xoshiro::named(seeds[t], "cells");
     const auto c = draw_cells(cs, grid.capacity, n);
-    std::memcpy(hcells.as<std::uint64_t>() + t * n, c.data(), n * 8);
+    std::memcpy(hcells.data() + t * n, c.data(), n * 8);
     fail[t] = Xoshiro::named(seeds[t], "failures");
     clock[t] = Xoshiro::named(seeds[t], "priorities");
   });
-  MB_CUDA(cudaMemcpyAsync(cellb.ptr, hcells.ptr, rows * 8, cudaMemcpyHostToDevice, st.s));
+  MB_CUDA(cudaMemcpyAsync(cellb.ptr, hcells.data(), rows * 8, cudaMemcpyHostToDevice, st.s));
   launch_initial_keys(cellb.as<std::uint64_t>(), keys.as<std::uint64_t>(), rows, M, d, st.s);
   const bool dg = diag != MOSHPIT_DIAG_NONE;
   DeviceBuffer ref, mean, sq, out;
@@ -139,27 +140,36 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
                                                      out.as<double>(), 2 * rounds + 1);
     MB_LAUNCH_CHECK();
   }
-  cudaEvent_t ev[2];
-  for (auto& e : ev) MB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // All rounds' draws up front (protocols.hpp:143-150, per trial in parallel),
+  // in blocks of rounds that keep the pinned staging under ~256 MB; the GPU
+  // then runs the block's rounds back to back with no host synchronisation.
   std::vector<std::uint32_t> act_h((std::uint64_t)trials * rounds);
-  for (std::uint32_t r = 0; r < rounds; ++r) {
-    PinnedBuffer& hd = hdraw[r & 1];
-    if (r >= 2) MB_CUDA(cudaEventSynchronize(ev[r & 1]));
-    hd.resize(rows * 9 + 16);
-    auto* ts = hd.as<std::uint64_t>();
-    auto* failed = reinterpret_cast<std::uint8_t*>(ts + rows);
-    parallel_for(trials, [&](std::uint64_t t) {  // protocols.hpp:143-150, per trial
-      std::uint8_t* f = failed + t * n;
-      std::memset(f, 0, n);
-      std::uint32_t a = 0;
-      if (p > 0.0)
-        for (std::uint64_t i = 0; i < n; ++i) f[i] = fail[t].bernoulli(p) ? 1 : 0;
-      for (std::uint64_t i = 0; i < n; ++i) a += f[i] == 0;
-      for (std::uint64_t i = 0; i < n; ++i) ts[t * n + i] = clock[t].next() >> 16;
-      act_h[t * rounds + r] = a;
+  const std::uint64_t per_round = rows * 9;
+  std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (256ull << 20) / per_round);
+  if (rb > rounds) rb = rounds ? rounds : 1;
+  DeviceBuffer dblock(per_round * rb + 16);
+  std::vector<std::uint8_t> hd;
+  for (std::uint32_t r0 = 0; r0 < rounds; r0 += rb) {
+    const std::uint32_t nr = std::min(rb, rounds - r0);
+    MB_CUDA(cudaStreamSynchronize(st.s));  // staging reuse
+    hd.resize(per_round * rb + 16);
+    parallel_for(trials, [&](std::uint64_t t) {
+      for (std::uint32_t q = 0; q < nr; ++q) {
+        auto* ts = reinterpret_cast<std::uint64_t*>(hd.data() + q * per_round);
+        std::uint8_t* f = reinterpret_cast<std::uint8_t*>(ts + rows) + t * n;
+        std::memset(f, 0, n);
+        std::uint32_t act_n = 0;
+        if (p > 0.0)
+          for (std::uint64_t i = 0; i < n; ++i) f[i] = fail[t].bernoulli(p) ? 1 : 0;
+        for (std::uint64_t i = 0; i < n; ++i) act_n += f[i] == 0;
+        for (std::uint64_t i = 0; i < n; ++i) ts[t * n + i] = clock[t].next() >> 16;
+        act_h[t * rounds + r0 + q] = act_n;
+      }
     });
-    MB_CUDA(cudaMemcpyAsync(draws.ptr, hd.ptr, rows * 9, cudaMemcpyHostToDevice, st.s));
-    MB_CUDA(cudaEventRecord(ev[r & 1], st.s));
+    MB_CUDA(cudaMemcpyAsync(dblock.ptr, hd.data(), per_round * nr, cudaMemcpyHostToDevice, st.s));
+    for (std::uint32_t q = 0; q < nr; ++q) {
+    const std::uint32_t r = r0 + q;
+    std::uint8_t* draws_r = dblock.as<std::uint8_t>() + q * per_round;
     GroupArgs a;
     a.n = static_cast<std::uint32_t>(n);
     a.cap = M;
@@ -168,8 +178,8 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     a.advance_keys = 1;
     a.klen_zero = grid.klen == 0;
     a.keys = keys.as<std::uint64_t>();
-    a.ts = draws.as<std::uint64_t>();
-    a.failed = draws.as<std::uint8_t>() + rows * 8;
+    a.ts = reinterpret_cast<std::uint64_t*>(draws_r);
+    a.failed = draws_r + rows * 8;
     a.members = members.as<std::uint32_t>();
     a.goff = goff.as<std::uint32_t>();
     a.gvoid = gvoid.as<std::uint8_t>();
@@ -193,6 +203,7 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
                                                       2 * rounds + 1);
       MB_LAUNCH_CHECK();
     }
+    }
   }
   std::vector<double> h;
   if (dg) {
@@ -203,7 +214,6 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     MB_CUDA(cudaMemcpy2DAsync(final_out, dim * es, x.ptr, ld * es, dim * es, rows,
                               cudaMemcpyDeviceToHost, st.s));
   MB_CUDA(cudaStreamSynchronize(st.s));
-  for (auto& e : ev) cudaEventDestroy(e);
   const double nan = std::nan("");
   for (std::uint64_t t = 0; t < trials; ++t) {
     const std::uint64_t o = t * (2 * rounds + 1);
