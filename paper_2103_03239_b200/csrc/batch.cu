@@ -144,7 +144,9 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
   // in blocks of rounds that keep the pinned staging under ~256 MB; the GPU
   // then runs the block's rounds back to back with no host synchronisation.
   std::vector<std::uint32_t> act_h((std::uint64_t)trials * rounds);
-  const std::uint64_t per_round = rows * 9;
+  // per-round block: ts u64[rows] then failed u8[rows], padded to 16 bytes so
+  // every block's timestamps stay 8-byte aligned
+  const std::uint64_t per_round = (rows * 9 + 15) / 16 * 16;
   std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (256ull << 20) / per_round);
   if (rb > rounds) rb = rounds ? rounds : 1;
   DeviceBuffer dblock(per_round * rb + 16);
