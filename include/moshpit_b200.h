@@ -182,6 +182,37 @@ int moshpit_run_moshpit_sgd_quadratic(
 /* loop_ms (nullable): device time of the step loop (CUDA events on the call's
  * stream; excludes setup and the final copies). */
 
+/* ---- optimizer.hpp:75-146 LogisticRegression ----------------------------
+ * Dataset: xs [samples x dim] row-major fp64, ys [samples] in {-1, +1}.
+ * moshpit_logistic_synthetic replaces LogisticRegression::synthetic
+ * (optimizer.hpp:89-104): draws from *stream exactly as the reference (host).
+ * moshpit_logistic_eval replaces value()/gradient()/smoothness()
+ * (optimizer.hpp:106-140) [GPU; value and gradient in the reference's
+ * summation orders, exp/log1p from CUDA's libdevice -- see DESIGN.md]. */
+int moshpit_logistic_synthetic(uint64_t dim, uint64_t samples,
+                               moshpit_rng_state* stream, double* xs, double* ys);
+int moshpit_logistic_eval(const double* xs, const double* ys, uint64_t samples,
+                          uint64_t dim, double l2, const double* theta,
+                          double* value, double* grad, double* smoothness);
+/* optimizer.hpp:231-242 local_step with LogisticRegression [GPU]. */
+int moshpit_local_step_logistic(int dtype, void* theta, uint64_t dim,
+                                const double* xs, const double* ys,
+                                uint64_t samples, double l2, double gamma,
+                                double sigma, moshpit_rng_state* noise);
+/* optimizer.hpp:297-439 run_moshpit_sgd with LogisticRegression(xs, ys, l2)
+ * [GPU]: arguments and outputs as moshpit_run_moshpit_sgd_quadratic.  diag
+ * NONE skips the per-step diagnostics (NaN); FAST and EXACT both evaluate
+ * them in the reference's order.  mu = l2 (strong_convexity, :141). */
+int moshpit_run_moshpit_sgd_logistic(
+    int dtype, uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers,
+    uint64_t dim, const double* xs, const double* ys, uint64_t samples,
+    double l2, const double* theta0, double gamma, uint32_t tau,
+    uint32_t steps, double sigma, uint32_t inner_rounds, uint64_t seed,
+    const uint32_t* ev_step, const int32_t* ev_delta, uint64_t n_events,
+    int diag, int noise_mode, double* f_gap, double* grad_norm_sq,
+    double* f_gap_weighted, double* dispersion, double* final_mean,
+    double* diag6, void* final_thetas, double* loop_ms);
+
 /* ---- device-resident engine (the performance boundary) -----------------
  * One engine = one trial's integer plane (grid, keys, rng streams, group
  * tables) resident on `device`.  The peer state is caller-owned device

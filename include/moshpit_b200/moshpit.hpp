@@ -447,6 +447,60 @@ class Quadratic final : public Objective {
   double l_, mu_;
 };
 
+// optimizer.hpp:75-146.  value()/gradient() evaluate on the GPU (the
+// reference's summation orders; libdevice exp/log1p), smoothness() is the
+// constructor's trace bound, synthetic() draws the reference's dataset.
+class LogisticRegression final : public Objective {
+ public:
+  LogisticRegression(std::vector<ParamVector> xs, std::vector<double> ys, double l2)
+      : ys_(std::move(ys)), l2_(l2) {
+    if (xs.empty() || xs.size() != ys_.size())
+      throw std::invalid_argument("LogisticRegression: bad dataset");
+    dim_ = xs.front().size();
+    flat_.reserve(xs.size() * dim_);
+    for (const auto& x : xs) {
+      if (x.size() != dim_) throw std::invalid_argument("LogisticRegression: ragged dataset");
+      flat_.insert(flat_.end(), x.begin(), x.end());
+    }
+    b200::check(moshpit_logistic_eval(flat_.data(), ys_.data(), ys_.size(), dim_, l2_, nullptr,
+                                      nullptr, nullptr, &l_));
+  }
+  static LogisticRegression synthetic(std::size_t dim, std::size_t samples, double l2,
+                                      RngStream& stream) {
+    std::vector<double> flat(samples * dim), ys(samples);
+    b200::check(moshpit_logistic_synthetic(dim, samples, &stream.state(), flat.data(), ys.data()));
+    std::vector<ParamVector> xs(samples);
+    for (std::size_t i = 0; i < samples; ++i)
+      xs[i].assign(flat.begin() + i * dim, flat.begin() + (i + 1) * dim);
+    return LogisticRegression(std::move(xs), std::move(ys), l2);
+  }
+  double value(const ParamVector& theta) const override {
+    double v = 0.0;
+    b200::check(moshpit_logistic_eval(flat_.data(), ys_.data(), ys_.size(), dim_, l2_,
+                                      theta.data(), &v, nullptr, nullptr));
+    return v;
+  }
+  ParamVector gradient(const ParamVector& theta) const override {
+    ParamVector g(dim_);
+    b200::check(moshpit_logistic_eval(flat_.data(), ys_.data(), ys_.size(), dim_, l2_,
+                                      theta.data(), nullptr, g.data(), nullptr));
+    return g;
+  }
+  std::size_t dim() const override { return dim_; }
+  double smoothness() const override { return l_; }
+  double strong_convexity() const override { return l2_; }
+  // B200 extension: the row-major samples x dim dataset and labels.
+  const std::vector<double>& flat_xs() const { return flat_; }
+  const std::vector<double>& ys() const { return ys_; }
+  double l2() const { return l2_; }
+
+ private:
+  std::vector<double> flat_;
+  std::vector<double> ys_;
+  std::size_t dim_ = 0;
+  double l2_, l_ = 0.0;
+};
+
 struct OptimizerConfig {
   double gamma = 0.1;
   std::uint32_t tau = 1;
@@ -491,7 +545,9 @@ struct SgdResult {
 namespace b200_detail {
 inline const Quadratic& as_quadratic(const Objective& o) {
   const auto* q = dynamic_cast<const Quadratic*>(&o);
-  if (!q) throw std::invalid_argument("B200 optimizer path: only the Quadratic objective");
+  if (!q)
+    throw std::invalid_argument(
+        "B200 optimizer path: Quadratic and LogisticRegression objectives only");
   return *q;
 }
 inline double quad_l(const Quadratic& q) { return q.smoothness(); }
@@ -501,6 +557,13 @@ inline double quad_mu(const Quadratic& q) { return q.strong_convexity(); }
 // GPU, noise from the caller's stream (optimizer.hpp:231-242).
 inline void local_step(ParamVector& theta, const Objective& objective, double gamma, double sigma,
                        RngStream& noise) {
+  if (const auto* lr = dynamic_cast<const LogisticRegression*>(&objective)) {
+    b200::check(moshpit_local_step_logistic(MOSHPIT_F64, theta.data(), theta.size(),
+                                            lr->flat_xs().data(), lr->ys().data(),
+                                            lr->ys().size(), lr->l2(), gamma, sigma,
+                                            &noise.state()));
+    return;
+  }
   const Quadratic& q = b200_detail::as_quadratic(objective);
   b200::check(moshpit_local_step_quadratic(MOSHPIT_F64, theta.data(), theta.size(), q.smoothness(),
                                            q.strong_convexity(), q.optimum().data(), gamma, sigma,
@@ -515,7 +578,8 @@ inline SgdResult run_moshpit_sgd(const OptimizerConfig& config, const Objective&
   config.validate();
   if (theta0.size() != objective.dim())
     throw std::invalid_argument("run_moshpit_sgd: theta0 dimension mismatch");
-  const Quadratic& q = b200_detail::as_quadratic(objective);
+  const auto* lr = dynamic_cast<const LogisticRegression*>(&objective);
+  const Quadratic* q = lr ? nullptr : &b200_detail::as_quadratic(objective);
   std::vector<std::uint32_t> st;
   std::vector<std::int32_t> dl;
   for (const auto& e : schedule) {
@@ -530,13 +594,24 @@ inline SgdResult run_moshpit_sgd(const OptimizerConfig& config, const Objective&
   r.diagnostics.dispersion.resize(K);
   r.final_mean.resize(theta0.size());
   double d6[6] = {0, 0, 0, 0, 0, 0};
-  b200::check(moshpit_run_moshpit_sgd_quadratic(
-      MOSHPIT_F64, config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
-      config.n_peers, theta0.size(), q.smoothness(), q.strong_convexity(), q.optimum().data(),
-      theta0.data(), config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds,
-      rng.seed(), st.empty() ? nullptr : st.data(), dl.empty() ? nullptr : dl.data(), st.size(),
-      MOSHPIT_DIAG_EXACT, 0, r.f_gap.data(), r.grad_norm_sq.data(), r.f_gap_weighted.data(),
-      r.diagnostics.dispersion.data(), r.final_mean.data(), d6, nullptr, nullptr));
+  if (lr)
+    b200::check(moshpit_run_moshpit_sgd_logistic(
+        MOSHPIT_F64, config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
+        config.n_peers, theta0.size(), lr->flat_xs().data(), lr->ys().data(), lr->ys().size(),
+        lr->l2(), theta0.data(), config.gamma, config.tau, config.steps, config.sigma,
+        config.inner_rounds, rng.seed(), st.empty() ? nullptr : st.data(),
+        dl.empty() ? nullptr : dl.data(), st.size(), MOSHPIT_DIAG_EXACT, 0, r.f_gap.data(),
+        r.grad_norm_sq.data(), r.f_gap_weighted.data(), r.diagnostics.dispersion.data(),
+        r.final_mean.data(), d6, nullptr, nullptr));
+  else
+    b200::check(moshpit_run_moshpit_sgd_quadratic(
+        MOSHPIT_F64, config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
+        config.n_peers, theta0.size(), q->smoothness(), q->strong_convexity(),
+        q->optimum().data(), theta0.data(), config.gamma, config.tau, config.steps,
+        config.sigma, config.inner_rounds, rng.seed(), st.empty() ? nullptr : st.data(),
+        dl.empty() ? nullptr : dl.data(), st.size(), MOSHPIT_DIAG_EXACT, 0, r.f_gap.data(),
+        r.grad_norm_sq.data(), r.f_gap_weighted.data(), r.diagnostics.dispersion.data(),
+        r.final_mean.data(), d6, nullptr, nullptr));
   r.diagnostics.delta_aq_hat = d6[0];
   r.diagnostics.sigma_hat = d6[1];
   r.diagnostics.delta_pv1_hat = d6[2];

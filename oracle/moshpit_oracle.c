@@ -443,3 +443,146 @@ int orc_moshpit_trace(uint32_t M, uint32_t d, uint64_t n, double p,
 #include "oracle_real.inc"
 #undef REAL
 #undef SFX
+
+/* ------------------------------------------------------------------------ */
+/* LogisticRegression (optimizer.hpp:75-146), fp64                          */
+/* ------------------------------------------------------------------------ */
+
+/* optimizer.hpp:89-104 synthetic(dim, samples, l2, stream) */
+void orc_logistic_synthetic(uint64_t dim, uint64_t samples, orc_rng* st, double* xs,
+                            double* ys) {
+  double* truth = (double*)malloc((dim ? dim : 1) * sizeof(double));
+  for (uint64_t j = 0; j < dim; ++j) truth[j] = orc_rng_normal(st);
+  for (uint64_t i = 0; i < samples; ++i) {
+    double dot = 0.0;
+    for (uint64_t j = 0; j < dim; ++j) {
+      xs[i * dim + j] = orc_rng_normal(st);
+      dot += xs[i * dim + j] * truth[j];
+    }
+    ys[i] = dot + 0.1 * orc_rng_normal(st) > 0.0 ? 1.0 : -1.0;
+  }
+  free(truth);
+}
+
+/* optimizer.hpp:106-120 */
+double orc_logistic_value(const double* xs, const double* ys, uint64_t samples, uint64_t dim,
+                          double l2, const double* th) {
+  double f = 0.0;
+  for (uint64_t i = 0; i < samples; ++i) {
+    double margin = 0.0;
+    for (uint64_t j = 0; j < dim; ++j) margin += xs[i * dim + j] * th[j];
+    margin *= ys[i];
+    f += margin > 0.0 ? log1p(exp(-margin)) : -margin + log1p(exp(margin));
+  }
+  f /= (double)samples;
+  for (uint64_t j = 0; j < dim; ++j) f += 0.5 * l2 * th[j] * th[j];
+  return f;
+}
+
+/* optimizer.hpp:122-136 */
+void orc_logistic_gradient(const double* xs, const double* ys, uint64_t samples, uint64_t dim,
+                           double l2, const double* th, double* g) {
+  for (uint64_t j = 0; j < dim; ++j) g[j] = 0.0;
+  for (uint64_t i = 0; i < samples; ++i) {
+    double margin = 0.0;
+    for (uint64_t j = 0; j < dim; ++j) margin += xs[i * dim + j] * th[j];
+    const double coeff = -ys[i] / (1.0 + exp(ys[i] * margin));
+    for (uint64_t j = 0; j < dim; ++j) g[j] += coeff * xs[i * dim + j];
+  }
+  for (uint64_t j = 0; j < dim; ++j) g[j] = g[j] / (double)samples + l2 * th[j];
+}
+
+/* optimizer.hpp:82-86 smoothness L = trace / (4 m) + l2 */
+double orc_logistic_smoothness(const double* xs, uint64_t samples, uint64_t dim, double l2) {
+  double trace = 0.0;
+  for (uint64_t i = 0; i < samples * dim; ++i) trace += xs[i] * xs[i];
+  return trace / (4.0 * (double)samples) + l2;
+}
+
+/* run_moshpit_sgd (optimizer.hpp:297-439) with LogisticRegression, fp64;
+ * same outputs as orc_sgd_quadratic_f64. */
+int orc_sgd_logistic_f64(uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers, uint64_t dim,
+                         const double* xs, const double* ys, uint64_t samples, double l2,
+                         const double* theta0, double gamma, uint32_t tau, uint32_t steps,
+                         double sigma, uint32_t inner_rounds, uint64_t seed,
+                         double* f_gap, double* grad_norm_sq, double* f_gap_weighted,
+                         double* dispersion, double* final_mean, double* diag6,
+                         double* final_thetas) {
+  if (gamma <= 0.0 || tau < 1 || sigma < 0.0) return ORC_INVALID_ARGUMENT;
+  if (orc_grid_validate(M, d, T)) return ORC_INVALID_ARGUMENT;
+  if (n_peers < 1 || n_peers > orc_grid_capacity(M, d)) return ORC_INVALID_ARGUMENT;
+  const uint32_t inner = inner_rounds == 0 ? d : inner_rounds;
+  const uint64_t D = dim ? dim : 1;
+  const uint64_t n = n_peers;
+  double* th = (double*)malloc(n * D * sizeof(double));
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint64_t j = 0; j < dim; ++j) th[i * dim + j] = theta0[j];
+  orc_rng noise, avg;
+  orc_rng_stream(&noise, seed, "noise");
+  orc_rng_stream(&avg, seed, "averaging");
+  const double mu = l2;
+  double pv_max = 0.0, noise_sq_sum = 0.0, weight_total = 0.0, w_k = 1.0;
+  uint64_t noise_count = 0;
+  const double w_growth = mu > 0.0 ? 1.0 / (1.0 - gamma * mu) : 1.0;
+  double* g = (double*)malloc(D * sizeof(double));
+  double* hat = (double*)malloc(D * sizeof(double));
+  double* mean = (double*)malloc(D * sizeof(double));
+  double* wsum = (double*)calloc(D, sizeof(double));
+  double* wtd = (double*)malloc(D * sizeof(double));
+  int rc = ORC_OK;
+  for (uint32_t k = 0; k < steps && rc == ORC_OK; ++k) {
+    const double coord_std = sigma > 0.0 ? sigma / sqrt((double)dim) : 0.0;
+    for (uint64_t i = 0; i < n && rc == ORC_OK; ++i) {
+      orc_logistic_gradient(xs, ys, samples, dim, l2, th + i * dim, g);
+      for (uint64_t j = 0; j < dim; ++j) {
+        if (coord_std > 0.0) {
+          const double nj = coord_std * orc_rng_normal(&noise);
+          noise_sq_sum += nj * nj;
+          g[j] += nj;
+        }
+        if (!isfinite(g[j])) { rc = ORC_RUNTIME_ERROR; break; }
+        th[i * dim + j] -= gamma * g[j];
+      }
+      ++noise_count;
+    }
+    if (rc != ORC_OK) break;
+    colmean_d_f64(th, n, dim, hat);
+    if ((k + 1) % tau == 0) orc_moshpit_average_f64(th, n, dim, M, d, inner, &avg);
+    colmean_d_f64(th, n, dim, mean);
+    double ip = 0.0;
+    for (uint64_t j = 0; j < dim; ++j) ip += (mean[j] - hat[j]) * (mean[j] + hat[j]);
+    if (ip > pv_max) pv_max = ip;
+    double v = 0.0;
+    for (uint64_t i = 0; i < n; ++i)
+      for (uint64_t j = 0; j < dim; ++j) {
+        const double dd = th[i * dim + j] - mean[j];
+        v += dd * dd;
+      }
+    dispersion[k] = v / (double)n;
+    f_gap[k] = orc_logistic_value(xs, ys, samples, dim, l2, mean) - 0.0;
+    orc_logistic_gradient(xs, ys, samples, dim, l2, mean, g);
+    double gn = 0.0;
+    for (uint64_t j = 0; j < dim; ++j) gn += g[j] * g[j];
+    grad_norm_sq[k] = gn;
+    w_k *= w_growth;
+    for (uint64_t j = 0; j < dim; ++j) wsum[j] += w_k * mean[j];
+    weight_total += w_k;
+    for (uint64_t j = 0; j < dim; ++j) wtd[j] = wsum[j] / weight_total;
+    f_gap_weighted[k] = orc_logistic_value(xs, ys, samples, dim, l2, wtd) - 0.0;
+    memcpy(final_mean, mean, dim * sizeof(double));
+  }
+  if (rc == ORC_OK) {
+    double v_sync_max = 0.0;
+    for (uint32_t k = tau - 1; k < steps; k += tau)
+      if (dispersion[k] > v_sync_max) v_sync_max = dispersion[k];
+    diag6[0] = sqrt(v_sync_max) / gamma;
+    diag6[1] = noise_count > 0 && sigma > 0.0 ? sqrt(noise_sq_sum / (double)noise_count) : 0.0;
+    diag6[2] = 0.0;
+    diag6[3] = sqrt(pv_max > 0.0 ? pv_max : 0.0) / gamma;
+    diag6[4] = (double)n;
+    diag6[5] = (double)n;
+    if (final_thetas) memcpy(final_thetas, th, n * dim * sizeof(double));
+  }
+  free(th); free(g); free(hat); free(mean); free(wsum); free(wtd);
+  return rc;
+}

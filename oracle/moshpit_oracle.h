@@ -121,6 +121,22 @@ int orc_moshpit_trace(uint32_t M, uint32_t d, uint64_t n, double p,
 ORC_DECLARE_REAL(double, f64)
 ORC_DECLARE_REAL(float, f32)
 
+/* ---- LogisticRegression (optimizer.hpp:75-146), fp64 ---------------- */
+void orc_logistic_synthetic(uint64_t dim, uint64_t samples, orc_rng* st, double* xs,
+                            double* ys);
+double orc_logistic_value(const double* xs, const double* ys, uint64_t samples, uint64_t dim,
+                          double l2, const double* th);
+void orc_logistic_gradient(const double* xs, const double* ys, uint64_t samples, uint64_t dim,
+                           double l2, const double* th, double* g);
+double orc_logistic_smoothness(const double* xs, uint64_t samples, uint64_t dim, double l2);
+int orc_sgd_logistic_f64(uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers, uint64_t dim,
+                         const double* xs, const double* ys, uint64_t samples, double l2,
+                         const double* theta0, double gamma, uint32_t tau, uint32_t steps,
+                         double sigma, uint32_t inner_rounds, uint64_t seed,
+                         double* f_gap, double* grad_norm_sq, double* f_gap_weighted,
+                         double* dispersion, double* final_mean, double* diag6,
+                         double* final_thetas);
+
 #ifdef __cplusplus
 }
 #endif

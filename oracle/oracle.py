@@ -85,6 +85,13 @@ class Checker:
                   [u32, u32, u32, u32, u64, dbl, dbl, vp, vp, dbl, u32, u32, dbl, u32, u64, vp,
                    vp, u64, vp, vp, vp, vp, vp, vp, vp])
             f("rng_stream", None, [vp, u64, cstr])
+            f("logistic_synthetic", None, [u64, u64, vp, vp, vp])
+            f("logistic_value", dbl, [vp, vp, u64, u64, dbl, vp])
+            f("logistic_gradient", None, [vp, vp, u64, u64, dbl, vp, vp])
+            f("logistic_smoothness", dbl, [vp, u64, u64, dbl])
+            f("sgd_logistic_f64", C.c_int,
+              [u32, u32, u32, u32, u64, vp, vp, u64, dbl, vp, dbl, u32, u32, dbl, u32, u64, vp,
+               vp, vp, vp, vp, vp, vp])
         else:
             f("pairwise_sum", dbl, [vp, u64])
             f("group_mean", C.c_int, [vp, u64, u64, vp, vp])
@@ -100,6 +107,11 @@ class Checker:
               [u32, u32, u32, u32, u64, dbl, dbl, vp, vp, dbl, u32, u32, dbl, u32, u64, vp,
                vp, u64, vp, vp, vp, vp, vp, vp])
             f("local_step_quadratic", C.c_int, [vp, u64, dbl, dbl, vp, dbl, dbl, u64, cstr])
+            f("logistic_eval", C.c_int, [vp, vp, u64, u64, dbl, vp, vp, vp, vp])
+            f("logistic_synthetic_eval", C.c_int, [u64, u64, dbl, u64, cstr, vp, vp, vp, vp])
+            f("sgd_logistic", C.c_int,
+              [u32, u32, u32, u32, u64, u64, dbl, u64, cstr, vp, dbl, u32, u32, dbl, u32, u64,
+               vp, vp, vp, vp, vp, vp])
             f("slice_bench", C.c_int,
               [u32, u32, u64, u64, u64, u64, u64, u64, dbl, u32, u32, vp, vp, vp])
 
@@ -274,6 +286,60 @@ class Checker:
         _check(self._local_step_quadratic(_p(th), len(th), L, mu, _p(tgt), gamma, sigma, seed,
                                           name.encode()), "local_step")
         return th
+
+    # ---- LogisticRegression (optimizer.hpp:75-146) --------------------------------
+    def logistic_dataset(self, dim, samples, data_seed, name="objective"):
+        """LogisticRegression::synthetic over Rng(data_seed).stream(name) (oracle)."""
+        st = _Rng()
+        self._rng_stream(C.byref(st), data_seed, name.encode())
+        xs = np.zeros((samples, max(dim, 1)))
+        ys = np.zeros(max(samples, 1))
+        self._logistic_synthetic(dim, samples, C.byref(st), _p(xs), _p(ys))
+        return xs[:, :dim].copy(), ys[:samples].copy()
+
+    def logistic_eval(self, xs, ys, l2, theta):
+        """(value, gradient, smoothness) of LogisticRegression(xs, ys, l2) at theta."""
+        x = np.ascontiguousarray(xs, dtype=np.float64)
+        y = np.ascontiguousarray(ys, dtype=np.float64)
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        S, dim = x.shape
+        g = np.zeros(max(dim, 1))
+        if self.kind == "ref":
+            v, sm = C.c_double(0), C.c_double(0)
+            _check(self._logistic_eval(_p(x), _p(y), S, dim, l2, _p(th), C.byref(v), _p(g),
+                                       C.byref(sm)), "logistic_eval")
+            return v.value, g[:dim], sm.value
+        v = self._logistic_value(_p(x), _p(y), S, dim, l2, _p(th))
+        self._logistic_gradient(_p(x), _p(y), S, dim, l2, _p(th), _p(g))
+        return v, g[:dim], self._logistic_smoothness(_p(x), S, dim, l2)
+
+    def sgd_logistic(self, M, d, n_peers, dim, samples, l2, data_seed, theta0, gamma, tau, steps,
+                     sigma, seed, inner_rounds=0, T=1, name="objective"):
+        """run_moshpit_sgd(LogisticRegression::synthetic(dim, samples, l2,
+        Rng(data_seed).stream(name))); returns a dict (fp64, no schedule)."""
+        th0 = np.ascontiguousarray(theta0, dtype=np.float64)
+        K = max(steps, 1)
+        out = {k: np.zeros(K) for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion")}
+        fm = np.zeros(max(dim, 1))
+        diag = np.zeros(6)
+        tail = [_p(th0), gamma, tau, steps, sigma, inner_rounds, seed, _p(out["f_gap"]),
+                _p(out["grad_norm_sq"]), _p(out["f_gap_weighted"]), _p(out["dispersion"]),
+                _p(fm), _p(diag)]
+        fin = None
+        if self.kind == "ref":
+            _check(self._sgd_logistic(M, d, T, n_peers, dim, samples, l2, data_seed,
+                                      name.encode(), *tail), "sgd_logistic")
+        else:
+            xs, ys = self.logistic_dataset(dim, samples, data_seed, name)
+            fin = np.zeros((n_peers, max(dim, 1)))
+            _check(self._sgd_logistic_f64(M, d, T, n_peers, dim, _p(xs), _p(ys), samples, l2,
+                                          *tail, _p(fin)), "sgd_logistic")
+            fin = fin[: int(diag[5]), :dim]
+        res = {k: v[:steps] for k, v in out.items()}
+        res.update(final_mean=fm[:dim], delta_aq_hat=diag[0], sigma_hat=diag[1],
+                   delta_pv1_hat=diag[2], delta_pv2_hat=diag[3], n_min=int(diag[4]),
+                   final_thetas=fin)
+        return res
 
     # ---- oracle-only ------------------------------------------------------------
     def trace(self, M, d, n, p, seed, rounds):

@@ -327,6 +327,75 @@ int ref_local_step_quadratic(double* theta, std::uint64_t dim, double L, double 
   });
 }
 
+// LogisticRegression(xs, ys, l2) value / gradient / smoothness (optimizer.hpp:75-146).
+int ref_logistic_eval(const double* xs, const double* ys, std::uint64_t samples, std::uint64_t dim,
+                      double l2, const double* theta, double* value, double* grad,
+                      double* smooth) {
+  return guarded([&] {
+    const optimizer::LogisticRegression lr(rows_of(xs, samples, dim),
+                                           std::vector<double>(ys, ys + samples), l2);
+    const ParamVector th(theta, theta + dim);
+    *value = lr.value(th);
+    const auto g = lr.gradient(th);
+    std::memcpy(grad, g.data(), dim * sizeof(double));
+    *smooth = lr.smoothness();
+  });
+}
+
+// LogisticRegression::synthetic over Rng(data_seed).stream(name), evaluated at
+// theta: pins the oracle's dataset generation without exposing private data.
+int ref_logistic_synthetic_eval(std::uint64_t dim, std::uint64_t samples, double l2,
+                                std::uint64_t data_seed, const char* name, const double* theta,
+                                double* value, double* grad, double* smooth) {
+  return guarded([&] {
+    auto st = Rng(data_seed).stream(name);
+    const auto lr = optimizer::LogisticRegression::synthetic(dim, samples, l2, st);
+    const ParamVector th(theta, theta + dim);
+    *value = lr.value(th);
+    const auto g = lr.gradient(th);
+    std::memcpy(grad, g.data(), dim * sizeof(double));
+    *smooth = lr.smoothness();
+  });
+}
+
+// run_moshpit_sgd with LogisticRegression::synthetic(dim, samples, l2,
+// Rng(data_seed).stream(name)).
+int ref_sgd_logistic(std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
+                     std::uint64_t dim, std::uint64_t samples, double l2,
+                     std::uint64_t data_seed, const char* name, const double* theta0,
+                     double gamma, std::uint32_t tau, std::uint32_t steps, double sigma,
+                     std::uint32_t inner_rounds, std::uint64_t seed, double* f_gap,
+                     double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
+                     double* final_mean, double* diag6) {
+  return guarded([&] {
+    auto st = Rng(data_seed).stream(name);
+    const auto lr = optimizer::LogisticRegression::synthetic(dim, samples, l2, st);
+    optimizer::OptimizerConfig cfg;
+    cfg.gamma = gamma;
+    cfg.tau = tau;
+    cfg.steps = steps;
+    cfg.grid = GridConfig{M, d, T};
+    cfg.sigma = sigma;
+    cfg.n_peers = n_peers;
+    cfg.inner_rounds = inner_rounds;
+    const auto r = optimizer::run_moshpit_sgd(cfg, lr, ParamVector(theta0, theta0 + dim), {},
+                                              Rng(seed));
+    for (std::size_t k = 0; k < r.f_gap.size(); ++k) {
+      f_gap[k] = r.f_gap[k];
+      grad_norm_sq[k] = r.grad_norm_sq[k];
+      f_gap_weighted[k] = r.f_gap_weighted[k];
+      dispersion[k] = r.diagnostics.dispersion[k];
+    }
+    for (std::size_t j = 0; j < r.final_mean.size(); ++j) final_mean[j] = r.final_mean[j];
+    diag6[0] = r.diagnostics.delta_aq_hat;
+    diag6[1] = r.diagnostics.sigma_hat;
+    diag6[2] = r.diagnostics.delta_pv1_hat;
+    diag6[3] = r.diagnostics.delta_pv2_hat;
+    diag6[4] = r.diagnostics.n_min;
+    diag6[5] = 0;
+  });
+}
+
 // CPU baseline: the unmodified run_moshpit on `slices` column slices of
 // width `width` of the counter-initialised state, spread over
 // `threads` host threads.  Coordinates are independent, so each slice is

@@ -32,7 +32,7 @@ __all__ = [
     "complexity_estimate", "Engine", "fill_synthetic", "InvalidArgument", "OutOfRange",
     "CudaError", "MoshpitError", "device_count", "Shard", "Quadratic", "OptimizerConfig",
     "MembershipEvent", "SgdResult", "AssumptionDiagnostics", "local_step", "run_moshpit_sgd",
-    "run_moshpit_batch", "trial_seed",
+    "run_moshpit_batch", "trial_seed", "LogisticRegression",
 ]
 
 
@@ -444,6 +444,56 @@ class Quadratic:
         return self.target
 
 
+class LogisticRegression:
+    """L2-regularised logistic regression (optimizer.hpp:75-146): value and
+    gradient evaluate on the GPU in the reference's summation orders."""
+
+    def __init__(self, xs, ys, l2: float):
+        x = np.ascontiguousarray(xs, dtype=np.float64)
+        y = np.ascontiguousarray(ys, dtype=np.float64).reshape(-1)
+        if x.ndim != 2 or x.shape[0] == 0 or x.shape[0] != len(y):
+            raise InvalidArgument("LogisticRegression: bad dataset")
+        self.xs, self.ys, self.l2 = x, y, float(l2)
+        sm = C.c_double(0.0)
+        check(lib().moshpit_logistic_eval(_p(x), _p(y), len(y), x.shape[1], self.l2, None, None,
+                                          None, C.byref(sm)))
+        self._l = sm.value
+
+    @staticmethod
+    def synthetic(dim: int, samples: int, l2: float, stream: RngStream) -> "LogisticRegression":
+        xs = np.zeros((samples, dim))
+        ys = np.zeros(samples)
+        check(lib().moshpit_logistic_synthetic(dim, samples, C.byref(stream.state), _p(xs),
+                                               _p(ys)))
+        return LogisticRegression(xs, ys, l2)
+
+    def _eval(self, theta, want_grad):
+        th = np.ascontiguousarray(theta, dtype=np.float64).reshape(-1)
+        v = C.c_double(0.0)
+        g = np.zeros(max(self.dim(), 1)) if want_grad else None
+        check(lib().moshpit_logistic_eval(_p(self.xs), _p(self.ys), len(self.ys), self.dim(),
+                                          self.l2, _p(th), C.byref(v), _p(g), None))
+        return v.value, (g[:self.dim()] if want_grad else None)
+
+    def value(self, theta) -> float:
+        return self._eval(theta, False)[0]
+
+    def gradient(self, theta) -> np.ndarray:
+        return self._eval(theta, True)[1]
+
+    def dim(self):
+        return self.xs.shape[1]
+
+    def smoothness(self):
+        return self._l
+
+    def strong_convexity(self):
+        return self.l2
+
+    def optimum_value(self):
+        return 0.0
+
+
 @dataclass
 class OptimizerConfig:
     gamma: float = 0.1
@@ -493,18 +543,26 @@ class SgdResult:
     loop_ms: float = 0.0  # extension: device time of the step loop
 
 
-def local_step(theta: np.ndarray, objective: Quadratic, gamma: float, sigma: float,
+def local_step(theta: np.ndarray, objective, gamma: float, sigma: float,
                noise: RngStream) -> np.ndarray:
     """optimizer::local_step on the GPU (in place for float arrays)."""
     x = theta if (isinstance(theta, np.ndarray) and theta.dtype in (np.float32, np.float64)
                   and theta.flags.c_contiguous) else np.ascontiguousarray(theta, np.float64)
+    if isinstance(objective, LogisticRegression):
+        check(lib().moshpit_local_step_logistic(_dtype_code(x.dtype), _p(x), len(x),
+                                                _p(objective.xs), _p(objective.ys),
+                                                len(objective.ys), objective.l2, gamma, sigma,
+                                                C.byref(noise.state)))
+        return x
+    if not isinstance(objective, Quadratic):
+        raise InvalidArgument("local_step: objective must be Quadratic or LogisticRegression")
     check(lib().moshpit_local_step_quadratic(_dtype_code(x.dtype), _p(x), len(x), objective.l,
                                              objective.mu, _p(objective.target), gamma, sigma,
                                              C.byref(noise.state)))
     return x
 
 
-def run_moshpit_sgd(config: OptimizerConfig, objective: Quadratic, theta0,
+def run_moshpit_sgd(config: OptimizerConfig, objective, theta0,
                     schedule: Sequence[MembershipEvent], rng: Rng, *, dtype=np.float64,
                     diagnostics: str = "exact", noise: str = "reference",
                     return_thetas: bool = False) -> SgdResult:
@@ -525,14 +583,23 @@ def run_moshpit_sgd(config: OptimizerConfig, objective: Quadratic, theta0,
     n_max = config.n_peers + sum(max(e.delta, 0) for e in schedule)
     fin = np.zeros((n_max, max(dim, 1)), dtype=dtype) if return_thetas else None
     loop_ms = C.c_double(0.0)
-    check(lib().moshpit_run_moshpit_sgd_quadratic(
-        _dtype_code(dtype), config.grid.peers_per_axis, config.grid.dims, config.grid.rounds,
-        config.n_peers, dim, objective.l, objective.mu, _p(objective.target), _p(th0),
-        config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds, rng.seed(),
-        _p(evs) if len(evs) else None, _p(evd) if len(evd) else None, len(evs),
-        _DIAG[diagnostics], {"reference": 0, "device": 1}[noise], _p(out["f_gap"]),
-        _p(out["g"]), _p(out["fw"]), _p(out["disp"]), _p(fm), _p(d6), _p(fin),
-        C.byref(loop_ms)))
+    g = config.grid
+    tail = (_p(th0), config.gamma, config.tau, config.steps, config.sigma, config.inner_rounds,
+            rng.seed(), _p(evs) if len(evs) else None, _p(evd) if len(evd) else None, len(evs),
+            _DIAG[diagnostics], {"reference": 0, "device": 1}[noise], _p(out["f_gap"]),
+            _p(out["g"]), _p(out["fw"]), _p(out["disp"]), _p(fm), _p(d6), _p(fin),
+            C.byref(loop_ms))
+    if isinstance(objective, LogisticRegression):
+        check(lib().moshpit_run_moshpit_sgd_logistic(
+            _dtype_code(dtype), g.peers_per_axis, g.dims, g.rounds, config.n_peers, dim,
+            _p(objective.xs), _p(objective.ys), len(objective.ys), objective.l2, *tail))
+    elif isinstance(objective, Quadratic):
+        check(lib().moshpit_run_moshpit_sgd_quadratic(
+            _dtype_code(dtype), g.peers_per_axis, g.dims, g.rounds, config.n_peers, dim,
+            objective.l, objective.mu, _p(objective.target), *tail))
+    else:
+        raise InvalidArgument("run_moshpit_sgd: objective must be Quadratic or "
+                              "LogisticRegression")
     n_fin = int(d6[5])
     diag = AssumptionDiagnostics(list(out["disp"][:config.steps]), d6[0], d6[1], d6[2], d6[3],
                                  int(d6[4]))

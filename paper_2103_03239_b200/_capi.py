@@ -79,6 +79,14 @@ PROTOTYPES = {
                                                     vp, vp, dbl, u32, u32, dbl, u32, u64, vp, vp,
                                                     u64, C.c_int, C.c_int, vp, vp, vp, vp, vp,
                                                     vp, vp, P(dbl)]),
+    "moshpit_logistic_synthetic": (C.c_int, [u64, u64, P(RngState), vp, vp]),
+    "moshpit_logistic_eval": (C.c_int, [vp, vp, u64, u64, dbl, vp, P(dbl), vp, P(dbl)]),
+    "moshpit_local_step_logistic": (C.c_int, [C.c_int, vp, u64, vp, vp, u64, dbl, dbl, dbl,
+                                              P(RngState)]),
+    "moshpit_run_moshpit_sgd_logistic": (C.c_int, [C.c_int, u32, u32, u32, u32, u64, vp, vp,
+                                                   u64, dbl, vp, dbl, u32, u32, dbl, u32, u64,
+                                                   vp, vp, u64, C.c_int, C.c_int, vp, vp, vp,
+                                                   vp, vp, vp, vp, P(dbl)]),
     "moshpit_engine_create": (C.c_int, [u32, u32, u64, dbl, u64, C.c_int, P(vp)]),
     "moshpit_engine_destroy": (C.c_int, [vp]),
     "moshpit_engine_set_kernel": (C.c_int, [vp, C.c_int]),

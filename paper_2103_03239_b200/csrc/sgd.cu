@@ -223,6 +223,106 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
   return (unsigned)(b ? b : 1);
 }
 
+// ---- LogisticRegression (optimizer.hpp:75-146) ------------------------------
+// coeff[i][s] = -y_s / (1 + exp(y_s * margin)), margin = sum_j x_sj * theta_ij
+// in j order (optimizer.hpp:124-128); ymargin[i][s] = margin * y_s (value()).
+// CUDA's exp/log1p need not round like glibc's in the last bit, so logistic
+// parity is a tolerance; the summation orders are the reference's.
+template <typename T>
+__global__ void logit_coeff(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                            const double* __restrict__ xs, const double* __restrict__ ys,
+                            std::uint64_t S, double* __restrict__ coeff,
+                            double* __restrict__ ymargin) {
+  const std::uint64_t sidx = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  const std::uint64_t i = blockIdx.y;
+  if (sidx >= S) return;
+  const T* th = x + i * ld;
+  const double* xr = xs + sidx * dim;
+  double margin = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) margin = __dadd_rn(margin, __dmul_rn(xr[j], (double)th[j]));
+  const double y = ys[sidx];
+  if (coeff) coeff[i * S + sidx] = __ddiv_rn(-y, __dadd_rn(1.0, exp(__dmul_rn(y, margin))));
+  if (ymargin) ymargin[i * S + sidx] = __dmul_rn(margin, y);
+}
+
+// g_ij = (sum_s coeff_is * x_sj) / m + l2 * theta_ij  (optimizer.hpp:129-135), then
+// optionally the SGD update theta -= gamma (g + n_j) (optimizer.hpp:356-373).
+template <typename T>
+__global__ void logit_grad(T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                           const double* __restrict__ xs, std::uint64_t S,
+                           const double* __restrict__ coeff, double l2, int update, T gamma,
+                           const T* __restrict__ noise, double coord_std, int philox_mode,
+                           std::uint64_t seed, std::uint64_t step, std::uint32_t* nonfinite,
+                           double* nsq_out, double* __restrict__ g_out, std::uint64_t i0) {
+  const std::uint64_t j = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  const std::uint64_t i = blockIdx.y;
+  if (j >= dim) return;
+  const double* c = coeff + i * S;
+  double g = 0.0;
+  for (std::uint64_t sidx = 0; sidx < S; ++sidx) g = __dadd_rn(g, __dmul_rn(c[sidx], xs[sidx * dim + j]));
+  T* p = x + i * ld + j;
+  g = __dadd_rn(__ddiv_rn(g, (double)S), __dmul_rn(l2, (double)*p));
+  if (!update) {
+    g_out[j] = g;
+    return;
+  }
+  using O = SOps<T>;
+  T gt = (T)g;
+  if (noise) {
+    gt = O::add(gt, noise[i * dim + j]);
+  } else if (philox_mode) {
+    float z[4];
+    philox_normals4(seed, step, i0 + i, j / 4, z);
+    const T nj = noise_component(z[j % 4], coord_std, (T*)nullptr);
+    atomicAdd(nsq_out, (double)nj * (double)nj);
+    gt = O::add(gt, nj);
+  }
+  if (!isfinite(gt)) atomicOr(nonfinite, 1u);
+  *p = O::sub(*p, O::mul(gamma, gt));
+}
+
+// value(theta) = sum_s softplus(-y m) / m + sum_j 0.5 l2 t^2, in order
+// (optimizer.hpp:106-120), from the y*margin terms.
+__global__ void logit_value_finish(const double* __restrict__ ym, std::uint64_t S,
+                                   const double* __restrict__ th, std::uint64_t dim, double l2,
+                                   double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double f = 0.0;
+  for (std::uint64_t sidx = 0; sidx < S; ++sidx) {
+    const double m = ym[sidx];
+    f = __dadd_rn(f, m > 0.0 ? log1p(exp(-m)) : __dadd_rn(-m, log1p(exp(m))));
+  }
+  f = __ddiv_rn(f, (double)S);
+  for (std::uint64_t j = 0; j < dim; ++j)
+    f = __dadd_rn(f, __dmul_rn(__dmul_rn(__dmul_rn(0.5, l2), th[j]), th[j]));
+  *out = f;
+}
+
+// pv inner product (optimizer.hpp:386-391), the weighted iterate
+// (:411-417) and |g|^2 (:408), sequential in j.
+__global__ void logit_vec_diag(const double* __restrict__ mean, const double* __restrict__ hat,
+                               double* __restrict__ wsum, double w_k, double weight_total,
+                               std::uint64_t dim, double* __restrict__ wtd,
+                               double* __restrict__ pv_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double ip = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) {
+    ip = __dadd_rn(ip, __dmul_rn(__dsub_rn(mean[j], hat[j]), __dadd_rn(mean[j], hat[j])));
+    const double ws = __dadd_rn(wsum[j], __dmul_rn(w_k, mean[j]));
+    wsum[j] = ws;
+    wtd[j] = __ddiv_rn(ws, weight_total);
+  }
+  *pv_out = ip;
+}
+
+__global__ void sumsq_exact(const double* __restrict__ g, std::uint64_t dim,
+                            double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (std::uint64_t j = 0; j < dim; ++j) s = __dadd_rn(s, __dmul_rn(g[j], g[j]));
+  *out = s;
+}
+
 }  // namespace
 
 // optimizer.hpp:39-44
@@ -243,6 +343,74 @@ struct SgdRun {
   cudaStream_t s;
   DeviceBuffer c64, t64, cT, tT, noise_dev, flag, npart, hat, mean, wsum, vpart, vout, dpart;
   double noise_sq_host = 0.0;
+  // LogisticRegression(xs, ys, l2): samples S, rows of xs are dim doubles.
+  bool logit = false;
+  std::uint64_t S = 0;
+  double l2 = 0.0;
+  DeviceBuffer lxs, lys, coeff, ym, gm, wtd;
+
+  void logit_upload(const double* xs, const double* ys, std::uint64_t samples, double l2_,
+                    std::uint64_t n_max) {
+    logit = true;
+    S = samples;
+    l2 = l2_;
+    lxs.resize(S * dim * 8 + 16);
+    lys.resize(S * 8 + 16);
+    coeff.resize(n_max * S * 8 + 16);
+    ym.resize(S * 8 + 16);
+    gm.resize((dim ? dim : 1) * 8 + 16);
+    wtd.resize((dim ? dim : 1) * 8 + 16);
+    if (dim) MB_CUDA(cudaMemcpyAsync(lxs.ptr, xs, S * dim * 8, cudaMemcpyHostToDevice, s));
+    MB_CUDA(cudaMemcpyAsync(lys.ptr, ys, S * 8, cudaMemcpyHostToDevice, s));
+  }
+
+  // optimizer.hpp:356-373 with LogisticRegression::gradient: margins/coefficients
+  // for every (peer, sample), then gradient + update for every (peer, j).
+  template <typename T>
+  void lstep(void* x, std::uint64_t n, double gamma, double coord_std, int philox,
+             std::uint64_t seed, std::uint64_t k, const T* noise_host_rows) {
+    const T* nz = nullptr;
+    if (noise_host_rows) {
+      noise_dev.resize(n * dim * sizeof(T) + 16);
+      MB_CUDA(cudaMemcpyAsync(noise_dev.ptr, noise_host_rows, n * dim * sizeof(T),
+                              cudaMemcpyHostToDevice, s));
+      nz = noise_dev.as<T>();
+    }
+    if (dim == 0) return;
+    for (std::uint64_t i0 = 0; i0 < n; i0 += 65535) {
+      const unsigned rows = (unsigned)std::min<std::uint64_t>(65535, n - i0);
+      T* xr = static_cast<T*>(x) + i0 * ld;
+      logit_coeff<T><<<dim3((unsigned)((S + 127) / 128), rows), 128, 0, s>>>(
+          xr, ld, dim, lxs.as<double>(), lys.as<double>(), S, coeff.as<double>(), nullptr);
+      logit_grad<T><<<dim3((unsigned)((dim + 127) / 128), rows), 128, 0, s>>>(
+          xr, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, 1, (T)gamma,
+          nz ? nz + i0 * dim : nullptr, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
+          npart.as<double>() + k * 148 * 16, nullptr, i0);
+      MB_LAUNCH_CHECK();
+    }
+  }
+
+  // f(mean), |grad f(mean)|^2, f(weighted) and the pv product into o[0..3]
+  // (optimizer.hpp:383-417), each in the reference's summation order.
+  void logit_diag(double w_k, double weight_total, double* o) {
+    logit_vec_diag<<<1, 1, 0, s>>>(mean.as<double>(), hat.as<double>(), wsum.as<double>(), w_k,
+                                   weight_total, dim, wtd.as<double>(), o);
+    const unsigned sb = (unsigned)((S + 127) / 128);
+    logit_coeff<double><<<dim3(sb, 1), 128, 0, s>>>(mean.as<double>(), dim, dim,
+                                                   lxs.as<double>(), lys.as<double>(), S,
+                                                   coeff.as<double>(), ym.as<double>());
+    logit_value_finish<<<1, 1, 0, s>>>(ym.as<double>(), S, mean.as<double>(), dim, l2, o + 1);
+    if (dim)
+      logit_grad<double><<<dim3((unsigned)((dim + 127) / 128), 1), 128, 0, s>>>(
+          mean.as<double>(), dim, dim, lxs.as<double>(), S, coeff.as<double>(), l2, 0, 0.0,
+          nullptr, 0.0, 0, 0, 0, flag.as<std::uint32_t>(), nullptr, gm.as<double>(), 0);
+    sumsq_exact<<<1, 1, 0, s>>>(gm.as<double>(), dim, o + 2);
+    logit_coeff<double><<<dim3(sb, 1), 128, 0, s>>>(wtd.as<double>(), dim, dim,
+                                                   lxs.as<double>(), lys.as<double>(), S,
+                                                   nullptr, ym.as<double>());
+    logit_value_finish<<<1, 1, 0, s>>>(ym.as<double>(), S, wtd.as<double>(), dim, l2, o + 3);
+    MB_LAUNCH_CHECK();
+  }
 
   template <typename T>
   void step(void* x, std::uint64_t n, double gamma, double coord_std, int philox,
@@ -324,14 +492,12 @@ int moshpit_local_step_quadratic(int dtype, void* theta, std::uint64_t dim, doub
   });
 }
 
-// optimizer.hpp:297-439 run_moshpit_sgd with Quadratic(dim, L, mu, target).
-// noise_mode 0: the reference "noise" stream (host draws, bit-exact);
-// noise_mode 1: device Philox normals (statistical parity).
-// diag: MOSHPIT_DIAG_EXACT or MOSHPIT_DIAG_FAST.  diag6 = {delta_aq_hat,
-// sigma_hat, delta_pv1_hat, delta_pv2_hat, n_min, n_final}.
-int moshpit_run_moshpit_sgd_quadratic(
+// The shared driver; lxs != nullptr selects LogisticRegression(lxs, lys, l2)
+// (mu = l2, optimizer.hpp:141), else Quadratic(dim, L, mu, target).
+static int run_sgd(
     int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
-    std::uint64_t dim, double L, double mu, const double* target, const double* theta0,
+    std::uint64_t dim, double L, double mu, const double* target, const double* lxs,
+    const double* lys, std::uint64_t samples, double l2, const double* theta0,
     double gamma, std::uint32_t tau, std::uint32_t steps, double sigma,
     std::uint32_t inner_rounds, std::uint64_t seed, const std::uint32_t* ev_step,
     const std::int32_t* ev_delta, std::uint64_t n_events, int diag, int noise_mode,
@@ -339,7 +505,13 @@ int moshpit_run_moshpit_sgd_quadratic(
     double* final_mean, double* diag6, void* final_thetas, double* loop_ms) {
   return guarded([&] {
     const std::size_t es = elem_size(dtype);
-    if (L < mu || mu < 0.0) throw std::invalid_argument("Quadratic: need L >= mu >= 0");
+    const bool logit = lxs != nullptr;
+    if (logit) {
+      if (samples == 0 || !lys) throw std::invalid_argument("LogisticRegression: bad dataset");
+      mu = l2;
+    } else if (L < mu || mu < 0.0) {
+      throw std::invalid_argument("Quadratic: need L >= mu >= 0");
+    }
     // OptimizerConfig::validate (optimizer.hpp:195-202)
     if (gamma <= 0.0) throw std::invalid_argument("OptimizerConfig: gamma > 0");
     if (tau < 1) throw std::invalid_argument("OptimizerConfig: tau >= 1");
@@ -382,9 +554,13 @@ int moshpit_run_moshpit_sgd_quadratic(
     MB_CUDA(cudaMemsetAsync(r.flag.ptr, 0, 16, h.s));
     MB_CUDA(cudaMemsetAsync(r.wsum.ptr, 0, D * 8, h.s));
     MB_CUDA(cudaMemsetAsync(r.npart.ptr, 0, r.npart.bytes, h.s));
-    const auto c = quad_curvature(dim, L, mu);
-    MB_CUDA(cudaMemcpyAsync(r.c64.ptr, c.data(), dim * 8, cudaMemcpyHostToDevice, h.s));
-    MB_CUDA(cudaMemcpyAsync(r.t64.ptr, target, dim * 8, cudaMemcpyHostToDevice, h.s));
+    if (logit) {
+      r.logit_upload(lxs, lys, samples, l2, n_max);
+    } else {
+      const auto c = quad_curvature(dim, L, mu);
+      MB_CUDA(cudaMemcpyAsync(r.c64.ptr, c.data(), dim * 8, cudaMemcpyHostToDevice, h.s));
+      MB_CUDA(cudaMemcpyAsync(r.t64.ptr, target, dim * 8, cudaMemcpyHostToDevice, h.s));
+    }
     MB_CUDA(cudaMemcpyAsync(th0.ptr, theta0, dim * 8, cudaMemcpyHostToDevice, h.s));
     const unsigned b = (unsigned)((D + 255) / 256);
     if (dtype == MOSHPIT_F32) {
@@ -413,7 +589,10 @@ int moshpit_run_moshpit_sgd_quadratic(
     const int exact = diag == MOSHPIT_DIAG_EXACT;
     // DIAG_NONE: kernel 3 -- the local step rides in the first averaging
     // round's loads (one read + one write of the state for step + round 1).
-    const bool fused = diag == MOSHPIT_DIAG_NONE && !(coord_std > 0.0 && noise_mode == 0);
+    const bool fused =
+        !logit && diag == MOSHPIT_DIAG_NONE && !(coord_std > 0.0 && noise_mode == 0);
+    // no per-step diagnostics: fused quadratic runs and logistic DIAG_NONE
+    const bool skip_diag = fused || (logit && diag == MOSHPIT_DIAG_NONE);
     DeviceBuffer cpad, tpad;
     if (fused) {  // curvature / target padded to the row stride (zeros)
       cpad.resize(r.ld * es + 16);
@@ -496,14 +675,25 @@ int moshpit_run_moshpit_sgd_quadratic(
         }
         continue;
       }
-      if (dtype == MOSHPIT_F32) {
-        r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
-                      static_cast<const float*>(host_noise));
+      if (logit) {
+        if (dtype == MOSHPIT_F32)
+          r.lstep<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                         static_cast<const float*>(host_noise));
+        else
+          r.lstep<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                          static_cast<const double*>(host_noise));
+      }
+      if (skip_diag) {
+      } else if (dtype == MOSHPIT_F32) {
+        if (!logit)
+          r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                        static_cast<const float*>(host_noise));
         launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.hat.as<double>(),
                                       h.s);
       } else {
-        r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
-                       static_cast<const double*>(host_noise));
+        if (!logit)
+          r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                         static_cast<const double*>(host_noise));
         launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
                                        r.hat.as<double>(), h.s);
       }
@@ -515,6 +705,7 @@ int moshpit_run_moshpit_sgd_quadratic(
         for (std::uint32_t q = 0; q < inner; ++q)
           plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
       }
+      if (skip_diag) continue;
       double* o = out.as<double>() + (std::uint64_t)k * 8;
       if (dtype == MOSHPIT_F32)
         launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
@@ -525,7 +716,15 @@ int moshpit_run_moshpit_sgd_quadratic(
       w_k *= w_growth;
       weight_total += w_k;
       wt_hist[k] = weight_total;
-      if (exact) {
+      if (logit) {
+        r.logit_diag(w_k, weight_total, o);
+        if (dtype == MOSHPIT_F32)
+          dispersion_exact<float><<<1, 1, 0, h.s>>>(x.as<float>(), n, r.ld, dim,
+                                                    r.mean.as<double>(), o + 4);
+        else
+          dispersion_exact<double><<<1, 1, 0, h.s>>>(x.as<double>(), n, r.ld, dim,
+                                                     r.mean.as<double>(), o + 4);
+      } else if (exact) {
         sgd_vec_exact<<<1, 1, 0, h.s>>>(r.mean.as<double>(), r.hat.as<double>(),
                                         r.c64.as<double>(), r.t64.as<double>(),
                                         r.wsum.as<double>(), w_k, weight_total, dim, o);
@@ -553,7 +752,7 @@ int moshpit_run_moshpit_sgd_quadratic(
       MB_LAUNCH_CHECK();
     }
     if (loop_ms) MB_CUDA(cudaEventRecord(ev1, h.s));
-    if (fused) {
+    if (skip_diag) {
       if (dtype == MOSHPIT_F32)
         launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
                                       h.s);
@@ -590,8 +789,8 @@ int moshpit_run_moshpit_sgd_quadratic(
     MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
     if (bad) throw std::runtime_error("run_moshpit_sgd: non-finite gradient");
     for (double v : hnp) noise_sq_sum += v;
-    double pv_max = fused ? std::nan("") : 0.0;
-    for (std::uint32_t k = 0; k < steps && !fused; ++k) {
+    double pv_max = skip_diag ? std::nan("") : 0.0;
+    for (std::uint32_t k = 0; k < steps && !skip_diag; ++k) {
       const double* o = hout.data() + (std::uint64_t)k * 8;
       pv_max = std::max(pv_max, o[0]);
       f_gap[k] = o[1] - 0.0;
@@ -599,11 +798,11 @@ int moshpit_run_moshpit_sgd_quadratic(
       f_gap_weighted[k] = o[3] - 0.0;
       dispersion[k] = o[4];
     }
-    if (fused)
+    if (skip_diag)
       for (std::uint32_t k = 0; k < steps; ++k)
         f_gap[k] = grad_norm_sq[k] = f_gap_weighted[k] = dispersion[k] = std::nan("");
-    double v_sync_max = fused ? std::nan("") : 0.0;
-    for (std::uint32_t k = tau - 1; k < steps && !fused; k += tau)
+    double v_sync_max = skip_diag ? std::nan("") : 0.0;
+    for (std::uint32_t k = tau - 1; k < steps && !skip_diag; k += tau)
       v_sync_max = std::max(v_sync_max, dispersion[k]);
     diag6[0] = std::sqrt(v_sync_max) / gamma;
     diag6[1] = noise_count > 0 && sigma > 0.0
@@ -613,6 +812,152 @@ int moshpit_run_moshpit_sgd_quadratic(
     diag6[3] = std::sqrt(std::max(0.0, pv_max)) / gamma;
     diag6[4] = n_min;
     diag6[5] = static_cast<double>(n);
+  });
+}
+
+// optimizer.hpp:297-439 run_moshpit_sgd with Quadratic(dim, L, mu, target).
+// noise_mode 0: the reference "noise" stream (host draws, bit-exact);
+// noise_mode 1: device Philox normals (statistical parity).
+// diag: MOSHPIT_DIAG_EXACT or MOSHPIT_DIAG_FAST.  diag6 = {delta_aq_hat,
+// sigma_hat, delta_pv1_hat, delta_pv2_hat, n_min, n_final}.
+int moshpit_run_moshpit_sgd_quadratic(
+    int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
+    std::uint64_t dim, double L, double mu, const double* target, const double* theta0,
+    double gamma, std::uint32_t tau, std::uint32_t steps, double sigma,
+    std::uint32_t inner_rounds, std::uint64_t seed, const std::uint32_t* ev_step,
+    const std::int32_t* ev_delta, std::uint64_t n_events, int diag, int noise_mode,
+    double* f_gap, double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
+    double* final_mean, double* diag6, void* final_thetas, double* loop_ms) {
+  return run_sgd(dtype, M, d, T, n_peers, dim, L, mu, target, nullptr, nullptr, 0, 0.0, theta0,
+                 gamma, tau, steps, sigma, inner_rounds, seed, ev_step, ev_delta, n_events, diag,
+                 noise_mode, f_gap, grad_norm_sq, f_gap_weighted, dispersion, final_mean, diag6,
+                 final_thetas, loop_ms);
+}
+
+// optimizer.hpp:297-439 run_moshpit_sgd with LogisticRegression(xs, ys, l2)
+// (optimizer.hpp:75-146): xs is samples x dim row-major fp64, ys in {-1,+1}.
+// Diagnostics are always the reference's sequential orders (the objective's
+// own evaluation dominates them); diag only selects NONE vs. computed.
+int moshpit_run_moshpit_sgd_logistic(
+    int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T, std::uint32_t n_peers,
+    std::uint64_t dim, const double* xs, const double* ys, std::uint64_t samples, double l2,
+    const double* theta0, double gamma, std::uint32_t tau, std::uint32_t steps, double sigma,
+    std::uint32_t inner_rounds, std::uint64_t seed, const std::uint32_t* ev_step,
+    const std::int32_t* ev_delta, std::uint64_t n_events, int diag, int noise_mode,
+    double* f_gap, double* grad_norm_sq, double* f_gap_weighted, double* dispersion,
+    double* final_mean, double* diag6, void* final_thetas, double* loop_ms) {
+  if (!xs) return guarded([] { throw std::invalid_argument("LogisticRegression: bad dataset"); });
+  return run_sgd(dtype, M, d, T, n_peers, dim, 0.0, 0.0, nullptr, xs, ys, samples, l2, theta0,
+                 gamma, tau, steps, sigma, inner_rounds, seed, ev_step, ev_delta, n_events, diag,
+                 noise_mode, f_gap, grad_norm_sq, f_gap_weighted, dispersion, final_mean, diag6,
+                 final_thetas, loop_ms);
+}
+
+// LogisticRegression::synthetic (optimizer.hpp:89-104): the dataset is drawn
+// on the host from the caller's stream (it is setup, not the hot path).
+int moshpit_logistic_synthetic(std::uint64_t dim, std::uint64_t samples,
+                               moshpit_rng_state* stream, double* xs, double* ys) {
+  return guarded([&] {
+    Xoshiro st;
+    std::memcpy(st.s, stream->s, sizeof(st.s));
+    st.have_spare = stream->have_spare != 0;
+    st.spare = stream->spare;
+    std::vector<double> truth(dim);
+    for (auto& t : truth) t = st.normal();
+    for (std::uint64_t i = 0; i < samples; ++i) {
+      double dot = 0.0;
+      for (std::uint64_t j = 0; j < dim; ++j) {
+        xs[i * dim + j] = st.normal();
+        dot += xs[i * dim + j] * truth[j];
+      }
+      ys[i] = dot + 0.1 * st.normal() > 0.0 ? 1.0 : -1.0;
+    }
+    std::memcpy(stream->s, st.s, sizeof(st.s));
+    stream->have_spare = st.have_spare ? 1 : 0;
+    stream->spare = st.spare;
+  });
+}
+
+// value / gradient (GPU) and smoothness (the constructor's trace bound,
+// optimizer.hpp:82-86) of LogisticRegression(xs, ys, l2) at theta.
+int moshpit_logistic_eval(const double* xs, const double* ys, std::uint64_t samples,
+                          std::uint64_t dim, double l2, const double* theta, double* value,
+                          double* grad, double* smoothness) {
+  return guarded([&] {
+    if (!xs || !ys || samples == 0) throw std::invalid_argument("LogisticRegression: bad dataset");
+    if (smoothness) {
+      double trace = 0.0;
+      for (std::uint64_t i = 0; i < samples * dim; ++i) trace += xs[i] * xs[i];
+      *smoothness = trace / (4.0 * static_cast<double>(samples)) + l2;
+    }
+    if (!value && !grad) return;
+    require_device();
+    StreamHolder h;
+    SgdRun r{MOSHPIT_F64, 8, dim, dim, h.s};
+    r.flag.resize(16);
+    r.logit_upload(xs, ys, samples, l2, 1);
+    DeviceBuffer th((dim ? dim : 1) * 8 + 16), o(64);
+    if (dim) MB_CUDA(cudaMemcpyAsync(th.ptr, theta, dim * 8, cudaMemcpyHostToDevice, h.s));
+    MB_CUDA(cudaMemsetAsync(r.gm.ptr, 0, (dim ? dim : 1) * 8, h.s));
+    logit_coeff<double><<<dim3((unsigned)((samples + 127) / 128), 1), 128, 0, h.s>>>(
+        th.as<double>(), dim, dim, r.lxs.as<double>(), r.lys.as<double>(), samples,
+        r.coeff.as<double>(), r.ym.as<double>());
+    logit_value_finish<<<1, 1, 0, h.s>>>(r.ym.as<double>(), samples, th.as<double>(), dim, l2,
+                                         o.as<double>());
+    if (dim)
+      logit_grad<double><<<dim3((unsigned)((dim + 127) / 128), 1), 128, 0, h.s>>>(
+          th.as<double>(), dim, dim, r.lxs.as<double>(), samples, r.coeff.as<double>(), l2, 0,
+          0.0, nullptr, 0.0, 0, 0, 0, r.flag.as<std::uint32_t>(), nullptr, r.gm.as<double>(), 0);
+    MB_LAUNCH_CHECK();
+    if (value) MB_CUDA(cudaMemcpyAsync(value, o.ptr, 8, cudaMemcpyDeviceToHost, h.s));
+    if (grad && dim)
+      MB_CUDA(cudaMemcpyAsync(grad, r.gm.ptr, dim * 8, cudaMemcpyDeviceToHost, h.s));
+    MB_CUDA(cudaStreamSynchronize(h.s));
+  });
+}
+
+// optimizer.hpp:231-242 local_step with LogisticRegression(xs, ys, l2).
+int moshpit_local_step_logistic(int dtype, void* theta, std::uint64_t dim, const double* xs,
+                                const double* ys, std::uint64_t samples, double l2,
+                                double gamma, double sigma, moshpit_rng_state* noise) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (!xs || !ys || samples == 0) throw std::invalid_argument("LogisticRegression: bad dataset");
+    if (dim == 0) return;
+    require_device();
+    Xoshiro st;
+    std::memcpy(st.s, noise->s, sizeof(st.s));
+    st.have_spare = noise->have_spare != 0;
+    st.spare = noise->spare;
+    const double coord_std = sigma > 0.0 ? sigma / std::sqrt(static_cast<double>(dim)) : 0.0;
+    std::vector<double> nz;
+    if (coord_std > 0.0) {
+      nz.resize(dim);
+      for (auto& v : nz) v = coord_std * st.normal();
+    }
+    StreamHolder h;
+    SgdRun r{dtype, es, dim, dim, h.s};
+    r.flag.resize(16);
+    r.npart.resize(148 * 16 * 8 + 16);
+    MB_CUDA(cudaMemsetAsync(r.flag.ptr, 0, 16, h.s));
+    r.logit_upload(xs, ys, samples, l2, 1);
+    DeviceBuffer x(dim * es + 16);
+    MB_CUDA(cudaMemcpyAsync(x.ptr, theta, dim * es, cudaMemcpyHostToDevice, h.s));
+    if (dtype == MOSHPIT_F32) {
+      std::vector<float> nzf(nz.begin(), nz.end());
+      r.lstep<float>(x.ptr, 1, gamma, coord_std, 0, 0, 0, nz.empty() ? nullptr : nzf.data());
+      MB_CUDA(cudaStreamSynchronize(h.s));
+    } else {
+      r.lstep<double>(x.ptr, 1, gamma, coord_std, 0, 0, 0, nz.empty() ? nullptr : nz.data());
+      MB_CUDA(cudaStreamSynchronize(h.s));
+    }
+    std::uint32_t bad = 0;
+    MB_CUDA(cudaMemcpy(&bad, r.flag.ptr, 4, cudaMemcpyDeviceToHost));
+    if (bad) throw std::runtime_error("local_step: non-finite gradient");
+    MB_CUDA(cudaMemcpy(theta, x.ptr, dim * es, cudaMemcpyDeviceToHost));
+    std::memcpy(noise->s, st.s, sizeof(st.s));
+    noise->have_spare = st.have_spare ? 1 : 0;
+    noise->spare = st.spare;
   });
 }
 

@@ -6,6 +6,8 @@
 // absent in this image, so a minimal CHECK macro stands in.
 // Final line: a TrialReport for the golden C2-shaped case, as hex, which
 // tests/test_cpp_dropin.py compares bit-for-bit with tests/golden/golden.json.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <map>
 #include <set>
@@ -245,6 +247,48 @@ int main() {
     bad.grid = GridConfig{2, 2, 1};
     bad.n_peers = 5;
     CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  }
+  // test_optimizer.cpp:30-58 (LogisticRegression through the drop-in: GPU
+  // value/gradient vs central finite differences, objective constants) and a
+  // GPU run_moshpit_sgd on the logistic objective.
+  {
+    Rng rng(21);
+    auto stream = rng.stream("theta");
+    (void)stream.normals(6);  // the Quadratic's target in the reference test
+    const auto logit = optimizer::LogisticRegression::synthetic(5, 80, 0.05, stream);
+    for (int trial = 0; trial < 10; ++trial) {
+      const ParamVector theta = stream.normals(5);
+      const ParamVector g = logit.gradient(theta);
+      for (std::size_t j = 0; j < theta.size(); ++j) {
+        const double h = 1e-6 * std::max(1.0, std::abs(theta[j]));
+        ParamVector lo = theta, hi = theta;
+        lo[j] -= h;
+        hi[j] += h;
+        const double fd = (logit.value(hi) - logit.value(lo)) / (2.0 * h);
+        const double scale = std::max({std::abs(g[j]), std::abs(fd), 1e-8});
+        CHECK(std::abs(g[j] - fd) / scale <= 1e-6);
+      }
+    }
+    Rng r22(22);
+    auto st22 = r22.stream("t");
+    const auto l4 = optimizer::LogisticRegression::synthetic(4, 50, 0.1, st22);
+    CHECK(l4.smoothness() >= l4.strong_convexity());
+    CHECK_THROWS_AS(optimizer::LogisticRegression({}, {}, 0.1), std::invalid_argument);
+    optimizer::OptimizerConfig cfg;
+    cfg.gamma = 0.3;
+    cfg.tau = 2;
+    cfg.steps = 30;
+    cfg.sigma = 0.2;
+    cfg.grid = GridConfig{4, 2, 1};
+    cfg.n_peers = 16;
+    const auto res = optimizer::run_moshpit_sgd(cfg, l4, ParamVector(4, 0.0), {}, Rng(3));
+    CHECK(res.f_gap.size() == cfg.steps);
+    CHECK(res.f_gap.back() < l4.value(ParamVector(4, 0.0)));
+    ParamVector th(4, 0.0);
+    auto nz = Rng(5).stream("noise");
+    optimizer::local_step(th, l4, 0.5, 0.0, nz);
+    const auto g0 = l4.gradient(ParamVector(4, 0.0));
+    for (std::size_t j = 0; j < 4; ++j) CHECK(std::abs(th[j] + 0.5 * g0[j]) <= 1e-15);
   }
   // golden case: counter init, C2-shaped (32x32, p=0.01, 10 rounds), dim 4
   {

@@ -34,6 +34,17 @@ def hxa(a):
     return [hx(v) for v in np.asarray(a, dtype=np.float64).reshape(-1)]
 
 
+def C_eval(r, dim, S, l2, dseed, th):
+    import ctypes as C
+    v, sm = C.c_double(0), C.c_double(0)
+    g = np.zeros(dim)
+    rc = r._logistic_synthetic_eval(dim, S, l2, dseed, b"objective",
+                                    th.ctypes.data_as(C.c_void_p), C.byref(v),
+                                    g.ctypes.data_as(C.c_void_p), C.byref(sm))
+    assert rc == 0
+    return v.value, g, sm.value
+
+
 def main():
     r = Checker("ref")
     out = {"source": "oracle/_ref (unmodified reference headers via ref_shim.cpp)",
@@ -150,6 +161,32 @@ def main():
                               out=hxa(r.local_step_quadratic(np.arange(1.0, 6.0), 3.0, 0.5,
                                                              [0.1, -0.2, 0.3, 0.4, -0.5], 0.1,
                                                              2.0, 4, "noise")))]
+
+    # LogisticRegression (optimizer.hpp:75-146): synthetic(dim, samples, l2,
+    # Rng(data_seed).stream("objective")) evaluated at theta, and
+    # run_moshpit_sgd over it -- both from the unmodified reference.
+    logit = []
+    for (dim, S, l2, dseed) in [(4, 32, 0.01, 11), (16, 200, 0.1, 12), (1, 5, 0.0, 13)]:
+        th = r.stream_draws(dseed, "theta", dim, "normal")
+        v, g, sm = C_eval(r, dim, S, l2, dseed, th)
+        logit.append(dict(dim=dim, samples=S, l2=l2, data_seed=dseed, theta=hxa(th),
+                          value=hx(v), grad=hxa(g), smoothness=hx(sm)))
+    out["logistic_eval"] = logit
+    lsgd = []
+    for (M, d, n, dim, S, l2, gamma, tau, K, sigma, seed) in [
+            (4, 2, 9, 4, 32, 0.01, 0.2, 1, 25, 0.0, 31),
+            (4, 2, 12, 8, 64, 0.1, 0.1, 3, 20, 1.0, 32),
+            (8, 2, 40, 16, 100, 0.05, 0.3, 1, 10, 0.5, 33)]:
+        res = r.sgd_logistic(M, d, n, dim, S, l2, seed, np.zeros(dim), gamma, tau, K, sigma,
+                             seed)
+        lsgd.append(dict(M=M, d=d, n=n, dim=dim, samples=S, l2=l2, gamma=gamma, tau=tau,
+                         steps=K, sigma=sigma, seed=seed, data_seed=seed,
+                         f_gap=hxa(res["f_gap"]), grad_norm_sq=hxa(res["grad_norm_sq"]),
+                         f_gap_weighted=hxa(res["f_gap_weighted"]),
+                         dispersion=hxa(res["dispersion"]), final_mean=hxa(res["final_mean"]),
+                         delta_aq_hat=hx(res["delta_aq_hat"]), sigma_hat=hx(res["sigma_hat"]),
+                         delta_pv2_hat=hx(res["delta_pv2_hat"])))
+    out["sgd_logistic"] = lsgd
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:

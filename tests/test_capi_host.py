@@ -187,3 +187,20 @@ def test_trial_seed_matches_reference_harness(mb):
     for n, p, k in [(1024, 0.0, 0), (768, 0.005, 17), (512, 0.01, 99), (900, 1e-3, 3)]:
         assert mb.trial_seed(0, "moshpit", n, p, k) == h.trial_seed(0, n, p, k)
         assert mb.trial_seed(12345, "moshpit", n, p, k) == h.trial_seed(12345, n, p, k)
+
+
+def test_logistic_synthetic_and_smoothness_on_host(mb, golden, oracle):
+    """LogisticRegression::synthetic draws (optimizer.hpp:89-104) and the
+    smoothness bound (:82-86) are host setup: bit-exact without a device."""
+    from tests._util import bits_equal, unhex
+    for c in golden["logistic_eval"]:
+        lr = mb.LogisticRegression.synthetic(c["dim"], c["samples"], c["l2"],
+                                             mb.Rng(c["data_seed"]).stream("objective"))
+        xs, ys = oracle.logistic_dataset(c["dim"], c["samples"], c["data_seed"])
+        assert bits_equal(lr.xs, xs) and bits_equal(lr.ys, ys)
+        assert lr.smoothness() == unhex(c["smoothness"])
+        assert lr.strong_convexity() == c["l2"] and lr.optimum_value() == 0.0
+    with pytest.raises(ValueError):  # optimizer.hpp:80-81
+        mb.LogisticRegression(np.zeros((0, 3)), [], 0.1)
+    with pytest.raises(ValueError):
+        mb.LogisticRegression(np.zeros((2, 3)), [1.0], 0.1)

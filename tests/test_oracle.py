@@ -158,3 +158,38 @@ def test_sgd_oracle_equals_reference_with_schedule(oracle, ref):
     for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion", "final_mean"):
         assert bits_equal(a[k], b[k]), k
     assert a["sigma_hat"] == b["sigma_hat"] and a["n_min"] == b["n_min"] == 7
+
+
+# ---- LogisticRegression (optimizer.hpp:75-146), SURVEY 8f rank 3 ----------------
+def test_logistic_oracle_matches_golden(oracle, golden):
+    """The oracle's synthetic dataset, value, gradient and smoothness are
+    bit-identical to the unmodified reference's (golden vectors)."""
+    for c in golden["logistic_eval"]:
+        xs, ys = oracle.logistic_dataset(c["dim"], c["samples"], c["data_seed"])
+        assert set(np.unique(ys).tolist()) <= {-1.0, 1.0}
+        v, g, sm = oracle.logistic_eval(xs, ys, c["l2"], unhexa(c["theta"]))
+        assert v == unhex(c["value"])
+        assert bits_equal(g, unhexa(c["grad"]))
+        assert sm == unhex(c["smoothness"])
+
+
+def test_logistic_oracle_equals_reference_eval(oracle, ref):
+    rng = np.random.default_rng(5)
+    for S, dim in [(1, 1), (7, 3), (64, 33)]:
+        xs = rng.normal(size=(S, dim)) * 3
+        ys = np.where(rng.random(S) < 0.5, -1.0, 1.0)
+        th = rng.normal(size=dim) * 5  # both tails of the stable softplus
+        a, b = oracle.logistic_eval(xs, ys, 0.05, th), ref.logistic_eval(xs, ys, 0.05, th)
+        assert a[0] == b[0] and bits_equal(a[1], b[1]) and a[2] == b[2]
+
+
+def test_sgd_logistic_oracle_matches_golden(oracle, golden):
+    for c in golden["sgd_logistic"]:
+        res = oracle.sgd_logistic(c["M"], c["d"], c["n"], c["dim"], c["samples"], c["l2"],
+                                  c["data_seed"], np.zeros(c["dim"]), c["gamma"], c["tau"],
+                                  c["steps"], c["sigma"], c["seed"])
+        for k in ("f_gap", "grad_norm_sq", "f_gap_weighted", "dispersion", "final_mean"):
+            assert bits_equal(res[k], unhexa(c[k])), k
+        assert res["delta_aq_hat"] == unhex(c["delta_aq_hat"])
+        assert res["sigma_hat"] == unhex(c["sigma_hat"])
+        assert res["delta_pv2_hat"] == unhex(c["delta_pv2_hat"])
