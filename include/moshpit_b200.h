@@ -201,8 +201,9 @@ int moshpit_local_step_logistic(int dtype, void* theta, uint64_t dim,
                                 double sigma, moshpit_rng_state* noise);
 /* optimizer.hpp:297-439 run_moshpit_sgd with LogisticRegression(xs, ys, l2)
  * [GPU]: arguments and outputs as moshpit_run_moshpit_sgd_quadratic.  diag
- * NONE skips the per-step diagnostics (NaN); FAST and EXACT both evaluate
- * them in the reference's order.  mu = l2 (strong_convexity, :141). */
+ * NONE skips the per-step diagnostics (NaN); EXACT evaluates all of them in
+ * the reference's order; FAST differs only in the dispersion V_k (fixed-order
+ * block partials).  mu = l2 (strong_convexity, :141). */
 int moshpit_run_moshpit_sgd_logistic(
     int dtype, uint32_t M, uint32_t d, uint32_t T, uint32_t n_peers,
     uint64_t dim, const double* xs, const double* ys, uint64_t samples,

@@ -225,7 +225,7 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 
 // ---- LogisticRegression (optimizer.hpp:75-146) ------------------------------
 // coeff[i][s] = -y_s / (1 + exp(y_s * margin)), margin = sum_j x_sj * theta_ij
-// in j order (optimizer.hpp:124-128); ymargin[i][s] = margin * y_s (value()).
+// in j order (optimizer.hpp:124-128); ymargin[i][s] = value()'s softplus term.
 // CUDA's exp/log1p need not round like glibc's in the last bit, so logistic
 // parity is a tolerance; the summation orders are the reference's.
 template <typename T>
@@ -242,7 +242,10 @@ __global__ void logit_coeff(const T* __restrict__ x, std::uint64_t ld, std::uint
   for (std::uint64_t j = 0; j < dim; ++j) margin = __dadd_rn(margin, __dmul_rn(xr[j], (double)th[j]));
   const double y = ys[sidx];
   if (coeff) coeff[i * S + sidx] = __ddiv_rn(-y, __dadd_rn(1.0, exp(__dmul_rn(y, margin))));
-  if (ymargin) ymargin[i * S + sidx] = __dmul_rn(margin, y);
+  if (ymargin) {  // the value() term log(1 + exp(-m)), m = margin * y, both tails
+    const double m = __dmul_rn(margin, y);
+    ymargin[i * S + sidx] = m > 0.0 ? log1p(exp(-m)) : __dadd_rn(-m, log1p(exp(m)));
+  }
 }
 
 // g_ij = (sum_s coeff_is * x_sj) / m + l2 * theta_ij  (optimizer.hpp:129-135), then
@@ -281,17 +284,177 @@ __global__ void logit_grad(T* __restrict__ x, std::uint64_t ld, std::uint64_t di
   *p = O::sub(*p, O::mul(gamma, gt));
 }
 
+// Tiled forms of the two kernels above for the per-peer step: both are
+// GEMM-shaped (margins = Theta . X^T, gradient = C . X) but every output must
+// be summed sequentially in k from 0.0 with separately rounded products (the
+// reference's order), so they run on the fp64 SIMT pipes (DMUL + DADD, no
+// tensor cores, no FMA): 64x64 output tiles per 256-thread CTA, 4x4 outputs
+// per thread, k staged through shared memory 16 at a time.  Each output's
+// k-loop is still the plain sequential chain.
+constexpr int kLT = 64, kLK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    logit_coeff_tiled(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                      std::uint64_t dim, const double* __restrict__ xs,
+                      const double* __restrict__ ys, std::uint64_t S,
+                      double* __restrict__ coeff) {
+  __shared__ double As[kLK][kLT + 1];  // theta[i][k] -> As[k][i - i0]
+  __shared__ double Bs[kLK][kLT + 1];  // xs[s][k]    -> Bs[k][s - s0]
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const std::uint64_t i0 = (std::uint64_t)blockIdx.y * kLT, s0 = (std::uint64_t)blockIdx.x * kLT;
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  for (std::uint64_t k0 = 0; k0 < dim; k0 += kLK) {
+    for (int e = threadIdx.x; e < kLT * kLK; e += 256) {
+      const int r = e / kLK, kk = e % kLK;
+      const std::uint64_t k = k0 + kk;
+      const std::uint64_t i = i0 + r, sm = s0 + r;
+      As[kk][r] = (i < n && k < dim) ? (double)x[i * ld + k] : 0.0;
+      Bs[kk][r] = (sm < S && k < dim) ? xs[sm * dim + k] : 0.0;
+    }
+    __syncthreads();
+    const int kn = dim - k0 < (std::uint64_t)kLK ? (int)(dim - k0) : kLK;
+    if (kn == kLK) {
+#pragma unroll
+      for (int kk = 0; kk < kLK; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(b[c], a[r]));
+      }
+    } else {
+      for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(Bs[kk][tx + 16 * c], As[kk][ty + 16 * r]));
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const std::uint64_t i = i0 + ty + 16 * r;
+    if (i >= n) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const std::uint64_t sm = s0 + tx + 16 * c;
+      if (sm >= S) continue;
+      const double y = ys[sm];
+      coeff[i * S + sm] = __ddiv_rn(-y, __dadd_rn(1.0, exp(__dmul_rn(y, acc[r][c]))));
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    logit_grad_tiled(T* __restrict__ x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                     const double* __restrict__ xs, std::uint64_t S,
+                     const double* __restrict__ coeff, double l2, T gamma,
+                     const T* __restrict__ noise, double coord_std, int philox_mode,
+                     std::uint64_t seed, std::uint64_t step, std::uint32_t* nonfinite,
+                     double* nsq_out) {
+  __shared__ double As[kLK][kLT + 1];            // coeff[i][s] -> As[s - k0][i - i0]
+  __shared__ __align__(16) double Bs[kLK][kLT];  // xs[s][j]    -> Bs[s - k0][j - j0]
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const std::uint64_t i0 = (std::uint64_t)blockIdx.y * kLT, j0 = (std::uint64_t)blockIdx.x * kLT;
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  for (std::uint64_t k0 = 0; k0 < S; k0 += kLK) {
+    for (int e = threadIdx.x; e < kLT * kLK; e += 256) {
+      {
+        const int r = e / kLK, kk = e % kLK;
+        const std::uint64_t i = i0 + r, k = k0 + kk;
+        As[kk][r] = (i < n && k < S) ? coeff[i * S + k] : 0.0;
+      }
+      {
+        const int kk = e / kLT, cc = e % kLT;
+        const std::uint64_t k = k0 + kk, j = j0 + cc;
+        Bs[kk][cc] = (k < S && j < dim) ? xs[k * dim + j] : 0.0;
+      }
+    }
+    __syncthreads();
+    const int kn = S - k0 < (std::uint64_t)kLK ? (int)(S - k0) : kLK;
+    if (kn == kLK) {
+#pragma unroll
+      for (int kk = 0; kk < kLK; ++kk) {
+        double a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4 + 2]);
+        const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(a[r], b[c]));
+      }
+    } else {
+      for (int kk = 0; kk < kn; ++kk) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(As[kk][ty + 16 * r], Bs[kk][tx * 4 + c]));
+      }
+    }
+    __syncthreads();
+  }
+  using O = SOps<T>;
+  double nsq = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const std::uint64_t i = i0 + ty + 16 * r;
+    if (i >= n) continue;
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    if (philox_mode) philox_normals4(seed, step, i, (j0 >> 2) + tx, z);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const std::uint64_t j = j0 + tx * 4 + c;
+      if (j >= dim) continue;
+      T* p = x + i * ld + j;
+      const double g = __dadd_rn(__ddiv_rn(acc[r][c], (double)S), __dmul_rn(l2, (double)*p));
+      T gt = (T)g;
+      if (noise) {
+        gt = O::add(gt, noise[i * dim + j]);
+      } else if (philox_mode) {
+        const T nj = noise_component(z[c], coord_std, (T*)nullptr);
+        nsq += (double)nj * (double)nj;
+        gt = O::add(gt, nj);
+      }
+      if (!isfinite(gt)) bad = true;
+      *p = O::sub(*p, O::mul(gamma, gt));
+    }
+  }
+  if (bad) atomicOr(nonfinite, 1u);
+  if (philox_mode) {
+    for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(nsq_out, nsq);
+  }
+}
+
 // value(theta) = sum_s softplus(-y m) / m + sum_j 0.5 l2 t^2, in order
-// (optimizer.hpp:106-120), from the y*margin terms.
+// (optimizer.hpp:106-120), from the per-sample terms logit_coeff wrote.
 __global__ void logit_value_finish(const double* __restrict__ ym, std::uint64_t S,
                                    const double* __restrict__ th, std::uint64_t dim, double l2,
                                    double* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double f = 0.0;
-  for (std::uint64_t sidx = 0; sidx < S; ++sidx) {
-    const double m = ym[sidx];
-    f = __dadd_rn(f, m > 0.0 ? log1p(exp(-m)) : __dadd_rn(-m, log1p(exp(m))));
-  }
+  for (std::uint64_t sidx = 0; sidx < S; ++sidx) f = __dadd_rn(f, ym[sidx]);
   f = __ddiv_rn(f, (double)S);
   for (std::uint64_t j = 0; j < dim; ++j)
     f = __dadd_rn(f, __dmul_rn(__dmul_rn(__dmul_rn(0.5, l2), th[j]), th[j]));
@@ -377,17 +540,15 @@ struct SgdRun {
       nz = noise_dev.as<T>();
     }
     if (dim == 0) return;
-    for (std::uint64_t i0 = 0; i0 < n; i0 += 65535) {
-      const unsigned rows = (unsigned)std::min<std::uint64_t>(65535, n - i0);
-      T* xr = static_cast<T*>(x) + i0 * ld;
-      logit_coeff<T><<<dim3((unsigned)((S + 127) / 128), rows), 128, 0, s>>>(
-          xr, ld, dim, lxs.as<double>(), lys.as<double>(), S, coeff.as<double>(), nullptr);
-      logit_grad<T><<<dim3((unsigned)((dim + 127) / 128), rows), 128, 0, s>>>(
-          xr, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, 1, (T)gamma,
-          nz ? nz + i0 * dim : nullptr, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
-          npart.as<double>() + k * 148 * 16, nullptr, i0);
-      MB_LAUNCH_CHECK();
-    }
+    const unsigned ty = (unsigned)((n + kLT - 1) / kLT);
+    logit_coeff_tiled<T><<<dim3((unsigned)((S + kLT - 1) / kLT), ty), 256, 0, s>>>(
+        static_cast<const T*>(x), n, ld, dim, lxs.as<double>(), lys.as<double>(), S,
+        coeff.as<double>());
+    logit_grad_tiled<T><<<dim3((unsigned)((dim + kLT - 1) / kLT), ty), 256, 0, s>>>(
+        static_cast<T*>(x), n, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, (T)gamma,
+        nz, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
+        npart.as<double>() + k * 148 * 16);
+    MB_LAUNCH_CHECK();
   }
 
   // f(mean), |grad f(mean)|^2, f(weighted) and the pv product into o[0..3]
@@ -718,12 +879,23 @@ static int run_sgd(
       wt_hist[k] = weight_total;
       if (logit) {
         r.logit_diag(w_k, weight_total, o);
-        if (dtype == MOSHPIT_F32)
-          dispersion_exact<float><<<1, 1, 0, h.s>>>(x.as<float>(), n, r.ld, dim,
-                                                    r.mean.as<double>(), o + 4);
-        else
-          dispersion_exact<double><<<1, 1, 0, h.s>>>(x.as<double>(), n, r.ld, dim,
-                                                     r.mean.as<double>(), o + 4);
+        if (exact) {
+          if (dtype == MOSHPIT_F32)
+            dispersion_exact<float><<<1, 1, 0, h.s>>>(x.as<float>(), n, r.ld, dim,
+                                                      r.mean.as<double>(), o + 4);
+          else
+            dispersion_exact<double><<<1, 1, 0, h.s>>>(x.as<double>(), n, r.ld, dim,
+                                                       r.mean.as<double>(), o + 4);
+        } else {
+          const std::uint64_t ch = nch ? nch : 1;
+          if (dtype == MOSHPIT_F32)
+            dispersion_fast<float><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+                x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+          else
+            dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+                x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+          fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, o + 4);
+        }
       } else if (exact) {
         sgd_vec_exact<<<1, 1, 0, h.s>>>(r.mean.as<double>(), r.hat.as<double>(),
                                         r.c64.as<double>(), r.t64.as<double>(),

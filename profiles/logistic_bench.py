@@ -23,7 +23,7 @@ def main():
     cfg = mb.OptimizerConfig(gamma=gamma, tau=1, steps=steps, grid=mb.GridConfig(M, 2, 1),
                              sigma=sigma, n_peers=n)
     out = {"config": dict(n_peers=n, dim=dim, samples=S, steps=steps, grid=[M, 2])}
-    for diag in ("exact", "none"):
+    for diag in ("exact", "fast", "none"):
         for noise in ("reference", "device"):
             mb.run_moshpit_sgd(cfg, lr, np.zeros(dim), [], mb.Rng(seed), diagnostics=diag,
                                noise=noise)  # warm-up

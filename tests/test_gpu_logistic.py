@@ -80,9 +80,11 @@ def test_sgd_logistic_f64_vs_golden(mb, golden):
         assert _close([r.diagnostics.delta_aq_hat], [unhex(c["delta_aq_hat"])], 1e-6)
 
 
-def test_sgd_logistic_matches_reference_larger(mb, ref):
-    """A larger run (N=256 peers on 16x16, 64 features, 512 samples)."""
-    M, d, n, dim, S, l2 = 16, 2, 256, 64, 512, 0.02
+@pytest.mark.parametrize("M,n,dim,S", [(16, 256, 64, 512), (12, 130, 70, 333)])
+def test_sgd_logistic_matches_reference_larger(mb, ref, M, n, dim, S):
+    """Larger runs through the tiled step kernels: tile-aligned (N=256 peers
+    on 16x16, 64 features, 512 samples) and ragged in every dimension."""
+    d, l2 = 2, 0.02
     want = ref.sgd_logistic(M, d, n, dim, S, l2, 41, np.zeros(dim), 0.5, 2, 16, 0.3, 41)
     lr = mb.LogisticRegression.synthetic(dim, S, l2, mb.Rng(41).stream("objective"))
     cfg = mb.OptimizerConfig(gamma=0.5, tau=2, steps=16, grid=mb.GridConfig(M, d, 1), sigma=0.3,
@@ -188,3 +190,18 @@ def test_logistic_gradient_matches_finite_differences(mb):
             hi[j] += h
             fd = (lr.value(hi) - lr.value(lo)) / (2.0 * h)
             assert abs(g[j] - fd) / max(abs(g[j]), abs(fd), 1e-8) <= 1e-6
+
+
+def test_sgd_logistic_fast_diagnostics(mb, golden):
+    """FAST differs from EXACT only in the dispersion's summation order."""
+    c = golden["sgd_logistic"][1]
+    lr = _lr(mb, c)
+    cfg = mb.OptimizerConfig(gamma=c["gamma"], tau=c["tau"], steps=c["steps"],
+                             grid=mb.GridConfig(c["M"], c["d"], 1), sigma=c["sigma"],
+                             n_peers=c["n"])
+    a = mb.run_moshpit_sgd(cfg, lr, np.zeros(c["dim"]), [], mb.Rng(c["seed"]), diagnostics="fast")
+    b = mb.run_moshpit_sgd(cfg, lr, np.zeros(c["dim"]), [], mb.Rng(c["seed"]))
+    assert np.array_equal(a.f_gap, b.f_gap) and np.array_equal(a.final_mean, b.final_mean)
+    assert np.array_equal(a.f_gap_weighted, b.f_gap_weighted)
+    d_a, d_b = np.array(a.diagnostics.dispersion), np.array(b.diagnostics.dispersion)
+    assert np.all(np.abs(d_a - d_b) <= 1e-12 * np.abs(d_b) + 1e-30)
