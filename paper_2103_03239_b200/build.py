@@ -38,29 +38,45 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)
-            if f.endswith((".cuh", ".cu", ".hpp"))] + [os.path.join(ROOT, "include", "moshpit_b200.h")]
-
-
 def up_to_date():
+    """The library is current when every object is fresh and the library is
+    newer than every object."""
     if not os.path.exists(LIB):
         return False
     t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in _deps())
+    for src in sources():
+        obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+        if not _obj_fresh(src, obj) or os.path.getmtime(obj) > t:
+            return False
+    return True
 
 
-def _headers():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))] + \
-        [os.path.join(ROOT, "include", "moshpit_b200.h")]
+def _includes(path, seen=None):
+    """Local headers a source pulls in (#include "...", transitively)."""
+    import re
+    seen = set() if seen is None else seen
+    try:
+        text = open(path).read()
+    except OSError:
+        return seen
+    for name in re.findall(r'^\s*#\s*include\s+"([^"]+)"', text, re.M):
+        for d in (os.path.dirname(path), CSRC, os.path.join(ROOT, "include")):
+            h = os.path.normpath(os.path.join(d, name))
+            if os.path.exists(h):
+                if h not in seen:
+                    seen.add(h)
+                    _includes(h, seen)
+                break
+    return seen
 
 
 def _obj_fresh(src, obj):
-    """An object is reused when it is newer than its .cu and every header."""
+    """An object is reused when it is newer than its .cu and every local
+    header it includes."""
     if not os.path.exists(obj):
         return False
     t = os.path.getmtime(obj)
-    return all(os.path.getmtime(d) <= t for d in [src, *_headers()])
+    return all(os.path.getmtime(d) <= t for d in [src, *_includes(src)])
 
 
 def _compile(src, nvcc, force=False):

@@ -5,13 +5,19 @@
 // diagnostic per round for the whole batch.  This is the shape of
 // harness::run_experiment's sweeps (harness.hpp:195-280: thousands of small
 // trials, dim 1 for Table 3), where per-trial launches would be pure overhead.
-// The sequential xoshiro draws of different trials are independent, so the
-// host draws them in parallel threads.
+// The sequential xoshiro draws of different trials are independent: the
+// per-round failure and priority streams run on the device, one thread per
+// (trial, stream); the once-per-trial cell draws stay on the host threads.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
+#include <memory>
 #include <thread>
 
 #include "pairwise.cuh"
+#include "blocktree.cuh"
 #include "plane.cuh"
 
 namespace mb200 {
@@ -47,16 +53,33 @@ __global__ void dist_rows_b(const T* __restrict__ x, std::uint64_t n, std::uint6
   sq[r] = acc;
 }
 
-// per trial: pairwise over its n row sums, / n  (core.hpp:125)
-__global__ void finish_b(const double* __restrict__ sq, std::uint64_t n, std::uint64_t trials,
-                         double* __restrict__ out, std::uint64_t out_stride) {
-  const std::uint64_t t = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
-  if (t >= trials) return;
-  const double* s = sq + t * n;
+// The distortion finish (pairwise over the trial's n row sums, / n;
+// core.hpp:125) and the column means of narrow vectors, with the tree over
+// peers evaluated by a whole CTA (blocktree.cuh, bit-identical): one CTA per
+// trial, or per (column, trial).  The harness sweeps run dim = 1, where one
+// thread per trial walking an n-deep serial tree dominated every round.
+constexpr int kTreeThreads = 256;
+
+__global__ void __launch_bounds__(kTreeThreads)
+    finish_tree_b(const double* __restrict__ sq, std::uint32_t n, double* __restrict__ out,
+                  std::uint64_t out_stride) {
+  __shared__ double lvl[2 * kBlockTreeMaxNodes];
+  const double* s = sq + (std::uint64_t)blockIdx.x * n;
   auto ld_fn = [&](std::uint32_t i) { return s[i]; };
-  const double v = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
-                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
-  out[t * out_stride] = __ddiv_rn(v, (double)n);
+  const double v = pairwise_block(ld_fn, n, lvl);
+  if (threadIdx.x == 0) out[(std::uint64_t)blockIdx.x * out_stride] = __ddiv_rn(v, (double)n);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTreeThreads)
+    colmean_tree_b(const T* __restrict__ x, std::uint32_t n, std::uint64_t ld, std::uint64_t dim,
+                   double* __restrict__ out) {
+  __shared__ double lvl[2 * kBlockTreeMaxNodes];
+  const std::uint64_t j = blockIdx.x;
+  const T* xt = x + (std::uint64_t)blockIdx.y * n * ld + j;
+  auto ld_fn = [&](std::uint32_t i) -> double { return (double)xt[(std::uint64_t)i * ld]; };
+  const double v = pairwise_block(ld_fn, n, lvl);
+  if (threadIdx.x == 0) out[(std::uint64_t)blockIdx.y * dim + j] = __ddiv_rn(v, (double)n);
 }
 
 // per trial: drift (protocols.hpp:75-81) in j order
@@ -75,6 +98,96 @@ __global__ void drift_b(const double* __restrict__ mean, const double* __restric
   }
   out[t * out_stride] = __ddiv_rn(__dsqrt_rn(drift_sq), fmax(__dsqrt_rn(ref_sq), 1e-300));
 }
+
+// Per-trial protocol draws on the device (protocols.hpp:86-97, 146-150).
+// Each trial's "failures" and "priorities" streams are sequential xoshiro256**
+// sequences (rng.hpp:35-91), but the trials are independent: thread
+// (trial, stream) continues its stream over a block of rounds and writes the
+// draws in the layout kernel 1 reads (ts u64[rows] | failed u8[rows] per
+// round).  Same generator, same call order, so the draws equal the host's.
+__device__ __forceinline__ std::uint64_t rotl64(std::uint64_t x, int k) {
+  return (x << k) | (x >> (64 - k));
+}
+__device__ __forceinline__ std::uint64_t xnext(std::uint64_t (&s)[4]) {
+  const std::uint64_t result = rotl64(s[1] * 5, 7) * 9;
+  const std::uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+  return result;
+}
+
+__global__ void draws_kernel(std::uint64_t* __restrict__ fail_state,
+                             std::uint64_t* __restrict__ clock_state, std::uint32_t trials,
+                             std::uint32_t n, std::uint32_t nr, std::uint64_t per_round,
+                             double p, std::uint8_t* __restrict__ block,
+                             std::uint32_t* __restrict__ act, std::uint32_t rounds,
+                             std::uint32_t r0) {
+  const std::uint32_t id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 2 * trials) return;
+  const std::uint32_t t = id >> 1;
+  const std::uint64_t rows = (std::uint64_t)trials * n;
+  std::uint64_t* st = (id & 1) ? clock_state + 4 * t : fail_state + 4 * t;
+  std::uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+  for (std::uint32_t q = 0; q < nr; ++q) {
+    std::uint64_t* ts = reinterpret_cast<std::uint64_t*>(block + q * per_round) + (std::uint64_t)t * n;
+    std::uint8_t* f = block + q * per_round + rows * 8 + (std::uint64_t)t * n;
+    if (id & 1) {  // priorities: clock() >> 16 (protocols.hpp:148-150)
+      for (std::uint32_t i = 0; i < n; ++i) ts[i] = xnext(s) >> 16;
+    } else {  // failures: bernoulli(p) per peer, no draws at p <= 0 (:89)
+      std::uint32_t alive = n;
+      if (p > 0.0) {
+        for (std::uint32_t i = 0; i < n; ++i) {
+          const bool dead = (double)(xnext(s) >> 11) * 0x1.0p-53 < p;
+          f[i] = dead ? 1 : 0;
+          alive -= dead ? 1u : 0u;
+        }
+      } else {
+        for (std::uint32_t i = 0; i < n; ++i) f[i] = 0;
+      }
+      act[(std::uint64_t)t * rounds + r0 + q] = alive;
+    }
+  }
+  st[0] = s[0];
+  st[1] = s[1];
+  st[2] = s[2];
+  st[3] = s[3];
+}
+
+// Stream-ordered buffers from the device's default memory pool (release
+// threshold raised once, so freed blocks stay in the pool).  Sweeps call the
+// batch entry point once per harness cell, often from many host threads at
+// once; cudaMalloc/cudaFree per call synchronise the device and serialise the
+// callers, pool allocations on the call's own stream do neither.
+struct PoolBuffer {
+  void* ptr = nullptr;
+  cudaStream_t s = nullptr;
+  PoolBuffer(std::size_t bytes, cudaStream_t stream) : s(stream) {
+    static thread_local int configured = -1;
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    if (configured != dev) {
+      cudaMemPool_t pool;
+      MB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      std::uint64_t keep = UINT64_MAX;
+      MB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      configured = dev;
+    }
+    MB_CUDA(cudaMallocAsync(&ptr, bytes ? bytes : 16, s));
+  }
+  PoolBuffer(const PoolBuffer&) = delete;
+  PoolBuffer& operator=(const PoolBuffer&) = delete;
+  ~PoolBuffer() {
+    if (ptr) cudaFreeAsync(ptr, s);
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
 
 template <typename F>
 void parallel_for(std::uint64_t count, F&& f) {
@@ -99,76 +212,90 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
                std::uint32_t* active, T* final_out) {
   const std::size_t es = sizeof(T);
   const Grid grid(M, d);
+  // MOSHPIT_PROFILE=1: host-side phase times of this call on stderr
+  static const bool prof = std::getenv("MOSHPIT_PROFILE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t_begin = now();
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* what) {
+    if (prof) marks.emplace_back(what, std::chrono::duration<double, std::milli>(now() - t_begin).count());
+  };
   StreamHolder st;
   const std::uint64_t ld = padded_ld(dim, es), rows = (std::uint64_t)trials * n;
   std::uint64_t np = 1;
   while (np < n) np <<= 1;
-  DeviceBuffer x(rows * ld * es + 16), keys(rows * 8), cellb(rows * 8),
-      members(rows * 4), goff((std::uint64_t)trials * (n + 1) * 4), gvoid(rows), act(rows * 4),
-      counts((std::uint64_t)trials * 16), sidx((std::uint64_t)trials * np * 4), scs(rows * 4),
-      sgi(rows * 4);
+  PoolBuffer x(rows * ld * es + 16, st.s), keys(rows * 8, st.s), cellb(rows * 8, st.s),
+      members(rows * 4, st.s), goff((std::uint64_t)trials * (n + 1) * 4, st.s), gvoid(rows, st.s),
+      act(rows * 4, st.s), counts((std::uint64_t)trials * 16, st.s),
+      sidx((std::uint64_t)trials * np * 4, st.s), scs(rows * 4, st.s), sgi(rows * 4, st.s);
   MB_CUDA(cudaMemcpy2DAsync(x.ptr, ld * es, initial, dim * es, dim * es, rows,
                             cudaMemcpyHostToDevice, st.s));
   // host: cells of every trial (protocols.hpp:124-130), in parallel
   // one-shot staging: pageable memory (a cudaMallocHost per call costs more
   // than the copy it would speed up, and serialises concurrent callers)
   std::vector<std::uint64_t> hcells(rows);
-  std::vector<Xoshiro> fail(trials), clock(trials);
+  std::vector<std::uint64_t> hstate((std::uint64_t)trials * 8);  // failures | priorities
+  mark("alloc+h2d");
   parallel_for(trials, [&](std::uint64_t t) {
     Xoshiro cs = Xoshiro::named(seeds[t], "cells");
     const auto c = draw_cells(cs, grid.capacity, n);
     std::memcpy(hcells.data() + t * n, c.data(), n * 8);
-    fail[t] = Xoshiro::named(seeds[t], "failures");
-    clock[t] = Xoshiro::named(seeds[t], "priorities");
+    const Xoshiro f = Xoshiro::named(seeds[t], "failures");
+    const Xoshiro k = Xoshiro::named(seeds[t], "priorities");
+    std::memcpy(hstate.data() + t * 4, f.s, 32);
+    std::memcpy(hstate.data() + ((std::uint64_t)trials + t) * 4, k.s, 32);
   });
+  mark("cells");
+  PoolBuffer rstate(hstate.size() * 8, st.s), act_d((std::uint64_t)trials * rounds * 4 + 16, st.s);
+  MB_CUDA(cudaMemcpyAsync(rstate.ptr, hstate.data(), hstate.size() * 8, cudaMemcpyHostToDevice,
+                          st.s));
   MB_CUDA(cudaMemcpyAsync(cellb.ptr, hcells.data(), rows * 8, cudaMemcpyHostToDevice, st.s));
   launch_initial_keys(cellb.as<std::uint64_t>(), keys.as<std::uint64_t>(), rows, M, d, st.s);
   const bool dg = diag != MOSHPIT_DIAG_NONE;
-  DeviceBuffer ref, mean, sq, out;
+  const bool dg0 = diag != MOSHPIT_DIAG_NONE;
+  PoolBuffer ref(dg0 ? (std::uint64_t)trials * dim * 8 + 16 : 16, st.s),
+      mean(dg0 ? (std::uint64_t)trials * dim * 8 + 16 : 16, st.s), sq(dg0 ? rows * 8 + 16 : 16, st.s),
+      out(dg0 ? (std::uint64_t)trials * (2 * rounds + 1) * 8 + 16 : 16, st.s);
   const unsigned cb = 128;
   const dim3 cgrid((unsigned)((dim + cb - 1) / cb), trials);
+  // narrow vectors: a CTA per (column, trial) evaluates the tree over peers
+  const bool narrow = dim < cb;
+  auto colmean = [&](double* o) {
+    if (!dim) return;
+    if (narrow)
+      colmean_tree_b<T><<<dim3((unsigned)dim, trials), kTreeThreads, 0, st.s>>>(
+          x.as<T>(), (std::uint32_t)n, ld, dim, o);
+    else
+      colmean_b<T><<<cgrid, cb, 0, st.s>>>(x.as<T>(), n, ld, dim, o);
+  };
+  auto finish = [&](double* o) {
+    finish_tree_b<<<trials, kTreeThreads, 0, st.s>>>(sq.as<double>(), (std::uint32_t)n, o,
+                                                     2 * rounds + 1);
+  };
   if (dg) {
-    ref.resize((std::uint64_t)trials * dim * 8 + 16);
-    mean.resize((std::uint64_t)trials * dim * 8 + 16);
-    sq.resize(rows * 8 + 16);
-    out.resize((std::uint64_t)trials * (2 * rounds + 1) * 8 + 16);
-    if (dim) colmean_b<T><<<cgrid, cb, 0, st.s>>>(x.as<T>(), n, ld, dim, ref.as<double>());
+    colmean(ref.as<double>());
     dist_rows_b<T><<<(unsigned)((rows + 127) / 128), 128, 0, st.s>>>(x.as<T>(), n, rows, ld, dim,
                                                                      ref.as<double>(),
                                                                      sq.as<double>());
-    finish_b<<<(trials + 127) / 128, 128, 0, st.s>>>(sq.as<double>(), n, trials,
-                                                     out.as<double>(), 2 * rounds + 1);
+    finish(out.as<double>());
     MB_LAUNCH_CHECK();
   }
-  // All rounds' draws up front (protocols.hpp:143-150, per trial in parallel),
-  // in blocks of rounds that keep the pinned staging under ~256 MB; the GPU
-  // then runs the block's rounds back to back with no host synchronisation.
+  // The draws of a block of rounds are generated on the device (draws_kernel)
+  // right before the rounds that consume them: no host synchronisation.
   std::vector<std::uint32_t> act_h((std::uint64_t)trials * rounds);
   // per-round block: ts u64[rows] then failed u8[rows], padded to 16 bytes so
   // every block's timestamps stay 8-byte aligned
   const std::uint64_t per_round = (rows * 9 + 15) / 16 * 16;
   std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (256ull << 20) / per_round);
   if (rb > rounds) rb = rounds ? rounds : 1;
-  DeviceBuffer dblock(per_round * rb + 16);
-  std::vector<std::uint8_t> hd;
+  PoolBuffer dblock(per_round * rb + 16, st.s);
   for (std::uint32_t r0 = 0; r0 < rounds; r0 += rb) {
     const std::uint32_t nr = std::min(rb, rounds - r0);
-    MB_CUDA(cudaStreamSynchronize(st.s));  // staging reuse
-    hd.resize(per_round * rb + 16);
-    parallel_for(trials, [&](std::uint64_t t) {
-      for (std::uint32_t q = 0; q < nr; ++q) {
-        auto* ts = reinterpret_cast<std::uint64_t*>(hd.data() + q * per_round);
-        std::uint8_t* f = reinterpret_cast<std::uint8_t*>(ts + rows) + t * n;
-        std::memset(f, 0, n);
-        std::uint32_t act_n = 0;
-        if (p > 0.0)
-          for (std::uint64_t i = 0; i < n; ++i) f[i] = fail[t].bernoulli(p) ? 1 : 0;
-        for (std::uint64_t i = 0; i < n; ++i) act_n += f[i] == 0;
-        for (std::uint64_t i = 0; i < n; ++i) ts[t * n + i] = clock[t].next() >> 16;
-        act_h[t * rounds + r0 + q] = act_n;
-      }
-    });
-    MB_CUDA(cudaMemcpyAsync(dblock.ptr, hd.data(), per_round * nr, cudaMemcpyHostToDevice, st.s));
+    draws_kernel<<<(2 * trials + 63) / 64, 64, 0, st.s>>>(
+        rstate.as<std::uint64_t>(), rstate.as<std::uint64_t>() + (std::uint64_t)trials * 4,
+        trials, (std::uint32_t)n, nr, per_round, p, dblock.as<std::uint8_t>(),
+        act_d.as<std::uint32_t>(), rounds, r0);
+    MB_LAUNCH_CHECK();
     for (std::uint32_t q = 0; q < nr; ++q) {
     const std::uint32_t r = r0 + q;
     std::uint8_t* draws_r = dblock.as<std::uint8_t>() + q * per_round;
@@ -197,9 +324,8 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     if (dg) {
       dist_rows_b<T><<<(unsigned)((rows + 127) / 128), 128, 0, st.s>>>(
           x.as<T>(), n, rows, ld, dim, ref.as<double>(), sq.as<double>());
-      finish_b<<<(trials + 127) / 128, 128, 0, st.s>>>(sq.as<double>(), n, trials,
-                                                       out.as<double>() + 1 + r, 2 * rounds + 1);
-      if (dim) colmean_b<T><<<cgrid, cb, 0, st.s>>>(x.as<T>(), n, ld, dim, mean.as<double>());
+      finish(out.as<double>() + 1 + r);
+      colmean(mean.as<double>());
       drift_b<<<(trials + 127) / 128, 128, 0, st.s>>>(mean.as<double>(), ref.as<double>(), dim,
                                                       trials, out.as<double>() + 1 + rounds + r,
                                                       2 * rounds + 1);
@@ -207,6 +333,9 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     }
     }
   }
+  if (rounds)
+    MB_CUDA(cudaMemcpyAsync(act_h.data(), act_d.ptr, act_h.size() * 4, cudaMemcpyDeviceToHost,
+                            st.s));
   std::vector<double> h;
   if (dg) {
     h.resize((std::uint64_t)trials * (2 * rounds + 1));
@@ -215,7 +344,9 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
   if (final_out)
     MB_CUDA(cudaMemcpy2DAsync(final_out, dim * es, x.ptr, ld * es, dim * es, rows,
                               cudaMemcpyDeviceToHost, st.s));
+  mark("enqueued");
   MB_CUDA(cudaStreamSynchronize(st.s));
+  mark("synced");
   const double nan = std::nan("");
   for (std::uint64_t t = 0; t < trials; ++t) {
     const std::uint64_t o = t * (2 * rounds + 1);
@@ -225,6 +356,12 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
       drift[t * rounds + r] = dg ? h[o + 1 + rounds + r] : nan;
       active[t * rounds + r] = act_h[t * rounds + r];
     }
+  }
+  mark("reports");
+  if (prof) {
+    std::string line = "[moshpit batch] trials=" + std::to_string(trials) + " n=" + std::to_string(n);
+    for (auto& m : marks) line += std::string(" ") + m.first + "=" + std::to_string(m.second) + "ms";
+    fprintf(stderr, "%s\n", line.c_str());
   }
 }
 

@@ -281,6 +281,13 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
                        std::uint32_t max_group, int variant, cudaStream_t s,
                        const StepPrologue<T>* step = nullptr);
 int group_mean_grid_size(bool f64, bool step);
+// Kernel 3 leaf-streamed form (step_kernel.cu), groups of <= 32 members.
+template <typename T>
+void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
+                            const std::uint32_t* members, const std::uint32_t* goff,
+                            const std::uint32_t* act, const std::uint32_t* counts,
+                            const StepPrologue<T>& sp, int prefetch, cudaStream_t s);
+int group_mean_step_grid(bool f64, bool noisy, int prefetch);
 
 // Diagnostics and helpers.
 template <typename T, typename Acc>

@@ -147,16 +147,18 @@ __device__ __forceinline__ V apply_step(const StepPrologue<T>& sp, V v, std::uin
   float z[4] = {0, 0, 0, 0};
   const bool noisy = sp.philox != 0;
   if (noisy) philox_normals4(sp.seed, sp.step_no, peer, j0 / 4, z);
+  T q = T(0);
 #pragma unroll
   for (int u = 0; u < kV; ++u) {
     const std::uint64_t j = j0 + u;
     if (j >= sp.dim) break;
     const T nj = noisy ? noise_component(z[j % 4], sp.coord_std, (T*)nullptr) : T(0);
-    if (noisy) nsq += (double)nj * (double)nj;
+    if (noisy) nsq_add(q, nj);
     const T g = sgd_grad(pv[u], pc[u], pt[u], nj, noisy);
     bad |= !isfinite(g);
     pv[u] = sgd_update(pv[u], sp.gamma, g);
   }
+  if (noisy) nsq += (double)q;
   return v;
 }
 
@@ -582,6 +584,18 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     // the split form pays off when the per-element step is compute-heavy
     // (device noise): C4 sigma=1 7.8 -> 4.8 ms/step; at sigma=0 the
     // one-thread-per-column form is slightly faster.
+    // Leaf-streamed kernel 3 (step_kernel.cu) unless MOSHPIT_STEP_KERNEL=old;
+    // MOSHPIT_STEP_PREFETCH=0 drops the next-leaf prefetch (more CTAs/SM).
+    static const int leaf_mode = [] {
+      const char* e = std::getenv("MOSHPIT_STEP_KERNEL");
+      if (e && std::string(e) == "old") return -1;
+      const char* p = std::getenv("MOSHPIT_STEP_PREFETCH");
+      return (p && std::string(p) == "0") ? 0 : 1;
+    }();
+    if (max_group <= 32 && leaf_mode >= 0) {
+      launch_group_mean_step<T>(state, ld, dim, members, goff, act, counts, *step, leaf_mode, s);
+      return;
+    }
     if (max_group <= 32 && !split_off && step->philox) {
       static thread_local int grid_split[2] = {0, 0};
       const int slot = sizeof(T) == 4 ? 0 : 1;

@@ -34,12 +34,21 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
   for (int h = 0; h < 2; ++h) {
     const float u1 = (float)((a[2 * h] >> 8) + 1u) * 0x1.0p-24f;  // (0, 1]
     const float u2 = (float)(a[2 * h + 1] >> 8) * 0x1.0p-24f;     // [0, 1)
-    const float rr = __fsqrt_rn(-2.0f * __logf(u1));
+    float rr;  // sqrt on the SFU (MUFU.SQRT), like __logf / __sincosf
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(rr) : "f"(-2.0f * __logf(u1)));
     float s, c;
     __sincosf(6.283185307179586f * u2, &s, &c);
     z[2 * h] = rr * c;
     z[2 * h + 1] = rr * s;
   }
+}
+
+// n_j^2 summed for sigma_hat: per 4-coordinate quad in the state's
+// precision (fp32: one fp32 partial per quad), then into the caller's fp64
+// accumulator -- the same terms in the fused and the standalone step.
+__device__ __forceinline__ void nsq_add(float& q, float nj) { q = __fadd_rn(q, __fmul_rn(nj, nj)); }
+__device__ __forceinline__ void nsq_add(double& q, double nj) {
+  q = __dadd_rn(q, __dmul_rn(nj, nj));
 }
 
 // One noise component n_j = coord_std * z in the state's precision; both the

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kStepThreads)
     const std::uint64_t i = e / quads, q = e % quads;
     float z[4] = {0, 0, 0, 0};
     if (philox_mode) philox_normals4(seed, step, i, q, z);
+    T nq = T(0);  // per-quad n_j^2 partial (the fused kernel's terms)
     for (int u = 0; u < 4; ++u) {
       const std::uint64_t j = q * 4 + u;
       if (j >= dim) break;
@@ -65,12 +66,13 @@ __global__ void __launch_bounds__(kStepThreads)
         g = O::add(g, noise[i * dim + j]);
       } else if (philox_mode) {
         const T nj = noise_component(z[u], coord_std, (T*)nullptr);
-        nsq += (double)nj * (double)nj;
+        nsq_add(nq, nj);
         g = O::add(g, nj);
       }
       if (!isfinite(g)) atomicOr(nonfinite, 1u);
       *p = O::sub(*p, O::mul(gamma, g));
     }
+    nsq += (double)nq;
   }
   if (philox_mode) {
     red[threadIdx.x] = nsq;
@@ -767,6 +769,10 @@ static int run_sgd(
     std::vector<float> nz32;
     PinnedBuffer nz_pin;
     std::vector<double> wt_hist(steps);
+    // the averaging plane of the initial population is built before the timed
+    // loop (allocations are not part of a step); membership changes rebuild it
+    if (n_peers > 1 && n_peers <= cap && steps >= tau)
+      plane = std::make_unique<Plane>(M, d, n_peers, dev);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (loop_ms) {
       MB_CUDA(cudaEventCreate(&ev0));
