@@ -585,14 +585,16 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     // (device noise): C4 sigma=1 7.8 -> 4.8 ms/step; at sigma=0 the
     // one-thread-per-column form is slightly faster.
     // Leaf-streamed kernel 3 (step_kernel.cu) unless MOSHPIT_STEP_KERNEL=old;
-    // MOSHPIT_STEP_PREFETCH=0 drops the next-leaf prefetch (more CTAs/SM).
-    static const int leaf_mode = [] {
+    // MOSHPIT_STEP_MODE=0|1|2 forces its load-batch mode (default: by noise).
+    static const bool old_step = [] {
       const char* e = std::getenv("MOSHPIT_STEP_KERNEL");
-      if (e && std::string(e) == "old") return -1;
-      const char* p = std::getenv("MOSHPIT_STEP_PREFETCH");
-      return (p && std::string(p) == "0") ? 0 : 1;
+      return e && std::string(e) == "old";
     }();
-    if (max_group <= 32 && leaf_mode >= 0) {
+    static const int leaf_mode = [] {
+      const char* p = std::getenv("MOSHPIT_STEP_MODE");
+      return p ? std::atoi(p) : -1;
+    }();
+    if (max_group <= 32 && !old_step) {
       launch_group_mean_step<T>(state, ld, dim, members, goff, act, counts, *step, leaf_mode, s);
       return;
     }

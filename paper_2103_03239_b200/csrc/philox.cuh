@@ -32,12 +32,16 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
   const std::uint32_t a[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const float u1 = (float)((a[2 * h] >> 8) + 1u) * 0x1.0p-24f;  // (0, 1]
-    const float u2 = (float)(a[2 * h + 1] >> 8) * 0x1.0p-24f;     // [0, 1)
-    float rr;  // sqrt on the SFU (MUFU.SQRT), like __logf / __sincosf
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(rr) : "f"(-2.0f * __logf(u1)));
-    float s, c;
-    __sincosf(6.283185307179586f * u2, &s, &c);
+    // u1 = v / 2^24 in (0, 1] with v = (a >> 8) + 1, so
+    // -2 ln u1 = -2 ln2 * (log2 v - 24): one MUFU.LG2 and one FFMA.
+    const float v = (float)((a[2 * h] >> 8) + 1u);
+    float l2;
+    asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(v));
+    const float e = fmaxf(__fmaf_rn(l2, -1.3862943611198906f, 33.271064666877374f), 0.0f);
+    float rr;  // sqrt on the SFU (MUFU.SQRT)
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(rr) : "f"(e));
+    float s, c;  // angle 2*pi*u2, u2 = (a >> 8) / 2^24 in [0, 1)
+    __sincosf((float)(a[2 * h + 1] >> 8) * 3.7450702e-07f, &s, &c);
     z[2 * h] = rr * c;
     z[2 * h + 1] = rr * s;
   }
@@ -46,10 +50,8 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
 // n_j^2 summed for sigma_hat: per 4-coordinate quad in the state's
 // precision (fp32: one fp32 partial per quad), then into the caller's fp64
 // accumulator -- the same terms in the fused and the standalone step.
-__device__ __forceinline__ void nsq_add(float& q, float nj) { q = __fadd_rn(q, __fmul_rn(nj, nj)); }
-__device__ __forceinline__ void nsq_add(double& q, double nj) {
-  q = __dadd_rn(q, __dmul_rn(nj, nj));
-}
+__device__ __forceinline__ void nsq_add(float& q, float nj) { q = __fmaf_rn(nj, nj, q); }
+__device__ __forceinline__ void nsq_add(double& q, double nj) { q = __fma_rn(nj, nj, q); }
 
 // One noise component n_j = coord_std * z in the state's precision; both the
 // standalone step kernel and the fused kernel 3 use it (bit-identical noise).

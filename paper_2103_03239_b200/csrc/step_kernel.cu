@@ -13,9 +13,9 @@
 // most four sequential LEAVES of <= 8 consecutive members (n <= 8: one leaf;
 // n <= 16: two, split at floor(n/2); n <= 32: the two halves split again,
 // a half of exactly 8 staying one leaf), joined as L0 | L0+L1 | L0+(L1+L2) |
-// (L0+L1)+(L2+L3).  Streaming leaf by leaf (8 loads in flight, the next leaf
-// prefetched while the current one is stepped) needs a quarter of the
-// registers of holding all 32 member vectors, and one runtime-n code body
+// (L0+L1)+(L2+L3).  Streaming leaf by leaf (a few loads in flight per thread, many
+// warps per SM) needs a fraction of the registers of holding all 32 member
+// vectors, and one runtime-n code body
 // replaces 32 unrolled specialisations -- the fully unrolled step+Philox form
 // was 2.3 MB of SASS, and instruction-cache misses ("no_instruction" stalls,
 // 34 % of samples) held it at ~50 % of HBM bandwidth.
@@ -144,9 +144,14 @@ __device__ __forceinline__ double2 vdivn(double2 a, std::uint32_t n) {
   return make_double2(ldiv(a.x, f), ldiv(a.y, f));
 }
 
-template <typename T, bool NOISY, bool PREFETCH>
-__global__ void __launch_bounds__(kLThreads, PREFETCH ? 4 : 6)
+// MODE 0: 8-member load batches; 1: 8-member batches with the next leaf
+// prefetched; 2 (default): 4-member batches at 64 registers, 8 CTAs/SM --
+// more warps to hide the Philox/SFU latency of the device-noise step and the
+// load latency of the plain one.  Same arithmetic in every mode.
+template <typename T, bool NOISY, int MODE>
+__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
     group_mean_step_leaf(LArgs<T> a) {
+  constexpr bool PREFETCH = MODE == 1;
   using V = typename LVec<T>::V;
   constexpr int kV = LVec<T>::kN;
   __shared__ std::uint32_t sids[32];
@@ -210,6 +215,32 @@ __global__ void __launch_bounds__(kLThreads, PREFETCH ? 4 : 6)
     // L0 | L0+L1 | L0+(L1+L2) | (L0+L1)+(L2+L3) for nl = 1..4.
     const std::uint32_t r = nl == 4 ? 2u : 1u;
     V P = vz<V>(), Q = vz<V>();
+    if constexpr (MODE == 2) {
+      std::uint32_t lb = b0;
+#pragma unroll 1
+      for (std::uint32_t l = 0; l < nl; ++l) {
+        const std::uint32_t le = l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4;
+        V sl = vz<V>();
+#pragma unroll 1
+        for (std::uint32_t c0 = lb; c0 < le; c0 += 4) {
+          V X[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            X[k] = (c0 + k < le) ? colp[(std::uint64_t)sids[c0 + k] * ld_vec] : vz<V>();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (c0 + k < le) {
+              step_vec<T, NOISY>(X[k], c, t, gamma, coord_std, seed, step_no, sids[c0 + k], j0,
+                                 full, dim, chk, nsq);
+              sl = vsum(sl, X[k]);
+            }
+          }
+        }
+        if (l < r) P = l == 0 ? sl : vsum(P, sl);
+        else Q = l == r ? sl : vsum(Q, sl);
+        lb = le;
+      }
+    } else {
     V A[8], B[8];
     load_leaf(A, b0, b1);
     std::uint32_t lb = b0, le = b1;
@@ -235,6 +266,7 @@ __global__ void __launch_bounds__(kLThreads, PREFETCH ? 4 : 6)
       lb = nb;
       le = ne;
     }
+    }
     const V sum = nl == 1 ? P : vsum(P, Q);
     const V m = vdivn(sum, cnt);
 #pragma unroll 8
@@ -258,7 +290,7 @@ __global__ void __launch_bounds__(kLThreads, PREFETCH ? 4 : 6)
   if (chk != T(0)) atomicOr(a.nonfinite, 1u);
 }
 
-template <typename T, bool NOISY, bool PREFETCH>
+template <typename T, bool NOISY, int MODE>
 int leaf_grid() {
   static thread_local int dev_cached = -1, grid = 0;
   int dev = 0;
@@ -267,16 +299,16 @@ int leaf_grid() {
     int sms = 0, per = 0;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per, group_mean_step_leaf<T, NOISY, PREFETCH>, kLThreads, 0));
+        &per, group_mean_step_leaf<T, NOISY, MODE>, kLThreads, 0));
     grid = sms * (per > 0 ? per : 1);
     dev_cached = dev;
   }
   return grid;
 }
 
-template <typename T, bool NOISY, bool PREFETCH>
+template <typename T, bool NOISY, int MODE>
 void launch_leaf(const LArgs<T>& a, cudaStream_t s) {
-  group_mean_step_leaf<T, NOISY, PREFETCH><<<leaf_grid<T, NOISY, PREFETCH>(), kLThreads, 0, s>>>(a);
+  group_mean_step_leaf<T, NOISY, MODE><<<leaf_grid<T, NOISY, MODE>(), kLThreads, 0, s>>>(a);
 }
 
 }  // namespace
@@ -306,23 +338,30 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
   a.dim = sp.dim;
   a.nonfinite = sp.nonfinite;
   a.noise_partial = sp.noise_partial;
+  // mode < 0: the default, 4-wide batches at 8 CTAs/SM -- measured best on
+  // B200 for both sigma = 0 (2.86 vs 2.91 / 2.94 ms per C4 step for modes
+  // 1 / 0) and device noise (3.60 vs 3.80 / 3.69 ms)
+  const int mode = prefetch >= 0 ? prefetch : 2;
   if (sp.philox) {
-    if (prefetch) launch_leaf<T, true, true>(a, s);
-    else launch_leaf<T, true, false>(a, s);
+    if (mode == 2) launch_leaf<T, true, 2>(a, s);
+    else if (mode == 1) launch_leaf<T, true, 1>(a, s);
+    else launch_leaf<T, true, 0>(a, s);
   } else {
-    if (prefetch) launch_leaf<T, false, true>(a, s);
-    else launch_leaf<T, false, false>(a, s);
+    if (mode == 2) launch_leaf<T, false, 2>(a, s);
+    else if (mode == 1) launch_leaf<T, false, 1>(a, s);
+    else launch_leaf<T, false, 0>(a, s);
   }
   MB_LAUNCH_CHECK();
 }
 
-int group_mean_step_grid(bool f64, bool noisy, int prefetch) {
+int group_mean_step_grid(bool f64, bool noisy, int mode) {
+  if (mode < 0) mode = 2;
   if (f64) {
-    if (noisy) return prefetch ? leaf_grid<double, true, true>() : leaf_grid<double, true, false>();
-    return prefetch ? leaf_grid<double, false, true>() : leaf_grid<double, false, false>();
+    if (noisy) return mode == 2 ? leaf_grid<double, true, 2>() : mode == 1 ? leaf_grid<double, true, 1>() : leaf_grid<double, true, 0>();
+    return mode == 2 ? leaf_grid<double, false, 2>() : mode == 1 ? leaf_grid<double, false, 1>() : leaf_grid<double, false, 0>();
   }
-  if (noisy) return prefetch ? leaf_grid<float, true, true>() : leaf_grid<float, true, false>();
-  return prefetch ? leaf_grid<float, false, true>() : leaf_grid<float, false, false>();
+  if (noisy) return mode == 2 ? leaf_grid<float, true, 2>() : mode == 1 ? leaf_grid<float, true, 1>() : leaf_grid<float, true, 0>();
+  return mode == 2 ? leaf_grid<float, false, 2>() : mode == 1 ? leaf_grid<float, false, 1>() : leaf_grid<float, false, 0>();
 }
 
 template void launch_group_mean_step<float>(float*, std::uint64_t, std::uint64_t,

@@ -4,7 +4,7 @@ tau=1, inner=2, fp32, device noise, no diagnostics).
     python profiles/sgd_prof.py [sigma] [steps]
 
 Kernel-3 variant via env: MOSHPIT_STEP_KERNEL=old (register/split forms),
-MOSHPIT_STEP_PREFETCH=0|1 (leaf-streamed form)."""
+MOSHPIT_STEP_MODE=0|1|2 (leaf-streamed form load batches)."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, paper_2103_03239_b200 as mb
@@ -18,6 +18,6 @@ best = None
 for _ in range(2 if steps > 6 else 1):
     r = mb.run_moshpit_sgd(cfg, quad, np.zeros(D), [], mb.Rng(7), dtype=np.float32, diagnostics="none", noise="device")
     best = r.loop_ms if best is None else min(best, r.loop_ms)
-tag = os.environ.get("MOSHPIT_STEP_KERNEL", "leaf") + "/pf" + os.environ.get("MOSHPIT_STEP_PREFETCH", "1")
+tag = os.environ.get("MOSHPIT_STEP_KERNEL", "leaf") + "/mode" + os.environ.get("MOSHPIT_STEP_MODE", "auto")
 print(f"sigma={sigma} {tag} loop_ms {best:.3f} per step {best / steps:.4f} ms "
       f"hbm_frac {2*2*N*D*4/(best/steps/1e3)/1e9/6552.6:.3f} sigma_hat {r.diagnostics.sigma_hat:.6f}")
