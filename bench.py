@@ -388,6 +388,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
         sh.round()
     torch.cuda.synchronize()
     c0 = sh.stats()
+    mv0 = sh.cross_detail()[2]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -402,6 +403,8 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     t_ms = ev0.elapsed_time(ev1)
     lms, ln, cms, cn = sh.kernel_time()
     c1 = sh.stats()
+    pa_ms, pb_ms, mv1 = sh.cross_detail()
+    moved = mv1 - mv0  # voided-group rows that moved onto this GPU (cross rounds)
     sh.set_timing(False)
     cross_rounds, cross_groups, local_rows = (c1[0] - c0[0], c1[1] - c0[1], c1[2] - c0[2])
     es, Mg = 4, M // world
@@ -410,16 +413,19 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     # chunk of every remote member (no pre-reduction: the tree spans GPUs) and
     # one copy of each foreign mean chunk.
     hbm_local = 2 * es * D * local_rows
-    hbm_cross = 2 * es * D * Mg * cross_groups
-    nvl_cross = cross_groups * es * (D / world) * ((M - Mg) + (world - 1)) if world > 1 else 0
+    # voided groups of a cross round move the rows whose new rank lives on
+    # another GPU: one full row over NVLink (pull) + its HBM read and write
+    hbm_cross = 2 * es * D * Mg * cross_groups + 2 * es * D * moved
+    nvl_cross = (cross_groups * es * (D / world) * ((M - Mg) + (world - 1))
+                 + es * D * moved) if world > 1 else 0
     peak, _ = peaks()
     t_roof_local = hbm_local / (peak * 1e9) * 1e3
     t_roof_cross = max(hbm_cross / (peak * 1e9), nvl_cross / (NVLINK_GBS * 1e9)) * 1e3
-    vals = torch.tensor([t_ms, lms, cms, t_roof_local, t_roof_cross], dtype=torch.float64,
-                        device="cuda")
+    vals = torch.tensor([t_ms, lms, cms, t_roof_local, t_roof_cross, pa_ms, pb_ms, nvl_cross],
+                        dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    t_max, lmax, cmax, trl, trc = vals.tolist()
+    t_max, lmax, cmax, trl, trc, pa_max, pb_max, nvl_max = vals.tolist()
     sh.close()
     torch.cuda.empty_cache()
     value = N * D * es * steps / (t_max / 1e3) / 1e9
@@ -436,14 +442,17 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
             "local": {"achieved": round(hbm_local / (lmax / 1e3) / 1e9, 1) if lmax else None,
                       "peak": peak, "unit": "GB/s",
                       "frac": round(trl / lmax, 4) if lmax else None},
-            "cross": {"nvlink_ingress_gb_per_gpu": round(nvl_cross / 1e9, 3),
-                      "achieved_nvlink": round(nvl_cross / (cmax / 1e3) / 1e9, 1) if cmax else None,
+            "cross": {"nvlink_ingress_gb_per_gpu": round(nvl_max / 1e9, 3),
+                      "voided_rows_moved_in": moved,
+                      "phase_a_ms": round(pa_max, 3), "phase_b_ms": round(pb_max, 3),
+                      "achieved_nvlink": round(nvl_max / (cmax / 1e3) / 1e9, 1) if cmax else None,
                       "peak_nvlink": NVLINK_GBS, "unit": "GB/s",
                       "frac": round(trc / cmax, 4) if cmax else None},
             "combined_frac": round((trl + trc) / (lmax + cmax), 4) if (lmax + cmax) else None,
             "note": "t_roof = max(HBM bytes / hbm_gbs, NVLink ingress / 770 GB/s) per round, "
                     "busiest GPU, minimal bytes (raw remote member chunks + one copy of each "
-                    "foreign mean chunk, all NVLink traffic as pulls); t_measured = data-plane "
+                    "foreign mean chunk + the voided-group rows whose new rank lives on another "
+                    "GPU, all NVLink traffic as pulls); t_measured = data-plane "
                     "kernels (phase A chunk means + phase B pulls); frac = sum t_roof / sum "
                     "t_measured",
         },

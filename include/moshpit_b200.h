@@ -290,6 +290,13 @@ int moshpit_shard_stats(moshpit_shard* s, int32_t k, uint64_t* cross_rounds,
                         uint64_t* local_active_rows);
 int moshpit_shard_pool(moshpit_shard* s, int32_t k, void** ptr, uint64_t* rows,
                        uint64_t* ld);
+/* Cross-round detail (synchronises): device ms of phase A (chunk means +
+ * voided-row pulls) and phase B (mean-chunk pulls + voided-row writes) as
+ * split by the last moshpit_shard_kernel_time call, and the cumulative
+ * number of voided-group rows that moved INTO rank k (each one row of dim
+ * elements over NVLink -- part of the cross round's minimal traffic). */
+int moshpit_shard_cross_detail(moshpit_shard* s, int32_t k, double* phase_a_ms,
+                               double* phase_b_ms, uint64_t* moved_rows_in);
 
 /* Counter-based synthetic init (bench / tests):
  * x(i,j) = (splitmix64(seed ^ (i<<32) ^ (col0+j)) >> 40) * 2^-24. */

@@ -799,6 +799,13 @@ class Shard:
         check(lib().moshpit_shard_stats(self._h, k, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
 
+    def cross_detail(self, k: int = 0):
+        """(phase A ms, phase B ms) of the cross rounds timed by the last
+        kernel_time() call, and voided rows moved into rank k so far."""
+        a, b, m = C.c_double(0), C.c_double(0), C.c_uint64(0)
+        check(lib().moshpit_shard_cross_detail(self._h, k, C.byref(a), C.byref(b), C.byref(m)))
+        return a.value, b.value, m.value
+
     def kernel_time(self):
         lm, ln, cm, cn = C.c_double(0), C.c_uint64(0), C.c_double(0), C.c_uint64(0)
         check(lib().moshpit_shard_kernel_time(self._h, C.byref(lm), C.byref(ln), C.byref(cm),

@@ -106,6 +106,7 @@ PROTOTYPES = {
     "moshpit_shard_set_timing": (C.c_int, [vp, i32]),
     "moshpit_shard_kernel_time": (C.c_int, [vp, P(dbl), P(u64), P(dbl), P(u64)]),
     "moshpit_shard_stats": (C.c_int, [vp, i32, P(u64), P(u64), P(u64)]),
+    "moshpit_shard_cross_detail": (C.c_int, [vp, i32, P(dbl), P(dbl), P(u64)]),
     "moshpit_shard_pool": (C.c_int, [vp, i32, P(vp), P(u64), P(u64)]),
     "moshpit_fill_synthetic": (C.c_int, [C.c_int, vp, u64, u64, u64, u64, u64, vp]),
 }

@@ -25,6 +25,7 @@
 // synchronise with a P2P flag barrier kernel (no host round-trip).  Emulation
 // mode runs all G "virtual GPUs" as separate pools on one device (tests).
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 
 #include "plane.cuh"
@@ -54,7 +55,8 @@ struct PlaceArgs {
   std::uint32_t* n_moves = nullptr;     // [world]
   std::uint32_t* err = nullptr;         // [1]
   unsigned long long* totals = nullptr; // [0] cross active groups, [1] cross rounds,
-                                        // [2+h] local active rows on GPU h
+                                        // [2+h] local active rows on GPU h,
+                                        // [2+kMaxWorld+h] voided rows moved to GPU h
 };
 
 // Replicated bookkeeping for one round (one CTA, one thread per group).
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
       if (voided && a.dst_row[pos] != a.src_row[pos]) {
         const std::uint32_t h = (std::uint32_t)(a.dst_row[pos] / a.R);
         const std::uint32_t k = atomicAdd(&a.n_moves[h], 1u);
+        atomicAdd(&a.totals[2 + kMaxWorld + h], 1ull);
         a.moves[((std::uint64_t)h * a.R + k) * 2] = a.src_row[pos];
         a.moves[((std::uint64_t)h * a.R + k) * 2 + 1] = a.dst_row[pos];
       }
@@ -413,6 +416,7 @@ struct Shard {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_local, tev_cross;
   std::size_t used_local = 0, used_cross = 0;
+  double last_a_ms = 0.0, last_b_ms = 0.0;  // cross phases of the last kernel_time
 
   ~Shard() {
     for (void* q : opened) cudaIpcCloseMemHandle(q);
@@ -467,6 +471,7 @@ struct Shard {
     int per = 0, sms = 0;
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_mean_kernel<T>,
                                                           kCrossThreads, 0));
+    if (const char* e = std::getenv("MOSHPIT_CROSS_CTAS")) per = std::min(per, std::atoi(e));
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     if (a.n_tiles) cross_mean_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(a);
     MB_LAUNCH_CHECK();
@@ -669,8 +674,8 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     S.n_moves.resize(world * 4 + 16);
     S.err.resize(16);
     MB_CUDA(cudaMemsetAsync(S.err.ptr, 0, 16, st.s));
-    S.totals.resize(8 * (kMaxWorld + 2));
-    MB_CUDA(cudaMemsetAsync(S.totals.ptr, 0, 8 * (kMaxWorld + 2), st.s));
+    S.totals.resize(8 * (2 * kMaxWorld + 2));
+    MB_CUDA(cudaMemsetAsync(S.totals.ptr, 0, 8 * (2 * kMaxWorld + 2), st.s));
     const std::uint32_t npools = S.emulate ? S.world : 1;
     for (std::uint32_t k = 0; k < npools; ++k) {
       S.own_pools.push_back(std::make_unique<DeviceBuffer>(S.R * S.ld * es));
@@ -846,6 +851,13 @@ int moshpit_shard_kernel_time(moshpit_shard* h, double* local_ms, std::uint64_t*
     *local_n = S.used_local;
     *cross_ms = sum(S.tev_cross, S.used_cross);
     *cross_n = S.used_cross;
+    // tev_cross alternates phase A, phase B of each cross round
+    S.last_a_ms = S.last_b_ms = 0.0;
+    for (std::size_t i = 0; i < S.used_cross; ++i) {
+      float ms = 0;
+      MB_CUDA(cudaEventElapsedTime(&ms, S.tev_cross[i].first, S.tev_cross[i].second));
+      (i % 2 == 0 ? S.last_a_ms : S.last_b_ms) += ms;
+    }
     S.used_local = S.used_cross = 0;
   });
 }
@@ -859,12 +871,27 @@ int moshpit_shard_stats(moshpit_shard* h, std::int32_t k, std::uint64_t* cross_r
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     MB_CUDA(cudaDeviceSynchronize());
-    unsigned long long t[kMaxWorld + 2];
+    unsigned long long t[2 * kMaxWorld + 2];
     MB_CUDA(cudaMemcpy(t, S.totals.ptr, sizeof(t), cudaMemcpyDeviceToHost));
     const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
     *cross_rounds = t[1];
     *cross_active_groups = t[0];
     *local_active_rows = t[2 + r];
+  });
+}
+
+int moshpit_shard_cross_detail(moshpit_shard* h, std::int32_t k, double* phase_a_ms,
+                               double* phase_b_ms, std::uint64_t* moved_rows_in) {
+  return guarded([&] {
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    MB_CUDA(cudaDeviceSynchronize());
+    unsigned long long t[2 * kMaxWorld + 2];
+    MB_CUDA(cudaMemcpy(t, S.totals.ptr, sizeof(t), cudaMemcpyDeviceToHost));
+    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    *phase_a_ms = S.last_a_ms;
+    *phase_b_ms = S.last_b_ms;
+    *moved_rows_in = t[2 + kMaxWorld + r];
   });
 }
 
