@@ -291,8 +291,9 @@ __global__ void logit_grad(T* __restrict__ x, std::uint64_t ld, std::uint64_t di
 // be summed sequentially in k from 0.0 with separately rounded products (the
 // reference's order), so they run on the fp64 SIMT pipes (DMUL + DADD, no
 // tensor cores, no FMA): 64x64 output tiles per 256-thread CTA, 4x4 outputs
-// per thread, k staged through shared memory 16 at a time.  Each output's
-// k-loop is still the plain sequential chain.
+// per thread, k staged through double-buffered shared memory 16 at a time
+// (the next tile's global loads in flight while the current one is used).
+// Each output's k-loop is still the plain sequential chain.
 constexpr int kLT = 64, kLK = 16;
 
 template <typename T>
@@ -301,33 +302,54 @@ __global__ void __launch_bounds__(256)
                       std::uint64_t dim, const double* __restrict__ xs,
                       const double* __restrict__ ys, std::uint64_t S,
                       double* __restrict__ coeff) {
-  __shared__ double As[kLK][kLT + 1];  // theta[i][k] -> As[k][i - i0]
-  __shared__ double Bs[kLK][kLT + 1];  // xs[s][k]    -> Bs[k][s - s0]
+  // double-buffered k-tiles; the next tile's global loads are in flight
+  // (registers) while the current one is multiplied
+  __shared__ double As[2][kLK][kLT + 1];  // theta[i][k] -> As[.][k][i - i0]
+  __shared__ double Bs[2][kLK][kLT + 1];  // xs[s][k]    -> Bs[.][k][s - s0]
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const std::uint64_t i0 = (std::uint64_t)blockIdx.y * kLT, s0 = (std::uint64_t)blockIdx.x * kLT;
+  constexpr int kPer = kLT * kLK / 256;  // elements of each tile loaded per thread
+  double ra[kPer], rb[kPer];
+  auto fetch = [&](std::uint64_t k0) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      const int r = e / kLK, kk = e % kLK;
+      const std::uint64_t k = k0 + kk, i = i0 + r, sm = s0 + r;
+      ra[q] = (i < n && k < dim) ? (double)x[i * ld + k] : 0.0;
+      rb[q] = (sm < S && k < dim) ? xs[sm * dim + k] : 0.0;
+    }
+  };
+  auto stash = [&](int b) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      const int r = e / kLK, kk = e % kLK;
+      As[b][kk][r] = ra[q];
+      Bs[b][kk][r] = rb[q];
+    }
+  };
   double acc[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int cur = 0;
   for (std::uint64_t k0 = 0; k0 < dim; k0 += kLK) {
-    for (int e = threadIdx.x; e < kLT * kLK; e += 256) {
-      const int r = e / kLK, kk = e % kLK;
-      const std::uint64_t k = k0 + kk;
-      const std::uint64_t i = i0 + r, sm = s0 + r;
-      As[kk][r] = (i < n && k < dim) ? (double)x[i * ld + k] : 0.0;
-      Bs[kk][r] = (sm < S && k < dim) ? xs[sm * dim + k] : 0.0;
-    }
-    __syncthreads();
+    const bool more = k0 + kLK < dim;
+    if (more) fetch(k0 + kLK);
     const int kn = dim - k0 < (std::uint64_t)kLK ? (int)(dim - k0) : kLK;
     if (kn == kLK) {
 #pragma unroll
       for (int kk = 0; kk < kLK; ++kk) {
         double a[4], b[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+        for (int r = 0; r < 4; ++r) a[r] = As[cur][kk][ty + 16 * r];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+        for (int c = 0; c < 4; ++c) b[c] = Bs[cur][kk][tx + 16 * c];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -339,10 +361,13 @@ __global__ void __launch_bounds__(256)
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(Bs[kk][tx + 16 * c], As[kk][ty + 16 * r]));
+            acc[r][c] = __dadd_rn(acc[r][c],
+                                  __dmul_rn(Bs[cur][kk][tx + 16 * c], As[cur][kk][ty + 16 * r]));
       }
     }
+    if (more) stash(cur ^ 1);
     __syncthreads();
+    cur ^= 1;
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -358,46 +383,75 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256)
+// Gradient tiles are TM x TN (4 x 4 outputs per thread, TM*TN/16 threads).
+// 64 x 64 is used: at N = dim = 1024 its 256 tiles leave 108 SMs with two
+// and 40 with one (fp64 pipe 57 % vs 73 % for the 1024-tile margins), but
+// 32 x 32 tiles (1024, balanced) measured slower still (0.88 vs 0.83 ms):
+// half the operand reuse per shared-memory load.
+template <typename T, int TM, int TN>
+__global__ void __launch_bounds__(TM * TN / 16)
     logit_grad_tiled(T* __restrict__ x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                      const double* __restrict__ xs, std::uint64_t S,
                      const double* __restrict__ coeff, double l2, T gamma,
                      const T* __restrict__ noise, double coord_std, int philox_mode,
                      std::uint64_t seed, std::uint64_t step, std::uint32_t* nonfinite,
                      double* nsq_out) {
-  __shared__ double As[kLK][kLT + 1];            // coeff[i][s] -> As[s - k0][i - i0]
-  __shared__ __align__(16) double Bs[kLK][kLT];  // xs[s][j]    -> Bs[s - k0][j - j0]
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const std::uint64_t i0 = (std::uint64_t)blockIdx.y * kLT, j0 = (std::uint64_t)blockIdx.x * kLT;
+  constexpr int NT = TM * TN / 16, CW = TN / 4, RS = TM / 4;
+  __shared__ double As[2][kLK][TM + 1];            // coeff[i][s] -> As[.][s - k0][i - i0]
+  __shared__ __align__(16) double Bs[2][kLK][TN];  // xs[s][j]    -> Bs[.][s - k0][j - j0]
+  const int tx = threadIdx.x % CW, ty = threadIdx.x / CW;
+  const std::uint64_t i0 = (std::uint64_t)blockIdx.y * TM, j0 = (std::uint64_t)blockIdx.x * TN;
+  constexpr int kPa = TM * kLK / NT, kPb = TN * kLK / NT;
+  double ra[kPa], rb[kPb];
+  auto fetch = [&](std::uint64_t k0) {
+#pragma unroll
+    for (int q = 0; q < kPa; ++q) {
+      const int e = threadIdx.x + NT * q;
+      const int r = e / kLK, kk = e % kLK;
+      const std::uint64_t i = i0 + r, k = k0 + kk;
+      ra[q] = (i < n && k < S) ? coeff[i * S + k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kPb; ++q) {
+      const int e = threadIdx.x + NT * q;
+      const int kk = e / TN, cc = e % TN;
+      const std::uint64_t k = k0 + kk, j = j0 + cc;
+      rb[q] = (k < S && j < dim) ? xs[k * dim + j] : 0.0;
+    }
+  };
+  auto stash = [&](int b) {
+#pragma unroll
+    for (int q = 0; q < kPa; ++q) {
+      const int e = threadIdx.x + NT * q;
+      As[b][e % kLK][e / kLK] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < kPb; ++q) {
+      const int e = threadIdx.x + NT * q;
+      Bs[b][e / TN][e % TN] = rb[q];
+    }
+  };
   double acc[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int cur = 0;
   for (std::uint64_t k0 = 0; k0 < S; k0 += kLK) {
-    for (int e = threadIdx.x; e < kLT * kLK; e += 256) {
-      {
-        const int r = e / kLK, kk = e % kLK;
-        const std::uint64_t i = i0 + r, k = k0 + kk;
-        As[kk][r] = (i < n && k < S) ? coeff[i * S + k] : 0.0;
-      }
-      {
-        const int kk = e / kLT, cc = e % kLT;
-        const std::uint64_t k = k0 + kk, j = j0 + cc;
-        Bs[kk][cc] = (k < S && j < dim) ? xs[k * dim + j] : 0.0;
-      }
-    }
-    __syncthreads();
+    const bool more = k0 + kLK < S;
+    if (more) fetch(k0 + kLK);
     const int kn = S - k0 < (std::uint64_t)kLK ? (int)(S - k0) : kLK;
     if (kn == kLK) {
 #pragma unroll
       for (int kk = 0; kk < kLK; ++kk) {
         double a[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
-        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4]);
-        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[kk][tx * 4 + 2]);
+        for (int r = 0; r < 4; ++r) a[r] = As[cur][kk][ty + RS * r];
+        const double2 b01 = *reinterpret_cast<const double2*>(&Bs[cur][kk][tx * 4]);
+        const double2 b23 = *reinterpret_cast<const double2*>(&Bs[cur][kk][tx * 4 + 2]);
         const double b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -410,17 +464,20 @@ __global__ void __launch_bounds__(256)
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(As[kk][ty + 16 * r], Bs[kk][tx * 4 + c]));
+            acc[r][c] = __dadd_rn(acc[r][c],
+                                  __dmul_rn(As[cur][kk][ty + RS * r], Bs[cur][kk][tx * 4 + c]));
       }
     }
+    if (more) stash(cur ^ 1);
     __syncthreads();
+    cur ^= 1;
   }
   using O = SOps<T>;
   double nsq = 0.0;
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
-    const std::uint64_t i = i0 + ty + 16 * r;
+    const std::uint64_t i = i0 + ty + RS * r;
     if (i >= n) continue;
     float z[4] = {0.f, 0.f, 0.f, 0.f};
     if (philox_mode) philox_normals4(seed, step, i, (j0 >> 2) + tx, z);
@@ -546,7 +603,9 @@ struct SgdRun {
     logit_coeff_tiled<T><<<dim3((unsigned)((S + kLT - 1) / kLT), ty), 256, 0, s>>>(
         static_cast<const T*>(x), n, ld, dim, lxs.as<double>(), lys.as<double>(), S,
         coeff.as<double>());
-    logit_grad_tiled<T><<<dim3((unsigned)((dim + kLT - 1) / kLT), ty), 256, 0, s>>>(
+    constexpr int GT = 64;  // gradient tile (see logit_grad_tiled)
+    logit_grad_tiled<T, GT, GT><<<dim3((unsigned)((dim + GT - 1) / GT),
+                                       (unsigned)((n + GT - 1) / GT)), GT * GT / 16, 0, s>>>(
         static_cast<T*>(x), n, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, (T)gamma,
         nz, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
         npart.as<double>() + k * 148 * 16);
