@@ -43,6 +43,9 @@ CONFIGS = {
     # C5 as written (8192 peers on 8^4) is rejected by the reference
     # (protocols.hpp:116-117); C5v is the closest valid config.
     "C5v": (8, 4, 4096, 18_000_000, 0.0, 4),
+    # the north-star 1-GPU target: C3 at full size (419 GB of fp32 state)
+    # runs as resident D-slabs (measure_full_slabbed)
+    "C3": (16, 3, 4096, 25_600_000, 0.0, 3),
 }
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 PROTOCOL_SEED = 7
@@ -316,6 +319,12 @@ def run_mine(args):
         except Exception as exc:  # noqa: BLE001
             peer = {"error": str(exc)}
 
+    full = None
+    if rank == 0 and world == 1 and not args.no_full:
+        try:
+            full = measure_full_slabbed(mb, torch, "C3", local)
+        except Exception as exc:  # noqa: BLE001
+            full = {"error": str(exc)}
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(mb, cfg)
@@ -364,6 +373,7 @@ def run_mine(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "peer_sharded": peer,
+            "c3_full_1gpu": full,
             "sgd_c4": sgd,
         }
         print(json.dumps(line), flush=True)
@@ -459,6 +469,63 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     }
 
 
+def measure_full_slabbed(mb, torch, cfg, local, slabs=4):
+    """A config whose state exceeds one GPU (C3: 4096 x 25.6M fp32 = 419 GB),
+    every coordinate of it, as `slabs` resident D-slabs (coordinates are
+    independent): per slab, counter-based init on the device
+    (timed separately), a fresh engine with the config's protocol seed (the
+    same draws and group tables for every slab) and the config's R rounds.
+    value = N * D * 4 * R / (sum of the slabs' round times)."""
+    M, d, N, D, p, R = CONFIGS[cfg]
+    W = -(-D // slabs)
+    W = (W + 3) // 4 * 4
+    stream = torch.cuda.current_stream()
+    x = torch.empty((N, W), dtype=torch.float32, device="cuda")
+    t_rounds = t_init = k_ms = 0.0
+    rows = launches = 0
+    for c0 in range(0, D, W):
+        w = min(W, D - c0)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        mb.fill_synthetic(x, INIT_SEED, dim=w, col0=c0)
+        e[1].record(stream)
+        eng = mb.Engine(mb.GridConfig(M, d, R), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
+                        device=local)
+        eng.set_timing(True)
+        r0 = eng.stats()[1]
+        torch.cuda.synchronize()
+        e[2].record(stream)
+        for _ in range(R):
+            eng.round(x, dim=w)
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        t_init += e[0].elapsed_time(e[1])
+        t_rounds += e[2].elapsed_time(e[3])
+        km, kn = eng.kernel_time()
+        k_ms += km
+        launches += kn
+        rows += (eng.stats()[1] - r0) * w
+        eng.close()
+    del x
+    torch.cuda.empty_cache()
+    peak, _ = peaks()
+    alg = 2 * 4 * rows  # rows x columns actually averaged, read + written once per round
+    return {"workload": f"{cfg}: {N} peers on {M}^{d}, D={D} fp32 (full size, "
+                        f"{N * D * 4 / 1e9:.1f} GB) as {-(-D // W)} resident D-slabs of {W} "
+                        f"columns, {R} rounds each",
+            "metric": "peer-vector GB/s averaged per Moshpit round",
+            "value": round(N * D * 4 * R / (t_rounds / 1e3) / 1e9, 3), "unit": "GB/s",
+            "ms_per_round": round(t_rounds / R, 3),
+            "init_ms_total": round(t_init, 3),
+            "roofline": {"bound": "hbm", "kernel": "group_mean_register (kernel 2)",
+                         "achieved": round(alg / (k_ms / 1e3) / 1e9, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(alg / (k_ms / 1e3) / 1e9 / peak, 4),
+                         "launches": launches,
+                         "frac_of_round_time": round(alg / (t_rounds / 1e3) / 1e9 / peak, 4)},
+            "timing": "CUDA events around each slab's R rounds (host draws + kernel 1 + "
+                      "kernel 2); the on-device init is reported apart"}
+
+
 def measure_sgd_c4(mb, steps=20, sigma=1.0):
     """C4 (configs[3]): Moshpit SGD, 1024 peers on 32x32, Quadratic(D=2^20,
     L=1, mu=0.1, target ~ N(0,1)), gamma=0.1, tau=1, inner=d=2, fp32,
@@ -550,11 +617,14 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C2", choices=[c for c in sorted(CONFIGS) if c != "C3"],
+                    help="C3 at full size exceeds one GPU: see the c3_full_1gpu key")
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sgd", action="store_true", help="skip the C4 Moshpit-SGD measurement")
+    ap.add_argument("--no-full", action="store_true",
+                    help="skip the full-size C3 (slab-streamed) measurement at N=1")
     ap.add_argument("--no-peer", action="store_true",
                     help="skip the peer-sharded (NVLink) measurement attached at N>1")
     ap.add_argument("--mode", default="coord", choices=["coord", "peer"],
