@@ -312,19 +312,30 @@ def run_mine(args):
 
     peer = None
     if world > 1 and not args.no_peer:
-        pcfg = "C5v" if 8 % world == 0 and world >= 4 else "C2"
+        # C5-valid (the north-star multi-GPU config, 295 GB) wherever its
+        # 1/world share fits this GPU (world >= 2 on 180 GB B200s), else C2
+        Mv, dv, Nv, Dv, _, _ = CONFIGS["C5v"]
+        need = Nv // world * ((Dv + 3) // 4 * 4) * 4 + (4 << 30)
+        fits = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] >= need else 0.0],
+                            device="cuda")
+        dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+        pcfg = "C5v" if Mv % world == 0 and fits.item() > 0 else "C2"
         try:
             peer = run_peer(mb, torch, dist, pcfg, max(8, min(args.steps, 40)), 4, rank, world,
                             local)
         except Exception as exc:  # noqa: BLE001
             peer = {"error": str(exc)}
 
-    full = None
+    full = full_c5 = None
     if rank == 0 and world == 1 and not args.no_full:
         try:
             full = measure_full_slabbed(mb, torch, "C3", local)
         except Exception as exc:  # noqa: BLE001
             full = {"error": str(exc)}
+        try:
+            full_c5 = measure_full_slabbed(mb, torch, "C5v", local, slabs=3)
+        except Exception as exc:  # noqa: BLE001
+            full_c5 = {"error": str(exc)}
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(mb, cfg)
@@ -374,6 +385,7 @@ def run_mine(args):
             "cpu_baseline": cpu,
             "peer_sharded": peer,
             "c3_full_1gpu": full,
+            "c5v_full_1gpu": full_c5,
             "sgd_c4": sgd,
         }
         print(json.dumps(line), flush=True)
@@ -470,7 +482,8 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
 
 
 def measure_full_slabbed(mb, torch, cfg, local, slabs=4):
-    """A config whose state exceeds one GPU (C3: 4096 x 25.6M fp32 = 419 GB),
+    """A config whose state exceeds one GPU (C3: 4096 x 25.6M fp32 = 419 GB;
+    C5-valid: 4096 x 18M = 295 GB, the 1-GPU point of the multi-GPU series),
     every coordinate of it, as `slabs` resident D-slabs (coordinates are
     independent): per slab, counter-based init on the device
     (timed separately), a fresh engine with the config's protocol seed (the
