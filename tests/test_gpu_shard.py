@@ -74,3 +74,40 @@ def test_emulated_c5_valid_slab(mb, oracle):
         _, want = oracle.run_moshpit(M, d, init, 0.0, 7, R)
         assert bits_equal(np.ascontiguousarray(got[:, c0:c0 + 16]), want)
     sh.close()
+
+
+@pytest.mark.parametrize("M,d,p,R,world", [(32, 2, 0.01, 10, 2), (8, 4, 0.05, 8, 4),
+                                           (8, 2, 0.2, 7, 8), (16, 3, 0.0, 6, 4)])
+def test_voided_row_moves_counted(mb, oracle, M, d, p, R, world):
+    """moshpit_shard_cross_detail counts, per GPU, the voided-group rows whose
+    new rank lives on another GPU (the cross round's extra NVLink traffic):
+    equal to a replay of the oracle's trace (cells, then x_axis := rank)."""
+    import torch
+    n = M ** d
+    sh = mb.Shard(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), 4, world=world,
+                  emulate=True)
+    sh.fill_synthetic(INIT_SEED)
+    for _ in range(R):
+        sh.round()
+    torch.cuda.synchronize()
+    got = [sh.cross_detail(k)[2] for k in range(world)]
+    sh.close()
+    tr = oracle.trace(M, d, n, p, 7, R)
+    cells = tr["cells"].astype(np.int64)
+    digits = np.stack([(cells // M ** k) % M for k in range(d)], axis=1)
+    mg = M // world
+    want = [0] * world
+    for t in range(R):
+        axis = t % d
+        off, mem = tr["group_off"][t], tr["members"][t]
+        for g in range(int(tr["n_groups"][t])):
+            ids = mem[off[g]:off[g + 1]]
+            for rank, i in enumerate(ids):
+                if axis == d - 1 and tr["void"][t][g]:
+                    old, new = digits[i, axis] // mg, rank // mg
+                    if old != new:
+                        want[new] += 1
+                digits[i, axis] = rank
+    assert got == want
+    if p == 0.0:
+        assert sum(got) == 0
