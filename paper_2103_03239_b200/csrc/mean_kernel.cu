@@ -616,6 +616,17 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
     MB_LAUNCH_CHECK();
     return;
   }
+  // MOSHPIT_K2_LEAF=4|8: the leaf-streamed body (4- / 8-member load batches)
+  // for groups of <= 32 instead of the register form (measurement knob).
+  static const int leaf_k2 = [] {
+    const char* e = std::getenv("MOSHPIT_K2_LEAF");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (variant == 0 && leaf_k2 && max_group <= 32) {
+    launch_group_mean_leaf<T>(state, ld, dim, members, goff, act, counts, leaf_k2 == 8 ? 1 : 0,
+                              s);
+    return;
+  }
   const bool bulk_ok = max_group <= (std::uint32_t)kBulkMaxRows;
   if (variant == 2 || (variant == 0 && bulk_ok && bulk_default())) {
     if (!bulk_ok) throw std::invalid_argument("bulk kernel: groups larger than 32 members");

@@ -147,11 +147,16 @@ __device__ __forceinline__ double2 vdivn(double2 a, std::uint32_t n) {
 // MODE 0: 8-member load batches; 1: 8-member batches with the next leaf
 // prefetched; 2 (default): 4-member batches at 64 registers, 8 CTAs/SM --
 // more warps to hide the Philox/SFU latency of the device-noise step and the
-// load latency of the plain one.  Same arithmetic in every mode.
+// load latency of the plain one.  Same arithmetic in every mode.  MODE 3 / 4
+// are the 4- / 8-wide forms WITHOUT the step: a plain Kernel-2 round (used
+// for groups of <= 8 members, where the register form's 32-slot body caps
+// residency at 3 CTAs/SM).
 template <typename T, bool NOISY, int MODE>
-__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
+__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE == 3) ? 8 : 6)
     group_mean_step_leaf(LArgs<T> a) {
   constexpr bool PREFETCH = MODE == 1;
+  constexpr bool STEP = MODE < 3;
+  constexpr bool WIDE4 = MODE == 2 || MODE == 3;
   using V = typename LVec<T>::V;
   constexpr int kV = LVec<T>::kN;
   __shared__ std::uint32_t sids[32];
@@ -187,8 +192,11 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
     if (col >= nvec) continue;
     const std::uint64_t j0 = col * kV;
     const bool full = j0 + kV <= dim;
-    const V c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
-    const V t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
+    V c = vz<V>(), t = vz<V>();
+    if constexpr (STEP) {
+      c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
+      t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
+    }
     V* const colp = base + col;
 
     // predicated 8-wide leaf loads (unloaded slots are zero and never used)
@@ -202,8 +210,9 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (b + k < e) {
-          step_vec<T, NOISY>(buf[k], c, t, gamma, coord_std, seed, step_no, sids[b + k], j0,
-                             full, dim, chk, nsq);
+          if constexpr (STEP)
+            step_vec<T, NOISY>(buf[k], c, t, gamma, coord_std, seed, step_no, sids[b + k], j0,
+                               full, dim, chk, nsq);
           s = vsum(s, buf[k]);
         }
       }
@@ -215,7 +224,7 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
     // L0 | L0+L1 | L0+(L1+L2) | (L0+L1)+(L2+L3) for nl = 1..4.
     const std::uint32_t r = nl == 4 ? 2u : 1u;
     V P = vz<V>(), Q = vz<V>();
-    if constexpr (MODE == 2) {
+    if constexpr (WIDE4) {
       std::uint32_t lb = b0;
 #pragma unroll 1
       for (std::uint32_t l = 0; l < nl; ++l) {
@@ -230,8 +239,9 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if (c0 + k < le) {
-              step_vec<T, NOISY>(X[k], c, t, gamma, coord_std, seed, step_no, sids[c0 + k], j0,
-                                 full, dim, chk, nsq);
+              if constexpr (STEP)
+                step_vec<T, NOISY>(X[k], c, t, gamma, coord_std, seed, step_no, sids[c0 + k],
+                                   j0, full, dim, chk, nsq);
               sl = vsum(sl, X[k]);
             }
           }
@@ -284,10 +294,10 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : MODE == 2 ? 8 : 6)
       for (int i = 0; i < kLThreads / 32; ++i) s += red[i];
       a.noise_partial[blockIdx.x] = s;
     }
-  } else if (threadIdx.x == 0 && a.noise_partial) {
+  } else if (STEP && threadIdx.x == 0 && a.noise_partial) {
     a.noise_partial[blockIdx.x] = 0.0;
   }
-  if (chk != T(0)) atomicOr(a.nonfinite, 1u);
+  if (STEP && chk != T(0)) atomicOr(a.nonfinite, 1u);
 }
 
 template <typename T, bool NOISY, int MODE>
@@ -353,6 +363,37 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
   }
   MB_LAUNCH_CHECK();
 }
+
+// Plain Kernel-2 round through the leaf-streamed body (groups of <= 32).
+template <typename T>
+void launch_group_mean_leaf(T* state, std::uint64_t ld, std::uint64_t dim,
+                            const std::uint32_t* members, const std::uint32_t* goff,
+                            const std::uint32_t* act, const std::uint32_t* counts, int wide8,
+                            cudaStream_t s) {
+  if (dim == 0) return;
+  constexpr int kV = LVec<T>::kN;
+  LArgs<T> a{};
+  a.state = state;
+  a.ld_vec = ld / kV;
+  a.nvec = (dim + kV - 1) / kV;
+  a.n_tiles = (a.nvec + kLThreads - 1) / kLThreads;
+  a.members = members;
+  a.goff = goff;
+  a.act = act;
+  a.counts = counts;
+  a.dim = dim;
+  if (wide8) launch_leaf<T, false, 4>(a, s);
+  else launch_leaf<T, false, 3>(a, s);
+  MB_LAUNCH_CHECK();
+}
+template void launch_group_mean_leaf<float>(float*, std::uint64_t, std::uint64_t,
+                                            const std::uint32_t*, const std::uint32_t*,
+                                            const std::uint32_t*, const std::uint32_t*, int,
+                                            cudaStream_t);
+template void launch_group_mean_leaf<double>(double*, std::uint64_t, std::uint64_t,
+                                             const std::uint32_t*, const std::uint32_t*,
+                                             const std::uint32_t*, const std::uint32_t*, int,
+                                             cudaStream_t);
 
 int group_mean_step_grid(bool f64, bool noisy, int mode) {
   if (mode < 0) mode = 2;
