@@ -292,6 +292,107 @@ __global__ void __launch_bounds__(kCrossThreads)
   }
 }
 
+// Copy-engine cross round (MOSHPIT_CROSS_CE=1).  SM loads from peer HBM top
+// out at ~660 GB/s of NVLink ingress per GPU, one large copy-engine pull
+// reaches ~760 GB/s (profiles/ce_probe.cu, profiles/r01/ce_probe.txt).  In
+// the round itself the staged form measured no faster (C5-valid on 2 GPUs:
+// phase A 115 vs 114 ms, phase B slower without the fused fan-out), so the
+// SM-pull kernels stay the default; this path is kept, tested, for the
+// comparison.  Phase A
+// stages the raw chunk-g vectors of each group's REMOTE members into local
+// HBM with peer copies (one async copy per member chunk on two copy streams,
+// double-buffered by batches of groups) and this kernel evaluates the same
+// tree from local memory: member k reads its local row, or staging slot
+// (group-in-batch * nrem + k-th remote member) when it lives on another GPU.
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads, 3)
+    cross_staged_kernel(CrossArgs<T> a, const T* stage, std::uint32_t gb, std::uint32_t ge,
+                        std::uint32_t nrem) {
+  using V = typename V16s<T>::type;
+  __shared__ const V* s_src[32];
+  __shared__ V* s_dst[32];
+  const std::uint64_t cvec = a.c1 - a.c0;
+  const std::uint64_t n_items = (std::uint64_t)(ge - gb) * a.n_tiles;
+  std::uint32_t cached = 0xffffffffu, cnt = 0;
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t gi = gb + (std::uint32_t)(w / a.n_tiles);
+    const std::uint32_t g = a.act[gi];
+    if (g != cached) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const std::uint32_t beg = a.goff[g];
+        cnt = a.goff[g + 1] - beg;
+        std::uint32_t slot = 0;
+        for (std::uint32_t k = 0; k < cnt; ++k) {
+          const std::uint32_t sr = a.src_row[beg + k], d = a.dst_row[beg + k];
+          // row-relative pointers: element col of member k is at s_src[k][col - c0]
+          if (sr / a.R == a.me)
+            s_src[k] = reinterpret_cast<const V*>(a.pools[a.me]) + (sr % a.R) * a.ld_vec + a.c0;
+          else
+            s_src[k] = reinterpret_cast<const V*>(stage) +
+                       ((std::uint64_t)(gi - gb) * nrem + slot++) * cvec;
+          const std::uint32_t dg = (std::uint32_t)(d / a.R);
+          s_dst[k] = dg == a.me ? reinterpret_cast<V*>(a.pools[dg]) + (d % a.R) * a.ld_vec + a.c0
+                                : nullptr;
+        }
+      }
+      cached = g;
+      __syncthreads();
+      cnt = a.goff[g + 1] - a.goff[g];
+    }
+    const std::uint64_t rel = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    if (rel >= cvec) continue;
+    switch (cnt) {
+#define MB_SCASE(N)                                          \
+  case N:                                                    \
+    cross_fixed<N, V>((V* const*)s_src, s_dst, rel);         \
+    break;
+      MB_SCASE(1) MB_SCASE(2) MB_SCASE(3) MB_SCASE(4) MB_SCASE(5) MB_SCASE(6) MB_SCASE(7)
+      MB_SCASE(8) MB_SCASE(9) MB_SCASE(10) MB_SCASE(11) MB_SCASE(12) MB_SCASE(13)
+      MB_SCASE(14) MB_SCASE(15) MB_SCASE(16) MB_SCASE(17) MB_SCASE(18) MB_SCASE(19)
+      MB_SCASE(20) MB_SCASE(21) MB_SCASE(22) MB_SCASE(23) MB_SCASE(24) MB_SCASE(25)
+      MB_SCASE(26) MB_SCASE(27) MB_SCASE(28) MB_SCASE(29) MB_SCASE(30) MB_SCASE(31)
+      MB_SCASE(32)
+#undef MB_SCASE
+      default: break;
+    }
+  }
+}
+
+// Phase B of the copy-engine round: the foreign chunk means were copied (by
+// the copy engines) into each group's FIRST local member row; fan them out to
+// the group's other local member rows (local HBM only; nothing for Mg = 1).
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads)
+    local_fanout_kernel(CrossArgs<T> a, std::uint64_t nvec) {
+  using V = typename V16s<T>::type;
+  __shared__ V* s_rows[32];
+  __shared__ std::uint32_t s_n;
+  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  std::uint32_t cached = 0xffffffffu;
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t g = a.act[w / a.n_tiles];
+    if (g != cached) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        std::uint32_t k = 0;
+        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
+          const std::uint32_t d = a.dst_row[pos];
+          if (d / a.R == a.me)
+            s_rows[k++] = reinterpret_cast<V*>(a.pools[a.me]) + (d % a.R) * a.ld_vec;
+        }
+        s_n = k;
+      }
+      cached = g;
+      __syncthreads();
+    }
+    const std::uint64_t col = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    if (col >= nvec || (col >= a.c0 && col < a.c1)) continue;
+    const V v = s_rows[0][col];
+    for (std::uint32_t k = 1; k < s_n; ++k) s_rows[k][col] = v;
+  }
+}
+
 // Voided cross groups: rows whose owner GPU changes are pulled into staging
 // (phase 0), then written to their new rows after a barrier (phase 1).
 template <typename T>
@@ -417,8 +518,20 @@ struct Shard {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_local, tev_cross;
   std::size_t used_local = 0, used_cross = 0;
   double last_a_ms = 0.0, last_b_ms = 0.0;  // cross phases of the last kernel_time
+  // copy-engine cross round (MOSHPIT_CROSS_CE=1; the default is the SM-pull
+  // kernels): host copy of the replicated tables, two copy streams with their
+  // staging buffers, and the events that order them against the main stream
+  bool ce = false;
+  PinnedBuffer htab;
+  std::unique_ptr<StreamHolder> cstream[2];
+  DeviceBuffer cstage[2];
+  cudaEvent_t ev_copied[2] = {}, ev_free[2] = {}, ev_go = nullptr;
+  std::vector<void*> cdst, csrc;
+  std::vector<std::size_t> csize;
 
   ~Shard() {
+    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1], ev_go})
+      if (e) cudaEventDestroy(e);
     for (void* q : opened) cudaIpcCloseMemHandle(q);
     for (auto* v : {&tev_local, &tev_cross})
       for (auto& pr : *v) {
@@ -500,6 +613,153 @@ struct Shard {
     MB_LAUNCH_CHECK();
   }
 
+  // Copy a list of (dst, src, bytes) on stream cs: one async copy each (the
+  // copy engines take peer pointers of the IPC-mapped pools directly).
+  void copy_list(cudaStream_t cs) {
+    for (std::size_t i = 0; i < cdst.size(); ++i)
+      MB_CUDA(cudaMemcpyAsync(cdst[i], csrc[i], csize[i], cudaMemcpyDefault, cs));
+    cdst.clear();
+    csrc.clear();
+    csize.clear();
+  }
+
+  void ce_init() {
+    if (cstream[0]) return;
+    for (int i = 0; i < 2; ++i) {
+      cstream[i] = std::make_unique<StreamHolder>();
+      MB_CUDA(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
+      MB_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
+    MB_CUDA(cudaEventCreateWithFlags(&ev_go, cudaEventDisableTiming));
+  }
+
+  // Host copy of the cross round's replicated tables (synchronises s once).
+  void ce_fetch_tables(cudaStream_t s) {
+    const std::uint64_t nn = n();
+    htab.resize((4 * nn + 8) * 4);
+    auto* h = htab.as<std::uint32_t>();
+    MB_CUDA(cudaMemcpyAsync(h, src_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + nn, dst_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 2 * nn, plane->goff.ptr, (nn + 1) * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 3 * nn + 1, act_cross.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 4 * nn + 1, cnt_cross.ptr, 16, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaStreamSynchronize(s));
+  }
+
+  template <typename T>
+  CrossArgs<T> cross_args(std::uint32_t r, bool full_row) {
+    CrossArgs<T> a;
+    for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
+    a.ld_vec = ld * es / 16;
+    a.R = R;
+    const std::uint64_t nv = nvec();
+    a.c0 = nv * r / world;
+    a.c1 = nv * (r + 1) / world;
+    a.n_tiles = ((full_row ? nv : a.c1 - a.c0) + kCrossThreads - 1) / kCrossThreads;
+    a.me = r;
+    a.world = world;
+    a.goff = plane->goff.as<std::uint32_t>();
+    a.src_row = src_row.as<std::uint32_t>();
+    a.dst_row = dst_row.as<std::uint32_t>();
+    a.act = act_cross.as<std::uint32_t>();
+    a.cnt = cnt_cross.as<std::uint32_t>();
+    return a;
+  }
+
+  // Phase A for rank r: staged remote chunks (copy engines) + tree kernel.
+  template <typename T>
+  void cross_ce(std::uint32_t r, cudaStream_t s) {
+    ce_init();
+    const std::uint64_t nn = n();
+    const auto* h = htab.as<std::uint32_t>();
+    const std::uint32_t* hsrc = h;
+    const std::uint32_t* hgoff = h + 2 * nn;
+    const std::uint32_t* hact = h + 3 * nn + 1;
+    const std::uint32_t nact = h[4 * nn + 1 + 1];
+    CrossArgs<T> a = cross_args<T>(r, false);
+    const std::uint64_t cbytes = (a.c1 - a.c0) * 16;
+    if (nact == 0 || cbytes == 0) return;
+    const std::uint32_t nrem = M - Mg;  // full grid: Mg members of a line per GPU
+    const std::uint64_t per_group = (std::uint64_t)nrem * cbytes;
+    std::uint32_t B = (std::uint32_t)std::max<std::uint64_t>(
+        1, std::min<std::uint64_t>(nact, (512ull << 20) / std::max<std::uint64_t>(per_group, 1)));
+    for (int i = 0; i < 2; ++i) cstage[i].resize(B * per_group + 16);
+    int per = 0, sms = 0;
+    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_staged_kernel<T>,
+                                                          kCrossThreads, 0));
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    MB_CUDA(cudaEventRecord(ev_go, s));  // after the barrier: peers' rows are final
+    for (int i = 0; i < 2; ++i) {
+      MB_CUDA(cudaStreamWaitEvent(cstream[i]->s, ev_go, 0));
+    }
+    std::uint32_t batch = 0;
+    for (std::uint32_t gb = 0; gb < nact; gb += B, ++batch) {
+      const std::uint32_t ge = std::min(nact, gb + B);
+      const int slot = batch & 1;
+      cudaStream_t cs = cstream[slot]->s;
+      if (batch >= 2) MB_CUDA(cudaStreamWaitEvent(cs, ev_free[slot], 0));
+      char* st = cstage[slot].as<char>();
+      for (std::uint32_t gi = gb; gi < ge; ++gi) {
+        const std::uint32_t g = hact[gi];
+        std::uint32_t k = 0;
+        for (std::uint32_t pos = hgoff[g]; pos < hgoff[g + 1]; ++pos) {
+          const std::uint32_t sr = hsrc[pos];
+          if (sr / R == r) continue;
+          cdst.push_back(st + ((std::uint64_t)(gi - gb) * nrem + k++) * cbytes);
+          csrc.push_back(static_cast<char*>(pools[sr / R]) + (sr % R) * ld * es + a.c0 * 16);
+          csize.push_back(cbytes);
+        }
+      }
+      copy_list(cs);
+      MB_CUDA(cudaEventRecord(ev_copied[slot], cs));
+      MB_CUDA(cudaStreamWaitEvent(s, ev_copied[slot], 0));
+      cross_staged_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(
+          a, cstage[slot].as<T>(), gb, ge, nrem);
+      MB_LAUNCH_CHECK();
+      MB_CUDA(cudaEventRecord(ev_free[slot], s));
+    }
+  }
+
+  // Phase B for rank r: copy-engine pulls of every foreign chunk mean into
+  // the group's first local member row, then the local fan-out.
+  template <typename T>
+  void pull_ce(std::uint32_t r, cudaStream_t s) {
+    if (world < 2) return;
+    const std::uint64_t nn = n();
+    const auto* h = htab.as<std::uint32_t>();
+    const std::uint32_t* hdst = h + nn;
+    const std::uint32_t* hgoff = h + 2 * nn;
+    const std::uint32_t* hact = h + 3 * nn + 1;
+    const std::uint32_t nact = h[4 * nn + 1 + 1];
+    const std::uint64_t nv = nvec();
+    for (std::uint32_t gi = 0; gi < nact; ++gi) {
+      const std::uint32_t g = hact[gi];
+      std::uint32_t rep[kMaxWorld];
+      for (std::uint32_t q = 0; q < world; ++q) rep[q] = 0xffffffffu;
+      for (std::uint32_t pos = hgoff[g]; pos < hgoff[g + 1]; ++pos) {
+        const std::uint32_t d = hdst[pos], q = (std::uint32_t)(d / R);
+        if (rep[q] == 0xffffffffu) rep[q] = d;
+      }
+      char* mine = static_cast<char*>(pools[r]) + (rep[r] % R) * ld * es;
+      for (std::uint32_t q = 0; q < world; ++q) {
+        if (q == r) continue;
+        const std::uint64_t c0 = nv * q / world, c1 = nv * (q + 1) / world;
+        if (c1 == c0) continue;
+        cdst.push_back(mine + c0 * 16);
+        csrc.push_back(static_cast<char*>(pools[q]) + (rep[q] % R) * ld * es + c0 * 16);
+        csize.push_back((c1 - c0) * 16);
+      }
+    }
+    copy_list(s);
+    if (Mg > 1) {
+      CrossArgs<T> a = cross_args<T>(r, true);
+      int sms = 0;
+      MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      local_fanout_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a, nv);
+      MB_LAUNCH_CHECK();
+    }
+  }
+
   template <typename T>
   void moves_launch(std::uint32_t r, int phase, cudaStream_t s) {
     if (p <= 0.0) return;  // no voided groups without failures
@@ -566,6 +826,7 @@ struct Shard {
       }
       if (timing) MB_CUDA(cudaEventRecord(te.second, s));
     } else {
+      if (ce) ce_fetch_tables(s);
       barrier(s);  // peers finished writing the rows we are about to read
       std::pair<cudaEvent_t, cudaEvent_t> te{};
       if (timing) {
@@ -575,10 +836,12 @@ struct Shard {
       for (std::uint32_t k = 0; k < nranks; ++k) {
         const std::uint32_t r = emulate ? k : me;
         if (dtype == MOSHPIT_F32) {
-          cross_launch<float>(r, s);
+          if (ce) cross_ce<float>(r, s);
+          else cross_launch<float>(r, s);
           moves_launch<float>(r, 0, s);
         } else {
-          cross_launch<double>(r, s);
+          if (ce) cross_ce<double>(r, s);
+          else cross_launch<double>(r, s);
           moves_launch<double>(r, 0, s);
         }
       }
@@ -592,10 +855,12 @@ struct Shard {
       for (std::uint32_t k = 0; k < nranks; ++k) {
         const std::uint32_t r = emulate ? k : me;
         if (dtype == MOSHPIT_F32) {
-          pull_launch<float>(r, s);
+          if (ce) pull_ce<float>(r, s);
+          else pull_launch<float>(r, s);
           moves_launch<float>(r, 1, s);
         } else {
-          pull_launch<double>(r, s);
+          if (ce) pull_ce<double>(r, s);
+          else pull_launch<double>(r, s);
           moves_launch<double>(r, 1, s);
         }
       }
@@ -653,6 +918,7 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     S.Mg = M / (std::uint32_t)world;
     S.R = cap / (std::uint64_t)world;
     S.p = p_round;
+    if (const char* e = std::getenv("MOSHPIT_CROSS_CE")) S.ce = std::atoi(e) != 0;
     S.plane = std::make_unique<Plane>(M, d, n, S.device);
     Xoshiro cells = Xoshiro::named(seed, "cells");
     S.fail = Xoshiro::named(seed, "failures");

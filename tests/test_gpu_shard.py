@@ -111,3 +111,25 @@ def test_voided_row_moves_counted(mb, oracle, M, d, p, R, world):
     assert got == want
     if p == 0.0:
         assert sum(got) == 0
+
+
+@pytest.mark.parametrize("M,d,p,R,dim,world", [(32, 2, 0.01, 6, 37, 2), (8, 4, 0.05, 8, 16, 4),
+                                               (8, 2, 0.2, 5, 12, 8)])
+def test_emulated_shards_copy_engine_path(mb, oracle, monkeypatch, M, d, p, R, dim, world):
+    """The copy-engine cross round (MOSHPIT_CROSS_CE=1: staged remote chunks +
+    copy-engine pulls of the chunk means) is bit-identical to the oracle too."""
+    import torch
+    monkeypatch.setenv("MOSHPIT_CROSS_CE", "1")
+    n = M ** d
+    sh = mb.Shard(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), dim, world=world,
+                  emulate=True)
+    sh.fill_synthetic(INIT_SEED)
+    for _ in range(R):
+        sh.round()
+    torch.cuda.synchronize()
+    got, mask = sh.read()
+    assert mask.all()
+    init = oracle.init_state(INIT_SEED, n, dim, dtype=np.float32)
+    _, want = oracle.run_moshpit(M, d, init, p, 7, R)
+    assert bits_equal(got, want)
+    sh.close()
