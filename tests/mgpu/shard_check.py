@@ -22,8 +22,9 @@ def main():
     dist.init_process_group("gloo")
     o = Checker("oracle")
     ok = True
+    # (16, 2, ..., 20001): rows of >= 64 KB get the 4 KB row pitch
     for (M, d, p, R, dim) in [(32, 2, 0.01, 10, 4099), (8, 4, 0.05, 8, 1000), (16, 3, 0.0, 6, 64),
-                              (8, 1, 0.2, 3, 17)]:
+                              (8, 1, 0.2, 3, 17), (16, 2, 0.02, 6, 20001)]:
         if M % world:
             continue
         n = M ** d
@@ -48,7 +49,9 @@ def main():
         sh.close()
     dist.destroy_process_group()
     if rank == 0:
-        print("SHARD CHECK", "PASS" if ok else "FAIL", flush=True)
+        print("SHARD CHECK", "PASS" if ok else "FAIL",
+              "(copy-engine cross round)" if os.environ.get("MOSHPIT_CROSS_CE") == "1" else "",
+              flush=True)
     sys.exit(0 if ok else 1)
 
 
