@@ -9,7 +9,9 @@
 //   void    = OR of the failure mask over the group (allreduce.hpp:95-102);
 //   next key= next_group_key(key, rank) for EVERY member (protocols.hpp:168).
 // One CTA of 1024 threads: a bitonic sort of peer indices under the
-// (key, timestamp, id, index) order, then segmented scans.  The peer count of
+// (key, timestamp, id, index) order (for <= 1024 peers with small keys: in
+// registers over a composite 64-bit key, shuffles for strides < 32), then
+// segmented scans.  The peer count of
 // a Moshpit trial is <= M^d (a few thousand at the north-star configs), so
 // the whole table fits in shared memory and the kernel costs microseconds
 // next to the HBM-bound group mean; larger n spills the sort to global memory
@@ -130,6 +132,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       ts = sts;
     }
   }
+  // Fast path (the engine's common case: n <= 1024 peers, packed keys below
+  // 2^16 - 1, ids == indices): one element per thread in REGISTERS, sorted by
+  // the composite (key << 48 | timestamp, index) -- the same strict order as
+  // the general comparator below -- with bitonic exchanges through warp
+  // shuffles for strides < 32 and shared memory (2 barriers) above.
+  bool fast = false;
+  if constexpr (std::is_same_v<View, PackedView>) {
+    const bool big = tid < n && (view.key[tid] >= 0xFFFFull || (ts[tid] >> 48) != 0);
+    fast = n <= (std::uint32_t)kThreads && a.ids == nullptr && !__syncthreads_or(big);
+  }
+  if (fast) {
+    std::uint64_t c = ~0ull;
+    std::uint32_t id = 0xFFFFFFFFu;  // padding sorts last
+    if (tid < n) {
+      std::uint64_t kv = 0;
+      if constexpr (std::is_same_v<View, PackedView>) kv = view.key[tid];
+      c = (kv << 48) | (ts[tid] & 0xFFFFFFFFFFFFull);
+      id = tid;
+    }
+    std::uint64_t* xc = reinterpret_cast<std::uint64_t*>(smem + np * 4 + ((np * 4) & 4)) + 2 * n;
+    std::uint32_t* xi = reinterpret_cast<std::uint32_t*>(xc + np);
+    for (std::uint32_t k = 2; k <= np; k <<= 1) {
+      for (std::uint32_t j = k >> 1; j > 0; j >>= 1) {
+        std::uint64_t oc;
+        std::uint32_t oi;
+        if (j < 32) {
+          oc = __shfl_xor_sync(0xffffffffu, c, j);
+          oi = __shfl_xor_sync(0xffffffffu, id, j);
+        } else {
+          if (tid < np) {
+            xc[tid] = c;
+            xi[tid] = id;
+          }
+          __syncthreads();
+          if (tid < np) {
+            oc = xc[tid ^ j];
+            oi = xi[tid ^ j];
+          }
+          __syncthreads();
+        }
+        if (tid < np) {
+          const bool other_less = oc < c || (oc == c && oi < id);
+          const bool lower = (tid & j) == 0, up = (tid & k) == 0;
+          // ascending blocks: the lower position keeps the min
+          if (lower == up ? other_less : !other_less) {
+            c = oc;
+            id = oi;
+          }
+        }
+      }
+    }
+    if (tid < np) idx[tid] = id;
+    __syncthreads();
+  } else {
   for (std::uint32_t i = tid; i < np; i += kThreads) idx[i] = i;
   __syncthreads();
 
@@ -161,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncthreads();
     }
+  }
   }
 
   // Each thread owns a contiguous run of sorted positions.
@@ -276,6 +333,7 @@ std::size_t group_smem_bytes(std::uint32_t n, bool packed) {
   std::size_t b = np * 4;
   b += b & 4;
   if (packed) b += std::size_t(n) * 16;
+  if (packed && n <= (std::uint32_t)kThreads) b += np * 12;  // fast-path exchange buffers
   return b;
 }
 
