@@ -99,6 +99,51 @@ __global__ void drift_b(const double* __restrict__ mean, const double* __restric
   out[t * out_stride] = __ddiv_rn(__dsqrt_rn(drift_sq), fmax(__dsqrt_rn(ref_sq), 1e-300));
 }
 
+// One round's whole record_round (protocols.hpp:68-84) for narrow vectors,
+// one CTA per trial: per-peer sums over j in order, the tree over peers for
+// the distortion, the column means (tree over peers per j), then the drift in
+// j order -- the four kernels above fused for dim < 32, where a sweep round
+// otherwise costs four launches for a few microseconds of work.
+template <typename T>
+__global__ void __launch_bounds__(kTreeThreads)
+    round_diag_narrow(const T* __restrict__ x, std::uint32_t n, std::uint64_t ld,
+                      std::uint32_t dim, const double* __restrict__ ref, double* __restrict__ sq,
+                      double* __restrict__ mean, double* __restrict__ dist_out,
+                      double* __restrict__ drift_out, std::uint64_t out_stride) {
+  __shared__ double lvl[2 * kBlockTreeMaxNodes];
+  const std::uint64_t t = blockIdx.x;
+  const T* xt = x + t * n * ld;
+  const double* rf = ref + t * dim;
+  double* sqt = sq + t * n;
+  double* mt = mean + t * dim;
+  for (std::uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double acc = 0.0;
+    for (std::uint32_t j = 0; j < dim; ++j) {
+      const double diff = __dsub_rn((double)xt[(std::uint64_t)i * ld + j], rf[j]);
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    sqt[i] = acc;
+  }
+  __syncthreads();
+  auto ld_sq = [&](std::uint32_t i) { return sqt[i]; };
+  const double dsum = pairwise_block(ld_sq, n, lvl);
+  if (threadIdx.x == 0) dist_out[t * out_stride] = __ddiv_rn(dsum, (double)n);
+  for (std::uint32_t j = 0; j < dim; ++j) {
+    auto ld_x = [&](std::uint32_t i) -> double { return (double)xt[(std::uint64_t)i * ld + j]; };
+    const double v = pairwise_block(ld_x, n, lvl);
+    if (threadIdx.x == 0) mt[j] = __ddiv_rn(v, (double)n);
+  }
+  if (threadIdx.x == 0) {
+    double drift_sq = 0.0, ref_sq = 0.0;
+    for (std::uint32_t j = 0; j < dim; ++j) {
+      const double dm = __dsub_rn(mt[j], rf[j]);
+      drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
+      ref_sq = __dadd_rn(ref_sq, __dmul_rn(rf[j], rf[j]));
+    }
+    drift_out[t * out_stride] = __ddiv_rn(__dsqrt_rn(drift_sq), fmax(__dsqrt_rn(ref_sq), 1e-300));
+  }
+}
+
 // Per-trial protocol draws on the device (protocols.hpp:86-97, 146-150).
 // Each trial's "failures" and "priorities" streams are sequential xoshiro256**
 // sequences (rng.hpp:35-91), but the trials are independent: thread
@@ -140,8 +185,11 @@ __global__ void draws_kernel(std::uint64_t* __restrict__ fail_state,
     } else {  // failures: bernoulli(p) per peer, no draws at p <= 0 (:89)
       std::uint32_t alive = n;
       if (p > 0.0) {
+        // uniform() < p  <=>  (next >> 11) < ceil(p * 2^53): v * 2^-53 and
+        // p * 2^53 are exact (power-of-two scaling), v is an integer
+        const std::uint64_t thr = (std::uint64_t)ceil(p * 0x1.0p53);
         for (std::uint32_t i = 0; i < n; ++i) {
-          const bool dead = (double)(xnext(s) >> 11) * 0x1.0p-53 < p;
+          const bool dead = (xnext(s) >> 11) < thr;
           f[i] = dead ? 1 : 0;
           alive -= dead ? 1u : 0u;
         }
@@ -280,22 +328,57 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     finish(out.as<double>());
     MB_LAUNCH_CHECK();
   }
-  // The draws of a block of rounds are generated on the device (draws_kernel)
-  // right before the rounds that consume them: no host synchronisation.
+  // The draws of a block of rounds are generated on the device (draws_kernel,
+  // a serial xoshiro chain per trial stream) on a side stream, one block
+  // ahead of the rounds that consume them: blocks of a few rounds in two
+  // buffers, so the chains of block b+1 run under the rounds of block b.
   std::vector<std::uint32_t> act_h((std::uint64_t)trials * rounds);
   // per-round block: ts u64[rows] then failed u8[rows], padded to 16 bytes so
   // every block's timestamps stay 8-byte aligned
   const std::uint64_t per_round = (rows * 9 + 15) / 16 * 16;
-  std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (256ull << 20) / per_round);
+  std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (128ull << 20) / per_round);
+  if (rb > 4) rb = 4;
   if (rb > rounds) rb = rounds ? rounds : 1;
-  PoolBuffer dblock(per_round * rb + 16, st.s);
-  for (std::uint32_t r0 = 0; r0 < rounds; r0 += rb) {
+  PoolBuffer dbuf0(per_round * rb + 16, st.s), dbuf1(per_round * rb + 16, st.s);
+  PoolBuffer* dbufs[2] = {&dbuf0, &dbuf1};
+  StreamHolder ds;
+  cudaEvent_t ev_ready = nullptr, ev_drawn[2] = {}, ev_free[2] = {};
+  MB_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    MB_CUDA(cudaEventCreateWithFlags(&ev_drawn[i], cudaEventDisableTiming));
+    MB_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+  }
+  struct EvGuard {
+    cudaEvent_t* e;
+    int k;
+    ~EvGuard() {
+      for (int i = 0; i < k; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t all_ev[5] = {ev_ready, ev_drawn[0], ev_drawn[1], ev_free[0], ev_free[1]};
+  EvGuard guard{all_ev, 5};
+  MB_CUDA(cudaEventRecord(ev_ready, st.s));  // stream states + buffers are in place
+  MB_CUDA(cudaStreamWaitEvent(ds.s, ev_ready, 0));
+  auto draw_block = [&](std::uint32_t b) {
+    const std::uint32_t r0 = b * rb;
     const std::uint32_t nr = std::min(rb, rounds - r0);
-    draws_kernel<<<(2 * trials + 63) / 64, 64, 0, st.s>>>(
+    if (b >= 2) MB_CUDA(cudaStreamWaitEvent(ds.s, ev_free[b & 1], 0));
+    draws_kernel<<<(2 * trials + 63) / 64, 64, 0, ds.s>>>(
         rstate.as<std::uint64_t>(), rstate.as<std::uint64_t>() + (std::uint64_t)trials * 4,
-        trials, (std::uint32_t)n, nr, per_round, p, dblock.as<std::uint8_t>(),
+        trials, (std::uint32_t)n, nr, per_round, p, dbufs[b & 1]->as<std::uint8_t>(),
         act_d.as<std::uint32_t>(), rounds, r0);
     MB_LAUNCH_CHECK();
+    MB_CUDA(cudaEventRecord(ev_drawn[b & 1], ds.s));
+  };
+  const std::uint32_t nblocks = rounds ? (rounds + rb - 1) / rb : 0;
+  if (nblocks) draw_block(0);
+  for (std::uint32_t b = 0; b < nblocks; ++b) {
+    const std::uint32_t r0 = b * rb;
+    const std::uint32_t nr = std::min(rb, rounds - r0);
+    if (b + 1 < nblocks) draw_block(b + 1);
+    MB_CUDA(cudaStreamWaitEvent(st.s, ev_drawn[b & 1], 0));
+    PoolBuffer& dblock = *dbufs[b & 1];
     for (std::uint32_t q = 0; q < nr; ++q) {
     const std::uint32_t r = r0 + q;
     std::uint8_t* draws_r = dblock.as<std::uint8_t>() + q * per_round;
@@ -321,7 +404,13 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     launch_form_groups(a, true, st.s);
     launch_group_mean_batch<T>(x.as<T>(), n * ld, ld, dim, (std::uint32_t)n, trials, a.members,
                                a.goff, a.act, a.counts, st.s);
-    if (dg) {
+    if (dg && dim < 32) {
+      round_diag_narrow<T><<<trials, kTreeThreads, 0, st.s>>>(
+          x.as<T>(), (std::uint32_t)n, ld, (std::uint32_t)dim, ref.as<double>(), sq.as<double>(),
+          mean.as<double>(), out.as<double>() + 1 + r, out.as<double>() + 1 + rounds + r,
+          2 * rounds + 1);
+      MB_LAUNCH_CHECK();
+    } else if (dg) {
       dist_rows_b<T><<<(unsigned)((rows + 127) / 128), 128, 0, st.s>>>(
           x.as<T>(), n, rows, ld, dim, ref.as<double>(), sq.as<double>());
       finish(out.as<double>() + 1 + r);
@@ -332,10 +421,13 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
       MB_LAUNCH_CHECK();
     }
     }
+    MB_CUDA(cudaEventRecord(ev_free[b & 1], st.s));  // block b's draws consumed
   }
-  if (rounds)
+  if (rounds) {
+    MB_CUDA(cudaStreamWaitEvent(st.s, ev_drawn[(nblocks - 1) & 1], 0));  // act counts complete
     MB_CUDA(cudaMemcpyAsync(act_h.data(), act_d.ptr, act_h.size() * 4, cudaMemcpyDeviceToHost,
                             st.s));
+  }
   std::vector<double> h;
   if (dg) {
     h.resize((std::uint64_t)trials * (2 * rounds + 1));
