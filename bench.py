@@ -343,6 +343,8 @@ def run_mine(args):
     if rank == 0 and world == 1 and not args.no_sgd:
         try:
             sgd = measure_sgd_c4(mb)
+            s0 = measure_sgd_c4(mb, sigma=0.0)
+            sgd["sigma0"] = {k: s0[k] for k in ("ms_per_sgd_step", "peer_vector_gbs", "hbm_frac")}
         except Exception as exc:  # noqa: BLE001
             sgd = {"error": str(exc)}
     cpu = None

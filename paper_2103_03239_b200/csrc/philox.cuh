@@ -36,10 +36,10 @@ __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_
     // -2 ln u1 = -2 ln2 * (log2 v - 24): one MUFU.LG2 and one FFMA.
     const float v = (float)((a[2 * h] >> 8) + 1u);
     float l2;
-    asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(v));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(v));  // v >= 1: no denormals
     const float e = fmaxf(__fmaf_rn(l2, -1.3862943611198906f, 33.271064666877374f), 0.0f);
     float rr;  // sqrt on the SFU (MUFU.SQRT)
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(rr) : "f"(e));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rr) : "f"(e));
     float s, c;  // angle 2*pi*u2, u2 = (a >> 8) / 2^24 in [0, 1)
     __sincosf((float)(a[2 * h + 1] >> 8) * 3.7450702e-07f, &s, &c);
     z[2 * h] = rr * c;
