@@ -19,16 +19,53 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
   return c;
 }
 
+// The same generator with the 10 round keys precomputed (kernel parameters,
+// i.e. constant-bank operands of the XORs): round r uses
+// (seed_lo + r * 0x9E3779B9, seed_hi + r * 0xBB67AE85), as above.
+struct PhiloxKeys {
+  uint2 k[10];
+};
+inline PhiloxKeys philox_keys(std::uint64_t seed) {
+  PhiloxKeys p;
+  std::uint32_t a = (std::uint32_t)seed, b = (std::uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    p.k[r] = make_uint2(a, b);
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
+  return p;
+}
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys& kk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const std::uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ kk.k[r].x, lo1, hi0 ^ c.w ^ kk.k[r].y, lo0);
+  }
+  return c;
+}
+
 // Four standard normals for (step, peer, quad): Box-Muller on SFU intrinsics
 // (the device-noise path promises statistical parity only, and this keeps the
 // fused step + averaging kernel memory-bound).
+__device__ __forceinline__ void box_muller4(uint4 r, float z[4]);
 __device__ __forceinline__ void philox_normals4(std::uint64_t seed, std::uint64_t step,
                                                 std::uint64_t peer, std::uint64_t quad,
                                                 float z[4]) {
-  const uint4 r = philox4x32_10(
-      make_uint4((std::uint32_t)step, (std::uint32_t)peer, (std::uint32_t)quad,
-                 (std::uint32_t)(quad >> 32)),
-      make_uint2((std::uint32_t)seed, (std::uint32_t)(seed >> 32)));
+  box_muller4(philox4x32_10(make_uint4((std::uint32_t)step, (std::uint32_t)peer,
+                                       (std::uint32_t)quad, (std::uint32_t)(quad >> 32)),
+                            make_uint2((std::uint32_t)seed, (std::uint32_t)(seed >> 32))),
+              z);
+}
+__device__ __forceinline__ void philox_normals4(const PhiloxKeys& kk, std::uint64_t step,
+                                                std::uint64_t peer, std::uint64_t quad,
+                                                float z[4]) {
+  box_muller4(philox4x32_10(make_uint4((std::uint32_t)step, (std::uint32_t)peer,
+                                       (std::uint32_t)quad, (std::uint32_t)(quad >> 32)),
+                            kk),
+              z);
+}
+__device__ __forceinline__ void box_muller4(uint4 r, float z[4]) {
   const std::uint32_t a[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
   for (int h = 0; h < 2; ++h) {

@@ -71,6 +71,7 @@ struct LArgs {
   std::uint64_t seed, step_no, dim;
   std::uint32_t* nonfinite;
   double* noise_partial;
+  PhiloxKeys pk;  // Philox round keys of `seed` (constant-bank operands)
 };
 
 // Leaf boundaries of the reference tree for n <= 32 (see header comment).
@@ -96,7 +97,7 @@ __device__ __forceinline__ int leaf_bounds(std::uint32_t n, std::uint32_t* b) {
 // One member vector: the step, lane by lane (element j of the row).
 template <typename T, bool NOISY, typename V>
 __device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, double coord_std,
-                                         std::uint64_t seed, std::uint64_t step_no,
+                                         const PhiloxKeys& seed, std::uint64_t step_no,
                                          std::uint32_t peer, std::uint64_t j0, bool full,
                                          std::uint64_t dim, T& chk, double& nsq) {
   constexpr int kV = LVec<T>::kN;
@@ -163,7 +164,8 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
   __shared__ std::uint32_t sb[6];
   const T gamma = a.gamma;
   const double coord_std = a.coord_std;
-  const std::uint64_t seed = a.seed, step_no = a.step_no, dim = a.dim;
+  const std::uint64_t step_no = a.step_no, dim = a.dim;
+  const PhiloxKeys& seed = a.pk;
   const std::uint64_t ld_vec = a.ld_vec, nvec = a.nvec, n_tiles = a.n_tiles;
   V* const base = reinterpret_cast<V*>(a.state);
   T chk = T(0);
@@ -344,6 +346,7 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
   a.gamma = sp.gamma;
   a.coord_std = sp.coord_std;
   a.seed = sp.seed;
+  a.pk = philox_keys(sp.seed);
   a.step_no = sp.step_no;
   a.dim = sp.dim;
   a.nonfinite = sp.nonfinite;
