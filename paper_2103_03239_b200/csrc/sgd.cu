@@ -13,6 +13,9 @@
 // (bit-exact; O(N*D) host draws per step) or a counter-based Philox4x32-10
 // normal on the device (statistical parity; the performance path).
 #include <cmath>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 #include <memory>
 
 #include "philox.cuh"
@@ -603,12 +606,26 @@ struct SgdRun {
     logit_coeff_tiled<T><<<dim3((unsigned)((S + kLT - 1) / kLT), ty), 256, 0, s>>>(
         static_cast<const T*>(x), n, ld, dim, lxs.as<double>(), lys.as<double>(), S,
         coeff.as<double>());
-    constexpr int GT = 64;  // gradient tile (see logit_grad_tiled)
-    logit_grad_tiled<T, GT, GT><<<dim3((unsigned)((dim + GT - 1) / GT),
-                                       (unsigned)((n + GT - 1) / GT)), GT * GT / 16, 0, s>>>(
-        static_cast<T*>(x), n, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, (T)gamma,
-        nz, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
-        npart.as<double>() + k * 148 * 16);
+    // gradient tile TM x TN (see logit_grad_tiled); MOSHPIT_LOGIT_GTILE=64x32|64x16
+    // are measurement knobs
+    static const int gt = [] {
+      const char* e = std::getenv("MOSHPIT_LOGIT_GTILE");
+      if (!e) return 0;
+      const std::string v(e);
+      return v == "64x32" ? 1 : v == "64x16" ? 2 : 0;
+    }();
+    auto grad = [&](auto tm, auto tn) {
+      constexpr int TM = decltype(tm)::value, TN = decltype(tn)::value;
+      logit_grad_tiled<T, TM, TN><<<dim3((unsigned)((dim + TN - 1) / TN),
+                                         (unsigned)((n + TM - 1) / TM)), TM * TN / 16, 0, s>>>(
+          static_cast<T*>(x), n, ld, dim, lxs.as<double>(), S, coeff.as<double>(), l2, (T)gamma,
+          nz, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
+          npart.as<double>() + k * 148 * 16);
+    };
+    using I64 = std::integral_constant<int, 64>;
+    if (gt == 1) grad(I64{}, std::integral_constant<int, 32>{});
+    else if (gt == 2) grad(I64{}, std::integral_constant<int, 16>{});
+    else grad(I64{}, I64{});
     MB_LAUNCH_CHECK();
   }
 
