@@ -94,9 +94,13 @@ __device__ __forceinline__ int leaf_bounds(std::uint32_t n, std::uint32_t* b) {
   return 4;
 }
 
-// One member vector: the step, lane by lane (element j of the row).
+// One member vector: the step, lane by lane (element j of the row).  `cst`
+// is coord_std in the state's precision ((T)coord_std, hoisted), so
+// cst * z is noise_component() exactly.  Full vectors (every thread but the
+// row tail's) run the lanes without per-lane exits: the Box-Muller SFU ops
+// and the lane steps schedule as one block instead of four.
 template <typename T, bool NOISY, typename V>
-__device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, double coord_std,
+__device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, T cst,
                                          const PhiloxKeys& seed, std::uint64_t step_no,
                                          std::uint32_t peer, std::uint64_t j0, bool full,
                                          std::uint64_t dim, T& chk, double& nsq) {
@@ -107,17 +111,25 @@ __device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, 
   float z[4] = {0.f, 0.f, 0.f, 0.f};
   if constexpr (NOISY) philox_normals4(seed, step_no, peer, j0 / 4, z);
   T q = T(0);
-#pragma unroll
-  for (int u = 0; u < kV; ++u) {
-    if (!full && j0 + u >= dim) break;
+  auto lane = [&](int u) {
     T g = lmul(pc[u], lsub(pv[u], pt[u]));
     if constexpr (NOISY) {
-      const T nj = noise_component(z[(j0 + u) & 3], coord_std, (T*)nullptr);
+      const T nj = lmul(cst, (T)z[(j0 + u) & 3]);
       nsq_add(q, nj);
       g = ladd(g, nj);
     }
     chk = lfma0(g, chk);  // stays 0 unless some g is inf/NaN
     pv[u] = lsub(pv[u], lmul(gamma, g));
+  };
+  if (full) {
+#pragma unroll
+    for (int u = 0; u < kV; ++u) lane(u);
+  } else {
+#pragma unroll
+    for (int u = 0; u < kV; ++u) {
+      if (j0 + u >= dim) break;
+      lane(u);
+    }
   }
   if constexpr (NOISY) nsq += (double)q;
 }
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
   __shared__ std::uint32_t sids[32];
   __shared__ std::uint32_t sb[6];
   const T gamma = a.gamma;
-  const double coord_std = a.coord_std;
+  const T cst = (T)a.coord_std;  // noise_component's multiplier
   const std::uint64_t step_no = a.step_no, dim = a.dim;
   const PhiloxKeys& seed = a.pk;
   const std::uint64_t ld_vec = a.ld_vec, nvec = a.nvec, n_tiles = a.n_tiles;
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
       for (int k = 0; k < 8; ++k) {
         if (b + k < e) {
           if constexpr (STEP)
-            step_vec<T, NOISY>(buf[k], c, t, gamma, coord_std, seed, step_no, sids[b + k], j0,
+            step_vec<T, NOISY>(buf[k], c, t, gamma, cst, seed, step_no, sids[b + k], j0,
                                full, dim, chk, nsq);
           s = vsum(s, buf[k]);
         }
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
           for (int k = 0; k < 4; ++k) {
             if (c0 + k < le) {
               if constexpr (STEP)
-                step_vec<T, NOISY>(X[k], c, t, gamma, coord_std, seed, step_no, sids[c0 + k],
+                step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k],
                                    j0, full, dim, chk, nsq);
               sl = vsum(sl, X[k]);
             }
