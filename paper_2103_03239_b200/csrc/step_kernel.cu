@@ -31,6 +31,14 @@ namespace mb200 {
 namespace {
 
 constexpr int kLThreads = 128;
+#ifndef MB_K3_ILP
+#define MB_K3_ILP 4
+#endif
+constexpr int kIlp = MB_K3_ILP;  // members whose Philox chains interleave
+#ifndef MB_K3_MINB
+#define MB_K3_MINB 5
+#endif
+constexpr int kNoisyMinB = MB_K3_MINB;  // CTAs/SM of the noisy 4-wide form
 
 template <typename T>
 struct LVec;
@@ -99,17 +107,16 @@ __device__ __forceinline__ int leaf_bounds(std::uint32_t n, std::uint32_t* b) {
 // cst * z is noise_component() exactly.  Full vectors (every thread but the
 // row tail's) run the lanes without per-lane exits: the Box-Muller SFU ops
 // and the lane steps schedule as one block instead of four.
+// The lanes of one member vector given its four normals z (unused when
+// !NOISY).
 template <typename T, bool NOISY, typename V>
-__device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, T cst,
-                                         const PhiloxKeys& seed, std::uint64_t step_no,
-                                         std::uint32_t peer, std::uint64_t j0, bool full,
-                                         std::uint64_t dim, T& chk, double& nsq) {
+__device__ __forceinline__ void step_lanes(V& v, const V& c, const V& t, T gamma, T cst,
+                                           const float (&z)[4], std::uint64_t j0, bool full,
+                                           std::uint64_t dim, T& chk, double& nsq) {
   constexpr int kV = LVec<T>::kN;
   T* pv = reinterpret_cast<T*>(&v);
   const T* pc = reinterpret_cast<const T*>(&c);
   const T* pt = reinterpret_cast<const T*>(&t);
-  float z[4] = {0.f, 0.f, 0.f, 0.f};
-  if constexpr (NOISY) philox_normals4(seed, step_no, peer, j0 / 4, z);
   T q = T(0);
   auto lane = [&](int u) {
     T g = lmul(pc[u], lsub(pv[u], pt[u]));
@@ -132,6 +139,16 @@ __device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, 
     }
   }
   if constexpr (NOISY) nsq += (double)q;
+}
+
+template <typename T, bool NOISY, typename V>
+__device__ __forceinline__ void step_vec(V& v, const V& c, const V& t, T gamma, T cst,
+                                         const PhiloxKeys& seed, std::uint64_t step_no,
+                                         std::uint32_t peer, std::uint64_t j0, bool full,
+                                         std::uint64_t dim, T& chk, double& nsq) {
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  if constexpr (NOISY) philox_normals4(seed, step_no, peer, j0 / 4, z);
+  step_lanes<T, NOISY>(v, c, t, gamma, cst, z, j0, full, dim, chk, nsq);
 }
 
 template <typename V>
@@ -158,14 +175,18 @@ __device__ __forceinline__ double2 vdivn(double2 a, std::uint32_t n) {
 }
 
 // MODE 0: 8-member load batches; 1: 8-member batches with the next leaf
-// prefetched; 2 (default): 4-member batches at 64 registers, 8 CTAs/SM --
-// more warps to hide the Philox/SFU latency of the device-noise step and the
-// load latency of the plain one.  Same arithmetic in every mode.  MODE 3 / 4
+// prefetched; 2 (default): 4-member batches.  Without noise: 64 registers,
+// 8 CTAs/SM (warps hide the load latency).  With device noise the batch's
+// four Philox chains are computed together (kIlp) so their dependent
+// IMAD/LOP3 rounds interleave, at kNoisyMinB = 5 CTAs/SM (94 registers, no
+// spills): C4 sigma=1 step 3.34 -> 3.18 ms; at 8 CTAs/SM the same code
+// spills (3.21 ms) and one chain at a time measured 3.34 ms
+// (profiles/k3_variants.sh).  Same arithmetic in every mode.  MODE 3 / 4
 // are the 4- / 8-wide forms WITHOUT the step: a plain Kernel-2 round (used
 // for groups of <= 8 members, where the register form's 32-slot body caps
 // residency at 3 CTAs/SM).
 template <typename T, bool NOISY, int MODE>
-__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE == 3) ? 8 : 6)
+__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE == 3) ? (NOISY ? kNoisyMinB : 8) : 6)
     group_mean_step_leaf(LArgs<T> a) {
   constexpr bool PREFETCH = MODE == 1;
   constexpr bool STEP = MODE < 3;
@@ -250,13 +271,35 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             X[k] = (c0 + k < le) ? colp[(std::uint64_t)sids[c0 + k] * ld_vec] : vz<V>();
+          if (c0 + 4 <= le) {
+            // whole batch: the four members' Philox chains are independent
+            // and interleave (ILP against the dependent IMAD/LOP3 rounds)
+            if constexpr (STEP) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (c0 + k < le) {
-              if constexpr (STEP)
-                step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k],
-                                   j0, full, dim, chk, nsq);
-              sl = vsum(sl, X[k]);
+              for (int k = 0; k < 4; k += kIlp) {
+                float z[kIlp][4] = {};
+                if constexpr (NOISY) {
+#pragma unroll
+                  for (int e = 0; e < kIlp; ++e)
+                    philox_normals4(seed, step_no, sids[c0 + k + e], j0 / 4, z[e]);
+                }
+#pragma unroll
+                for (int e = 0; e < kIlp; ++e)
+                  step_lanes<T, NOISY>(X[k + e], c, t, gamma, cst, z[e], j0, full, dim, chk,
+                                       nsq);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sl = vsum(sl, X[k]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (c0 + k < le) {
+                if constexpr (STEP)
+                  step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k],
+                                     j0, full, dim, chk, nsq);
+                sl = vsum(sl, X[k]);
+              }
             }
           }
         }
