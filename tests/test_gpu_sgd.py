@@ -166,7 +166,11 @@ def test_c4_shaped_run_device_noise(mb):
 
 @pytest.mark.parametrize("f64", [False, True])
 @pytest.mark.parametrize("sigma,tau,M,d,n", [(0.0, 1, 4, 2, 16), (1.0, 1, 8, 2, 64),
-                                             (0.7, 3, 4, 3, 50), (1.0, 1, 40, 2, 1600)])
+                                             (0.7, 3, 4, 3, 50), (1.0, 1, 40, 2, 1600),
+                                             # groups of 7 / 13 / <= 31: whole 4-member
+                                             # batches (interleaved Philox) + partial ones
+                                             (1.0, 1, 7, 2, 49), (1.0, 1, 13, 2, 150),
+                                             (0.5, 2, 31, 2, 900)])
 def test_fused_kernel3_equals_unfused(mb, f64, sigma, tau, M, d, n):
     """Kernel 3 (local step fused into averaging round 1) == step kernel +
     averaging, bit for bit, with the same device noise."""
