@@ -39,6 +39,14 @@ constexpr int kIlp = MB_K3_ILP;  // members whose Philox chains interleave
 #define MB_K3_MINB 5
 #endif
 constexpr int kNoisyMinB = MB_K3_MINB;  // CTAs/SM of the noisy 4-wide form
+#ifndef MB_K3_PF
+#define MB_K3_PF 0
+#endif
+// Noisy 4-wide form with the next batch's loads issued under this batch's
+// Philox rounds: parity-green but measured slower (C4 sigma=1 3.18 -> 3.67 ms
+// at 4 CTAs/SM / 127 registers, 3.60 ms at 5 CTAs/SM with spills;
+// profiles/r01/k3_variants_prefetch.txt), so off by default.
+constexpr bool kPf = MB_K3_PF != 0;
 
 template <typename T>
 struct LVec;
@@ -259,7 +267,78 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
     // L0 | L0+L1 | L0+(L1+L2) | (L0+L1)+(L2+L3) for nl = 1..4.
     const std::uint32_t r = nl == 4 ? 2u : 1u;
     V P = vz<V>(), Q = vz<V>();
-    if constexpr (WIDE4) {
+    auto load4 = [&](V(&X)[4], std::uint32_t c0, std::uint32_t le) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        X[k] = (c0 + k < le) ? colp[(std::uint64_t)sids[c0 + k] * ld_vec] : vz<V>();
+    };
+    // One 4-member batch [c0, min(c0+4, le)) stepped and added into sl.
+    auto batch4 = [&](V(&X)[4], std::uint32_t c0, std::uint32_t le, V& sl) {
+      if (c0 + 4 <= le) {
+        // whole batch: the four members' Philox chains are independent
+        // and interleave (ILP against the dependent IMAD/LOP3 rounds)
+        if constexpr (STEP) {
+#pragma unroll
+          for (int k = 0; k < 4; k += kIlp) {
+            float z[kIlp][4] = {};
+            if constexpr (NOISY) {
+#pragma unroll
+              for (int e = 0; e < kIlp; ++e)
+                philox_normals4(seed, step_no, sids[c0 + k + e], j0 / 4, z[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < kIlp; ++e)
+              step_lanes<T, NOISY>(X[k + e], c, t, gamma, cst, z[e], j0, full, dim, chk, nsq);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sl = vsum(sl, X[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (c0 + k < le) {
+            if constexpr (STEP)
+              step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k], j0,
+                                 full, dim, chk, nsq);
+            sl = vsum(sl, X[k]);
+          }
+        }
+      }
+    };
+    if constexpr (WIDE4 && NOISY && kPf) {
+      // Same batches, same order, flattened over the leaves so batch i+1's
+      // member loads are in flight while batch i runs its Philox rounds.
+      auto lend = [&](std::uint32_t l) { return l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4; };
+      std::uint32_t l = 0, c0 = b0, le = b1;
+      V X[4];
+      load4(X, c0, le);
+      V sl = vz<V>();
+#pragma unroll 1
+      while (true) {
+        std::uint32_t nl2 = l, nc = c0 + 4, ne = le;
+        const bool leaf_end = nc >= le;
+        if (leaf_end) {
+          nl2 = l + 1;
+          nc = le;
+          ne = nl2 < nl ? lend(nl2) : le;
+        }
+        const bool more = nl2 < nl;
+        V Y[4];
+        if (more) load4(Y, nc, ne);
+        batch4(X, c0, le, sl);
+        if (leaf_end) {
+          if (l < r) P = l == 0 ? sl : vsum(P, sl);
+          else Q = l == r ? sl : vsum(Q, sl);
+          sl = vz<V>();
+        }
+        if (!more) break;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) X[k] = Y[k];
+        l = nl2;
+        c0 = nc;
+        le = ne;
+      }
+    } else if constexpr (WIDE4) {
       std::uint32_t lb = b0;
 #pragma unroll 1
       for (std::uint32_t l = 0; l < nl; ++l) {
