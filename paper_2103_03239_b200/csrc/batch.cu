@@ -9,11 +9,14 @@
 // per-round failure and priority streams run on the device, one thread per
 // (trial, stream); the once-per-trial cell draws stay on the host threads.
 #include <algorithm>
+#include <bitset>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <thread>
 
 #include "pairwise.cuh"
@@ -205,6 +208,186 @@ __global__ void draws_kernel(std::uint64_t* __restrict__ fail_state,
   st[3] = s[3];
 }
 
+// Lane-parallel form of draws_kernel: one warp per (trial, stream).  A block
+// of nr rounds is nr*n consecutive draws of the stream; lane L takes draws
+// [L*C, (L+1)*C) (C = ceil(nr*n / 32)) and starts from the block's state
+// jumped ahead by L*C steps.  The jump is q_L(T) s with q_L = x^(L*C) mod the
+// characteristic polynomial of the xoshiro256 transition T (Cayley-Hamilton),
+// evaluated as sum_i q_i T^i s: 256 steps instead of L*C.  Every lane then
+// runs the reference's generator over its own chunk, so each draw is the one
+// the serial chain produces at that position (bit-identical by construction).
+struct LanePolys {
+  std::uint64_t w[32][4];  // q_L, bit i = coefficient of x^i
+};
+constexpr std::uint32_t kMaxBlockRounds = 4;
+
+__global__ void __launch_bounds__(64)
+    draws_lanes_kernel(std::uint64_t* __restrict__ fail_state,
+                       std::uint64_t* __restrict__ clock_state, std::uint32_t trials,
+                       std::uint32_t n, std::uint32_t nr, std::uint64_t per_round, double p,
+                       std::uint8_t* __restrict__ block, std::uint32_t* __restrict__ act,
+                       std::uint32_t rounds, std::uint32_t r0, std::uint64_t chunk,
+                       const __grid_constant__ LanePolys polys) {
+  __shared__ std::uint32_t dead[2][kMaxBlockRounds];
+  const std::uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t id = blockIdx.x * 2 + wib;
+  if (lane < kMaxBlockRounds) dead[wib][lane] = 0;
+  __syncwarp();
+  if (id >= 2 * trials) return;
+  const std::uint32_t t = id >> 1;
+  const bool clock = id & 1;
+  const std::uint64_t rows = (std::uint64_t)trials * n;
+  std::uint64_t* st = clock ? clock_state + 4 * t : fail_state + 4 * t;
+  if (!clock && !(p > 0.0)) {  // failures at p <= 0: no draws (protocols.hpp:89)
+    for (std::uint32_t q = 0; q < nr; ++q) {
+      std::uint8_t* f = block + q * per_round + rows * 8 + (std::uint64_t)t * n;
+      for (std::uint32_t i = lane; i < n; i += 32) f[i] = 0;
+      if (lane == 0) act[(std::uint64_t)t * rounds + r0 + q] = n;
+    }
+    return;
+  }
+  const std::uint64_t total = (std::uint64_t)nr * n;
+  const std::uint64_t beg = (std::uint64_t)lane * chunk;
+  const std::uint64_t end = beg + chunk < total ? beg + chunk : total;
+  std::uint64_t s[4] = {st[0], st[1], st[2], st[3]};
+  __syncwarp();
+  if (beg < total && lane) {
+    std::uint64_t a[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int wi = 0; wi < 4; ++wi) {
+      const std::uint64_t word = polys.w[lane][wi];
+#pragma unroll 4
+      for (int b = 0; b < 64; ++b) {
+        if ((word >> b) & 1) {
+          a[0] ^= s[0]; a[1] ^= s[1]; a[2] ^= s[2]; a[3] ^= s[3];
+        }
+        xnext(s);
+      }
+    }
+    s[0] = a[0]; s[1] = a[1]; s[2] = a[2]; s[3] = a[3];
+  }
+  const std::uint64_t thr = clock ? 0 : (std::uint64_t)ceil(p * 0x1.0p53);
+  if (beg < total) {
+    std::uint32_t q = (std::uint32_t)(beg / n), i = (std::uint32_t)(beg % n);
+    std::uint32_t dq = 0;
+    for (std::uint64_t g = beg; g < end; ++g) {
+      const std::uint64_t v = xnext(s);
+      if (clock) {  // priorities: clock() >> 16 (protocols.hpp:148-150)
+        reinterpret_cast<std::uint64_t*>(block + q * per_round)[(std::uint64_t)t * n + i] = v >> 16;
+      } else {  // failures: uniform() < p  <=>  (next >> 11) < ceil(p * 2^53)
+        const bool d = (v >> 11) < thr;
+        block[q * per_round + rows * 8 + (std::uint64_t)t * n + i] = d ? 1 : 0;
+        dq += d ? 1u : 0u;
+      }
+      if (++i == n) {
+        if (!clock && dq) atomicAdd(&dead[wib][q], dq);
+        dq = 0;
+        i = 0;
+        ++q;
+      }
+    }
+    if (!clock && dq) atomicAdd(&dead[wib][q], dq);
+    if (end == total) {  // the lane holding the block's last draw carries the stream on
+      st[0] = s[0];
+      st[1] = s[1];
+      st[2] = s[2];
+      st[3] = s[3];
+    }
+  }
+  __syncwarp();
+  if (!clock && lane < nr) act[(std::uint64_t)t * rounds + r0 + lane] = n - dead[wib][lane];
+}
+
+// GF(2) polynomials of degree < 512 (host).
+using Poly = std::bitset<512>;
+
+// Minimal polynomial of the xoshiro256 state transition, by Berlekamp-Massey
+// over 512 bits of one state bit; degree 256 (the transition's characteristic
+// polynomial, which is primitive) is checked.
+const Poly& xoshiro_charpoly() {
+  static const Poly m = [] {
+    Xoshiro g(0x2545F4914F6CDD1DULL);
+    const int N = 512;
+    std::vector<int> a(N), C(N + 1, 0), B(N + 1, 0);
+    for (int k = 0; k < N; ++k) {
+      a[k] = (int)(g.s[0] & 1);
+      g.next();
+    }
+    C[0] = B[0] = 1;
+    int L = 0, mm = 1;
+    for (int k = 0; k < N; ++k) {
+      int d = a[k];
+      for (int i = 1; i <= L; ++i) d ^= C[i] & a[k - i];
+      if (!d) {
+        ++mm;
+      } else if (2 * L <= k) {
+        const std::vector<int> Tm = C;
+        for (int i = 0; i + mm <= N; ++i) C[i + mm] ^= B[i];
+        L = k + 1 - L;
+        B = Tm;
+        mm = 1;
+      } else {
+        for (int i = 0; i + mm <= N; ++i) C[i + mm] ^= B[i];
+        ++mm;
+      }
+    }
+    if (L != 256) throw std::runtime_error("xoshiro256 minimal polynomial is not of degree 256");
+    Poly r;
+    for (int i = 0; i <= L; ++i) r[i] = C[L - i];  // reciprocal of the connection polynomial
+    return r;
+  }();
+  return m;
+}
+
+Poly poly_mulmod(const Poly& a, const Poly& b) {
+  const Poly& m = xoshiro_charpoly();
+  Poly r;
+  for (int i = 0; i < 256; ++i)
+    if (a[i]) r ^= b << i;
+  for (int k = 510; k >= 256; --k)
+    if (r[k]) r ^= m << (k - 256);
+  return r;
+}
+
+// q_L = x^(L*chunk) mod m for the 32 lanes, self-checked once per chunk
+// against stepping the generator chunk times.
+const LanePolys& lane_polys(std::uint64_t chunk) {
+  static std::mutex mu;
+  static std::map<std::uint64_t, LanePolys> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(chunk);
+  if (it != cache.end()) return it->second;
+  Poly x, base, acc;
+  x[1] = 1;
+  acc[0] = 1;
+  base = x;
+  for (std::uint64_t e = chunk; e; e >>= 1) {  // x^chunk
+    if (e & 1) acc = poly_mulmod(acc, base);
+    base = poly_mulmod(base, base);
+  }
+  LanePolys lp{};
+  Poly q;
+  q[0] = 1;
+  for (int L = 0; L < 32; ++L) {
+    for (int i = 0; i < 256; ++i)
+      if (q[i]) lp.w[L][i >> 6] |= 1ull << (i & 63);
+    q = poly_mulmod(q, acc);
+  }
+  {  // self-check: lane 1's jump equals chunk serial steps
+    Xoshiro g(0x9E3779B97F4A7C15ULL ^ chunk), h = g;
+    for (std::uint64_t k = 0; k < chunk; ++k) h.next();
+    std::uint64_t a[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 256; ++i) {
+      if ((lp.w[1][i >> 6] >> (i & 63)) & 1)
+        for (int w = 0; w < 4; ++w) a[w] ^= g.s[w];
+      g.next();
+    }
+    for (int w = 0; w < 4; ++w)
+      if (a[w] != h.s[w]) throw std::runtime_error("xoshiro256 jump polynomial self-check failed");
+  }
+  return cache.emplace(chunk, lp).first->second;
+}
+
 // Stream-ordered buffers from the device's default memory pool (release
 // threshold raised once, so freed blocks stay in the pool).  Sweeps call the
 // batch entry point once per harness cell, often from many host threads at
@@ -337,7 +520,12 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
   // every block's timestamps stay 8-byte aligned
   const std::uint64_t per_round = (rows * 9 + 15) / 16 * 16;
   std::uint32_t rb = (std::uint32_t)std::max<std::uint64_t>(1, (128ull << 20) / per_round);
-  if (rb > 4) rb = 4;
+  if (rb > kMaxBlockRounds) rb = kMaxBlockRounds;
+  // lane-parallel draws for blocks of >= 512 draws per stream (enough per
+  // lane to pay for the 256-step jump); MOSHPIT_SERIAL_DRAWS=1 keeps one
+  // thread per stream
+  static const bool serial_draws = std::getenv("MOSHPIT_SERIAL_DRAWS") != nullptr;
+  const bool lanes = !serial_draws;
   if (rb > rounds) rb = rounds ? rounds : 1;
   PoolBuffer dbuf0(per_round * rb + 16, st.s), dbuf1(per_round * rb + 16, st.s);
   PoolBuffer* dbufs[2] = {&dbuf0, &dbuf1};
@@ -364,10 +552,18 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     const std::uint32_t r0 = b * rb;
     const std::uint32_t nr = std::min(rb, rounds - r0);
     if (b >= 2) MB_CUDA(cudaStreamWaitEvent(ds.s, ev_free[b & 1], 0));
-    draws_kernel<<<(2 * trials + 63) / 64, 64, 0, ds.s>>>(
-        rstate.as<std::uint64_t>(), rstate.as<std::uint64_t>() + (std::uint64_t)trials * 4,
-        trials, (std::uint32_t)n, nr, per_round, p, dbufs[b & 1]->as<std::uint8_t>(),
-        act_d.as<std::uint32_t>(), rounds, r0);
+    if (lanes && (std::uint64_t)nr * n >= 512) {
+      const std::uint64_t chunk = ((std::uint64_t)nr * n + 31) / 32;
+      draws_lanes_kernel<<<trials, 64, 0, ds.s>>>(
+          rstate.as<std::uint64_t>(), rstate.as<std::uint64_t>() + (std::uint64_t)trials * 4,
+          trials, (std::uint32_t)n, nr, per_round, p, dbufs[b & 1]->as<std::uint8_t>(),
+          act_d.as<std::uint32_t>(), rounds, r0, chunk, lane_polys(chunk));
+    } else {
+      draws_kernel<<<(2 * trials + 63) / 64, 64, 0, ds.s>>>(
+          rstate.as<std::uint64_t>(), rstate.as<std::uint64_t>() + (std::uint64_t)trials * 4,
+          trials, (std::uint32_t)n, nr, per_round, p, dbufs[b & 1]->as<std::uint8_t>(),
+          act_d.as<std::uint32_t>(), rounds, r0);
+    }
     MB_LAUNCH_CHECK();
     MB_CUDA(cudaEventRecord(ev_drawn[b & 1], ds.s));
   };

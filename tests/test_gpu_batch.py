@@ -48,10 +48,14 @@ def test_batch_equals_reference_harness(mb, refh, n, p, dim, init):
         assert rep.active_counts == want["active_counts"].tolist()
 
 
+# (n, R): blocks of 4 rounds hold n*rounds draws per stream; >= 512 take the
+# lane-parallel jump-ahead draws, fewer the serial chain.  (130, 9) mixes
+# both in one call (520, 520, then 130 draws), (100, 3) is serial only.
+@pytest.mark.parametrize("n,R", [(500, 7), (130, 9), (100, 3)])
 @pytest.mark.parametrize("f64", [False, True])
-def test_batch_equals_single_trials(mb, oracle, f64):
+def test_batch_equals_single_trials(mb, oracle, f64, n, R):
     dt = np.float64 if f64 else np.float32
-    M, d, n, dim, p, R = 8, 3, 500, 37, 0.05, 7
+    M, d, dim, p = 8, 3, 37, 0.05
     seeds = [11, 12, 13, 2**40 + 5, 7]
     x = np.stack([oracle.init_state(1000 + t, n, dim, dtype=dt) for t in range(len(seeds))])
     reps = mb.run_moshpit_batch(mb.GridConfig(M, d, 1), x, mb.FailureModel(p), seeds, R,
