@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 
 #include "pairwise.cuh"
 #include "blocktree.cuh"
@@ -567,6 +568,14 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     MB_LAUNCH_CHECK();
     MB_CUDA(cudaEventRecord(ev_drawn[b & 1], ds.s));
   };
+  // Narrow vectors (the harness's dim-1/2 sweeps): one launch per round, the
+  // group means computed by kernel 1's CTA of each trial.  MOSHPIT_BATCH_FUSE=0
+  // keeps the separate kernel-2 launch (same results bit for bit).
+  static const bool fuse_env = [] {
+    const char* e = std::getenv("MOSHPIT_BATCH_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  const bool fuse = fuse_env && dim > 0 && dim <= 4;
   const std::uint32_t nblocks = rounds ? (rounds + rb - 1) / rb : 0;
   if (nblocks) draw_block(0);
   for (std::uint32_t b = 0; b < nblocks; ++b) {
@@ -597,9 +606,17 @@ void run_batch(std::uint32_t M, std::uint32_t d, std::uint32_t trials, const T* 
     a.scs = scs.as<std::uint32_t>();
     a.sgi = sgi.as<std::uint32_t>();
     a.batch = trials;
+    if (fuse) {  // kernel 2 inside kernel 1's CTA (see GroupArgs::fuse_x)
+      a.fuse_x = x.ptr;
+      a.fuse_ld = ld;
+      a.fuse_dim = dim;
+      a.fuse_stride = n * ld;
+      a.fuse_f64 = std::is_same_v<T, double> ? 1 : 0;
+    }
     launch_form_groups(a, true, st.s);
-    launch_group_mean_batch<T>(x.as<T>(), n * ld, ld, dim, (std::uint32_t)n, trials, a.members,
-                               a.goff, a.act, a.counts, st.s);
+    if (!fuse)
+      launch_group_mean_batch<T>(x.as<T>(), n * ld, ld, dim, (std::uint32_t)n, trials,
+                                 a.members, a.goff, a.act, a.counts, st.s);
     if (dg && dim < 32) {
       round_diag_narrow<T><<<trials, kTreeThreads, 0, st.s>>>(
           x.as<T>(), (std::uint32_t)n, ld, (std::uint32_t)dim, ref.as<double>(), sq.as<double>(),

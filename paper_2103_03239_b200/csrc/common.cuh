@@ -242,6 +242,13 @@ struct GroupArgs {
   // per-peer array above is [batch][n] (goff [batch][n+1], counts [batch][4],
   // sidx [batch][pow2(n)]).  0 = a single trial.
   std::uint32_t batch = 0;
+  // Fused narrow round (trial batching, tiny dim): after the tables, the same
+  // CTA averages the non-voided groups of its trial's state rows in place --
+  // kernel 2's work, same tree, same rounding.  Rows at fuse_x + t*fuse_stride
+  // (elements), pitch fuse_ld, fuse_dim columns, fp64 when fuse_f64.
+  void* fuse_x = nullptr;
+  std::uint64_t fuse_ld = 0, fuse_dim = 0, fuse_stride = 0;
+  int fuse_f64 = 0;
 };
 
 std::size_t group_smem_bytes(std::uint32_t n, bool packed);

@@ -19,6 +19,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "pairwise.cuh"
 
 namespace mb200 {
 namespace {
@@ -88,6 +89,32 @@ __device__ std::uint32_t block_exclusive_scan(std::uint32_t v,
   if (total) *total = warp_tot[kThreads / 32 - 1];
   __syncthreads();
   return r;
+}
+
+// Kernel 2 for narrow vectors inside kernel 1's CTA: one thread per
+// (active group, column), the reference pairwise tree (core.hpp:72-81) over
+// the members in group order, divided by the member count (core.hpp:91-106),
+// written back to every member.  Items touch disjoint (row, column) sets.
+template <typename T>
+__device__ void fused_group_means(const GroupArgs& a, std::uint32_t n_act) {
+  T* x = static_cast<T*>(a.fuse_x) + (a.batch ? blockIdx.x * a.fuse_stride : 0);
+  const std::uint64_t dim = a.fuse_dim, ld = a.fuse_ld, items = (std::uint64_t)n_act * dim;
+  for (std::uint64_t it = threadIdx.x; it < items; it += kThreads) {
+    const std::uint32_t g = a.act[it / dim];
+    const std::uint64_t j = it % dim;
+    const std::uint32_t beg = a.goff[g], cnt = a.goff[g + 1] - beg;
+    const std::uint32_t* mem = a.members + beg;
+    auto ld_fn = [&](std::uint32_t k) -> T { return x[(std::uint64_t)mem[k] * ld + j]; };
+    T m;
+    if constexpr (std::is_same_v<T, double>) {
+      const double s = pairwise_rt<double>(ld_fn, cnt, [](double u, double v) { return __dadd_rn(u, v); }, 0.0);
+      m = __ddiv_rn(s, (double)cnt);
+    } else {
+      const float s = pairwise_rt<float>(ld_fn, cnt, [](float u, float v) { return __fadd_rn(u, v); }, 0.0f);
+      m = __fdiv_rn(s, (float)cnt);
+    }
+    for (std::uint32_t k = 0; k < cnt; ++k) x[(std::uint64_t)mem[k] * ld + j] = m;
+  }
 }
 
 template <class View>
@@ -308,6 +335,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       a.counts[2] = n_rows;
     }
     if (a.totals) a.totals[0] += n_rows;
+  }
+  if (a.fuse_x && a.act) {
+    __syncthreads();  // act / goff / members of this CTA are written
+    if (a.fuse_f64) fused_group_means<double>(a, n_act);
+    else fused_group_means<float>(a, n_act);
   }
 }
 
