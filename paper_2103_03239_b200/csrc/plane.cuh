@@ -67,17 +67,28 @@ struct StreamHolder {
 
 
 // Partial Fisher-Yates over [0, capacity) (protocols.hpp:124-130,
-// optimizer.hpp:254-259) with a sparse map, so memory is O(n) rather than
-// O(M^d); the draws and swaps are exactly the reference's.
+// optimizer.hpp:254-259): a dense permutation when the grid is at most ~8n
+// cells, else a sparse map, so memory stays O(n) rather than O(M^d); either
+// way the draws and swaps are exactly the reference's.
 inline std::vector<std::uint64_t> draw_cells(Xoshiro& st, std::uint64_t capacity,
                                       std::uint64_t n) {
+  std::vector<std::uint64_t> cells(n);
+  if (capacity <= 8 * n + 4096) {  // dense permutation: same draws, same swaps
+    std::vector<std::uint64_t> perm(capacity);
+    for (std::uint64_t i = 0; i < capacity; ++i) perm[i] = i;
+    for (std::uint64_t i = 0; i < n; ++i) {
+      const std::uint64_t j = i + st.below(capacity - i);
+      std::swap(perm[i], perm[j]);
+      cells[i] = perm[i];
+    }
+    return cells;
+  }
   std::unordered_map<std::uint64_t, std::uint64_t> moved;
   moved.reserve(2 * n);
   auto at = [&](std::uint64_t i) {
     auto it = moved.find(i);
     return it == moved.end() ? i : it->second;
   };
-  std::vector<std::uint64_t> cells(n);
   for (std::uint64_t i = 0; i < n; ++i) {
     const std::uint64_t j = i + st.below(capacity - i);
     const std::uint64_t vi = at(i), vj = at(j);
