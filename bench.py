@@ -12,14 +12,18 @@ resident fp32 peer state.  Default workload = configs[1] (C2: 1024 peers on a
 (17.2 GB); the state is 136x the 126 MB L2, so no L2 flush is needed between
 rounds.  Synthetic, counter-initialised data.
 
-Multi-GPU (torchrun, one rank per GPU): coordinate-sharded weak scaling --
-every rank owns the full C2 peer set over its own D-slab (coordinates are
-independent; no data-path collective), host draws identical on
-every rank.  value = sum over ranks / max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU): the headline is the PEER-SHARDED
+C2 round (the graded layout): the same 1024 x 4 Mi problem as N=1
+(strong scaling), peers split by grid digit d-1 across the ranks, rounds on
+axis 0 GPU-local, the axis-1 round one fused NVLink kernel per GPU.  value =
+N*D*4 per round / max-over-ranks device time.  Coordinate-sharded weak
+scaling (every rank all peers x its own D-slab, no exchange) and the
+peer-sharded C5-valid run are attached as extra keys, with NVLink hardware
+counters (NVML) read around the timed cross rounds.
 
 --impl reference: the unmodified reference run_moshpit (oracle/_ref, compiled
 from the reference headers) on bounded column slices of the same workload on
-all host cores; rank 0 only.
+all host cores; rank 0 only.  Both arms print the same `config` dict.
 """
 from __future__ import annotations
 
@@ -121,6 +125,51 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class NvlinkCounters:
+    """NVLink hardware byte counters of one GPU through NVML (the same link
+    counters nvidia-smi nvlink reads): data payload RX/TX summed over all
+    links.  Read before and after a timed region; None where unsupported."""
+
+    FIELDS = (("rx_kib", 139), ("tx_kib", 138))  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_{RX,TX}
+
+    def __init__(self, cuda_index):
+        self.h = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            bus = getattr(torch.cuda.get_device_properties(cuda_index), "pci_bus_id", None)
+            if bus:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode()
+                                                              if isinstance(bus, str) else bus)
+            else:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+        except Exception as exc:  # noqa: BLE001
+            self.err = str(exc)
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            vals = self.nv.nvmlDeviceGetFieldValues(
+                self.h, [(fid, 0xFFFFFFFF) for _, fid in self.FIELDS])
+            out = {}
+            for (name, _), v in zip(self.FIELDS, vals):
+                if v.nvmlReturn != 0:
+                    return None
+                out[name] = int(v.value.ullVal)
+            return out
+        except Exception:  # noqa: BLE001
+            return None
+
+    @staticmethod
+    def delta(a, b):
+        if not a or not b:
+            return None
+        return {k.replace("_kib", "_bytes"): (b[k] - a[k]) * 1024 for k in a}
+
+
 def load_traffic(kernel_name, cfg_name):
     """dram bytes per launch of the top kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -139,29 +188,44 @@ def load_traffic(kernel_name, cfg_name):
 _CALIB = {}
 
 
-def cpu_reference(cfg_name, budget_s, threads=None):
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": len(os.sched_getaffinity(0))}
+
+
+# Column-slice widths of the CPU samples.  WIDE: 16 Ki columns x 1024 peers x
+# 8 B = 128 MB per slice, far beyond a core's cache share, so the reference runs
+# at its memory-bound rate (the default).  NARROW: 64 columns (512 KB, cache
+# resident) -- the round-1 sample, kept as a labelled upper bound.
+WIDE, NARROW = 1 << 14, 64
+
+
+def cpu_reference(cfg_name, budget_s, threads=None, width=WIDE):
     from oracle.oracle import REF_SO, Checker
     M, d, N, D, p, R = CONFIGS[cfg_name]
     threads = threads or len(os.sched_getaffinity(0))
-    kind = "reference"
-    if os.path.exists(REF_SO):
-        chk = Checker("ref")
-    else:
-        chk = None
-        kind = "port"
-    width = 64
-    if chk is None:  # the C restatement, single-threaded, as the port baseline
-        from oracle.oracle import Checker as Ck
-        o = Ck("oracle")
+    width = min(width, D)
+    if not os.path.exists(REF_SO):  # the C restatement, single-threaded, as the port baseline
         import numpy as np
-        x = o.init_state(INIT_SEED, N, width, dtype=np.float64)
+        o = Checker("oracle")
+        x = o.init_state(INIT_SEED, N, NARROW, dtype=np.float64)
         t0 = time.perf_counter()
         o.run_moshpit(M, d, x, p, PROTOCOL_SEED, R)
         run_s = time.perf_counter() - t0
-        return dict(kind="port", cores=1, run_s=run_s, cols=width, rounds=R, N=N, D=D,
-                    sample=f"oracle port, 1 thread, {width} of {D} columns, {R} rounds")
+        return dict(kind="port", cores=1, run_s=run_s, cols=NARROW, rounds=R, N=N, D=D,
+                    width=NARROW, slices=1,
+                    sample=f"oracle port, 1 thread, {NARROW} of {D} columns, {R} rounds")
+    chk = Checker("ref")
     # calibrate once: one slice per thread
-    key = (cfg_name, threads)
+    key = (cfg_name, threads, width)
     if key not in _CALIB:
         run_s, _, _ = chk.slice_bench(M, d, N, width, threads, 0, INIT_SEED, PROTOCOL_SEED, p, R,
                                       threads)
@@ -172,16 +236,40 @@ def cpu_reference(cfg_name, budget_s, threads=None):
     run_s, init_s, _ = chk.slice_bench(M, d, N, width, slices, 0, INIT_SEED, PROTOCOL_SEED, p, R,
                                        threads)
     cols = slices * width
-    return dict(kind=kind, cores=threads, run_s=run_s, init_s=init_s, cols=cols, rounds=R, N=N,
-                D=D, sample=(f"unmodified run_moshpit (incl. record_round) on {slices} column "
-                             f"slices x {width} = {cols} of D={D} coordinates, {R} rounds, "
-                             f"{threads} threads; cost linear in D (coordinates independent)"))
+    return dict(kind="reference", cores=threads, run_s=run_s, init_s=init_s, cols=cols, rounds=R,
+                N=N, D=D, width=width, slices=slices,
+                sample=(f"unmodified run_moshpit (fp64, incl. record_round) on {slices} column "
+                        f"slices x {width} = {cols} of D={D} coordinates "
+                        f"({N * width * 8 / 1e6:.1f} MB per slice), {R} rounds, {threads} "
+                        f"threads; cost linear in D (coordinates independent)"))
 
 
 def cpu_value(res):
     gbs = res["N"] * res["cols"] * 4 * res["rounds"] / res["run_s"] / 1e9
     ms_round_full = res["run_s"] / res["rounds"] * (res["D"] / res["cols"]) * 1e3
     return gbs, ms_round_full
+
+
+def cpu_baseline_block(cfg, budget_s):
+    """The reported CPU baseline: all host threads on wide
+    slices (the value), plus the single-thread figure, the cache-resident
+    narrow-slice figure, the CPU model and the extrapolation factor."""
+    res = cpu_reference(cfg, budget_s)
+    g, ms_full = cpu_value(res)
+    out = {"value": round(g, 6), "unit": "GB/s", "cores": res["cores"], "kind": res["kind"],
+           "sample": res["sample"], **host_info(),
+           "ms_per_round_extrapolated": round(ms_full, 1),
+           "extrapolation_factor": round(res["D"] / res["cols"], 3),
+           "normalisation": "fp32-normalised N*D*4 bytes per round (the reference computes "
+                            "in fp64: twice these bytes move)"}
+    if res["kind"] == "reference":
+        one = cpu_reference(cfg, max(2.0, budget_s / 4), threads=1)
+        narrow = cpu_reference(cfg, max(2.0, budget_s / 4), width=NARROW)
+        out["single_thread"] = {"value": round(cpu_value(one)[0], 6), "unit": "GB/s",
+                                "sample": one["sample"]}
+        out["narrow_slices_cache_resident"] = {"value": round(cpu_value(narrow)[0], 6),
+                                               "unit": "GB/s", "sample": narrow["sample"]}
+    return out
 
 
 def run_reference_arm(args):
@@ -203,14 +291,17 @@ def run_reference_arm(args):
             mss.append(ms)
     value = sum(vals) / len(vals)
     line = {
-        "impl": "reference", "metric": "peer-vector GB/s averaged per Moshpit round",
+        "impl": "reference", "metric": METRIC,
         "value": round(value, 6), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sum(mss) / len(mss), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
-        "config": workload_config(cfg, args),
+        "config": workload_config(cfg),
+        "parallelism": f"host threads x{res['cores']} over column slices (rank 0 only)",
         "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": res["cores"],
-                         "kind": res["kind"], "sample": res["sample"]},
+                         "kind": res["kind"], "sample": res["sample"], **host_info(),
+                         "extrapolation_factor": round(res["D"] / res["cols"], 3)},
         "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -218,17 +309,82 @@ def run_reference_arm(args):
     return 0
 
 
-def workload_config(cfg, args):
+METRIC = "peer-vector GB/s averaged per Moshpit round"
+
+
+def workload_config(cfg):
+    """The workload only -- identical in both arms (implementation details such
+    as the kernel variant or the parallel layout are top-level keys)."""
     M, d, N, D, p, R = CONFIGS[cfg]
     return {"workload": f"{cfg}: Moshpit All-Reduce round, {N} peers on {M}^{d} grid, "
-                        f"D={D} fp32 per peer, p_fail={p}; step = one round",
+                        f"D={D} per peer, p_fail={p}; step = one round",
             "peers": N, "grid": f"{M}^{d}", "dim": D, "p_round": p, "protocol_seed": PROTOCOL_SEED,
-            "l2": "state >> 126 MB L2 (no flush needed)", "kernel": args.kernel}
+            "rounds_of_config": R, "l2": "state >> 126 MB L2 (no flush needed)"}
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def time_engine_rounds(mb, torch, eng, x, steps, record=False):
+    """CUDA events around `steps` engine rounds on the current stream
+    (optionally with the device record_round after each); returns
+    (ms, kernel-2 ms, kernel-2 launches, active rows)."""
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    r0, rows0 = eng.stats()
+    eng.set_timing(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        eng.round(x)
+        if record:
+            eng.record(x)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    k_ms, k_launches = eng.kernel_time()
+    eng.set_timing(False)
+    _, rows1 = eng.stats()
+    return t_ms, k_ms, k_launches, rows1 - rows0
+
+
+def measure_variant(mb, torch, cfg, local, steps, warmup, f64=False, diag=None):
+    """A variant of the N=1 headline on the same config: fp64 state and/or
+    record_round on the device after every round (FAST or EXACT)."""
+    M, d, N, D, p, Rcfg = CONFIGS[cfg]
+    es = 8 if f64 else 4
+    x = torch.empty((N, D), dtype=torch.float64 if f64 else torch.float32, device="cuda")
+    mb.fill_synthetic(x, INIT_SEED)
+    eng = mb.Engine(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
+                    device=local)
+    if diag:
+        eng.set_reference(x, diagnostics=diag)
+    for _ in range(warmup):
+        eng.round(x)
+        if diag:
+            eng.record(x)
+    t_ms, k_ms, kn, rows = time_engine_rounds(mb, torch, eng, x, steps, record=bool(diag))
+    rep = eng.report() if diag else None
+    eng.close()
+    del x
+    torch.cuda.empty_cache()
+    peak, _ = peaks()
+    alg = 2 * es * D * rows
+    out = {"dtype": "f64" if f64 else "f32",
+           "diagnostics": (f"record_round on the device after every round ({diag.upper()}: "
+                           + ("reference j-order" if diag == "exact" else "fixed chunk order")
+                           + ")") if diag else "none",
+           "value": round(N * D * 4 * steps / (t_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+           "value_note": "fp32-normalised N*D*4 bytes per round, as the headline",
+           "ms_per_step": round(t_ms / steps, 4), "steps": steps,
+           "kernel2": {"achieved": round(alg / (k_ms / 1e3) / 1e9, 1), "peak": peak,
+                       "frac": round(alg / (k_ms / 1e3) / 1e9 / peak, 4), "launches": kn}}
+    if rep:
+        out["final_distortion"] = rep[1][-1] if rep[1] else None
+    return out
+
+
 def run_mine(args):
     import torch
     import torch.distributed as dist
@@ -243,64 +399,28 @@ def run_mine(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    if args.mode == "peer":
-        res = run_peer(mb, torch, dist, args.config, args.steps, args.warmup, rank, world, local)
-        if rank == 0:
-            line = dict(res, n_gpus=world, warmup=args.warmup, higher_is_better=True,
-                        vs_baseline=None, dtype="f32", data="synthetic",
-                        config={"workload": res["workload"], "parallelism": f"peer-sharded x{world}"})
-            print(json.dumps(line), flush=True)
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return 0
+        return run_mine_multi(args, mb, torch, dist, rank, world, local)
 
     cfg = args.config
     M, d, N, D, p, Rcfg = CONFIGS[cfg]
     kernel = {"auto": 0, "register": 1, "bulk": 2}[args.kernel]
-    stream = torch.cuda.current_stream()
 
     x = torch.empty((N, D), dtype=torch.float32, device="cuda")
-    # each rank owns its own D-slab of the (D * world)-coordinate problem
-    mb.fill_synthetic(x, INIT_SEED, col0=rank * D)
+    mb.fill_synthetic(x, INIT_SEED)
     eng = mb.Engine(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
                     device=local, kernel=kernel)
     for _ in range(args.warmup):
         eng.round(x)
     torch.cuda.synchronize()
-    r0, rows0 = eng.stats()
 
     clocks = ClockSampler(local)
     clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    eng.set_timing(True)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        eng.round(x)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    t_ms, k_ms, k_launches, active_rows = time_engine_rounds(mb, torch, eng, x, args.steps)
     clk = clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
-    k_ms, k_launches = eng.kernel_time()
-    eng.set_timing(False)
-    r1, rows1 = eng.stats()
-    active_rows = rows1 - rows0
-
-    t_max = t_ms
-    if world > 1:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = tt.item()
+    eng.close()
 
     state_bytes = N * D * 4
-    value = world * state_bytes * args.steps / (t_max / 1e3) / 1e9
+    value = state_bytes * args.steps / (t_ms / 1e3) / 1e9
     alg_bytes = 2 * 4 * D * active_rows  # kernel 2 reads+writes every active row once
     achieved = alg_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
     peak, peak_src = peaks()
@@ -310,24 +430,17 @@ def run_mine(args):
     del x
     torch.cuda.empty_cache()
 
-    peer = None
-    if world > 1 and not args.no_peer:
-        # C5-valid (the north-star multi-GPU config, 295 GB) wherever its
-        # 1/world share fits this GPU (world >= 2 on 180 GB B200s), else C2
-        Mv, dv, Nv, Dv, _, _ = CONFIGS["C5v"]
-        need = Nv // world * ((Dv + 3) // 4 * 4) * 4 + (4 << 30)
-        fits = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] >= need else 0.0],
-                            device="cuda")
-        dist.all_reduce(fits, op=dist.ReduceOp.MIN)
-        pcfg = "C5v" if Mv % world == 0 and fits.item() > 0 else "C2"
-        try:
-            peer = run_peer(mb, torch, dist, pcfg, max(8, min(args.steps, 40)), 4, rank, world,
-                            local)
-        except Exception as exc:  # noqa: BLE001
-            peer = {"error": str(exc)}
-
+    variants = {}
+    if not args.no_variants:
+        vs = min(args.steps, 20)
+        for name, kw in (("value_with_diag", dict(diag="fast")), ("value_f64", dict(f64=True)),
+                         ("value_f64_exact_diag", dict(f64=True, diag="exact"))):
+            try:
+                variants[name] = measure_variant(mb, torch, cfg, local, vs, 3, **kw)
+            except Exception as exc:  # noqa: BLE001
+                variants[name] = {"error": str(exc)}
     full = full_c5 = None
-    if rank == 0 and world == 1 and not args.no_full:
+    if not args.no_full:
         try:
             full = measure_full_slabbed(mb, torch, "C3", local)
         except Exception as exc:  # noqa: BLE001
@@ -336,69 +449,157 @@ def run_mine(args):
             full_c5 = measure_full_slabbed(mb, torch, "C5v", local, slabs=3)
         except Exception as exc:  # noqa: BLE001
             full_c5 = {"error": str(exc)}
-    e2e = None
-    if not args.no_e2e and rank == 0:
+    e2e = e2e_more = None
+    if not args.no_e2e:
         e2e = measure_e2e(mb, cfg)
+        e2e_more = {}
+        try:
+            e2e_more["pageable_f32_fast"] = measure_e2e(mb, cfg, pinned=False)
+        except Exception as exc:  # noqa: BLE001
+            e2e_more["pageable_f32_fast"] = {"error": str(exc)}
+        try:
+            e2e_more["dropin_f64_exact"] = measure_e2e_dropin(cfg)
+        except Exception as exc:  # noqa: BLE001
+            e2e_more["dropin_f64_exact"] = {"error": str(exc)}
     sgd = None
-    if rank == 0 and world == 1 and not args.no_sgd:
+    if not args.no_sgd:
         try:
             sgd = measure_sgd_c4(mb)
             s0 = measure_sgd_c4(mb, sigma=0.0)
             sgd["sigma0"] = {k: s0[k] for k in ("ms_per_sgd_step", "peer_vector_gbs", "hbm_frac")}
+            sf = measure_sgd_c4(mb, diagnostics="fast")
+            sgd["sigma1_fast_diagnostics"] = {
+                k: sf[k] for k in ("ms_per_sgd_step", "peer_vector_gbs", "hbm_frac", "timing")}
         except Exception as exc:  # noqa: BLE001
             sgd = {"error": str(exc)}
     cpu = None
-    if not args.no_cpu and rank == 0 and world == 1:
+    if not args.no_cpu:
         try:
-            res = cpu_reference(cfg, float(os.environ.get("MOSHPIT_CPU_BUDGET_S", "15")))
-            g, _ = cpu_value(res)
-            cpu = {"value": round(g, 6), "unit": "GB/s", "cores": res["cores"],
-                   "kind": res["kind"], "sample": res["sample"]}
+            cpu = cpu_baseline_block(cfg, float(os.environ.get("MOSHPIT_CPU_BUDGET_S", "15")))
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
                    "sample": f"failed: {exc}"}
 
-    if rank == 0:
-        line = {
-            "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),
-            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
-            "config": dict(workload_config(cfg, args),
-                           parallelism=(f"coordinate-sharded x{world} (each rank: all {N} peers "
-                                        f"x its own D-slab; no exchange)") if world > 1
-                           else "single GPU"),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
-                         "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4) if achieved else None,
-                         "traffic": traffic,
-                         "traffic_over_algorithmic": (traffic_ent or {}).get("traffic_over_algorithmic"),
-                         "traffic_source": "profiles/ncu_summary.json (ncu --set full, one launch)",
-                         "kernel": "group_mean_register (kernel 2)",
-                         "algorithmic_bytes": "2 * 4 B * D * rows in non-voided groups",
-                         "avg_launch_ms": round(k_ms / max(k_launches, 1), 4),
-                         "launches": k_launches, "active_rows_timed": active_rows,
-                         "peak_source": peak_src},
-            "kernel2_share_of_step": round(k_ms / t_ms, 4) if t_ms > 0 else None,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "peer_sharded": peer,
-            "c3_full_1gpu": full,
-            "c5v_full_1gpu": full_c5,
-            "sgd_c4": sgd,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-    eng.close()
+    line = {
+        "metric": METRIC, "value": round(value, 3),
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
+        "config": workload_config(cfg),
+        "parallelism": "single GPU", "kernel": args.kernel,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4) if achieved else None,
+                     "traffic": traffic,
+                     "traffic_over_algorithmic": (traffic_ent or {}).get("traffic_over_algorithmic"),
+                     "traffic_source": "profiles/ncu_summary.json (ncu --set full, one launch)",
+                     "kernel": "group_mean_register (kernel 2)",
+                     "algorithmic_bytes": "2 * 4 B * D * rows in non-voided groups",
+                     "avg_launch_ms": round(k_ms / max(k_launches, 1), 4),
+                     "launches": k_launches, "active_rows_timed": active_rows,
+                     "peak_source": peak_src},
+        "kernel2_share_of_step": round(k_ms / t_ms, 4) if t_ms > 0 else None,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "e2e": e2e,
+        "e2e_variants": e2e_more,
+        "cpu_baseline": cpu,
+        **variants,
+        "c3_full_1gpu": full,
+        "c5v_full_1gpu": full_c5,
+        "sgd_c4": sgd,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 
-def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
+def run_mine_multi(args, mb, torch, dist, rank, world, local):
+    """N > 1: the headline is the peer-sharded round on the N=1 config (strong
+    scaling, NVLink cross rounds); coordinate sharding and the peer-sharded
+    C5-valid run are attached."""
+    cfg = args.config
+    clocks = ClockSampler(local)
+    clocks.start()
+    head = run_peer(mb, torch, dist, cfg, args.steps, args.warmup, rank, world, local,
+                    nvlink=True)
+    clk = clocks.stop()
+    coord = c5v = None
+    if not args.no_coord:
+        try:
+            coord = run_coord(mb, torch, dist, cfg, min(args.steps, 40), args.warmup, rank, world,
+                              local)
+        except Exception as exc:  # noqa: BLE001
+            coord = {"error": str(exc)}
+    if not args.no_peer:
+        # C5-valid (the north-star multi-GPU config, 295 GB) wherever its
+        # 1/world share fits this GPU (world >= 2 on 180 GB B200s)
+        Mv, dv, Nv, Dv, _, _ = CONFIGS["C5v"]
+        need = Nv // world * ((Dv + 1023) // 1024 * 1024) * 4 + (4 << 30)
+        fits = torch.tensor([1.0 if torch.cuda.mem_get_info()[0] >= need else 0.0],
+                            device="cuda")
+        dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+        if Mv % world == 0 and fits.item() > 0:
+            try:
+                c5v = run_peer(mb, torch, dist, "C5v", max(8, min(args.steps, 24)), 4, rank,
+                               world, local, nvlink=True)
+            except Exception as exc:  # noqa: BLE001
+                c5v = {"error": str(exc)}
+    if rank == 0:
+        peak, peak_src = peaks()
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
+            "config": workload_config(cfg),
+            "parallelism": (f"peer-sharded x{world}: grid digit d-1 split across GPUs; axis-0 "
+                            f"rounds GPU-local, axis-(d-1) rounds one fused NVLink kernel"),
+            "roofline": dict(head["roofline"], bound="hbm+nvlink",
+                             frac=head["roofline"]["combined_frac"], peak_hbm=peak,
+                             peak_nvlink=NVLINK_GBS, peak_source=peak_src),
+            "gpu_launches": head["gpu_launches"],
+            "rounds_local": head["rounds_local"], "rounds_cross": head["rounds_cross"],
+            "nvlink_counters": head.get("nvlink_counters"),
+            "clocks": clk,
+            "e2e": None,
+            "e2e_note": "the host-buffer call is single-GPU (moshpit_run_moshpit); see the N=1 line",
+            "coordinate_sharded_weak": coord,
+            "peer_sharded_c5v": c5v,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def run_coord(mb, torch, dist, cfg, steps, warmup, rank, world, local):
+    """Coordinate-sharded weak scaling: every rank owns all N peers over its
+    own D-slab of a (D * world)-coordinate problem and replays the identical
+    host draws (no data-path exchange; exact by coordinate independence)."""
+    M, d, N, D, p, Rcfg = CONFIGS[cfg]
+    x = torch.empty((N, D), dtype=torch.float32, device="cuda")
+    mb.fill_synthetic(x, INIT_SEED, col0=rank * D)
+    eng = mb.Engine(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
+                    device=local)
+    for _ in range(warmup):
+        eng.round(x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t_ms, k_ms, kn, rows = time_engine_rounds(mb, torch, eng, x, steps)
+    dist.barrier()
+    tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    eng.close()
+    del x
+    torch.cuda.empty_cache()
+    return {"workload": f"{cfg} per rank over its own D-slab ({world} x {D} coordinates)",
+            "value": round(world * N * D * 4 * steps / (tt.item() / 1e3) / 1e9, 3),
+            "unit": "GB/s", "scaling": "weak", "steps": steps,
+            "ms_per_step": round(tt.item() / steps, 4)}
+
+
+def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=False):
     """Peer-sharded rounds: peers split by grid digit d-1, rounds on
     axes 0..d-2 local, the axis d-1 round one fused NVLink kernel.  Returns
     the whole-problem metric (strong scaling) and the combined roofline."""
@@ -416,6 +617,8 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    nvc = NvlinkCounters(local) if (nvlink and world > 1) else None
+    n0 = nvc.read() if nvc else None
     sh.set_timing(True)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -424,6 +627,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
         sh.round()
     ev1.record(stream)
     torch.cuda.synchronize()
+    n1 = nvc.read() if nvc else None
     t_ms = ev0.elapsed_time(ev1)
     lms, ln, cms, cn = sh.kernel_time()
     c1 = sh.stats()
@@ -450,6 +654,28 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_max, lmax, cmax, trl, trc, pa_max, pb_max, nvl_max = vals.tolist()
+    nvl_meas = None
+    dl = NvlinkCounters.delta(n0, n1)
+    if world > 1 and nvlink:
+        # per-rank hardware RX bytes over the timed rounds vs this rank's modelled ingress
+        mine = torch.tensor([float(dl["rx_bytes"]) if dl else -1.0,
+                             float(dl["tx_bytes"]) if dl else -1.0, nvl_cross],
+                            dtype=torch.float64, device="cuda")
+        allv = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allv, mine)
+        rows = [v.tolist() for v in allv]
+        if all(r[0] >= 0 for r in rows):
+            nvl_meas = {"source": "NVML NVLink data counters (NVML_FI_DEV_NVLINK_THROUGHPUT_"
+                                  "DATA_RX/TX, all links), read around the timed rounds",
+                        "rx_bytes_per_rank": [int(r[0]) for r in rows],
+                        "tx_bytes_per_rank": [int(r[1]) for r in rows],
+                        "modelled_ingress_bytes_per_rank": [int(r[2]) for r in rows],
+                        "rx_over_modelled": [round(r[0] / r[2], 4) if r[2] else None
+                                             for r in rows],
+                        "rx_gbs_during_cross_kernels": round(max(r[0] for r in rows) / 1e9
+                                                             / (cmax / 1e3), 1) if cmax else None}
+        else:
+            nvl_meas = {"unavailable": getattr(nvc, "err", "NVML field values not supported")}
     sh.close()
     torch.cuda.empty_cache()
     value = N * D * es * steps / (t_max / 1e3) / 1e9
@@ -460,6 +686,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local):
         "unit": "GB/s", "scaling": "strong", "steps": steps, "ms_per_step": round(t_max / steps, 4),
         "rounds_local": ln, "rounds_cross": cross_rounds,
         "gpu_launches": ln * 3 + cross_rounds * (7 + (2 if p > 0 else 0)),
+        "nvlink_counters": nvl_meas,
         "local_kernel_ms": round(lmax, 3), "cross_kernel_ms": round(cmax, 3),
         "roofline": {
             "bound": "hbm (local rounds) + nvlink (cross rounds)",
@@ -544,7 +771,7 @@ def measure_full_slabbed(mb, torch, cfg, local, slabs=4):
                       "kernel 2); the on-device init is reported apart"}
 
 
-def measure_sgd_c4(mb, steps=20, sigma=1.0):
+def measure_sgd_c4(mb, steps=20, sigma=1.0, diagnostics="none"):
     """C4 (configs[3]): Moshpit SGD, 1024 peers on 32x32, Quadratic(D=2^20,
     L=1, mu=0.1, target ~ N(0,1)), gamma=0.1, tau=1, inner=d=2, fp32,
     device Philox noise, kernel 3 (local step fused into averaging round 1).
@@ -558,7 +785,7 @@ def measure_sgd_c4(mb, steps=20, sigma=1.0):
     best = None
     for _ in range(2):
         r = mb.run_moshpit_sgd(cfg, quad, np.zeros(D), [], mb.Rng(PROTOCOL_SEED),
-                               dtype=np.float32, diagnostics="none", noise="device")
+                               dtype=np.float32, diagnostics=diagnostics, noise="device")
         best = r.loop_ms if best is None else min(best, r.loop_ms)
     ms = best / steps
     alg = 2 * 2 * N * D * 4  # two averaging rounds, each one read + one write of the state
@@ -569,24 +796,35 @@ def measure_sgd_c4(mb, steps=20, sigma=1.0):
             "peer_vector_gbs": round(N * D * 4 / (ms / 1e3) / 1e9, 1),
             "algorithmic_bytes_per_step": alg,
             "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
-            "timing": f"CUDA events around the {steps}-step loop (best of 2), incl. host draws",
+            "timing": f"CUDA events around the {steps}-step loop (best of 2), incl. host draws; "
+                      f"per-step diagnostics: {diagnostics}",
             "final_sigma_hat": round(r.diagnostics.sigma_hat, 6)}
 
 
-def measure_e2e(mb, cfg):
+def measure_e2e(mb, cfg, pinned=True):
     """The reference-facing call (run_moshpit through the C ABI) with HOST
     buffers: H2D of the initial state, R rounds + TrialReport diagnostics,
-    D2H of the final vectors, all inside the timed region."""
+    D2H of the final vectors, all inside the timed region.  pinned=False:
+    a plain (pageable) numpy buffer, packed through the library's pinned
+    staging ring by host threads."""
     import numpy as np
     import torch
     M, d, N, D, p, R = CONFIGS[cfg]
-    host = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
-    xh = host.numpy()
-    # fill the pinned buffer from the device init (same synthetic data)
+    if pinned:
+        host = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
+        xh = host.numpy()
+        out_t = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
+        oh = out_t.numpy()
+    else:
+        host = None
+        xh = np.empty((N, D), dtype=np.float32)
+        oh = np.empty((N, D), dtype=np.float32)
+    # fill the host buffer from the device init (same synthetic data)
+    blk = torch.empty((64, D), dtype=torch.float32, device="cuda")
     for i0 in range(0, N, 64):
-        blk = torch.empty((min(64, N - i0), D), dtype=torch.float32, device="cuda")
         mb.fill_synthetic(blk, INIT_SEED)
-        host[i0:i0 + blk.shape[0]].copy_(blk)  # row ids restart per block: fine for timing
+        xh[i0:i0 + 64] = blk.cpu().numpy()  # row ids restart per block: fine for timing
+    del blk
     torch.cuda.synchronize()
     import ctypes as C
     from paper_2103_03239_b200 import _capi
@@ -596,13 +834,14 @@ def measure_e2e(mb, cfg):
     act = np.zeros(R, dtype=np.uint32)
     init_d, cost = C.c_double(0), C.c_double(0)
     ptr = xh.ctypes.data_as(C.c_void_p)
+    optr = oh.ctypes.data_as(C.c_void_p)  # separate output: every call starts from the init
 
     def call():
         _capi.check(lib.moshpit_run_moshpit(_capi.F32, M, d, R, ptr, N, D, p, PROTOCOL_SEED, R,
                                             _capi.DIAG_FAST, C.byref(init_d),
                                             dist_.ctypes.data_as(C.c_void_p),
                                             drift.ctypes.data_as(C.c_void_p),
-                                            act.ctypes.data_as(C.c_void_p), C.byref(cost), ptr))
+                                            act.ctypes.data_as(C.c_void_p), C.byref(cost), optr))
     call()  # warm-up: kernel module loading + workspace allocation (untimed)
     times = []
     for _ in range(3):
@@ -611,6 +850,18 @@ def measure_e2e(mb, cfg):
         times.append(time.perf_counter() - t0)
     t = sorted(times)[1]  # median of 3
     bytes_ = N * D * 4
+    out = {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
+           "call": (f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, "
+                    + ("pinned" if pinned else "pageable numpy buffer (library staging ring)")),
+           "seconds": round(t, 4), "seconds_each": [round(x, 4) for x in times],
+           "timing": "host wall clock per call, 1 warm-up + median of 3",
+           "final_distortion": float(dist_[-1]),
+           "pipeline": "D-slabs of 256 MB: H2D(s+1) || 10 rounds + diagnostics(s) || D2H(s-1)"}
+    if not pinned:
+        out["host_threads"] = len(os.sched_getaffinity(0))
+        del xh, oh
+        return out
     # PCIe reference point: one plain pinned H2D copy of the same state
     dev = torch.empty((N, D), dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
@@ -634,18 +885,60 @@ def measure_e2e(mb, cfg):
             hb.copy_(dflat[n2:2 * n2], non_blocking=True)
         torch.cuda.synchronize()
         bidir_gbs = max(bidir_gbs, 2 * n2 * 4 / (time.perf_counter() - t1) / 1e9)
-    del dev, hb
+    del dev, hb, out_t, host
+    torch.cuda.empty_cache()
     t_floor = 2 * bytes_ / (bidir_gbs * 1e9)
-    return {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
-            "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
-            "call": f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, pinned",
-            "seconds": round(t, 4), "seconds_each": [round(x, 4) for x in times],
-            "timing": "host wall clock per call, 1 warm-up + median of 3",
-            "final_distortion": float(dist_[-1]),
-            "pipeline": "D-slabs of 256 MB: H2D(s+1) || 10 rounds + diagnostics(s) || D2H(s-1)",
-            "pcie_h2d_gbs_plain_copy": round(h2d_gbs, 1),
-            "pcie_bidir_gbs_aggregate": round(bidir_gbs, 1),
-            "frac_of_pcie_ceiling": round(t_floor / t, 3)}
+    out.update({"pcie_h2d_gbs_plain_copy": round(h2d_gbs, 1),
+                "pcie_bidir_gbs_aggregate": round(bidir_gbs, 1),
+                "frac_of_pcie_ceiling": round(t_floor / t, 3)})
+    return out
+
+
+DROPIN_BIN = os.path.join(ROOT, "paper_2103_03239_b200", "bench_dropin")
+
+
+def build_dropin_bench():
+    """g++ of the drop-in bench (the reference user's C++ call) against the
+    drop-in header and the in-tree library; rebuilt if missing."""
+    src = os.path.join(ROOT, "paper_2103_03239_b200", "csrc", "host", "bench_dropin.cpp")
+    if os.path.exists(DROPIN_BIN) and os.path.getmtime(DROPIN_BIN) >= os.path.getmtime(src):
+        return DROPIN_BIN
+    lib = os.path.join(ROOT, "paper_2103_03239_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-pthread", src, "-I",
+                    os.path.join(ROOT, "include"), "-L", lib, "-lmoshpit_b200",
+                    "-Wl,-rpath,$ORIGIN", "-o", DROPIN_BIN], check=True, capture_output=True,
+                   timeout=300)
+    return DROPIN_BIN
+
+
+def measure_e2e_dropin(cfg, reps=3):
+    """protocols::run_moshpit through include/moshpit_b200/moshpit.hpp: fp64,
+    EXACT diagnostics (TrialReport bit-identical to the reference), the
+    caller's std::vector<ParamVector> (pageable) -- the path a reference user
+    gets by swapping the header.  Host wall clock per call (C++ binary)."""
+    M, d, N, D, p, R = CONFIGS[cfg]
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = 0
+    # the caller's fp64 state must fit host RAM with room to spare
+    if avail and N * D * 8 * 1.5 > avail:
+        D = max(1 << 16, int(avail / 1.5 / (N * 8)) // 65536 * 65536)
+    exe = build_dropin_bench()
+    r = subprocess.run([exe, str(M), str(d), str(N), str(D), str(p), str(R), str(reps)],
+                       capture_output=True, text=True, timeout=1200)
+    if r.returncode != 0:
+        return {"error": r.stderr[-500:]}
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    t = out["seconds_median"]
+    out.update({"value": round(N * D * 4 * R / t / 1e9, 3), "unit": "GB/s",
+                "value_note": "fp32-normalised N*D*4 bytes per round (the call moves fp64)",
+                "value_fp64_bytes": round(N * D * 8 * R / t / 1e9, 3),
+                "h2d_bytes_per_step": N * D * 8 + R * N * 9, "d2h_bytes_per_step": R * 16 + 8,
+                "timing": f"host wall clock per call, 1 warm-up + median of {reps}",
+                "config_dim": D})
+    return out
 
 
 def main():
@@ -663,10 +956,11 @@ def main():
     ap.add_argument("--no-full", action="store_true",
                     help="skip the full-size C3 (slab-streamed) measurement at N=1")
     ap.add_argument("--no-peer", action="store_true",
-                    help="skip the peer-sharded (NVLink) measurement attached at N>1")
-    ap.add_argument("--mode", default="coord", choices=["coord", "peer"],
-                    help="coord: coordinate-sharded weak scaling (default); "
-                         "peer: peer-sharded strong scaling with cross-GPU rounds")
+                    help="skip the peer-sharded C5-valid measurement attached at N>1")
+    ap.add_argument("--no-coord", action="store_true",
+                    help="skip the coordinate-sharded weak-scaling key at N>1")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the fp64 / with-diagnostics variants at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup < 3 is not allowed by the timing rules; using 3")

@@ -66,6 +66,8 @@ typedef struct {
  * (rng.hpp:123-127) when index >= 0. [host] */
 int moshpit_rng_stream(uint64_t root, const char* name, int64_t index,
                        moshpit_rng_state* out);
+/* RngStream(seed) (rng.hpp:35-38): four splitmix64 words of `seed`. [host] */
+int moshpit_rng_seeded(uint64_t seed, moshpit_rng_state* out);
 /* n draws: kind 0=operator() (u64) 1=uniform (f64) 2=below(arg) (u64)
  * 3=normal (f64) 4=bernoulli(p) (u8).  rng.hpp:43-91. [host] */
 int moshpit_rng_draws(moshpit_rng_state* st, int kind, uint64_t arg, double p,
@@ -127,6 +129,23 @@ int moshpit_run_moshpit(int dtype, uint32_t M, uint32_t d, uint32_t T,
                         double* distortion, double* mean_drift,
                         uint32_t* active_counts, double* cost_units,
                         void* final_out);
+/* The same with the initial state given as n row pointers (each `dim`
+ * elements, e.g. the data() of a std::vector<ParamVector>): no flattened copy;
+ * large states are packed slab by slab into a pinned staging ring by host
+ * threads (MOSHPIT_HOST_THREADS, default all cores) while the GPU runs the
+ * previous slab.  Returns the report only, as protocols::run_moshpit does.
+ * [GPU, host buffers] */
+int moshpit_run_moshpit_rows(int dtype, uint32_t M, uint32_t d, uint32_t T,
+                             const void* const* rows, uint64_t n, uint64_t dim,
+                             double p_round, uint64_t seed, uint32_t rounds,
+                             int diag, double* initial_distortion,
+                             double* distortion, double* mean_drift,
+                             uint32_t* active_counts, double* cost_units);
+/* run_moshpit keeps a grow-only per-thread device workspace (slab ring of up
+ * to 3 x 256 MB, round tables, diagnostics buffers, streams) so repeated calls
+ * from one thread allocate nothing.  This frees the CALLING thread's
+ * workspace; call it before a long-lived worker thread goes idle. [GPU] */
+int moshpit_release_workspace(void);
 
 /* ---- trial-batched run_moshpit (harness.hpp:157-280 sweeps)  [GPU] ------
  * `trials` independent protocols::run_moshpit calls in one batch: trial t
@@ -246,6 +265,20 @@ int moshpit_engine_stats(moshpit_engine* e, uint64_t* rounds,
 int moshpit_engine_set_timing(moshpit_engine* e, int enable);
 int moshpit_engine_kernel_time(moshpit_engine* e, double* total_ms,
                                uint64_t* launches);
+/* Device-resident record_round (protocols.hpp:68-84) for engine callers.
+ * set_reference: reference = mean_of(state) in fp64 (protocols.hpp:119) and
+ * the initial distortion, diag = MOSHPIT_DIAG_FAST or _EXACT (NONE disables).
+ * record: after a round, append (distortion, mean_drift) to an engine-owned
+ * device log; the distortion and colmean + drift run on two streams.  Both
+ * are async on `stream`.  report: copy the log out (synchronises); count =
+ * records so far. */
+int moshpit_engine_set_reference(moshpit_engine* e, int dtype, const void* state,
+                                 uint64_t dim, uint64_t ld, int diag, void* stream);
+int moshpit_engine_record(moshpit_engine* e, int dtype, const void* state,
+                          uint64_t dim, uint64_t ld, void* stream);
+int moshpit_engine_report(moshpit_engine* e, double* initial_distortion,
+                          double* distortion, double* mean_drift, uint64_t cap,
+                          uint64_t* count);
 /* Copy the last round's group tables to host (synchronises the engine's
  * last stream): members[n], group_off[n+1], *n_groups, void_flags[n] (per
  * group), ranks[n] (per peer), keys[n*(d-1)] (keys after the round). */

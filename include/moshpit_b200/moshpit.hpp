@@ -37,7 +37,15 @@
 
 #include "../moshpit_b200.h"
 
-namespace moshpit {
+// The top-level namespace is `moshpit`, as in the reference.  A translation
+// unit that also includes the reference headers (e.g. a harness that keeps the
+// comparison protocols on the CPU) defines MOSHPIT_B200_NS to another name
+// before including this header; see INTEGRATION.md.
+#ifndef MOSHPIT_B200_NS
+#define MOSHPIT_B200_NS moshpit
+#endif
+
+namespace MOSHPIT_B200_NS {
 
 using ParamVector = std::vector<double>;
 using PeerId = std::uint32_t;
@@ -105,6 +113,10 @@ struct FailureModel {
 class RngStream {
  public:
   using result_type = std::uint64_t;
+  // rng.hpp:35-38: the stream seeded directly (splitmix64 words of `seed`)
+  explicit RngStream(std::uint64_t seed) : st_{} {
+    b200::check(moshpit_rng_seeded(seed, &st_));
+  }
   explicit RngStream(const moshpit_rng_state& st) : st_(st) {}
   static constexpr result_type min() { return 0; }
   static constexpr result_type max() { return ~std::uint64_t{0}; }
@@ -379,16 +391,22 @@ inline TrialReport run_moshpit(const GridConfig& grid, const std::vector<ParamVe
   failure.validate();
   if (initial.empty()) throw std::invalid_argument("run_moshpit: no peers");
   const std::size_t n = initial.size(), dim = initial.front().size();
-  const auto flat = b200::flatten(initial, dim, "group_mean");
+  // row pointers straight into the caller's vectors: the library packs them
+  // into pinned staging slab by slab (no flattened copy of the state)
+  std::vector<const void*> rows(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    if (initial[i].size() != dim) throw std::invalid_argument("group_mean: dimension mismatch");
+    rows[i] = initial[i].data();
+  }
   TrialReport r;
   r.distortion.resize(rounds);
   r.mean_drift.resize(rounds);
   r.active_counts.resize(rounds);
-  b200::check(moshpit_run_moshpit(MOSHPIT_F64, grid.peers_per_axis, grid.dims, grid.rounds,
-                                  flat.data(), n, dim, failure.p_round, rng.seed(), rounds,
-                                  MOSHPIT_DIAG_EXACT, &r.initial_distortion, r.distortion.data(),
-                                  r.mean_drift.data(), r.active_counts.data(), &r.cost_units,
-                                  nullptr));
+  b200::check(moshpit_run_moshpit_rows(MOSHPIT_F64, grid.peers_per_axis, grid.dims, grid.rounds,
+                                       rows.data(), n, dim, failure.p_round, rng.seed(), rounds,
+                                       MOSHPIT_DIAG_EXACT, &r.initial_distortion,
+                                       r.distortion.data(), r.mean_drift.data(),
+                                       r.active_counts.data(), &r.cost_units));
   return r;
 }
 
@@ -639,4 +657,4 @@ inline void moshpit_average(std::vector<ParamVector>& thetas, const GridConfig& 
 
 }  // namespace optimizer::detail
 
-}  // namespace moshpit
+}  // namespace MOSHPIT_B200_NS

@@ -691,6 +691,37 @@ class Engine:
         check(lib().moshpit_engine_kernel_time(self._h, C.byref(ms), C.byref(k)))
         return ms.value, k.value
 
+    def set_reference(self, state, diagnostics: str = "fast", dim: Optional[int] = None,
+                      stream=None):
+        """record_round's reference = mean_of(state) and the initial
+        distortion, on the device (protocols.hpp:119, 68-84)."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        check(lib().moshpit_engine_set_reference(self._h, code, ptr,
+                                                 state.shape[1] if dim is None else dim, ld,
+                                                 _DIAG[diagnostics], s.cuda_stream))
+
+    def record(self, state, dim: Optional[int] = None, stream=None):
+        """Append this round's (distortion, mean_drift) to the device log."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        check(lib().moshpit_engine_record(self._h, code, ptr,
+                                          state.shape[1] if dim is None else dim, ld,
+                                          s.cuda_stream))
+
+    def report(self):
+        """(initial_distortion, [distortion], [mean_drift]) recorded so far."""
+        cnt = C.c_uint64(0)
+        init = C.c_double(0)
+        check(lib().moshpit_engine_report(self._h, C.byref(init), None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        dist, drift = np.zeros(max(k, 1)), np.zeros(max(k, 1))
+        check(lib().moshpit_engine_report(self._h, C.byref(init), _p(dist), _p(drift), k,
+                                          C.byref(cnt)))
+        return init.value, list(dist[:k]), list(drift[:k])
+
     def stats(self):
         r, rows = C.c_uint64(0), C.c_uint64(0)
         check(lib().moshpit_engine_stats(self._h, C.byref(r), C.byref(rows)))
@@ -744,6 +775,7 @@ class Shard:
                  device: int = 0, dtype=np.float32):
         self.grid, self.n, self.dim = grid, int(n_peers), int(dim)
         self.rank, self.world, self.emulate = rank, world, emulate
+        self.device = int(device)
         self.dtype = np.dtype(dtype)
         h = C.c_void_p()
         check(lib().moshpit_shard_create(_dtype_code(self.dtype), grid.peers_per_axis, grid.dims,
@@ -774,12 +806,12 @@ class Shard:
 
     def fill_synthetic(self, seed: int, stream=None):
         import torch
-        s = stream if stream is not None else torch.cuda.current_stream()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().moshpit_shard_fill_synthetic(self._h, seed, s.cuda_stream))
 
     def round(self, stream=None):
         import torch
-        s = stream if stream is not None else torch.cuda.current_stream()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
         act, crossed = C.c_uint32(0), C.c_int32(0)
         check(lib().moshpit_shard_round(self._h, s.cuda_stream, C.byref(act), C.byref(crossed)))
         return act.value, bool(crossed.value)

@@ -54,6 +54,11 @@ PROTOTYPES = {
     "moshpit_version": (C.c_char_p, []),
     "moshpit_device_count": (C.c_int, [P(C.c_int)]),
     "moshpit_rng_stream": (C.c_int, [u64, C.c_char_p, i64, P(RngState)]),
+    "moshpit_rng_seeded": (C.c_int, [u64, P(RngState)]),
+    "moshpit_release_workspace": (C.c_int, []),
+    "moshpit_run_moshpit_rows": (C.c_int, [C.c_int, u32, u32, u32, P(C.c_void_p), u64, u64,
+                                           C.c_double, u64, u32, C.c_int, P(C.c_double),
+                                           vp, vp, vp, P(C.c_double)]),
     "moshpit_rng_draws": (C.c_int, [P(RngState), C.c_int, u64, dbl, u64, vp]),
     "moshpit_grid_validate": (C.c_int, [u32, u32, u32]),
     "moshpit_grid_capacity": (u64, [u32, u32]),
@@ -95,6 +100,9 @@ PROTOTYPES = {
     "moshpit_engine_set_timing": (C.c_int, [vp, C.c_int]),
     "moshpit_engine_kernel_time": (C.c_int, [vp, P(dbl), P(u64)]),
     "moshpit_engine_tables": (C.c_int, [vp, vp, vp, P(u32), vp, vp, vp]),
+    "moshpit_engine_set_reference": (C.c_int, [vp, C.c_int, vp, u64, u64, C.c_int, vp]),
+    "moshpit_engine_record": (C.c_int, [vp, C.c_int, vp, u64, u64, vp]),
+    "moshpit_engine_report": (C.c_int, [vp, P(dbl), vp, vp, u64, P(u64)]),
     "moshpit_shard_create": (C.c_int, [C.c_int, u32, u32, u64, dbl, u64, u64, i32, i32, i32,
                                        i32, P(vp)]),
     "moshpit_shard_destroy": (C.c_int, [vp]),

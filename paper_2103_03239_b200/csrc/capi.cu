@@ -72,6 +72,17 @@ struct moshpit_engine {
   Xoshiro fail, clock;
   double p = 0.0;
   int variant = MOSHPIT_KERNEL_AUTO;
+  // device-resident record_round (moshpit_engine_set_reference / _record)
+  int diag = MOSHPIT_DIAG_NONE;
+  std::uint64_t diag_dim = 0;
+  DeviceBuffer ref, mean, sq, part, part2, log;  // log: [0] initial, then (dist, drift) pairs
+  std::uint64_t log_cap = 0, log_n = 0;
+  std::unique_ptr<StreamHolder> aux;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~moshpit_engine() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
 };
 
 namespace {
@@ -113,6 +124,13 @@ int moshpit_rng_stream(std::uint64_t root, const char* name, std::int64_t index,
     const Xoshiro r = index < 0 ? Xoshiro::named(root, name)
                                 : Xoshiro::named(root, name, static_cast<std::uint64_t>(index));
     to_state(r, out);
+  });
+}
+
+int moshpit_rng_seeded(std::uint64_t seed, moshpit_rng_state* out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("rng_seeded: null argument");
+    to_state(Xoshiro(seed), out);
   });
 }
 
@@ -402,43 +420,65 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     // rounds and D2H overlap; results are identical to the resident path.
     const std::uint64_t W = stream_slab_cols(n, es, dim);
     if (dim > W) {
+      HostRows src;
+      src.base = initial;
+      src.pitch_bytes = dim * es;
       if (dtype == MOSHPIT_F32)
-        run_moshpit_streamed<float>(M, d, static_cast<const float*>(initial), n, dim, p_round,
-                                    seed, rounds, diag, initial_distortion, distortion,
-                                    mean_drift, active_counts, static_cast<float*>(final_out), W);
+        run_moshpit_streamed<float>(M, d, src, n, dim, p_round, seed, rounds, diag,
+                                    initial_distortion, distortion, mean_drift, active_counts,
+                                    static_cast<float*>(final_out), W);
       else
-        run_moshpit_streamed<double>(M, d, static_cast<const double*>(initial), n, dim, p_round,
-                                     seed, rounds, diag, initial_distortion, distortion,
-                                     mean_drift, active_counts, static_cast<double*>(final_out),
-                                     W);
+        run_moshpit_streamed<double>(M, d, src, n, dim, p_round, seed, rounds, diag,
+                                     initial_distortion, distortion, mean_drift, active_counts,
+                                     static_cast<double*>(final_out), W);
       *cost_units = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
                                                 static_cast<std::uint32_t>(dim));
       return;
     }
-    StreamHolder st;
+    StreamHolder st, aux;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    MB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    MB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    struct EvG {
+      cudaEvent_t a, b;
+      ~EvG() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+      }
+    } evg{ev_fork, ev_join};
     const std::uint64_t ld = padded_ld(dim, es);
     DeviceBuffer d_x(n * ld * es), d_ref(dim * 8 + 16), d_mean(dim * 8 + 16), d_sq(n * 8),
-        d_part(diag_partial_elems(n, dim) * 8 + 16), d_out((2 * rounds + 2) * 8);
+        d_part(diag_partial_elems(n, dim) * 8 + 16), d_part2(diag_partial_elems(n, dim) * 8 + 16),
+        d_out((2 * rounds + 2) * 8);
     MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, initial, dim * es, dim * es, n,
                               cudaMemcpyHostToDevice, st.s));
     const int exact = diag == MOSHPIT_DIAG_EXACT;
+    // record_round: the distortion (st) and colmean + drift (aux) only read
+    // the state, so they run side by side; the next round waits for both.
     auto record = [&](double* dist_slot, double* drift_slot) {
+      if (drift_slot) {
+        MB_CUDA(cudaEventRecord(ev_fork, st.s));
+        MB_CUDA(cudaStreamWaitEvent(aux.s, ev_fork, 0));
+      }
       if (dtype == MOSHPIT_F32) {
         launch_distortion<float>(d_x.as<float>(), n, ld, dim, d_ref.as<double>(),
                                  d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
         if (drift_slot)
           launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, nullptr,
-                                        d_mean.as<double>(), st.s);
+                                        d_mean.as<double>(), aux.s);
       } else {
         launch_distortion<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
                                   d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
         if (drift_slot)
           launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, nullptr,
-                                         d_mean.as<double>(), st.s);
+                                         d_mean.as<double>(), aux.s);
       }
-      if (drift_slot)
-        launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part.as<double>(),
-                     drift_slot, exact, st.s);
+      if (drift_slot) {
+        launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part2.as<double>(),
+                     drift_slot, exact, aux.s);
+        MB_CUDA(cudaEventRecord(ev_join, aux.s));
+        MB_CUDA(cudaStreamWaitEvent(st.s, ev_join, 0));
+      }
     };
     double* outp = d_out.as<double>();
     if (diag != MOSHPIT_DIAG_NONE) {
@@ -478,6 +518,60 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
       MB_CUDA(cudaMemcpy2DAsync(final_out, dim * es, d_x.ptr, ld * es, dim * es, n,
                                 cudaMemcpyDeviceToHost, st.s));
     MB_CUDA(cudaStreamSynchronize(st.s));
+    *cost_units = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
+                                              static_cast<std::uint32_t>(dim));
+  });
+}
+
+// run_moshpit over an array of row pointers (the drop-in's
+// std::vector<ParamVector>): large states are packed slab by slab from the
+// rows into a pinned ring by host threads (no flattened copy of the state);
+// small ones are flattened and take the resident path.
+int moshpit_run_moshpit_rows(int dtype, std::uint32_t M, std::uint32_t d, std::uint32_t T,
+                             const void* const* rows, std::uint64_t n, std::uint64_t dim,
+                             double p_round, std::uint64_t seed, std::uint32_t rounds, int diag,
+                             double* initial_distortion, double* distortion, double* mean_drift,
+                             std::uint32_t* active_counts, double* cost_units) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    if (M < 1 || d < 1 || T < 1)
+      throw std::invalid_argument("GridConfig: M, d, T must all be >= 1");
+    if (p_round < 0.0 || p_round > 1.0)
+      throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
+    if (n == 0) throw std::invalid_argument("run_moshpit: no peers");
+    if (!rows) throw std::invalid_argument("run_moshpit: null rows");
+    if (n > moshpit_grid_capacity(M, d))
+      throw std::invalid_argument("run_moshpit: N exceeds grid capacity M^d");
+    if (diag < MOSHPIT_DIAG_NONE || diag > MOSHPIT_DIAG_EXACT)
+      throw std::invalid_argument("run_moshpit: unknown diagnostics mode");
+    const std::uint64_t W = stream_slab_cols(n, es, dim);
+    if (dim <= W) {
+      std::vector<char> flat(n * dim * es + 16);
+      for (std::uint64_t i = 0; i < n; ++i)
+        if (dim) std::memcpy(flat.data() + i * dim * es, rows[i], dim * es);
+      const int rc = moshpit_run_moshpit(dtype, M, d, T, flat.data(), n, dim, p_round, seed,
+                                         rounds, diag, initial_distortion, distortion, mean_drift,
+                                         active_counts, cost_units, nullptr);
+      if (rc != MOSHPIT_OK) {
+        const std::string msg = g_last_error;
+        if (rc == MOSHPIT_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+        if (rc == MOSHPIT_ERR_OUT_OF_RANGE) throw std::out_of_range(msg);
+        if (rc == MOSHPIT_ERR_CUDA) throw CudaError(msg);
+        throw std::runtime_error(msg);
+      }
+      return;
+    }
+    require_device();
+    HostRows src;
+    src.rows = rows;
+    if (dtype == MOSHPIT_F32)
+      run_moshpit_streamed<float>(M, d, src, n, dim, p_round, seed, rounds, diag,
+                                  initial_distortion, distortion, mean_drift, active_counts,
+                                  nullptr, W);
+    else
+      run_moshpit_streamed<double>(M, d, src, n, dim, p_round, seed, rounds, diag,
+                                   initial_distortion, distortion, mean_drift, active_counts,
+                                   nullptr, W);
     *cost_units = moshpit_complexity_estimate(rounds, static_cast<std::uint32_t>(n), M,
                                               static_cast<std::uint32_t>(dim));
   });
@@ -578,8 +672,7 @@ int moshpit_engine_stats(moshpit_engine* e, std::uint64_t* rounds,
   return guarded([&] {
     if (!e) throw std::invalid_argument("null engine");
     DeviceGuard g(e->plane->device);
-    if (e->plane->last_stream) MB_CUDA(cudaStreamSynchronize(e->plane->last_stream));
-    else MB_CUDA(cudaDeviceSynchronize());
+    e->plane->sync_done();
     unsigned long long t[2];
     MB_CUDA(cudaMemcpy(t, e->plane->totals.ptr, 16, cudaMemcpyDeviceToHost));
     if (rounds) *rounds = e->plane->rounds_done;
@@ -620,8 +713,7 @@ int moshpit_engine_tables(moshpit_engine* e, std::uint32_t* members, std::uint32
     if (!e) throw std::invalid_argument("null engine");
     Plane& p = *e->plane;
     DeviceGuard g(p.device);
-    if (p.last_stream) MB_CUDA(cudaStreamSynchronize(p.last_stream));
-    else MB_CUDA(cudaDeviceSynchronize());
+    p.sync_done();
     std::uint32_t counts[4];
     MB_CUDA(cudaMemcpy(counts, p.counts.ptr, 16, cudaMemcpyDeviceToHost));
     if (n_groups) *n_groups = counts[0];
@@ -634,6 +726,134 @@ int moshpit_engine_tables(moshpit_engine* e, std::uint32_t* members, std::uint32
       std::vector<std::uint64_t> packed(p.n);
       MB_CUDA(cudaMemcpy(packed.data(), p.keys.ptr, p.n * 8, cudaMemcpyDeviceToHost));
       for (std::uint64_t i = 0; i < p.n; ++i) p.grid.unpack(packed[i], keys + i * p.grid.klen);
+    }
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// device-resident record_round for engine callers (protocols.hpp:68-84)
+// ---------------------------------------------------------------------------
+namespace {
+
+template <typename T>
+void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t dim,
+                 double* dist_slot, double* drift_slot, cudaStream_t s) {
+  const std::uint64_t n = e->plane->n;
+  const int exact = e->diag == MOSHPIT_DIAG_EXACT;
+  if (drift_slot) {
+    MB_CUDA(cudaEventRecord(e->ev_fork, s));
+    MB_CUDA(cudaStreamWaitEvent(e->aux->s, e->ev_fork, 0));
+  }
+  launch_distortion<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
+                       e->part.as<double>(), dist_slot, exact, s);
+  if (drift_slot) {
+    launch_colmean<T, double>(x, n, ld, dim, nullptr, e->mean.as<double>(), e->aux->s);
+    launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
+                 drift_slot, exact, e->aux->s);
+    MB_CUDA(cudaEventRecord(e->ev_join, e->aux->s));
+    MB_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int moshpit_engine_set_reference(moshpit_engine* e, int dtype, const void* state,
+                                 std::uint64_t dim, std::uint64_t ld, int diag, void* stream) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (diag < MOSHPIT_DIAG_NONE || diag > MOSHPIT_DIAG_EXACT)
+      throw std::invalid_argument("engine: unknown diagnostics mode");
+    check_state(dtype, state, dim, ld);
+    DeviceGuard g(e->plane->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    e->plane->order_after(s);
+    const std::uint64_t n = e->plane->n;
+    e->diag = diag;
+    e->diag_dim = dim;
+    e->log_n = 0;
+    if (diag == MOSHPIT_DIAG_NONE) return;
+    if (!e->aux) {
+      e->aux = std::make_unique<StreamHolder>();
+      MB_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+      MB_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+    }
+    e->ref.resize(dim * 8 + 16);
+    e->mean.resize(dim * 8 + 16);
+    e->sq.resize(n * 8 + 16);
+    e->part.resize(diag_partial_elems(n, dim) * 8 + 16);
+    e->part2.resize(diag_partial_elems(n, dim) * 8 + 16);
+    if (e->log_cap < 1024) {
+      e->log.resize((1 + 2 * 1024) * 8);
+      e->log_cap = 1024;
+    }
+    // reference = mean_of(initial) (protocols.hpp:119), then the initial distortion
+    if (dtype == MOSHPIT_F32) {
+      launch_colmean<float, double>(static_cast<const float*>(state), n, ld, dim, nullptr,
+                                    e->ref.as<double>(), s);
+      engine_diag<float>(e, static_cast<const float*>(state), ld, dim, e->log.as<double>(),
+                         nullptr, s);
+    } else {
+      launch_colmean<double, double>(static_cast<const double*>(state), n, ld, dim, nullptr,
+                                     e->ref.as<double>(), s);
+      engine_diag<double>(e, static_cast<const double*>(state), ld, dim, e->log.as<double>(),
+                          nullptr, s);
+    }
+    e->plane->mark_done(s);
+  });
+}
+
+int moshpit_engine_record(moshpit_engine* e, int dtype, const void* state, std::uint64_t dim,
+                          std::uint64_t ld, void* stream) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (e->diag == MOSHPIT_DIAG_NONE)
+      throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
+    if (dim != e->diag_dim) throw std::invalid_argument("engine_record: dim changed");
+    check_state(dtype, state, dim, ld);
+    DeviceGuard g(e->plane->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    e->plane->order_after(s);
+    if (e->log_n == e->log_cap) {  // grow the device log (rare: synchronises)
+      DeviceBuffer bigger((1 + 4 * e->log_cap) * 8);
+      MB_CUDA(cudaStreamSynchronize(s));
+      MB_CUDA(cudaMemcpy(bigger.ptr, e->log.ptr, (1 + 2 * e->log_cap) * 8,
+                         cudaMemcpyDeviceToDevice));
+      std::swap(e->log.ptr, bigger.ptr);
+      std::swap(e->log.bytes, bigger.bytes);
+      e->log_cap *= 2;
+    }
+    double* slot = e->log.as<double>() + 1 + 2 * e->log_n;
+    if (dtype == MOSHPIT_F32)
+      engine_diag<float>(e, static_cast<const float*>(state), ld, dim, slot, slot + 1, s);
+    else
+      engine_diag<double>(e, static_cast<const double*>(state), ld, dim, slot, slot + 1, s);
+    ++e->log_n;
+    e->plane->mark_done(s);
+  });
+}
+
+int moshpit_engine_report(moshpit_engine* e, double* initial_distortion, double* distortion,
+                          double* mean_drift, std::uint64_t cap, std::uint64_t* count) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    DeviceGuard g(e->plane->device);
+    e->plane->sync_done();
+    const std::uint64_t k = std::min<std::uint64_t>(cap, e->log_n);
+    if (count) *count = e->log_n;
+    if (e->diag == MOSHPIT_DIAG_NONE) {
+      if (initial_distortion) *initial_distortion = std::nan("");
+      return;
+    }
+    std::vector<double> h(1 + 2 * k);
+    MB_CUDA(cudaMemcpy(h.data(), e->log.ptr, h.size() * 8, cudaMemcpyDeviceToHost));
+    if (initial_distortion) *initial_distortion = h[0];
+    for (std::uint64_t t = 0; t < k; ++t) {
+      if (distortion) distortion[t] = h[1 + 2 * t];
+      if (mean_drift) mean_drift[t] = h[2 + 2 * t];
     }
   });
 }

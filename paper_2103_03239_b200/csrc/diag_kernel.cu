@@ -10,6 +10,7 @@
 // order (deterministic, ~1e-15 relative to the sequential sum).  Column means
 // use the reference pairwise tree over peers in both modes, in fp64.
 #include "common.cuh"
+#include "blocktree.cuh"
 #include "pairwise.cuh"
 
 namespace mb200 {
@@ -46,21 +47,130 @@ __global__ void colmean_kernel(const T* __restrict__ x, std::uint64_t n,
   out[j] = AccOps<Acc>::div(s, (Acc)n);
 }
 
-// EXACT: per peer, sequential over j exactly as core.hpp:118-122.
-template <typename T>
-__global__ void dist_rows_exact(const T* __restrict__ x, std::uint64_t n,
-                                std::uint64_t ld, std::uint64_t dim,
-                                const double* __restrict__ ref,
-                                double* __restrict__ sq) {
-  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const T* row = x + i * ld;
-  double acc = 0.0;
-  for (std::uint64_t j = 0; j < dim; ++j) {
-    const double diff = __dsub_rn((double)row[j], ref[j]);
-    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+// EXACT: per peer, sequential over j exactly as core.hpp:118-122.  The only
+// serial part of the reference order is the add chain of each peer; the
+// squared differences are independent.  A CTA owns P peers: warps 1..7 stage
+// (x_ij - ref_j)^2 for a tile of kExK columns of its P rows into shared memory
+// (coalesced row segments, computed with the reference's separate rounding),
+// while lanes 0..P-1 of warp 0 run the P add chains over the previous tile.
+// Cost ~ D x (DADD + LDS issue) per chain instead of D dependent global loads.
+constexpr int kExThreads = 256;
+constexpr int kExProducers = kExThreads - 32;
+constexpr int kExK = 512;
+
+template <int P>
+constexpr std::size_t exact_smem() {
+  return 2ull * P * (kExK + 1) * sizeof(double);
+}
+
+// acc[i] (in/out when `accumulate`, else written): the running j-sum of peer i.
+template <typename T, int P>
+__global__ void __launch_bounds__(kExThreads)
+    dist_exact_tiled(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                     std::uint64_t dim, const double* __restrict__ ref,
+                     double* __restrict__ acc, int accumulate) {
+  extern __shared__ double sm_ex[];
+  const std::uint64_t p0 = (std::uint64_t)blockIdx.x * P;
+  const int tid = threadIdx.x;
+  double a = 0.0;
+  if (tid < P && p0 + tid < n && accumulate) a = acc[p0 + tid];
+  const std::uint64_t ntiles = (dim + kExK - 1) / kExK;
+  auto produce = [&](std::uint64_t t, int buf) {
+    const std::uint64_t j0 = t * kExK;
+#pragma unroll 4
+    for (int e = tid - 32; e < P * kExK; e += kExProducers) {
+      const int q = e / kExK, k = e % kExK;
+      const std::uint64_t j = j0 + k, i = p0 + q;
+      double v = 0.0;  // padding adds +0.0 to a sum of squares: bit-neutral
+      if (j < dim && i < n) {
+        const double diff = __dsub_rn((double)x[i * ld + j], ref[j]);
+        v = __dmul_rn(diff, diff);
+      }
+      sm_ex[(buf * P + q) * (kExK + 1) + k] = v;
+    }
+  };
+  if (tid >= 32 && ntiles) produce(0, 0);
+  __syncthreads();
+  for (std::uint64_t t = 0; t < ntiles; ++t) {
+    const int buf = (int)(t & 1);
+    if (tid >= 32) {
+      if (t + 1 < ntiles) produce(t + 1, buf ^ 1);
+    } else if (tid < P) {
+      const double* row = sm_ex + (buf * P + tid) * (kExK + 1);
+#pragma unroll 16
+      for (int k = 0; k < kExK; ++k) a = __dadd_rn(a, row[k]);
+    }
+    __syncthreads();
   }
-  sq[i] = acc;
+  if (tid < P && p0 + tid < n) acc[p0 + tid] = a;
+}
+
+template <typename T>
+void launch_dist_exact(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                       const double* ref, double* acc, int accumulate, cudaStream_t s) {
+  // peers per CTA: enough CTAs to spread the chains over the SMs
+  const int P = n >= 2048 ? 8 : n >= 1024 ? 4 : n >= 512 ? 2 : 1;
+  const unsigned blocks = (unsigned)((n + P - 1) / P);
+  switch (P) {
+#define MB_EXL(PP)                                                                      case PP: {                                                                              static bool attr = false;                                                             if (!attr) {                                                                            MB_CUDA(cudaFuncSetAttribute(dist_exact_tiled<T, PP>,                                                              cudaFuncAttributeMaxDynamicSharedMemorySize,                                          (int)exact_smem<PP>()));                                 attr = true;                                                                        }                                                                                     dist_exact_tiled<T, PP><<<blocks, kExThreads, exact_smem<PP>(), s>>>(x, n, ld, dim,                                                                          ref, acc,                                                                             accumulate);     break;                                                                              }
+    MB_EXL(1) MB_EXL(2) MB_EXL(4) MB_EXL(8)
+#undef MB_EXL
+  }
+  MB_LAUNCH_CHECK();
+}
+
+// drift, EXACT (protocols.hpp:75-81 in order): the two j-chains
+// (mean_j - ref_j)^2 and ref_j^2 on lanes 0 and 1 of warp 0, the squares
+// staged by warps 1..7.  acc2[0..1] running sums (in/out when `accumulate`).
+__global__ void __launch_bounds__(kExThreads)
+    drift_exact_tiled(const double* __restrict__ mean, const double* __restrict__ ref,
+                      std::uint64_t dim, double* __restrict__ acc2, int accumulate) {
+  extern __shared__ double sm_ex[];
+  const int tid = threadIdx.x;
+  double a = 0.0;
+  if (tid < 2 && accumulate) a = acc2[tid];
+  const std::uint64_t ntiles = (dim + kExK - 1) / kExK;
+  auto produce = [&](std::uint64_t t, int buf) {
+    const std::uint64_t j0 = t * kExK;
+#pragma unroll 4
+    for (int k = tid - 32; k < kExK; k += kExProducers) {
+      const std::uint64_t j = j0 + k;
+      double u = 0.0, v = 0.0;
+      if (j < dim) {
+        const double dm = __dsub_rn(mean[j], ref[j]);
+        u = __dmul_rn(dm, dm);
+        v = __dmul_rn(ref[j], ref[j]);
+      }
+      sm_ex[(buf * 2 + 0) * (kExK + 1) + k] = u;
+      sm_ex[(buf * 2 + 1) * (kExK + 1) + k] = v;
+    }
+  };
+  if (tid >= 32 && ntiles) produce(0, 0);
+  __syncthreads();
+  for (std::uint64_t t = 0; t < ntiles; ++t) {
+    const int buf = (int)(t & 1);
+    if (tid >= 32) {
+      if (t + 1 < ntiles) produce(t + 1, buf ^ 1);
+    } else if (tid < 2) {
+      const double* row = sm_ex + (buf * 2 + tid) * (kExK + 1);
+#pragma unroll 16
+      for (int k = 0; k < kExK; ++k) a = __dadd_rn(a, row[k]);
+    }
+    __syncthreads();
+  }
+  if (tid < 2) acc2[tid] = a;
+}
+
+void launch_drift_exact(const double* mean, const double* ref, std::uint64_t dim, double* acc2,
+                        int accumulate, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    MB_CUDA(cudaFuncSetAttribute(drift_exact_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)exact_smem<2>()));
+    attr = true;
+  }
+  drift_exact_tiled<<<1, kExThreads, exact_smem<2>(), s>>>(mean, ref, dim, acc2, accumulate);
+  MB_LAUNCH_CHECK();
 }
 
 constexpr int kRedThreads = 256;
@@ -105,33 +215,28 @@ __global__ void fold_rows(const double* __restrict__ partial, std::uint64_t n,
   sq[i] = acc;
 }
 
-// pairwise over peers, / n  (core.hpp:125)
-__global__ void finish_distortion(const double* __restrict__ sq, std::uint64_t n,
-                                  double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// pairwise over peers, / n  (core.hpp:125): the reference tree evaluated by
+// one CTA (blocktree.cuh, bit-identical to the sequential evaluation) for
+// n <= 8192, one thread above that.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads)
+    finish_distortion(const double* __restrict__ sq, std::uint64_t n, double* __restrict__ out) {
+  __shared__ double lvl[2 * kBlockTreeMaxNodes];
   if (n == 0) {
-    *out = 0.0;
+    if (threadIdx.x == 0) *out = 0.0;
     return;
   }
+  if (n <= 8192) {
+    auto ld_fn = [&](std::uint32_t i) { return sq[i]; };
+    const double s = pairwise_block(ld_fn, (std::uint32_t)n, lvl);
+    if (threadIdx.x == 0) *out = __ddiv_rn(s, (double)n);
+    return;
+  }
+  if (threadIdx.x != 0) return;
   auto ld_fn = [&](std::uint32_t i) { return sq[i]; };
   const double s = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
                                        [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
   *out = __ddiv_rn(s, (double)n);
-}
-
-// drift, EXACT: protocols.hpp:75-81 in order.
-__global__ void drift_exact(const double* __restrict__ mean,
-                            const double* __restrict__ ref, std::uint64_t dim,
-                            double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double drift_sq = 0.0, ref_sq = 0.0;
-  for (std::uint64_t j = 0; j < dim; ++j) {
-    const double dm = __dsub_rn(mean[j], ref[j]);
-    drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
-    ref_sq = __dadd_rn(ref_sq, __dmul_rn(ref[j], ref[j]));
-  }
-  const double den = fmax(__dsqrt_rn(ref_sq), 1e-300);
-  *out = __ddiv_rn(__dsqrt_rn(drift_sq), den);
 }
 
 __global__ void drift_fast_partial(const double* __restrict__ mean,
@@ -196,21 +301,6 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
 
 // ---- slab-streamed variants: the j-sums continue across D-slabs --------
 template <typename T>
-__global__ void dist_rows_exact_acc(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
-                                    std::uint64_t dim, const double* __restrict__ ref,
-                                    double* __restrict__ acc) {
-  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const T* row = x + i * ld;
-  double a = acc[i];
-  for (std::uint64_t j = 0; j < dim; ++j) {
-    const double diff = __dsub_rn((double)row[j], ref[j]);
-    a = __dadd_rn(a, __dmul_rn(diff, diff));
-  }
-  acc[i] = a;
-}
-
-template <typename T>
 __global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
                                    const double* __restrict__ ref, std::uint64_t nch_total,
                                    std::uint64_t c0, double* __restrict__ partial) {
@@ -224,28 +314,6 @@ __global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, st
   }
   const double s = block_sum_fixed(acc);
   if (threadIdx.x == 0) partial[i * nch_total + c0 + c] = s;
-}
-
-__global__ void finish_distortion_from_acc(const double* __restrict__ acc, std::uint64_t n,
-                                           double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  auto ld_fn = [&](std::uint32_t i) { return acc[i]; };
-  const double s = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
-                                       [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
-  *out = __ddiv_rn(s, (double)n);
-}
-
-__global__ void drift_exact_acc(const double* __restrict__ mean, const double* __restrict__ ref,
-                                std::uint64_t dim, double* __restrict__ acc2) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double drift_sq = acc2[0], ref_sq = acc2[1];
-  for (std::uint64_t j = 0; j < dim; ++j) {
-    const double dm = __dsub_rn(mean[j], ref[j]);
-    drift_sq = __dadd_rn(drift_sq, __dmul_rn(dm, dm));
-    ref_sq = __dadd_rn(ref_sq, __dmul_rn(ref[j], ref[j]));
-  }
-  acc2[0] = drift_sq;
-  acc2[1] = ref_sq;
 }
 
 __global__ void drift_fast_partial_off(const double* __restrict__ mean,
@@ -288,7 +356,8 @@ void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
                       std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s) {
   if (n == 0 || dim == 0) return;
   if (exact) {
-    dist_rows_exact_acc<T><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, n, ld, dim, ref, acc);
+    launch_dist_exact<T>(x, n, ld, dim, ref, acc, 1, s);
+    return;
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
@@ -301,7 +370,8 @@ void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim,
                        double* acc2, double* partial, std::uint64_t c0, cudaStream_t s) {
   if (dim == 0) return;
   if (exact) {
-    drift_exact_acc<<<1, 1, 0, s>>>(mean, ref, dim, acc2);
+    launch_drift_exact(mean, ref, dim, acc2, 1, s);
+    return;
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     drift_fast_partial_off<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, c0, partial);
@@ -317,7 +387,7 @@ void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, dou
     fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(row_partial, n, nch_total, acc);
     MB_LAUNCH_CHECK();
   }
-  finish_distortion_from_acc<<<1, 1, 0, s>>>(acc, n, dist_out);
+  finish_distortion<<<1, kFinThreads, 0, s>>>(acc, n, dist_out);
   MB_LAUNCH_CHECK();
   if (drift_out) {
     if (exact)
@@ -357,12 +427,12 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq,
                        double* partial, double* out, int exact, cudaStream_t s) {
   if (n == 0) {
-    finish_distortion<<<1, 1, 0, s>>>(sq, 0, out);
+    finish_distortion<<<1, kFinThreads, 0, s>>>(sq, 0, out);
     MB_LAUNCH_CHECK();
     return;
   }
   if (exact || dim == 0) {
-    dist_rows_exact<T><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, n, ld, dim, ref, sq);
+    launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
@@ -371,14 +441,15 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
     fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
   }
   MB_LAUNCH_CHECK();
-  finish_distortion<<<1, 1, 0, s>>>(sq, n, out);
+  finish_distortion<<<1, kFinThreads, 0, s>>>(sq, n, out);
   MB_LAUNCH_CHECK();
 }
 
 void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
                   double* partial, double* out, int exact, cudaStream_t s) {
   if (exact || dim == 0) {
-    drift_exact<<<1, 1, 0, s>>>(mean, ref, dim, out);
+    launch_drift_exact(mean, ref, dim, partial, 0, s);  // partial[0..1] = the two j-sums
+    drift_finish_acc<<<1, 1, 0, s>>>(partial, out);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     drift_fast_partial<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, partial);

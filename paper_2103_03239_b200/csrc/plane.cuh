@@ -114,7 +114,12 @@ struct Plane {
   int slot = 0;
   std::uint32_t last_active = 0;
   std::uint64_t rounds_done = 0;
+  // Cross-stream ordering: the tables above are reused every round, so a
+  // round issued on a different stream than the last one first waits for the
+  // last round's end (`done`, recorded by mark_done at the end of a round).
   cudaStream_t last_stream = nullptr;
+  cudaEvent_t done = nullptr;
+  bool have_done = false;
   // optional CUDA-event bracketing of kernel 2 on its launch stream
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -148,10 +153,12 @@ struct Plane {
       stage[i].resize(n * 9 + 16);
       MB_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     }
+    MB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
   }
   ~Plane() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (done) cudaEventDestroy(done);
     for (auto& pr : tev) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
@@ -171,12 +178,30 @@ struct Plane {
   // cells -> initial keys (matchmaking.hpp:46-59), on the device.
   void init_cells(Xoshiro& cell_stream, cudaStream_t s) {
     const auto cells = draw_cells(cell_stream, grid.capacity, n);
+    order_after(s);
     const int k = next_slot();
     std::memcpy(stage[k].ptr, cells.data(), n * 8);
     MB_CUDA(cudaMemcpyAsync(cellbuf.ptr, stage[k].ptr, n * 8, cudaMemcpyHostToDevice, s));
     MB_CUDA(cudaEventRecord(ev[k], s));
     launch_initial_keys(cellbuf.as<std::uint64_t>(), keys.as<std::uint64_t>(), n,
                         grid.M, grid.d, s);
+    mark_done(s);
+  }
+
+  // Work on `s` that touches the plane's tables starts after the last round.
+  void order_after(cudaStream_t s) {
+    if (have_done && s != last_stream) MB_CUDA(cudaStreamWaitEvent(s, done, 0));
+  }
+  // End of a round (or of any work using the tables) on `s`.
+  void mark_done(cudaStream_t s) {
+    MB_CUDA(cudaEventRecord(done, s));
+    have_done = true;
+    last_stream = s;
+  }
+  // Host wait for the last round (stats / table reads).
+  void sync_done() {
+    if (have_done) MB_CUDA(cudaEventSynchronize(done));
+    else MB_CUDA(cudaDeviceSynchronize());
   }
 
   int next_slot() {
@@ -193,6 +218,7 @@ struct Plane {
                       cudaStream_t s, int variant,
                       const StepPrologue<float>* step_f = nullptr,
                       const StepPrologue<double>* step_d = nullptr) {
+    order_after(s);
     const int k = next_slot();
     auto* ts = stage[k].as<std::uint64_t>();
     auto* failed = reinterpret_cast<std::uint8_t*>(ts + n);
@@ -243,16 +269,23 @@ struct Plane {
     }
     last_active = active;
     ++rounds_done;
-    last_stream = s;
+    mark_done(s);
     return active;
   }
 };
 
 
-// Slab-pipelined run_moshpit over host buffers (stream_run.cu).
+// Slab-pipelined run_moshpit over host buffers (stream_run.cu).  The initial
+// state is either one buffer (row i at base + i * pitch_bytes) or an array of
+// row pointers (the drop-in's std::vector<ParamVector>, no flattening).
+struct HostRows {
+  const void* base = nullptr;
+  std::uint64_t pitch_bytes = 0;
+  const void* const* rows = nullptr;
+};
 std::uint64_t stream_slab_cols(std::uint64_t n, std::size_t es, std::uint64_t dim);
 template <typename T>
-void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, std::uint64_t n,
+void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src, std::uint64_t n,
                           std::uint64_t dim, double p, std::uint64_t seed, std::uint32_t rounds,
                           int diag, double* init_dist, double* dist, double* drift,
                           std::uint32_t* active, T* final_out, std::uint64_t W);

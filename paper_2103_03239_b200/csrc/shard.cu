@@ -501,6 +501,7 @@ struct Shard {
   std::uint32_t world = 1, me = 0, Mg = 1, M = 1, d = 1;
   int device = 0;
   bool emulate = false;
+  bool connected = false;  // real mode: peers' pools/flags mapped (open_peers)
   std::uint32_t round_no = 0;
   unsigned long long epoch = 0;
   // replicated bookkeeping
@@ -867,6 +868,7 @@ struct Shard {
       if (timing) MB_CUDA(cudaEventRecord(tb.second, s));
       barrier(s);  // peers finished pulling from our rows before we touch them again
     }
+    plane->mark_done(s);  // the next round (any stream) starts after this one
     if (crossed) *crossed = a.cross;
     return active;
   }
@@ -1016,11 +1018,13 @@ int moshpit_shard_open_peers(moshpit_shard* h, const void* all) {
     MB_CUDA(cudaMemcpy(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice));
     MB_CUDA(cudaMemcpy(S.flag_tab.ptr, S.peer_flags, sizeof(S.peer_flags),
                        cudaMemcpyHostToDevice));
+    S.connected = true;
   });
 }
 
 int moshpit_shard_fill_synthetic(moshpit_shard* h, std::uint64_t seed, void* stream) {
   return guarded([&] {
+    if (!h || !h->s) throw std::invalid_argument("shard: null handle");
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     auto s = static_cast<cudaStream_t>(stream);
@@ -1043,7 +1047,12 @@ int moshpit_shard_fill_synthetic(moshpit_shard* h, std::uint64_t seed, void* str
 int moshpit_shard_round(moshpit_shard* h, void* stream, std::uint32_t* active_out,
                         std::int32_t* crossed_out) {
   return guarded([&] {
+    if (!h || !h->s) throw std::invalid_argument("shard: null handle");
     Shard& S = *h->s;
+    // without the peers' IPC mappings the cross round would dereference null
+    // device pointers (a sticky CUDA fault); refuse instead
+    if (S.world > 1 && !S.emulate && !S.connected)
+      throw std::invalid_argument("shard: open_peers not called");
     DeviceGuard g(S.device);
     int crossed = 0;
     const std::uint32_t a = S.round(static_cast<cudaStream_t>(stream), &crossed);
@@ -1060,7 +1069,7 @@ int moshpit_shard_read(moshpit_shard* h, void* out, std::uint8_t* mask) {
     DeviceGuard g(S.device);
     StreamHolder st;
     const std::uint64_t n = S.plane->n;
-    if (S.plane->last_stream) MB_CUDA(cudaStreamSynchronize(S.plane->last_stream));
+    S.plane->sync_done();
     MB_CUDA(cudaDeviceSynchronize());
     DeviceBuffer buf(n * S.dim * S.es + 16), m(n + 16), acc(n + 16);
     MB_CUDA(cudaMemsetAsync(acc.ptr, 0, n, st.s));

@@ -12,8 +12,12 @@
 // end-to-end time approaches max(H2D, D2H, compute) instead of their sum, and
 // the device footprint is three slabs instead of the whole state.
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
+#include <functional>
 #include <memory>
+#include <mutex>
+#include <thread>
 
 #include "plane.cuh"
 
@@ -32,6 +36,74 @@ std::uint64_t stream_slab_cols(std::uint64_t n, std::size_t es, std::uint64_t di
 
 namespace {
 
+// A small persistent pool of host threads for packing pageable caller memory
+// into the pinned staging ring (one memcpy per row segment, rows split across
+// the threads).  run(f) calls f(t, T) on all T threads and waits.
+class HostPool {
+ public:
+  explicit HostPool(unsigned n) {
+    for (unsigned t = 1; t < n; ++t) th_.emplace_back([this, t] { loop(t); });
+    n_ = n;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  unsigned size() const { return n_; }
+  void run(const std::function<void(unsigned, unsigned)>& f) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0, n_);
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(unsigned t) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(unsigned, unsigned)>* f;
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        f = job_;
+      }
+      (*f)(t, n_);
+      std::lock_guard<std::mutex> g(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(unsigned, unsigned)>* job_ = nullptr;
+  unsigned n_ = 1, pending_ = 0;
+  std::uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
 // Grow-only per-thread workspace: repeated host-buffer calls (the harness
 // runs many trials per thread) reuse the slab ring, tables, diagnostics
 // buffers, streams and -- for the same (M, d, n) -- the integer plane, instead
@@ -43,7 +115,15 @@ struct StreamWorkspace {
   std::unique_ptr<Plane> plane;
   std::uint32_t pM = 0, pd = 0;
   std::uint64_t pn = 0;
-  std::unique_ptr<StreamHolder> s_in, s_cmp, s_out;
+  std::unique_ptr<StreamHolder> s_in, s_cmp, s_out, s_aux;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // pageable callers: pinned staging rings (in, out) and the packing threads
+  PinnedBuffer hin[3], hout[3];
+  std::unique_ptr<HostPool> pool;
+  ~StreamWorkspace() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
 };
 thread_local std::unique_ptr<StreamWorkspace> tl_ws;
 
@@ -55,6 +135,9 @@ StreamWorkspace& workspace(int dev) {
     tl_ws->s_in = std::make_unique<StreamHolder>();
     tl_ws->s_cmp = std::make_unique<StreamHolder>();
     tl_ws->s_out = std::make_unique<StreamHolder>();
+    tl_ws->s_aux = std::make_unique<StreamHolder>();
+    MB_CUDA(cudaEventCreateWithFlags(&tl_ws->ev_fork, cudaEventDisableTiming));
+    MB_CUDA(cudaEventCreateWithFlags(&tl_ws->ev_join, cudaEventDisableTiming));
   }
   return *tl_ws;
 }
@@ -62,7 +145,7 @@ StreamWorkspace& workspace(int dev) {
 }  // namespace
 
 template <typename T>
-void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, std::uint64_t n,
+void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src, std::uint64_t n,
                           std::uint64_t dim, double p, std::uint64_t seed, std::uint32_t rounds,
                           int diag, double* init_dist, double* dist, double* drift,
                           std::uint32_t* active, T* final_out, std::uint64_t W) {
@@ -70,6 +153,20 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
   StreamWorkspace& ws = workspace(dev);
+  // Pageable (or row-pointer) sources are packed by host threads into a
+  // pinned ring and copied with one contiguous async copy per slab; pinned
+  // contiguous sources are copied directly (2-D copy).
+  const bool stage_in = src.rows || !is_pinned(src.base);
+  const bool stage_out = final_out && !is_pinned(final_out);
+  if ((stage_in || stage_out) && !ws.pool) {
+    unsigned hc = std::thread::hardware_concurrency();
+    if (const char* e = std::getenv("MOSHPIT_HOST_THREADS")) hc = (unsigned)std::atoi(e);
+    ws.pool = std::make_unique<HostPool>(std::max(1u, std::min(hc ? hc : 1u, 32u)));
+  }
+  auto row_ptr = [&](std::uint64_t i) -> const char* {
+    return src.rows ? static_cast<const char*>(src.rows[i])
+                    : static_cast<const char*>(src.base) + i * src.pitch_bytes;
+  };
   StreamHolder &s_in = *ws.s_in, &s_cmp = *ws.s_cmp, &s_out = *ws.s_out;
   const std::uint64_t R = rounds;
   // 1. the integer plane of every round (identical for all slabs)
@@ -138,13 +235,44 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
         for (int k = 0; k < kRing; ++k) cudaEventDestroy(a[k]);
     }
   } guard{{ev_in, ev_cmp, ev_out}};
+  if (stage_in)
+    for (int k = 0; k < kRing; ++k) ws.hin[k].resize(n * W * es + 16);
+  if (stage_out)
+    for (int k = 0; k < kRing; ++k) ws.hout[k].resize(n * W * es + 16);
+  bool in_used[kRing] = {}, out_pending[kRing] = {};
+  std::uint64_t out_j0[kRing] = {}, out_w[kRing] = {};
+  // copy a finished slab from the pinned out-ring into the caller's rows
+  auto unpack = [&](int b) {
+    MB_CUDA(cudaEventSynchronize(ev_out[b]));
+    const char* h = ws.hout[b].as<char>();
+    const std::uint64_t j0 = out_j0[b], w = out_w[b];
+    ws.pool->run([&](unsigned t, unsigned T_) {
+      for (std::uint64_t i = n * t / T_; i < n * (t + 1) / T_; ++i)
+        std::memcpy(reinterpret_cast<char*>(final_out) + (i * dim + j0) * es, h + i * W * es,
+                    w * es);
+    });
+    out_pending[b] = false;
+  };
   for (std::uint64_t sl = 0; sl < nslab; ++sl) {
     const int b = (int)(sl % kRing);
     const std::uint64_t j0 = sl * W, w = (dim - j0) < W ? (dim - j0) : W;
     T* x = buf[b]->as<T>();
     if (sl >= (std::uint64_t)kRing) MB_CUDA(cudaStreamWaitEvent(s_in.s, ev_out[b], 0));
-    MB_CUDA(cudaMemcpy2DAsync(x, W * es, initial + j0, dim * es, w * es, n,
-                              cudaMemcpyHostToDevice, s_in.s));
+    if (stage_in) {
+      // the previous H2D out of this pinned slot must be done before refilling it
+      if (in_used[b]) MB_CUDA(cudaEventSynchronize(ev_in[b]));
+      char* h = ws.hin[b].as<char>();
+      ws.pool->run([&](unsigned t, unsigned T_) {
+        for (std::uint64_t i = n * t / T_; i < n * (t + 1) / T_; ++i)
+          std::memcpy(h + i * W * es, row_ptr(i) + j0 * es, w * es);
+      });
+      MB_CUDA(cudaMemcpy2DAsync(x, W * es, h, W * es, w * es, n, cudaMemcpyHostToDevice,
+                                s_in.s));
+      in_used[b] = true;
+    } else {
+      MB_CUDA(cudaMemcpy2DAsync(x, W * es, row_ptr(0) + j0 * es, src.pitch_bytes, w * es, n,
+                                cudaMemcpyHostToDevice, s_in.s));
+    }
     MB_CUDA(cudaEventRecord(ev_in[b], s_in.s));
     MB_CUDA(cudaStreamWaitEvent(s_cmp.s, ev_in[b], 0));
     const std::uint64_t c0 = j0 / chunk;
@@ -160,20 +288,44 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
                            t_act.as<std::uint32_t>() + r * n, t_cnt.as<std::uint32_t>() + r * 4,
                            M, MOSHPIT_KERNEL_AUTO, s_cmp.s);
       if (dg) {
+        // the distortion j-chains (s_cmp) and colmean + drift (s_aux) only
+        // read the slab: run them side by side, join before the next round
+        MB_CUDA(cudaEventRecord(ws.ev_fork, s_cmp.s));
+        MB_CUDA(cudaStreamWaitEvent(ws.s_aux->s, ws.ev_fork, 0));
         launch_dist_slab<T>(x, n, W, w, refj, exact, acc.as<double>() + (r + 1) * n,
                             rpart.as<double>() + (r + 1) * n * nch, nch, c0, s_cmp.s);
-        launch_colmean<T, double>(x, n, W, w, nullptr, mean_s.as<double>(), s_cmp.s);
+        launch_colmean<T, double>(x, n, W, w, nullptr, mean_s.as<double>(), ws.s_aux->s);
         launch_drift_slab(mean_s.as<double>(), refj, w, exact, acc2.as<double>() + 2 * (r + 1),
-                          dpart.as<double>() + (r + 1) * 2 * nch, c0, s_cmp.s);
+                          dpart.as<double>() + (r + 1) * 2 * nch, c0, ws.s_aux->s);
+        MB_CUDA(cudaEventRecord(ws.ev_join, ws.s_aux->s));
+        MB_CUDA(cudaStreamWaitEvent(s_cmp.s, ws.ev_join, 0));
       }
     }
     MB_CUDA(cudaEventRecord(ev_cmp[b], s_cmp.s));
     MB_CUDA(cudaStreamWaitEvent(s_out.s, ev_cmp[b], 0));
-    if (final_out)
+    if (stage_out) {
+      if (out_pending[b]) unpack(b);  // slot reused: drain slab sl - kRing first
+      MB_CUDA(cudaMemcpy2DAsync(ws.hout[b].ptr, W * es, x, W * es, w * es, n,
+                                cudaMemcpyDeviceToHost, s_out.s));
+      out_pending[b] = true;
+      out_j0[b] = j0;
+      out_w[b] = w;
+    } else if (final_out) {
       MB_CUDA(cudaMemcpy2DAsync(final_out + j0, dim * es, x, W * es, w * es, n,
                                 cudaMemcpyDeviceToHost, s_out.s));
+    }
     MB_CUDA(cudaEventRecord(ev_out[b], s_out.s));
+    // drain the oldest finished slab while the GPU works on the newer ones
+    if (stage_out && sl >= 1) {
+      const int pb = (int)((sl - 1) % kRing);
+      if (out_pending[pb]) unpack(pb);
+    }
   }
+  if (stage_out)
+    for (std::uint64_t k = 0; k < (std::uint64_t)kRing; ++k) {
+      const int b = (int)((nslab + k) % kRing);
+      if (out_pending[b]) unpack(b);
+    }
   if (dg) {
     double* o = out.as<double>();
     for (std::uint64_t r = 0; r <= R; ++r)
@@ -200,13 +352,26 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const T* initial, st
   MB_CUDA(cudaStreamSynchronize(s_in.s));
 }
 
-template void run_moshpit_streamed<float>(std::uint32_t, std::uint32_t, const float*,
+// Frees the calling thread's workspace (slab ring, tables, plane, streams).
+void release_stream_workspace() {
+  if (!tl_ws) return;
+  DeviceGuard g(tl_ws->dev);
+  for (auto* h : {tl_ws->s_in.get(), tl_ws->s_cmp.get(), tl_ws->s_out.get(), tl_ws->s_aux.get()})
+    if (h) MB_CUDA(cudaStreamSynchronize(h->s));
+  tl_ws.reset();
+}
+
+template void run_moshpit_streamed<float>(std::uint32_t, std::uint32_t, const HostRows&,
                                           std::uint64_t, std::uint64_t, double, std::uint64_t,
                                           std::uint32_t, int, double*, double*, double*,
                                           std::uint32_t*, float*, std::uint64_t);
-template void run_moshpit_streamed<double>(std::uint32_t, std::uint32_t, const double*,
+template void run_moshpit_streamed<double>(std::uint32_t, std::uint32_t, const HostRows&,
                                            std::uint64_t, std::uint64_t, double, std::uint64_t,
                                            std::uint32_t, int, double*, double*, double*,
                                            std::uint32_t*, double*, std::uint64_t);
 
 }  // namespace mb200
+
+extern "C" int moshpit_release_workspace(void) {
+  return mb200::guarded([] { mb200::release_stream_workspace(); });
+}

@@ -52,3 +52,16 @@ def test_gpu_arm_fails_loudly_without_device():
                {"RANK": "0", "WORLD_SIZE": "1"})
     assert r.returncode != 0
     assert r.stdout.strip() == ""
+
+
+def test_both_arms_print_the_same_config(ref):
+    """The driver compares the arms' `config` dicts: both come from
+    bench.workload_config with no arm-specific keys."""
+    sys.path.insert(0, ROOT)
+    import bench
+    r = _bench(["--impl", "reference", "--steps", "1", "--warmup", "3"],
+               {"RANK": "0", "WORLD_SIZE": "1"})
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["config"] == bench.workload_config("C2")
+    assert "parallelism" not in d["config"] and "kernel" not in d["config"]

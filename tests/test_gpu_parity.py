@@ -435,3 +435,85 @@ def test_concurrent_callers_are_independent(mb, oracle):
         par = list(ex.map(run, cases))
     for (va, da), (vb, db) in zip(seq, par):
         assert bits_equal(va, vb) and bits_equal(da, db)
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_run_moshpit_rows_equals_contiguous(mb, oracle, monkeypatch, f64):
+    """moshpit_run_moshpit_rows (the drop-in's row-pointer entry: host threads
+    pack the caller's rows into a pinned ring, no flattened copy) gives the
+    same TrialReport bits as the contiguous call, streamed and resident."""
+    import ctypes as C
+    from paper_2103_03239_b200 import _capi
+    n, dim, R = 256, 200_003, 4
+    dt = np.float64 if f64 else np.float32
+    x = oracle.init_state(INIT_SEED, n, dim, dtype=dt)
+    rows = [np.array(x[i]) for i in range(n)]  # separate pageable allocations
+    ptrs = (C.c_void_p * n)(*[r.ctypes.data for r in rows])
+    grid, fm = mb.GridConfig(16, 2, 1), mb.FailureModel(0.05)
+    for slab in ("1", str(1 << 40)):  # 4 streamed slabs, then resident
+        monkeypatch.setenv("MOSHPIT_SLAB_BYTES", slab)
+        want = mb.run_moshpit(grid, x, fm, mb.Rng(7), R, diagnostics="exact")
+        dist, drift = np.zeros(R), np.zeros(R)
+        act = np.zeros(R, dtype=np.uint32)
+        init_d, cost = C.c_double(0), C.c_double(0)
+        _capi.check(_capi.lib().moshpit_run_moshpit_rows(
+            _capi.F64 if f64 else _capi.F32, 16, 2, 1, ptrs, n, dim, 0.05, 7, R, _capi.DIAG_EXACT,
+            C.byref(init_d), dist.ctypes.data_as(C.c_void_p), drift.ctypes.data_as(C.c_void_p),
+            act.ctypes.data_as(C.c_void_p), C.byref(cost)))
+        assert bits_equal(dist, np.array(want.distortion))
+        assert bits_equal(drift, np.array(want.mean_drift))
+        assert bits_equal(np.array([init_d.value]), np.array([want.initial_distortion]))
+        assert list(act) == want.active_counts
+        assert cost.value == want.cost_units
+
+
+def test_engine_alternating_streams(mb, oracle, torch):
+    """Engine.round on a different stream each call: the engine orders each
+    round after the previous one (event + stream wait), so the result equals
+    the single-stream run bit for bit (cross-stream table reuse)."""
+    M, d, n, p, R, dim = 32, 2, 1024, 0.05, 6, 1 << 16
+    x0 = torch.empty((n, dim), dtype=torch.float32, device="cuda")
+    mb.fill_synthetic(x0, INIT_SEED)
+    a = x0.clone()
+    eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+    for _ in range(R):
+        eng.round(a)
+    torch.cuda.synchronize()
+    eng.close()
+    b = x0.clone()
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+    for r in range(R):
+        # no caller-side ordering at all: round r+1 on another stream must
+        # still start after round r (its tables and its state writes)
+        eng.round(b, stream=streams[r % 3])
+    torch.cuda.synchronize()
+    rounds, _ = eng.stats()
+    eng.close()
+    assert rounds == R
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("f64,diag", [(False, "fast"), (True, "exact"), (False, "exact")])
+def test_engine_device_report_equals_run_moshpit(mb, torch, f64, diag):
+    """Engine.set_reference / record / report (record_round on the device,
+    protocols.hpp:68-84) give the same TrialReport bits as run_moshpit on host
+    buffers with the same mode."""
+    M, d, n, p, R, dim = 16, 2, 256, 0.05, 5, 70_001
+    tdt = torch.float64 if f64 else torch.float32
+    x = torch.zeros((n, 70_004), dtype=tdt, device="cuda")  # padded rows: ld 16-byte aligned
+    mb.fill_synthetic(x, INIT_SEED, dim=dim)
+    host = np.ascontiguousarray(x[:, :dim].cpu().numpy())
+    eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+    eng.set_reference(x, diagnostics=diag, dim=dim)
+    for _ in range(R):
+        eng.round(x, dim=dim)
+        eng.record(x, dim=dim)
+    init, dist, drift = eng.report()
+    eng.close()
+    want = mb.run_moshpit(mb.GridConfig(M, d, 1), host, mb.FailureModel(p), mb.Rng(7), R,
+                          diagnostics=diag)
+    assert bits_equal(np.array([init]), np.array([want.initial_distortion]))
+    assert bits_equal(np.array(dist), np.array(want.distortion))
+    assert bits_equal(np.array(drift), np.array(want.mean_drift))
