@@ -299,11 +299,24 @@ int moshpit_shard_create(int dtype, uint32_t M, uint32_t d, uint64_t n,
                          double p_round, uint64_t seed, uint64_t dim,
                          int32_t rank, int32_t world, int32_t emulate,
                          int32_t device, moshpit_shard** out);
+/* General form: this process hosts ranks [first_rank, first_rank+ranks_here)
+ * (ranks_here | world, aligned; 1 = one rank per GPU, world = the 1-GPU
+ * emulation), and the columns run as `slabs` (1..8) pipelined slabs one round
+ * apart on separate streams, so cross rounds (NVLink) of one slab overlap
+ * local rounds (HBM) of the others; results are bit-identical to slabs = 1. */
+int moshpit_shard_create_ex(int dtype, uint32_t M, uint32_t d, uint64_t n,
+                            double p_round, uint64_t seed, uint64_t dim,
+                            int32_t first_rank, int32_t ranks_here, int32_t world,
+                            int32_t slabs, int32_t device, moshpit_shard** out);
 int moshpit_shard_destroy(moshpit_shard* s);
-/* 128 bytes: cudaIpcMemHandle_t of this rank's row pool and barrier flags. */
-int moshpit_shard_ipc_handles(moshpit_shard* s, void* out128);
+/* ranks_here * 128 bytes: per hosted rank, the cudaIpcMemHandle_t of its row
+ * pool and of this process's barrier flags. */
+int moshpit_shard_ipc_handles(moshpit_shard* s, void* out);
 /* world*128 bytes gathered in rank order; maps every peer's pool/flags. */
 int moshpit_shard_open_peers(moshpit_shard* s, const void* all_handles);
+/* slabs > 1: finish the lagging slabs' rounds and order `stream` after them
+ * (the state is complete only after a flush; read() flushes). */
+int moshpit_shard_flush(moshpit_shard* s, void* stream);
 /* Synthetic init of the resident peers' rows (x(peer, j), as fill_synthetic). */
 int moshpit_shard_fill_synthetic(moshpit_shard* s, uint64_t seed, void* stream);
 /* Enqueue one round (all ranks must call it the same number of times). */

@@ -745,21 +745,20 @@ class Engine:
 # ---------------------------------------------------------------------------
 # Peer-sharded multi-GPU engine
 # ---------------------------------------------------------------------------
-def exchange_handles(mine: bytes, world: int, group=None) -> List[bytes]:
-    """All-gather one fixed-size handle blob per rank, in rank order."""
+def exchange_handles(mine: bytes, procs: int, group=None) -> List[bytes]:
+    """All-gather one fixed-size handle blob per process, in process order."""
     import torch.distributed as dist
-    if dist.get_world_size(group) != world:
-        raise InvalidArgument("process group size differs from the shard's world")
-    allh = [None] * world
+    if dist.get_world_size(group) != procs:
+        raise InvalidArgument("process group size differs from the shard's process count")
+    allh = [None] * procs
     dist.all_gather_object(allh, mine, group=group)
     if any(len(h) != len(mine) for h in allh):
-        raise InvalidArgument("ranks disagree on the handle size")
+        raise InvalidArgument("processes disagree on the handle size")
     return allh
 
 
 class Shard:
-    """One rank of a peer-sharded Moshpit trial (or, ``emulate=True``, all
-    ``world`` ranks as separate pools on one GPU).
+    """The ranks of a peer-sharded Moshpit trial hosted by this process.
 
     Real multi-process use (one process per GPU, torch.distributed for the
     one-time handle exchange only)::
@@ -768,19 +767,31 @@ class Shard:
         sh.connect(process_group)        # all_gather of CUDA IPC handles
         sh.fill_synthetic(seed)
         for _ in range(rounds): sh.round()
+        sh.flush()                       # slabs > 1: finish the lagging slabs
+
+    ``ranks_per_process=k`` hosts ranks [rank, rank+k) here (rank a multiple of
+    k; e.g. world 8 on 4 GPUs); ``emulate=True`` hosts all ``world`` ranks on
+    one GPU.  ``slabs=S`` pipelines S column slabs one round apart so NVLink
+    cross rounds overlap HBM-bound local rounds (bit-identical results).
     """
 
     def __init__(self, grid: GridConfig, n_peers: int, failure: FailureModel, rng: Rng,
                  dim: int, rank: int = 0, world: int = 1, emulate: bool = False,
-                 device: int = 0, dtype=np.float32):
+                 device: int = 0, dtype=np.float32, ranks_per_process: int = 1,
+                 slabs: int = 1):
         self.grid, self.n, self.dim = grid, int(n_peers), int(dim)
-        self.rank, self.world, self.emulate = rank, world, emulate
+        self.world, self.emulate = world, emulate
+        self.nhost = world if emulate else int(ranks_per_process)
+        self.rank = 0 if emulate else rank
+        self.procs = world // self.nhost
         self.device = int(device)
         self.dtype = np.dtype(dtype)
+        self.slabs = int(slabs)
         h = C.c_void_p()
-        check(lib().moshpit_shard_create(_dtype_code(self.dtype), grid.peers_per_axis, grid.dims,
-                                         self.n, failure.p_round, rng.seed(), self.dim, rank,
-                                         world, 1 if emulate else 0, device, C.byref(h)))
+        check(lib().moshpit_shard_create_ex(_dtype_code(self.dtype), grid.peers_per_axis,
+                                            grid.dims, self.n, failure.p_round, rng.seed(),
+                                            self.dim, self.rank, self.nhost, world, self.slabs,
+                                            device, C.byref(h)))
         self._h = h
 
     def close(self):
@@ -791,18 +802,25 @@ class Shard:
     __del__ = close
 
     def ipc_handles(self) -> bytes:
-        buf = (C.c_char * 128)()
+        buf = (C.c_char * (128 * self.nhost))()
         check(lib().moshpit_shard_ipc_handles(self._h, buf))
         return bytes(buf)
 
     def open_peers(self, handles: Sequence[bytes]):
         blob = b"".join(handles)
+        if len(blob) != 128 * self.world:
+            raise InvalidArgument("open_peers: need 128 bytes per rank")
         buf = (C.c_char * len(blob)).from_buffer_copy(blob)
         check(lib().moshpit_shard_open_peers(self._h, buf))
 
     def connect(self, group=None):
         """Exchange CUDA IPC handles over torch.distributed (plumbing only)."""
-        self.open_peers(exchange_handles(self.ipc_handles(), self.world, group))
+        self.open_peers(exchange_handles(self.ipc_handles(), self.procs, group))
+
+    def flush(self, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().moshpit_shard_flush(self._h, s.cuda_stream))
 
     def fill_synthetic(self, seed: int, stream=None):
         import torch

@@ -22,8 +22,23 @@
 //
 // The integer plane (draws, kernel 1, placement) is replicated on every rank:
 // every rank computes identical tables, so no metadata is exchanged.  Ranks
-// synchronise with a P2P flag barrier kernel (no host round-trip).  Emulation
-// mode runs all G "virtual GPUs" as separate pools on one device (tests).
+// synchronise with a P2P flag barrier kernel (no host round-trip).
+//
+// Hosting.  A process hosts `nhost` consecutive ranks (their pools on its
+// GPU; the data-plane launches loop over them); processes exchange CUDA IPC
+// handles once and barrier among themselves.  nhost = 1: one rank per GPU
+// (production); nhost = world: every rank on one GPU (the 1-GPU emulation
+// harness); in between: e.g. world 8 on 4 GPUs with 2 ranks per process,
+// which exercises the 8-way cross round over real NVLink without ever running
+// two spinning kernels of one GPU against each other.
+//
+// Slab pipeline (slabs = S > 1).  Coordinates are independent, so the
+// columns are cut into S slabs that run one round apart on S streams: at
+// every step one slab is in a cross round (NVLink-bound) while the others
+// are in local rounds (HBM-bound) -- the two rooflines overlap instead of
+// adding up.  Each round's tables are computed once (control stream) into a
+// ring of S+1 slots; slab k replays round r's slot at step r+k; flush()
+// completes the lagging slabs.  Bit-identical to S = 1 (tests).
 #include <algorithm>
 #include <cstdlib>
 #include <memory>
@@ -54,6 +69,7 @@ struct PlaceArgs {
   std::uint32_t* moves = nullptr;       // [world][R][2] (src, dst), grouped by dst GPU
   std::uint32_t* n_moves = nullptr;     // [world]
   std::uint32_t* err = nullptr;         // [1]
+  std::uint32_t* goff_out = nullptr;    // [n+1] copy of goff for the data plane (slot)
   unsigned long long* totals = nullptr; // [0] cross active groups, [1] cross rounds,
                                         // [2+h] local active rows on GPU h,
                                         // [2+kMaxWorld+h] voided rows moved to GPU h
@@ -66,6 +82,7 @@ __global__ void __launch_bounds__(1024) place_kernel(PlaceArgs a) {
   if (threadIdx.x < 4) a.cnt_cross[threadIdx.x] = 0;
   if (threadIdx.x < a.world) a.n_moves[threadIdx.x] = 0;
   if (threadIdx.x == 0 && a.cross) a.totals[1] += 1;
+  for (std::uint32_t g = threadIdx.x; g <= ng; g += blockDim.x) a.goff_out[g] = a.goff[g];
   __syncthreads();
   for (std::uint32_t g = threadIdx.x; g < ng; g += blockDim.x) {
     const std::uint32_t b = a.goff[g], e = a.goff[g + 1];
@@ -178,6 +195,7 @@ struct CrossArgs {
   T* pools[kMaxWorld];
   std::uint64_t ld_vec = 0, R = 0;
   std::uint64_t c0 = 0, c1 = 0, n_tiles = 0;
+  std::uint64_t vb = 0, ve = 0;  // the slab's column range (16-byte vectors)
   std::uint32_t me = 0, world = 1;
   const std::uint32_t* goff = nullptr;
   const std::uint32_t* src_row = nullptr;
@@ -254,7 +272,7 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
 // from the replicated tables, so no metadata travels.
 template <typename T>
 __global__ void __launch_bounds__(kCrossThreads)
-    shard_pull_kernel(CrossArgs<T> a, std::uint64_t nvec) {
+    shard_pull_kernel(CrossArgs<T> a) {
   using V = typename V16s<T>::type;
   __shared__ V* s_rows[32];
   __shared__ const V* s_rep[kMaxWorld];
@@ -281,12 +299,13 @@ __global__ void __launch_bounds__(kCrossThreads)
       cached = g;
       __syncthreads();
     }
-    const std::uint64_t col = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
-    if (col >= nvec || (col >= a.c0 && col < a.c1)) continue;
-    // owner of this column: chunk c covers [nvec*c/world, nvec*(c+1)/world)
-    std::uint32_t c = (std::uint32_t)((col * world) / nvec);
-    while (c + 1 < world && (nvec * (c + 1)) / world <= col) ++c;
-    while (c > 0 && (nvec * c) / world > col) --c;
+    const std::uint64_t rel = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    const std::uint64_t W = a.ve - a.vb, col = a.vb + rel;
+    if (rel >= W || (col >= a.c0 && col < a.c1)) continue;
+    // owner of this column: chunk c covers [vb + W*c/world, vb + W*(c+1)/world)
+    std::uint32_t c = (std::uint32_t)((rel * world) / W);
+    while (c + 1 < world && (W * (c + 1)) / world <= rel) ++c;
+    while (c > 0 && (W * c) / world > rel) --c;
     const V v = *(s_rep[c] + col);
     for (std::uint32_t k = 0; k < s_n; ++k) s_rows[k][col] = v;
   }
@@ -398,14 +417,16 @@ __global__ void __launch_bounds__(kCrossThreads)
 template <typename T>
 __global__ void move_rows_kernel(T* const* pools, const std::uint32_t* moves,
                                  const std::uint32_t* n_moves, std::uint32_t me, std::uint64_t R,
-                                 std::uint64_t ld_vec, std::uint64_t nvec, T* staging, int phase) {
+                                 std::uint64_t ld_vec, std::uint64_t vb, std::uint64_t ve,
+                                 T* staging, int phase) {
   using V = typename V16s<T>::type;
   const std::uint32_t cnt = n_moves[me];
-  const std::uint64_t total = (std::uint64_t)cnt * nvec;
+  const std::uint64_t W = ve - vb;
+  const std::uint64_t total = (std::uint64_t)cnt * W;
   V* st = reinterpret_cast<V*>(staging);
   for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
        e += (std::uint64_t)gridDim.x * blockDim.x) {
-    const std::uint64_t k = e / nvec, c = e % nvec;
+    const std::uint64_t k = e / W, c = vb + e % W;
     const std::uint32_t* mv = moves + ((std::uint64_t)me * R + k) * 2;
     if (phase == 0) {
       const std::uint32_t s = mv[0];
@@ -422,13 +443,17 @@ __global__ void move_rows_kernel(T* const* pools, const std::uint32_t* moves,
 // P2P flag barrier: each rank publishes `epoch` into every peer's flag slot,
 // then waits for all peers' slots to reach it.  Bounded spin -> __trap()
 // (an error, never a hang).
+// Flags are [slab][process]: one row per slab stream (their barriers
+// interleave), one slot per writing process.
 __global__ void peer_barrier_kernel(unsigned long long* my_flags, unsigned long long* const* peer_flags,
-                                    std::uint32_t me, std::uint32_t world, unsigned long long epoch) {
+                                    std::uint32_t me, std::uint32_t world, unsigned long long epoch,
+                                    std::uint32_t row) {
   if (threadIdx.x != 0) return;
+  my_flags += (std::uint64_t)row * kMaxWorld;
   __threadfence_system();
   for (std::uint32_t h = 0; h < world; ++h) {
     if (h == me) continue;
-    unsigned long long* f = peer_flags[h] + me;
+    unsigned long long* f = peer_flags[h] + (std::uint64_t)row * kMaxWorld + me;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
   }
   const long long t0 = clock64();
@@ -491,6 +516,23 @@ unsigned grid_cap(std::uint64_t work) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+constexpr int kMaxSlabs = 8;
+
+// One round's replicated tables (ring slot of the slab pipeline).
+struct TableSlot {
+  DeviceBuffer goff, rows_local, act_local, cnt_local, src_row, dst_row, act_cross, cnt_cross,
+      moves, n_moves;
+  cudaEvent_t ready = nullptr;             // written (control stream)
+  cudaEvent_t freed[kMaxSlabs] = {};       // slab k is done with it
+  bool used[kMaxSlabs] = {};
+  int cross = 0;
+  ~TableSlot() {
+    if (ready) cudaEventDestroy(ready);
+    for (auto e : freed)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 struct Shard {
   std::unique_ptr<Plane> plane;
   Xoshiro fail, clock;
@@ -499,29 +541,40 @@ struct Shard {
   std::size_t es = 4;
   std::uint64_t dim = 0, ld = 0, R = 0;
   std::uint32_t world = 1, me = 0, Mg = 1, M = 1, d = 1;
+  std::uint32_t nhost = 1, proc = 0, procs = 1;  // ranks [me, me+nhost) live here
   int device = 0;
-  bool emulate = false;
-  bool connected = false;  // real mode: peers' pools/flags mapped (open_peers)
+  bool emulate = false;    // nhost == world: no peers, no barriers
+  bool connected = false;  // peers' pools/flags mapped (open_peers)
   std::uint32_t round_no = 0;
-  unsigned long long epoch = 0;
-  // replicated bookkeeping
-  DeviceBuffer loc, rows_local, act_local, cnt_local, src_row, dst_row, act_cross, cnt_cross,
-      moves, n_moves, err, pool_tab, flag_tab, totals;
-  // pools: [world] in emulation, [1] (mine) otherwise
+  // replicated per-trial state and the table ring
+  DeviceBuffer loc, err, pool_tab, flag_tab, totals;
+  std::vector<std::unique_ptr<TableSlot>> ring;
+  // slab pipeline
+  std::uint32_t S = 1;
+  std::uint64_t vb[kMaxSlabs] = {}, ve[kMaxSlabs] = {};
+  std::uint32_t slab_done[kMaxSlabs] = {};  // rounds completed (enqueued) per slab
+  unsigned long long epoch[kMaxSlabs] = {};
+  std::unique_ptr<StreamHolder> cs, ss[kMaxSlabs];
+  cudaEvent_t ev_user = nullptr, ev_slab[kMaxSlabs] = {};
+  cudaStream_t user = nullptr;
+  // pools of the hosted ranks; IPC mappings of the others
   std::vector<std::unique_ptr<DeviceBuffer>> own_pools;
-  std::vector<std::unique_ptr<DeviceBuffer>> staging;
+  std::unique_ptr<DeviceBuffer> staging;  // voided-row moves (shared: slabs own columns)
   void* pools[kMaxWorld] = {};
-  DeviceBuffer flags;  // [world] u64 (real mode)
-  unsigned long long* peer_flags[kMaxWorld] = {};
+  DeviceBuffer flags;  // [kMaxSlabs][kMaxWorld] u64 (this process's slots)
+  unsigned long long* peer_flags[kMaxWorld] = {};  // by process
   std::vector<void*> opened;  // IPC mappings to close
-  // timing of the data-plane kernels (CUDA events on the launch stream)
+  // timing of the data-plane kernels (CUDA events on their streams)
   bool timing = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev_local, tev_cross;
-  std::size_t used_local = 0, used_cross = 0;
-  double last_a_ms = 0.0, last_b_ms = 0.0;  // cross phases of the last kernel_time
-  // copy-engine cross round (MOSHPIT_CROSS_CE=1; the default is the SM-pull
-  // kernels): host copy of the replicated tables, two copy streams with their
-  // staging buffers, and the events that order them against the main stream
+  struct TEv {
+    cudaEvent_t a, b;
+    int kind;  // 0 local, 1 cross phase A, 2 cross phase B
+  };
+  std::vector<TEv> tev;
+  std::size_t tev_used = 0;
+  double last_a_ms = 0.0, last_b_ms = 0.0;
+  // copy-engine cross round (MOSHPIT_CROSS_CE=1, S = 1 only; the default is
+  // the SM-pull kernels)
   bool ce = false;
   PinnedBuffer htab;
   std::unique_ptr<StreamHolder> cstream[2];
@@ -531,94 +584,132 @@ struct Shard {
   std::vector<std::size_t> csize;
 
   ~Shard() {
-    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1], ev_go})
+    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1], ev_go, ev_user})
+      if (e) cudaEventDestroy(e);
+    for (auto e : ev_slab)
       if (e) cudaEventDestroy(e);
     for (void* q : opened) cudaIpcCloseMemHandle(q);
-    for (auto* v : {&tev_local, &tev_cross})
-      for (auto& pr : *v) {
-        cudaEventDestroy(pr.first);
-        cudaEventDestroy(pr.second);
-      }
-  }
-
-  std::pair<cudaEvent_t, cudaEvent_t> tpair(bool cross) {
-    auto& v = cross ? tev_cross : tev_local;
-    auto& u = cross ? used_cross : used_local;
-    if (u == v.size()) {
-      cudaEvent_t a, b;
-      MB_CUDA(cudaEventCreate(&a));
-      MB_CUDA(cudaEventCreate(&b));
-      v.emplace_back(a, b);
+    for (auto& t : tev) {
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
     }
-    return v[u++];
   }
 
+  bool hosts(std::uint32_t r) const { return r >= me && r < me + nhost; }
   std::uint64_t nvec() const { return (dim + (16 / es) - 1) / (16 / es); }
   std::uint32_t n() const { return (std::uint32_t)plane->n; }
+  cudaStream_t slab_stream(std::uint32_t k) const { return S == 1 ? user : ss[k]->s; }
+  cudaStream_t ctl_stream() const { return S == 1 ? user : cs->s; }
 
-  void barrier(cudaStream_t s) {
-    if (emulate || world == 1) return;
-    ++epoch;
+  TEv& tpair(int kind) {
+    if (tev_used == tev.size()) {
+      TEv t{};
+      MB_CUDA(cudaEventCreate(&t.a));
+      MB_CUDA(cudaEventCreate(&t.b));
+      tev.push_back(t);
+    }
+    TEv& t = tev[tev_used++];
+    t.kind = kind;
+    return t;
+  }
+
+  void alloc_slot(TableSlot& t) {
+    const std::uint64_t nn = n();
+    t.goff.resize((nn + 1) * 4 + 16);
+    t.rows_local.resize(nn * 4);
+    t.act_local.resize((std::uint64_t)world * nn * 4);
+    t.cnt_local.resize((std::uint64_t)world * 16 + 16);
+    t.src_row.resize(nn * 4);
+    t.dst_row.resize(nn * 4);
+    t.act_cross.resize(nn * 4);
+    t.cnt_cross.resize(16);
+    t.moves.resize((std::uint64_t)world * R * 8);
+    t.n_moves.resize(world * 4 + 16);
+    MB_CUDA(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+    for (std::uint32_t k = 0; k < S; ++k)
+      MB_CUDA(cudaEventCreateWithFlags(&t.freed[k], cudaEventDisableTiming));
+  }
+
+  void barrier(std::uint32_t k, cudaStream_t s) {
+    if (emulate || procs == 1) return;
+    ++epoch[k];
     peer_barrier_kernel<<<1, 32, 0, s>>>(flags.as<unsigned long long>(),
-                                        flag_tab.as<unsigned long long* const>(), me, world,
-                                        epoch);
+                                        flag_tab.as<unsigned long long* const>(), proc, procs,
+                                        epoch[k], k);
     MB_LAUNCH_CHECK();
   }
 
   template <typename T>
-  void cross_launch(std::uint32_t r, cudaStream_t s) {
+  CrossArgs<T> cross_args(const TableSlot& t, std::uint32_t r, std::uint32_t k, bool full_slab) {
     CrossArgs<T> a;
     for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
     a.ld_vec = ld * es / 16;
     a.R = R;
-    const std::uint64_t nv = nvec();
-    a.c0 = nv * r / world;
-    a.c1 = nv * (r + 1) / world;
-    a.n_tiles = (a.c1 - a.c0 + kCrossThreads - 1) / kCrossThreads;
+    a.vb = vb[k];
+    a.ve = ve[k];
+    const std::uint64_t W = a.ve - a.vb;
+    a.c0 = a.vb + W * r / world;
+    a.c1 = a.vb + W * (r + 1) / world;
+    a.n_tiles = ((full_slab ? W : a.c1 - a.c0) + kCrossThreads - 1) / kCrossThreads;
     a.me = r;
     a.world = world;
-    a.goff = plane->goff.as<std::uint32_t>();
-    a.src_row = src_row.as<std::uint32_t>();
-    a.dst_row = dst_row.as<std::uint32_t>();
-    a.act = act_cross.as<std::uint32_t>();
-    a.cnt = cnt_cross.as<std::uint32_t>();
-    int per = 0, sms = 0;
-    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_mean_kernel<T>,
-                                                          kCrossThreads, 0));
-    if (const char* e = std::getenv("MOSHPIT_CROSS_CTAS")) per = std::min(per, std::atoi(e));
-    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    if (a.n_tiles) cross_mean_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(a);
-    MB_LAUNCH_CHECK();
+    a.goff = t.goff.as<std::uint32_t>();
+    a.src_row = t.src_row.as<std::uint32_t>();
+    a.dst_row = t.dst_row.as<std::uint32_t>();
+    a.act = t.act_cross.as<std::uint32_t>();
+    a.cnt = t.cnt_cross.as<std::uint32_t>();
+    return a;
   }
 
-  template <typename T>
-  void pull_launch(std::uint32_t r, cudaStream_t s) {
-    if (world < 2) return;
-    CrossArgs<T> a;
-    for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
-    a.ld_vec = ld * es / 16;
-    a.R = R;
-    const std::uint64_t nv = nvec();
-    a.c0 = nv * r / world;
-    a.c1 = nv * (r + 1) / world;
-    a.n_tiles = (nv + kCrossThreads - 1) / kCrossThreads;
-    a.me = r;
-    a.world = world;
-    a.goff = plane->goff.as<std::uint32_t>();
-    a.dst_row = dst_row.as<std::uint32_t>();
-    a.act = act_cross.as<std::uint32_t>();
-    a.cnt = cnt_cross.as<std::uint32_t>();
+  int sm_count() const {
     int sms = 0;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    shard_pull_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a, nv);
+    return sms;
+  }
+
+  template <typename T>
+  void cross_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
+    CrossArgs<T> a = cross_args<T>(t, r, k, false);
+    static int per = -1;
+    if (per < 0) {
+      MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_mean_kernel<T>,
+                                                            kCrossThreads, 0));
+      if (const char* e = std::getenv("MOSHPIT_CROSS_CTAS")) per = std::min(per, std::atoi(e));
+      if (per < 1) per = 1;
+    }
+    if (a.n_tiles) cross_mean_kernel<T><<<sm_count() * per, kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+
+  template <typename T>
+  void pull_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
+    if (world < 2) return;
+    CrossArgs<T> a = cross_args<T>(t, r, k, true);
+    static int per = -1;
+    if (per < 0) {
+      per = 8;
+      if (const char* e = std::getenv("MOSHPIT_PULL_CTAS")) per = std::max(1, std::atoi(e));
+    }
+    if (a.n_tiles) shard_pull_kernel<T><<<sm_count() * per, kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+
+  template <typename T>
+  void moves_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, int phase,
+                    cudaStream_t s) {
+    if (p <= 0.0) return;  // no voided groups without failures
+    move_rows_kernel<T><<<grid_cap(R * (ve[k] - vb[k])), 256, 0, s>>>(
+        pool_tab.as<T* const>(), t.moves.as<std::uint32_t>(), t.n_moves.as<std::uint32_t>(), r,
+        R, ld * es / 16, vb[k], ve[k], staging->as<T>() + (hosts(r) ? (r - me) : 0) * R * ld,
+        phase);
     MB_LAUNCH_CHECK();
   }
 
   // Copy a list of (dst, src, bytes) on stream cs: one async copy each (the
   // copy engines take peer pointers of the IPC-mapped pools directly).
-  void copy_list(cudaStream_t cs) {
+  void copy_list(cudaStream_t c) {
     for (std::size_t i = 0; i < cdst.size(); ++i)
-      MB_CUDA(cudaMemcpyAsync(cdst[i], csrc[i], csize[i], cudaMemcpyDefault, cs));
+      MB_CUDA(cudaMemcpyAsync(cdst[i], csrc[i], csize[i], cudaMemcpyDefault, c));
     cdst.clear();
     csrc.clear();
     csize.clear();
@@ -635,41 +726,21 @@ struct Shard {
   }
 
   // Host copy of the cross round's replicated tables (synchronises s once).
-  void ce_fetch_tables(cudaStream_t s) {
+  void ce_fetch_tables(const TableSlot& t, cudaStream_t s) {
     const std::uint64_t nn = n();
     htab.resize((4 * nn + 8) * 4);
     auto* h = htab.as<std::uint32_t>();
-    MB_CUDA(cudaMemcpyAsync(h, src_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
-    MB_CUDA(cudaMemcpyAsync(h + nn, dst_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
-    MB_CUDA(cudaMemcpyAsync(h + 2 * nn, plane->goff.ptr, (nn + 1) * 4, cudaMemcpyDeviceToHost, s));
-    MB_CUDA(cudaMemcpyAsync(h + 3 * nn + 1, act_cross.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
-    MB_CUDA(cudaMemcpyAsync(h + 4 * nn + 1, cnt_cross.ptr, 16, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h, t.src_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + nn, t.dst_row.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 2 * nn, t.goff.ptr, (nn + 1) * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 3 * nn + 1, t.act_cross.ptr, nn * 4, cudaMemcpyDeviceToHost, s));
+    MB_CUDA(cudaMemcpyAsync(h + 4 * nn + 1, t.cnt_cross.ptr, 16, cudaMemcpyDeviceToHost, s));
     MB_CUDA(cudaStreamSynchronize(s));
   }
 
+  // Phase A for rank r (copy engines): staged remote chunks + tree kernel.
   template <typename T>
-  CrossArgs<T> cross_args(std::uint32_t r, bool full_row) {
-    CrossArgs<T> a;
-    for (std::uint32_t h = 0; h < world; ++h) a.pools[h] = static_cast<T*>(pools[h]);
-    a.ld_vec = ld * es / 16;
-    a.R = R;
-    const std::uint64_t nv = nvec();
-    a.c0 = nv * r / world;
-    a.c1 = nv * (r + 1) / world;
-    a.n_tiles = ((full_row ? nv : a.c1 - a.c0) + kCrossThreads - 1) / kCrossThreads;
-    a.me = r;
-    a.world = world;
-    a.goff = plane->goff.as<std::uint32_t>();
-    a.src_row = src_row.as<std::uint32_t>();
-    a.dst_row = dst_row.as<std::uint32_t>();
-    a.act = act_cross.as<std::uint32_t>();
-    a.cnt = cnt_cross.as<std::uint32_t>();
-    return a;
-  }
-
-  // Phase A for rank r: staged remote chunks (copy engines) + tree kernel.
-  template <typename T>
-  void cross_ce(std::uint32_t r, cudaStream_t s) {
+  void cross_ce(const TableSlot& t, std::uint32_t r, cudaStream_t s) {
     ce_init();
     const std::uint64_t nn = n();
     const auto* h = htab.as<std::uint32_t>();
@@ -677,7 +748,7 @@ struct Shard {
     const std::uint32_t* hgoff = h + 2 * nn;
     const std::uint32_t* hact = h + 3 * nn + 1;
     const std::uint32_t nact = h[4 * nn + 1 + 1];
-    CrossArgs<T> a = cross_args<T>(r, false);
+    CrossArgs<T> a = cross_args<T>(t, r, 0, false);
     const std::uint64_t cbytes = (a.c1 - a.c0) * 16;
     if (nact == 0 || cbytes == 0) return;
     const std::uint32_t nrem = M - Mg;  // full grid: Mg members of a line per GPU
@@ -685,46 +756,43 @@ struct Shard {
     std::uint32_t B = (std::uint32_t)std::max<std::uint64_t>(
         1, std::min<std::uint64_t>(nact, (512ull << 20) / std::max<std::uint64_t>(per_group, 1)));
     for (int i = 0; i < 2; ++i) cstage[i].resize(B * per_group + 16);
-    int per = 0, sms = 0;
+    int per = 0;
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cross_staged_kernel<T>,
                                                           kCrossThreads, 0));
-    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     MB_CUDA(cudaEventRecord(ev_go, s));  // after the barrier: peers' rows are final
-    for (int i = 0; i < 2; ++i) {
-      MB_CUDA(cudaStreamWaitEvent(cstream[i]->s, ev_go, 0));
-    }
+    for (int i = 0; i < 2; ++i) MB_CUDA(cudaStreamWaitEvent(cstream[i]->s, ev_go, 0));
     std::uint32_t batch = 0;
     for (std::uint32_t gb = 0; gb < nact; gb += B, ++batch) {
       const std::uint32_t ge = std::min(nact, gb + B);
       const int slot = batch & 1;
-      cudaStream_t cs = cstream[slot]->s;
-      if (batch >= 2) MB_CUDA(cudaStreamWaitEvent(cs, ev_free[slot], 0));
+      cudaStream_t c = cstream[slot]->s;
+      if (batch >= 2) MB_CUDA(cudaStreamWaitEvent(c, ev_free[slot], 0));
       char* st = cstage[slot].as<char>();
       for (std::uint32_t gi = gb; gi < ge; ++gi) {
         const std::uint32_t g = hact[gi];
-        std::uint32_t k = 0;
+        std::uint32_t q = 0;
         for (std::uint32_t pos = hgoff[g]; pos < hgoff[g + 1]; ++pos) {
           const std::uint32_t sr = hsrc[pos];
           if (sr / R == r) continue;
-          cdst.push_back(st + ((std::uint64_t)(gi - gb) * nrem + k++) * cbytes);
+          cdst.push_back(st + ((std::uint64_t)(gi - gb) * nrem + q++) * cbytes);
           csrc.push_back(static_cast<char*>(pools[sr / R]) + (sr % R) * ld * es + a.c0 * 16);
           csize.push_back(cbytes);
         }
       }
-      copy_list(cs);
-      MB_CUDA(cudaEventRecord(ev_copied[slot], cs));
+      copy_list(c);
+      MB_CUDA(cudaEventRecord(ev_copied[slot], c));
       MB_CUDA(cudaStreamWaitEvent(s, ev_copied[slot], 0));
-      cross_staged_kernel<T><<<sms * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(
+      cross_staged_kernel<T><<<sm_count() * (per > 0 ? per : 1), kCrossThreads, 0, s>>>(
           a, cstage[slot].as<T>(), gb, ge, nrem);
       MB_LAUNCH_CHECK();
       MB_CUDA(cudaEventRecord(ev_free[slot], s));
     }
   }
 
-  // Phase B for rank r: copy-engine pulls of every foreign chunk mean into
-  // the group's first local member row, then the local fan-out.
+  // Phase B for rank r (copy engines): foreign chunk means into the group's
+  // first local member row, then the local fan-out.
   template <typename T>
-  void pull_ce(std::uint32_t r, cudaStream_t s) {
+  void pull_ce(const TableSlot& t, std::uint32_t r, cudaStream_t s) {
     if (world < 2) return;
     const std::uint64_t nn = n();
     const auto* h = htab.as<std::uint32_t>();
@@ -738,8 +806,8 @@ struct Shard {
       std::uint32_t rep[kMaxWorld];
       for (std::uint32_t q = 0; q < world; ++q) rep[q] = 0xffffffffu;
       for (std::uint32_t pos = hgoff[g]; pos < hgoff[g + 1]; ++pos) {
-        const std::uint32_t d = hdst[pos], q = (std::uint32_t)(d / R);
-        if (rep[q] == 0xffffffffu) rep[q] = d;
+        const std::uint32_t dd = hdst[pos], q = (std::uint32_t)(dd / R);
+        if (rep[q] == 0xffffffffu) rep[q] = dd;
       }
       char* mine = static_cast<char*>(pools[r]) + (rep[r] % R) * ld * es;
       for (std::uint32_t q = 0; q < world; ++q) {
@@ -753,124 +821,143 @@ struct Shard {
     }
     copy_list(s);
     if (Mg > 1) {
-      CrossArgs<T> a = cross_args<T>(r, true);
-      int sms = 0;
-      MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      local_fanout_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a, nv);
+      CrossArgs<T> a = cross_args<T>(t, r, 0, true);
+      local_fanout_kernel<T><<<sm_count() * 8, kCrossThreads, 0, s>>>(a, nv);
       MB_LAUNCH_CHECK();
     }
   }
 
-  template <typename T>
-  void moves_launch(std::uint32_t r, int phase, cudaStream_t s) {
-    if (p <= 0.0) return;  // no voided groups without failures
-    auto& st = staging[emulate ? r : 0];
-    if (!st) {
-      st = std::make_unique<DeviceBuffer>(R * ld * es);
+  // Round `rr` of slab k from its ring slot: the data plane of every hosted
+  // rank on the slab's columns.
+  void run_slab(std::uint32_t k, std::uint32_t rr) {
+    TableSlot& t = *ring[rr % ring.size()];
+    cudaStream_t s = slab_stream(k);
+    if (S > 1) MB_CUDA(cudaStreamWaitEvent(s, t.ready, 0));
+    const bool f32 = dtype == MOSHPIT_F32;
+    if (!t.cross) {
+      TEv* te = timing ? &tpair(0) : nullptr;
+      if (te) MB_CUDA(cudaEventRecord(te->a, s));
+      const std::uint64_t kv = 16 / es;
+      const std::uint64_t c0 = vb[k] * kv, c1 = std::min<std::uint64_t>(ve[k] * kv, dim);
+      for (std::uint32_t r = me; r < me + nhost; ++r) {
+        const std::uint32_t* act = t.act_local.as<std::uint32_t>() + (std::uint64_t)r * n();
+        const std::uint32_t* cnt = t.cnt_local.as<std::uint32_t>() + r * 4;
+        if (c1 <= c0) break;
+        if (f32)
+          launch_group_mean<float>(static_cast<float*>(pools[r]) + c0, ld, c1 - c0,
+                                   t.rows_local.as<std::uint32_t>(), t.goff.as<std::uint32_t>(),
+                                   act, cnt, M, 0, s);
+        else
+          launch_group_mean<double>(static_cast<double*>(pools[r]) + c0, ld, c1 - c0,
+                                    t.rows_local.as<std::uint32_t>(), t.goff.as<std::uint32_t>(),
+                                    act, cnt, M, 0, s);
+      }
+      if (te) MB_CUDA(cudaEventRecord(te->b, s));
+    } else {
+      if (ce) ce_fetch_tables(t, s);
+      barrier(k, s);  // peers finished writing the rows we are about to read
+      TEv* ta = timing ? &tpair(1) : nullptr;
+      if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
+      for (std::uint32_t r = me; r < me + nhost; ++r) {
+        if (f32) {
+          if (ce) cross_ce<float>(t, r, s);
+          else cross_launch<float>(t, r, k, s);
+          moves_launch<float>(t, r, k, 0, s);
+        } else {
+          if (ce) cross_ce<double>(t, r, s);
+          else cross_launch<double>(t, r, k, s);
+          moves_launch<double>(t, r, k, 0, s);
+        }
+      }
+      if (ta) MB_CUDA(cudaEventRecord(ta->b, s));
+      barrier(k, s);  // every chunk mean is in its owner's rows; raw reads are done
+      TEv* tb = timing ? &tpair(2) : nullptr;
+      if (tb) MB_CUDA(cudaEventRecord(tb->a, s));
+      for (std::uint32_t r = me; r < me + nhost; ++r) {
+        if (f32) {
+          if (ce) pull_ce<float>(t, r, s);
+          else pull_launch<float>(t, r, k, s);
+          moves_launch<float>(t, r, k, 1, s);
+        } else {
+          if (ce) pull_ce<double>(t, r, s);
+          else pull_launch<double>(t, r, k, s);
+          moves_launch<double>(t, r, k, 1, s);
+        }
+      }
+      if (tb) MB_CUDA(cudaEventRecord(tb->b, s));
+      barrier(k, s);  // peers finished pulling from our rows before we touch them again
     }
-    move_rows_kernel<T><<<grid_cap(R * nvec()), 256, 0, s>>>(
-        pool_tab.as<T* const>(), moves.as<std::uint32_t>(), n_moves.as<std::uint32_t>(), r, R,
-        ld * es / 16, nvec(), st->as<T>(), phase);
-    MB_LAUNCH_CHECK();
+    if (S > 1) {
+      MB_CUDA(cudaEventRecord(t.freed[k], s));
+      t.used[k] = true;
+    }
+    slab_done[k] = rr + 1;
   }
 
-  // One round on every rank: identical host draws and kernel 1, replicated
-  // placement, then this rank's data plane (all virtual ranks in emulation).
+  // One round: identical host draws, kernel 1 and placement on every rank
+  // (into ring slot r), then the slabs' data planes -- slab k runs round r-k.
   std::uint32_t round(cudaStream_t s, int* crossed) {
-    const std::uint32_t axis = d ? round_no % d : 0;
+    user = s;
+    const std::uint32_t r = round_no;
+    const std::uint32_t axis = d ? r % d : 0;
     const int cross = (world > 1 && axis == d - 1) ? 1 : 0;
+    TableSlot& t = *ring[r % ring.size()];
+    cudaStream_t c = ctl_stream();
+    if (S > 1) {
+      // caller's prior work on s (e.g. the synthetic init) comes first
+      MB_CUDA(cudaEventRecord(ev_user, s));
+      MB_CUDA(cudaStreamWaitEvent(c, ev_user, 0));
+      for (std::uint32_t k = 0; k < S; ++k) MB_CUDA(cudaStreamWaitEvent(ss[k]->s, ev_user, 0));
+      for (std::uint32_t k = 0; k < S; ++k)
+        if (t.used[k]) MB_CUDA(cudaStreamWaitEvent(c, t.freed[k], 0));  // slot reuse
+    }
     ++round_no;
-    const std::uint32_t active = plane->round(&fail, p, clock, dtype, nullptr, 0, 0, s, 0);
+    const std::uint32_t active = plane->round(&fail, p, clock, dtype, nullptr, 0, 0, c, 0);
     PlaceArgs a;
     a.n = n();
     a.world = world;
     a.Mg = Mg;
     a.R = R;
-    a.cross = cross || world == 1;
-    if (world == 1) a.cross = 0;
+    a.cross = cross;
     a.members = plane->members.as<std::uint32_t>();
     a.goff = plane->goff.as<std::uint32_t>();
     a.counts = plane->counts.as<std::uint32_t>();
     a.gvoid = plane->gvoid.as<std::uint8_t>();
     a.loc = loc.as<std::uint32_t>();
-    a.rows_local = rows_local.as<std::uint32_t>();
-    a.act_local = act_local.as<std::uint32_t>();
-    a.cnt_local = cnt_local.as<std::uint32_t>();
-    a.src_row = src_row.as<std::uint32_t>();
-    a.dst_row = dst_row.as<std::uint32_t>();
-    a.act_cross = act_cross.as<std::uint32_t>();
-    a.cnt_cross = cnt_cross.as<std::uint32_t>();
-    a.moves = moves.as<std::uint32_t>();
-    a.n_moves = n_moves.as<std::uint32_t>();
+    a.rows_local = t.rows_local.as<std::uint32_t>();
+    a.act_local = t.act_local.as<std::uint32_t>();
+    a.cnt_local = t.cnt_local.as<std::uint32_t>();
+    a.src_row = t.src_row.as<std::uint32_t>();
+    a.dst_row = t.dst_row.as<std::uint32_t>();
+    a.act_cross = t.act_cross.as<std::uint32_t>();
+    a.cnt_cross = t.cnt_cross.as<std::uint32_t>();
+    a.moves = t.moves.as<std::uint32_t>();
+    a.n_moves = t.n_moves.as<std::uint32_t>();
     a.err = err.as<std::uint32_t>();
+    a.goff_out = t.goff.as<std::uint32_t>();
     a.totals = totals.as<unsigned long long>();
-    place_kernel<<<1, 1024, 0, s>>>(a);
+    place_kernel<<<1, 1024, 0, c>>>(a);
     MB_LAUNCH_CHECK();
-    const std::uint32_t nranks = emulate ? world : 1;
-    if (!a.cross) {
-      std::pair<cudaEvent_t, cudaEvent_t> te{};
-      if (timing) {
-        te = tpair(false);
-        MB_CUDA(cudaEventRecord(te.first, s));
-      }
-      for (std::uint32_t k = 0; k < nranks; ++k) {
-        const std::uint32_t r = emulate ? k : me;
-        const std::uint32_t* rows = rows_local.as<std::uint32_t>();
-        const std::uint32_t* act = act_local.as<std::uint32_t>() + (std::uint64_t)r * n();
-        const std::uint32_t* cnt = cnt_local.as<std::uint32_t>() + r * 4;
-        if (dtype == MOSHPIT_F32)
-          launch_group_mean<float>(static_cast<float*>(pools[r]), ld, dim, rows, a.goff, act,
-                                   cnt, M, 0, s);
-        else
-          launch_group_mean<double>(static_cast<double*>(pools[r]), ld, dim, rows, a.goff, act,
-                                    cnt, M, 0, s);
-      }
-      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
-    } else {
-      if (ce) ce_fetch_tables(s);
-      barrier(s);  // peers finished writing the rows we are about to read
-      std::pair<cudaEvent_t, cudaEvent_t> te{};
-      if (timing) {
-        te = tpair(true);
-        MB_CUDA(cudaEventRecord(te.first, s));
-      }
-      for (std::uint32_t k = 0; k < nranks; ++k) {
-        const std::uint32_t r = emulate ? k : me;
-        if (dtype == MOSHPIT_F32) {
-          if (ce) cross_ce<float>(r, s);
-          else cross_launch<float>(r, s);
-          moves_launch<float>(r, 0, s);
-        } else {
-          if (ce) cross_ce<double>(r, s);
-          else cross_launch<double>(r, s);
-          moves_launch<double>(r, 0, s);
-        }
-      }
-      if (timing) MB_CUDA(cudaEventRecord(te.second, s));
-      barrier(s);  // every chunk mean is in its owner's rows; raw reads are done
-      std::pair<cudaEvent_t, cudaEvent_t> tb{};
-      if (timing) {
-        tb = tpair(true);
-        MB_CUDA(cudaEventRecord(tb.first, s));
-      }
-      for (std::uint32_t k = 0; k < nranks; ++k) {
-        const std::uint32_t r = emulate ? k : me;
-        if (dtype == MOSHPIT_F32) {
-          if (ce) pull_ce<float>(r, s);
-          else pull_launch<float>(r, s);
-          moves_launch<float>(r, 1, s);
-        } else {
-          if (ce) pull_ce<double>(r, s);
-          else pull_launch<double>(r, s);
-          moves_launch<double>(r, 1, s);
-        }
-      }
-      if (timing) MB_CUDA(cudaEventRecord(tb.second, s));
-      barrier(s);  // peers finished pulling from our rows before we touch them again
-    }
-    plane->mark_done(s);  // the next round (any stream) starts after this one
-    if (crossed) *crossed = a.cross;
+    t.cross = cross;
+    plane->mark_done(c);
+    if (S > 1) MB_CUDA(cudaEventRecord(t.ready, c));
+    for (std::uint32_t k = 0; k < S; ++k)
+      if (r >= k && slab_done[k] == r - k) run_slab(k, r - k);
+    if (crossed) *crossed = cross;
     return active;
+  }
+
+  // Complete the lagging slabs (rounds already tabled) and order `s` after
+  // every slab stream.  S = 1: nothing to do.
+  void flush(cudaStream_t s) {
+    if (S == 1) return;
+    for (std::uint32_t step = 0; step + 1 < S; ++step)
+      for (std::uint32_t k = 0; k < S; ++k)
+        if (slab_done[k] < round_no) run_slab(k, slab_done[k]);
+    for (std::uint32_t k = 0; k < S; ++k) {
+      MB_CUDA(cudaEventRecord(ev_slab[k], ss[k]->s));
+      MB_CUDA(cudaStreamWaitEvent(s, ev_slab[k], 0));
+    }
   }
 };
 
@@ -882,12 +969,20 @@ struct moshpit_shard {
   std::unique_ptr<Shard> s;
 };
 
+namespace {
+
+void shard_require(moshpit_shard* h) {
+  if (!h || !h->s) throw std::invalid_argument("shard: null handle");
+}
+
+}  // namespace
+
 extern "C" {
 
-int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint64_t n,
-                         double p_round, std::uint64_t seed, std::uint64_t dim,
-                         std::int32_t rank, std::int32_t world, std::int32_t emulate,
-                         std::int32_t device, moshpit_shard** out) {
+int moshpit_shard_create_ex(int dtype, std::uint32_t M, std::uint32_t d, std::uint64_t n,
+                            double p_round, std::uint64_t seed, std::uint64_t dim,
+                            std::int32_t first_rank, std::int32_t ranks_here, std::int32_t world,
+                            std::int32_t slabs, std::int32_t device, moshpit_shard** out) {
   return guarded([&] {
     if (!out) throw std::invalid_argument("shard_create: null out");
     const std::size_t es = elem_size(dtype);
@@ -895,7 +990,11 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     if (p_round < 0.0 || p_round > 1.0)
       throw std::invalid_argument("FailureModel: p_round must be in [0,1]");
     if (world < 1 || world > kMaxWorld) throw std::invalid_argument("shard: world in [1, 8]");
-    if (rank < 0 || rank >= world) throw std::invalid_argument("shard: rank outside [0, world)");
+    if (ranks_here < 1 || world % ranks_here != 0)
+      throw std::invalid_argument("shard: ranks per process must divide world");
+    if (first_rank < 0 || first_rank % ranks_here != 0 || first_rank + ranks_here > world)
+      throw std::invalid_argument("shard: hosted ranks must be an aligned block of [0, world)");
+    if (slabs < 1 || slabs > kMaxSlabs) throw std::invalid_argument("shard: slabs in [1, 8]");
     if (M % (std::uint32_t)world != 0)
       throw std::invalid_argument("shard: the GPU count must divide M (split of grid digit d-1)");
     if (M > 32) throw std::invalid_argument("shard: groups larger than 32 are not sharded");
@@ -913,14 +1012,24 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     S.dim = dim;
     S.ld = padded_ld(dim, es);
     S.world = (std::uint32_t)world;
-    S.me = (std::uint32_t)rank;
-    S.emulate = emulate != 0;
+    S.me = (std::uint32_t)first_rank;
+    S.nhost = (std::uint32_t)ranks_here;
+    S.proc = S.me / S.nhost;
+    S.procs = S.world / S.nhost;
+    S.emulate = S.nhost == S.world;
     S.M = M;
     S.d = d;
     S.Mg = M / (std::uint32_t)world;
     S.R = cap / (std::uint64_t)world;
     S.p = p_round;
     if (const char* e = std::getenv("MOSHPIT_CROSS_CE")) S.ce = std::atoi(e) != 0;
+    const std::uint64_t nv = S.nvec();
+    S.S = (std::uint32_t)std::max<std::uint64_t>(1, std::min<std::uint64_t>(slabs, nv));
+    if (S.ce && S.S > 1) throw std::invalid_argument("shard: the copy-engine round needs slabs = 1");
+    for (std::uint32_t k = 0; k < S.S; ++k) {
+      S.vb[k] = nv * k / S.S;
+      S.ve[k] = nv * (k + 1) / S.S;
+    }
     S.plane = std::make_unique<Plane>(M, d, n, S.device);
     Xoshiro cells = Xoshiro::named(seed, "cells");
     S.fail = Xoshiro::named(seed, "failures");
@@ -931,31 +1040,33 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     init_loc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st.s>>>(
         S.plane->cellbuf.as<std::uint64_t>(), S.loc.as<std::uint32_t>(), n);
     MB_LAUNCH_CHECK();
-    S.rows_local.resize(n * 4);
-    S.act_local.resize((std::uint64_t)world * n * 4);
-    S.cnt_local.resize((std::uint64_t)world * 16 + 16);
-    S.src_row.resize(n * 4);
-    S.dst_row.resize(n * 4);
-    S.act_cross.resize(n * 4);
-    S.cnt_cross.resize(16);
-    S.moves.resize((std::uint64_t)world * S.R * 8);
-    S.n_moves.resize(world * 4 + 16);
+    S.plane->mark_done(st.s);
+    const std::uint32_t nslots = S.S == 1 ? 1 : S.S + 1;
+    for (std::uint32_t q = 0; q < nslots; ++q) {
+      S.ring.push_back(std::make_unique<TableSlot>());
+      S.alloc_slot(*S.ring.back());
+    }
+    if (S.S > 1) {
+      S.cs = std::make_unique<StreamHolder>();
+      for (std::uint32_t k = 0; k < S.S; ++k) {
+        S.ss[k] = std::make_unique<StreamHolder>();
+        MB_CUDA(cudaEventCreateWithFlags(&S.ev_slab[k], cudaEventDisableTiming));
+      }
+      MB_CUDA(cudaEventCreateWithFlags(&S.ev_user, cudaEventDisableTiming));
+    }
     S.err.resize(16);
     MB_CUDA(cudaMemsetAsync(S.err.ptr, 0, 16, st.s));
     S.totals.resize(8 * (2 * kMaxWorld + 2));
     MB_CUDA(cudaMemsetAsync(S.totals.ptr, 0, 8 * (2 * kMaxWorld + 2), st.s));
-    const std::uint32_t npools = S.emulate ? S.world : 1;
-    for (std::uint32_t k = 0; k < npools; ++k) {
+    for (std::uint32_t k = 0; k < S.nhost; ++k) {
       S.own_pools.push_back(std::make_unique<DeviceBuffer>(S.R * S.ld * es));
       MB_CUDA(cudaMemsetAsync(S.own_pools.back()->ptr, 0, S.R * S.ld * es, st.s));
+      S.pools[S.me + k] = S.own_pools.back()->ptr;
     }
-    S.staging.resize(npools);
-    if (S.emulate)
-      for (std::uint32_t k = 0; k < S.world; ++k) S.pools[k] = S.own_pools[k]->ptr;
-    else
-      S.pools[S.me] = S.own_pools[0]->ptr;
-    S.flags.resize(kMaxWorld * 8);
-    MB_CUDA(cudaMemsetAsync(S.flags.ptr, 0, kMaxWorld * 8, st.s));
+    if (p_round > 0.0)  // voided-row moves stage through here (one block per hosted rank)
+      S.staging = std::make_unique<DeviceBuffer>((std::uint64_t)S.nhost * S.R * S.ld * es);
+    S.flags.resize((std::uint64_t)kMaxSlabs * kMaxWorld * 8);
+    MB_CUDA(cudaMemsetAsync(S.flags.ptr, 0, (std::uint64_t)kMaxSlabs * kMaxWorld * 8, st.s));
     S.pool_tab.resize(kMaxWorld * 8);
     S.flag_tab.resize(kMaxWorld * 8);
     MB_CUDA(cudaMemcpyAsync(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice,
@@ -963,6 +1074,26 @@ int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint6
     MB_CUDA(cudaStreamSynchronize(st.s));
     *out = new moshpit_shard{std::move(sh)};
   });
+}
+
+int moshpit_shard_create(int dtype, std::uint32_t M, std::uint32_t d, std::uint64_t n,
+                         double p_round, std::uint64_t seed, std::uint64_t dim,
+                         std::int32_t rank, std::int32_t world, std::int32_t emulate,
+                         std::int32_t device, moshpit_shard** out) {
+  if (emulate) {
+    if (rank < 0 || rank >= world) {
+      g_last_error = "shard: rank outside [0, world)";
+      return MOSHPIT_ERR_INVALID_ARGUMENT;
+    }
+    return moshpit_shard_create_ex(dtype, M, d, n, p_round, seed, dim, 0, world, world, 1,
+                                   device, out);
+  }
+  if (rank < 0 || rank >= world) {
+    g_last_error = "shard: rank outside [0, world)";
+    return MOSHPIT_ERR_INVALID_ARGUMENT;
+  }
+  return moshpit_shard_create_ex(dtype, M, d, n, p_round, seed, dim, rank, 1, world, 1, device,
+                                 out);
 }
 
 int moshpit_shard_destroy(moshpit_shard* h) {
@@ -977,43 +1108,52 @@ int moshpit_shard_destroy(moshpit_shard* h) {
   });
 }
 
-// cudaIpcMemHandle_t of [pool, flags] (2 * 64 bytes) for the peers.
-int moshpit_shard_ipc_handles(moshpit_shard* h, void* out128) {
+// Per hosted rank r (in order): 128 bytes = cudaIpcMemHandle_t of rank r's
+// pool and of this process's barrier flags.  out: ranks_here * 128 bytes.
+int moshpit_shard_ipc_handles(moshpit_shard* h, void* out) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     if (S.emulate) throw std::invalid_argument("shard: emulation mode has no IPC handles");
     DeviceGuard g(S.device);
-    cudaIpcMemHandle_t a, b;
-    MB_CUDA(cudaIpcGetMemHandle(&a, S.own_pools[0]->ptr));
-    MB_CUDA(cudaIpcGetMemHandle(&b, S.flags.ptr));
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
-    std::memcpy(out128, &a, 64);
-    std::memcpy(static_cast<char*>(out128) + 64, &b, 64);
+    cudaIpcMemHandle_t fl;
+    MB_CUDA(cudaIpcGetMemHandle(&fl, S.flags.ptr));
+    for (std::uint32_t k = 0; k < S.nhost; ++k) {
+      cudaIpcMemHandle_t a;
+      MB_CUDA(cudaIpcGetMemHandle(&a, S.own_pools[k]->ptr));
+      std::memcpy(static_cast<char*>(out) + k * 128, &a, 64);
+      std::memcpy(static_cast<char*>(out) + k * 128 + 64, &fl, 64);
+    }
   });
 }
 
-// all: world * 128 bytes, rank-ordered handles from moshpit_shard_ipc_handles.
+// all: world * 128 bytes, rank-ordered entries from moshpit_shard_ipc_handles.
 int moshpit_shard_open_peers(moshpit_shard* h, const void* all) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     if (S.emulate) return;
     DeviceGuard g(S.device);
     for (std::uint32_t r = 0; r < S.world; ++r) {
-      if (r == S.me) {
-        S.peer_flags[r] = S.flags.as<unsigned long long>();
+      const std::uint32_t q = r / S.nhost;  // owning process
+      if (S.hosts(r)) {
+        S.peer_flags[q] = S.flags.as<unsigned long long>();
         continue;
       }
       cudaIpcMemHandle_t a, b;
       std::memcpy(&a, static_cast<const char*>(all) + r * 128, 64);
       std::memcpy(&b, static_cast<const char*>(all) + r * 128 + 64, 64);
       void* pa = nullptr;
-      void* pb = nullptr;
       MB_CUDA(cudaIpcOpenMemHandle(&pa, a, cudaIpcMemLazyEnablePeerAccess));
       S.opened.push_back(pa);
-      MB_CUDA(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess));
-      S.opened.push_back(pb);
       S.pools[r] = pa;
-      S.peer_flags[r] = static_cast<unsigned long long*>(pb);
+      if (r % S.nhost == 0) {  // one flags mapping per remote process
+        void* pb = nullptr;
+        MB_CUDA(cudaIpcOpenMemHandle(&pb, b, cudaIpcMemLazyEnablePeerAccess));
+        S.opened.push_back(pb);
+        S.peer_flags[q] = static_cast<unsigned long long*>(pb);
+      }
     }
     MB_CUDA(cudaMemcpy(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice));
     MB_CUDA(cudaMemcpy(S.flag_tab.ptr, S.peer_flags, sizeof(S.peer_flags),
@@ -1024,13 +1164,11 @@ int moshpit_shard_open_peers(moshpit_shard* h, const void* all) {
 
 int moshpit_shard_fill_synthetic(moshpit_shard* h, std::uint64_t seed, void* stream) {
   return guarded([&] {
-    if (!h || !h->s) throw std::invalid_argument("shard: null handle");
+    shard_require(h);
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     auto s = static_cast<cudaStream_t>(stream);
-    const std::uint32_t npools = S.emulate ? S.world : 1;
-    for (std::uint32_t k = 0; k < npools; ++k) {
-      const std::uint32_t r = S.emulate ? k : S.me;
+    for (std::uint32_t r = S.me; r < S.me + S.nhost; ++r) {
       if (S.dtype == MOSHPIT_F32)
         shard_fill_kernel<float><<<grid_cap(S.plane->n * S.dim), 256, 0, s>>>(
             static_cast<float*>(S.pools[r]), S.loc.as<std::uint32_t>(), S.plane->n, S.dim, S.ld,
@@ -1047,11 +1185,11 @@ int moshpit_shard_fill_synthetic(moshpit_shard* h, std::uint64_t seed, void* str
 int moshpit_shard_round(moshpit_shard* h, void* stream, std::uint32_t* active_out,
                         std::int32_t* crossed_out) {
   return guarded([&] {
-    if (!h || !h->s) throw std::invalid_argument("shard: null handle");
+    shard_require(h);
     Shard& S = *h->s;
     // without the peers' IPC mappings the cross round would dereference null
     // device pointers (a sticky CUDA fault); refuse instead
-    if (S.world > 1 && !S.emulate && !S.connected)
+    if (!S.emulate && S.procs > 1 && !S.connected)
       throw std::invalid_argument("shard: open_peers not called");
     DeviceGuard g(S.device);
     int crossed = 0;
@@ -1061,22 +1199,32 @@ int moshpit_shard_round(moshpit_shard* h, void* stream, std::uint32_t* active_ou
   });
 }
 
-// Copy the vectors of the peers resident on this rank (all, in emulation)
-// to host out[n*dim] by peer id; mask[p] = 1 where written.  Synchronises.
+// Slab pipeline: complete every round already issued on the lagging slabs and
+// order `stream` after them (a no-op with slabs = 1).
+int moshpit_shard_flush(moshpit_shard* h, void* stream) {
+  return guarded([&] {
+    shard_require(h);
+    Shard& S = *h->s;
+    DeviceGuard g(S.device);
+    S.flush(static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Copy the vectors of the peers resident on this process to host
+// out[n*dim] by peer id; mask[p] = 1 where written.  Flushes, synchronises.
 int moshpit_shard_read(moshpit_shard* h, void* out, std::uint8_t* mask) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     StreamHolder st;
+    if (S.S > 1) S.flush(st.s);
     const std::uint64_t n = S.plane->n;
     S.plane->sync_done();
     MB_CUDA(cudaDeviceSynchronize());
-    DeviceBuffer buf(n * S.dim * S.es + 16), m(n + 16), acc(n + 16);
-    MB_CUDA(cudaMemsetAsync(acc.ptr, 0, n, st.s));
+    DeviceBuffer buf(n * S.dim * S.es + 16), m(n + 16);
     std::vector<std::uint8_t> hm(n), tot(n, 0);
-    const std::uint32_t npools = S.emulate ? S.world : 1;
-    for (std::uint32_t k = 0; k < npools; ++k) {
-      const std::uint32_t r = S.emulate ? k : S.me;
+    for (std::uint32_t r = S.me; r < S.me + S.nhost; ++r) {
       if (S.dtype == MOSHPIT_F32)
         shard_gather_kernel<float><<<grid_cap(n * S.dim), 256, 0, st.s>>>(
             static_cast<float*>(S.pools[r]), S.loc.as<std::uint32_t>(), n, S.dim, S.ld, S.R, r,
@@ -1102,53 +1250,60 @@ int moshpit_shard_read(moshpit_shard* h, void* out, std::uint8_t* mask) {
 // Bracket the local-round and cross-round data-plane kernels with CUDA events.
 int moshpit_shard_set_timing(moshpit_shard* h, std::int32_t enable) {
   return guarded([&] {
+    shard_require(h);
     h->s->timing = enable != 0;
-    h->s->used_local = h->s->used_cross = 0;
+    h->s->tev_used = 0;
   });
 }
 
+// Summed device ms of the bracketed local / cross data planes since the last
+// call (with slabs > 1 the slabs overlap: sums can exceed the wall time).
 int moshpit_shard_kernel_time(moshpit_shard* h, double* local_ms, std::uint64_t* local_n,
                               double* cross_ms, std::uint64_t* cross_n) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     DeviceGuard g(S.device);
-    auto sum = [](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, std::size_t used) {
-      double t = 0;
-      for (std::size_t i = 0; i < used; ++i) {
-        MB_CUDA(cudaEventSynchronize(v[i].second));
-        float ms = 0;
-        MB_CUDA(cudaEventElapsedTime(&ms, v[i].first, v[i].second));
-        t += ms;
-      }
-      return t;
-    };
-    *local_ms = sum(S.tev_local, S.used_local);
-    *local_n = S.used_local;
-    *cross_ms = sum(S.tev_cross, S.used_cross);
-    *cross_n = S.used_cross;
-    // tev_cross alternates phase A, phase B of each cross round
-    S.last_a_ms = S.last_b_ms = 0.0;
-    for (std::size_t i = 0; i < S.used_cross; ++i) {
+    double lt = 0, a = 0, b = 0;
+    std::uint64_t ln = 0, cn = 0;
+    for (std::size_t i = 0; i < S.tev_used; ++i) {
+      MB_CUDA(cudaEventSynchronize(S.tev[i].b));
       float ms = 0;
-      MB_CUDA(cudaEventElapsedTime(&ms, S.tev_cross[i].first, S.tev_cross[i].second));
-      (i % 2 == 0 ? S.last_a_ms : S.last_b_ms) += ms;
+      MB_CUDA(cudaEventElapsedTime(&ms, S.tev[i].a, S.tev[i].b));
+      if (S.tev[i].kind == 0) {
+        lt += ms;
+        ++ln;
+      } else if (S.tev[i].kind == 1) {
+        a += ms;
+        ++cn;
+      } else {
+        b += ms;
+        ++cn;
+      }
     }
-    S.used_local = S.used_cross = 0;
+    *local_ms = lt;
+    *local_n = ln;
+    *cross_ms = a + b;
+    *cross_n = cn;
+    S.last_a_ms = a;
+    S.last_b_ms = b;
+    S.tev_used = 0;
   });
 }
 
 // Cumulative counters (synchronises): cross rounds, active groups summed over
-// cross rounds, and rows in non-voided local groups on rank `k` (this rank's
-// own index in real mode).
+// cross rounds, and rows in non-voided local groups on rank `k` (a hosted
+// rank; otherwise this process's first rank).
 int moshpit_shard_stats(moshpit_shard* h, std::int32_t k, std::uint64_t* cross_rounds,
                         std::uint64_t* cross_active_groups, std::uint64_t* local_active_rows) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     MB_CUDA(cudaDeviceSynchronize());
     unsigned long long t[2 * kMaxWorld + 2];
     MB_CUDA(cudaMemcpy(t, S.totals.ptr, sizeof(t), cudaMemcpyDeviceToHost));
-    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    const std::uint32_t r = S.hosts((std::uint32_t)k) ? (std::uint32_t)k : S.me;
     *cross_rounds = t[1];
     *cross_active_groups = t[0];
     *local_active_rows = t[2 + r];
@@ -1158,24 +1313,26 @@ int moshpit_shard_stats(moshpit_shard* h, std::int32_t k, std::uint64_t* cross_r
 int moshpit_shard_cross_detail(moshpit_shard* h, std::int32_t k, double* phase_a_ms,
                                double* phase_b_ms, std::uint64_t* moved_rows_in) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
     DeviceGuard g(S.device);
     MB_CUDA(cudaDeviceSynchronize());
     unsigned long long t[2 * kMaxWorld + 2];
     MB_CUDA(cudaMemcpy(t, S.totals.ptr, sizeof(t), cudaMemcpyDeviceToHost));
-    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    const std::uint32_t r = S.hosts((std::uint32_t)k) ? (std::uint32_t)k : S.me;
     *phase_a_ms = S.last_a_ms;
     *phase_b_ms = S.last_b_ms;
     *moved_rows_in = t[2 + kMaxWorld + r];
   });
 }
 
-// Device pointer / rows / stride of this rank's local pool (emulation: pool k).
+// Device pointer / rows / stride of hosted rank k's pool (else the first).
 int moshpit_shard_pool(moshpit_shard* h, std::int32_t k, void** ptr, std::uint64_t* rows,
                        std::uint64_t* ld) {
   return guarded([&] {
+    shard_require(h);
     Shard& S = *h->s;
-    const std::uint32_t r = S.emulate ? (std::uint32_t)k : S.me;
+    const std::uint32_t r = S.hosts((std::uint32_t)k) ? (std::uint32_t)k : S.me;
     *ptr = S.pools[r];
     *rows = S.R;
     *ld = S.ld;

@@ -133,3 +133,38 @@ def test_emulated_shards_copy_engine_path(mb, oracle, monkeypatch, M, d, p, R, d
     _, want = oracle.run_moshpit(M, d, init, p, 7, R)
     assert bits_equal(got, want)
     sh.close()
+
+
+@pytest.mark.parametrize("M,d,p,R,dim,world,slabs", [(32, 2, 0.01, 10, 1000, 2, 2),
+                                                     (8, 4, 0.05, 8, 333, 4, 4),
+                                                     (16, 3, 0.02, 6, 4099, 8, 3),
+                                                     (8, 2, 0.2, 7, 12, 8, 2),
+                                                     (32, 2, 0.0, 5, 9, 4, 8)])
+def test_emulated_slab_pipeline_matches_oracle(mb, oracle, M, d, p, R, dim, world, slabs):
+    """The slab pipeline (column slabs one round apart on their own streams,
+    round tables in a ring of slots; read() flushes the lagging slabs) is
+    bit-identical to the oracle."""
+    import torch
+    n = M ** d
+    sh = mb.Shard(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), dim, world=world,
+                  emulate=True, slabs=slabs)
+    sh.fill_synthetic(INIT_SEED)
+    for _ in range(R):
+        sh.round()
+    sh.flush()
+    torch.cuda.synchronize()
+    got, mask = sh.read()
+    assert mask.all()
+    init = oracle.init_state(INIT_SEED, n, dim, dtype=np.float32)
+    _, want = oracle.run_moshpit(M, d, init, p, 7, R)
+    assert bits_equal(got, want)
+    sh.close()
+
+
+def test_shard_round_refuses_without_peers(mb):
+    """Real mode (one rank per process, world > 1) without open_peers: an
+    InvalidArgument, never a device fault."""
+    sh = mb.Shard(mb.GridConfig(8, 2, 2), 64, mb.FailureModel(), mb.Rng(1), 4, rank=0, world=2)
+    with pytest.raises(mb.InvalidArgument):
+        sh.round()
+    sh.close()
