@@ -125,51 +125,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-class NvlinkCounters:
-    """NVLink hardware byte counters of one GPU through NVML (the same link
-    counters nvidia-smi nvlink reads): data payload RX/TX summed over all
-    links.  Read before and after a timed region; None where unsupported."""
-
-    FIELDS = (("rx_kib", 139), ("tx_kib", 138))  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_{RX,TX}
-
-    def __init__(self, cuda_index):
-        self.h = None
-        try:
-            import pynvml
-            import torch
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            bus = getattr(torch.cuda.get_device_properties(cuda_index), "pci_bus_id", None)
-            if bus:
-                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode()
-                                                              if isinstance(bus, str) else bus)
-            else:
-                self.h = pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
-        except Exception as exc:  # noqa: BLE001
-            self.err = str(exc)
-
-    def read(self):
-        if self.h is None:
-            return None
-        try:
-            vals = self.nv.nvmlDeviceGetFieldValues(
-                self.h, [(fid, 0xFFFFFFFF) for _, fid in self.FIELDS])
-            out = {}
-            for (name, _), v in zip(self.FIELDS, vals):
-                if v.nvmlReturn != 0:
-                    return None
-                out[name] = int(v.value.ullVal)
-            return out
-        except Exception:  # noqa: BLE001
-            return None
-
-    @staticmethod
-    def delta(a, b):
-        if not a or not b:
-            return None
-        return {k.replace("_kib", "_bytes"): (b[k] - a[k]) * 1024 for k in a}
-
-
 def load_traffic(kernel_name, cfg_name):
     """dram bytes per launch of the top kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -620,8 +575,6 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    nvc = NvlinkCounters(local) if (nvlink and world > 1) else None
-    n0 = nvc.read() if nvc else None
     sh.set_timing(True)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -631,7 +584,6 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     sh.flush()  # the lagging slabs finish their rounds inside the timed region
     ev1.record(stream)
     torch.cuda.synchronize()
-    n1 = nvc.read() if nvc else None
     t_ms = ev0.elapsed_time(ev1)
     lms, ln, cms, cn = sh.kernel_time()
     c1 = sh.stats()
@@ -660,28 +612,11 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     t_max, lmax, cmax, trl, trc, pa_max, pb_max, nvl_max, hbm_cross_ms = vals.tolist()
-    nvl_meas = None
-    dl = NvlinkCounters.delta(n0, n1)
-    if world > 1 and nvlink:
-        # per-rank hardware RX bytes over the timed rounds vs this rank's modelled ingress
-        mine = torch.tensor([float(dl["rx_bytes"]) if dl else -1.0,
-                             float(dl["tx_bytes"]) if dl else -1.0, nvl_cross],
-                            dtype=torch.float64, device="cuda")
-        allv = [torch.zeros_like(mine) for _ in range(world)]
-        dist.all_gather(allv, mine)
-        rows = [v.tolist() for v in allv]
-        if all(r[0] >= 0 for r in rows):
-            nvl_meas = {"source": "NVML NVLink data counters (NVML_FI_DEV_NVLINK_THROUGHPUT_"
-                                  "DATA_RX/TX, all links), read around the timed rounds",
-                        "rx_bytes_per_rank": [int(r[0]) for r in rows],
-                        "tx_bytes_per_rank": [int(r[1]) for r in rows],
-                        "modelled_ingress_bytes_per_rank": [int(r[2]) for r in rows],
-                        "rx_over_modelled": [round(r[0] / r[2], 4) if r[2] else None
-                                             for r in rows],
-                        "rx_gbs_during_cross_kernels": round(max(r[0] for r in rows) / 1e9
-                                                             / (cmax / 1e3), 1) if cmax else None}
-        else:
-            nvl_meas = {"unavailable": getattr(nvc, "err", "NVML field values not supported")}
+    # NVLink bytes are modelled here; the measured counterpart is the ncu
+    # nvlrx__bytes capture of the cross kernels (profiles/nvlink_ncu.py; NVML's
+    # NVLink throughput counters read N/A on this driver)
+    nvl_meas = {"source": "modelled (see profiles/ncu_summary.json nvlink entries for the "
+                          "ncu-measured nvlrx bytes of the same kernels)"} if nvlink else None
     sh.close()
     torch.cuda.empty_cache()
     value = N * D * es * steps / (t_max / 1e3) / 1e9

@@ -147,6 +147,26 @@ int moshpit_run_moshpit_rows(int dtype, uint32_t M, uint32_t d, uint32_t T,
  * workspace; call it before a long-lived worker thread goes idle. [GPU] */
 int moshpit_release_workspace(void);
 
+/* ---- one round over an externally formed group table  [GPU] -------------
+ * For callers that form groups themselves, e.g. the reference's contested
+ * matchmaking::form_groups / GroupFormation with FailStop injections
+ * (matchmaking.hpp:104-294, 325-333), which stays on the CPU: group g is
+ * members[group_off[g] .. group_off[g+1]) (row indices in the group's
+ * priority order = the reference's SealedGroup::members), void_flags[g] != 0
+ * voids it (inputs kept, allreduce.hpp:95-102); every other group's rows get
+ * the butterfly_allreduce mean (reference pairwise tree, allreduce.hpp:79-121).
+ * Groups must be non-empty and disjoint.  The device form is async on
+ * `stream` (state: n_rows x ld, 16-byte aligned); the host form copies in and
+ * out and synchronises. */
+int moshpit_round_from_groups(int dtype, void* state, uint64_t n_rows, uint64_t dim,
+                              uint64_t ld, const uint32_t* members,
+                              const uint32_t* group_off, uint64_t n_groups,
+                              const uint8_t* void_flags, void* stream);
+int moshpit_round_from_groups_host(int dtype, void* vectors, uint64_t n_rows,
+                                   uint64_t dim, const uint32_t* members,
+                                   const uint32_t* group_off, uint64_t n_groups,
+                                   const uint8_t* void_flags);
+
 /* ---- trial-batched run_moshpit (harness.hpp:157-280 sweeps)  [GPU] ------
  * `trials` independent protocols::run_moshpit calls in one batch: trial t
  * uses initial + t*n*dim and Rng(seeds[t]); reports are [trials] and

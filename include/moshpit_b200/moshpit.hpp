@@ -355,6 +355,31 @@ inline AllReduceOutcome butterfly_allreduce(const std::vector<ParamVector>& inpu
   return o;
 }
 
+// Extension: one whole round of butterfly_allreduce over
+// an externally formed group table -- e.g. the SealedGroups of the
+// reference's contested matchmaking::form_groups, which stays on the CPU --
+// in one GPU launch.  vectors[m] for every member m of groups[g] becomes the
+// group's mean unless group_failed[g] (then the group keeps its inputs, as
+// butterfly_allreduce with a failed member does).  Equal, bit for bit, to
+// calling butterfly_allreduce per group with uniform weights.
+inline void butterfly_round(std::vector<ParamVector>& vectors,
+                            const std::vector<matchmaking::SealedGroup>& groups,
+                            const std::vector<bool>& group_failed = {}) {
+  if (vectors.empty() || groups.empty()) return;
+  const std::size_t n = vectors.size(), dim = vectors.front().size();
+  std::vector<std::uint32_t> members, off{0};
+  std::vector<std::uint8_t> vf(groups.size(), 0);
+  for (std::size_t g = 0; g < groups.size(); ++g) {
+    for (PeerId m : groups[g].members) members.push_back(m);
+    off.push_back(static_cast<std::uint32_t>(members.size()));
+    if (g < group_failed.size()) vf[g] = group_failed[g] ? 1 : 0;
+  }
+  auto flat = b200::flatten(vectors, dim, "butterfly_allreduce");
+  b200::check(moshpit_round_from_groups_host(MOSHPIT_F64, flat.data(), n, dim, members.data(),
+                                             off.data(), groups.size(), vf.data()));
+  vectors = b200::unflatten(flat, n, dim);
+}
+
 }  // namespace allreduce
 
 namespace theory {

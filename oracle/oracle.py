@@ -96,6 +96,7 @@ class Checker:
             f("pairwise_sum", dbl, [vp, u64])
             f("group_mean", C.c_int, [vp, u64, u64, vp, vp])
             f("butterfly", C.c_int, [vp, u64, u64, vp, vp, vp, vp])
+            f("contested_round", C.c_int, [u64, u32, u32, u32, vp, u64, vp, vp, vp, vp, vp])
             f("distortion", dbl, [vp, u64, u64, vp])
             f("mean_of", C.c_int, [vp, u64, u64, vp])
             f("run_moshpit", C.c_int,
@@ -197,6 +198,22 @@ class Checker:
             _check(getattr(self, "_butterfly" + self._sfx(x.dtype))(
                 _p(x), n, dim, _p(f), _p(out), C.byref(done)), "butterfly")
         return out, bool(done.value)
+
+    def contested_round(self, trial_seed, x, nkeys=3, cap=0):
+        """The unmodified reference's contested form_groups (skewed arrivals,
+        FailStop) + butterfly_allreduce per sealed group (ref only):
+        returns (members, group_off, void_flags, vectors after the round)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, dim = x.shape
+        mem = np.zeros(n, dtype=np.uint32)
+        off = np.zeros(n + 1, dtype=np.uint32)
+        vf = np.zeros(n, dtype=np.uint8)
+        ng = C.c_uint32(0)
+        out = np.zeros_like(x)
+        _check(self._contested_round(trial_seed, n, nkeys, cap, _p(x), dim, _p(mem), _p(off),
+                                     C.byref(ng), _p(vf), _p(out)), "contested_round")
+        g = ng.value
+        return mem[:off[g]], off[:g + 1], vf[:g], out
 
     def distortion(self, peers, ref):
         x = np.ascontiguousarray(peers)

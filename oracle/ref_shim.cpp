@@ -165,6 +165,59 @@ int ref_butterfly(const double* inputs, std::uint64_t n, std::uint64_t dim,
   });
 }
 
+// One CONTESTED matchmaking round (matchmaking.hpp:104-294, form_groups
+// :325-333) with skewed arrivals and FailStop injections, drawn as in
+// test_matchmaking.cpp:153-181, followed by butterfly_allreduce of every
+// sealed group (allreduce.hpp:79-121) with failed = "the member fail-stopped
+// this round" (a group with any such member is void, protocols.hpp:162-170).
+// Outputs the group table (members in sealed priority order, offsets, void
+// flags) and the vectors after the round (peers in no group keep theirs).
+int ref_contested_round(std::uint64_t trial_seed, std::uint32_t n, std::uint32_t nkeys,
+                        std::uint32_t cap, const double* x, std::uint64_t dim,
+                        std::uint32_t* members, std::uint32_t* goff, std::uint32_t* n_groups,
+                        std::uint8_t* void_flags, double* out) {
+  using namespace matchmaking;
+  return guarded([&] {
+    auto stream = Rng(trial_seed).stream("trial");
+    std::vector<MatchPeer> peers;
+    for (std::uint32_t i = 0; i < n; ++i)
+      peers.push_back(MatchPeer{static_cast<PeerId>(i),
+                                GroupKey{{static_cast<std::uint32_t>(stream.below(nkeys))}},
+                                stream() >> 16, stream.below(3)});
+    std::vector<FailStop> failures;
+    const std::size_t n_failures = stream.below(n / 2 + 1);
+    std::vector<bool> dead(n, false);
+    for (std::size_t f = 0; f < n_failures; ++f) {
+      failures.push_back(FailStop{stream.below(8), static_cast<PeerId>(stream.below(n))});
+      dead[failures.back().peer] = true;
+    }
+    Dht dht(1000);
+    const auto result = form_groups(0, peers, dht, failures, cap ? 3 + 2 * (LogicalTime)n : 3,
+                                    cap ? cap : std::numeric_limits<std::uint32_t>::max());
+    auto v = rows_of(x, n, dim);
+    std::uint32_t k = 0, g = 0;
+    goff[0] = 0;
+    for (const auto& sg : result.groups) {
+      std::vector<ParamVector> in;
+      std::vector<bool> failed;
+      bool any = false;
+      for (PeerId m : sg.members) {
+        members[k++] = m;
+        in.push_back(v[m]);
+        failed.push_back(dead[m]);
+        any = any || dead[m];
+      }
+      const auto o = allreduce::butterfly_allreduce(
+          in, allreduce::PartitionWeights::uniform(in.size()), failed);
+      for (std::size_t q = 0; q < sg.members.size(); ++q) v[sg.members[q]] = o.vectors[q];
+      void_flags[g] = any ? 1 : 0;
+      goff[++g] = k;
+    }
+    *n_groups = g;
+    for (std::uint32_t i = 0; i < n; ++i) std::memcpy(out + i * dim, v[i].data(), dim * 8);
+  });
+}
+
 double ref_distortion(const double* peers, std::uint64_t n, std::uint64_t dim,
                       const double* ref) {
   return distortion(rows_of(peers, n, dim), ParamVector(ref, ref + dim));

@@ -364,6 +364,32 @@ def run_moshpit(grid: GridConfig, initial, failure: FailureModel, rng: Rng, roun
                        [int(a) for a in act[:rounds]], cost.value, final)
 
 
+def round_from_groups(state, members, group_off, void_flags=None, dim: Optional[int] = None,
+                      stream=None):
+    """One round over an externally formed group table:
+    ``state`` a CUDA tensor [n_rows, ld] averaged in place, or a host numpy
+    array [n_rows, dim] (copied in and out).  ``members``/``group_off`` as in
+    a CSR table of the groups in priority order; ``void_flags[g]`` voids g."""
+    mem = np.ascontiguousarray(members, dtype=np.uint32)
+    off = np.ascontiguousarray(group_off, dtype=np.uint32)
+    ng = max(len(off) - 1, 0)
+    vf = None if void_flags is None else np.ascontiguousarray(void_flags, dtype=np.uint8)
+    if isinstance(state, np.ndarray):
+        if not state.flags.c_contiguous or state.dtype not in (np.float32, np.float64):
+            raise InvalidArgument("round_from_groups: C-contiguous float32/float64 rows")
+        check(lib().moshpit_round_from_groups_host(_dtype_code(state.dtype), _p(state),
+                                                   state.shape[0], state.shape[1], _p(mem),
+                                                   _p(off), ng, _p(vf)))
+        return state
+    import torch
+    code, ptr, ld = _tensor_args(state)
+    s = stream if stream is not None else torch.cuda.current_stream(state.device)
+    check(lib().moshpit_round_from_groups(code, ptr, state.shape[0],
+                                          state.shape[1] if dim is None else dim, ld, _p(mem),
+                                          _p(off), ng, _p(vf), s.cuda_stream))
+    return state
+
+
 def trial_seed(seed_base: int, protocol: str, n: int, p: float, seed_index: int) -> int:
     """harness::trial_rng (harness.hpp:145-155) root seed."""
     return int(lib().moshpit_trial_seed(seed_base, protocol.encode(), n, p, seed_index))

@@ -56,6 +56,8 @@ PROTOTYPES = {
     "moshpit_rng_stream": (C.c_int, [u64, C.c_char_p, i64, P(RngState)]),
     "moshpit_rng_seeded": (C.c_int, [u64, P(RngState)]),
     "moshpit_release_workspace": (C.c_int, []),
+    "moshpit_round_from_groups": (C.c_int, [C.c_int, vp, u64, u64, u64, vp, vp, u64, vp, vp]),
+    "moshpit_round_from_groups_host": (C.c_int, [C.c_int, vp, u64, u64, vp, vp, u64, vp]),
     "moshpit_run_moshpit_rows": (C.c_int, [C.c_int, u32, u32, u32, P(C.c_void_p), u64, u64,
                                            C.c_double, u64, u32, C.c_int, P(C.c_double),
                                            vp, vp, vp, P(C.c_double)]),

@@ -453,9 +453,27 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, initial, dim * es, dim * es, n,
                               cudaMemcpyHostToDevice, st.s));
     const int exact = diag == MOSHPIT_DIAG_EXACT;
-    // record_round: the distortion (st) and colmean + drift (aux) only read
-    // the state, so they run side by side; the next round waits for both.
+    // record_round.  FAST: one pass gives the column means and the distortion
+    // chunk partials.  EXACT: the distortion j-chains (st) and colmean + drift
+    // (aux) only read the state, so they run side by side; the next round
+    // waits for both.
+    const std::uint64_t nch = (dim + diag_chunk() - 1) / diag_chunk();
     auto record = [&](double* dist_slot, double* drift_slot) {
+      if (!exact) {
+        if (dtype == MOSHPIT_F32)
+          launch_diag_pass<float>(d_x.as<float>(), n, ld, dim, d_ref.as<double>(),
+                                  drift_slot ? d_mean.as<double>() : nullptr,
+                                  d_part.as<double>(), nch, 0, st.s);
+        else
+          launch_diag_pass<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
+                                   drift_slot ? d_mean.as<double>() : nullptr,
+                                   d_part.as<double>(), nch, 0, st.s);
+        launch_fold_finish(d_part.as<double>(), n, nch, d_sq.as<double>(), dist_slot, st.s);
+        if (drift_slot)
+          launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part2.as<double>(),
+                       drift_slot, 0, st.s);
+        return;
+      }
       if (drift_slot) {
         MB_CUDA(cudaEventRecord(ev_fork, st.s));
         MB_CUDA(cudaStreamWaitEvent(aux.s, ev_fork, 0));
@@ -576,6 +594,120 @@ int moshpit_run_moshpit_rows(int dtype, std::uint32_t M, std::uint32_t d, std::u
                                               static_cast<std::uint32_t>(dim));
   });
 }
+
+// ---------------------------------------------------------------------------
+// one round over an externally formed group table (e.g. the reference's
+// contested form_groups, matchmaking.hpp:104-294 / 325-333): kernel 2 over
+// the table; voided groups (any member failed, allreduce.hpp:95-102) keep
+// their rows.  SURVEY 8f rank 4: the control plane stays on the CPU.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct GroupTable {
+  std::vector<std::uint32_t> tab;  // members | goff | act | counts(4)
+  std::uint32_t n_members = 0, n_groups = 0, max_group = 1;
+};
+
+GroupTable build_group_table(std::uint64_t n_rows, const std::uint32_t* members,
+                             const std::uint32_t* group_off, std::uint64_t n_groups,
+                             const std::uint8_t* void_flags) {
+  if (n_groups > 0x7fffffffull) throw std::invalid_argument("round_from_groups: too many groups");
+  if (n_groups && (!members || !group_off))
+    throw std::invalid_argument("round_from_groups: null table");
+  GroupTable t;
+  t.n_groups = static_cast<std::uint32_t>(n_groups);
+  if (n_groups && group_off[0] != 0)
+    throw std::invalid_argument("round_from_groups: group_off[0] must be 0");
+  const std::uint32_t m = n_groups ? group_off[n_groups] : 0;
+  t.n_members = m;
+  std::vector<std::uint8_t> seen(n_rows, 0);
+  std::uint32_t active = 0, rows = 0;
+  for (std::uint64_t g = 0; g < n_groups; ++g) {
+    if (group_off[g + 1] < group_off[g])
+      throw std::invalid_argument("round_from_groups: group_off must be non-decreasing");
+    if (group_off[g + 1] == group_off[g])
+      throw std::invalid_argument("butterfly_allreduce: empty group");
+    t.max_group = std::max(t.max_group, group_off[g + 1] - group_off[g]);
+  }
+  for (std::uint32_t k = 0; k < m; ++k) {
+    if (members[k] >= n_rows) throw std::out_of_range("round_from_groups: member outside rows");
+    if (seen[members[k]]++) throw std::invalid_argument("round_from_groups: a row in two groups");
+  }
+  t.tab.resize(m + (n_groups + 1) + n_groups + 4 + 4);
+  std::copy(members, members + m, t.tab.begin());
+  std::copy(group_off, group_off + n_groups + 1, t.tab.begin() + m);
+  std::uint32_t* act = t.tab.data() + m + n_groups + 1;
+  for (std::uint64_t g = 0; g < n_groups; ++g)
+    if (!(void_flags && void_flags[g])) {
+      act[active++] = static_cast<std::uint32_t>(g);
+      rows += group_off[g + 1] - group_off[g];
+    }
+  std::uint32_t* cnt = act + n_groups;
+  cnt[0] = t.n_groups;
+  cnt[1] = active;
+  cnt[2] = rows;
+  cnt[3] = 0;
+  return t;
+}
+
+void launch_table_round(int dtype, void* state, std::uint64_t dim, std::uint64_t ld,
+                        const GroupTable& t, cudaStream_t s) {
+  if (dim == 0 || t.n_groups == 0) return;
+  void* d_tab = nullptr;
+  MB_CUDA(cudaMallocAsync(&d_tab, t.tab.size() * 4, s));
+  MB_CUDA(cudaMemcpyAsync(d_tab, t.tab.data(), t.tab.size() * 4, cudaMemcpyHostToDevice, s));
+  const auto* dm = static_cast<const std::uint32_t*>(d_tab);
+  const std::uint32_t* goff = dm + t.n_members;
+  const std::uint32_t* act = goff + t.n_groups + 1;
+  const std::uint32_t* cnt = act + t.n_groups;
+  if (dtype == MOSHPIT_F32)
+    launch_group_mean<float>(static_cast<float*>(state), ld, dim, dm, goff, act, cnt,
+                             t.max_group, 0, s);
+  else
+    launch_group_mean<double>(static_cast<double*>(state), ld, dim, dm, goff, act, cnt,
+                              t.max_group, 0, s);
+  MB_CUDA(cudaFreeAsync(d_tab, s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int moshpit_round_from_groups(int dtype, void* state, std::uint64_t n_rows, std::uint64_t dim,
+                              std::uint64_t ld, const std::uint32_t* members,
+                              const std::uint32_t* group_off, std::uint64_t n_groups,
+                              const std::uint8_t* void_flags, void* stream) {
+  return guarded([&] {
+    elem_size(dtype);
+    if (state) check_state(dtype, state, dim, ld);
+    const GroupTable t = build_group_table(n_rows, members, group_off, n_groups, void_flags);
+    require_device();
+    launch_table_round(dtype, state, dim, ld, t, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int moshpit_round_from_groups_host(int dtype, void* vectors, std::uint64_t n_rows,
+                                   std::uint64_t dim, const std::uint32_t* members,
+                                   const std::uint32_t* group_off, std::uint64_t n_groups,
+                                   const std::uint8_t* void_flags) {
+  return guarded([&] {
+    const std::size_t es = elem_size(dtype);
+    const GroupTable t = build_group_table(n_rows, members, group_off, n_groups, void_flags);
+    if (dim == 0 || n_rows == 0 || t.n_groups == 0) return;
+    require_device();
+    StreamHolder st;
+    const std::uint64_t ld = padded_ld(dim, es);
+    DeviceBuffer d_x(n_rows * ld * es);
+    MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, vectors, dim * es, dim * es, n_rows,
+                              cudaMemcpyHostToDevice, st.s));
+    launch_table_round(dtype, d_x.ptr, dim, ld, t, st.s);
+    MB_CUDA(cudaMemcpy2DAsync(vectors, dim * es, d_x.ptr, ld * es, dim * es, n_rows,
+                              cudaMemcpyDeviceToHost, st.s));
+    MB_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+}  // extern "C"
 
 // ---------------------------------------------------------------------------
 // optimizer::detail::moshpit_average (optimizer.hpp:249-284) with host buffers
@@ -742,6 +874,17 @@ void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t 
                  double* dist_slot, double* drift_slot, cudaStream_t s) {
   const std::uint64_t n = e->plane->n;
   const int exact = e->diag == MOSHPIT_DIAG_EXACT;
+  if (!exact) {  // one pass: column means + distortion chunk partials
+    const std::uint64_t nch = (dim + diag_chunk() - 1) / diag_chunk();
+    launch_diag_pass<T>(x, n, ld, dim, e->ref.as<double>(),
+                        drift_slot ? e->mean.as<double>() : nullptr, e->part.as<double>(), nch, 0,
+                        s);
+    launch_fold_finish(e->part.as<double>(), n, nch, e->sq.as<double>(), dist_slot, s);
+    if (drift_slot)
+      launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
+                   drift_slot, 0, s);
+    return;
+  }
   if (drift_slot) {
     MB_CUDA(cudaEventRecord(e->ev_fork, s));
     MB_CUDA(cudaStreamWaitEvent(e->aux->s, e->ev_fork, 0));

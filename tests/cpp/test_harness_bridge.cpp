@@ -42,8 +42,61 @@ static bool same(const protocols::TrialReport& a, const protocols::TrialReport& 
          a.active_counts == b.active_counts && a.cost_units == b.cost_units;
 }
 
+// SURVEY 8f rank 4 in C++: the reference's contested matchmaking (skewed
+// arrivals + FailStop, matchmaking.hpp:104-294) forms the groups on the CPU;
+// the drop-in's butterfly_round averages all of them in one GPU launch; the
+// reference's butterfly_allreduce per sealed group is the expected result.
+static bool contested_round_case(std::uint64_t seed) {
+  using namespace matchmaking;
+  auto stream = Rng(seed).stream("trial");
+  const std::size_t n = 4 + stream.below(24), dim = 1 + stream.below(40);
+  std::vector<MatchPeer> peers;
+  for (std::size_t i = 0; i < n; ++i)
+    peers.push_back(MatchPeer{static_cast<PeerId>(i),
+                              GroupKey{{static_cast<std::uint32_t>(stream.below(3))}},
+                              stream() >> 16, stream.below(3)});
+  std::vector<FailStop> failures;
+  std::vector<bool> dead(n, false);
+  for (std::size_t f = stream.below(n / 2 + 1); f > 0; --f) {
+    failures.push_back(FailStop{stream.below(8), static_cast<PeerId>(stream.below(n))});
+    dead[failures.back().peer] = true;
+  }
+  Dht dht(1000);
+  const auto result = form_groups(0, peers, dht, failures);
+  std::vector<ParamVector> x(n);
+  for (auto& v : x) v = stream.normals(dim);
+  auto want = x;
+  std::vector<::moshpit_b200::matchmaking::SealedGroup> groups;
+  std::vector<bool> gfail;
+  for (const auto& sg : result.groups) {
+    std::vector<ParamVector> in;
+    std::vector<bool> failed;
+    bool any = false;
+    for (PeerId m : sg.members) {
+      in.push_back(x[m]);
+      failed.push_back(dead[m]);
+      any = any || dead[m];
+    }
+    const auto o = allreduce::butterfly_allreduce(
+        in, allreduce::PartitionWeights::uniform(in.size()), failed);
+    for (std::size_t q = 0; q < sg.members.size(); ++q) want[sg.members[q]] = o.vectors[q];
+    groups.push_back({sg.leader, sg.members});
+    gfail.push_back(any);
+  }
+  auto got = x;
+  ::moshpit_b200::allreduce::butterfly_round(got, groups, gfail);
+  for (std::size_t i = 0; i < n; ++i)
+    if (std::memcmp(got[i].data(), want[i].data(), dim * sizeof(double)) != 0) return false;
+  return true;
+}
+
 int main() {
   int pass = 0, fail = 0;
+  for (std::uint64_t s = 0; s < 40; ++s) {
+    const bool ok = contested_round_case(900 + s);
+    ok ? ++pass : ++fail;
+    if (!ok) std::printf("MISMATCH contested round seed=%llu\n", (unsigned long long)(900 + s));
+  }
   harness::ExperimentConfig cfg;
   cfg.grid = GridConfig{32, 2, 1};
   cfg.round_cap = 50;

@@ -89,4 +89,4 @@ def test_harness_run_trial_through_bridge_is_bit_identical():
         pytest.skip("bridge binary not built (needs the reference tree at build time)")
     r = subprocess.run([BRIDGE_BIN], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert r.stdout.strip().splitlines()[-1] == "PASS=18 FAIL=0"
+    assert r.stdout.strip().splitlines()[-1] == "PASS=58 FAIL=0"

@@ -517,3 +517,42 @@ def test_engine_device_report_equals_run_moshpit(mb, torch, f64, diag):
     assert bits_equal(np.array([init]), np.array([want.initial_distortion]))
     assert bits_equal(np.array(dist), np.array(want.distortion))
     assert bits_equal(np.array(drift), np.array(want.mean_drift))
+
+
+@pytest.mark.parametrize("trial", range(6))
+@pytest.mark.parametrize("cap", [0, 3])
+def test_round_from_contested_groups_matches_reference(mb, ref, oracle, torch, trial, cap):
+    """the unmodified reference's CONTESTED form_groups
+    (skewed arrivals + FailStop, matchmaking.hpp:104-294) feeds the GPU data
+    plane through moshpit_round_from_groups; the vectors after the round are
+    bit-identical to the reference's butterfly_allreduce per sealed group (fp64),
+    and the fp32 path to the fp32 restatement's butterfly."""
+    rng = np.random.default_rng(100 + trial)
+    n, dim = 6 + 5 * trial, 37
+    x = rng.random((n, dim))
+    mem, off, vf, want = ref.contested_round(1000 + trial, x, nkeys=3, cap=cap)
+    assert len(off) > 1
+    got = mb.round_from_groups(x.copy(), mem, off, vf)
+    assert bits_equal(got, want)
+    # device form, padded rows, fp32 vs the restatement group by group
+    x32 = x.astype(np.float32)
+    t = torch.zeros((n, 40), dtype=torch.float32, device="cuda")
+    t[:, :dim] = torch.from_numpy(x32).cuda()
+    mb.round_from_groups(t, mem, off, vf, dim=dim)
+    torch.cuda.synchronize()
+    want32 = x32.copy()
+    for g in range(len(off) - 1):
+        rows = mem[off[g]:off[g + 1]]
+        out, done = oracle.butterfly(x32[rows], failed=np.full(len(rows), vf[g], np.uint8))
+        want32[rows] = out
+    assert bits_equal(t[:, :dim].cpu().numpy(), want32)
+
+
+def test_round_from_groups_validates_like_the_reference(mb):
+    x = np.zeros((4, 3))
+    with pytest.raises(mb.InvalidArgument):  # empty group (allreduce.hpp:83)
+        mb.round_from_groups(x, [0, 1], [0, 0, 2])
+    with pytest.raises(mb.OutOfRange):
+        mb.round_from_groups(x, [0, 7], [0, 2])
+    with pytest.raises(mb.InvalidArgument):  # a row in two groups
+        mb.round_from_groups(x, [0, 1, 1], [0, 2, 3])
