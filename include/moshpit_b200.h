@@ -334,6 +334,11 @@ int moshpit_shard_destroy(moshpit_shard* s);
 int moshpit_shard_ipc_handles(moshpit_shard* s, void* out);
 /* world*128 bytes gathered in rank order; maps every peer's pool/flags. */
 int moshpit_shard_open_peers(moshpit_shard* s, const void* all_handles);
+/* PROFILING ONLY: take the other ranks' pools as device pointers of this
+ * process (peer access enabled) and disable the inter-rank barriers, so one
+ * process can run one rank's cross-round kernels under ncu (NVLink counters)
+ * without waiting on other GPUs.  The averages are not valid. */
+int moshpit_shard_probe_peers(moshpit_shard* s, void* const* pools_by_rank);
 /* slabs > 1: finish the lagging slabs' rounds and order `stream` after them
  * (the state is complete only after a flush; read() flushes). */
 int moshpit_shard_flush(moshpit_shard* s, void* stream);

@@ -110,6 +110,7 @@ PROTOTYPES = {
     "moshpit_shard_create_ex": (C.c_int, [C.c_int, u32, u32, u64, dbl, u64, u64, i32, i32, i32,
                                           i32, i32, P(vp)]),
     "moshpit_shard_flush": (C.c_int, [vp, vp]),
+    "moshpit_shard_probe_peers": (C.c_int, [vp, P(vp)]),
     "moshpit_shard_destroy": (C.c_int, [vp]),
     "moshpit_shard_ipc_handles": (C.c_int, [vp, vp]),
     "moshpit_shard_open_peers": (C.c_int, [vp, vp]),

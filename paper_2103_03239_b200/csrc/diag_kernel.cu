@@ -79,18 +79,31 @@ __global__ void __launch_bounds__(kExThreads)
   double a = 0.0;
   if (tid < P && p0 + tid < n && accumulate) a = acc[p0 + tid];
   const std::uint64_t ntiles = (dim + kExK - 1) / kExK;
+  // all of a producer thread's loads for a tile are issued before any use
+  // (the latency of one batch per tile, hidden behind the chains' tile)
   auto produce = [&](std::uint64_t t, int buf) {
     const std::uint64_t j0 = t * kExK;
-#pragma unroll 4
-    for (int e = tid - 32; e < P * kExK; e += kExProducers) {
+    constexpr int kE = P * kExK;
+    constexpr int kIt = (kE + kExProducers - 1) / kExProducers;
+    double xv[kIt], rv[kIt];
+#pragma unroll
+    for (int u = 0; u < kIt; ++u) {
+      const int e = tid - 32 + u * kExProducers;
       const int q = e / kExK, k = e % kExK;
       const std::uint64_t j = j0 + k, i = p0 + q;
-      double v = 0.0;  // padding adds +0.0 to a sum of squares: bit-neutral
-      if (j < dim && i < n) {
-        const double diff = __dsub_rn((double)x[i * ld + j], ref[j]);
-        v = __dmul_rn(diff, diff);
+      const bool ok = e < kE && j < dim && i < n;
+      // padding: (0 - 0)^2 = +0.0 added to a sum of squares is bit-neutral
+      xv[u] = ok ? (double)x[i * ld + j] : 0.0;
+      rv[u] = ok ? ref[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kIt; ++u) {
+      const int e = tid - 32 + u * kExProducers;
+      if (e < kE) {
+        const int q = e / kExK, k = e % kExK;
+        const double diff = __dsub_rn(xv[u], rv[u]);
+        sm_ex[(buf * P + q) * (kExK + 1) + k] = __dmul_rn(diff, diff);
       }
-      sm_ex[(buf * P + q) * (kExK + 1) + k] = v;
     }
   };
   if (tid >= 32 && ntiles) produce(0, 0);
@@ -136,17 +149,24 @@ __global__ void __launch_bounds__(kExThreads)
   const std::uint64_t ntiles = (dim + kExK - 1) / kExK;
   auto produce = [&](std::uint64_t t, int buf) {
     const std::uint64_t j0 = t * kExK;
-#pragma unroll 4
-    for (int k = tid - 32; k < kExK; k += kExProducers) {
+    constexpr int kIt = (kExK + kExProducers - 1) / kExProducers;
+    double mv[kIt], rv[kIt];
+#pragma unroll
+    for (int u = 0; u < kIt; ++u) {
+      const int k = tid - 32 + u * kExProducers;
       const std::uint64_t j = j0 + k;
-      double u = 0.0, v = 0.0;
-      if (j < dim) {
-        const double dm = __dsub_rn(mean[j], ref[j]);
-        u = __dmul_rn(dm, dm);
-        v = __dmul_rn(ref[j], ref[j]);
+      const bool ok = k < kExK && j < dim;
+      mv[u] = ok ? mean[j] : 0.0;
+      rv[u] = ok ? ref[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kIt; ++u) {
+      const int k = tid - 32 + u * kExProducers;
+      if (k < kExK) {
+        const double dm = __dsub_rn(mv[u], rv[u]);
+        sm_ex[(buf * 2 + 0) * (kExK + 1) + k] = __dmul_rn(dm, dm);
+        sm_ex[(buf * 2 + 1) * (kExK + 1) + k] = __dmul_rn(rv[u], rv[u]);
       }
-      sm_ex[(buf * 2 + 0) * (kExK + 1) + k] = u;
-      sm_ex[(buf * 2 + 1) * (kExK + 1) + k] = v;
     }
   };
   if (tid >= 32 && ntiles) produce(0, 0);

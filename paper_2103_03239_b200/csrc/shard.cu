@@ -545,6 +545,7 @@ struct Shard {
   int device = 0;
   bool emulate = false;    // nhost == world: no peers, no barriers
   bool connected = false;  // peers' pools/flags mapped (open_peers)
+  bool probe = false;      // profiling only: no inter-rank barriers (results invalid)
   std::uint32_t round_no = 0;
   // replicated per-trial state and the table ring
   DeviceBuffer loc, err, pool_tab, flag_tab, totals;
@@ -631,7 +632,7 @@ struct Shard {
   }
 
   void barrier(std::uint32_t k, cudaStream_t s) {
-    if (emulate || procs == 1) return;
+    if (emulate || procs == 1 || probe) return;
     ++epoch[k];
     peer_barrier_kernel<<<1, 32, 0, s>>>(flags.as<unsigned long long>(),
                                         flag_tab.as<unsigned long long* const>(), proc, procs,
@@ -1158,6 +1159,38 @@ int moshpit_shard_open_peers(moshpit_shard* h, const void* all) {
     MB_CUDA(cudaMemcpy(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice));
     MB_CUDA(cudaMemcpy(S.flag_tab.ptr, S.peer_flags, sizeof(S.peer_flags),
                        cudaMemcpyHostToDevice));
+    S.connected = true;
+  });
+}
+
+// Profiling harness (profiles/nvlink_ncu.py): map the other ranks' pools from
+// raw device pointers of THIS process (other GPUs, peer access enabled here)
+// instead of IPC handles, and switch the inter-rank barriers off, so that one
+// process can drive one rank's cross-round kernels under ncu without any
+// kernel waiting on another GPU.  The averages it computes are meaningless.
+int moshpit_shard_probe_peers(moshpit_shard* h, void* const* pools_by_rank) {
+  return guarded([&] {
+    shard_require(h);
+    Shard& S = *h->s;
+    if (S.emulate) throw std::invalid_argument("shard: emulation mode has no peers");
+    DeviceGuard g(S.device);
+    for (std::uint32_t r = 0; r < S.world; ++r) {
+      if (S.hosts(r)) continue;
+      cudaPointerAttributes a{};
+      MB_CUDA(cudaPointerGetAttributes(&a, pools_by_rank[r]));
+      if (a.type != cudaMemoryTypeDevice) throw std::invalid_argument("probe_peers: not device memory");
+      if (a.device != S.device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MB_CUDA(e);
+        cudaGetLastError();
+      }
+      S.pools[r] = pools_by_rank[r];
+    }
+    for (std::uint32_t q = 0; q < S.procs; ++q) S.peer_flags[q] = S.flags.as<unsigned long long>();
+    MB_CUDA(cudaMemcpy(S.pool_tab.ptr, S.pools, sizeof(S.pools), cudaMemcpyHostToDevice));
+    MB_CUDA(cudaMemcpy(S.flag_tab.ptr, S.peer_flags, sizeof(S.peer_flags),
+                       cudaMemcpyHostToDevice));
+    S.probe = true;
     S.connected = true;
   });
 }
