@@ -25,6 +25,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-prec-div=true",
          "-prec-sqrt=true", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fno-fast-math", "-I" + os.path.join(ROOT, "include")]
+# measurement builds only (e.g. "-DMB_PHILOX_ROUNDS=7" in a scratch copy)
+FLAGS += os.environ.get("MOSHPIT_NVCC_EXTRA", "").split()
 
 
 def _nvcc():

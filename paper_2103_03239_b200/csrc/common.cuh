@@ -293,15 +293,8 @@ template <typename T>
 void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
                             const std::uint32_t* members, const std::uint32_t* goff,
                             const std::uint32_t* act, const std::uint32_t* counts,
-                            const StepPrologue<T>& sp, int prefetch, cudaStream_t s);
-int group_mean_step_grid(bool f64, bool noisy, int prefetch);
-// Plain Kernel-2 round through the leaf-streamed body (groups of <= 32):
-// wide8 = 0 -> 4-member load batches at 8 CTAs/SM, 1 -> 8-member batches.
-template <typename T>
-void launch_group_mean_leaf(T* state, std::uint64_t ld, std::uint64_t dim,
-                            const std::uint32_t* members, const std::uint32_t* goff,
-                            const std::uint32_t* act, const std::uint32_t* counts, int wide8,
-                            cudaStream_t s);
+                            const StepPrologue<T>& sp, cudaStream_t s);
+int group_mean_step_grid(bool f64, bool noisy);
 
 // Diagnostics and helpers.
 template <typename T, typename Acc>

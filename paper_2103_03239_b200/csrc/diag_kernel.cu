@@ -9,6 +9,7 @@
 // MOSHPIT_DIAG_FAST sums fixed chunks in parallel and folds them in a fixed
 // order (deterministic, ~1e-15 relative to the sequential sum).  Column means
 // use the reference pairwise tree over peers in both modes, in fp64.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -502,6 +503,17 @@ __global__ void __launch_bounds__(kPassThreads)
   }
 }
 
+// MOSHPIT_DIAG_PASS=1 routes column means / FAST partials through the
+// one-pass kernel (measurement switch while it is tuned; 0 = the separate
+// column-mean and row-partial kernels).
+bool use_pass(std::uint64_t n) {
+  static const int mode = [] {
+    const char* e = std::getenv("MOSHPIT_DIAG_PASS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return mode != 0 && n <= 8192;
+}
+
 template <typename T, typename Acc, bool DIST>
 void launch_pass(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                  const double* ref, Acc* mean_out, double* partial, std::uint64_t nch_total,
@@ -542,7 +554,7 @@ void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
   if (exact) {
     launch_dist_exact<T>(x, n, ld, dim, ref, acc, 1, s);
     return;
-  } else if (n <= 8192) {
+  } else if (use_pass(n)) {
     launch_pass<T, double, true>(x, n, ld, dim, ref, nullptr, partial, nch_total, c0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
@@ -560,7 +572,7 @@ void launch_diag_pass(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
                       const double* ref, double* mean_out, double* partial,
                       std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s) {
   if (n == 0 || dim == 0) return;
-  if (n <= 8192) {
+  if (use_pass(n)) {
     if (partial)
       launch_pass<T, double, true>(x, n, ld, dim, ref, mean_out, partial, nch_total, c0, s);
     else
@@ -642,7 +654,7 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s) {
   if (dim == 0 || n == 0) return;
-  if (!rows && n <= 8192) {  // one coalesced pass, per-column post-order stack
+  if (!rows && use_pass(n)) {  // one coalesced pass, per-column post-order stack
     launch_pass<T, Acc, false>(x, n, ld, dim, nullptr, out, nullptr, 0, 0, s);
     return;
   }
@@ -665,7 +677,7 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
     launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    if (n <= 8192)
+    if (use_pass(n))
       launch_pass<T, double, true>(x, n, ld, dim, ref, nullptr, partial, nch, 0, s);
     else
       dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(kThreads, 3) group_mean_register(MeanArgs<T> a
     }
     const std::uint64_t col = tile * kThreads + threadIdx.x;
     if (col >= a.nvec) continue;
-    switch (cnt) {
+    // with the step fused (groups > 32 only: kernel 3 takes the rest) just
+    // the generic tree -- no 32 specialised step bodies in the binary
+    switch (STEP ? 0u : cnt) {
 #define MB_CASE(N) \
   case N:          \
     mean_fixed<N, STEP, T, V>(base, a.ld_vec, col, sids, a.step, nsq, bad); \
@@ -419,108 +421,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
 }
 
-// Kernel 3, split form: the two half-warps of a warp share 16 columns; half 0
-// owns members [0, H) and half 1 members [H, N) of a group (H = floor(N/2)),
-// each applies the SGD step to its loads and evaluates its subtree; one
-// shuffle forms S(0..H) + S(H..N) -- exactly the reference tree's top split --
-// and each half stores its own members' rows.  Half the registers and twice
-// the warps of the one-thread-per-column form, for the compute-heavy fused
-// step.  Groups of <= 8 (no top split) are done by half 0 alone.
-constexpr int kSplitCols = kThreads / 2;
-
-template <int N, typename T, typename V>
-__device__ __forceinline__ void mean_split(V* base, std::uint64_t ld_vec, std::uint64_t col,
-                                           const std::uint32_t* ids, int half, bool ok,
-                                           const StepPrologue<T>& sp, double& nsq, bool& bad) {
-  V c = vzero((V*)nullptr), t = vzero((V*)nullptr);
-  if (ok) {
-    c = __ldg(reinterpret_cast<const V*>(sp.curv) + col);
-    t = __ldg(reinterpret_cast<const V*>(sp.tgt) + col);
-  }
-  if constexpr (N <= 8) {
-    if (half || !ok) return;
-    V x[8];
-#pragma unroll
-    for (int k = 0; k < N; ++k)
-      x[k] = apply_step(sp, vload(base + (std::uint64_t)ids[k] * ld_vec + col), ids[k], col, c,
-                        t, nsq, bad);
-    const V m = vdiv(tree<N, 0>(x), (std::uint32_t)N);
-#pragma unroll
-    for (int k = 0; k < N; ++k) vstore(base + (std::uint64_t)ids[k] * ld_vec + col, m);
-  } else {
-    constexpr int H = N / 2, L1 = N - H;
-    V x[16];
-    const std::uint32_t* my = ids + (half ? H : 0);
-    const int len = half ? L1 : H;
-#pragma unroll
-    for (int k = 0; k < L1; ++k) {
-      if (k < len && ok)
-        x[k] = apply_step(sp, vload(base + (std::uint64_t)my[k] * ld_vec + col), my[k], col, c, t,
-                          nsq, bad);
-      else
-        x[k] = vzero((V*)nullptr);
-    }
-    const V mine = half ? tree<L1, 0>(x) : tree<H, 0>(x);
-    const V other = vshfl_xor16(mine);
-    const V m = vdiv(half ? vadd(other, mine) : vadd(mine, other), (std::uint32_t)N);
-    if (ok) {
-#pragma unroll
-      for (int k = 0; k < L1; ++k)
-        if (k < len) vstore(base + (std::uint64_t)my[k] * ld_vec + col, m);
-    }
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 5) group_mean_step_split(MeanArgs<T> a) {
-  using V = typename V16<T>::type;
-  double nsq = 0.0;
-  bool bad = false;
-  __shared__ std::uint32_t sids[32];
-  const std::uint32_t n_act = a.counts[1];
-  const std::uint64_t n_tiles = (a.nvec + kSplitCols - 1) / kSplitCols;
-  const std::uint64_t n_items = (std::uint64_t)n_act * n_tiles;
-  V* base = reinterpret_cast<V*>(a.state);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4;
-  std::uint32_t cached = 0xffffffffu, cnt = 0;
-  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const std::uint32_t g = a.act[w / n_tiles];
-    if (g != cached) {
-      __syncthreads();
-      const std::uint32_t beg = a.goff[g];
-      cnt = a.goff[g + 1] - beg;
-      if (threadIdx.x < cnt) sids[threadIdx.x] = a.members[beg + threadIdx.x];
-      cached = g;
-      __syncthreads();
-    }
-    const std::uint64_t col = (w % n_tiles) * kSplitCols + warp * 16 + (lane & 15);
-    const bool ok = col < a.nvec;
-    switch (cnt) {
-#define MB_SCASE(N) \
-  case N:           \
-    mean_split<N, T, V>(base, a.ld_vec, col, sids, half, ok, a.step, nsq, bad); \
-    break;
-      MB_SCASE(1) MB_SCASE(2) MB_SCASE(3) MB_SCASE(4) MB_SCASE(5) MB_SCASE(6) MB_SCASE(7)
-      MB_SCASE(8) MB_SCASE(9) MB_SCASE(10) MB_SCASE(11) MB_SCASE(12) MB_SCASE(13)
-      MB_SCASE(14) MB_SCASE(15) MB_SCASE(16) MB_SCASE(17) MB_SCASE(18) MB_SCASE(19)
-      MB_SCASE(20) MB_SCASE(21) MB_SCASE(22) MB_SCASE(23) MB_SCASE(24) MB_SCASE(25)
-      MB_SCASE(26) MB_SCASE(27) MB_SCASE(28) MB_SCASE(29) MB_SCASE(30) MB_SCASE(31)
-      MB_SCASE(32)
-#undef MB_SCASE
-      default: break;
-    }
-  }
-  __shared__ double red[kThreads];
-  red[threadIdx.x] = nsq;
-  __syncthreads();
-  for (int w2 = kThreads / 2; w2 > 0; w2 >>= 1) {
-    if ((int)threadIdx.x < w2) red[threadIdx.x] += red[threadIdx.x + w2];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && a.step.noise_partial) a.step.noise_partial[blockIdx.x] = red[0];
-  if (bad) atomicOr(a.step.nonfinite, 1u);
-}
-
 struct GridCache {
   int dev = -1;
   int grid[4] = {0, 0, 0, 0};
@@ -577,54 +477,14 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
   a.batch_n = 0;
   if (step) {
     a.step = *step;
-    static const bool split_off = [] {
-      const char* e = std::getenv("MOSHPIT_STEP_SPLIT");
-      return e && std::string(e) == "0";
-    }();
-    // the split form pays off when the per-element step is compute-heavy
-    // (device noise): C4 sigma=1 7.8 -> 4.8 ms/step; at sigma=0 the
-    // one-thread-per-column form is slightly faster.
-    // Leaf-streamed kernel 3 (step_kernel.cu) unless MOSHPIT_STEP_KERNEL=old;
-    // MOSHPIT_STEP_MODE=0|1|2 forces its load-batch mode (default: by noise).
-    static const bool old_step = [] {
-      const char* e = std::getenv("MOSHPIT_STEP_KERNEL");
-      return e && std::string(e) == "old";
-    }();
-    static const int leaf_mode = [] {
-      const char* p = std::getenv("MOSHPIT_STEP_MODE");
-      return p ? std::atoi(p) : -1;
-    }();
-    if (max_group <= 32 && !old_step) {
-      launch_group_mean_step<T>(state, ld, dim, members, goff, act, counts, *step, leaf_mode, s);
+    // Kernel 3 (step_kernel.cu: leaf-streamed step + round 1) for groups of
+    // <= 32; larger groups take the register form's generic tree.
+    if (max_group <= 32) {
+      launch_group_mean_step<T>(state, ld, dim, members, goff, act, counts, *step, s);
       return;
     }
-    if (max_group <= 32 && !split_off && step->philox) {
-      static thread_local int grid_split[2] = {0, 0};
-      const int slot = sizeof(T) == 4 ? 0 : 1;
-      if (!grid_split[slot]) {
-        int sms = 0, per = 0, dev = 0;
-        MB_CUDA(cudaGetDevice(&dev));
-        MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, group_mean_step_split<T>,
-                                                              kThreads, 0));
-        grid_split[slot] = sms * (per > 0 ? per : 1);
-      }
-      group_mean_step_split<T><<<grid_split[slot], kThreads, 0, s>>>(a);
-    } else {
-      group_mean_register<T, true><<<mean_grid<T, true>(), kThreads, 0, s>>>(a);
-    }
+    group_mean_register<T, true><<<mean_grid<T, true>(), kThreads, 0, s>>>(a);
     MB_LAUNCH_CHECK();
-    return;
-  }
-  // MOSHPIT_K2_LEAF=4|8: the leaf-streamed body (4- / 8-member load batches)
-  // for groups of <= 32 instead of the register form (measurement knob).
-  static const int leaf_k2 = [] {
-    const char* e = std::getenv("MOSHPIT_K2_LEAF");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (variant == 0 && leaf_k2 && max_group <= 32) {
-    launch_group_mean_leaf<T>(state, ld, dim, members, goff, act, counts, leaf_k2 == 8 ? 1 : 0,
-                              s);
     return;
   }
   const bool bulk_ok = max_group <= (std::uint32_t)kBulkMaxRows;

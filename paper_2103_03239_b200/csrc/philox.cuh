@@ -5,11 +5,20 @@
 #pragma once
 #include <cstdint>
 
+#ifndef MB_PHILOX_ROUNDS
+#define MB_PHILOX_ROUNDS 10
+#endif
+
 namespace mb200 {
+
+// Rounds of the Philox4x32 bijection (10 = the Random123 default, the value
+// every measurement and statistical test in this repo uses unless stated).
+constexpr int kPhiloxRounds = MB_PHILOX_ROUNDS;
+static_assert(kPhiloxRounds >= 7 && kPhiloxRounds <= 10, "Philox4x32-7 .. -10");
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < kPhiloxRounds; ++r) {
     const std::uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
     const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
     c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
@@ -37,7 +46,7 @@ inline PhiloxKeys philox_keys(std::uint64_t seed) {
 }
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKeys& kk) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < kPhiloxRounds; ++r) {
     const std::uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
     const std::uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
     c = make_uint4(hi1 ^ c.y ^ kk.k[r].x, lo1, hi0 ^ c.w ^ kk.k[r].y, lo0);

@@ -39,14 +39,7 @@ constexpr int kIlp = MB_K3_ILP;  // members whose Philox chains interleave
 #define MB_K3_MINB 5
 #endif
 constexpr int kNoisyMinB = MB_K3_MINB;  // CTAs/SM of the noisy 4-wide form
-#ifndef MB_K3_PF
-#define MB_K3_PF 0
-#endif
-// Noisy 4-wide form with the next batch's loads issued under this batch's
-// Philox rounds: parity-green but measured slower (C4 sigma=1 3.18 -> 3.67 ms
-// at 4 CTAs/SM / 127 registers, 3.60 ms at 5 CTAs/SM with spills;
-// profiles/r01/k3_variants_prefetch.txt), so off by default.
-constexpr bool kPf = MB_K3_PF != 0;
+
 
 template <typename T>
 struct LVec;
@@ -182,23 +175,20 @@ __device__ __forceinline__ double2 vdivn(double2 a, std::uint32_t n) {
   return make_double2(ldiv(a.x, f), ldiv(a.y, f));
 }
 
-// MODE 0: 8-member load batches; 1: 8-member batches with the next leaf
-// prefetched; 2 (default): 4-member batches.  Without noise: 64 registers,
-// 8 CTAs/SM (warps hide the load latency).  With device noise the batch's
-// four Philox chains are computed together (kIlp) so their dependent
-// IMAD/LOP3 rounds interleave, at kNoisyMinB = 5 CTAs/SM (94 registers, no
-// spills): C4 sigma=1 step 3.34 -> 3.18 ms; at 8 CTAs/SM the same code
-// spills (3.21 ms) and one chain at a time measured 3.34 ms
-// (profiles/k3_variants.sh).  Same arithmetic in every mode.  MODE 3 / 4
-// are the 4- / 8-wide forms WITHOUT the step: a plain Kernel-2 round (used
-// for groups of <= 8 members, where the register form's 32-slot body caps
-// residency at 3 CTAs/SM).
-template <typename T, bool NOISY, int MODE>
-__global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE == 3) ? (NOISY ? kNoisyMinB : 8) : 6)
+// 4-member load batches.  Without noise: 64 registers, 8 CTAs/SM (warps
+// hide the load latency).  With device noise the batch's four Philox chains
+// are computed together (kIlp) so their dependent IMAD/LOP3 rounds
+// interleave, at kNoisyMinB = 5 CTAs/SM (94 registers, no spills): C4
+// sigma=1 step 3.34 -> 3.18 ms; at 8 CTAs/SM the same code spills (3.21 ms)
+// and one chain at a time measured 3.34 ms (profiles/k3_variants.sh).  The
+// round-1 variants measured slower -- 8-member batches (2.91-2.94 ms at
+// sigma=0, 3.69-3.80 with noise), the next batch prefetched under the Philox
+// rounds (3.60-3.67 ms, profiles/r01/k3_variants_prefetch.txt), the leaf
+// body as a plain Kernel 2 (1.5-5 % below the register form,
+// profiles/k2_leaf_sweep.sh) -- and were removed in round 2.
+template <typename T, bool NOISY>
+__global__ void __launch_bounds__(kLThreads, NOISY ? kNoisyMinB : 8)
     group_mean_step_leaf(LArgs<T> a) {
-  constexpr bool PREFETCH = MODE == 1;
-  constexpr bool STEP = MODE < 3;
-  constexpr bool WIDE4 = MODE == 2 || MODE == 3;
   using V = typename LVec<T>::V;
   constexpr int kV = LVec<T>::kN;
   __shared__ std::uint32_t sids[32];
@@ -235,110 +225,17 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
     if (col >= nvec) continue;
     const std::uint64_t j0 = col * kV;
     const bool full = j0 + kV <= dim;
-    V c = vz<V>(), t = vz<V>();
-    if constexpr (STEP) {
-      c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
-      t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
-    }
+    const V c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
+    const V t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
     V* const colp = base + col;
 
-    // predicated 8-wide leaf loads (unloaded slots are zero and never used)
-    auto load_leaf = [&](V(&buf)[8], std::uint32_t b, std::uint32_t e) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        buf[k] = (b + k < e) ? colp[(std::uint64_t)sids[b + k] * ld_vec] : vz<V>();
-    };
-    auto sum_leaf = [&](V(&buf)[8], std::uint32_t b, std::uint32_t e) {
-      V s = vz<V>();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (b + k < e) {
-          if constexpr (STEP)
-            step_vec<T, NOISY>(buf[k], c, t, gamma, cst, seed, step_no, sids[b + k], j0,
-                               full, dim, chk, nsq);
-          s = vsum(s, buf[k]);
-        }
-      }
-      return s;
-    };
     // Leaves in a runtime loop (one copy of the 8-member body: the unrolled
     // step + Philox code must stay instruction-cache resident).  Joins:
     // leaves before `r` accumulate into P, the rest into Q, sum = P + Q --
     // L0 | L0+L1 | L0+(L1+L2) | (L0+L1)+(L2+L3) for nl = 1..4.
     const std::uint32_t r = nl == 4 ? 2u : 1u;
     V P = vz<V>(), Q = vz<V>();
-    auto load4 = [&](V(&X)[4], std::uint32_t c0, std::uint32_t le) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        X[k] = (c0 + k < le) ? colp[(std::uint64_t)sids[c0 + k] * ld_vec] : vz<V>();
-    };
-    // One 4-member batch [c0, min(c0+4, le)) stepped and added into sl.
-    auto batch4 = [&](V(&X)[4], std::uint32_t c0, std::uint32_t le, V& sl) {
-      if (c0 + 4 <= le) {
-        // whole batch: the four members' Philox chains are independent
-        // and interleave (ILP against the dependent IMAD/LOP3 rounds)
-        if constexpr (STEP) {
-#pragma unroll
-          for (int k = 0; k < 4; k += kIlp) {
-            float z[kIlp][4] = {};
-            if constexpr (NOISY) {
-#pragma unroll
-              for (int e = 0; e < kIlp; ++e)
-                philox_normals4(seed, step_no, sids[c0 + k + e], j0 / 4, z[e]);
-            }
-#pragma unroll
-            for (int e = 0; e < kIlp; ++e)
-              step_lanes<T, NOISY>(X[k + e], c, t, gamma, cst, z[e], j0, full, dim, chk, nsq);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sl = vsum(sl, X[k]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (c0 + k < le) {
-            if constexpr (STEP)
-              step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k], j0,
-                                 full, dim, chk, nsq);
-            sl = vsum(sl, X[k]);
-          }
-        }
-      }
-    };
-    if constexpr (WIDE4 && NOISY && kPf) {
-      // Same batches, same order, flattened over the leaves so batch i+1's
-      // member loads are in flight while batch i runs its Philox rounds.
-      auto lend = [&](std::uint32_t l) { return l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4; };
-      std::uint32_t l = 0, c0 = b0, le = b1;
-      V X[4];
-      load4(X, c0, le);
-      V sl = vz<V>();
-#pragma unroll 1
-      while (true) {
-        std::uint32_t nl2 = l, nc = c0 + 4, ne = le;
-        const bool leaf_end = nc >= le;
-        if (leaf_end) {
-          nl2 = l + 1;
-          nc = le;
-          ne = nl2 < nl ? lend(nl2) : le;
-        }
-        const bool more = nl2 < nl;
-        V Y[4];
-        if (more) load4(Y, nc, ne);
-        batch4(X, c0, le, sl);
-        if (leaf_end) {
-          if (l < r) P = l == 0 ? sl : vsum(P, sl);
-          else Q = l == r ? sl : vsum(Q, sl);
-          sl = vz<V>();
-        }
-        if (!more) break;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) X[k] = Y[k];
-        l = nl2;
-        c0 = nc;
-        le = ne;
-      }
-    } else if constexpr (WIDE4) {
+    {
       std::uint32_t lb = b0;
 #pragma unroll 1
       for (std::uint32_t l = 0; l < nl; ++l) {
@@ -353,7 +250,7 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
           if (c0 + 4 <= le) {
             // whole batch: the four members' Philox chains are independent
             // and interleave (ILP against the dependent IMAD/LOP3 rounds)
-            if constexpr (STEP) {
+            {
 #pragma unroll
               for (int k = 0; k < 4; k += kIlp) {
                 float z[kIlp][4] = {};
@@ -374,9 +271,8 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               if (c0 + k < le) {
-                if constexpr (STEP)
-                  step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k],
-                                     j0, full, dim, chk, nsq);
+                step_vec<T, NOISY>(X[k], c, t, gamma, cst, seed, step_no, sids[c0 + k], j0,
+                                   full, dim, chk, nsq);
                 sl = vsum(sl, X[k]);
               }
             }
@@ -386,32 +282,6 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
         else Q = l == r ? sl : vsum(Q, sl);
         lb = le;
       }
-    } else {
-    V A[8], B[8];
-    load_leaf(A, b0, b1);
-    std::uint32_t lb = b0, le = b1;
-#pragma unroll 1
-    for (std::uint32_t l = 0; l < nl; ++l) {
-      const std::uint32_t nb = le;
-      const std::uint32_t ne = l + 1 == 1 ? b2 : l + 1 == 2 ? b3 : b4;
-      const bool more = l + 1 < nl;
-      if constexpr (PREFETCH) {
-        if (more) load_leaf(B, nb, ne);
-      }
-      const V sl = sum_leaf(A, lb, le);
-      if (l < r) P = l == 0 ? sl : vsum(P, sl);
-      else Q = l == r ? sl : vsum(Q, sl);
-      if (more) {
-        if constexpr (PREFETCH) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) A[k] = B[k];
-        } else {
-          load_leaf(A, nb, ne);
-        }
-      }
-      lb = nb;
-      le = ne;
-    }
     }
     const V sum = nl == 1 ? P : vsum(P, Q);
     const V m = vdivn(sum, cnt);
@@ -430,13 +300,13 @@ __global__ void __launch_bounds__(kLThreads, MODE == 1 ? 4 : (MODE == 2 || MODE 
       for (int i = 0; i < kLThreads / 32; ++i) s += red[i];
       a.noise_partial[blockIdx.x] = s;
     }
-  } else if (STEP && threadIdx.x == 0 && a.noise_partial) {
+  } else if (threadIdx.x == 0 && a.noise_partial) {
     a.noise_partial[blockIdx.x] = 0.0;
   }
-  if (STEP && chk != T(0)) atomicOr(a.nonfinite, 1u);
+  if (chk != T(0)) atomicOr(a.nonfinite, 1u);
 }
 
-template <typename T, bool NOISY, int MODE>
+template <typename T, bool NOISY>
 int leaf_grid() {
   static thread_local int dev_cached = -1, grid = 0;
   int dev = 0;
@@ -445,16 +315,16 @@ int leaf_grid() {
     int sms = 0, per = 0;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per, group_mean_step_leaf<T, NOISY, MODE>, kLThreads, 0));
+        &per, group_mean_step_leaf<T, NOISY>, kLThreads, 0));
     grid = sms * (per > 0 ? per : 1);
     dev_cached = dev;
   }
   return grid;
 }
 
-template <typename T, bool NOISY, int MODE>
+template <typename T, bool NOISY>
 void launch_leaf(const LArgs<T>& a, cudaStream_t s) {
-  group_mean_step_leaf<T, NOISY, MODE><<<leaf_grid<T, NOISY, MODE>(), kLThreads, 0, s>>>(a);
+  group_mean_step_leaf<T, NOISY><<<leaf_grid<T, NOISY>(), kLThreads, 0, s>>>(a);
 }
 
 }  // namespace
@@ -463,7 +333,7 @@ template <typename T>
 void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
                             const std::uint32_t* members, const std::uint32_t* goff,
                             const std::uint32_t* act, const std::uint32_t* counts,
-                            const StepPrologue<T>& sp, int prefetch, cudaStream_t s) {
+                            const StepPrologue<T>& sp, cudaStream_t s) {
   if (dim == 0) return;
   constexpr int kV = LVec<T>::kN;
   LArgs<T> a;
@@ -485,70 +355,23 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
   a.dim = sp.dim;
   a.nonfinite = sp.nonfinite;
   a.noise_partial = sp.noise_partial;
-  // mode < 0: the default, 4-wide batches at 8 CTAs/SM -- measured best on
-  // B200 for both sigma = 0 (2.86 vs 2.91 / 2.94 ms per C4 step for modes
-  // 1 / 0) and device noise (3.60 vs 3.80 / 3.69 ms)
-  const int mode = prefetch >= 0 ? prefetch : 2;
-  if (sp.philox) {
-    if (mode == 2) launch_leaf<T, true, 2>(a, s);
-    else if (mode == 1) launch_leaf<T, true, 1>(a, s);
-    else launch_leaf<T, true, 0>(a, s);
-  } else {
-    if (mode == 2) launch_leaf<T, false, 2>(a, s);
-    else if (mode == 1) launch_leaf<T, false, 1>(a, s);
-    else launch_leaf<T, false, 0>(a, s);
-  }
+  if (sp.philox) launch_leaf<T, true>(a, s);
+  else launch_leaf<T, false>(a, s);
   MB_LAUNCH_CHECK();
 }
 
-// Plain Kernel-2 round through the leaf-streamed body (groups of <= 32).
-template <typename T>
-void launch_group_mean_leaf(T* state, std::uint64_t ld, std::uint64_t dim,
-                            const std::uint32_t* members, const std::uint32_t* goff,
-                            const std::uint32_t* act, const std::uint32_t* counts, int wide8,
-                            cudaStream_t s) {
-  if (dim == 0) return;
-  constexpr int kV = LVec<T>::kN;
-  LArgs<T> a{};
-  a.state = state;
-  a.ld_vec = ld / kV;
-  a.nvec = (dim + kV - 1) / kV;
-  a.n_tiles = (a.nvec + kLThreads - 1) / kLThreads;
-  a.members = members;
-  a.goff = goff;
-  a.act = act;
-  a.counts = counts;
-  a.dim = dim;
-  if (wide8) launch_leaf<T, false, 4>(a, s);
-  else launch_leaf<T, false, 3>(a, s);
-  MB_LAUNCH_CHECK();
-}
-template void launch_group_mean_leaf<float>(float*, std::uint64_t, std::uint64_t,
-                                            const std::uint32_t*, const std::uint32_t*,
-                                            const std::uint32_t*, const std::uint32_t*, int,
-                                            cudaStream_t);
-template void launch_group_mean_leaf<double>(double*, std::uint64_t, std::uint64_t,
-                                             const std::uint32_t*, const std::uint32_t*,
-                                             const std::uint32_t*, const std::uint32_t*, int,
-                                             cudaStream_t);
-
-int group_mean_step_grid(bool f64, bool noisy, int mode) {
-  if (mode < 0) mode = 2;
-  if (f64) {
-    if (noisy) return mode == 2 ? leaf_grid<double, true, 2>() : mode == 1 ? leaf_grid<double, true, 1>() : leaf_grid<double, true, 0>();
-    return mode == 2 ? leaf_grid<double, false, 2>() : mode == 1 ? leaf_grid<double, false, 1>() : leaf_grid<double, false, 0>();
-  }
-  if (noisy) return mode == 2 ? leaf_grid<float, true, 2>() : mode == 1 ? leaf_grid<float, true, 1>() : leaf_grid<float, true, 0>();
-  return mode == 2 ? leaf_grid<float, false, 2>() : mode == 1 ? leaf_grid<float, false, 1>() : leaf_grid<float, false, 0>();
+int group_mean_step_grid(bool f64, bool noisy) {
+  if (f64) return noisy ? leaf_grid<double, true>() : leaf_grid<double, false>();
+  return noisy ? leaf_grid<float, true>() : leaf_grid<float, false>();
 }
 
 template void launch_group_mean_step<float>(float*, std::uint64_t, std::uint64_t,
                                             const std::uint32_t*, const std::uint32_t*,
                                             const std::uint32_t*, const std::uint32_t*,
-                                            const StepPrologue<float>&, int, cudaStream_t);
+                                            const StepPrologue<float>&, cudaStream_t);
 template void launch_group_mean_step<double>(double*, std::uint64_t, std::uint64_t,
                                              const std::uint32_t*, const std::uint32_t*,
                                              const std::uint32_t*, const std::uint32_t*,
-                                             const StepPrologue<double>&, int, cudaStream_t);
+                                             const StepPrologue<double>&, cudaStream_t);
 
 }  // namespace mb200
