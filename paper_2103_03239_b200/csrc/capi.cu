@@ -453,27 +453,10 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     MB_CUDA(cudaMemcpy2DAsync(d_x.ptr, ld * es, initial, dim * es, dim * es, n,
                               cudaMemcpyHostToDevice, st.s));
     const int exact = diag == MOSHPIT_DIAG_EXACT;
-    // record_round.  FAST: one pass gives the column means and the distortion
-    // chunk partials.  EXACT: the distortion j-chains (st) and colmean + drift
-    // (aux) only read the state, so they run side by side; the next round
-    // waits for both.
-    const std::uint64_t nch = (dim + diag_chunk() - 1) / diag_chunk();
+    // record_round: the distortion (st; EXACT j-chains or FAST chunk
+    // partials) and colmean + drift (aux) only read the state, so they run
+    // side by side; the next round waits for both.
     auto record = [&](double* dist_slot, double* drift_slot) {
-      if (!exact) {
-        if (dtype == MOSHPIT_F32)
-          launch_diag_pass<float>(d_x.as<float>(), n, ld, dim, d_ref.as<double>(),
-                                  drift_slot ? d_mean.as<double>() : nullptr,
-                                  d_part.as<double>(), nch, 0, st.s);
-        else
-          launch_diag_pass<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
-                                   drift_slot ? d_mean.as<double>() : nullptr,
-                                   d_part.as<double>(), nch, 0, st.s);
-        launch_fold_finish(d_part.as<double>(), n, nch, d_sq.as<double>(), dist_slot, st.s);
-        if (drift_slot)
-          launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part2.as<double>(),
-                       drift_slot, 0, st.s);
-        return;
-      }
       if (drift_slot) {
         MB_CUDA(cudaEventRecord(ev_fork, st.s));
         MB_CUDA(cudaStreamWaitEvent(aux.s, ev_fork, 0));
@@ -874,17 +857,6 @@ void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t 
                  double* dist_slot, double* drift_slot, cudaStream_t s) {
   const std::uint64_t n = e->plane->n;
   const int exact = e->diag == MOSHPIT_DIAG_EXACT;
-  if (!exact) {  // one pass: column means + distortion chunk partials
-    const std::uint64_t nch = (dim + diag_chunk() - 1) / diag_chunk();
-    launch_diag_pass<T>(x, n, ld, dim, e->ref.as<double>(),
-                        drift_slot ? e->mean.as<double>() : nullptr, e->part.as<double>(), nch, 0,
-                        s);
-    launch_fold_finish(e->part.as<double>(), n, nch, e->sq.as<double>(), dist_slot, s);
-    if (drift_slot)
-      launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
-                   drift_slot, 0, s);
-    return;
-  }
   if (drift_slot) {
     MB_CUDA(cudaEventRecord(e->ev_fork, s));
     MB_CUDA(cudaStreamWaitEvent(e->aux->s, e->ev_fork, 0));

@@ -295,6 +295,8 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
                             const std::uint32_t* act, const std::uint32_t* counts,
                             const StepPrologue<T>& sp, cudaStream_t s);
 int group_mean_step_grid(bool f64, bool noisy);
+// Kernel-2 grid cap for launches from the calling thread (0 = every SM).
+void set_k2_grid_sms(int sms);
 
 // Diagnostics and helpers.
 template <typename T, typename Acc>
@@ -318,14 +320,6 @@ template <typename T>
 void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                       const double* ref, int exact, double* acc, double* partial,
                       std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s);
-// One pass over the state: column means (the reference tree over peers) into
-// mean_out, and with `partial` the FAST distortion chunk partials (offset c0).
-template <typename T>
-void launch_diag_pass(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
-                      const double* ref, double* mean_out, double* partial,
-                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s);
-void launch_fold_finish(const double* partial, std::uint64_t n, std::uint64_t nch, double* sq,
-                        double* out, cudaStream_t s);
 void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim, int exact,
                        double* acc2, double* partial, std::uint64_t c0, cudaStream_t s);
 void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, double* acc,

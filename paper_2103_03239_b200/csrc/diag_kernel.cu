@@ -9,11 +9,6 @@
 // MOSHPIT_DIAG_FAST sums fixed chunks in parallel and folds them in a fixed
 // order (deterministic, ~1e-15 relative to the sequential sum).  Column means
 // use the reference pairwise tree over peers in both modes, in fp64.
-#include <cstdlib>
-#include <map>
-#include <mutex>
-#include <vector>
-
 #include "common.cuh"
 #include "blocktree.cuh"
 #include "pairwise.cuh"
@@ -225,6 +220,7 @@ __global__ void dist_rows_fast(const T* __restrict__ x, std::uint64_t ld,
   const T* row = x + i * ld;
   const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
   double acc = 0.0;
+#pragma unroll 8
   for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
     const double diff = __dsub_rn((double)row[j], ref[j]);
     acc = __dadd_rn(acc, __dmul_rn(diff, diff));
@@ -335,6 +331,7 @@ __global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, st
   const T* row = x + i * ld;
   const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
   double acc = 0.0;
+#pragma unroll 8
   for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
     const double diff = __dsub_rn((double)row[j], ref[j]);
     acc = __dadd_rn(acc, __dmul_rn(diff, diff));
@@ -367,175 +364,6 @@ __global__ void drift_finish_acc(const double* __restrict__ acc2, double* __rest
   *out = __ddiv_rn(__dsqrt_rn(acc2[0]), fmax(__dsqrt_rn(acc2[1]), 1e-300));
 }
 
-// ---- one pass over the state: column means + FAST distortion partials ----
-// The column mean is the reference pairwise tree over the peers of a column
-// (core.hpp:72-81 via mean_of, core.hpp:128-133).  A CTA owns a chunk of
-// kChunk columns and walks it in sub-tiles of one column per thread; for each
-// sub-tile it streams the rows leaf by leaf in the tree's post-order (a
-// host-built program of (leaf length, merges after it)), keeping the partial
-// sums of the open tree nodes on a per-column stack in shared memory -- so
-// each element is read once, by coalesced row segments, and the sum is the
-// reference tree bit for bit.  With DIST the same pass stages each leaf's
-// squared differences (x - ref)^2 and reduces them per row (fixed order: lane
-// sums of 8, a shuffle tree, sub-tiles in order) into the FAST distortion
-// partial of (row, chunk).
-constexpr int kPassThreads = 256;
-constexpr int kTreeDepth = 12;  // post-order stack depth for n <= 8192
-
-std::vector<std::uint16_t> tree_program(std::uint32_t n) {
-  std::vector<std::uint16_t> prog;
-  // iterative post-order over (len) nodes; a node of <= 8 rows is a leaf
-  struct F {
-    std::uint32_t len;
-    int state;
-  };
-  std::vector<F> st{{n, 0}};
-  std::uint32_t pending_merges = 0;
-  while (!st.empty()) {
-    F& f = st.back();
-    if (f.len <= 8) {
-      prog.push_back((std::uint16_t)f.len);
-      st.pop_back();
-      continue;
-    }
-    if (f.state == 0) {
-      f.state = 1;
-      st.push_back({f.len / 2, 0});
-    } else if (f.state == 1) {
-      f.state = 2;
-      st.push_back({f.len - f.len / 2, 0});
-    } else {
-      prog.back() = (std::uint16_t)(prog.back() + 16);  // one more merge after the last leaf
-      st.pop_back();
-    }
-  }
-  (void)pending_merges;
-  return prog;
-}
-
-// Device copy of tree_program(n), cached per (device, n).
-const std::uint16_t* tree_program_dev(std::uint32_t n, std::uint32_t* nleaves) {
-  static std::mutex mu;
-  static std::map<std::pair<int, std::uint32_t>, std::pair<DeviceBuffer*, std::uint32_t>> cache;
-  int dev = 0;
-  MB_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> g(mu);
-  auto it = cache.find({dev, n});
-  if (it == cache.end()) {
-    const auto prog = tree_program(n);
-    auto* buf = new DeviceBuffer(prog.size() * 2 + 16);  // lives for the process
-    MB_CUDA(cudaMemcpy(buf->ptr, prog.data(), prog.size() * 2, cudaMemcpyHostToDevice));
-    it = cache.emplace(std::make_pair(dev, n), std::make_pair(buf, (std::uint32_t)prog.size()))
-             .first;
-  }
-  *nleaves = it->second.second;
-  return it->second.first->as<std::uint16_t>();
-}
-
-template <typename T, typename Acc, bool DIST>
-__global__ void __launch_bounds__(kPassThreads)
-    diag_pass_kernel(const T* __restrict__ x, std::uint32_t n, std::uint64_t ld,
-                     std::uint64_t dim, const std::uint16_t* __restrict__ prog,
-                     std::uint32_t nleaves, const double* __restrict__ ref,
-                     Acc* __restrict__ mean_out, double* __restrict__ partial,
-                     std::uint64_t nch_total, std::uint64_t c0) {
-  extern __shared__ double sm_pass[];
-  Acc* stk = reinterpret_cast<Acc*>(sm_pass);            // [kTreeDepth][256]
-  double* sq = sm_pass + kTreeDepth * kPassThreads;      // [8][256]   (DIST)
-  double* racc = sq + 8 * kPassThreads;                  // [n]        (DIST)
-  const int tid = threadIdx.x;
-  const std::uint64_t cb = (std::uint64_t)blockIdx.x * kChunk;
-  if (DIST) {
-    for (std::uint32_t i = tid; i < n; i += kPassThreads) racc[i] = 0.0;
-    __syncthreads();
-  }
-  for (std::uint64_t sub = 0; sub < kChunk && cb + sub < dim; sub += kPassThreads) {
-    const std::uint64_t j = cb + sub + tid;
-    const bool in = j < dim;
-    const T* col = x + (in ? j : 0);
-    const double r = (DIST && in) ? ref[j] : 0.0;
-    int sp = 0;
-    std::uint32_t row = 0;
-    for (std::uint32_t L = 0; L < nleaves; ++L) {
-      const std::uint32_t pg = prog[L];
-      const std::uint32_t len = pg & 15u, merges = pg >> 4;
-      T v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = (in && (std::uint32_t)q < len) ? col[(row + q) * ld] : T(0);
-      Acc s = Acc(0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if ((std::uint32_t)q < len) s = AccOps<Acc>::add(s, (Acc)v[q]);
-      if constexpr (DIST) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double dd = __dsub_rn((double)v[q], r);
-          sq[q * kPassThreads + tid] = in ? __dmul_rn(dd, dd) : 0.0;
-        }
-        __syncthreads();
-        const int w = tid >> 5, l = tid & 31;
-        if ((std::uint32_t)w < len) {
-          double a = 0.0;
-#pragma unroll
-          for (int k = 0; k < kPassThreads / 32; ++k) a = __dadd_rn(a, sq[w * kPassThreads + l + 32 * k]);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
-          if (l == 0) racc[row + w] = __dadd_rn(racc[row + w], a);
-        }
-        __syncthreads();
-      }
-      stk[sp * kPassThreads + tid] = s;
-      ++sp;
-      for (std::uint32_t m = 0; m < merges; ++m) {
-        const Acc b = stk[(sp - 1) * kPassThreads + tid];
-        const Acc a = stk[(sp - 2) * kPassThreads + tid];
-        stk[(sp - 2) * kPassThreads + tid] = AccOps<Acc>::add(a, b);
-        --sp;
-      }
-      row += len;
-    }
-    if (mean_out && in) mean_out[j] = AccOps<Acc>::div(stk[tid], (Acc)n);
-  }
-  if constexpr (DIST) {
-    __syncthreads();
-    for (std::uint32_t i = tid; i < n; i += kPassThreads)
-      partial[(std::uint64_t)i * nch_total + c0 + blockIdx.x] = racc[i];
-  }
-}
-
-// MOSHPIT_DIAG_PASS=1 routes column means / FAST partials through the
-// one-pass kernel (measurement switch while it is tuned; 0 = the separate
-// column-mean and row-partial kernels).
-bool use_pass(std::uint64_t n) {
-  static const int mode = [] {
-    const char* e = std::getenv("MOSHPIT_DIAG_PASS");
-    return e ? std::atoi(e) : 0;
-  }();
-  return mode != 0 && n <= 8192;
-}
-
-template <typename T, typename Acc, bool DIST>
-void launch_pass(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
-                 const double* ref, Acc* mean_out, double* partial, std::uint64_t nch_total,
-                 std::uint64_t c0, cudaStream_t s) {
-  std::uint32_t nleaves = 0;
-  const std::uint16_t* prog = tree_program_dev((std::uint32_t)n, &nleaves);
-  const std::size_t smem =
-      (std::size_t)kTreeDepth * kPassThreads * 8 + (DIST ? (8 * kPassThreads + n) * 8 : 0);
-  static int attr_dev = -1;
-  int dev = 0;
-  MB_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    MB_CUDA(cudaFuncSetAttribute(diag_pass_kernel<T, Acc, DIST>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    attr_dev = dev;
-  }
-  const unsigned blocks = (unsigned)((dim + kChunk - 1) / kChunk);
-  diag_pass_kernel<T, Acc, DIST><<<blocks, kPassThreads, smem, s>>>(
-      x, (std::uint32_t)n, ld, dim, prog, nleaves, ref, mean_out, partial, nch_total, c0);
-  MB_LAUNCH_CHECK();
-}
-
 unsigned grid_for(std::uint64_t work, unsigned threads) {
   std::uint64_t b = (work + threads - 1) / threads;
   if (b > 148ull * 64) b = 148ull * 64;
@@ -554,33 +382,12 @@ void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
   if (exact) {
     launch_dist_exact<T>(x, n, ld, dim, ref, acc, 1, s);
     return;
-  } else if (use_pass(n)) {
-    launch_pass<T, double, true>(x, n, ld, dim, ref, nullptr, partial, nch_total, c0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
         x, ld, dim, ref, nch_total, c0, partial);
   }
   MB_LAUNCH_CHECK();
-}
-
-// One pass: column means (reference tree) into mean_out and, with `partial`,
-// the FAST distortion partials at chunk offset c0 (n <= 8192; otherwise the
-// two separate kernels).
-template <typename T>
-void launch_diag_pass(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
-                      const double* ref, double* mean_out, double* partial,
-                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s) {
-  if (n == 0 || dim == 0) return;
-  if (use_pass(n)) {
-    if (partial)
-      launch_pass<T, double, true>(x, n, ld, dim, ref, mean_out, partial, nch_total, c0, s);
-    else
-      launch_pass<T, double, false>(x, n, ld, dim, nullptr, mean_out, nullptr, 0, 0, s);
-    return;
-  }
-  if (partial) launch_dist_slab<T>(x, n, ld, dim, ref, 0, nullptr, partial, nch_total, c0, s);
-  if (mean_out) launch_colmean<T, double>(x, n, ld, dim, nullptr, mean_out, s);
 }
 
 void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim, int exact,
@@ -593,21 +400,6 @@ void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim,
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     drift_fast_partial_off<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, c0, partial);
   }
-  MB_LAUNCH_CHECK();
-}
-
-// FAST distortion from chunk partials: fold per row in chunk order, then the
-// pairwise tree over peers / n.
-void launch_fold_finish(const double* partial, std::uint64_t n, std::uint64_t nch, double* sq,
-                        double* out, cudaStream_t s) {
-  if (n == 0) {
-    finish_distortion<<<1, kFinThreads, 0, s>>>(sq, 0, out);
-    MB_LAUNCH_CHECK();
-    return;
-  }
-  fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
-  MB_LAUNCH_CHECK();
-  finish_distortion<<<1, kFinThreads, 0, s>>>(sq, n, out);
   MB_LAUNCH_CHECK();
 }
 
@@ -630,12 +422,6 @@ void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, dou
   }
 }
 
-template void launch_diag_pass<float>(const float*, std::uint64_t, std::uint64_t, std::uint64_t,
-                                      const double*, double*, double*, std::uint64_t,
-                                      std::uint64_t, cudaStream_t);
-template void launch_diag_pass<double>(const double*, std::uint64_t, std::uint64_t,
-                                       std::uint64_t, const double*, double*, double*,
-                                       std::uint64_t, std::uint64_t, cudaStream_t);
 template void launch_dist_slab<float>(const float*, std::uint64_t, std::uint64_t, std::uint64_t,
                                       const double*, int, double*, double*, std::uint64_t,
                                       std::uint64_t, cudaStream_t);
@@ -654,10 +440,6 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s) {
   if (dim == 0 || n == 0) return;
-  if (!rows && use_pass(n)) {  // one coalesced pass, per-column post-order stack
-    launch_pass<T, Acc, false>(x, n, ld, dim, nullptr, out, nullptr, 0, 0, s);
-    return;
-  }
   const unsigned threads = 128;
   colmean_kernel<T, Acc><<<(unsigned)((dim + threads - 1) / threads), threads, 0, s>>>(
       x, n, ld, dim, rows, out);
@@ -677,11 +459,8 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
     launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    if (use_pass(n))
-      launch_pass<T, double, true>(x, n, ld, dim, ref, nullptr, partial, nch, 0, s);
-    else
-      dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
-          x, ld, dim, ref, nch, partial);
+    dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch, partial);
     MB_LAUNCH_CHECK();
     fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
   }

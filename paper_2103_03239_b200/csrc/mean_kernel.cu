@@ -421,6 +421,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
 }
 
+// Grid cap (in SMs' worth of CTAs) for kernel 2 launched from this thread; 0 =
+// every SM.  The peer-sharded slab pipeline lowers it while a cross round of
+// another slab shares the GPU.
+thread_local int t_k2_grid_sms = 0;
+
 struct GridCache {
   int dev = -1;
   int grid[4] = {0, 0, 0, 0};
@@ -455,6 +460,8 @@ bool bulk_default() {
 }
 
 }  // namespace
+
+void set_k2_grid_sms(int sms) { t_k2_grid_sms = sms; }
 
 template <typename T>
 void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
@@ -545,7 +552,8 @@ void launch_group_mean(T* state, std::uint64_t ld, std::uint64_t dim,
         fprintf(stderr, "[moshpit] kernel2 max_group=%u occ=%d per=%d pin=%zu grid=%d\n",
                 max_group, occ, per, pin, sms * per);
     }
-    group_mean_register<T, false><<<sms * per, kThreads, pin, s>>>(a);
+    const int gsms = t_k2_grid_sms > 0 && t_k2_grid_sms < sms ? t_k2_grid_sms : sms;
+    group_mean_register<T, false><<<gsms * per, kThreads, pin, s>>>(a);
   }
   MB_LAUNCH_CHECK();
 }

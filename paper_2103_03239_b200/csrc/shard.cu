@@ -546,6 +546,10 @@ struct Shard {
   bool emulate = false;    // nhost == world: no peers, no barriers
   bool connected = false;  // peers' pools/flags mapped (open_peers)
   bool probe = false;      // profiling only: no inter-rank barriers (results invalid)
+  // slab pipeline: SMs' worth of CTAs for the local (kernel 2) and cross
+  // kernels while they share the GPU (0 = all; MOSHPIT_PIPE_LOCAL_SMS /
+  // MOSHPIT_PIPE_CROSS_SMS)
+  int pipe_local_sms = 0, pipe_cross_sms = 0;
   std::uint32_t round_no = 0;
   // replicated per-trial state and the table ring
   DeviceBuffer loc, err, pool_tab, flag_tab, totals;
@@ -678,7 +682,9 @@ struct Shard {
       if (const char* e = std::getenv("MOSHPIT_CROSS_CTAS")) per = std::min(per, std::atoi(e));
       if (per < 1) per = 1;
     }
-    if (a.n_tiles) cross_mean_kernel<T><<<sm_count() * per, kCrossThreads, 0, s>>>(a);
+    int sms = sm_count();
+    if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
+    if (a.n_tiles) cross_mean_kernel<T><<<sms * per, kCrossThreads, 0, s>>>(a);
     MB_LAUNCH_CHECK();
   }
 
@@ -691,7 +697,9 @@ struct Shard {
       per = 8;
       if (const char* e = std::getenv("MOSHPIT_PULL_CTAS")) per = std::max(1, std::atoi(e));
     }
-    if (a.n_tiles) shard_pull_kernel<T><<<sm_count() * per, kCrossThreads, 0, s>>>(a);
+    int sms = sm_count();
+    if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
+    if (a.n_tiles) shard_pull_kernel<T><<<sms * per, kCrossThreads, 0, s>>>(a);
     MB_LAUNCH_CHECK();
   }
 
@@ -840,6 +848,7 @@ struct Shard {
       if (te) MB_CUDA(cudaEventRecord(te->a, s));
       const std::uint64_t kv = 16 / es;
       const std::uint64_t c0 = vb[k] * kv, c1 = std::min<std::uint64_t>(ve[k] * kv, dim);
+      if (S > 1) set_k2_grid_sms(pipe_local_sms);
       for (std::uint32_t r = me; r < me + nhost; ++r) {
         const std::uint32_t* act = t.act_local.as<std::uint32_t>() + (std::uint64_t)r * n();
         const std::uint32_t* cnt = t.cnt_local.as<std::uint32_t>() + r * 4;
@@ -853,6 +862,7 @@ struct Shard {
                                     t.rows_local.as<std::uint32_t>(), t.goff.as<std::uint32_t>(),
                                     act, cnt, M, 0, s);
       }
+      if (S > 1) set_k2_grid_sms(0);
       if (te) MB_CUDA(cudaEventRecord(te->b, s));
     } else {
       if (ce) ce_fetch_tables(t, s);
@@ -1027,6 +1037,8 @@ int moshpit_shard_create_ex(int dtype, std::uint32_t M, std::uint32_t d, std::ui
     const std::uint64_t nv = S.nvec();
     S.S = (std::uint32_t)std::max<std::uint64_t>(1, std::min<std::uint64_t>(slabs, nv));
     if (S.ce && S.S > 1) throw std::invalid_argument("shard: the copy-engine round needs slabs = 1");
+    if (const char* e = std::getenv("MOSHPIT_PIPE_LOCAL_SMS")) S.pipe_local_sms = std::atoi(e);
+    if (const char* e = std::getenv("MOSHPIT_PIPE_CROSS_SMS")) S.pipe_cross_sms = std::atoi(e);
     for (std::uint32_t k = 0; k < S.S; ++k) {
       S.vb[k] = nv * k / S.S;
       S.ve[k] = nv * (k + 1) / S.S;

@@ -287,13 +287,7 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src,
                            t_goff.as<std::uint32_t>() + r * (n + 1),
                            t_act.as<std::uint32_t>() + r * n, t_cnt.as<std::uint32_t>() + r * 4,
                            M, MOSHPIT_KERNEL_AUTO, s_cmp.s);
-      if (dg && !exact) {
-        // one pass: column means + distortion chunk partials, then the drift
-        launch_diag_pass<T>(x, n, W, w, refj, mean_s.as<double>(),
-                            rpart.as<double>() + (r + 1) * n * nch, nch, c0, s_cmp.s);
-        launch_drift_slab(mean_s.as<double>(), refj, w, exact, acc2.as<double>() + 2 * (r + 1),
-                          dpart.as<double>() + (r + 1) * 2 * nch, c0, s_cmp.s);
-      } else if (dg) {
+      if (dg) {
         // the distortion j-chains (s_cmp) and colmean + drift (s_aux) only
         // read the slab: run them side by side, join before the next round
         MB_CUDA(cudaEventRecord(ws.ev_fork, s_cmp.s));
