@@ -559,8 +559,8 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     axes 0..d-2 local, the axis d-1 round one fused NVLink kernel.  Returns
     the whole-problem metric (strong scaling) and the combined roofline."""
     M, d, N, D, p, Rcfg = CONFIGS[cfg]
-    if slabs is None:  # one slab per grid axis: at every step one slab crosses GPUs
-        slabs = int(os.environ.get("MOSHPIT_SHARD_SLABS", d if world > 1 else 1))
+    if slabs is None:  # slab pipeline: cross rounds of some slabs under local rounds of others
+        slabs = int(os.environ.get("MOSHPIT_SHARD_SLABS", 8 if world > 1 else 1))
     sh = mb.Shard(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED), D,
                   rank=rank, world=world, device=local, slabs=slabs)
     if world > 1:

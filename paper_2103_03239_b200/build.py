@@ -112,5 +112,36 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_host_tools(verbose=False):
+    """g++ of the host-side programs over the drop-in header: the drop-in
+    bench (bench.py's e2e_dropin_f64) and, where the reference tree is present
+    (the build container), the reference-harness bridge test binary -- both
+    travel to the GPU box with the snapshot."""
+    lib_dir = HERE
+    out = []
+    src = os.path.join(CSRC, "host", "bench_dropin.cpp")
+    exe = os.path.join(HERE, "bench_dropin")
+    cmd = ["g++", "-std=c++20", "-O2", "-pthread", src, "-I", os.path.join(ROOT, "include"),
+           "-L", lib_dir, "-lmoshpit_b200", "-Wl,-rpath,$ORIGIN", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, timeout=300)
+    out.append(exe)
+    ref_inc = "/root/reference/proj/include"
+    json_inc = os.path.join(sys.prefix, "lib", "python3.12", "site-packages", "include",
+                            "cudnn_frontend", "thirdparty", "nlohmann")
+    if os.path.isdir(os.path.join(ref_inc, "moshpit")) and os.path.exists(
+            os.path.join(json_inc, "json.hpp")):
+        src = os.path.join(ROOT, "tests", "cpp", "test_harness_bridge.cpp")
+        exe = os.path.join(ROOT, "tests", "cpp", "test_harness_bridge")
+        cmd = ["g++", "-std=c++20", "-O2", src, "-I", os.path.join(ROOT, "include"), "-I",
+               ref_inc, "-I", json_inc, "-L", lib_dir, "-lmoshpit_b200",
+               "-Wl,-rpath,$ORIGIN/../../paper_2103_03239_b200", "-o", exe]
+        subprocess.run(cmd, check=True, capture_output=True, timeout=300)
+        out.append(exe)
+    if verbose:
+        print("built", *out)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    build_host_tools(verbose=True)

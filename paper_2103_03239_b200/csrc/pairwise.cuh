@@ -23,16 +23,8 @@ __device__ V pairwise_rt(Load& ld, std::uint32_t n, Add add, V zero) {
     const int t = sp - 1;
     const std::uint32_t lo = f_lo[t], cnt = f_n[t];
     if (cnt <= 8) {
-      // the leaf's loads are issued together (up to 8 in flight), then added
-      // sequentially from +0 as the reference does
-      V v[8];
-#pragma unroll
-      for (std::uint32_t i = 0; i < 8; ++i)
-        if (i < cnt) v[i] = ld(lo + i);
       V s = zero;
-#pragma unroll
-      for (std::uint32_t i = 0; i < 8; ++i)
-        if (i < cnt) s = add(s, v[i]);
+      for (std::uint32_t i = 0; i < cnt; ++i) s = add(s, ld(lo + i));
       vals[vsp++] = s;
       --sp;
       continue;

@@ -1037,6 +1037,15 @@ int moshpit_shard_create_ex(int dtype, std::uint32_t M, std::uint32_t d, std::ui
     const std::uint64_t nv = S.nvec();
     S.S = (std::uint32_t)std::max<std::uint64_t>(1, std::min<std::uint64_t>(slabs, nv));
     if (S.ce && S.S > 1) throw std::invalid_argument("shard: the copy-engine round needs slabs = 1");
+    // measured on 2 and 4 B200s (C2, profiles/r02/pipe_sweep_*.txt): ~70 % of the
+    // SMs' worth of kernel-2 CTAs and ~30 % for the cross kernels beat
+    // uncapped grids (4080 vs 3570 GB/s at 2 GPUs, slabs = 4)
+    if (S.S > 1) {
+      int sms = 0;
+      MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, S.device));
+      S.pipe_local_sms = (sms * 104 + 74) / 148;
+      S.pipe_cross_sms = sms - S.pipe_local_sms;
+    }
     if (const char* e = std::getenv("MOSHPIT_PIPE_LOCAL_SMS")) S.pipe_local_sms = std::atoi(e);
     if (const char* e = std::getenv("MOSHPIT_PIPE_CROSS_SMS")) S.pipe_cross_sms = std::atoi(e);
     for (std::uint32_t k = 0; k < S.S; ++k) {
