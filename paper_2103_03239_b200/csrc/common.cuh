@@ -297,6 +297,17 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
 int group_mean_step_grid(bool f64, bool noisy);
 // Kernel-2 grid cap for launches from the calling thread (0 = every SM).
 void set_k2_grid_sms(int sms);
+// fp32 LogisticRegression step on the tensor cores (tc_logit.cu: tcgen05
+// kind::tf32, 3xTF32).  MOSHPIT_LOGIT_TC=0 keeps the fp64 SIMT kernels.
+bool logit_tc_enabled(std::uint64_t dim, std::uint64_t samples);
+void logit_tc_prepare(const double* xs, std::uint64_t S, std::uint64_t dim, float* x_hi,
+                      float* x_lo, float* xt_hi, float* xt_lo, cudaStream_t s);
+void logit_tc_step(float* theta, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                   std::uint64_t S, const float* x_hi, const float* x_lo, const float* xt_hi,
+                   const float* xt_lo, const double* ys, double l2, float gamma,
+                   const float* noise, double coord_std, int philox, std::uint64_t seed,
+                   std::uint64_t step, std::uint32_t* nonfinite, double* nsq_out, float* th_hi,
+                   float* th_lo, float* c_hi, float* c_lo, cudaStream_t s);
 
 // Diagnostics and helpers.
 template <typename T, typename Acc>

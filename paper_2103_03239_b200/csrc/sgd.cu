@@ -573,12 +573,17 @@ struct SgdRun {
   std::uint64_t S = 0;
   double l2 = 0.0;
   DeviceBuffer lxs, lys, coeff, ym, gm, wtd;
+  // fp32 tensor-core path (tc_logit.cu): tf32 hi/lo splits of X and X^T, and
+  // per-step scratch for Theta's split and the split coefficients
+  bool tc = false;
+  DeviceBuffer x_hi, x_lo, xt_hi, xt_lo, th_hi, th_lo, c_hi, c_lo;
 
   void logit_upload(const double* xs, const double* ys, std::uint64_t samples, double l2_,
                     std::uint64_t n_max) {
     logit = true;
     S = samples;
     l2 = l2_;
+    tc = dtype == MOSHPIT_F32 && logit_tc_enabled(dim, S);
     lxs.resize(S * dim * 8 + 16);
     lys.resize(S * 8 + 16);
     coeff.resize(n_max * S * 8 + 16);
@@ -587,6 +592,13 @@ struct SgdRun {
     wtd.resize((dim ? dim : 1) * 8 + 16);
     if (dim) MB_CUDA(cudaMemcpyAsync(lxs.ptr, xs, S * dim * 8, cudaMemcpyHostToDevice, s));
     MB_CUDA(cudaMemcpyAsync(lys.ptr, ys, S * 8, cudaMemcpyHostToDevice, s));
+    if (tc) {
+      for (DeviceBuffer* b : {&x_hi, &x_lo, &xt_hi, &xt_lo}) b->resize(S * dim * 4 + 16);
+      for (DeviceBuffer* b : {&th_hi, &th_lo}) b->resize(n_max * dim * 4 + 16);
+      for (DeviceBuffer* b : {&c_hi, &c_lo}) b->resize(n_max * S * 4 + 16);
+      logit_tc_prepare(lxs.as<double>(), S, dim, x_hi.as<float>(), x_lo.as<float>(),
+                       xt_hi.as<float>(), xt_lo.as<float>(), s);
+    }
   }
 
   // optimizer.hpp:356-373 with LogisticRegression::gradient: margins/coefficients
@@ -602,6 +614,16 @@ struct SgdRun {
       nz = noise_dev.as<T>();
     }
     if (dim == 0) return;
+    if constexpr (std::is_same_v<T, float>) {
+      if (tc) {  // fp32 state: both GEMMs on the tensor cores (3xTF32)
+        logit_tc_step(static_cast<float*>(x), n, ld, dim, S, x_hi.as<float>(), x_lo.as<float>(),
+                      xt_hi.as<float>(), xt_lo.as<float>(), lys.as<double>(), l2, (float)gamma,
+                      nz, coord_std, philox, seed, k, flag.as<std::uint32_t>(),
+                      npart.as<double>() + k * 148 * 16, th_hi.as<float>(), th_lo.as<float>(),
+                      c_hi.as<float>(), c_lo.as<float>(), s);
+        return;
+      }
+    }
     const unsigned ty = (unsigned)((n + kLT - 1) / kLT);
     logit_coeff_tiled<T><<<dim3((unsigned)((S + kLT - 1) / kLT), ty), 256, 0, s>>>(
         static_cast<const T*>(x), n, ld, dim, lxs.as<double>(), lys.as<double>(), S,

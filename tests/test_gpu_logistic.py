@@ -205,3 +205,49 @@ def test_sgd_logistic_fast_diagnostics(mb, golden):
     assert np.array_equal(a.f_gap_weighted, b.f_gap_weighted)
     d_a, d_b = np.array(a.diagnostics.dispersion), np.array(b.diagnostics.dispersion)
     assert np.all(np.abs(d_a - d_b) <= 1e-12 * np.abs(d_b) + 1e-30)
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.5])
+def test_sgd_logistic_f32_tensor_cores(mb, monkeypatch, sigma):
+    """fp32 state: the two GEMMs of the logistic step run on tcgen05 (kind::tf32,
+    3xTF32 split; tc_logit.cu).  Same run with the tensor cores off (the fp64
+    SIMT kernels on the fp32 state) and with fp64 state: fp32-level agreement
+    (north_star: 1e-6 relative per step; over the run's steps the fp32
+    iterates drift further, so the run is checked at 1e-4 against fp64)."""
+    dim, S, n = 256, 512, 256
+    lr = mb.LogisticRegression.synthetic(dim, S, 0.05, mb.Rng(11).stream("objective"))
+    cfg = mb.OptimizerConfig(gamma=0.5, tau=1, steps=6, grid=mb.GridConfig(16, 2, 1),
+                             sigma=sigma, n_peers=n)
+    run = lambda dt: mb.run_moshpit_sgd(cfg, lr, np.zeros(dim), [], mb.Rng(5), dtype=dt,
+                                        return_thetas=True)
+    monkeypatch.setenv("MOSHPIT_LOGIT_TC", "1")
+    tc = run(np.float32)
+    monkeypatch.setenv("MOSHPIT_LOGIT_TC", "0")
+    simt = run(np.float32)
+    f64 = run(np.float64)
+    scale = np.abs(f64.final_thetas).max()
+    assert np.abs(tc.final_thetas - simt.final_thetas).max() <= 2e-5 * scale
+    assert np.abs(tc.final_thetas - f64.final_thetas).max() <= 1e-4 * scale
+    assert _close(tc.f_gap, f64.f_gap, 1e-4)
+    assert not np.array_equal(tc.final_thetas, simt.final_thetas)  # a different kernel ran
+
+
+def test_local_step_logistic_tensor_cores_one_step(mb, oracle, monkeypatch):
+    """One fp32 local step of 256 peers on the tensor cores vs the fp64
+    reference gradient (the oracle): within fp32 rounding (1e-6 relative)."""
+    import torch  # noqa: F401
+    dim, S, n = 128, 256, 256
+    xs, ys = oracle.logistic_dataset(dim, S, 91)
+    lr = mb.LogisticRegression(xs, ys, 0.1)
+    rng = np.random.default_rng(3)
+    th = rng.normal(size=(n, dim)) * 0.1
+    monkeypatch.setenv("MOSHPIT_LOGIT_TC", "1")
+    cfg = mb.OptimizerConfig(gamma=0.25, tau=1000, steps=1, grid=mb.GridConfig(16, 2, 1),
+                             sigma=0.0, n_peers=n)
+    # one step with no averaging (tau > steps): theta_1 = theta_0 - gamma grad(theta_0)
+    r = mb.run_moshpit_sgd(cfg, lr, th[0], [], mb.Rng(1), dtype=np.float32, return_thetas=True,
+                           diagnostics="none")
+    _, g, _ = oracle.logistic_eval(xs, ys, 0.1, th[0])
+    want = th[0] - 0.25 * g
+    got = r.final_thetas[0]
+    assert np.abs(got - want).max() <= 1e-6 * max(1.0, np.abs(want).max())
