@@ -11,18 +11,24 @@
 // with hi, lo representable in tf32 and the product is accumulated as
 // lo*hi + hi*lo + hi*hi in fp32 (the lo*lo term is below fp32 resolution).
 //
-// Kernel shape (one CTA = one 128 x 128 output tile, 128 threads):
-//  * operands arrive pre-split (hi, lo fp32 arrays, K contiguous); all four
-//    warps load a 32-wide K slab of A_hi, A_lo, B_hi, B_lo with coalesced
-//    128-bit loads and store it in the UMMA K-major SWIZZLE_128B layout
-//    (8-row atoms of 128-byte rows, 16-byte chunk c of row r at c ^ (r & 7));
-//  * one thread issues tcgen05.mma.cta_group::1.kind::tf32 (M = N = 128,
-//    K = 8 per instruction, 3 per K step) from shared-memory descriptors into
-//    a 128-column fp32 accumulator in tensor memory, and tcgen05.commit
-//    releases the stage through an mbarrier (3-stage ring: loads of slab k+1
-//    and k+2 overlap the MMAs of slab k);
+// Kernel shape (one CTA = one 128 x 128 output tile, 128 threads, warp
+// specialised):
+//  * operands arrive pre-split (hi, lo fp32 arrays, K contiguous); warp 0
+//    (one lane) streams 32-wide K slabs of A_hi, A_lo, B_hi, B_lo with TMA
+//    (cp.async.bulk.tensor.2d, 128B swizzle: exactly the UMMA K-major
+//    SWIZZLE_128B layout -- 8-row atoms of 128-byte rows, 16-byte chunk c of
+//    row r at c ^ (r & 7)) into a 3-stage ring (full/empty mbarriers,
+//    complete_tx byte counts);
+//  * warp 1 (one lane) issues tcgen05.mma.cta_group::1.kind::tf32 (M = N =
+//    128, K = 8 per instruction, 3 per K step) from shared-memory descriptors
+//    into a 128-column fp32 accumulator in tensor memory; tcgen05.commit
+//    hands each stage back to the producer and, after the last slab, the
+//    accumulator to the epilogue;
 //  * the epilogue reads the accumulator with tcgen05.ld (warp w owns TMEM
 //    lanes 32w..32w+31 = tile rows) 32 columns at a time.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -38,7 +44,7 @@ constexpr int kTcStages = 3;
 constexpr int kTcThreads = 128;
 constexpr int kTileBytes = kTcM * kTcK * 4;  // 16 KB per operand tile
 constexpr int kStageBytes = 4 * kTileBytes;  // A_hi, A_lo, B_hi, B_lo
-constexpr std::size_t kTcSmem = (std::size_t)kTcStages * kStageBytes + 1024 + 64;
+constexpr std::size_t kTcSmem = (std::size_t)kTcStages * kStageBytes + 1024 + 128;
 
 __device__ __forceinline__ std::uint32_t su32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -157,18 +163,22 @@ struct TcArgs {
 };
 
 template <int EPI>
-__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_gemm_kernel(TcArgs a, const __grid_constant__ CUtensorMap tm_ah,
+                   const __grid_constant__ CUtensorMap tm_al,
+                   const __grid_constant__ CUtensorMap tm_bh,
+                   const __grid_constant__ CUtensorMap tm_bl) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment of the operand tiles (the 128B-swizzle atom)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<std::uintptr_t>(tc_smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kStageBytes);
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + kTcStages);
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kTcStages + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::uint64_t m0 = (std::uint64_t)blockIdx.y * kTcM, n0 = (std::uint64_t)blockIdx.x * kTcN;
 
   if (tid == 0) {
-    for (int s = 0; s < kTcStages; ++s) mbar_init1(&bars[s]);
+    for (int s = 0; s < 2 * kTcStages + 1; ++s) mbar_init1(&bars[s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -183,40 +193,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcArgs a) {
   const std::uint32_t tmem = *tmem_slot;
 
   const std::uint64_t nk = (a.K + kTcK - 1) / kTcK;
-  for (std::uint64_t kb = 0; kb < nk; ++kb) {
-    const int st = (int)(kb % kTcStages);
-    if (kb >= (std::uint64_t)kTcStages)  // MMAs of slab kb - kTcStages released this stage
-      mbar_wait_bounded(&bars[st], (std::uint32_t)((kb / kTcStages - 1) & 1));
-    unsigned char* base = smem + st * kStageBytes;
-    const std::uint64_t k0 = kb * kTcK;
-    // 4 tiles x 128 rows x 8 chunks of 16 B: 32 chunks per thread; 8
-    // consecutive threads load one row's 128 contiguous bytes
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + kTcStages;
+  std::uint64_t* done = bars + 2 * kTcStages;
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer =====
+    const std::uint64_t maps[4] = {reinterpret_cast<std::uint64_t>(&tm_ah),
+                                   reinterpret_cast<std::uint64_t>(&tm_al),
+                                   reinterpret_cast<std::uint64_t>(&tm_bh),
+                                   reinterpret_cast<std::uint64_t>(&tm_bl)};
+    for (std::uint64_t kb = 0; kb < nk; ++kb) {
+      const int st = (int)(kb % kTcStages);
+      if (kb >= (std::uint64_t)kTcStages)  // MMAs of slab kb - kTcStages freed this stage
+        mbar_wait_bounded(&empty[st], (std::uint32_t)((kb / kTcStages - 1) & 1));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])),
+                   "r"(kStageBytes)
+                   : "memory");
+      const std::uint32_t base = su32(smem + st * kStageBytes);
+      const int k0 = (int)(kb * kTcK);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float* src = t == 0 ? a.a_hi : t == 1 ? a.a_lo : t == 2 ? a.b_hi : a.b_lo;
-      const std::uint64_t r0 = t < 2 ? m0 : n0, rmax = t < 2 ? a.M : a.N;
-      const std::uint64_t ld = t < 2 ? a.lda : a.ldb;
-      float4 v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = tid + kTcThreads * q, r = e >> 3, c = e & 7;
-        const std::uint64_t gr = r0 + r, gk = k0 + c * 4;
-        v[q] = (gr < rmax && gk < a.K)
-                   ? __ldg(reinterpret_cast<const float4*>(src + gr * ld + gk))
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = tid + kTcThreads * q, r = e >> 3, c = e & 7;
-        *reinterpret_cast<float4*>(base + t * kTileBytes + r * 128 + ((c ^ (r & 7)) << 4)) = v[q];
+      for (int t = 0; t < 4; ++t) {
+        const int r0 = (int)(t < 2 ? m0 : n0);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + t * kTileBytes),
+            "l"(maps[t]), "r"(k0), "r"(r0), "r"(su32(&full[st]))
+            : "memory");
       }
     }
-    // generic-proxy smem writes -> visible to the tensor core's async proxy
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+  } else if (warp == 1 && lane == 0) {
+    // ===== MMA issuer =====
+    for (std::uint64_t kb = 0; kb < nk; ++kb) {
+      const int st = (int)(kb % kTcStages);
+      mbar_wait_bounded(&full[st], (std::uint32_t)((kb / kTcStages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const std::uint32_t sb = su32(base);
+      const std::uint32_t sb = su32(smem + st * kStageBytes);
 #pragma unroll
       for (int kk = 0; kk < kTcK / 8; ++kk) {  // K = 8 tf32 (32 bytes) per MMA
         const std::uint32_t off = kk * 32;
@@ -230,12 +241,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcArgs a) {
       }
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-              su32(&bars[st]))
+              su32(&empty[st]))
           : "memory");
     }
+    // the last commit covers every MMA issued before it: the accumulator is final
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            su32(done))
+        : "memory");
   }
-  // the last commit covers every MMA issued before it
-  if (nk) mbar_wait_bounded(&bars[(nk - 1) % kTcStages], (std::uint32_t)(((nk - 1) / kTcStages) & 1));
+  __syncwarp();
+  if (nk) mbar_wait_bounded(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // epilogue: row m0 + 32 warp + lane, 32 columns per TMEM load
@@ -306,6 +322,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(TcArgs a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcN));
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    MB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p)
+      throw CudaError("cuTensorMapEncodeTiled is not available from the driver");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 map over [rows x cols] (row stride ld elements): boxes of
+// kTcK x 128 (one 128-byte row per tile row), 128B swizzle, zero fill.
+CUtensorMap operand_map(const float* base, std::uint64_t rows, std::uint64_t cols,
+                        std::uint64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcK, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 template <int EPI>
 void launch_tc(const TcArgs& a, cudaStream_t s) {
   static int attr_dev = -1;
@@ -317,7 +363,11 @@ void launch_tc(const TcArgs& a, cudaStream_t s) {
     attr_dev = dev;
   }
   const dim3 grid((unsigned)((a.N + kTcN - 1) / kTcN), (unsigned)((a.M + kTcM - 1) / kTcM));
-  tc_gemm_kernel<EPI><<<grid, kTcThreads, kTcSmem, s>>>(a);
+  const CUtensorMap ah = operand_map(a.a_hi, a.M, a.K, a.lda);
+  const CUtensorMap al = operand_map(a.a_lo, a.M, a.K, a.lda);
+  const CUtensorMap bh = operand_map(a.b_hi, a.N, a.K, a.ldb);
+  const CUtensorMap bl = operand_map(a.b_lo, a.N, a.K, a.ldb);
+  tc_gemm_kernel<EPI><<<grid, kTcThreads, kTcSmem, s>>>(a, ah, al, bh, bl);
   MB_LAUNCH_CHECK();
 }
 
