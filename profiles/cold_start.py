@@ -15,9 +15,19 @@ from paper_2103_03239_b200 import _capi  # noqa: E402
 
 lib = _capi.lib()
 t_load = time.perf_counter() - t0
+# the driver's share: cuInit + primary context of device 0 (what any CUDA
+# program pays before its first kernel), timed through libcuda directly
+cu = C.CDLL("libcuda.so.1")
+t1 = time.perf_counter()
+cu.cuInit(0)
+dev, ctx = C.c_int(0), C.c_void_p()
+cu.cuDeviceGet(C.byref(dev), 0)
+cu.cuDevicePrimaryCtxRetain(C.byref(ctx), dev)
+t_ctx = time.perf_counter() - t1
 n, dim, R = 1024, 1, 50
 x = np.random.default_rng(0).random((n, dim))
-out = {"lib_bytes": os.path.getsize(_capi.LIB_PATH), "load_s": round(t_load, 4)}
+out = {"lib_bytes": os.path.getsize(_capi.LIB_PATH), "load_s": round(t_load, 4),
+       "cuda_primary_context_s": round(t_ctx, 4)}
 for k in ("first_call_s", "second_call_s", "third_call_s"):
     dist, drift = np.zeros(R), np.zeros(R)
     act = np.zeros(R, dtype=np.uint32)

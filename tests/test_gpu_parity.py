@@ -556,3 +556,20 @@ def test_round_from_groups_validates_like_the_reference(mb):
         mb.round_from_groups(x, [0, 7], [0, 2])
     with pytest.raises(mb.InvalidArgument):  # a row in two groups
         mb.round_from_groups(x, [0, 1, 1], [0, 2, 3])
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 16, 17, 31, 100, 255, 256, 257, 777, 1000, 1024,
+                               1025])
+def test_column_means_tiled_equal_reference(mb, ref, monkeypatch, n):
+    """mean_of on the GPU (the colmean used by every diagnostic): the tiled
+    kernel (n <= 1024: warps sum the tree's deepest leaves, the levels combine
+    in shared memory) and the one-thread-per-column kernel both equal the
+    unmodified reference's pairwise tree bit for bit (core.hpp:72-81, 128-133)."""
+    x = np.random.default_rng(n).standard_normal((n, 45))
+    want = ref.mean_of(x)
+    got32 = {}
+    for tiles in ("1", "0"):
+        monkeypatch.setenv("MOSHPIT_COLMEAN_TILES", tiles)
+        assert bits_equal(mb.mean_of(x), want), tiles
+        got32[tiles] = mb.mean_of(x.astype(np.float32))
+    assert bits_equal(got32["1"], got32["0"])
