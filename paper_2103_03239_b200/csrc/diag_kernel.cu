@@ -49,75 +49,6 @@ __global__ void colmean_kernel(const T* __restrict__ x, std::uint64_t n,
   out[j] = AccOps<Acc>::div(s, (Acc)n);
 }
 
-// Column means for n <= 1024 peers: one CTA per 32-column tile.  The 2^K
-// nodes of the deepest level of the reference tree (every node there has <= 8
-// rows, so all are leaves) are summed by the CTA's 8 warps -- lane = column,
-// each row a coalesced 32-column segment, two leaves (up to 16 rows) in
-// flight per warp -- and the levels K-1 .. 0 combine in shared memory as
-// pairwise_block does (a node of <= 8 rows at a shallower level is a leaf
-// there and is summed from its rows).  Bit-identical to colmean_kernel's
-// pairwise_rt, with every element read once by a coalesced load.
-constexpr int kCmThreads = 256, kCmCols = 32, kCmMaxNodes = 128;
-
-template <typename T, typename Acc>
-__global__ void __launch_bounds__(kCmThreads)
-    colmean_tiles(const T* __restrict__ x, std::uint32_t n, std::uint64_t ld, std::uint64_t dim,
-                  Acc* __restrict__ out) {
-  extern __shared__ double sm_cm_raw[];
-  Acc* lv = reinterpret_cast<Acc*>(sm_cm_raw);  // [2][kCmMaxNodes][kCmCols]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::uint64_t c0 = (std::uint64_t)blockIdx.x * kCmCols;
-  int K = 0;
-  while (((n + (1u << K) - 1) >> K) > 8) ++K;  // ceil(n / 2^K) <= 8
-  auto leaf = [&](std::uint32_t lo, std::uint32_t len, std::uint64_t col) {
-    Acc s = Acc(0);
-    if (col < dim)
-      for (std::uint32_t q = 0; q < len; ++q) s = AccOps<Acc>::add(s, (Acc)x[(lo + q) * ld + col]);
-    return s;
-  };
-  {
-    Acc* cur = lv + (K & 1) * kCmMaxNodes * kCmCols;
-    const std::uint64_t col = c0 + lane;
-    const std::uint32_t nodes = 1u << K;
-    for (std::uint32_t i = warp; i < nodes; i += 2 * (kCmThreads / 32)) {
-      // two leaves per step: their loads are independent (ILP)
-      const std::uint32_t j = i + kCmThreads / 32;
-      std::uint32_t lo0, len0, lo1 = 0, len1 = 0;
-      tree_node_range(n, K, i, lo0, len0);
-      if (j < nodes) tree_node_range(n, K, j, lo1, len1);
-      T a[8], b[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        a[q] = ((std::uint32_t)q < len0 && col < dim) ? x[(lo0 + q) * ld + col] : T(0);
-        b[q] = ((std::uint32_t)q < len1 && col < dim) ? x[(lo1 + q) * ld + col] : T(0);
-      }
-      Acc sa = Acc(0), sb = Acc(0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if ((std::uint32_t)q < len0) sa = AccOps<Acc>::add(sa, (Acc)a[q]);
-        if ((std::uint32_t)q < len1) sb = AccOps<Acc>::add(sb, (Acc)b[q]);
-      }
-      cur[i * kCmCols + lane] = sa;
-      if (j < nodes) cur[j * kCmCols + lane] = sb;
-    }
-  }
-  __syncthreads();
-  for (int k = K - 1; k >= 0; --k) {
-    Acc* cur = lv + (k & 1) * kCmMaxNodes * kCmCols;
-    const Acc* kid = lv + ((k + 1) & 1) * kCmMaxNodes * kCmCols;
-    for (std::uint32_t t = threadIdx.x; t < (1u << k) * kCmCols; t += kCmThreads) {
-      const std::uint32_t i = t / kCmCols, c = t % kCmCols;
-      std::uint32_t lo, len;
-      tree_node_range(n, k, i, lo, len);
-      cur[i * kCmCols + c] = len <= 8 ? leaf(lo, len, c0 + c)
-                                      : AccOps<Acc>::add(kid[(2 * i) * kCmCols + c],
-                                                         kid[(2 * i + 1) * kCmCols + c]);
-    }
-    __syncthreads();
-  }
-  if (warp == 0 && c0 + lane < dim) out[c0 + lane] = AccOps<Acc>::div(lv[lane], (Acc)n);
-}
-
 // EXACT: per peer, sequential over j exactly as core.hpp:118-122.  The only
 // serial part of the reference order is the add chain of each peer; the
 // squared differences are independent.  A CTA owns P peers: warps 1..7 stage
@@ -435,12 +366,6 @@ __global__ void drift_finish_acc(const double* __restrict__ acc2, double* __rest
   *out = __ddiv_rn(__dsqrt_rn(acc2[0]), fmax(__dsqrt_rn(acc2[1]), 1e-300));
 }
 
-// MOSHPIT_COLMEAN_TILES=0 keeps the one-thread-per-column kernel (A/B switch).
-bool colmean_tiles_on() {
-  const char* e = std::getenv("MOSHPIT_COLMEAN_TILES");
-  return !e || std::atoi(e) != 0;
-}
-
 unsigned grid_for(std::uint64_t work, unsigned threads) {
   std::uint64_t b = (work + threads - 1) / threads;
   if (b > 148ull * 64) b = 148ull * 64;
@@ -517,21 +442,6 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s) {
   if (dim == 0 || n == 0) return;
-  if (!rows && n <= 1024 && colmean_tiles_on()) {
-    const std::size_t smem = 2ull * kCmMaxNodes * kCmCols * sizeof(Acc);
-    static int attr_dev = -1;
-    int dev = 0;
-    MB_CUDA(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
-      MB_CUDA(cudaFuncSetAttribute(colmean_tiles<T, Acc>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_dev = dev;
-    }
-    colmean_tiles<T, Acc><<<(unsigned)((dim + kCmCols - 1) / kCmCols), kCmThreads, smem, s>>>(
-        x, (std::uint32_t)n, ld, dim, out);
-    MB_LAUNCH_CHECK();
-    return;
-  }
   const unsigned threads = 128;
   colmean_kernel<T, Acc><<<(unsigned)((dim + threads - 1) / threads), threads, 0, s>>>(
       x, n, ld, dim, rows, out);

@@ -120,13 +120,14 @@ def test_sgd_logistic_diag_none_same_iterates(mb):
     assert a.diagnostics.sigma_hat == b.diagnostics.sigma_hat
 
 
-def test_sgd_logistic_device_noise_statistics(mb):
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])  # fp32: the tensor-core path
+def test_sgd_logistic_device_noise_statistics(mb, dtype):
     """Philox noise: sigma_hat ~ sigma (test_optimizer.cpp's sigma check),
     loss decreases, peers agree after averaging."""
     lr = mb.LogisticRegression.synthetic(32, 256, 0.05, mb.Rng(8).stream("objective"))
     cfg = mb.OptimizerConfig(gamma=0.3, tau=1, steps=40, grid=mb.GridConfig(8, 2, 1), sigma=1.0,
                              n_peers=64)
-    r = mb.run_moshpit_sgd(cfg, lr, np.zeros(32), [], mb.Rng(2), noise="device")
+    r = mb.run_moshpit_sgd(cfg, lr, np.zeros(32), [], mb.Rng(2), noise="device", dtype=dtype)
     assert abs(r.diagnostics.sigma_hat - 1.0) < 0.05
     assert r.f_gap[-1] < r.f_gap[0]
     f0 = lr.value(np.zeros(32))
