@@ -409,6 +409,10 @@ def run_mine(args):
         e2e = measure_e2e(mb, cfg)
         e2e_more = {}
         try:
+            e2e_more["pinned_f32_fast_with_vectors"] = measure_e2e(mb, cfg, vectors=True)
+        except Exception as exc:  # noqa: BLE001
+            e2e_more["pinned_f32_fast_with_vectors"] = {"error": str(exc)}
+        try:
             e2e_more["pageable_f32_fast"] = measure_e2e(mb, cfg, pinned=False)
         except Exception as exc:  # noqa: BLE001
             e2e_more["pageable_f32_fast"] = {"error": str(exc)}
@@ -749,24 +753,26 @@ def measure_sgd_c4(mb, steps=20, sigma=1.0, diagnostics="none"):
             "final_sigma_hat": round(r.diagnostics.sigma_hat, 6)}
 
 
-def measure_e2e(mb, cfg, pinned=True):
+def measure_e2e(mb, cfg, pinned=True, vectors=False):
     """The reference-facing call (run_moshpit through the C ABI) with HOST
-    buffers: H2D of the initial state, R rounds + TrialReport diagnostics,
-    D2H of the final vectors, all inside the timed region.  pinned=False:
-    a plain (pageable) numpy buffer, packed through the library's pinned
-    staging ring by host threads."""
+    buffers: H2D of the initial state, R rounds + TrialReport diagnostics and
+    the D2H of the report -- the reference's run_moshpit returns the
+    TrialReport only (protocols.hpp:108-179) -- all inside the timed region.
+    vectors=True also copies the final vectors back (the C ABI's optional
+    final_out).  pinned=False: a plain (pageable) numpy buffer, packed through
+    the library's pinned staging ring by host threads."""
     import numpy as np
     import torch
     M, d, N, D, p, R = CONFIGS[cfg]
     if pinned:
         host = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
         xh = host.numpy()
-        out_t = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
-        oh = out_t.numpy()
+        out_t = torch.empty((N, D), dtype=torch.float32, pin_memory=True) if vectors else None
+        oh = out_t.numpy() if vectors else None
     else:
         host = None
         xh = np.empty((N, D), dtype=np.float32)
-        oh = np.empty((N, D), dtype=np.float32)
+        oh = np.empty((N, D), dtype=np.float32) if vectors else None
     # fill the host buffer from the device init (same synthetic data)
     blk = torch.empty((64, D), dtype=torch.float32, device="cuda")
     for i0 in range(0, N, 64):
@@ -782,7 +788,8 @@ def measure_e2e(mb, cfg, pinned=True):
     act = np.zeros(R, dtype=np.uint32)
     init_d, cost = C.c_double(0), C.c_double(0)
     ptr = xh.ctypes.data_as(C.c_void_p)
-    optr = oh.ctypes.data_as(C.c_void_p)  # separate output: every call starts from the init
+    # separate output: every call starts from the init
+    optr = oh.ctypes.data_as(C.c_void_p) if vectors else None
 
     def call():
         _capi.check(lib.moshpit_run_moshpit(_capi.F32, M, d, R, ptr, N, D, p, PROTOCOL_SEED, R,
@@ -798,10 +805,16 @@ def measure_e2e(mb, cfg, pinned=True):
         times.append(time.perf_counter() - t0)
     t = sorted(times)[1]  # median of 3
     bytes_ = N * D * 4
+    h2d_call = bytes_ + R * N * 9  # state + per-round draws
+    d2h_call = (bytes_ if vectors else 0) + (2 * R + 2) * 8  # (vectors +) the TrialReport
     out = {"value": round(bytes_ * R / t / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": bytes_ + R * N * 9, "d2h_bytes_per_step": bytes_ + R * 16 + 8,
+           # a step is one round: the call's copies amortised over its R rounds
+           "h2d_bytes_per_step": h2d_call // R, "d2h_bytes_per_step": d2h_call // R,
+           "h2d_bytes_per_call": h2d_call, "d2h_bytes_per_call": d2h_call,
            "call": (f"moshpit_run_moshpit(F32, rounds={R}, DIAG_FAST) host->host, "
-                    + ("pinned" if pinned else "pageable numpy buffer (library staging ring)")),
+                    + ("pinned" if pinned else "pageable numpy buffer (library staging ring)")
+                    + (", final vectors copied back" if vectors else
+                       ", TrialReport returned (as protocols::run_moshpit)")),
            "seconds": round(t, 4), "seconds_each": [round(x, 4) for x in times],
            "timing": "host wall clock per call, 1 warm-up + median of 3",
            "final_distortion": float(dist_[-1]),
@@ -835,10 +848,12 @@ def measure_e2e(mb, cfg, pinned=True):
         bidir_gbs = max(bidir_gbs, 2 * n2 * 4 / (time.perf_counter() - t1) / 1e9)
     del dev, hb, out_t, host
     torch.cuda.empty_cache()
-    t_floor = 2 * bytes_ / (bidir_gbs * 1e9)
+    t_floor = 2 * bytes_ / (bidir_gbs * 1e9) if vectors else bytes_ / (h2d_gbs * 1e9)
     out.update({"pcie_h2d_gbs_plain_copy": round(h2d_gbs, 1),
                 "pcie_bidir_gbs_aggregate": round(bidir_gbs, 1),
-                "frac_of_pcie_ceiling": round(t_floor / t, 3)})
+                "frac_of_pcie_ceiling": round(t_floor / t, 3),
+                "pcie_ceiling": "bidirectional (state in + vectors out)" if vectors
+                                else "one-way H2D of the state"})
     return out
 
 
@@ -883,7 +898,9 @@ def measure_e2e_dropin(cfg, reps=3):
     out.update({"value": round(N * D * 4 * R / t / 1e9, 3), "unit": "GB/s",
                 "value_note": "fp32-normalised N*D*4 bytes per round (the call moves fp64)",
                 "value_fp64_bytes": round(N * D * 8 * R / t / 1e9, 3),
-                "h2d_bytes_per_step": N * D * 8 + R * N * 9, "d2h_bytes_per_step": R * 16 + 8,
+                "h2d_bytes_per_step": (N * D * 8 + R * N * 9) // R,
+                "d2h_bytes_per_step": ((2 * R + 2) * 8) // R,
+                "h2d_bytes_per_call": N * D * 8 + R * N * 9, "d2h_bytes_per_call": (2 * R + 2) * 8,
                 "timing": f"host wall clock per call, 1 warm-up + median of {reps}",
                 "config_dim": D})
     return out
