@@ -10,6 +10,7 @@
 // order (deterministic, ~1e-15 relative to the sequential sum).  Column means
 // use the reference pairwise tree over peers in both modes, in fp64.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "blocktree.cuh"
@@ -47,6 +48,67 @@ __global__ void colmean_kernel(const T* __restrict__ x, std::uint64_t n,
                                  [](Acc a, Acc b) { return AccOps<Acc>::add(a, b); },
                                  (Acc)0);
   out[j] = AccOps<Acc>::div(s, (Acc)n);
+}
+
+// Column means for the configs' peer counts (N = 256 / 1024): the
+// reference tree over the N rows unrolled at compile time (n <= 8 sequential
+// from +0, else split at floor(n/2): exactly pairwise_rt's tree), each thread
+// owning one 16-byte column vector (4 fp32 or 2 fp64 columns).  No stack, no
+// runtime leaf loop: every row load is independent of the adds, so a thread
+// keeps many 16-byte loads in flight (the runtime-tree kernel keeps one
+// 4-byte load per thread in flight).
+template <typename T>
+struct ColVec;
+template <>
+struct ColVec<float> {
+  using V = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct ColVec<double> {
+  using V = double2;
+  static constexpr int W = 2;
+};
+
+template <int N, typename T, typename Acc>
+__device__ __forceinline__ void ctree(const typename ColVec<T>::V* __restrict__ col,
+                                      std::uint64_t ldv, int base,
+                                      Acc (&out)[ColVec<T>::W]) {
+  constexpr int W = ColVec<T>::W;
+  if constexpr (N <= 8) {
+    typename ColVec<T>::V v[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = __ldg(col + (std::uint64_t)(base + q) * ldv);
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[w] = Acc(0);
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const T* e = reinterpret_cast<const T*>(&v[q]);
+#pragma unroll
+      for (int w = 0; w < W; ++w) out[w] = AccOps<Acc>::add(out[w], (Acc)e[w]);
+    }
+  } else {
+    Acc a[W], b[W];
+    ctree<N / 2, T, Acc>(col, ldv, base, a);
+    ctree<N - N / 2, T, Acc>(col, ldv, base + N / 2, b);
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[w] = AccOps<Acc>::add(a[w], b[w]);
+  }
+}
+
+template <int N, typename T, typename Acc>
+__global__ void __launch_bounds__(128)
+    colmean_unrolled(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                     Acc* __restrict__ out) {
+  using V = typename ColVec<T>::V;
+  constexpr int W = ColVec<T>::W;
+  const std::uint64_t cv = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (cv * W >= dim) return;
+  Acc s[W];
+  ctree<N, T, Acc>(reinterpret_cast<const V*>(x) + cv, ld / W, 0, s);
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (cv * W + w < dim) out[cv * W + w] = AccOps<Acc>::div(s[w], (Acc)N);
 }
 
 // EXACT: per peer, sequential over j exactly as core.hpp:118-122.  The only
@@ -213,24 +275,6 @@ __device__ double block_sum_fixed(double v) {
   return r;
 }
 
-// FAST: block (c, i) sums chunk c of row i in a fixed order.
-template <typename T>
-__global__ void dist_rows_fast(const T* __restrict__ x, std::uint64_t ld,
-                               std::uint64_t dim, const double* __restrict__ ref,
-                               std::uint64_t nch, double* __restrict__ partial) {
-  const std::uint64_t c = blockIdx.x, i = blockIdx.y;
-  const T* row = x + i * ld;
-  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
-  double acc = 0.0;
-#pragma unroll 8
-  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
-    const double diff = __dsub_rn((double)row[j], ref[j]);
-    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-  }
-  const double s = block_sum_fixed(acc);
-  if (threadIdx.x == 0) partial[i * nch + c] = s;
-}
-
 __global__ void fold_rows(const double* __restrict__ partial, std::uint64_t n,
                           std::uint64_t nch, double* __restrict__ sq) {
   const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
@@ -325,18 +369,38 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
 }
 
 // ---- slab-streamed variants: the j-sums continue across D-slabs --------
+// FAST: block (c, i) sums chunk c of row i in a fixed order (chunk offset c0
+// in the row's partials, so the slab-streamed and resident paths agree): each
+// thread takes 16-byte vectors (4 fp32 / 2 fp64 coordinates) 256 vectors
+// apart, sums its elements sequentially, then the block tree.
 template <typename T>
 __global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
                                    const double* __restrict__ ref, std::uint64_t nch_total,
                                    std::uint64_t c0, double* __restrict__ partial) {
+  using V = typename ColVec<T>::V;
+  constexpr int W = ColVec<T>::W;
   const std::uint64_t c = blockIdx.x, i = blockIdx.y;
   const T* row = x + i * ld;
   const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  const bool vec = (ld % W == 0) && (reinterpret_cast<std::uintptr_t>(x) % 16 == 0);
   double acc = 0.0;
-#pragma unroll 8
-  for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRedThreads) {
-    const double diff = __dsub_rn((double)row[j], ref[j]);
-    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+#pragma unroll 4
+  for (std::uint64_t j = lo + (std::uint64_t)threadIdx.x * W; j < hi; j += kRedThreads * W) {
+    T e[W];
+    if (vec && j + W <= hi) {
+      const V v = __ldg(reinterpret_cast<const V*>(row + j));
+#pragma unroll
+      for (int w = 0; w < W; ++w) e[w] = reinterpret_cast<const T*>(&v)[w];
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) e[w] = j + w < hi ? row[j + w] : T(0);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if (j + w >= hi) break;
+      const double diff = __dsub_rn((double)e[w], ref[j + w]);
+      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
   }
   const double s = block_sum_fixed(acc);
   if (threadIdx.x == 0) partial[i * nch_total + c0 + c] = s;
@@ -442,6 +506,19 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s) {
   if (dim == 0 || n == 0) return;
+  // the diagnostics' fp64 column means only (keeps the library small)
+  if constexpr (std::is_same<Acc, double>::value) {
+    constexpr int W = ColVec<T>::W;
+    const bool vec_ok = !rows && ld % W == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0;
+    if (vec_ok && (n == 256 || n == 1024)) {
+      const std::uint64_t nv = (dim + W - 1) / W;
+      const unsigned blocks = (unsigned)((nv + 127) / 128);
+      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, out);
+      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, out);
+      MB_LAUNCH_CHECK();
+      return;
+    }
+  }
   const unsigned threads = 128;
   colmean_kernel<T, Acc><<<(unsigned)((dim + threads - 1) / threads), threads, 0, s>>>(
       x, n, ld, dim, rows, out);
@@ -461,8 +538,8 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
     launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s);
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    dist_rows_fast<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
-        x, ld, dim, ref, nch, partial);
+    dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch, 0, partial);
     MB_LAUNCH_CHECK();
     fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
   }

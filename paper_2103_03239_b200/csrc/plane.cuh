@@ -147,8 +147,16 @@ struct Plane {
     scs.resize(n * 4);
     sgi.resize(n * 4);
     cellbuf.resize(n * 8);
-    MB_CUDA(cudaMemset(totals.ptr, 0, 16));
-    MB_CUDA(cudaMemset(counts.ptr, 0, 16));
+    {
+      // zeroed on a private stream and waited for: a plain cudaMemset goes to
+      // the legacy stream, which the engines' non-blocking streams do not
+      // order against -- kernel 1 could write `counts` before the memset
+      // lands (seen with concurrent host threads)
+      StreamHolder z;
+      MB_CUDA(cudaMemsetAsync(totals.ptr, 0, 16, z.s));
+      MB_CUDA(cudaMemsetAsync(counts.ptr, 0, 16, z.s));
+      MB_CUDA(cudaStreamSynchronize(z.s));
+    }
     for (int i = 0; i < kStages; ++i) {
       stage[i].resize(n * 9 + 16);
       MB_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
