@@ -292,9 +292,10 @@ def time_engine_rounds(mb, torch, eng, x, steps, record=False):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(steps):
-        eng.round(x)
-        if record:
-            eng.record(x)
+        if record:  # the round and its record_round (representative rows)
+            eng.round_record(x)
+        else:
+            eng.round(x)
     ev1.record(stream)
     torch.cuda.synchronize()
     t_ms = ev0.elapsed_time(ev1)
@@ -316,9 +317,10 @@ def measure_variant(mb, torch, cfg, local, steps, warmup, f64=False, diag=None):
     if diag:
         eng.set_reference(x, diagnostics=diag)
     for _ in range(warmup):
-        eng.round(x)
         if diag:
-            eng.record(x)
+            eng.round_record(x)
+        else:
+            eng.round(x)
     t_ms, k_ms, kn, rows = time_engine_rounds(mb, torch, eng, x, steps, record=bool(diag))
     rep = eng.report() if diag else None
     eng.close()

@@ -296,6 +296,13 @@ int moshpit_engine_set_reference(moshpit_engine* e, int dtype, const void* state
                                  uint64_t dim, uint64_t ld, int diag, void* stream);
 int moshpit_engine_record(moshpit_engine* e, int dtype, const void* state,
                           uint64_t dim, uint64_t ld, void* stream);
+/* A round and its record_round in one call: the diagnostics then read one
+ * representative row per averaged group (all its members hold the same
+ * mean) -- the same bits as moshpit_engine_round + moshpit_engine_record,
+ * fewer HBM bytes. */
+int moshpit_engine_round_record(moshpit_engine* e, int dtype, void* state,
+                                uint64_t dim, uint64_t ld, void* stream,
+                                uint32_t* active_out);
 int moshpit_engine_report(moshpit_engine* e, double* initial_distortion,
                           double* distortion, double* mean_drift, uint64_t cap,
                           uint64_t* count);

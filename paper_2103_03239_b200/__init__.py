@@ -728,6 +728,18 @@ class Engine:
                                                  state.shape[1] if dim is None else dim, ld,
                                                  _DIAG[diagnostics], s.cuda_stream))
 
+    def round_record(self, state, dim: Optional[int] = None, stream=None) -> int:
+        """One round and its record_round (reads one representative row per
+        averaged group: same bits as round() + record())."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        act = C.c_uint32(0)
+        check(lib().moshpit_engine_round_record(self._h, code, ptr,
+                                                state.shape[1] if dim is None else dim, ld,
+                                                s.cuda_stream, C.byref(act)))
+        return act.value
+
     def record(self, state, dim: Optional[int] = None, stream=None):
         """Append this round's (distortion, mean_drift) to the device log."""
         import torch

@@ -76,6 +76,7 @@ struct moshpit_engine {
   int diag = MOSHPIT_DIAG_NONE;
   std::uint64_t diag_dim = 0;
   DeviceBuffer ref, mean, sq, part, part2, log;  // log: [0] initial, then (dist, drift) pairs
+  DeviceBuffer rep, rlist, rcount;               // representatives of the last round
   std::uint64_t log_cap = 0, log_n = 0;
   std::unique_ptr<StreamHolder> aux;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -456,22 +457,32 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     // record_round: the distortion (st; EXACT j-chains or FAST chunk
     // partials) and colmean + drift (aux) only read the state, so they run
     // side by side; the next round waits for both.
+    // after a round, the rows of each averaged group are identical: the
+    // per-row diagnostics read one representative row per such group
+    // (RepRows; bit-identical results, fewer HBM bytes)
+    DeviceBuffer d_rep(n * 4 + 16), d_rlist(n * 4 + 16), d_rcount(16);
+    const RepRows reps{d_rep.as<std::uint32_t>(), d_rlist.as<std::uint32_t>(),
+                       d_rcount.as<std::uint32_t>()};
     auto record = [&](double* dist_slot, double* drift_slot) {
+      const RepRows* rr = drift_slot ? &reps : nullptr;  // the initial record has no round
+      const std::uint32_t* rows = rr ? reps.rep : nullptr;
       if (drift_slot) {
         MB_CUDA(cudaEventRecord(ev_fork, st.s));
         MB_CUDA(cudaStreamWaitEvent(aux.s, ev_fork, 0));
       }
       if (dtype == MOSHPIT_F32) {
         launch_distortion<float>(d_x.as<float>(), n, ld, dim, d_ref.as<double>(),
-                                 d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
+                                 d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s,
+                                 rr);
         if (drift_slot)
-          launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, nullptr,
+          launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, rows,
                                         d_mean.as<double>(), aux.s);
       } else {
         launch_distortion<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
-                                  d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s);
+                                  d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s,
+                                  rr);
         if (drift_slot)
-          launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, nullptr,
+          launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, rows,
                                          d_mean.as<double>(), aux.s);
       }
       if (drift_slot) {
@@ -500,7 +511,13 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
     for (std::uint32_t r = 0; r < rounds; ++r) {
       active_counts[r] = plane.round(&fail, p_round, clock, dtype, d_x.ptr, dim, ld, st.s,
                                      MOSHPIT_KERNEL_AUTO);
-      if (diag != MOSHPIT_DIAG_NONE) record(outp + 2 + r, outp + 2 + rounds + r);
+      if (diag != MOSHPIT_DIAG_NONE) {
+        launch_build_reps(plane.members.as<std::uint32_t>(), plane.goff.as<std::uint32_t>(),
+                          plane.gvoid.as<std::uint8_t>(), plane.counts.as<std::uint32_t>(), n,
+                          d_rep.as<std::uint32_t>(), d_rlist.as<std::uint32_t>(),
+                          d_rcount.as<std::uint32_t>(), st.s);
+        record(outp + 2 + r, outp + 2 + rounds + r);
+      }
     }
     if (diag != MOSHPIT_DIAG_NONE) {
       std::vector<double> h(2 * rounds + 2);
@@ -854,7 +871,8 @@ namespace {
 
 template <typename T>
 void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t dim,
-                 double* dist_slot, double* drift_slot, cudaStream_t s) {
+                 double* dist_slot, double* drift_slot, cudaStream_t s,
+                 const RepRows* reps = nullptr) {
   const std::uint64_t n = e->plane->n;
   const int exact = e->diag == MOSHPIT_DIAG_EXACT;
   if (drift_slot) {
@@ -862,9 +880,10 @@ void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t 
     MB_CUDA(cudaStreamWaitEvent(e->aux->s, e->ev_fork, 0));
   }
   launch_distortion<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
-                       e->part.as<double>(), dist_slot, exact, s);
+                       e->part.as<double>(), dist_slot, exact, s, reps);
   if (drift_slot) {
-    launch_colmean<T, double>(x, n, ld, dim, nullptr, e->mean.as<double>(), e->aux->s);
+    launch_colmean<T, double>(x, n, ld, dim, reps ? reps->rep : nullptr, e->mean.as<double>(),
+                              e->aux->s);
     launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
                  drift_slot, exact, e->aux->s);
     MB_CUDA(cudaEventRecord(e->ev_join, e->aux->s));
@@ -921,33 +940,79 @@ int moshpit_engine_set_reference(moshpit_engine* e, int dtype, const void* state
   });
 }
 
+namespace {
+
+// record_round after the state's latest change; with `after_round` the
+// state is exactly the output of the engine's last round, so its averaged
+// groups' rows are identical and only representative rows are read.
+void engine_record_impl(moshpit_engine* e, int dtype, const void* state, std::uint64_t dim,
+                        std::uint64_t ld, cudaStream_t s, bool after_round) {
+  if (e->diag == MOSHPIT_DIAG_NONE)
+    throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
+  if (dim != e->diag_dim) throw std::invalid_argument("engine_record: dim changed");
+  e->plane->order_after(s);
+  if (e->log_n == e->log_cap) {  // grow the device log (rare: synchronises)
+    DeviceBuffer bigger((1 + 4 * e->log_cap) * 8);
+    MB_CUDA(cudaStreamSynchronize(s));
+    MB_CUDA(cudaMemcpy(bigger.ptr, e->log.ptr, (1 + 2 * e->log_cap) * 8,
+                       cudaMemcpyDeviceToDevice));
+    std::swap(e->log.ptr, bigger.ptr);
+    std::swap(e->log.bytes, bigger.bytes);
+    e->log_cap *= 2;
+  }
+  RepRows reps;
+  if (after_round) {
+    const std::uint64_t n = e->plane->n;
+    e->rep.resize(n * 4 + 16);
+    e->rlist.resize(n * 4 + 16);
+    e->rcount.resize(16);
+    Plane& p = *e->plane;
+    launch_build_reps(p.members.as<std::uint32_t>(), p.goff.as<std::uint32_t>(),
+                      p.gvoid.as<std::uint8_t>(), p.counts.as<std::uint32_t>(), n,
+                      e->rep.as<std::uint32_t>(), e->rlist.as<std::uint32_t>(),
+                      e->rcount.as<std::uint32_t>(), s);
+    reps = RepRows{e->rep.as<std::uint32_t>(), e->rlist.as<std::uint32_t>(),
+                   e->rcount.as<std::uint32_t>()};
+  }
+  double* slot = e->log.as<double>() + 1 + 2 * e->log_n;
+  if (dtype == MOSHPIT_F32)
+    engine_diag<float>(e, static_cast<const float*>(state), ld, dim, slot, slot + 1, s,
+                       after_round ? &reps : nullptr);
+  else
+    engine_diag<double>(e, static_cast<const double*>(state), ld, dim, slot, slot + 1, s,
+                        after_round ? &reps : nullptr);
+  ++e->log_n;
+  e->plane->mark_done(s);
+}
+
+}  // namespace
+
 int moshpit_engine_record(moshpit_engine* e, int dtype, const void* state, std::uint64_t dim,
                           std::uint64_t ld, void* stream) {
   return guarded([&] {
     if (!e) throw std::invalid_argument("null engine");
-    if (e->diag == MOSHPIT_DIAG_NONE)
-      throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
-    if (dim != e->diag_dim) throw std::invalid_argument("engine_record: dim changed");
     check_state(dtype, state, dim, ld);
     DeviceGuard g(e->plane->device);
+    engine_record_impl(e, dtype, state, dim, ld, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+// One round and its record_round in one call (protocols.hpp:142-173): the
+// diagnostics read one representative row per averaged group.
+int moshpit_engine_round_record(moshpit_engine* e, int dtype, void* state, std::uint64_t dim,
+                                std::uint64_t ld, void* stream, std::uint32_t* active_out) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (!state) throw std::invalid_argument("engine_round_record: null state");
+    check_state(dtype, state, dim, ld);
+    if (e->diag == MOSHPIT_DIAG_NONE)
+      throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
+    DeviceGuard g(e->plane->device);
     auto s = static_cast<cudaStream_t>(stream);
-    e->plane->order_after(s);
-    if (e->log_n == e->log_cap) {  // grow the device log (rare: synchronises)
-      DeviceBuffer bigger((1 + 4 * e->log_cap) * 8);
-      MB_CUDA(cudaStreamSynchronize(s));
-      MB_CUDA(cudaMemcpy(bigger.ptr, e->log.ptr, (1 + 2 * e->log_cap) * 8,
-                         cudaMemcpyDeviceToDevice));
-      std::swap(e->log.ptr, bigger.ptr);
-      std::swap(e->log.bytes, bigger.bytes);
-      e->log_cap *= 2;
-    }
-    double* slot = e->log.as<double>() + 1 + 2 * e->log_n;
-    if (dtype == MOSHPIT_F32)
-      engine_diag<float>(e, static_cast<const float*>(state), ld, dim, slot, slot + 1, s);
-    else
-      engine_diag<double>(e, static_cast<const double*>(state), ld, dim, slot, slot + 1, s);
-    ++e->log_n;
-    e->plane->mark_done(s);
+    const std::uint32_t a =
+        e->plane->round(&e->fail, e->p, e->clock, dtype, state, dim, ld, s, e->variant);
+    if (active_out) *active_out = a;
+    engine_record_impl(e, dtype, state, dim, ld, s, true);
   });
 }
 

@@ -310,6 +310,20 @@ void logit_tc_step(float* theta, std::uint64_t n, std::uint64_t ld, std::uint64_
                    float* th_lo, float* c_hi, float* c_lo, cudaStream_t s);
 
 // Diagnostics and helpers.
+// Representative rows of a round: after averaging, every member of a
+// non-voided group holds the identical group mean, so per-row diagnostics
+// need to read only one row per such group (plus every voided row).  rep[i]
+// = the representative of row i; list[0 .. *count) = the representatives.
+// Results are bit-identical to reading every row (the values are the same).
+struct RepRows {
+  const std::uint32_t* rep = nullptr;
+  const std::uint32_t* list = nullptr;
+  const std::uint32_t* count = nullptr;
+};
+void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
+                       const std::uint8_t* gvoid, const std::uint32_t* counts, std::uint64_t n,
+                       std::uint32_t* rep, std::uint32_t* list, std::uint32_t* count,
+                       cudaStream_t s);
 template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
@@ -318,7 +332,7 @@ template <typename T>
 void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq_scratch,
                        double* partial_scratch, double* out, int exact,
-                       cudaStream_t s);
+                       cudaStream_t s, const RepRows* reps = nullptr);
 void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
                   double* partial_scratch, double* out, int exact,
                   cudaStream_t s);
@@ -330,12 +344,14 @@ std::uint64_t diag_chunk();
 template <typename T>
 void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                       const double* ref, int exact, double* acc, double* partial,
-                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s);
+                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s,
+                      const RepRows* reps = nullptr);
 void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim, int exact,
                        double* acc2, double* partial, std::uint64_t c0, cudaStream_t s);
 void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, double* acc,
                         double* row_partial, double* acc2, double* drift_partial,
-                        double* dist_out, double* drift_out, cudaStream_t s);
+                        double* dist_out, double* drift_out, cudaStream_t s,
+                        const std::uint32_t* rep = nullptr);
 template <typename T>
 void launch_fill_synthetic(T* x, std::uint64_t n, std::uint64_t dim,
                            std::uint64_t ld, std::uint64_t seed,

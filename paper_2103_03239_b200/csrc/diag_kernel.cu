@@ -9,6 +9,7 @@
 // MOSHPIT_DIAG_FAST sums fixed chunks in parallel and folds them in a fixed
 // order (deterministic, ~1e-15 relative to the sequential sum).  Column means
 // use the reference pairwise tree over peers in both modes, in fp64.
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -72,13 +73,14 @@ struct ColVec<double> {
 
 template <int N, typename T, typename Acc>
 __device__ __forceinline__ void ctree(const typename ColVec<T>::V* __restrict__ col,
-                                      std::uint64_t ldv, int base,
+                                      std::uint64_t ldv, int base, const std::uint32_t* rows,
                                       Acc (&out)[ColVec<T>::W]) {
   constexpr int W = ColVec<T>::W;
   if constexpr (N <= 8) {
     typename ColVec<T>::V v[N];
 #pragma unroll
-    for (int q = 0; q < N; ++q) v[q] = __ldg(col + (std::uint64_t)(base + q) * ldv);
+    for (int q = 0; q < N; ++q)
+      v[q] = __ldg(col + (std::uint64_t)(rows ? rows[base + q] : (std::uint32_t)(base + q)) * ldv);
 #pragma unroll
     for (int w = 0; w < W; ++w) out[w] = Acc(0);
 #pragma unroll
@@ -89,23 +91,30 @@ __device__ __forceinline__ void ctree(const typename ColVec<T>::V* __restrict__ 
     }
   } else {
     Acc a[W], b[W];
-    ctree<N / 2, T, Acc>(col, ldv, base, a);
-    ctree<N - N / 2, T, Acc>(col, ldv, base + N / 2, b);
+    ctree<N / 2, T, Acc>(col, ldv, base, rows, a);
+    ctree<N - N / 2, T, Acc>(col, ldv, base + N / 2, rows, b);
 #pragma unroll
     for (int w = 0; w < W; ++w) out[w] = AccOps<Acc>::add(a[w], b[w]);
   }
 }
 
+// rows (optional): element i of the tree is row rows[i] -- the representative
+// gather (RepRows): identical values, fewer distinct rows read from HBM.
 template <int N, typename T, typename Acc>
 __global__ void __launch_bounds__(128)
     colmean_unrolled(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
-                     Acc* __restrict__ out) {
+                     const std::uint32_t* __restrict__ rows, Acc* __restrict__ out) {
   using V = typename ColVec<T>::V;
   constexpr int W = ColVec<T>::W;
+  __shared__ std::uint32_t s_rows[N];
+  if (rows) {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_rows[i] = rows[i];
+    __syncthreads();
+  }
   const std::uint64_t cv = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
   if (cv * W >= dim) return;
   Acc s[W];
-  ctree<N, T, Acc>(reinterpret_cast<const V*>(x) + cv, ld / W, 0, s);
+  ctree<N, T, Acc>(reinterpret_cast<const V*>(x) + cv, ld / W, 0, rows ? s_rows : nullptr, s);
 #pragma unroll
   for (int w = 0; w < W; ++w)
     if (cv * W + w < dim) out[cv * W + w] = AccOps<Acc>::div(s[w], (Acc)N);
@@ -132,12 +141,19 @@ template <typename T, int P>
 __global__ void __launch_bounds__(kExThreads)
     dist_exact_tiled(const T* __restrict__ x, std::uint64_t n, std::uint64_t ld,
                      std::uint64_t dim, const double* __restrict__ ref,
-                     double* __restrict__ acc, int accumulate) {
+                     double* __restrict__ acc, int accumulate,
+                     const std::uint32_t* __restrict__ list,
+                     const std::uint32_t* __restrict__ list_count) {
   extern __shared__ double sm_ex[];
+  // chains of rows list[p0 .. p0+P) (or rows p0 .. p0+P): acc is by row id
+  const std::uint64_t rows = list ? *list_count : n;
   const std::uint64_t p0 = (std::uint64_t)blockIdx.x * P;
+  if (p0 >= rows) return;  // uniform across the CTA
+  n = rows;
+  auto row_of = [&](std::uint64_t q) -> std::uint64_t { return list ? list[q] : q; };
   const int tid = threadIdx.x;
   double a = 0.0;
-  if (tid < P && p0 + tid < n && accumulate) a = acc[p0 + tid];
+  if (tid < P && p0 + tid < n && accumulate) a = acc[row_of(p0 + tid)];
   const std::uint64_t ntiles = (dim + kExK - 1) / kExK;
   // all of a producer thread's loads for a tile are issued before any use
   // (the latency of one batch per tile, hidden behind the chains' tile)
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(kExThreads)
       const std::uint64_t j = j0 + k, i = p0 + q;
       const bool ok = e < kE && j < dim && i < n;
       // padding: (0 - 0)^2 = +0.0 added to a sum of squares is bit-neutral
-      xv[u] = ok ? (double)x[i * ld + j] : 0.0;
+      xv[u] = ok ? (double)x[row_of(i) * ld + j] : 0.0;
       rv[u] = ok ? ref[j] : 0.0;
     }
 #pragma unroll
@@ -179,19 +195,37 @@ __global__ void __launch_bounds__(kExThreads)
     }
     __syncthreads();
   }
-  if (tid < P && p0 + tid < n) acc[p0 + tid] = a;
+  if (tid < P && p0 + tid < n) acc[row_of(p0 + tid)] = a;
 }
 
+template <typename T, int P>
+void launch_dist_exact_p(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                         const double* ref, double* acc, int accumulate, cudaStream_t s,
+                         const std::uint32_t* list, const std::uint32_t* count) {
+  static bool attr = false;
+  if (!attr) {
+    MB_CUDA(cudaFuncSetAttribute(dist_exact_tiled<T, P>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)exact_smem<P>()));
+    attr = true;
+  }
+  const unsigned blocks = (unsigned)((n + P - 1) / P);
+  dist_exact_tiled<T, P><<<blocks, kExThreads, exact_smem<P>(), s>>>(x, n, ld, dim, ref, acc,
+                                                                   accumulate, list, count);
+}
+
+// list / count: chains only for the representative rows (RepRows); acc by row.
 template <typename T>
 void launch_dist_exact(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
-                       const double* ref, double* acc, int accumulate, cudaStream_t s) {
-  // peers per CTA: enough CTAs to spread the chains over the SMs
+                       const double* ref, double* acc, int accumulate, cudaStream_t s,
+                       const std::uint32_t* list = nullptr, const std::uint32_t* count = nullptr) {
+  // rows per CTA: enough CTAs to spread the chains over the SMs
   const int P = n >= 2048 ? 8 : n >= 1024 ? 4 : n >= 512 ? 2 : 1;
-  const unsigned blocks = (unsigned)((n + P - 1) / P);
   switch (P) {
-#define MB_EXL(PP)                                                                      case PP: {                                                                              static bool attr = false;                                                             if (!attr) {                                                                            MB_CUDA(cudaFuncSetAttribute(dist_exact_tiled<T, PP>,                                                              cudaFuncAttributeMaxDynamicSharedMemorySize,                                          (int)exact_smem<PP>()));                                 attr = true;                                                                        }                                                                                     dist_exact_tiled<T, PP><<<blocks, kExThreads, exact_smem<PP>(), s>>>(x, n, ld, dim,                                                                          ref, acc,                                                                             accumulate);     break;                                                                              }
-    MB_EXL(1) MB_EXL(2) MB_EXL(4) MB_EXL(8)
-#undef MB_EXL
+    case 1: launch_dist_exact_p<T, 1>(x, n, ld, dim, ref, acc, accumulate, s, list, count); break;
+    case 2: launch_dist_exact_p<T, 2>(x, n, ld, dim, ref, acc, accumulate, s, list, count); break;
+    case 4: launch_dist_exact_p<T, 4>(x, n, ld, dim, ref, acc, accumulate, s, list, count); break;
+    default: launch_dist_exact_p<T, 8>(x, n, ld, dim, ref, acc, accumulate, s, list, count);
   }
   MB_LAUNCH_CHECK();
 }
@@ -276,12 +310,45 @@ __device__ double block_sum_fixed(double v) {
 }
 
 __global__ void fold_rows(const double* __restrict__ partial, std::uint64_t n,
-                          std::uint64_t nch, double* __restrict__ sq) {
+                          std::uint64_t nch, double* __restrict__ sq,
+                          const std::uint32_t* __restrict__ rep) {
   const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const std::uint64_t r = rep ? rep[i] : i;  // identical rows share their partials
   double acc = 0.0;
-  for (std::uint64_t c = 0; c < nch; ++c) acc = __dadd_rn(acc, partial[i * nch + c]);
+  for (std::uint64_t c = 0; c < nch; ++c) acc = __dadd_rn(acc, partial[r * nch + c]);
   sq[i] = acc;
+}
+
+// Representatives of a round (RepRows, common.cuh): one thread per group.
+__global__ void build_reps_kernel(const std::uint32_t* __restrict__ members,
+                                  const std::uint32_t* __restrict__ goff,
+                                  const std::uint8_t* __restrict__ gvoid,
+                                  const std::uint32_t* __restrict__ counts,
+                                  std::uint32_t* __restrict__ rep, std::uint32_t* __restrict__ list,
+                                  std::uint32_t* __restrict__ count) {
+  const std::uint32_t ng = counts[0];
+  for (std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng;
+       g += gridDim.x * blockDim.x) {
+    const std::uint32_t b = goff[g], e = goff[g + 1];
+    if (!gvoid[g]) {  // averaged: every member now equals the first member's row
+      const std::uint32_t first = members[b];
+      for (std::uint32_t k = b; k < e; ++k) rep[members[k]] = first;
+      list[atomicAdd(count, 1u)] = first;
+    } else {  // voided: the members keep their own rows
+      for (std::uint32_t k = b; k < e; ++k) {
+        rep[members[k]] = members[k];
+        list[atomicAdd(count, 1u)] = members[k];
+      }
+    }
+  }
+}
+
+// in-place expansion sq[i] = sq[rep[i]] (representatives are their own rep)
+__global__ void expand_reps(double* __restrict__ sq, const std::uint32_t* __restrict__ rep,
+                            std::uint64_t n) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i < n && rep[i] != i) sq[i] = sq[rep[i]];
 }
 
 // pairwise over peers, / n  (core.hpp:125): the reference tree evaluated by
@@ -369,17 +436,14 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
 }
 
 // ---- slab-streamed variants: the j-sums continue across D-slabs --------
-// FAST: block (c, i) sums chunk c of row i in a fixed order (chunk offset c0
-// in the row's partials, so the slab-streamed and resident paths agree): each
-// thread takes 16-byte vectors (4 fp32 / 2 fp64 coordinates) 256 vectors
-// apart, sums its elements sequentially, then the block tree.
 template <typename T>
-__global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
-                                   const double* __restrict__ ref, std::uint64_t nch_total,
-                                   std::uint64_t c0, double* __restrict__ partial) {
+__device__ __forceinline__ void dist_row_chunk(const T* __restrict__ x, std::uint64_t ld,
+                                               std::uint64_t dim, const double* __restrict__ ref,
+                                               std::uint64_t nch_total, std::uint64_t c0,
+                                               double* __restrict__ partial, std::uint64_t i) {
   using V = typename ColVec<T>::V;
   constexpr int W = ColVec<T>::W;
-  const std::uint64_t c = blockIdx.x, i = blockIdx.y;
+  const std::uint64_t c = blockIdx.x;
   const T* row = x + i * ld;
   const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
   const bool vec = (ld % W == 0) && (reinterpret_cast<std::uintptr_t>(x) % 16 == 0);
@@ -405,6 +469,22 @@ __global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, st
   const double s = block_sum_fixed(acc);
   if (threadIdx.x == 0) partial[i * nch_total + c0 + c] = s;
 }
+
+// FAST: block (c, i) sums chunk c of row i in a fixed order (chunk offset c0
+// in the row's partials, so the slab-streamed and resident paths agree): each
+// thread takes 16-byte vectors (4 fp32 / 2 fp64 coordinates) 256 vectors
+// apart, sums its elements sequentially, then the block tree.
+template <typename T>
+__global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                                   const double* __restrict__ ref, std::uint64_t nch_total,
+                                   std::uint64_t c0, double* __restrict__ partial,
+                                   std::uint64_t n, const std::uint32_t* __restrict__ list,
+                                   const std::uint32_t* __restrict__ list_count) {
+  const std::uint64_t rows = list ? *list_count : n;
+  for (std::uint64_t y = blockIdx.y; y < rows; y += gridDim.y)
+    dist_row_chunk<T>(x, ld, dim, ref, nch_total, c0, partial, list ? list[y] : y);
+}
+
 
 __global__ void drift_fast_partial_off(const double* __restrict__ mean,
                                        const double* __restrict__ ref, std::uint64_t dim,
@@ -440,19 +520,40 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 
 std::uint64_t diag_chunk() { return kChunk; }
 
+// grid rows for the FAST partials over a representative list (the count is
+// on the device): about two waves of CTAs, each looping over rows
+unsigned fast_rows_grid(std::uint64_t n, std::uint64_t nch) {
+  const std::uint64_t y = std::max<std::uint64_t>(1, 2368 / std::max<std::uint64_t>(nch, 1));
+  return (unsigned)std::min<std::uint64_t>(n, y);
+}
+
 template <typename T>
 void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                       const double* ref, int exact, double* acc, double* partial,
-                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s) {
+                      std::uint64_t nch_total, std::uint64_t c0, cudaStream_t s,
+                      const RepRows* reps) {
   if (n == 0 || dim == 0) return;
+  const std::uint32_t* list = reps ? reps->list : nullptr;
+  const std::uint32_t* count = reps ? reps->count : nullptr;
   if (exact) {
-    launch_dist_exact<T>(x, n, ld, dim, ref, acc, 1, s);
+    launch_dist_exact<T>(x, n, ld, dim, ref, acc, 1, s, list, count);
     return;
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
-        x, ld, dim, ref, nch_total, c0, partial);
+    const unsigned gy = list ? fast_rows_grid(n, nch) : (unsigned)n;
+    dist_rows_fast_off<T><<<dim3((unsigned)nch, gy), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch_total, c0, partial, n, list, count);
   }
+  MB_LAUNCH_CHECK();
+}
+
+void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
+                       const std::uint8_t* gvoid, const std::uint32_t* counts, std::uint64_t n,
+                       std::uint32_t* rep, std::uint32_t* list, std::uint32_t* count,
+                       cudaStream_t s) {
+  MB_CUDA(cudaMemsetAsync(count, 0, 4, s));
+  build_reps_kernel<<<(unsigned)std::max<std::uint64_t>(1, (n + 255) / 256), 256, 0, s>>>(
+      members, goff, gvoid, counts, rep, list, count);
   MB_LAUNCH_CHECK();
 }
 
@@ -472,9 +573,13 @@ void launch_drift_slab(const double* mean, const double* ref, std::uint64_t dim,
 // Final reductions of the slab-streamed diagnostics.
 void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, double* acc,
                         double* row_partial, double* acc2, double* drift_partial,
-                        double* dist_out, double* drift_out, cudaStream_t s) {
+                        double* dist_out, double* drift_out, cudaStream_t s,
+                        const std::uint32_t* rep) {
   if (!exact) {
-    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(row_partial, n, nch_total, acc);
+    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(row_partial, n, nch_total, acc, rep);
+    MB_LAUNCH_CHECK();
+  } else if (rep) {
+    expand_reps<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(acc, rep, n);
     MB_LAUNCH_CHECK();
   }
   finish_distortion<<<1, kFinThreads, 0, s>>>(acc, n, dist_out);
@@ -490,10 +595,11 @@ void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, dou
 
 template void launch_dist_slab<float>(const float*, std::uint64_t, std::uint64_t, std::uint64_t,
                                       const double*, int, double*, double*, std::uint64_t,
-                                      std::uint64_t, cudaStream_t);
+                                      std::uint64_t, cudaStream_t, const RepRows*);
 template void launch_dist_slab<double>(const double*, std::uint64_t, std::uint64_t,
                                        std::uint64_t, const double*, int, double*, double*,
-                                       std::uint64_t, std::uint64_t, cudaStream_t);
+                                       std::uint64_t, std::uint64_t, cudaStream_t,
+                                       const RepRows*);
 
 std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
   const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
@@ -509,12 +615,12 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
   // the diagnostics' fp64 column means only (keeps the library small)
   if constexpr (std::is_same<Acc, double>::value) {
     constexpr int W = ColVec<T>::W;
-    const bool vec_ok = !rows && ld % W == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0;
+    const bool vec_ok = ld % W == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0;
     if (vec_ok && (n == 256 || n == 1024)) {
       const std::uint64_t nv = (dim + W - 1) / W;
       const unsigned blocks = (unsigned)((nv + 127) / 128);
-      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, out);
-      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, out);
+      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, rows, out);
+      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, rows, out);
       MB_LAUNCH_CHECK();
       return;
     }
@@ -528,20 +634,29 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
 template <typename T>
 void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq,
-                       double* partial, double* out, int exact, cudaStream_t s) {
+                       double* partial, double* out, int exact, cudaStream_t s,
+                       const RepRows* reps) {
   if (n == 0) {
     finish_distortion<<<1, kFinThreads, 0, s>>>(sq, 0, out);
     MB_LAUNCH_CHECK();
     return;
   }
+  const std::uint32_t* list = reps ? reps->list : nullptr;
+  const std::uint32_t* count = reps ? reps->count : nullptr;
+  const std::uint32_t* rep = reps ? reps->rep : nullptr;
   if (exact || dim == 0) {
-    launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s);
+    launch_dist_exact<T>(x, n, ld, dim, ref, sq, 0, s, list, count);
+    if (rep) {
+      expand_reps<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sq, rep, n);
+      MB_LAUNCH_CHECK();
+    }
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    dist_rows_fast_off<T><<<dim3((unsigned)nch, (unsigned)n), kRedThreads, 0, s>>>(
-        x, ld, dim, ref, nch, 0, partial);
+    const unsigned gy = list ? fast_rows_grid(n, nch) : (unsigned)n;
+    dist_rows_fast_off<T><<<dim3((unsigned)nch, gy), kRedThreads, 0, s>>>(
+        x, ld, dim, ref, nch, 0, partial, n, list, count);
     MB_LAUNCH_CHECK();
-    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq);
+    fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq, rep);
   }
   MB_LAUNCH_CHECK();
   finish_distortion<<<1, kFinThreads, 0, s>>>(sq, n, out);
@@ -585,7 +700,7 @@ void launch_broadcast_rows(T* dst, std::uint64_t ld, const T* row,
                                           cudaStream_t);                                \
   template void launch_distortion<T>(const T*, std::uint64_t, std::uint64_t,            \
                                      std::uint64_t, const double*, double*, double*,    \
-                                     double*, int, cudaStream_t);                       \
+                                     double*, int, cudaStream_t, const RepRows*);       \
   template void launch_fill_synthetic<T>(T*, std::uint64_t, std::uint64_t,              \
                                          std::uint64_t, std::uint64_t, std::uint64_t,   \
                                          cudaStream_t);                                 \

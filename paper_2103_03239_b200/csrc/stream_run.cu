@@ -112,6 +112,7 @@ struct StreamWorkspace {
   int dev = -1;
   std::unique_ptr<DeviceBuffer> ring[3];
   DeviceBuffer t_mem, t_goff, t_act, t_cnt, ref, mean_s, acc, acc2, rpart, dpart, out;
+  DeviceBuffer t_rep, t_rlist, t_rcount;  // representatives of every round (RepRows)
   std::unique_ptr<Plane> plane;
   std::uint32_t pM = 0, pd = 0;
   std::uint64_t pn = 0;
@@ -187,8 +188,20 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src,
   t_goff.resize(R * (n + 1) * 4 + 16);
   t_act.resize(R * n * 4 + 16);
   t_cnt.resize(R * 16 + 16);
+  const bool dgr = diag != MOSHPIT_DIAG_NONE;
+  if (dgr) {
+    ws.t_rep.resize(R * n * 4 + 16);
+    ws.t_rlist.resize(R * n * 4 + 16);
+    ws.t_rcount.resize(R * 4 + 16);
+  }
   for (std::uint64_t r = 0; r < R; ++r) {
     active[r] = plane.round(&fail, p, clock, 0, nullptr, 0, 0, s_cmp.s, 0);
+    if (dgr)  // the rows of every averaged group are identical after round r
+      launch_build_reps(plane.members.as<std::uint32_t>(), plane.goff.as<std::uint32_t>(),
+                        plane.gvoid.as<std::uint8_t>(), plane.counts.as<std::uint32_t>(), n,
+                        ws.t_rep.as<std::uint32_t>() + r * n,
+                        ws.t_rlist.as<std::uint32_t>() + r * n,
+                        ws.t_rcount.as<std::uint32_t>() + r, s_cmp.s);
     MB_CUDA(cudaMemcpyAsync(t_mem.as<std::uint32_t>() + r * n, plane.members.ptr, n * 4,
                             cudaMemcpyDeviceToDevice, s_cmp.s));
     MB_CUDA(cudaMemcpyAsync(t_goff.as<std::uint32_t>() + r * (n + 1), plane.goff.ptr,
@@ -292,9 +305,12 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src,
         // read the slab: run them side by side, join before the next round
         MB_CUDA(cudaEventRecord(ws.ev_fork, s_cmp.s));
         MB_CUDA(cudaStreamWaitEvent(ws.s_aux->s, ws.ev_fork, 0));
+        const RepRows rr{ws.t_rep.as<std::uint32_t>() + r * n,
+                         ws.t_rlist.as<std::uint32_t>() + r * n,
+                         ws.t_rcount.as<std::uint32_t>() + r};
         launch_dist_slab<T>(x, n, W, w, refj, exact, acc.as<double>() + (r + 1) * n,
-                            rpart.as<double>() + (r + 1) * n * nch, nch, c0, s_cmp.s);
-        launch_colmean<T, double>(x, n, W, w, nullptr, mean_s.as<double>(), ws.s_aux->s);
+                            rpart.as<double>() + (r + 1) * n * nch, nch, c0, s_cmp.s, &rr);
+        launch_colmean<T, double>(x, n, W, w, rr.rep, mean_s.as<double>(), ws.s_aux->s);
         launch_drift_slab(mean_s.as<double>(), refj, w, exact, acc2.as<double>() + 2 * (r + 1),
                           dpart.as<double>() + (r + 1) * 2 * nch, c0, ws.s_aux->s);
         MB_CUDA(cudaEventRecord(ws.ev_join, ws.s_aux->s));
@@ -334,7 +350,7 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src,
                          acc2.as<double>() + 2 * r,
                          exact ? nullptr : dpart.as<double>() + r * 2 * nch,
                          r == 0 ? o : o + 2 + (r - 1), r == 0 ? nullptr : o + 2 + R + (r - 1),
-                         s_cmp.s);
+                         s_cmp.s, r == 0 ? nullptr : ws.t_rep.as<std::uint32_t>() + (r - 1) * n);
     std::vector<double> h(2 * R + 2);
     MB_CUDA(cudaMemcpyAsync(h.data(), o, h.size() * 8, cudaMemcpyDeviceToHost, s_cmp.s));
     MB_CUDA(cudaStreamSynchronize(s_cmp.s));

@@ -566,3 +566,30 @@ def test_column_means_equal_reference(mb, ref, n):
     every leaf / split boundary (core.hpp:72-81, 128-133)."""
     x = np.random.default_rng(n).standard_normal((n, 45))
     assert bits_equal(mb.mean_of(x), ref.mean_of(x))
+
+
+@pytest.mark.parametrize("diag", ["fast", "exact"])
+def test_engine_round_record_equals_round_then_record(mb, torch, diag):
+    """round_record reads one representative row per averaged group (every
+    member holds the same mean); the report must equal round() + record()
+    bit for bit (which read every row)."""
+    M, d, n, p, R, dim = 32, 2, 1024, 0.05, 5, 4096
+    x0 = torch.empty((n, dim), dtype=torch.float32, device="cuda")
+    mb.fill_synthetic(x0, INIT_SEED)
+    reports = []
+    for combined in (False, True):
+        x = x0.clone()
+        eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+        eng.set_reference(x, diagnostics=diag)
+        for _ in range(R):
+            if combined:
+                eng.round_record(x)
+            else:
+                eng.round(x)
+                eng.record(x)
+        reports.append(eng.report())
+        eng.close()
+    (i0, d0, f0), (i1, d1, f1) = reports
+    assert bits_equal(np.array([i0]), np.array([i1]))
+    assert bits_equal(np.array(d0), np.array(d1))
+    assert bits_equal(np.array(f0), np.array(f1))
