@@ -476,14 +476,14 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
                                  rr);
         if (drift_slot)
           launch_colmean<float, double>(d_x.as<float>(), n, ld, dim, rows,
-                                        d_mean.as<double>(), aux.s);
+                                        d_mean.as<double>(), aux.s, true);
       } else {
         launch_distortion<double>(d_x.as<double>(), n, ld, dim, d_ref.as<double>(),
                                   d_sq.as<double>(), d_part.as<double>(), dist_slot, exact, st.s,
                                   rr);
         if (drift_slot)
           launch_colmean<double, double>(d_x.as<double>(), n, ld, dim, rows,
-                                         d_mean.as<double>(), aux.s);
+                                         d_mean.as<double>(), aux.s, true);
       }
       if (drift_slot) {
         launch_drift(d_mean.as<double>(), d_ref.as<double>(), dim, d_part2.as<double>(),
@@ -883,7 +883,7 @@ void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t 
                        e->part.as<double>(), dist_slot, exact, s, reps);
   if (drift_slot) {
     launch_colmean<T, double>(x, n, ld, dim, reps ? reps->rep : nullptr, e->mean.as<double>(),
-                              e->aux->s);
+                              e->aux->s, true);
     launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
                  drift_slot, exact, e->aux->s);
     MB_CUDA(cudaEventRecord(e->ev_join, e->aux->s));

@@ -327,7 +327,7 @@ void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
 template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
-                    cudaStream_t s);
+                    cudaStream_t s, bool rows_optional = false);
 template <typename T>
 void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq_scratch,

@@ -521,9 +521,9 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 std::uint64_t diag_chunk() { return kChunk; }
 
 // grid rows for the FAST partials over a representative list (the count is
-// on the device): about two waves of CTAs, each looping over rows
+// on the device): ~16 waves of CTAs, each looping over a few rows
 unsigned fast_rows_grid(std::uint64_t n, std::uint64_t nch) {
-  const std::uint64_t y = std::max<std::uint64_t>(1, 2368 / std::max<std::uint64_t>(nch, 1));
+  const std::uint64_t y = std::max<std::uint64_t>(1, 16 * 2368 / std::max<std::uint64_t>(nch, 1));
   return (unsigned)std::min<std::uint64_t>(n, y);
 }
 
@@ -610,7 +610,7 @@ std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
 template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool rows_optional) {
   if (dim == 0 || n == 0) return;
   // the diagnostics' fp64 column means only (keeps the library small)
   if constexpr (std::is_same<Acc, double>::value) {
@@ -619,8 +619,12 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
     if (vec_ok && (n == 256 || n == 1024)) {
       const std::uint64_t nv = (dim + W - 1) / W;
       const unsigned blocks = (unsigned)((nv + 127) / 128);
-      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, rows, out);
-      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, rows, out);
+      // the representative gather pays off for fp64 rows (C2: 2.0 vs 4.7 ms)
+      // but not for fp32 (6.2 vs 2.6 ms: the gather's shared-memory index
+      // loads cost more than the HBM bytes it saves)
+      const std::uint32_t* g = (rows_optional && !std::is_same<T, double>::value) ? nullptr : rows;
+      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
+      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
       MB_LAUNCH_CHECK();
       return;
     }
@@ -697,7 +701,7 @@ void launch_broadcast_rows(T* dst, std::uint64_t ld, const T* row,
 #define MB_INST(T)                                                                      \
   template void launch_colmean<T, double>(const T*, std::uint64_t, std::uint64_t,       \
                                           std::uint64_t, const std::uint32_t*, double*, \
-                                          cudaStream_t);                                \
+                                          cudaStream_t, bool);                          \
   template void launch_distortion<T>(const T*, std::uint64_t, std::uint64_t,            \
                                      std::uint64_t, const double*, double*, double*,    \
                                      double*, int, cudaStream_t, const RepRows*);       \
@@ -710,7 +714,7 @@ MB_INST(float)
 MB_INST(double)
 template void launch_colmean<float, float>(const float*, std::uint64_t, std::uint64_t,
                                           std::uint64_t, const std::uint32_t*, float*,
-                                          cudaStream_t);
+                                          cudaStream_t, bool);
 #undef MB_INST
 
 }  // namespace mb200

@@ -310,7 +310,7 @@ void run_moshpit_streamed(std::uint32_t M, std::uint32_t d, const HostRows& src,
                          ws.t_rcount.as<std::uint32_t>() + r};
         launch_dist_slab<T>(x, n, W, w, refj, exact, acc.as<double>() + (r + 1) * n,
                             rpart.as<double>() + (r + 1) * n * nch, nch, c0, s_cmp.s, &rr);
-        launch_colmean<T, double>(x, n, W, w, rr.rep, mean_s.as<double>(), ws.s_aux->s);
+        launch_colmean<T, double>(x, n, W, w, rr.rep, mean_s.as<double>(), ws.s_aux->s, true);
         launch_drift_slab(mean_s.as<double>(), refj, w, exact, acc2.as<double>() + 2 * (r + 1),
                           dpart.as<double>() + (r + 1) * 2 * nch, c0, ws.s_aux->s);
         MB_CUDA(cudaEventRecord(ws.ev_join, ws.s_aux->s));
