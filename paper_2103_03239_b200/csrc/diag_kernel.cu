@@ -521,9 +521,14 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 std::uint64_t diag_chunk() { return kChunk; }
 
 // grid rows for the FAST partials over a representative list (the count is
-// on the device): ~16 waves of CTAs, each looping over a few rows
+// on the device): ~2 waves of CTAs, each looping over rows (1, 4 and 16
+// waves measured the same)
 unsigned fast_rows_grid(std::uint64_t n, std::uint64_t nch) {
-  const std::uint64_t y = std::max<std::uint64_t>(1, 16 * 2368 / std::max<std::uint64_t>(nch, 1));
+  static const std::uint64_t waves = [] {
+    const char* e = std::getenv("MOSHPIT_FAST_ROW_WAVES");
+    return (std::uint64_t)(e ? std::max(1, std::atoi(e)) : 2);
+  }();
+  const std::uint64_t y = std::max<std::uint64_t>(1, waves * 2368 / std::max<std::uint64_t>(nch, 1));
   return (unsigned)std::min<std::uint64_t>(n, y);
 }
 
@@ -619,10 +624,18 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
     if (vec_ok && (n == 256 || n == 1024)) {
       const std::uint64_t nv = (dim + W - 1) / W;
       const unsigned blocks = (unsigned)((nv + 127) / 128);
-      // the representative gather pays off for fp64 rows (C2: 2.0 vs 4.7 ms)
-      // but not for fp32 (6.2 vs 2.6 ms: the gather's shared-memory index
-      // loads cost more than the HBM bytes it saves)
-      const std::uint32_t* g = (rows_optional && !std::is_same<T, double>::value) ? nullptr : rows;
+      // the representative gather: alone, the fp32 kernel is slower with it
+      // (6.2 vs 2.6 ms at C2: the index loads cost more than the HBM bytes
+      // saved; fp64 2.0 vs 4.7 ms), but beside the distortion on the other
+      // stream the saved bytes win: C2 round + FAST record 10.25 vs 11.74 ms
+      // (profiles/r02/reps_gather_ab.txt).  MOSHPIT_REP_GATHER_F32=0 turns
+      // it off for fp32.
+      static const bool gather32 = [] {
+        const char* e = std::getenv("MOSHPIT_REP_GATHER_F32");
+        return !e || std::atoi(e) != 0;
+      }();
+      const std::uint32_t* g =
+          (rows_optional && !std::is_same<T, double>::value && !gather32) ? nullptr : rows;
       if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
       else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
       MB_LAUNCH_CHECK();
