@@ -39,12 +39,15 @@
 namespace mb200 {
 namespace {
 
-constexpr int kTcM = 128, kTcN = 128, kTcK = 32;  // tile; kTcK fp32 = one 128-byte row
+constexpr int kTcM = 128, kTcK = 32;  // tile rows; kTcK fp32 = one 128-byte row
 constexpr int kTcStages = 3;
 constexpr int kTcThreads = 128;
-constexpr int kTileBytes = kTcM * kTcK * 4;  // 16 KB per operand tile
-constexpr int kStageBytes = 4 * kTileBytes;  // A_hi, A_lo, B_hi, B_lo
-constexpr std::size_t kTcSmem = (std::size_t)kTcStages * kStageBytes + 1024 + 128;
+constexpr int kTileBytes = kTcM * kTcK * 4;  // 16 KB per A tile
+// stage: A_hi, A_lo (128 rows) + B_hi, B_lo (BN rows)
+template <int BN>
+__host__ __device__ constexpr int stage_bytes() { return 2 * kTileBytes + 2 * BN * kTcK * 4; }
+template <int BN>
+__host__ __device__ constexpr std::size_t tc_smem() { return (std::size_t)kTcStages * stage_bytes<BN>() + 1024 + 128; }
 
 __device__ __forceinline__ std::uint32_t su32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -65,16 +68,18 @@ __device__ __forceinline__ std::uint64_t sw128_desc(std::uint32_t saddr) {
 
 // Instruction descriptor kind::tf32 (InstrDescriptor): D f32 (bits 4-5 = 1),
 // A, B tf32 (bits 7-9, 10-12 = 2), both K-major, N >> 3 at bit 17, M >> 4 at 24.
-constexpr std::uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                                 ((std::uint32_t)(kTcN >> 3) << 17) |
-                                 ((std::uint32_t)(kTcM >> 4) << 24);
+template <int BN>
+__host__ __device__ constexpr std::uint32_t idesc_tf32() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((std::uint32_t)(BN >> 3) << 17) |
+         ((std::uint32_t)(kTcM >> 4) << 24);
+}
 
 __device__ __forceinline__ void mma_tf32(std::uint32_t tmem_d, std::uint64_t a, std::uint64_t b,
-                                         std::uint32_t accumulate) {
+                                         std::uint32_t idesc, std::uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mbar_init1(std::uint64_t* bar) {
@@ -162,20 +167,22 @@ struct TcArgs {
   double* nsq_out;
 };
 
-template <int EPI>
+template <int EPI, int BN>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_gemm_kernel(TcArgs a, const __grid_constant__ CUtensorMap tm_ah,
                    const __grid_constant__ CUtensorMap tm_al,
                    const __grid_constant__ CUtensorMap tm_bh,
                    const __grid_constant__ CUtensorMap tm_bl) {
+  constexpr int kStage = stage_bytes<BN>();
+  constexpr int kBTile = BN * kTcK * 4;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment of the operand tiles (the 128B-swizzle atom)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<std::uintptr_t>(tc_smem_raw) + 1023) & ~std::uintptr_t(1023));
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kStageBytes);
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kTcStages * kStage);
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kTcStages + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const std::uint64_t m0 = (std::uint64_t)blockIdx.y * kTcM, n0 = (std::uint64_t)blockIdx.x * kTcN;
+  const std::uint64_t m0 = (std::uint64_t)blockIdx.y * kTcM, n0 = (std::uint64_t)blockIdx.x * BN;
 
   if (tid == 0) {
     for (int s = 0; s < 2 * kTcStages + 1; ++s) mbar_init1(&bars[s]);
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "n"(kTcN));
+                 "n"(BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -202,42 +209,45 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                    reinterpret_cast<std::uint64_t>(&tm_al),
                                    reinterpret_cast<std::uint64_t>(&tm_bh),
                                    reinterpret_cast<std::uint64_t>(&tm_bl)};
+    const std::uint32_t toff[4] = {0u, (std::uint32_t)kTileBytes, 2u * kTileBytes,
+                                   2u * kTileBytes + kBTile};
     for (std::uint64_t kb = 0; kb < nk; ++kb) {
       const int st = (int)(kb % kTcStages);
       if (kb >= (std::uint64_t)kTcStages)  // MMAs of slab kb - kTcStages freed this stage
         mbar_wait_bounded(&empty[st], (std::uint32_t)((kb / kTcStages - 1) & 1));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])),
-                   "r"(kStageBytes)
+                   "r"(kStage)
                    : "memory");
-      const std::uint32_t base = su32(smem + st * kStageBytes);
+      const std::uint32_t base = su32(smem + st * kStage);
       const int k0 = (int)(kb * kTcK);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int r0 = (int)(t < 2 ? m0 : n0);
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + t * kTileBytes),
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(base + toff[t]),
             "l"(maps[t]), "r"(k0), "r"(r0), "r"(su32(&full[st]))
             : "memory");
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ===== MMA issuer =====
+    constexpr std::uint32_t idesc = idesc_tf32<BN>();
     for (std::uint64_t kb = 0; kb < nk; ++kb) {
       const int st = (int)(kb % kTcStages);
       mbar_wait_bounded(&full[st], (std::uint32_t)((kb / kTcStages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const std::uint32_t sb = su32(smem + st * kStageBytes);
+      const std::uint32_t sb = su32(smem + st * kStage);
 #pragma unroll
       for (int kk = 0; kk < kTcK / 8; ++kk) {  // K = 8 tf32 (32 bytes) per MMA
         const std::uint32_t off = kk * 32;
-        const std::uint64_t ah = sw128_desc(sb + 0 * kTileBytes + off);
-        const std::uint64_t al = sw128_desc(sb + 1 * kTileBytes + off);
+        const std::uint64_t ah = sw128_desc(sb + off);
+        const std::uint64_t al = sw128_desc(sb + kTileBytes + off);
         const std::uint64_t bh = sw128_desc(sb + 2 * kTileBytes + off);
-        const std::uint64_t bl = sw128_desc(sb + 3 * kTileBytes + off);
-        mma_tf32(tmem, al, bh, (kb | kk) != 0);
-        mma_tf32(tmem, ah, bl, 1);
-        mma_tf32(tmem, ah, bh, 1);
+        const std::uint64_t bl = sw128_desc(sb + 2 * kTileBytes + kBTile + off);
+        mma_tf32(tmem, al, bh, idesc, (kb | kk) != 0);
+        mma_tf32(tmem, ah, bl, idesc, 1);
+        mma_tf32(tmem, ah, bh, idesc, 1);
       }
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -254,59 +264,90 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (nk) mbar_wait_bounded(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // epilogue: row m0 + 32 warp + lane, 32 columns per TMEM load
+  // Epilogue: thread (warp, lane) owns tile row 32 warp + lane (its TMEM lane),
+  // 32 columns per TMEM load.  Global traffic goes through a per-warp 32 x 33
+  // shared-memory transpose (the operand ring is idle now), so every global
+  // access is a 128-byte row segment.
+  float* tw = reinterpret_cast<float*>(smem) + warp * 3 * 32 * 33;  // 3 tiles per warp
+  float* t0 = tw;
+  float* t1 = tw + 32 * 33;
+  float* t2 = tw + 2 * 32 * 33;
   const std::uint64_t row = m0 + warp * 32 + lane;
+  const std::uint64_t rbase = m0 + warp * 32;
   double nsq = 0.0;
   bool bad = false;
-  for (int cc = 0; cc < kTcN; cc += 32) {
+  for (int cc = 0; cc < BN; cc += 32) {
     float acc[32];
     tmem_ld32(tmem + ((std::uint32_t)(warp * 32) << 16) + (std::uint32_t)cc, acc);
     if (nk == 0) {
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = 0.f;
     }
-    if (row >= a.M) continue;
+    const std::uint64_t col = n0 + cc + lane;  // this lane's column in the coalesced passes
     if constexpr (EPI == 0) {
-      // c = -y / (1 + exp(y m))  (optimizer.hpp:126), then the tf32 split
+      // c = -y / (1 + exp(y m))  (optimizer.hpp:126) in fp32 (this is the fp32
+      // path), then the tf32 split; y of column cc + q
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
-        const std::uint64_t col = n0 + cc + q;
-        if (col >= a.N) break;
-        const double y = a.ys[col];
-        const float c = (float)(-y / (1.0 + exp(y * (double)acc[q])));
+        const std::uint64_t cq = n0 + cc + q;
+        const float y = cq < a.N ? (float)a.ys[cq] : 0.f;
+        const float c = __fdiv_rn(-y, __fadd_rn(1.0f, expf(__fmul_rn(y, acc[q]))));
         float h, l;
         tf32_split(c, h, l);
-        a.c_hi[row * a.N + col] = h;
-        a.c_lo[row * a.N + col] = l;
+        t0[lane * 33 + q] = h;
+        t1[lane * 33 + q] = l;
       }
-    } else {
-      // g = G / S + l2 theta (+ noise); theta -= gamma g  (optimizer.hpp:133-135, 356-373):
-      // the same per-element arithmetic and Philox quads as logit_grad_tiled
-#pragma unroll
-      for (int q4 = 0; q4 < 8; ++q4) {
-        const std::uint64_t j4 = n0 + cc + q4 * 4;
-        if (j4 >= a.N) break;
-        float z[4] = {0.f, 0.f, 0.f, 0.f};
-        if (a.philox) philox_normals4(a.pk, a.step, row, j4 >> 2, z);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const std::uint64_t j = j4 + u;
-          if (j >= a.N) break;
-          float* p = a.theta + row * a.ld_theta + j;
-          const double g = __dadd_rn(__ddiv_rn((double)acc[q4 * 4 + u], a.S),
-                                     __dmul_rn(a.l2, (double)*p));
-          float gt = (float)g;
-          if (a.noise) {
-            gt = __fadd_rn(gt, a.noise[row * a.N + j]);
-          } else if (a.philox) {
-            const float nj = noise_component(z[u], a.coord_std, (float*)nullptr);
-            nsq += (double)nj * (double)nj;
-            gt = __fadd_rn(gt, nj);
-          }
-          if (!isfinite(gt)) bad = true;
-          *p = __fsub_rn(*p, __fmul_rn(a.gamma, gt));
+      __syncwarp();
+      for (int r = 0; r < 32; ++r) {
+        const std::uint64_t gr = rbase + r;
+        if (gr < a.M && col < a.N) {
+          a.c_hi[gr * a.N + col] = t0[r * 33 + lane];
+          a.c_lo[gr * a.N + col] = t1[r * 33 + lane];
         }
       }
+      __syncwarp();
+    } else {
+      // g = G / S + l2 theta (+ noise); theta -= gamma g  (optimizer.hpp:133-135,
+      // 356-373): the same per-element arithmetic and Philox quads as
+      // logit_grad_tiled.  theta rows in and out through the transpose tile.
+      for (int r = 0; r < 32; ++r) {
+        const std::uint64_t gr = rbase + r;
+        t2[r * 33 + lane] = (gr < a.M && col < a.N) ? a.theta[gr * a.ld_theta + col] : 0.f;
+      }
+      __syncwarp();
+      if (row < a.M) {
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const std::uint64_t j4 = n0 + cc + q4 * 4;
+          if (j4 >= a.N) break;
+          float z[4] = {0.f, 0.f, 0.f, 0.f};
+          if (a.philox && !a.noise) philox_normals4(a.pk, a.step, row, j4 >> 2, z);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const std::uint64_t j = j4 + u;
+            if (j >= a.N) break;
+            float& th = t2[lane * 33 + q4 * 4 + u];
+            const double g = __dadd_rn(__ddiv_rn((double)acc[q4 * 4 + u], a.S),
+                                       __dmul_rn(a.l2, (double)th));
+            float gt = (float)g;
+            if (a.noise) {
+              gt = __fadd_rn(gt, a.noise[row * a.N + j]);
+            } else if (a.philox) {
+              const float nj = noise_component(z[u], a.coord_std, (float*)nullptr);
+              nsq += (double)nj * (double)nj;
+              gt = __fadd_rn(gt, nj);
+            }
+            if (!isfinite(gt)) bad = true;
+            th = __fsub_rn(th, __fmul_rn(a.gamma, gt));
+          }
+        }
+      }
+      __syncwarp();
+      for (int r = 0; r < 32; ++r) {
+        const std::uint64_t gr = rbase + r;
+        if (gr < a.M && col < a.N) a.theta[gr * a.ld_theta + col] = t2[r * 33 + lane];
+      }
+      __syncwarp();
     }
   }
   if constexpr (EPI == 1) {
@@ -319,7 +360,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -338,11 +379,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // 2-D fp32 map over [rows x cols] (row stride ld elements): boxes of
 // kTcK x 128 (one 128-byte row per tile row), 128B swizzle, zero fill.
 CUtensorMap operand_map(const float* base, std::uint64_t rows, std::uint64_t cols,
-                        std::uint64_t ld) {
+                        std::uint64_t ld, std::uint32_t box_rows) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {ld * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kTcK, 128};
+  const cuuint32_t box[2] = {(cuuint32_t)kTcK, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = tensor_map_encoder()(
       &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
@@ -352,22 +393,22 @@ CUtensorMap operand_map(const float* base, std::uint64_t rows, std::uint64_t col
   return m;
 }
 
-template <int EPI>
+template <int EPI, int BN>
 void launch_tc(const TcArgs& a, cudaStream_t s) {
   static int attr_dev = -1;
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
   if (attr_dev != dev) {
-    MB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTcSmem));
+    MB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<EPI, BN>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem<BN>()));
     attr_dev = dev;
   }
-  const dim3 grid((unsigned)((a.N + kTcN - 1) / kTcN), (unsigned)((a.M + kTcM - 1) / kTcM));
-  const CUtensorMap ah = operand_map(a.a_hi, a.M, a.K, a.lda);
-  const CUtensorMap al = operand_map(a.a_lo, a.M, a.K, a.lda);
-  const CUtensorMap bh = operand_map(a.b_hi, a.N, a.K, a.ldb);
-  const CUtensorMap bl = operand_map(a.b_lo, a.N, a.K, a.ldb);
-  tc_gemm_kernel<EPI><<<grid, kTcThreads, kTcSmem, s>>>(a, ah, al, bh, bl);
+  const dim3 grid((unsigned)((a.N + BN - 1) / BN), (unsigned)((a.M + kTcM - 1) / kTcM));
+  const CUtensorMap ah = operand_map(a.a_hi, a.M, a.K, a.lda, kTcM);
+  const CUtensorMap al = operand_map(a.a_lo, a.M, a.K, a.lda, kTcM);
+  const CUtensorMap bh = operand_map(a.b_hi, a.N, a.K, a.ldb, BN);
+  const CUtensorMap bl = operand_map(a.b_lo, a.N, a.K, a.ldb, BN);
+  tc_gemm_kernel<EPI, BN><<<grid, kTcThreads, tc_smem<BN>(), s>>>(a, ah, al, bh, bl);
   MB_LAUNCH_CHECK();
 }
 
@@ -414,7 +455,7 @@ void logit_tc_step(float* theta, std::uint64_t n, std::uint64_t ld, std::uint64_
   a.ys = ys;
   a.c_hi = c_hi;
   a.c_lo = c_lo;
-  launch_tc<0>(a, s);
+  launch_tc<0, 128>(a, s);
   TcArgs b{};
   b.a_hi = c_hi;
   b.a_lo = c_lo;
@@ -437,7 +478,8 @@ void logit_tc_step(float* theta, std::uint64_t n, std::uint64_t ld, std::uint64_
   b.step = step;
   b.nonfinite = nonfinite;
   b.nsq_out = nsq_out;
-  launch_tc<1>(b, s);
+  // 64-wide tiles: 128 output tiles for N = D = 1024 instead of 64 on 148 SMs
+  launch_tc<1, 64>(b, s);
 }
 
 }  // namespace mb200
