@@ -40,14 +40,21 @@ namespace mb200 {
 namespace {
 
 constexpr int kTcM = 128, kTcK = 32;  // tile rows; kTcK fp32 = one 128-byte row
-constexpr int kTcStages = 3;
 constexpr int kTcThreads = 128;
 constexpr int kTileBytes = kTcM * kTcK * 4;  // 16 KB per A tile
 // stage: A_hi, A_lo (128 rows) + B_hi, B_lo (BN rows)
 template <int BN>
 __host__ __device__ constexpr int stage_bytes() { return 2 * kTileBytes + 2 * BN * kTcK * 4; }
+// as many ring stages as fit (the K loop is TMA-latency bound): 3 of 64 KB for
+// 128-wide tiles, 4 of 48 KB for 64-wide
 template <int BN>
-__host__ __device__ constexpr std::size_t tc_smem() { return (std::size_t)kTcStages * stage_bytes<BN>() + 1024 + 128; }
+__host__ __device__ constexpr int tc_stages() {
+  return (200 * 1024) / stage_bytes<BN>() > 4 ? 4 : (200 * 1024) / stage_bytes<BN>();
+}
+template <int BN>
+__host__ __device__ constexpr std::size_t tc_smem() {
+  return (std::size_t)tc_stages<BN>() * stage_bytes<BN>() + 1024 + 128;
+}
 
 __device__ __forceinline__ std::uint32_t su32(const void* p) {
   return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -175,6 +182,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const __grid_constant__ CUtensorMap tm_bl) {
   constexpr int kStage = stage_bytes<BN>();
   constexpr int kBTile = BN * kTcK * 4;
+  constexpr int kTcStages = tc_stages<BN>();
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   // 1024-byte alignment of the operand tiles (the 128B-swizzle atom)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -479,7 +487,10 @@ void logit_tc_step(float* theta, std::uint64_t n, std::uint64_t ld, std::uint64_
   b.nonfinite = nonfinite;
   b.nsq_out = nsq_out;
   // 64-wide tiles: 128 output tiles for N = D = 1024 instead of 64 on 148 SMs
-  launch_tc<1, 64>(b, s);
+  // (MOSHPIT_TC_GRAD_BN=128 for the 128-wide form)
+  const char* e = std::getenv("MOSHPIT_TC_GRAD_BN");
+  if (e && std::atoi(e) == 128) launch_tc<1, 128>(b, s);
+  else launch_tc<1, 64>(b, s);
 }
 
 }  // namespace mb200
