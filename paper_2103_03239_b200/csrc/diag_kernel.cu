@@ -51,13 +51,20 @@ __global__ void colmean_kernel(const T* __restrict__ x, std::uint64_t n,
   out[j] = AccOps<Acc>::div(s, (Acc)n);
 }
 
-// Column means for the configs' peer counts (N = 256 / 1024): the
-// reference tree over the N rows unrolled at compile time (n <= 8 sequential
-// from +0, else split at floor(n/2): exactly pairwise_rt's tree), each thread
-// owning one 16-byte column vector (4 fp32 or 2 fp64 columns).  No stack, no
-// runtime leaf loop: every row load is independent of the adds, so a thread
-// keeps many 16-byte loads in flight (the runtime-tree kernel keeps one
-// 4-byte load per thread in flight).
+// Column means for peer counts n = 8 * 2^K (the configs' 256, 1024, 4096):
+// the reference tree (n <= 8 summed sequentially from +0, else split at
+// floor(n/2); core.hpp:72-81) is then a perfect binary tree over n/8
+// sequential 8-row blocks, evaluated left to right with a K-level binary
+// counter of pending left subtrees (block b merges with the pending sums at
+// the levels where b has a 1 bit: left + right, exactly the tree's adds).
+// Each thread owns one 16-byte column vector (4 fp32 or 2 fp64 columns) and
+// streams its own 16-byte pieces of the block rows into shared memory with
+// cp.async, kCmStages blocks ahead: no thread reads another's data, so the
+// pipeline needs no barriers, and the registers hold only the K-level stack
+// (the previous fully unrolled tree let the compiler hoist every row load:
+// 255 registers and a 1.2 KB stack frame, 8 warps/SM, latency-bound).
+// rows (optional): element i of the tree is row rows[i] -- the representative
+// gather (RepRows): identical values, fewer distinct rows read from HBM.
 template <typename T>
 struct ColVec;
 template <>
@@ -71,6 +78,120 @@ struct ColVec<double> {
   static constexpr int W = 2;
 };
 
+constexpr int kCmThreads = 128;
+constexpr int kCmStages = 4;
+constexpr int kCmMaxK = 10;  // n up to 8192
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<std::uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(kCmThreads)
+    colmean_staged(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                   const std::uint32_t* __restrict__ rows, double* __restrict__ out) {
+  using V = typename ColVec<T>::V;
+  constexpr int W = ColVec<T>::W;
+  constexpr int N = 8 << K, NB = 1 << K;
+  extern __shared__ __align__(16) unsigned char cm_smem[];
+  V* const ring = reinterpret_cast<V*>(cm_smem);  // [stage][8 rows][kCmThreads]
+  std::uint32_t* const s_rows =
+      reinterpret_cast<std::uint32_t*>(ring + kCmStages * 8 * kCmThreads);
+  if (rows) {
+    for (int i = threadIdx.x; i < N; i += kCmThreads) s_rows[i] = rows[i];
+    __syncthreads();
+  }
+  const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
+  if (cv * W >= dim) return;
+  const std::uint64_t ldv = ld / W;
+  const V* const col = reinterpret_cast<const V*>(x) + cv;
+  V* const mine = ring + threadIdx.x;
+  auto issue = [&](int b) {
+    if (b < NB) {
+      V* dst = mine + (b % kCmStages) * 8 * kCmThreads;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const std::uint32_t r = rows ? s_rows[b * 8 + q] : (std::uint32_t)(b * 8 + q);
+        cp_async16(dst + q * kCmThreads, col + (std::uint64_t)r * ldv);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  };
+#pragma unroll
+  for (int b = 0; b < kCmStages - 1; ++b) issue(b);
+  double stk[K > 0 ? K : 1][W];
+  double v[W];
+#pragma unroll 1
+  for (int b = 0; b < NB; ++b) {
+    issue(b + kCmStages - 1);
+    cp_async_wait<kCmStages - 1>();
+    const V* src = mine + (b % kCmStages) * 8 * kCmThreads;
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const V e = src[q * kCmThreads];
+      const T* pe = reinterpret_cast<const T*>(&e);
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = __dadd_rn(v[w], (double)pe[w]);
+    }
+    bool placed = false;
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      if (!placed) {
+        if ((b >> l) & 1) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) v[w] = __dadd_rn(stk[l][w], v[w]);
+        } else {
+#pragma unroll
+          for (int w = 0; w < W; ++w) stk[l][w] = v[w];
+          placed = true;
+        }
+      }
+    }
+  }
+  // after block NB - 1 (all bits set) v holds the whole tree
+#pragma unroll
+  for (int w = 0; w < W; ++w)
+    if (cv * W + w < dim) out[cv * W + w] = __ddiv_rn(v[w], (double)N);
+}
+
+template <int K, typename T>
+void launch_colmean_staged(const T* x, std::uint64_t ld, std::uint64_t dim,
+                           const std::uint32_t* rows, double* out, cudaStream_t s) {
+  constexpr int W = ColVec<T>::W;
+  constexpr std::size_t smem =
+      (std::size_t)kCmStages * 8 * kCmThreads * 16 + ((std::size_t)8 << K) * 4;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  MB_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    MB_CUDA(cudaFuncSetAttribute(colmean_staged<K, T>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev = dev;
+  }
+  const std::uint64_t nv = (dim + W - 1) / W;
+  colmean_staged<K, T><<<(unsigned)((nv + kCmThreads - 1) / kCmThreads), kCmThreads, smem, s>>>(
+      x, ld, dim, rows, out);
+}
+
+// fp64 state, n = 256 / 1024: the tree fully unrolled at compile time, one
+// 16-byte column vector (2 columns) per thread, no shared memory.  Measured
+// against the staged form at C2 (1024 x 4 Mi fp64): 1.9-2.2 vs 2.6 ms with the
+// representative gather, and beside the EXACT distortion on the other stream
+// it leaves that kernel's CTAs room (the staged form's 68 KB of shared memory
+// per CTA cost the EXACT record 2.6 ms per round).  The same unrolled form
+// for fp32 state hoists every row load (255 registers, 1.2 KB of stack).
 template <int N, typename T, typename Acc>
 __device__ __forceinline__ void ctree(const typename ColVec<T>::V* __restrict__ col,
                                       std::uint64_t ldv, int base, const std::uint32_t* rows,
@@ -118,6 +239,30 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int w = 0; w < W; ++w)
     if (cv * W + w < dim) out[cv * W + w] = AccOps<Acc>::div(s[w], (Acc)N);
+}
+
+template <typename T>
+bool try_colmean_staged(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                        const std::uint32_t* rows, double* out, cudaStream_t s) {
+  constexpr int W = ColVec<T>::W;
+  if (ld % W != 0 || reinterpret_cast<std::uintptr_t>(x) % 16 != 0) return false;
+  if (n < 8 || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
+  switch (__builtin_ctzll(n) - 3) {
+    case 0: launch_colmean_staged<0, T>(x, ld, dim, rows, out, s); break;
+    case 1: launch_colmean_staged<1, T>(x, ld, dim, rows, out, s); break;
+    case 2: launch_colmean_staged<2, T>(x, ld, dim, rows, out, s); break;
+    case 3: launch_colmean_staged<3, T>(x, ld, dim, rows, out, s); break;
+    case 4: launch_colmean_staged<4, T>(x, ld, dim, rows, out, s); break;
+    case 5: launch_colmean_staged<5, T>(x, ld, dim, rows, out, s); break;
+    case 6: launch_colmean_staged<6, T>(x, ld, dim, rows, out, s); break;
+    case 7: launch_colmean_staged<7, T>(x, ld, dim, rows, out, s); break;
+    case 8: launch_colmean_staged<8, T>(x, ld, dim, rows, out, s); break;
+    case 9: launch_colmean_staged<9, T>(x, ld, dim, rows, out, s); break;
+    case 10: launch_colmean_staged<10, T>(x, ld, dim, rows, out, s); break;
+    default: return false;
+  }
+  MB_LAUNCH_CHECK();
+  return true;
 }
 
 // EXACT: per peer, sequential over j exactly as core.hpp:118-122.  The only
@@ -436,55 +581,94 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
 }
 
 // ---- slab-streamed variants: the j-sums continue across D-slabs --------
+// FAST: block (c, y) sums chunk c of kFastRows rows in a fixed order (chunk
+// offset c0 in the row's partials, so the slab-streamed and resident paths
+// agree): each thread takes 16-byte vectors (4 fp32 / 2 fp64 coordinates)
+// 256 vectors apart and sums its elements sequentially, one chain per row,
+// then the block tree of block_sum_fixed per row.  The rows of a block share
+// every reference load (the fp64 reference is twice the bytes of an fp32
+// row: one row per block read 12 bytes per fp32 coordinate through L2).
+constexpr int kFastRows = 4;
+
 template <typename T>
-__device__ __forceinline__ void dist_row_chunk(const T* __restrict__ x, std::uint64_t ld,
-                                               std::uint64_t dim, const double* __restrict__ ref,
-                                               std::uint64_t nch_total, std::uint64_t c0,
-                                               double* __restrict__ partial, std::uint64_t i) {
+__global__ void __launch_bounds__(kRedThreads)
+    dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                       const double* __restrict__ ref, std::uint64_t nch_total,
+                       std::uint64_t c0, double* __restrict__ partial, std::uint64_t n,
+                       const std::uint32_t* __restrict__ list,
+                       const std::uint32_t* __restrict__ list_count) {
   using V = typename ColVec<T>::V;
   constexpr int W = ColVec<T>::W;
+  __shared__ double buf[kFastRows][kRedThreads];
+  const std::uint64_t rows = list ? *list_count : n;
   const std::uint64_t c = blockIdx.x;
-  const T* row = x + i * ld;
   const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
   const bool vec = (ld % W == 0) && (reinterpret_cast<std::uintptr_t>(x) % 16 == 0);
-  double acc = 0.0;
-#pragma unroll 4
-  for (std::uint64_t j = lo + (std::uint64_t)threadIdx.x * W; j < hi; j += kRedThreads * W) {
-    T e[W];
-    if (vec && j + W <= hi) {
-      const V v = __ldg(reinterpret_cast<const V*>(row + j));
+  for (std::uint64_t y0 = (std::uint64_t)blockIdx.y * kFastRows; y0 < rows;
+       y0 += (std::uint64_t)gridDim.y * kFastRows) {
+    const T* rp[kFastRows];
+    std::uint64_t ri[kFastRows];
 #pragma unroll
-      for (int w = 0; w < W; ++w) e[w] = reinterpret_cast<const T*>(&v)[w];
-    } else {
+    for (int r = 0; r < kFastRows; ++r) {
+      const std::uint64_t y = y0 + r < rows ? y0 + r : y0;  // short tail: repeat, not stored
+      ri[r] = list ? list[y] : y;
+      rp[r] = x + ri[r] * ld;
+    }
+    double acc[kFastRows];
 #pragma unroll
-      for (int w = 0; w < W; ++w) e[w] = j + w < hi ? row[j + w] : T(0);
+    for (int r = 0; r < kFastRows; ++r) acc[r] = 0.0;
+#pragma unroll 2
+    for (std::uint64_t j = lo + (std::uint64_t)threadIdx.x * W; j < hi; j += kRedThreads * W) {
+      const bool whole = vec && j + W <= hi;
+      double rf[W];
+      if (j + W <= hi) {  // ref: a cudaMalloc'd fp64 vector, j a multiple of W
+#pragma unroll
+        for (int w = 0; w < W; w += 2) {
+          const double2 r2 = __ldg(reinterpret_cast<const double2*>(ref + j + w));
+          rf[w] = r2.x;
+          rf[w + 1] = r2.y;
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) rf[w] = j + w < hi ? __ldg(ref + j + w) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kFastRows; ++r) {
+        T e[W];
+        if (whole) {
+          const V v = __ldg(reinterpret_cast<const V*>(rp[r] + j));
+#pragma unroll
+          for (int w = 0; w < W; ++w) e[w] = reinterpret_cast<const T*>(&v)[w];
+        } else {
+#pragma unroll
+          for (int w = 0; w < W; ++w) e[w] = j + w < hi ? rp[r][j + w] : T(0);
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          if (j + w >= hi) break;
+          const double diff = __dsub_rn((double)e[w], rf[w]);
+          acc[r] = __dadd_rn(acc[r], __dmul_rn(diff, diff));
+        }
+      }
+    }
+    // block_sum_fixed's tree, all rows at once
+#pragma unroll
+    for (int r = 0; r < kFastRows; ++r) buf[r][threadIdx.x] = acc[r];
+    __syncthreads();
+    for (int st = kRedThreads / 2; st > 0; st >>= 1) {
+      if ((int)threadIdx.x < st) {
+#pragma unroll
+        for (int r = 0; r < kFastRows; ++r)
+          buf[r][threadIdx.x] = __dadd_rn(buf[r][threadIdx.x], buf[r][threadIdx.x + st]);
+      }
+      __syncthreads();
     }
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      if (j + w >= hi) break;
-      const double diff = __dsub_rn((double)e[w], ref[j + w]);
-      acc = __dadd_rn(acc, __dmul_rn(diff, diff));
-    }
+    for (int r = 0; r < kFastRows; ++r)
+      if ((int)threadIdx.x == r && y0 + r < rows) partial[ri[r] * nch_total + c0 + c] = buf[r][0];
+    __syncthreads();
   }
-  const double s = block_sum_fixed(acc);
-  if (threadIdx.x == 0) partial[i * nch_total + c0 + c] = s;
 }
-
-// FAST: block (c, i) sums chunk c of row i in a fixed order (chunk offset c0
-// in the row's partials, so the slab-streamed and resident paths agree): each
-// thread takes 16-byte vectors (4 fp32 / 2 fp64 coordinates) 256 vectors
-// apart, sums its elements sequentially, then the block tree.
-template <typename T>
-__global__ void dist_rows_fast_off(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
-                                   const double* __restrict__ ref, std::uint64_t nch_total,
-                                   std::uint64_t c0, double* __restrict__ partial,
-                                   std::uint64_t n, const std::uint32_t* __restrict__ list,
-                                   const std::uint32_t* __restrict__ list_count) {
-  const std::uint64_t rows = list ? *list_count : n;
-  for (std::uint64_t y = blockIdx.y; y < rows; y += gridDim.y)
-    dist_row_chunk<T>(x, ld, dim, ref, nch_total, c0, partial, list ? list[y] : y);
-}
-
 
 __global__ void drift_fast_partial_off(const double* __restrict__ mean,
                                        const double* __restrict__ ref, std::uint64_t dim,
@@ -520,16 +704,19 @@ unsigned grid_for(std::uint64_t work, unsigned threads) {
 
 std::uint64_t diag_chunk() { return kChunk; }
 
-// grid rows for the FAST partials over a representative list (the count is
-// on the device): ~2 waves of CTAs, each looping over rows (1, 4 and 16
-// waves measured the same)
-unsigned fast_rows_grid(std::uint64_t n, std::uint64_t nch) {
+// grid rows (groups of kFastRows rows) for the FAST partials: every group
+// of the n rows, or, over a representative list (its length is on the
+// device), ~2 waves of CTAs looping over the groups (1, 4 and 16 waves
+// measured the same)
+unsigned fast_rows_grid(std::uint64_t n, std::uint64_t nch, bool listed) {
+  const std::uint64_t groups = (n + kFastRows - 1) / kFastRows;
+  if (!listed) return (unsigned)groups;
   static const std::uint64_t waves = [] {
     const char* e = std::getenv("MOSHPIT_FAST_ROW_WAVES");
     return (std::uint64_t)(e ? std::max(1, std::atoi(e)) : 2);
   }();
   const std::uint64_t y = std::max<std::uint64_t>(1, waves * 2368 / std::max<std::uint64_t>(nch, 1));
-  return (unsigned)std::min<std::uint64_t>(n, y);
+  return (unsigned)std::min<std::uint64_t>(groups, y);
 }
 
 template <typename T>
@@ -545,7 +732,7 @@ void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
     return;
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    const unsigned gy = list ? fast_rows_grid(n, nch) : (unsigned)n;
+    const unsigned gy = fast_rows_grid(n, nch, list != nullptr);
     dist_rows_fast_off<T><<<dim3((unsigned)nch, gy), kRedThreads, 0, s>>>(
         x, ld, dim, ref, nch_total, c0, partial, n, list, count);
   }
@@ -617,30 +804,27 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s, bool rows_optional) {
   if (dim == 0 || n == 0) return;
-  // the diagnostics' fp64 column means only (keeps the library small)
+  // fp64 accumulation (the diagnostics) for n = 8 * 2^K: the staged tree
   if constexpr (std::is_same<Acc, double>::value) {
-    constexpr int W = ColVec<T>::W;
-    const bool vec_ok = ld % W == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0;
-    if (vec_ok && (n == 256 || n == 1024)) {
-      const std::uint64_t nv = (dim + W - 1) / W;
-      const unsigned blocks = (unsigned)((nv + 127) / 128);
-      // the representative gather: alone, the fp32 kernel is slower with it
-      // (6.2 vs 2.6 ms at C2: the index loads cost more than the HBM bytes
-      // saved; fp64 2.0 vs 4.7 ms), but beside the distortion on the other
-      // stream the saved bytes win: C2 round + FAST record 10.25 vs 11.74 ms
-      // (profiles/r02/reps_gather_ab.txt).  MOSHPIT_REP_GATHER_F32=0 turns
-      // it off for fp32.
-      static const bool gather32 = [] {
-        const char* e = std::getenv("MOSHPIT_REP_GATHER_F32");
-        return !e || std::atoi(e) != 0;
-      }();
-      const std::uint32_t* g =
-          (rows_optional && !std::is_same<T, double>::value && !gather32) ? nullptr : rows;
-      if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
-      else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
-      MB_LAUNCH_CHECK();
-      return;
+    // the representative gather: the fp32 column means read every row of
+    // the tree either way; the gather trades HBM bytes for L2 hits
+    // (MOSHPIT_REP_GATHER_F32=0 reads the rows themselves)
+    static const bool gather32 = [] {
+      const char* e = std::getenv("MOSHPIT_REP_GATHER_F32");
+      return !e || std::atoi(e) != 0;
+    }();
+    const std::uint32_t* g =
+        (rows_optional && !std::is_same<T, double>::value && !gather32) ? nullptr : rows;
+    if constexpr (std::is_same<T, double>::value) {
+      if (ld % 2 == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0 && (n == 256 || n == 1024)) {
+        const unsigned blocks = (unsigned)(((dim + 1) / 2 + 127) / 128);
+        if (n == 256) colmean_unrolled<256, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
+        else colmean_unrolled<1024, T, Acc><<<blocks, 128, 0, s>>>(x, ld, dim, g, out);
+        MB_LAUNCH_CHECK();
+        return;
+      }
     }
+    if (try_colmean_staged<T>(x, n, ld, dim, g, out, s)) return;
   }
   const unsigned threads = 128;
   colmean_kernel<T, Acc><<<(unsigned)((dim + threads - 1) / threads), threads, 0, s>>>(
@@ -669,7 +853,7 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
     }
   } else {
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
-    const unsigned gy = list ? fast_rows_grid(n, nch) : (unsigned)n;
+    const unsigned gy = fast_rows_grid(n, nch, list != nullptr);
     dist_rows_fast_off<T><<<dim3((unsigned)nch, gy), kRedThreads, 0, s>>>(
         x, ld, dim, ref, nch, 0, partial, n, list, count);
     MB_LAUNCH_CHECK();

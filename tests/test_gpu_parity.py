@@ -568,6 +568,32 @@ def test_column_means_equal_reference(mb, ref, n):
     assert bits_equal(mb.mean_of(x), ref.mean_of(x))
 
 
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256, 512, 1024, 4096])
+@pytest.mark.parametrize("dim", [2, 66, 1030])
+def test_column_means_staged_tree_equal_reference(mb, ref, n, dim):
+    """n = 8 * 2^K with 16-byte rows: the cp.async-staged binary-counter
+    evaluation of the tree (diag_kernel.cu colmean_staged), with column
+    vectors past the row end in the last CTA, bit for bit."""
+    x = np.random.default_rng(n + dim).standard_normal((n, dim))
+    assert bits_equal(mb.mean_of(x), ref.mean_of(x))
+
+
+@pytest.mark.parametrize("n", [8, 256, 1024, 1000])
+def test_column_means_row_gather_equal_reference(mb, ref, n):
+    """group_mean over a member list with repeated rows (the representative
+    gather the diagnostics use after a round): tree element i is row
+    members[i]."""
+    import ctypes as C
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((300, 66))
+    mem = rng.integers(0, 300, n).astype(np.uint32)
+    out = np.zeros(66)
+    mb.check(mb._capi.lib().moshpit_group_mean(
+        1, x.ctypes.data_as(C.c_void_p), 300, 66, mem.ctypes.data_as(C.c_void_p), n,
+        out.ctypes.data_as(C.c_void_p)))
+    assert bits_equal(out, ref.mean_of(x[mem]))
+
+
 @pytest.mark.parametrize("diag", ["fast", "exact"])
 def test_engine_round_record_equals_round_then_record(mb, torch, diag):
     """round_record reads one representative row per averaged group (every
