@@ -96,13 +96,76 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// One thread's view of the staged tree: its column vector, the row map, its
+// 16-byte slots in the ring.  Block b (8 rows) lives in stage b % kCmStages.
+template <int K, typename T>
+struct CmThread {
+  using V = typename ColVec<T>::V;
+  static constexpr int W = ColVec<T>::W;
+  static constexpr int NB = 1 << K;
+  const V* col;
+  std::uint64_t ldv;
+  const std::uint32_t* s_rows;  // null: row i is i
+  V* mine;
+
+  __device__ __forceinline__ void issue(int b, int stage) const {
+    if (b < NB) {
+      V* dst = mine + stage * 8 * kCmThreads;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const std::uint32_t r = s_rows ? s_rows[b * 8 + q] : (std::uint32_t)(b * 8 + q);
+        cp_async16(dst + q * kCmThreads, col + (std::uint64_t)r * ldv);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  }
+  // block base + OFF: refill the ring kCmStages - 1 blocks ahead, then the
+  // block's sequential sum from +0 (core.hpp:74-77)
+  template <int OFF>
+  __device__ __forceinline__ void block(int base, double (&o)[W]) const {
+    issue(base + OFF + kCmStages - 1, (OFF + kCmStages - 1) % kCmStages);
+    cp_async_wait<kCmStages - 1>();
+    const V* src = mine + (OFF % kCmStages) * 8 * kCmThreads;
+#pragma unroll
+    for (int w = 0; w < W; ++w) o[w] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const V e = src[q * kCmThreads];
+      const T* pe = reinterpret_cast<const T*>(&e);
+#pragma unroll
+      for (int w = 0; w < W; ++w) o[w] = __dadd_rn(o[w], (double)pe[w]);
+    }
+  }
+};
+
+// the subtree over 2^L blocks starting at block base + OFF, at compile time
+template <int L, int OFF, int K, typename T>
+__device__ __forceinline__ void cm_subtree(const CmThread<K, T>& c, int base,
+                                           double (&o)[ColVec<T>::W]) {
+  constexpr int W = ColVec<T>::W;
+  if constexpr (L == 0) {
+    c.template block<OFF>(base, o);
+  } else {
+    double l[W], r[W];
+    cm_subtree<L - 1, OFF, K, T>(c, base, l);
+    cm_subtree<L - 1, OFF + (1 << (L - 1)), K, T>(c, base, r);
+#pragma unroll
+    for (int w = 0; w < W; ++w) o[w] = __dadd_rn(l[w], r[w]);
+  }
+}
+
 template <int K, typename T>
 __global__ void __launch_bounds__(kCmThreads)
     colmean_staged(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
                    const std::uint32_t* __restrict__ rows, double* __restrict__ out) {
   using V = typename ColVec<T>::V;
   constexpr int W = ColVec<T>::W;
-  constexpr int N = 8 << K, NB = 1 << K;
+  constexpr int N = 8 << K;
+  // the lowest KS levels of blocks at compile time (stage offsets constant:
+  // subtree bases are multiples of 2^KS >= kCmStages when K >= 2), the top
+  // KT = K - KS levels with a binary counter of pending left subtrees
+  constexpr int KS = K < 3 ? K : 3, KT = K - KS, NS = 1 << KT;
+  static_assert(KS >= 2 || KT == 0, "stage offsets need subtree bases % kCmStages == 0");
   extern __shared__ __align__(16) unsigned char cm_smem[];
   V* const ring = reinterpret_cast<V*>(cm_smem);  // [stage][8 rows][kCmThreads]
   std::uint32_t* const s_rows =
@@ -113,43 +176,20 @@ __global__ void __launch_bounds__(kCmThreads)
   }
   const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
   if (cv * W >= dim) return;
-  const std::uint64_t ldv = ld / W;
-  const V* const col = reinterpret_cast<const V*>(x) + cv;
-  V* const mine = ring + threadIdx.x;
-  auto issue = [&](int b) {
-    if (b < NB) {
-      V* dst = mine + (b % kCmStages) * 8 * kCmThreads;
+  const CmThread<K, T> c{reinterpret_cast<const V*>(x) + cv, ld / W, rows ? s_rows : nullptr,
+                         ring + threadIdx.x};
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const std::uint32_t r = rows ? s_rows[b * 8 + q] : (std::uint32_t)(b * 8 + q);
-        cp_async16(dst + q * kCmThreads, col + (std::uint64_t)r * ldv);
-      }
-    }
-    cp_async_commit();  // empty groups keep the wait count uniform
-  };
-#pragma unroll
-  for (int b = 0; b < kCmStages - 1; ++b) issue(b);
-  double stk[K > 0 ? K : 1][W];
+  for (int b = 0; b < kCmStages - 1; ++b) c.issue(b, b);
+  double stk[KT > 0 ? KT : 1][W];
   double v[W];
 #pragma unroll 1
-  for (int b = 0; b < NB; ++b) {
-    issue(b + kCmStages - 1);
-    cp_async_wait<kCmStages - 1>();
-    const V* src = mine + (b % kCmStages) * 8 * kCmThreads;
-#pragma unroll
-    for (int w = 0; w < W; ++w) v[w] = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const V e = src[q * kCmThreads];
-      const T* pe = reinterpret_cast<const T*>(&e);
-#pragma unroll
-      for (int w = 0; w < W; ++w) v[w] = __dadd_rn(v[w], (double)pe[w]);
-    }
+  for (int t = 0; t < NS; ++t) {
+    cm_subtree<KS, 0, K, T>(c, t << KS, v);
     bool placed = false;
 #pragma unroll
-    for (int l = 0; l < K; ++l) {
+    for (int l = 0; l < KT; ++l) {
       if (!placed) {
-        if ((b >> l) & 1) {
+        if ((t >> l) & 1) {
 #pragma unroll
           for (int w = 0; w < W; ++w) v[w] = __dadd_rn(stk[l][w], v[w]);
         } else {
@@ -160,7 +200,7 @@ __global__ void __launch_bounds__(kCmThreads)
       }
     }
   }
-  // after block NB - 1 (all bits set) v holds the whole tree
+  // after subtree NS - 1 (all bits set) v holds the whole tree
 #pragma unroll
   for (int w = 0; w < W; ++w)
     if (cv * W + w < dim) out[cv * W + w] = __ddiv_rn(v[w], (double)N);
