@@ -320,6 +320,16 @@ struct RepRows {
   const std::uint32_t* list = nullptr;
   const std::uint32_t* count = nullptr;
 };
+// Moshpit-SGD local step fused into hat theta (diag_kernel.cu): steps every
+// row in place (the standalone step kernel's arithmetic and Philox noise) and
+// writes mean_of(post) to hat.  False (nothing launched) unless n = 8 * 2^K,
+// 16-byte rows and at most partial_slots CTAs.
+template <typename T>
+bool launch_step_colmean(T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                         const T* curv, const T* tgt, T gamma, double coord_std, int philox,
+                         std::uint64_t seed, std::uint64_t step_no, std::uint32_t* nonfinite,
+                         double* noise_partial, std::uint64_t partial_slots, double* hat,
+                         cudaStream_t s);
 void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint8_t* gvoid, const std::uint32_t* counts, std::uint64_t n,
                        std::uint32_t* rep, std::uint32_t* list, std::uint32_t* count,

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "blocktree.cuh"
 #include "pairwise.cuh"
+#include "philox.cuh"
 
 namespace mb200 {
 namespace {
@@ -98,7 +99,14 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // One thread's view of the staged tree: its column vector, the row map, its
 // 16-byte slots in the ring.  Block b (8 rows) lives in stage b % kCmStages.
-template <int K, typename T>
+// `Leaf` may transform each row's vector as it enters the tree (the fused
+// Moshpit-SGD step below); NoLeaf leaves it alone.
+struct NoLeaf {
+  template <typename V>
+  __device__ __forceinline__ void operator()(V&, std::uint32_t) {}
+};
+
+template <int K, typename T, typename Leaf = NoLeaf>
 struct CmThread {
   using V = typename ColVec<T>::V;
   static constexpr int W = ColVec<T>::W;
@@ -107,9 +115,11 @@ struct CmThread {
   std::uint64_t ldv;
   const std::uint32_t* s_rows;  // null: row i is i
   V* mine;
+  bool live;                    // this thread's column vector is inside the row
+  Leaf leaf;
 
   __device__ __forceinline__ void issue(int b, int stage) const {
-    if (b < NB) {
+    if (b < NB && live) {
       V* dst = mine + stage * 8 * kCmThreads;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -122,7 +132,7 @@ struct CmThread {
   // block base + OFF: refill the ring kCmStages - 1 blocks ahead, then the
   // block's sequential sum from +0 (core.hpp:74-77)
   template <int OFF>
-  __device__ __forceinline__ void block(int base, double (&o)[W]) const {
+  __device__ __forceinline__ void block(int base, double (&o)[W]) {
     issue(base + OFF + kCmStages - 1, (OFF + kCmStages - 1) % kCmStages);
     cp_async_wait<kCmStages - 1>();
     const V* src = mine + (OFF % kCmStages) * 8 * kCmThreads;
@@ -130,7 +140,8 @@ struct CmThread {
     for (int w = 0; w < W; ++w) o[w] = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const V e = src[q * kCmThreads];
+      V e = src[q * kCmThreads];
+      leaf(e, (std::uint32_t)((base + OFF) * 8 + q));
       const T* pe = reinterpret_cast<const T*>(&e);
 #pragma unroll
       for (int w = 0; w < W; ++w) o[w] = __dadd_rn(o[w], (double)pe[w]);
@@ -139,52 +150,33 @@ struct CmThread {
 };
 
 // the subtree over 2^L blocks starting at block base + OFF, at compile time
-template <int L, int OFF, int K, typename T>
-__device__ __forceinline__ void cm_subtree(const CmThread<K, T>& c, int base,
-                                           double (&o)[ColVec<T>::W]) {
-  constexpr int W = ColVec<T>::W;
+template <int L, int OFF, class C>
+__device__ __forceinline__ void cm_subtree(C& c, int base, double (&o)[C::W]) {
+  constexpr int W = C::W;
   if constexpr (L == 0) {
     c.template block<OFF>(base, o);
   } else {
     double l[W], r[W];
-    cm_subtree<L - 1, OFF, K, T>(c, base, l);
-    cm_subtree<L - 1, OFF + (1 << (L - 1)), K, T>(c, base, r);
+    cm_subtree<L - 1, OFF>(c, base, l);
+    cm_subtree<L - 1, OFF + (1 << (L - 1))>(c, base, r);
 #pragma unroll
     for (int w = 0; w < W; ++w) o[w] = __dadd_rn(l[w], r[w]);
   }
 }
 
-template <int K, typename T>
-__global__ void __launch_bounds__(kCmThreads)
-    colmean_staged(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
-                   const std::uint32_t* __restrict__ rows, double* __restrict__ out) {
-  using V = typename ColVec<T>::V;
-  constexpr int W = ColVec<T>::W;
-  constexpr int N = 8 << K;
-  // the lowest KS levels of blocks at compile time (stage offsets constant:
-  // subtree bases are multiples of 2^KS >= kCmStages when K >= 2), the top
-  // KT = K - KS levels with a binary counter of pending left subtrees
+// The whole tree for one thread: compile-time subtrees of 2^KS blocks, the
+// top K - KS levels with a binary counter of pending left subtrees.
+template <int K, class C>
+__device__ __forceinline__ void cm_tree(C& c, double (&v)[C::W]) {
+  constexpr int W = C::W;
   constexpr int KS = K < 3 ? K : 3, KT = K - KS, NS = 1 << KT;
   static_assert(KS >= 2 || KT == 0, "stage offsets need subtree bases % kCmStages == 0");
-  extern __shared__ __align__(16) unsigned char cm_smem[];
-  V* const ring = reinterpret_cast<V*>(cm_smem);  // [stage][8 rows][kCmThreads]
-  std::uint32_t* const s_rows =
-      reinterpret_cast<std::uint32_t*>(ring + kCmStages * 8 * kCmThreads);
-  if (rows) {
-    for (int i = threadIdx.x; i < N; i += kCmThreads) s_rows[i] = rows[i];
-    __syncthreads();
-  }
-  const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
-  if (cv * W >= dim) return;
-  const CmThread<K, T> c{reinterpret_cast<const V*>(x) + cv, ld / W, rows ? s_rows : nullptr,
-                         ring + threadIdx.x};
 #pragma unroll
   for (int b = 0; b < kCmStages - 1; ++b) c.issue(b, b);
   double stk[KT > 0 ? KT : 1][W];
-  double v[W];
 #pragma unroll 1
   for (int t = 0; t < NS; ++t) {
-    cm_subtree<KS, 0, K, T>(c, t << KS, v);
+    cm_subtree<KS, 0>(c, t << KS, v);
     bool placed = false;
 #pragma unroll
     for (int l = 0; l < KT; ++l) {
@@ -201,9 +193,170 @@ __global__ void __launch_bounds__(kCmThreads)
     }
   }
   // after subtree NS - 1 (all bits set) v holds the whole tree
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(kCmThreads)
+    colmean_staged(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                   const std::uint32_t* __restrict__ rows, double* __restrict__ out) {
+  using V = typename ColVec<T>::V;
+  constexpr int W = ColVec<T>::W;
+  constexpr int N = 8 << K;
+  extern __shared__ __align__(16) unsigned char cm_smem[];
+  V* const ring = reinterpret_cast<V*>(cm_smem);  // [stage][8 rows][kCmThreads]
+  std::uint32_t* const s_rows =
+      reinterpret_cast<std::uint32_t*>(ring + kCmStages * 8 * kCmThreads);
+  if (rows) {
+    for (int i = threadIdx.x; i < N; i += kCmThreads) s_rows[i] = rows[i];
+    __syncthreads();
+  }
+  const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
+  if (cv * W >= dim) return;
+  CmThread<K, T> c{reinterpret_cast<const V*>(x) + cv, ld / W, rows ? s_rows : nullptr,
+                   ring + threadIdx.x, true, NoLeaf{}};
+  double v[W];
+  cm_tree<K>(c, v);
 #pragma unroll
   for (int w = 0; w < W; ++w)
     if (cv * W + w < dim) out[cv * W + w] = __ddiv_rn(v[w], (double)N);
+}
+
+// ---------------------------------------------------------------------------
+// Moshpit-SGD local step fused into hat theta = mean_of(post-step vectors)
+// (optimizer.hpp:356-376): every row of the tree is stepped as it enters it
+// -- g = c (theta - t) [+ n_j], theta' = theta - gamma g, separately rounded,
+// the same Philox normals (peer = row, quad of 4 coordinates) as the
+// standalone step kernel -- and written back; the tree then sums the post
+// values.  One read and one write of the state instead of the step's read +
+// write and the mean's read.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct StepArgs {
+  const T* curv;
+  const T* tgt;
+  T gamma;
+  double coord_std;
+  std::uint64_t step_no;
+  PhiloxKeys pk;
+  std::uint32_t* nonfinite;
+  double* noise_partial;  // [gridDim.x] sum of n_j^2 per CTA
+};
+
+template <typename T, bool NOISY>
+struct StepLeafOp {
+  using V = typename ColVec<T>::V;
+  static constexpr int W = ColVec<T>::W;
+  V c, t;
+  T gamma;
+  double coord_std;
+  std::uint64_t step_no, cv, dim;
+  const PhiloxKeys* pk;
+  V* out;  // this thread's column vector of row 0
+  std::uint64_t ldv;
+  bool live;
+  T chk;
+  double nsq;
+
+  __device__ __forceinline__ void operator()(V& e, std::uint32_t row) {
+    if (!live) return;
+    float z[4] = {0.f, 0.f, 0.f, 0.f};
+    // quad of 4 coordinates: fp32 vectors are quads, fp64 vectors halves
+    const std::uint64_t quad = W == 4 ? cv : cv >> 1;
+    const int zo = W == 4 ? 0 : (int)(cv & 1) * 2;
+    if constexpr (NOISY) philox_normals4(*pk, step_no, row, quad, z);
+    T* pe = reinterpret_cast<T*>(&e);
+    const T* pc = reinterpret_cast<const T*>(&c);
+    const T* pt = reinterpret_cast<const T*>(&t);
+    T q = T(0);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      if (cv * W + w >= dim) break;
+      T g = mul_rn(pc[w], sub_rn(pe[w], pt[w]));
+      if constexpr (NOISY) {
+        const T nj = noise_component(z[zo + w], coord_std, (T*)nullptr);
+        nsq_add(q, nj);
+        g = add_rn(g, nj);
+      }
+      chk = fma0(g, chk);
+      pe[w] = sub_rn(pe[w], mul_rn(gamma, g));
+    }
+    if constexpr (NOISY) nsq += (double)q;
+    out[(std::uint64_t)row * ldv] = e;
+  }
+  __device__ static float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+  __device__ static float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+  __device__ static float add_rn(float a, float b) { return __fadd_rn(a, b); }
+  __device__ static float fma0(float g, float acc) { return __fmaf_rn(g, 0.f, acc); }
+  __device__ static double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+  __device__ static double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+  __device__ static double add_rn(double a, double b) { return __dadd_rn(a, b); }
+  __device__ static double fma0(double g, double acc) { return __fma_rn(g, 0.0, acc); }
+};
+
+template <int K, typename T, bool NOISY>
+__global__ void __launch_bounds__(kCmThreads)
+    step_colmean_staged(T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
+                        double* __restrict__ hat, const __grid_constant__ StepArgs<T> a) {
+  using V = typename ColVec<T>::V;
+  constexpr int W = ColVec<T>::W;
+  constexpr int N = 8 << K;
+  extern __shared__ __align__(16) unsigned char cm_smem[];
+  V* const ring = reinterpret_cast<V*>(cm_smem);
+  const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
+  const bool live = cv * W < dim;  // no early exit: the CTA reduces nsq at the end
+  const std::uint64_t ldv = ld / W;
+  StepLeafOp<T, NOISY> op;
+  op.c = op.t = V{};
+  if (live) {
+    if (cv * W + W <= dim) {
+      op.c = __ldg(reinterpret_cast<const V*>(a.curv) + cv);
+      op.t = __ldg(reinterpret_cast<const V*>(a.tgt) + cv);
+    } else {
+      T* pc = reinterpret_cast<T*>(&op.c);
+      T* pt = reinterpret_cast<T*>(&op.t);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (cv * W + w < dim) {
+          pc[w] = a.curv[cv * W + w];
+          pt[w] = a.tgt[cv * W + w];
+        }
+      }
+    }
+  }
+  op.gamma = a.gamma;
+  op.coord_std = a.coord_std;
+  op.step_no = a.step_no;
+  op.cv = cv;
+  op.dim = dim;
+  op.pk = &a.pk;
+  op.out = reinterpret_cast<V*>(x) + cv;
+  op.ldv = ldv;
+  op.live = live;
+  op.chk = T(0);
+  op.nsq = 0.0;
+  CmThread<K, T, StepLeafOp<T, NOISY>> c{reinterpret_cast<const V*>(x) + cv, ldv, nullptr,
+                                         ring + threadIdx.x, live, op};
+  double v[W];
+  cm_tree<K>(c, v);
+  if (live) {
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      if (cv * W + w < dim) hat[cv * W + w] = __ddiv_rn(v[w], (double)N);
+  }
+  if (c.leaf.chk != T(0)) atomicOr(a.nonfinite, 1u);
+  if constexpr (NOISY) {
+    __shared__ double red[kCmThreads / 32];
+    double q = c.leaf.nsq;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+    __syncthreads();
+    if (threadIdx.x == 0 && a.noise_partial) {
+      double t = 0.0;
+      for (int i = 0; i < kCmThreads / 32; ++i) t += red[i];
+      a.noise_partial[blockIdx.x] = t;
+    }
+  }
 }
 
 template <int K, typename T>
@@ -838,6 +991,77 @@ std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
   const std::uint64_t a = n * (nch ? nch : 1), b = 2 * (nch ? nch : 1);
   return a > b ? a : b;
 }
+
+namespace {
+
+template <int K, typename T, bool NOISY>
+void launch_step_colmean_k(T* x, std::uint64_t ld, std::uint64_t dim, double* hat,
+                           const StepArgs<T>& a, unsigned grid, cudaStream_t s) {
+  constexpr std::size_t smem = (std::size_t)kCmStages * 8 * kCmThreads * 16;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  MB_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    MB_CUDA(cudaFuncSetAttribute(step_colmean_staged<K, T, NOISY>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev = dev;
+  }
+  step_colmean_staged<K, T, NOISY><<<grid, kCmThreads, smem, s>>>(x, ld, dim, hat, a);
+}
+
+template <typename T, bool NOISY>
+void launch_step_colmean_n(int k, T* x, std::uint64_t ld, std::uint64_t dim, double* hat,
+                           const StepArgs<T>& a, unsigned grid, cudaStream_t s) {
+  switch (k) {
+    case 0: launch_step_colmean_k<0, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 1: launch_step_colmean_k<1, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 2: launch_step_colmean_k<2, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 3: launch_step_colmean_k<3, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 4: launch_step_colmean_k<4, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 5: launch_step_colmean_k<5, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 6: launch_step_colmean_k<6, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 7: launch_step_colmean_k<7, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 8: launch_step_colmean_k<8, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    case 9: launch_step_colmean_k<9, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+    default: launch_step_colmean_k<10, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
+  }
+}
+
+}  // namespace
+
+template <typename T>
+bool launch_step_colmean(T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                         const T* curv, const T* tgt, T gamma, double coord_std, int philox,
+                         std::uint64_t seed, std::uint64_t step_no, std::uint32_t* nonfinite,
+                         double* noise_partial, std::uint64_t partial_slots, double* hat,
+                         cudaStream_t s) {
+  constexpr int W = ColVec<T>::W;
+  if (dim == 0 || ld % W != 0 || reinterpret_cast<std::uintptr_t>(x) % 16 != 0) return false;
+  if (reinterpret_cast<std::uintptr_t>(curv) % 16 != 0 ||
+      reinterpret_cast<std::uintptr_t>(tgt) % 16 != 0)
+    return false;
+  if (n < 8 || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
+  const std::uint64_t nv = (dim + W - 1) / W;
+  const std::uint64_t grid = (nv + kCmThreads - 1) / kCmThreads;
+  if (philox && grid > partial_slots) return false;
+  StepArgs<T> a{curv, tgt, gamma, coord_std, step_no, philox_keys(seed), nonfinite,
+                noise_partial};
+  const int k = __builtin_ctzll(n) - 3;
+  if (philox) launch_step_colmean_n<T, true>(k, x, ld, dim, hat, a, (unsigned)grid, s);
+  else launch_step_colmean_n<T, false>(k, x, ld, dim, hat, a, (unsigned)grid, s);
+  MB_LAUNCH_CHECK();
+  return true;
+}
+
+template bool launch_step_colmean<float>(float*, std::uint64_t, std::uint64_t, std::uint64_t,
+                                         const float*, const float*, float, double, int,
+                                         std::uint64_t, std::uint64_t, std::uint32_t*, double*,
+                                         std::uint64_t, double*, cudaStream_t);
+template bool launch_step_colmean<double>(double*, std::uint64_t, std::uint64_t,
+                                          std::uint64_t, const double*, const double*, double,
+                                          double, int, std::uint64_t, std::uint64_t,
+                                          std::uint32_t*, double*, std::uint64_t, double*,
+                                          cudaStream_t);
 
 template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,

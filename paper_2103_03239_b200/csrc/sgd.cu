@@ -88,6 +88,93 @@ __global__ void __launch_bounds__(kStepThreads)
   }
 }
 
+// The same step on 16-byte vectors (4 fp32 / 2 fp64 coordinates of one row)
+// for 16-byte-aligned rows: one thread per vector, grid-stride, curvature and
+// target read as vectors, the quad's Philox normals once per vector (fp64:
+// the vector's half of the quad).  Identical per-coordinate arithmetic; the
+// n_j^2 partials are per vector (fp32: per quad, as above).
+template <typename T>
+struct SVec;
+template <>
+struct SVec<float> {
+  using V = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct SVec<double> {
+  using V = double2;
+  static constexpr int W = 2;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kStepThreads)
+    sgd_step_vec(T* __restrict__ x, std::uint64_t n, std::uint64_t dim, std::uint64_t ld,
+                 const T* __restrict__ curv, const T* __restrict__ tgt, T gamma,
+                 const T* __restrict__ noise, double coord_std, int philox_mode,
+                 const __grid_constant__ PhiloxKeys pk, std::uint64_t step,
+                 std::uint32_t* nonfinite, double* noise_partial) {
+  using O = SOps<T>;
+  using V = typename SVec<T>::V;
+  constexpr int W = SVec<T>::W;
+  __shared__ double red[kStepThreads / 32];
+  double nsq = 0.0;
+  T chk = T(0);
+  const std::uint64_t nv = (dim + W - 1) / W, ldv = ld / W;
+  const std::uint64_t total = n * nv;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t i = e / nv, cv = e % nv, j0 = cv * W;
+    V* p = reinterpret_cast<V*>(x) + i * ldv + cv;
+    V v = *p, c, t;
+    T* pv = reinterpret_cast<T*>(&v);
+    T* pc = reinterpret_cast<T*>(&c);
+    T* pt = reinterpret_cast<T*>(&t);
+    if (j0 + W <= dim) {
+      c = __ldg(reinterpret_cast<const V*>(curv) + cv);
+      t = __ldg(reinterpret_cast<const V*>(tgt) + cv);
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        pc[w] = j0 + w < dim ? curv[j0 + w] : T(0);
+        pt[w] = j0 + w < dim ? tgt[j0 + w] : T(0);
+      }
+    }
+    float z[4] = {0, 0, 0, 0};
+    const int zo = W == 4 ? 0 : (int)(cv & 1) * 2;
+    if (philox_mode && !noise) philox_normals4(pk, step, i, W == 4 ? cv : cv >> 1, z);
+    T nq = T(0);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const std::uint64_t j = j0 + w;
+      if (j >= dim) break;
+      T g = O::mul(pc[w], O::sub(pv[w], pt[w]));
+      if (noise) {
+        g = O::add(g, noise[i * dim + j]);
+      } else if (philox_mode) {
+        const T nj = noise_component(z[zo + w], coord_std, (T*)nullptr);
+        nsq_add(nq, nj);
+        g = O::add(g, nj);
+      }
+      chk = O::add(chk, O::mul(g, T(0)));
+      pv[w] = O::sub(pv[w], O::mul(gamma, g));
+    }
+    *p = v;
+    nsq += (double)nq;
+  }
+  if (chk != T(0)) atomicOr(nonfinite, 1u);
+  if (philox_mode && !noise) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nsq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < kStepThreads / 32; ++k) t += red[k];
+      noise_partial[blockIdx.x] = t;
+    }
+  }
+}
+
 // Sequential D-vector diagnostics (EXACT, one thread, optimizer.hpp:386-418):
 // out[0] pv inner product, [1] f(mean), [2] |grad f(mean)|^2, [3] f(weighted);
 // wsum[j] += w_k * mean[j] in place.
@@ -196,6 +283,43 @@ __global__ void dispersion_fast(const T* __restrict__ x, std::uint64_t ld, std::
   }
   const double s = blk_sum(a, buf);
   if (threadIdx.x == 0) partial[i * nch + c] = s;
+}
+
+// The same partials for the representative rows only (list / count on the
+// device; after an averaging pass every member of a non-voided group holds
+// the identical row), grid-y looping over the list.
+template <typename T>
+__global__ void dispersion_fast_list(const T* __restrict__ x, std::uint64_t ld,
+                                     std::uint64_t dim, const double* __restrict__ mean,
+                                     std::uint64_t nch, double* __restrict__ partial,
+                                     const std::uint32_t* __restrict__ list,
+                                     const std::uint32_t* __restrict__ count) {
+  __shared__ double buf[kRed];
+  const std::uint64_t c = blockIdx.x;
+  const std::uint64_t lo = c * kChunk, hi = lo + kChunk < dim ? lo + kChunk : dim;
+  for (std::uint64_t y = blockIdx.y; y < *count; y += gridDim.y) {
+    const std::uint64_t i = list[y];
+    double a = 0.0;
+    for (std::uint64_t j = lo + threadIdx.x; j < hi; j += kRed) {
+      const double dd = __dsub_rn((double)x[i * ld + j], mean[j]);
+      a = __dadd_rn(a, __dmul_rn(dd, dd));
+    }
+    const double s = blk_sum(a, buf);
+    if (threadIdx.x == 0) partial[i * nch + c] = s;
+  }
+}
+
+// fold_all in (row, chunk) order with row i's partials read from rep[i]
+__global__ void fold_all_rep(const double* __restrict__ partial, std::uint64_t n,
+                             std::uint64_t nch, const std::uint32_t* __restrict__ rep,
+                             double div, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (std::uint64_t i = 0; i < n; ++i) {
+    const double* p = partial + (std::uint64_t)rep[i] * nch;
+    for (std::uint64_t c = 0; c < nch; ++c) s = __dadd_rn(s, p[c]);
+  }
+  *out = __ddiv_rn(s, div);
 }
 
 __global__ void fold_all(const double* __restrict__ partial, std::uint64_t count, double div,
@@ -567,6 +691,7 @@ struct SgdRun {
   std::uint64_t dim, ld;
   cudaStream_t s;
   DeviceBuffer c64, t64, cT, tT, noise_dev, flag, npart, hat, mean, wsum, vpart, vout, dpart;
+  DeviceBuffer rep, rlist, rcount;  // representatives after an averaging pass
   double noise_sq_host = 0.0;
   // LogisticRegression(xs, ys, l2): samples S, rows of xs are dim doubles.
   bool logit = false;
@@ -683,10 +808,19 @@ struct SgdRun {
                               cudaMemcpyHostToDevice, s));
       nz = noise_dev.as<T>();
     }
-    const unsigned grid = grid_for(n * ((dim + 3) / 4), kStepThreads);
-    sgd_step_kernel<T><<<grid, kStepThreads, 0, s>>>(
-        static_cast<T*>(x), n, dim, ld, cT.as<T>(), tT.as<T>(), (T)gamma, nz, coord_std,
-        philox, seed, k, flag.as<std::uint32_t>(), npart.as<double>() + k * 148 * 16);
+    constexpr int W = SVec<T>::W;
+    if (ld % W == 0 && reinterpret_cast<std::uintptr_t>(x) % 16 == 0) {
+      const unsigned grid = grid_for(n * ((dim + W - 1) / W), kStepThreads);
+      sgd_step_vec<T><<<grid, kStepThreads, 0, s>>>(
+          static_cast<T*>(x), n, dim, ld, cT.as<T>(), tT.as<T>(), (T)gamma, nz, coord_std,
+          philox, philox_keys(seed), k, flag.as<std::uint32_t>(),
+          npart.as<double>() + k * 148 * 16);
+    } else {
+      const unsigned grid = grid_for(n * ((dim + 3) / 4), kStepThreads);
+      sgd_step_kernel<T><<<grid, kStepThreads, 0, s>>>(
+          static_cast<T*>(x), n, dim, ld, cT.as<T>(), tT.as<T>(), (T)gamma, nz, coord_std,
+          philox, seed, k, flag.as<std::uint32_t>(), npart.as<double>() + k * 148 * 16);
+    }
     MB_LAUNCH_CHECK();
   }
 };
@@ -948,19 +1082,37 @@ static int run_sgd(
           r.lstep<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
                           static_cast<const double*>(host_noise));
       }
+      // the step fused into hat theta = mean_of(post) when the noise is the
+      // device's (or none) and n = 8 * 2^K: one pass over the state instead
+      // of the step's read + write and the mean's read
+      static const int fused_hat_mode = [] {  // 0 never, 1 sigma == 0 only, 2 always
+        const char* e = std::getenv("MOSHPIT_SGD_FUSED_HAT");
+        return e ? std::atoi(e) : 1;
+      }();
+      auto fused_hat = [&](auto* xs, auto* cs, auto* ts, auto g) {
+        return !logit && !host_noise && (fused_hat_mode == 2 || (fused_hat_mode == 1 && !philox)) &&
+               launch_step_colmean(xs, n, r.ld, dim, cs, ts, g, coord_std, philox, seed, k,
+                                   r.flag.as<std::uint32_t>(),
+                                   r.npart.as<double>() + (std::uint64_t)k * 148 * 16, 148 * 16,
+                                   r.hat.as<double>(), h.s);
+      };
       if (skip_diag) {
       } else if (dtype == MOSHPIT_F32) {
-        if (!logit)
-          r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
-                        static_cast<const float*>(host_noise));
-        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.hat.as<double>(),
-                                      h.s);
+        if (!fused_hat(x.as<float>(), r.cT.as<float>(), r.tT.as<float>(), (float)gamma)) {
+          if (!logit)
+            r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                          static_cast<const float*>(host_noise));
+          launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr,
+                                        r.hat.as<double>(), h.s);
+        }
       } else {
-        if (!logit)
-          r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
-                         static_cast<const double*>(host_noise));
-        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
-                                       r.hat.as<double>(), h.s);
+        if (!fused_hat(x.as<double>(), r.cT.as<double>(), r.tT.as<double>(), gamma)) {
+          if (!logit)
+            r.step<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
+                           static_cast<const double*>(host_noise));
+          launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
+                                         r.hat.as<double>(), h.s);
+        }
       }
       // averaging pass (optimizer.hpp:379-381, 249-284)
       if ((k + 1) % tau == 0 && n > 1) {
@@ -971,13 +1123,52 @@ static int run_sgd(
           plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
       }
       if (skip_diag) continue;
+      // after an averaging pass the diagnostics read one row per averaged
+      // group of its last round (identical rows: bit-identical results)
+      const bool synced = (k + 1) % tau == 0 && n > 1 && inner > 0;
+      if (synced) {
+        r.rep.resize(n * 4 + 16);
+        r.rlist.resize(n * 4 + 16);
+        r.rcount.resize(16);
+        launch_build_reps(plane->members.as<std::uint32_t>(), plane->goff.as<std::uint32_t>(),
+                          plane->gvoid.as<std::uint8_t>(), plane->counts.as<std::uint32_t>(), n,
+                          r.rep.as<std::uint32_t>(), r.rlist.as<std::uint32_t>(),
+                          r.rcount.as<std::uint32_t>(), h.s);
+      }
+      const std::uint32_t* rep_map = synced ? r.rep.as<std::uint32_t>() : nullptr;
       double* o = out.as<double>() + (std::uint64_t)k * 8;
       if (dtype == MOSHPIT_F32)
-        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, nullptr, r.mean.as<double>(),
-                                      h.s);
+        launch_colmean<float, double>(x.as<float>(), n, r.ld, dim, rep_map, r.mean.as<double>(),
+                                      h.s, true);
       else
-        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, nullptr,
-                                       r.mean.as<double>(), h.s);
+        launch_colmean<double, double>(x.as<double>(), n, r.ld, dim, rep_map,
+                                       r.mean.as<double>(), h.s, true);
+      // V_k, FAST: (row, chunk) partials folded in (row, chunk) order; after an
+      // averaging pass only the representatives' partials are computed
+      auto dispersion_fast_any = [&](double* dst) {
+        const std::uint64_t ch = nch ? nch : 1;
+        if (rep_map) {
+          const unsigned gy = (unsigned)std::min<std::uint64_t>(
+              n, std::max<std::uint64_t>(1, 2 * 2368 / ch));
+          if (dtype == MOSHPIT_F32)
+            dispersion_fast_list<float><<<dim3((unsigned)ch, gy), kRed, 0, h.s>>>(
+                x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>(),
+                r.rlist.as<std::uint32_t>(), r.rcount.as<std::uint32_t>());
+          else
+            dispersion_fast_list<double><<<dim3((unsigned)ch, gy), kRed, 0, h.s>>>(
+                x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>(),
+                r.rlist.as<std::uint32_t>(), r.rcount.as<std::uint32_t>());
+          fold_all_rep<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n, ch, rep_map, (double)n, dst);
+          return;
+        }
+        if (dtype == MOSHPIT_F32)
+          dispersion_fast<float><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+              x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+        else
+          dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
+              x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
+        fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, dst);
+      };
       w_k *= w_growth;
       weight_total += w_k;
       wt_hist[k] = weight_total;
@@ -991,14 +1182,7 @@ static int run_sgd(
             dispersion_exact<double><<<1, 1, 0, h.s>>>(x.as<double>(), n, r.ld, dim,
                                                        r.mean.as<double>(), o + 4);
         } else {
-          const std::uint64_t ch = nch ? nch : 1;
-          if (dtype == MOSHPIT_F32)
-            dispersion_fast<float><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
-                x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
-          else
-            dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
-                x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
-          fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, o + 4);
+          dispersion_fast_any(o + 4);
         }
       } else if (exact) {
         sgd_vec_exact<<<1, 1, 0, h.s>>>(r.mean.as<double>(), r.hat.as<double>(),
@@ -1017,13 +1201,7 @@ static int run_sgd(
                                                     r.wsum.as<double>(), w_k, weight_total, dim,
                                                     r.vpart.as<double>());
         sgd_vec_fold<<<1, 1, 0, h.s>>>(r.vpart.as<double>(), ch, o);
-        if (dtype == MOSHPIT_F32)
-          dispersion_fast<float><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
-              x.as<float>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
-        else
-          dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
-              x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
-        fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, o + 4);
+        dispersion_fast_any(o + 4);
       }
       MB_LAUNCH_CHECK();
     }
