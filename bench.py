@@ -483,7 +483,7 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     head = run_peer(mb, torch, dist, cfg, args.steps, args.warmup, rank, world, local,
-                    nvlink=True)
+                    nvlink=True, e2e=True)
     clk = clocks.stop()
     coord = c5v = None
     if not args.no_coord:
@@ -523,8 +523,7 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
             "rounds_local": head["rounds_local"], "rounds_cross": head["rounds_cross"],
             "nvlink_counters": head.get("nvlink_counters"),
             "clocks": clk,
-            "e2e": None,
-            "e2e_note": "the host-buffer call is single-GPU (moshpit_run_moshpit); see the N=1 line",
+            "e2e": head["e2e"],
             "coordinate_sharded_weak": coord,
             "peer_sharded_c5v": c5v,
         }
@@ -560,7 +559,51 @@ def run_coord(mb, torch, dist, cfg, steps, warmup, rank, world, local):
             "ms_per_step": round(tt.item() / steps, 4)}
 
 
-def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=False, slabs=None):
+def measure_e2e_peer(mb, torch, dist, sh, cfg, world, calls=3):
+    """End to end at N GPUs through the public Shard API: every rank loads its
+    own peers' rows from pinned host memory (Shard.load_rows), runs the
+    config's R rounds and stores the rows back (Shard.store_rows), host wall
+    clock between barriers, max over ranks, 1 warm-up + median of `calls`.
+    There is no distributed TrialReport, so the result read back is the
+    vectors (the N=1 line's e2e_variants.pinned_f32_fast_with_vectors is the
+    same call shape on one GPU)."""
+    M, d, N, D, p, R = CONFIGS[cfg]
+    rows = sh.rows()
+    host = torch.empty((rows, D), dtype=torch.float32, pin_memory=True).numpy()
+    sh.store_rows(host)  # the current state: the rows a caller would hold
+    torch.cuda.synchronize()
+    secs = []
+    for it in range(calls + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh.load_rows(host)
+        for _ in range(R):
+            sh.round()
+        sh.store_rows(host)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if it:
+            secs.append(t.item())
+    sec = sorted(secs)[len(secs) // 2]
+    moved = world * rows * D * 4
+    return {"value": round(N * D * 4 * R / sec / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": moved // R, "d2h_bytes_per_step": moved // R,
+            "h2d_bytes_per_call": moved, "d2h_bytes_per_call": moved,
+            "call": f"Shard.load_rows (pinned) + {R} rounds + Shard.store_rows on each of "
+                    f"{world} ranks (peer-sharded {cfg})",
+            "seconds": round(sec, 4), "seconds_each": [round(x, 4) for x in secs],
+            "timing": "host wall clock per call between barriers, max over ranks, "
+                      "1 warm-up + median of 3",
+            "bytes_note": "whole job: every rank copies its resident rows in and out"}
+
+
+def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=False, slabs=None,
+             e2e=False):
     """Peer-sharded rounds: peers split by grid digit d-1, rounds on
     axes 0..d-2 local, the axis d-1 round one fused NVLink kernel.  Returns
     the whole-problem metric (strong scaling) and the combined roofline."""
@@ -623,10 +666,17 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     # NVLink throughput counters read N/A on this driver)
     nvl_meas = {"source": "modelled (see profiles/ncu_summary.json nvlink entries for the "
                           "ncu-measured nvlrx bytes of the same kernels)"} if nvlink else None
+    e2e_line = None
+    if e2e:
+        try:
+            e2e_line = measure_e2e_peer(mb, torch, dist, sh, cfg, world)
+        except Exception as exc:  # noqa: BLE001
+            e2e_line = {"error": str(exc)}
     sh.close()
     torch.cuda.empty_cache()
     value = N * D * es * steps / (t_max / 1e3) / 1e9
     return {
+        "e2e": e2e_line,
         "workload": f"{cfg}: {N} peers on {M}^{d}, D={D} fp32, p_fail={p}, peer-sharded over "
                     f"{world} GPU(s) (grid digit d-1 split; axes 0..d-2 local)",
         "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),

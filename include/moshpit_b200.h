@@ -368,6 +368,22 @@ int moshpit_shard_stats(moshpit_shard* s, int32_t k, uint64_t* cross_rounds,
                         uint64_t* local_active_rows);
 int moshpit_shard_pool(moshpit_shard* s, int32_t k, void** ptr, uint64_t* rows,
                        uint64_t* ld);
+/* Host I/O of hosted rank k's pool (its R resident rows of dim elements):
+ * peer_of_row[R] = the peer each row holds (0xffffffff: none; synchronises),
+ * and host <-> pool copies of the R rows (host rows host_ld_bytes apart;
+ * pinned host memory for full PCIe rate), after the prior work on `stream`.
+ * With the slab pipeline (slabs > 1) each column slab moves on its own
+ * stream: a load overlaps the first slabs' rounds (the shard's later rounds,
+ * stores and reads are ordered after it; `stream` itself passes it at the
+ * next flush / store_rows), a store finishes the lagging slabs' rounds and
+ * lets each slab's columns leave as soon as its rounds are done; `stream`
+ * waits for the whole store.  The multi-GPU end-to-end path: each process
+ * loads its own peers, runs the rounds, stores them back. */
+int moshpit_shard_row_peers(moshpit_shard* s, int32_t k, uint32_t* peer_of_row);
+int moshpit_shard_load_rows(moshpit_shard* s, int32_t k, const void* host,
+                            uint64_t host_ld_bytes, void* stream);
+int moshpit_shard_store_rows(moshpit_shard* s, int32_t k, void* host,
+                             uint64_t host_ld_bytes, void* stream);
 /* Cross-round detail (synchronises): device ms of phase A (chunk means +
  * voided-row pulls) and phase B (mean-chunk pulls + voided-row writes) as
  * split by the last moshpit_shard_kernel_time call, and the cumulative

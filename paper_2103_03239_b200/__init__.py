@@ -878,6 +878,44 @@ class Shard:
         check(lib().moshpit_shard_read(self._h, _p(out), _p(mask)))
         return out, mask.astype(bool)
 
+    def _rank(self, k):
+        return self.rank if k is None else k
+
+    def rows(self) -> int:
+        """Rows of each rank's pool (its resident peers)."""
+        ptr, rows, ld = C.c_void_p(), C.c_uint64(0), C.c_uint64(0)
+        check(lib().moshpit_shard_pool(self._h, self.rank, C.byref(ptr), C.byref(rows),
+                                       C.byref(ld)))
+        return rows.value
+
+    def row_peers(self, k: Optional[int] = None) -> np.ndarray:
+        """The peer held by each row of rank k's pool (-1 as 0xffffffff: none)."""
+        out = np.zeros(self.rows(), dtype=np.uint32)
+        check(lib().moshpit_shard_row_peers(self._h, self._rank(k), _p(out)))
+        return out
+
+    def load_rows(self, host: np.ndarray, k: Optional[int] = None, stream=None):
+        """Host rows -> rank k's pool (row r holds row_peers(k)[r]); `host`
+        is rows() x dim (pinned memory for full PCIe rate), asynchronous on
+        `stream` -- keep `host` alive until the stream passes the copy."""
+        if host.dtype != self.dtype or host.ndim != 2 or host.shape[0] != self.rows() \
+                or host.shape[1] < self.dim:
+            raise InvalidArgument("shard: host rows must be rows() x dim of the shard dtype")
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().moshpit_shard_load_rows(self._h, self._rank(k), _p(host), host.strides[0],
+                                            s.cuda_stream))
+
+    def store_rows(self, host: np.ndarray, k: Optional[int] = None, stream=None):
+        """Rank k's pool -> host rows (after the lagging slabs finish)."""
+        if host.dtype != self.dtype or host.ndim != 2 or host.shape[0] != self.rows() \
+                or host.shape[1] < self.dim or not host.flags.writeable:
+            raise InvalidArgument("shard: host rows must be rows() x dim of the shard dtype")
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().moshpit_shard_store_rows(self._h, self._rank(k), _p(host), host.strides[0],
+                                             s.cuda_stream))
+
     def set_timing(self, enable: bool):
         check(lib().moshpit_shard_set_timing(self._h, 1 if enable else 0))
 

@@ -123,6 +123,9 @@ PROTOTYPES = {
     "moshpit_shard_stats": (C.c_int, [vp, i32, P(u64), P(u64), P(u64)]),
     "moshpit_shard_cross_detail": (C.c_int, [vp, i32, P(dbl), P(dbl), P(u64)]),
     "moshpit_shard_pool": (C.c_int, [vp, i32, P(vp), P(u64), P(u64)]),
+    "moshpit_shard_row_peers": (C.c_int, [vp, i32, vp]),
+    "moshpit_shard_load_rows": (C.c_int, [vp, i32, vp, u64, vp]),
+    "moshpit_shard_store_rows": (C.c_int, [vp, i32, vp, u64, vp]),
     "moshpit_fill_synthetic": (C.c_int, [C.c_int, vp, u64, u64, u64, u64, u64, vp]),
 }
 

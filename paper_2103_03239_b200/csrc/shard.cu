@@ -962,13 +962,52 @@ struct Shard {
   // every slab stream.  S = 1: nothing to do.
   void flush(cudaStream_t s) {
     if (S == 1) return;
+    catch_up();
+    join(s);
+  }
+  // issue every round still owed to the lagging slabs
+  void catch_up() {
     for (std::uint32_t step = 0; step + 1 < S; ++step)
       for (std::uint32_t k = 0; k < S; ++k)
         if (slab_done[k] < round_no) run_slab(k, slab_done[k]);
+  }
+  // order s after everything issued on the slab streams
+  void join(cudaStream_t s) {
     for (std::uint32_t k = 0; k < S; ++k) {
       MB_CUDA(cudaEventRecord(ev_slab[k], ss[k]->s));
       MB_CUDA(cudaStreamWaitEvent(s, ev_slab[k], 0));
     }
+  }
+  // Host <-> pool copies of hosted rank r's rows.  With the slab pipeline
+  // each slab's columns move on that slab's stream, so a load overlaps the
+  // first slabs' rounds and a store overlaps the last slabs' catch-up rounds.
+  void copy_rows(std::uint32_t r, void* host, std::uint64_t host_ld, bool to_host,
+                 cudaStream_t s) {
+    const auto kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+    auto copy = [&](std::uint64_t c0, std::uint64_t c1, cudaStream_t cs) {
+      if (c1 <= c0) return;
+      char* dev = static_cast<char*>(pools[r]) + c0 * es;
+      char* hst = static_cast<char*>(host) + c0 * es;
+      if (to_host)
+        MB_CUDA(cudaMemcpy2DAsync(hst, host_ld, dev, ld * es, (c1 - c0) * es, R, kind, cs));
+      else
+        MB_CUDA(cudaMemcpy2DAsync(dev, ld * es, hst, host_ld, (c1 - c0) * es, R, kind, cs));
+    };
+    if (S == 1) {
+      copy(0, dim, s);
+      return;
+    }
+    MB_CUDA(cudaEventRecord(ev_user, s));
+    for (std::uint32_t k = 0; k < S; ++k) MB_CUDA(cudaStreamWaitEvent(ss[k]->s, ev_user, 0));
+    if (to_host) catch_up();
+    const std::uint64_t kv = 16 / es;
+    for (std::uint32_t k = 0; k < S; ++k)
+      copy(vb[k] * kv, std::min<std::uint64_t>(ve[k] * kv, dim), ss[k]->s);
+    // a store joins the caller's stream; a load stays on the slab streams
+    // (joining would make every slab's first round wait for the whole load):
+    // the shard's later rounds / stores / reads are ordered after it, and
+    // `s` passes it at the next flush or store_rows
+    if (to_host) join(s);
   }
 };
 
@@ -1381,6 +1420,55 @@ int moshpit_shard_cross_detail(moshpit_shard* h, std::int32_t k, double* phase_a
 }
 
 // Device pointer / rows / stride of hosted rank k's pool (else the first).
+// Host I/O of a hosted rank's pool (its R resident rows, dim coordinates
+// each): the peer held by every row, and pinned-or-pageable host <-> pool
+// copies on `stream` (ordered with round / flush on the same stream).
+int moshpit_shard_row_peers(moshpit_shard* h, std::int32_t k, std::uint32_t* peer_of_row) {
+  return guarded([&] {
+    shard_require(h);
+    Shard& S = *h->s;
+    if (!S.hosts((std::uint32_t)k)) throw std::invalid_argument("shard: rank not hosted here");
+    DeviceGuard g(S.device);
+    StreamHolder st;
+    if (S.S > 1) S.flush(st.s);
+    S.plane->sync_done();
+    MB_CUDA(cudaDeviceSynchronize());
+    const std::uint64_t n = S.plane->n;
+    std::vector<std::uint32_t> loc(n);
+    MB_CUDA(cudaMemcpy(loc.data(), S.loc.ptr, n * 4, cudaMemcpyDeviceToHost));
+    for (std::uint64_t r = 0; r < S.R; ++r) peer_of_row[r] = 0xffffffffu;
+    for (std::uint64_t i = 0; i < n; ++i)
+      if (loc[i] / S.R == (std::uint64_t)k) peer_of_row[loc[i] % S.R] = (std::uint32_t)i;
+  });
+}
+
+int moshpit_shard_load_rows(moshpit_shard* h, std::int32_t k, const void* host,
+                            std::uint64_t host_ld_bytes, void* stream) {
+  return guarded([&] {
+    shard_require(h);
+    Shard& S = *h->s;
+    if (!S.hosts((std::uint32_t)k)) throw std::invalid_argument("shard: rank not hosted here");
+    if (host_ld_bytes < S.dim * S.es) throw std::invalid_argument("shard: host row stride");
+    DeviceGuard g(S.device);
+    S.copy_rows((std::uint32_t)k, const_cast<void*>(host), host_ld_bytes, false,
+                static_cast<cudaStream_t>(stream));
+  });
+}
+
+int moshpit_shard_store_rows(moshpit_shard* h, std::int32_t k, void* host,
+                             std::uint64_t host_ld_bytes, void* stream) {
+  return guarded([&] {
+    shard_require(h);
+    Shard& S = *h->s;
+    if (!S.hosts((std::uint32_t)k)) throw std::invalid_argument("shard: rank not hosted here");
+    if (host_ld_bytes < S.dim * S.es) throw std::invalid_argument("shard: host row stride");
+    DeviceGuard g(S.device);
+    // the lagging slabs finish their rounds first, each slab's columns leave
+    // as soon as its own rounds are done
+    S.copy_rows((std::uint32_t)k, host, host_ld_bytes, true, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int moshpit_shard_pool(moshpit_shard* h, std::int32_t k, void** ptr, std::uint64_t* rows,
                        std::uint64_t* ld) {
   return guarded([&] {
