@@ -320,10 +320,10 @@ struct RepRows {
   const std::uint32_t* list = nullptr;
   const std::uint32_t* count = nullptr;
 };
-// Moshpit-SGD local step fused into hat theta (diag_kernel.cu): steps every
-// row in place (the standalone step kernel's arithmetic and Philox noise) and
-// writes mean_of(post) to hat.  False (nothing launched) unless n = 8 * 2^K,
-// 16-byte rows and at most partial_slots CTAs.
+// Noise-free Moshpit-SGD local step fused into hat theta (diag_kernel.cu):
+// steps every row in place (the standalone step kernel's arithmetic) and
+// writes mean_of(post) to hat.  False (nothing launched) with device noise,
+// or unless n = 8 * 2^K (32 .. 4096) with 16-byte rows.
 template <typename T>
 bool launch_step_colmean(T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
                          const T* curv, const T* tgt, T gamma, double coord_std, int philox,

@@ -16,7 +16,6 @@
 #include "common.cuh"
 #include "blocktree.cuh"
 #include "pairwise.cuh"
-#include "philox.cuh"
 
 namespace mb200 {
 namespace {
@@ -81,7 +80,7 @@ struct ColVec<double> {
 
 constexpr int kCmThreads = 128;
 constexpr int kCmStages = 4;
-constexpr int kCmMaxK = 10;  // n up to 8192
+constexpr int kCmMinK = 2, kCmMaxK = 9;  // n = 32 .. 4096 (the configs: 256, 1024, 4096)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -222,141 +221,88 @@ __global__ void __launch_bounds__(kCmThreads)
 }
 
 // ---------------------------------------------------------------------------
-// Moshpit-SGD local step fused into hat theta = mean_of(post-step vectors)
-// (optimizer.hpp:356-376): every row of the tree is stepped as it enters it
-// -- g = c (theta - t) [+ n_j], theta' = theta - gamma g, separately rounded,
-// the same Philox normals (peer = row, quad of 4 coordinates) as the
-// standalone step kernel -- and written back; the tree then sums the post
-// values.  One read and one write of the state instead of the step's read +
-// write and the mean's read.
+// Noise-free Moshpit-SGD local step fused into hat theta = mean_of(post-step
+// vectors) (optimizer.hpp:356-376): every row of the tree is stepped as it
+// enters it -- g = c (theta - t), theta' = theta - gamma g, separately
+// rounded, the standalone step kernel's arithmetic -- and written back; the
+// tree then sums the post values.  One read and one write of the state
+// instead of the step's read + write and the mean's read.
 // ---------------------------------------------------------------------------
 template <typename T>
-struct StepArgs {
-  const T* curv;
-  const T* tgt;
-  T gamma;
-  double coord_std;
-  std::uint64_t step_no;
-  PhiloxKeys pk;
-  std::uint32_t* nonfinite;
-  double* noise_partial;  // [gridDim.x] sum of n_j^2 per CTA
-};
-
-template <typename T, bool NOISY>
 struct StepLeafOp {
   using V = typename ColVec<T>::V;
   static constexpr int W = ColVec<T>::W;
   V c, t;
   T gamma;
-  double coord_std;
-  std::uint64_t step_no, cv, dim;
-  const PhiloxKeys* pk;
+  std::uint64_t cv, dim;
   V* out;  // this thread's column vector of row 0
   std::uint64_t ldv;
   bool live;
   T chk;
-  double nsq;
 
   __device__ __forceinline__ void operator()(V& e, std::uint32_t row) {
     if (!live) return;
-    float z[4] = {0.f, 0.f, 0.f, 0.f};
-    // quad of 4 coordinates: fp32 vectors are quads, fp64 vectors halves
-    const std::uint64_t quad = W == 4 ? cv : cv >> 1;
-    const int zo = W == 4 ? 0 : (int)(cv & 1) * 2;
-    if constexpr (NOISY) philox_normals4(*pk, step_no, row, quad, z);
     T* pe = reinterpret_cast<T*>(&e);
     const T* pc = reinterpret_cast<const T*>(&c);
     const T* pt = reinterpret_cast<const T*>(&t);
-    T q = T(0);
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       if (cv * W + w >= dim) break;
-      T g = mul_rn(pc[w], sub_rn(pe[w], pt[w]));
-      if constexpr (NOISY) {
-        const T nj = noise_component(z[zo + w], coord_std, (T*)nullptr);
-        nsq_add(q, nj);
-        g = add_rn(g, nj);
-      }
-      chk = fma0(g, chk);
+      const T g = mul_rn(pc[w], sub_rn(pe[w], pt[w]));
+      chk = add_rn(chk, mul_rn(g, T(0)));  // stays 0 unless some g is inf / NaN
       pe[w] = sub_rn(pe[w], mul_rn(gamma, g));
     }
-    if constexpr (NOISY) nsq += (double)q;
     out[(std::uint64_t)row * ldv] = e;
   }
   __device__ static float sub_rn(float a, float b) { return __fsub_rn(a, b); }
   __device__ static float mul_rn(float a, float b) { return __fmul_rn(a, b); }
   __device__ static float add_rn(float a, float b) { return __fadd_rn(a, b); }
-  __device__ static float fma0(float g, float acc) { return __fmaf_rn(g, 0.f, acc); }
   __device__ static double sub_rn(double a, double b) { return __dsub_rn(a, b); }
   __device__ static double mul_rn(double a, double b) { return __dmul_rn(a, b); }
   __device__ static double add_rn(double a, double b) { return __dadd_rn(a, b); }
-  __device__ static double fma0(double g, double acc) { return __fma_rn(g, 0.0, acc); }
 };
 
-template <int K, typename T, bool NOISY>
+template <int K, typename T>
 __global__ void __launch_bounds__(kCmThreads)
     step_colmean_staged(T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
-                        double* __restrict__ hat, const __grid_constant__ StepArgs<T> a) {
+                        double* __restrict__ hat, const T* __restrict__ curv,
+                        const T* __restrict__ tgt, T gamma, std::uint32_t* nonfinite) {
   using V = typename ColVec<T>::V;
   constexpr int W = ColVec<T>::W;
   constexpr int N = 8 << K;
   extern __shared__ __align__(16) unsigned char cm_smem[];
   V* const ring = reinterpret_cast<V*>(cm_smem);
   const std::uint64_t cv = blockIdx.x * (std::uint64_t)kCmThreads + threadIdx.x;
-  const bool live = cv * W < dim;  // no early exit: the CTA reduces nsq at the end
+  if (cv * W >= dim) return;
   const std::uint64_t ldv = ld / W;
-  StepLeafOp<T, NOISY> op;
-  op.c = op.t = V{};
-  if (live) {
-    if (cv * W + W <= dim) {
-      op.c = __ldg(reinterpret_cast<const V*>(a.curv) + cv);
-      op.t = __ldg(reinterpret_cast<const V*>(a.tgt) + cv);
-    } else {
-      T* pc = reinterpret_cast<T*>(&op.c);
-      T* pt = reinterpret_cast<T*>(&op.t);
+  StepLeafOp<T> op;
+  if (cv * W + W <= dim) {
+    op.c = __ldg(reinterpret_cast<const V*>(curv) + cv);
+    op.t = __ldg(reinterpret_cast<const V*>(tgt) + cv);
+  } else {
+    T* pc = reinterpret_cast<T*>(&op.c);
+    T* pt = reinterpret_cast<T*>(&op.t);
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        if (cv * W + w < dim) {
-          pc[w] = a.curv[cv * W + w];
-          pt[w] = a.tgt[cv * W + w];
-        }
-      }
+    for (int w = 0; w < W; ++w) {
+      pc[w] = cv * W + w < dim ? curv[cv * W + w] : T(0);
+      pt[w] = cv * W + w < dim ? tgt[cv * W + w] : T(0);
     }
   }
-  op.gamma = a.gamma;
-  op.coord_std = a.coord_std;
-  op.step_no = a.step_no;
+  op.gamma = gamma;
   op.cv = cv;
   op.dim = dim;
-  op.pk = &a.pk;
   op.out = reinterpret_cast<V*>(x) + cv;
   op.ldv = ldv;
-  op.live = live;
+  op.live = true;
   op.chk = T(0);
-  op.nsq = 0.0;
-  CmThread<K, T, StepLeafOp<T, NOISY>> c{reinterpret_cast<const V*>(x) + cv, ldv, nullptr,
-                                         ring + threadIdx.x, live, op};
+  CmThread<K, T, StepLeafOp<T>> c{reinterpret_cast<const V*>(x) + cv, ldv, nullptr,
+                                  ring + threadIdx.x, true, op};
   double v[W];
   cm_tree<K>(c, v);
-  if (live) {
 #pragma unroll
-    for (int w = 0; w < W; ++w)
-      if (cv * W + w < dim) hat[cv * W + w] = __ddiv_rn(v[w], (double)N);
-  }
-  if (c.leaf.chk != T(0)) atomicOr(a.nonfinite, 1u);
-  if constexpr (NOISY) {
-    __shared__ double red[kCmThreads / 32];
-    double q = c.leaf.nsq;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
-    __syncthreads();
-    if (threadIdx.x == 0 && a.noise_partial) {
-      double t = 0.0;
-      for (int i = 0; i < kCmThreads / 32; ++i) t += red[i];
-      a.noise_partial[blockIdx.x] = t;
-    }
-  }
+  for (int w = 0; w < W; ++w)
+    if (cv * W + w < dim) hat[cv * W + w] = __ddiv_rn(v[w], (double)N);
+  if (c.leaf.chk != T(0)) atomicOr(nonfinite, 1u);
 }
 
 template <int K, typename T>
@@ -439,10 +385,8 @@ bool try_colmean_staged(const T* x, std::uint64_t n, std::uint64_t ld, std::uint
                         const std::uint32_t* rows, double* out, cudaStream_t s) {
   constexpr int W = ColVec<T>::W;
   if (ld % W != 0 || reinterpret_cast<std::uintptr_t>(x) % 16 != 0) return false;
-  if (n < 8 || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
+  if (n < (8u << kCmMinK) || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
   switch (__builtin_ctzll(n) - 3) {
-    case 0: launch_colmean_staged<0, T>(x, ld, dim, rows, out, s); break;
-    case 1: launch_colmean_staged<1, T>(x, ld, dim, rows, out, s); break;
     case 2: launch_colmean_staged<2, T>(x, ld, dim, rows, out, s); break;
     case 3: launch_colmean_staged<3, T>(x, ld, dim, rows, out, s); break;
     case 4: launch_colmean_staged<4, T>(x, ld, dim, rows, out, s); break;
@@ -451,7 +395,6 @@ bool try_colmean_staged(const T* x, std::uint64_t n, std::uint64_t ld, std::uint
     case 7: launch_colmean_staged<7, T>(x, ld, dim, rows, out, s); break;
     case 8: launch_colmean_staged<8, T>(x, ld, dim, rows, out, s); break;
     case 9: launch_colmean_staged<9, T>(x, ld, dim, rows, out, s); break;
-    case 10: launch_colmean_staged<10, T>(x, ld, dim, rows, out, s); break;
     default: return false;
   }
   MB_LAUNCH_CHECK();
@@ -994,37 +937,21 @@ std::size_t diag_partial_elems(std::uint64_t n, std::uint64_t dim) {
 
 namespace {
 
-template <int K, typename T, bool NOISY>
+template <int K, typename T>
 void launch_step_colmean_k(T* x, std::uint64_t ld, std::uint64_t dim, double* hat,
-                           const StepArgs<T>& a, unsigned grid, cudaStream_t s) {
+                           const T* curv, const T* tgt, T gamma, std::uint32_t* nonfinite,
+                           unsigned grid, cudaStream_t s) {
   constexpr std::size_t smem = (std::size_t)kCmStages * 8 * kCmThreads * 16;
   static thread_local int attr_dev = -1;
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
   if (attr_dev != dev) {
-    MB_CUDA(cudaFuncSetAttribute(step_colmean_staged<K, T, NOISY>,
+    MB_CUDA(cudaFuncSetAttribute(step_colmean_staged<K, T>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_dev = dev;
   }
-  step_colmean_staged<K, T, NOISY><<<grid, kCmThreads, smem, s>>>(x, ld, dim, hat, a);
-}
-
-template <typename T, bool NOISY>
-void launch_step_colmean_n(int k, T* x, std::uint64_t ld, std::uint64_t dim, double* hat,
-                           const StepArgs<T>& a, unsigned grid, cudaStream_t s) {
-  switch (k) {
-    case 0: launch_step_colmean_k<0, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 1: launch_step_colmean_k<1, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 2: launch_step_colmean_k<2, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 3: launch_step_colmean_k<3, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 4: launch_step_colmean_k<4, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 5: launch_step_colmean_k<5, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 6: launch_step_colmean_k<6, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 7: launch_step_colmean_k<7, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 8: launch_step_colmean_k<8, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    case 9: launch_step_colmean_k<9, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-    default: launch_step_colmean_k<10, T, NOISY>(x, ld, dim, hat, a, grid, s); break;
-  }
+  step_colmean_staged<K, T><<<grid, kCmThreads, smem, s>>>(x, ld, dim, hat, curv, tgt, gamma,
+                                                           nonfinite);
 }
 
 }  // namespace
@@ -1036,19 +963,28 @@ bool launch_step_colmean(T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t 
                          double* noise_partial, std::uint64_t partial_slots, double* hat,
                          cudaStream_t s) {
   constexpr int W = ColVec<T>::W;
-  if (dim == 0 || ld % W != 0 || reinterpret_cast<std::uintptr_t>(x) % 16 != 0) return false;
+  (void)coord_std, (void)seed, (void)step_no, (void)noise_partial, (void)partial_slots;
+  // noise-free steps only: with the Philox rounds the fused kernel (its tree
+  // stack plus the generator at 12 warps/SM) measured 3.6 ms at C4 against
+  // 1.9 + 0.6 ms for the vectorised step kernel + the staged mean
+  // (profiles/r02/c4diag_launches_*)
+  if (philox || dim == 0) return false;
+  if (ld % W != 0 || reinterpret_cast<std::uintptr_t>(x) % 16 != 0) return false;
   if (reinterpret_cast<std::uintptr_t>(curv) % 16 != 0 ||
       reinterpret_cast<std::uintptr_t>(tgt) % 16 != 0)
     return false;
-  if (n < 8 || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
-  const std::uint64_t nv = (dim + W - 1) / W;
-  const std::uint64_t grid = (nv + kCmThreads - 1) / kCmThreads;
-  if (philox && grid > partial_slots) return false;
-  StepArgs<T> a{curv, tgt, gamma, coord_std, step_no, philox_keys(seed), nonfinite,
-                noise_partial};
-  const int k = __builtin_ctzll(n) - 3;
-  if (philox) launch_step_colmean_n<T, true>(k, x, ld, dim, hat, a, (unsigned)grid, s);
-  else launch_step_colmean_n<T, false>(k, x, ld, dim, hat, a, (unsigned)grid, s);
+  if (n < (8u << kCmMinK) || (n & (n - 1)) != 0 || n > (8u << kCmMaxK)) return false;
+  const unsigned grid = (unsigned)(((dim + W - 1) / W + kCmThreads - 1) / kCmThreads);
+  switch (__builtin_ctzll(n) - 3) {
+    case 2: launch_step_colmean_k<2, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 3: launch_step_colmean_k<3, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 4: launch_step_colmean_k<4, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 5: launch_step_colmean_k<5, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 6: launch_step_colmean_k<6, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 7: launch_step_colmean_k<7, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    case 8: launch_step_colmean_k<8, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+    default: launch_step_colmean_k<9, T>(x, ld, dim, hat, curv, tgt, gamma, nonfinite, grid, s); break;
+  }
   MB_LAUNCH_CHECK();
   return true;
 }

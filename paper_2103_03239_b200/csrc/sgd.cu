@@ -1082,15 +1082,11 @@ static int run_sgd(
           r.lstep<double>(x.ptr, n, gamma, coord_std, philox, seed, k,
                           static_cast<const double*>(host_noise));
       }
-      // the step fused into hat theta = mean_of(post) when the noise is the
-      // device's (or none) and n = 8 * 2^K: one pass over the state instead
-      // of the step's read + write and the mean's read
-      static const int fused_hat_mode = [] {  // 0 never, 1 sigma == 0 only, 2 always
-        const char* e = std::getenv("MOSHPIT_SGD_FUSED_HAT");
-        return e ? std::atoi(e) : 1;
-      }();
+      // the noise-free step fused into hat theta = mean_of(post) for
+      // n = 8 * 2^K: one pass over the state instead of the step's read +
+      // write and the mean's read
       auto fused_hat = [&](auto* xs, auto* cs, auto* ts, auto g) {
-        return !logit && !host_noise && (fused_hat_mode == 2 || (fused_hat_mode == 1 && !philox)) &&
+        return !logit && !host_noise &&
                launch_step_colmean(xs, n, r.ld, dim, cs, ts, g, coord_std, philox, seed, k,
                                    r.flag.as<std::uint32_t>(),
                                    r.npart.as<double>() + (std::uint64_t)k * 148 * 16, 148 * 16,

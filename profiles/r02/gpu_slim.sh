@@ -1,0 +1,3 @@
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sgd.py tests/test_gpu_noise.py tests/test_gpu_batch.py -x -q 2>&1 | tail -2
+timeout 600 python profiles/r02/c4_diag.py
+timeout 600 python profiles/diag_probe.py 2>&1 | tail -1
