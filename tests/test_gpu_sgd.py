@@ -78,6 +78,36 @@ def test_sgd_f32_bit_exact_vs_oracle(mb, oracle, sigma, tau, sched):
                                atol=1e-300)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("n,M,tau,sched", [(64, 8, 1, ()), (32, 8, 2, ()), (256, 16, 1, ()),
+                                           (64, 8, 1, ((5, -32), (9, 32)))])
+def test_sgd_diagnostics_fused_paths_vs_oracle(mb, oracle, dt, n, M, tau, sched):
+    """n = 8 * 2^K peers with 16-byte rows: the noise-free step fused into the
+    post-step mean (hat theta) and the representative-row mean / dispersion
+    after each averaging pass -- EXACT diagnostics bit-exact vs the oracle,
+    FAST within its tolerance (membership events take n off the power of 2
+    and back)."""
+    dim = 40
+    tgt = oracle.stream_draws(11, "objective", dim, "normal")
+    res = oracle.sgd_quadratic(M, 2, n, dim, 2.0, 0.5, tgt, np.zeros(dim), 0.05, tau, 16, 0.0,
+                               99, schedule=sched, dtype=dt)
+    cfg = mb.OptimizerConfig(gamma=0.05, tau=tau, steps=16, grid=mb.GridConfig(M, 2, 1),
+                             sigma=0.0, n_peers=n)
+    ev = [mb.MembershipEvent(*e) for e in sched]
+    r = mb.run_moshpit_sgd(cfg, mb.Quadratic(dim, 2.0, 0.5, tgt), np.zeros(dim), ev, mb.Rng(99),
+                           dtype=dt, return_thetas=True)
+    assert bits_equal(r.final_thetas, res["final_thetas"])
+    assert bits_equal(np.array(r.f_gap), res["f_gap"])
+    assert bits_equal(np.array(r.grad_norm_sq), res["grad_norm_sq"])
+    assert bits_equal(np.array(r.diagnostics.dispersion), res["dispersion"])
+    fast = mb.run_moshpit_sgd(cfg, mb.Quadratic(dim, 2.0, 0.5, tgt), np.zeros(dim), ev,
+                              mb.Rng(99), dtype=dt, diagnostics="fast", return_thetas=True)
+    assert bits_equal(fast.final_thetas, res["final_thetas"])
+    np.testing.assert_allclose(fast.f_gap, res["f_gap"], rtol=1e-12)
+    np.testing.assert_allclose(fast.diagnostics.dispersion, res["dispersion"], rtol=1e-12,
+                               atol=1e-300)
+
+
 def test_sgd_validation_matches_reference(mb):
     quad = mb.Quadratic(2, 2.0, 1.0, [1.0, 1.0])
     cfg = mb.OptimizerConfig(gamma=0.1, tau=2, steps=20, grid=mb.GridConfig(4, 2, 1), sigma=0.5,
