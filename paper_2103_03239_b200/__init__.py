@@ -803,9 +803,10 @@ class Shard:
 
         sh = Shard(grid, n, failure, rng, dim, rank=r, world=w, device=local)
         sh.connect(process_group)        # all_gather of CUDA IPC handles
-        sh.fill_synthetic(seed)
+        sh.fill_synthetic(seed)          # or sh.load_rows(host) (sh.row_peers(): the placement)
         for _ in range(rounds): sh.round()
         sh.flush()                       # slabs > 1: finish the lagging slabs
+        sh.store_rows(host)              # optional: the rows back to the host
 
     ``ranks_per_process=k`` hosts ranks [rank, rank+k) here (rank a multiple of
     k; e.g. world 8 on 4 GPUs); ``emulate=True`` hosts all ``world`` ranks on
@@ -825,6 +826,7 @@ class Shard:
         self.device = int(device)
         self.dtype = np.dtype(dtype)
         self.slabs = int(slabs)
+        self._loading = []  # host buffers of load_rows copies possibly in flight
         h = C.c_void_p()
         check(lib().moshpit_shard_create_ex(_dtype_code(self.dtype), grid.peers_per_axis,
                                             grid.dims, self.n, failure.p_round, rng.seed(),
@@ -836,6 +838,7 @@ class Shard:
         if getattr(self, "_h", None):
             lib().moshpit_shard_destroy(self._h)
             self._h = None
+        self._loading = []
 
     __del__ = close
 
@@ -876,6 +879,7 @@ class Shard:
         out = np.zeros((self.n, self.dim), dtype=self.dtype)
         mask = np.zeros(self.n, dtype=np.uint8)
         check(lib().moshpit_shard_read(self._h, _p(out), _p(mask)))
+        self._loading = []
         return out, mask.astype(bool)
 
     def _rank(self, k):
@@ -892,6 +896,7 @@ class Shard:
         """The peer held by each row of rank k's pool (-1 as 0xffffffff: none)."""
         out = np.zeros(self.rows(), dtype=np.uint32)
         check(lib().moshpit_shard_row_peers(self._h, self._rank(k), _p(out)))
+        self._loading = []
         return out
 
     def load_rows(self, host: np.ndarray, k: Optional[int] = None, stream=None):
@@ -905,6 +910,9 @@ class Shard:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().moshpit_shard_load_rows(self._h, self._rank(k), _p(host), host.strides[0],
                                             s.cuda_stream))
+        # the copy may still be in flight: hold the buffer until a call that
+        # synchronises the device (row_peers, read, close)
+        self._loading.append(host)
 
     def store_rows(self, host: np.ndarray, k: Optional[int] = None, stream=None):
         """Rank k's pool -> host rows (after the lagging slabs finish)."""
