@@ -274,6 +274,15 @@ int moshpit_engine_set_kernel(moshpit_engine* e, int variant);
 int moshpit_engine_round(moshpit_engine* e, int dtype, void* state,
                          uint64_t dim, uint64_t ld, void* stream,
                          uint32_t* active_out);
+/* `rounds` rounds in ONE pass over the state (temporal blocking over column
+ * tiles; n <= 1800 peers): the same draws, groups and bits as `rounds` calls
+ * of moshpit_engine_round, 2 * n * dim * elem bytes of HBM traffic per pass
+ * of up to ~12 rounds (n = 1024) instead of per round -- a separate mode,
+ * not the per-round path.  active_out (nullable) = [rounds] non-failed
+ * peers.  Enqueued on `stream`, no synchronisation. */
+int moshpit_engine_rounds_fused(moshpit_engine* e, int dtype, void* state,
+                                uint64_t dim, uint64_t ld, uint32_t rounds,
+                                void* stream, uint32_t* active_out);
 /* Synchronise the engine's last stream and report how many rounds ran and
  * how many peer rows sat in non-voided groups, summed over those rounds.
  * Algorithmic HBM bytes of kernel 2 = 2 * elem * dim * active_rows_total. */

@@ -702,6 +702,19 @@ class Engine:
                                          s.cuda_stream, C.byref(act)))
         return act.value
 
+    def rounds_fused(self, state, rounds: int, dim: Optional[int] = None, stream=None):
+        """Enqueue ``rounds`` rounds in one pass over the state (temporal
+        blocking; n <= 1800): the same results as ``rounds`` calls of
+        round().  Returns the per-round active (non-failed) peer counts."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        act = np.zeros(max(int(rounds), 1), dtype=np.uint32)
+        check(lib().moshpit_engine_rounds_fused(self._h, code, ptr,
+                                                state.shape[1] if dim is None else dim, ld,
+                                                int(rounds), s.cuda_stream, _p(act)))
+        return act[:int(rounds)].tolist()
+
     def round_raw(self, dtype_code: int, ptr: int, dim: int, ld: int, stream_handle: int) -> int:
         act = C.c_uint32(0)
         check(lib().moshpit_engine_round(self._h, dtype_code, ptr, dim, ld, stream_handle,

@@ -98,6 +98,7 @@ PROTOTYPES = {
     "moshpit_engine_destroy": (C.c_int, [vp]),
     "moshpit_engine_set_kernel": (C.c_int, [vp, C.c_int]),
     "moshpit_engine_round": (C.c_int, [vp, C.c_int, vp, u64, u64, vp, P(u32)]),
+    "moshpit_engine_rounds_fused": (C.c_int, [vp, C.c_int, vp, u64, u64, u32, vp, vp]),
     "moshpit_engine_stats": (C.c_int, [vp, P(u64), P(u64)]),
     "moshpit_engine_set_timing": (C.c_int, [vp, C.c_int]),
     "moshpit_engine_kernel_time": (C.c_int, [vp, P(dbl), P(u64)]),

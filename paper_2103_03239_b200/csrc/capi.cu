@@ -77,6 +77,7 @@ struct moshpit_engine {
   std::uint64_t diag_dim = 0;
   DeviceBuffer ref, mean, sq, part, part2, log;  // log: [0] initial, then (dist, drift) pairs
   DeviceBuffer rep, rlist, rcount;               // representatives of the last round
+  RoundTables fused;                             // tables of moshpit_engine_rounds_fused
   std::uint64_t log_cap = 0, log_n = 0;
   std::unique_ptr<StreamHolder> aux;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -796,6 +797,37 @@ int moshpit_engine_round(moshpit_engine* e, int dtype, void* state, std::uint64_
     const std::uint32_t a = e->plane->round(&e->fail, e->p, e->clock, dtype, state, dim, ld,
                                             static_cast<cudaStream_t>(stream), e->variant);
     if (active_out) *active_out = a;
+  });
+}
+
+// Several rounds in one pass over the state (temporal blocking, a separate
+// mode from the per-round path): kernel 1 for each round, then one fused
+// kernel per chunk of at most fused_rounds_max(n) rounds.  Bit-identical to
+// `rounds` calls of moshpit_engine_round.
+int moshpit_engine_rounds_fused(moshpit_engine* e, int dtype, void* state, std::uint64_t dim,
+                                std::uint64_t ld, std::uint32_t rounds, void* stream,
+                                std::uint32_t* active_out) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (!state) throw std::invalid_argument("fused rounds: null state");
+    check_state(dtype, state, dim, ld);
+    Plane& p = *e->plane;
+    const std::uint32_t cap = fused_rounds_max(p.n);
+    if (cap == 0) throw std::invalid_argument("fused rounds: too many peers for one pass");
+    DeviceGuard g(p.device);
+    auto s = static_cast<cudaStream_t>(stream);
+    for (std::uint32_t done = 0; done < rounds;) {
+      const std::uint32_t R = std::min(cap, rounds - done);
+      e->fused.form(p, R, &e->fail, e->p, e->clock, s, active_out ? active_out + done : nullptr);
+      if (dtype == MOSHPIT_F32)
+        launch_rounds_fused<float>(static_cast<float*>(state), ld, dim, (std::uint32_t)p.n,
+                                   e->fused.dev(), R, nullptr, s);
+      else
+        launch_rounds_fused<double>(static_cast<double*>(state), ld, dim, (std::uint32_t)p.n,
+                                    e->fused.dev(), R, nullptr, s);
+      p.mark_done(s);
+      done += R;
+    }
   });
 }
 

@@ -295,6 +295,22 @@ void launch_group_mean_step(T* state, std::uint64_t ld, std::uint64_t dim,
                             const std::uint32_t* act, const std::uint32_t* counts,
                             const StepPrologue<T>& sp, cudaStream_t s);
 int group_mean_step_grid(bool f64, bool noisy);
+// Several rounds in one pass over the state (fused_rounds.cu): the device
+// tables of one round (kernel 1's output) ...
+struct FusedRound {
+  const std::uint32_t* members = nullptr;
+  const std::uint32_t* goff = nullptr;
+  const std::uint32_t* act = nullptr;
+  const std::uint32_t* counts = nullptr;
+};
+// ... the most rounds one pass can hold for n peers (0: n too large, > ~1800) ...
+std::uint32_t fused_rounds_max(std::uint64_t n);
+// ... and the pass: optional kernel-3 step, then R rounds (rounds_dev: [R]
+// tables in device memory), bit-identical to kernel 3 + R - 1 kernel-2 rounds.
+template <typename T>
+void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
+                         const FusedRound* rounds_dev, std::uint32_t R,
+                         const StepPrologue<T>* step, cudaStream_t s);
 // Kernel-2 grid cap for launches from the calling thread (0 = every SM).
 void set_k2_grid_sms(int sms);
 // fp32 LogisticRegression step on the tensor cores (tc_logit.cu: tcgen05

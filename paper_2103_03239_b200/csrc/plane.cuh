@@ -283,6 +283,39 @@ struct Plane {
 };
 
 
+// The tables of R consecutive rounds of a Plane (kernel 1 each, no data
+// pass) copied aside for the fused-rounds kernel (fused_rounds.cu).
+struct RoundTables {
+  DeviceBuffer members, goff, act, counts, rounds;
+  void form(Plane& p, std::uint32_t R, Xoshiro* fail, double prob, Xoshiro& clock,
+            cudaStream_t s, std::uint32_t* active_out = nullptr) {
+    const std::uint64_t n = p.n;
+    members.resize(R * n * 4 + 16);
+    goff.resize(R * (n + 1) * 4 + 16);
+    act.resize(R * n * 4 + 16);
+    counts.resize(R * 16 + 16);
+    rounds.resize(R * sizeof(FusedRound) + 16);
+    std::vector<FusedRound> h(R);
+    for (std::uint32_t r = 0; r < R; ++r) {
+      const std::uint32_t a = p.round(fail, prob, clock, MOSHPIT_F32, nullptr, 0, 0, s, 0);
+      if (active_out) active_out[r] = a;
+      auto* m = members.as<std::uint32_t>() + r * n;
+      auto* g = goff.as<std::uint32_t>() + r * (n + 1);
+      auto* ac = act.as<std::uint32_t>() + r * n;
+      auto* c = counts.as<std::uint32_t>() + r * 4;
+      MB_CUDA(cudaMemcpyAsync(m, p.members.ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+      MB_CUDA(cudaMemcpyAsync(g, p.goff.ptr, (n + 1) * 4, cudaMemcpyDeviceToDevice, s));
+      MB_CUDA(cudaMemcpyAsync(ac, p.act.ptr, n * 4, cudaMemcpyDeviceToDevice, s));
+      MB_CUDA(cudaMemcpyAsync(c, p.counts.ptr, 16, cudaMemcpyDeviceToDevice, s));
+      h[r] = FusedRound{m, g, ac, c};
+    }
+    // pageable source: staged before the call returns
+    MB_CUDA(cudaMemcpyAsync(rounds.ptr, h.data(), R * sizeof(FusedRound),
+                            cudaMemcpyHostToDevice, s));
+  }
+  const FusedRound* dev() const { return static_cast<const FusedRound*>(rounds.ptr); }
+};
+
 // Slab-pipelined run_moshpit over host buffers (stream_run.cu).  The initial
 // state is either one buffer (row i at base + i * pitch_bytes) or an array of
 // row pointers (the drop-in's std::vector<ParamVector>, no flattening).

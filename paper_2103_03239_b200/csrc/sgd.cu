@@ -692,6 +692,7 @@ struct SgdRun {
   cudaStream_t s;
   DeviceBuffer c64, t64, cT, tT, noise_dev, flag, npart, hat, mean, wsum, vpart, vout, dpart;
   DeviceBuffer rep, rlist, rcount;  // representatives after an averaging pass
+  RoundTables tables;               // the fused averaging pass's round tables
   double noise_sq_host = 0.0;
   // LogisticRegression(xs, ys, l2): samples S, rows of xs are dim doubles.
   bool logit = false;
@@ -986,6 +987,15 @@ static int run_sgd(
     // round's loads (one read + one write of the state for step + round 1).
     const bool fused =
         !logit && diag == MOSHPIT_DIAG_NONE && !(coord_std > 0.0 && noise_mode == 0);
+    // MOSHPIT_SGD_FUSED_ROUNDS=1: the step plus every inner round in one pass
+    // (temporal blocking, fused_rounds.cu; bit-identical).  Opt-in: at C4 it
+    // measured 4.4 / 5.1 ms per step (sigma 0 / 1) against 2.86 / 3.07 for
+    // kernel 3 + kernel 2 -- the shared-memory rounds are latency-bound
+    // (profiles/r02/fused_rounds.md)
+    const bool fused_rounds = [] {
+      const char* e = std::getenv("MOSHPIT_SGD_FUSED_ROUNDS");
+      return e && std::atoi(e) != 0;
+    }();
     // no per-step diagnostics: fused quadratic runs and logistic DIAG_NONE
     const bool skip_diag = fused || (logit && diag == MOSHPIT_DIAG_NONE);
     DeviceBuffer cpad, tpad;
@@ -1055,18 +1065,31 @@ static int run_sgd(
           StepPrologue<float> sf;
           StepPrologue<double> sd;
           double* np_slot = r.npart.as<double>() + (std::uint64_t)k * 148 * 16;
-          if (dtype == MOSHPIT_F32) {
-            sf = StepPrologue<float>{cpad.as<float>(), tpad.as<float>(), (float)gamma, coord_std,
-                                     philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
-            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO, &sf);
+          sf = StepPrologue<float>{cpad.as<float>(), tpad.as<float>(), (float)gamma, coord_std,
+                                   philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
+          sd = StepPrologue<double>{cpad.as<double>(), tpad.as<double>(), gamma, coord_std,
+                                    philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
+          if (fused_rounds && inner <= fused_rounds_max(n)) {
+            // the step and all `inner` rounds in one pass over the state
+            // (temporal blocking): bit-identical to kernel 3 + kernel 2
+            r.tables.form(*plane, inner, nullptr, 0.0, avg, h.s);
+            if (dtype == MOSHPIT_F32)
+              launch_rounds_fused<float>(x.as<float>(), r.ld, dim, (std::uint32_t)n,
+                                         r.tables.dev(), inner, &sf, h.s);
+            else
+              launch_rounds_fused<double>(x.as<double>(), r.ld, dim, (std::uint32_t)n,
+                                          r.tables.dev(), inner, &sd, h.s);
+            plane->mark_done(h.s);
           } else {
-            sd = StepPrologue<double>{cpad.as<double>(), tpad.as<double>(), gamma, coord_std,
-                                      philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
-            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO,
-                         nullptr, &sd);
+            if (dtype == MOSHPIT_F32)
+              plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO,
+                           &sf);
+            else
+              plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO,
+                           nullptr, &sd);
+            for (std::uint32_t q = 1; q < inner; ++q)
+              plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
           }
-          for (std::uint32_t q = 1; q < inner; ++q)
-            plane->round(nullptr, 0.0, avg, dtype, x.ptr, dim, r.ld, h.s, MOSHPIT_KERNEL_AUTO);
         } else if (dtype == MOSHPIT_F32) {
           r.step<float>(x.ptr, n, gamma, coord_std, philox, seed, k, nullptr);
         } else {
