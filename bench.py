@@ -305,6 +305,48 @@ def time_engine_rounds(mb, torch, eng, x, steps, record=False):
     return t_ms, k_ms, k_launches, rows1 - rows0
 
 
+def measure_rounds_fused(mb, torch, cfg, local, reps=3):
+    """SURVEY 8d's separately named temporal-blocking mode: the config's R
+    rounds in one pass over the state (Engine.rounds_fused; bit-identical to
+    R per-round calls, tests/test_gpu_fused_rounds.py) against R per-round
+    calls, CUDA events around the enqueued rounds (host draws + kernel 1
+    included), best of `reps`.  Its byte count is 2 * N * D * 4 per PASS, so
+    it is reported beside the per-round metric, never as it."""
+    M, d, N, D, p, R = CONFIGS[cfg]
+    x = torch.empty((N, D), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    res = {}
+    for mode in ("per_round", "fused"):
+        best = None
+        for _ in range(reps):
+            mb.fill_synthetic(x, INIT_SEED)
+            eng = mb.Engine(mb.GridConfig(M, d, R), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED),
+                            device=local)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if mode == "fused":
+                eng.rounds_fused(x, R)
+            else:
+                for _ in range(R):
+                    eng.round(x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+            eng.close()
+        res[mode] = best
+    del x
+    torch.cuda.empty_cache()
+    return {"workload": f"{cfg}: {R} rounds, fp32, one pass over column tiles of all {N} peers",
+            "ms_fused": round(res["fused"], 3), "ms_per_round_path": round(res["per_round"], 3),
+            "speedup": round(res["per_round"] / res["fused"], 3),
+            "peer_vector_gbs_per_round_equiv": round(N * D * 4 * R / (res["fused"] / 1e3) / 1e9, 1),
+            "hbm_bytes_per_pass": 2 * N * D * 4,
+            "note": "temporal blocking (SURVEY 8d): bytes per pass, not per round; the "
+                    "per-round metric stays kernel 2's one read + one write per round"}
+
+
 def measure_variant(mb, torch, cfg, local, steps, warmup, f64=False, diag=None):
     """A variant of the N=1 headline on the same config: fp64 state and/or
     record_round on the device after every round (FAST or EXACT)."""
@@ -396,6 +438,10 @@ def run_mine(args):
                 variants[name] = measure_variant(mb, torch, cfg, local, vs, 3, **kw)
             except Exception as exc:  # noqa: BLE001
                 variants[name] = {"error": str(exc)}
+        try:  # SURVEY 8d temporal-blocking mode: its own byte count, never the metric
+            variants["rounds_fused_mode"] = measure_rounds_fused(mb, torch, cfg, local)
+        except Exception as exc:  # noqa: BLE001
+            variants["rounds_fused_mode"] = {"error": str(exc)}
     full = full_c5 = None
     if not args.no_full:
         try:
