@@ -529,7 +529,7 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     head = run_peer(mb, torch, dist, cfg, args.steps, args.warmup, rank, world, local,
-                    nvlink=True, e2e=True)
+                    nvlink=True, e2e=not args.no_e2e)
     clk = clocks.stop()
     coord = c5v = None
     if not args.no_coord:
