@@ -16,12 +16,14 @@
 // + kernel 2 (tests/test_gpu_fused_rounds.py).
 //
 // Layout: a persistent CTA per SM (512 threads) keeps the R rounds' tables in
-// shared memory (members, and (beg, count) of every active group) and two
-// tile buffers of n rows x 4 16-byte vectors; the next tile streams in with
-// cp.async while the current one is stepped, averaged R times and stored.
-// Round phase: one thread per (active group, column) walks the group's tree
-// leaf by leaf (<= 4 sequential leaves of <= 8 members for n <= 32; the
-// runtime tree beyond).
+// shared memory (member rows, and (beg, count) of every active group) and two
+// tile buffers of n rows x 4 16-byte vectors (rows XOR-swizzled), one per
+// team of 256 threads: each team loads its tile with cp.async, steps it,
+// averages it R times and stores it, synchronising on its own named barrier,
+// so one team's load and barrier waits overlap the other's compute.  Round
+// phase: a quad of lanes per (active group, vector), one tree leaf per lane
+// (<= 4 sequential leaves of <= 8 members for n <= 32; the runtime tree
+// beyond).
 #include <algorithm>
 
 #include "common.cuh"
@@ -32,6 +34,7 @@ namespace mb200 {
 namespace {
 
 constexpr int kFrThreads = 512;
+constexpr int kFrTeams = 2, kFrTeamThreads = kFrThreads / kFrTeams;
 constexpr int kFrTV = 4;  // 16-byte vectors per row in a tile (64 bytes)
 constexpr std::size_t kFrSmemMax = 226 * 1024;  // 227 KB opt-in less the static reduction buffer
 
@@ -179,50 +182,51 @@ __global__ void __launch_bounds__(kFrThreads, 1)
     if (tid == 0) s_cnt[r] = A;
   }
 
-  V* const gvec = reinterpret_cast<V*>(a.state);
-  auto load = [&](std::uint64_t tile, int buf) {
-    const std::uint64_t v0 = tile * kFrTV;
-    V* dst = tiles + (std::size_t)buf * n * kFrTV;
-    for (std::uint32_t idx = tid; idx < n * kFrTV; idx += kFrThreads) {
-      const std::uint32_t row = idx / kFrTV, v = idx % kFrTV;
-      if (v0 + v < a.nvec)
-        fr_cp16(dst + fr_pos(row, v), gvec + (std::uint64_t)row * a.ld_vec + v0 + v);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  __syncthreads();  // the tables are in place
+
+  // Two teams of 256 threads, each with its own tile buffer, named barrier
+  // and tile sequence: while one team waits on its tile's loads or on a
+  // round barrier, the other computes.
+  const int team = tid / kFrTeamThreads, ttid = tid % kFrTeamThreads;
+  auto team_sync = [&] {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kFrTeamThreads) : "memory");
   };
+  V* const gvec = reinterpret_cast<V*>(a.state);
+  V* const tile = tiles + (std::size_t)team * n * kFrTV;
+  __shared__ V s_ct[kFrTeams][2][kFrTV];
 
   T chk = T(0);
   double nsq = 0.0;
-  int buf = 0;
-  std::uint64_t t = blockIdx.x;
-  if (t < a.n_tiles) load(t, 0);
-  for (; t < a.n_tiles; t += gridDim.x, buf ^= 1) {
-    if (t + gridDim.x < a.n_tiles) load(t + gridDim.x, buf ^ 1);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-    __syncthreads();  // every thread's copies of this tile have landed
-    V* const tile = tiles + (std::size_t)buf * n * kFrTV;
+  const std::uint64_t stride = (std::uint64_t)gridDim.x * kFrTeams;
+  for (std::uint64_t t = (std::uint64_t)blockIdx.x * kFrTeams + team; t < a.n_tiles; t += stride) {
     const std::uint64_t v0 = t * kFrTV;
+    for (std::uint32_t idx = ttid; idx < n * kFrTV; idx += kFrTeamThreads) {
+      const std::uint32_t row = idx / kFrTV, v = idx % kFrTV;
+      if (v0 + v < a.nvec)
+        fr_cp16(tile + fr_pos(row, v), gvec + (std::uint64_t)row * a.ld_vec + v0 + v);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    team_sync();  // every thread's copies of this tile have landed
 
     if constexpr (STEP) {
       // kernel 3's step on every (row, vector): g = c (theta - t) [+ n_j],
       // theta' = theta - gamma g, separately rounded; the tile's curvature and
       // target vectors staged in shared memory once
-      __shared__ V s_ct[2][kFrTV];
-      if (tid < 2 * kFrTV) {
-        const std::uint64_t cv = v0 + (tid % kFrTV);
-        const T* src = tid < kFrTV ? a.curv : a.tgt;
-        s_ct[tid / kFrTV][tid % kFrTV] =
+      if (ttid < 2 * kFrTV) {
+        const std::uint64_t cv = v0 + (ttid % kFrTV);
+        const T* src = ttid < kFrTV ? a.curv : a.tgt;
+        s_ct[team][ttid / kFrTV][ttid % kFrTV] =
             cv < a.nvec ? __ldg(reinterpret_cast<const V*>(src) + cv) : fr_zero<V>();
       }
-      __syncthreads();
-      for (std::uint32_t idx = tid; idx < n * kFrTV; idx += kFrThreads) {
+      team_sync();
+      for (std::uint32_t idx = ttid; idx < n * kFrTV; idx += kFrTeamThreads) {
         const std::uint32_t row = idx / kFrTV, v = idx % kFrTV;
         const std::uint64_t cv = v0 + v;
         if (cv >= a.nvec) continue;
         V e = tile[fr_pos(row, v)];
-        const V c = s_ct[0][v];
-        const V tg = s_ct[1][v];
+        const V c = s_ct[team][0][v];
+        const V tg = s_ct[team][1][v];
         T* pe = reinterpret_cast<T*>(&e);
         const T* pc = reinterpret_cast<const T*>(&c);
         const T* pt = reinterpret_cast<const T*>(&tg);
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kFrThreads, 1)
         if constexpr (NOISY) nsq += (double)q;
         tile[fr_pos(row, v)] = e;
       }
-      __syncthreads();
+      team_sync();
     }
 
     // R rounds on the tile: a quad of lanes per (active group, 16-byte
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kFrThreads, 1)
       const std::uint32_t lane4 = (std::uint32_t)tid & 3u;
       const int qbase = tid & 28;
       const unsigned qmask = 0xfu << qbase;
-      for (std::uint32_t item = tid; item < A * kFrTV * 4; item += kFrThreads) {
+      for (std::uint32_t item = ttid; item < A * kFrTV * 4; item += kFrTeamThreads) {
         const std::uint32_t gi = item / (kFrTV * 4), v = (item / 4) % kFrTV;
         const std::uint32_t pk = s_grp[(std::size_t)r * n + gi];
         const std::uint32_t beg = pk >> 16, cnt = pk & 0xffffu;
@@ -313,14 +317,14 @@ __global__ void __launch_bounds__(kFrThreads, 1)
           for (std::uint32_t k = 0; k < cnt; ++k) tile[fr_pos(m[k], v)] = mean;
         }
       }
-      __syncthreads();
+      team_sync();
     }
 
-    for (std::uint32_t idx = tid; idx < n * kFrTV; idx += kFrThreads) {
+    for (std::uint32_t idx = ttid; idx < n * kFrTV; idx += kFrTeamThreads) {
       const std::uint32_t row = idx / kFrTV, v = idx % kFrTV;
       if (v0 + v < a.nvec) gvec[(std::uint64_t)row * a.ld_vec + v0 + v] = tile[fr_pos(row, v)];
     }
-    __syncthreads();  // this buffer is refilled two tiles on
+    team_sync();  // the buffer is refilled by the team's next tile
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 
