@@ -989,7 +989,7 @@ static int run_sgd(
         !logit && diag == MOSHPIT_DIAG_NONE && !(coord_std > 0.0 && noise_mode == 0);
     // MOSHPIT_SGD_FUSED_ROUNDS=1: the step plus every inner round in one pass
     // (temporal blocking, fused_rounds.cu; bit-identical).  Opt-in: at C4 it
-    // measured 4.4 / 5.1 ms per step (sigma 0 / 1) against 2.86 / 3.07 for
+    // measured 3.96 / 4.60 ms per step (sigma 0 / 1) against 2.87 / 3.07 for
     // kernel 3 + kernel 2 -- the shared-memory rounds are latency-bound
     // (profiles/r02/fused_rounds.md)
     const bool fused_rounds = [] {
