@@ -183,7 +183,11 @@ def test_all_failed_round_leaves_state(mb):
 @pytest.mark.parametrize("M,d,n,p,R,dim", [(16, 2, 256, 0.0, 2, 64), (32, 2, 1024, 0.01, 10, 37),
                                            (16, 3, 4096, 0.0, 3, 8), (8, 4, 4096, 0.0, 4, 9),
                                            (5, 2, 24, 0.1, 10, 3), (40, 2, 1600, 0.02, 4, 13),
-                                           (8, 1, 8, 0.3, 3, 1)])
+                                           (8, 1, 8, 0.3, 3, 1),
+                                           # column means over the representative map:
+                                           # distinct rows within / past the staged budget
+                                           (32, 2, 1024, 0.01, 4, 68), (32, 2, 1024, 0.2, 3, 36),
+                                           (8, 2, 64, 0.05, 5, 20)])
 def test_run_moshpit_f32_bit_exact_vs_oracle(mb, oracle, M, d, n, p, R, dim):
     x = oracle.init_state(INIT_SEED, n, dim, dtype=np.float32)
     ro, fo = oracle.run_moshpit(M, d, x, p, 7, R)
