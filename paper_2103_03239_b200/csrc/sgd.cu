@@ -203,7 +203,9 @@ __global__ void sgd_vec_exact(const double* __restrict__ mean, const double* __r
 }
 
 constexpr int kRed = 256;
-constexpr std::uint64_t kChunk = 1 << 16;
+// FAST chunk: 4096 coordinates per CTA (256 CTAs at D = 2^20; 16 at 2^16
+// left the per-step vector sums latency-bound)
+constexpr std::uint64_t kChunk = 1 << 12;
 
 __device__ double blk_sum(double v, double* buf) {
   buf[threadIdx.x] = v;
@@ -268,7 +270,8 @@ __global__ void dispersion_exact(const T* __restrict__ x, std::uint64_t n, std::
   *out = __ddiv_rn(v, (double)n);
 }
 
-// FAST: block (chunk, row) partials, then one fold in (row, chunk) order.
+// FAST: block (chunk, row) partials, then per-row sums in chunk order
+// (row_sums) and one fold over the rows in row order.
 template <typename T>
 __global__ void dispersion_fast(const T* __restrict__ x, std::uint64_t ld, std::uint64_t dim,
                                 const double* __restrict__ mean, std::uint64_t nch,
@@ -309,17 +312,17 @@ __global__ void dispersion_fast_list(const T* __restrict__ x, std::uint64_t ld,
   }
 }
 
-// fold_all in (row, chunk) order with row i's partials read from rep[i]
-__global__ void fold_all_rep(const double* __restrict__ partial, std::uint64_t n,
-                             std::uint64_t nch, const std::uint32_t* __restrict__ rep,
-                             double div, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// V_k's FAST fold, part 1: each row's chunk partials in chunk order (row i's
+// read from rep[i] when given: identical rows share their partials), one
+// thread per row; part 2 is fold_all over the row sums in row order.
+__global__ void row_sums(const double* __restrict__ partial, std::uint64_t n, std::uint64_t nch,
+                         const std::uint32_t* __restrict__ rep, double* __restrict__ out) {
+  const std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* p = partial + (std::uint64_t)(rep ? rep[i] : i) * nch;
   double s = 0.0;
-  for (std::uint64_t i = 0; i < n; ++i) {
-    const double* p = partial + (std::uint64_t)rep[i] * nch;
-    for (std::uint64_t c = 0; c < nch; ++c) s = __dadd_rn(s, p[c]);
-  }
-  *out = __ddiv_rn(s, div);
+  for (std::uint64_t c = 0; c < nch; ++c) s = __dadd_rn(s, p[c]);
+  out[i] = s;
 }
 
 __global__ void fold_all(const double* __restrict__ partial, std::uint64_t count, double div,
@@ -945,7 +948,7 @@ static int run_sgd(
     r.wsum.resize(D * 8);
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     r.vpart.resize((nch + 1) * 4 * 8 + 64);
-    r.dpart.resize(n_max * (nch + 1) * 8 + 16);
+    r.dpart.resize(n_max * ((nch ? nch : 1) + 1) * 8 + 16);
     DeviceBuffer out((std::uint64_t)(steps + 1) * 8 * 8);
     MB_CUDA(cudaMemsetAsync(r.flag.ptr, 0, 16, h.s));
     MB_CUDA(cudaMemsetAsync(r.wsum.ptr, 0, D * 8, h.s));
@@ -1166,6 +1169,7 @@ static int run_sgd(
       // averaging pass only the representatives' partials are computed
       auto dispersion_fast_any = [&](double* dst) {
         const std::uint64_t ch = nch ? nch : 1;
+        double* rowsum = r.dpart.as<double>() + n_max * ch;  // the spare column
         if (rep_map) {
           const unsigned gy = (unsigned)std::min<std::uint64_t>(
               n, std::max<std::uint64_t>(1, 2 * 2368 / ch));
@@ -1177,7 +1181,9 @@ static int run_sgd(
             dispersion_fast_list<double><<<dim3((unsigned)ch, gy), kRed, 0, h.s>>>(
                 x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>(),
                 r.rlist.as<std::uint32_t>(), r.rcount.as<std::uint32_t>());
-          fold_all_rep<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n, ch, rep_map, (double)n, dst);
+          row_sums<<<(unsigned)((n + 255) / 256), 256, 0, h.s>>>(r.dpart.as<double>(), n, ch,
+                                                                  rep_map, rowsum);
+          fold_all<<<1, 1, 0, h.s>>>(rowsum, n, (double)n, dst);
           return;
         }
         if (dtype == MOSHPIT_F32)
@@ -1186,7 +1192,9 @@ static int run_sgd(
         else
           dispersion_fast<double><<<dim3((unsigned)ch, (unsigned)n), kRed, 0, h.s>>>(
               x.as<double>(), r.ld, dim, r.mean.as<double>(), ch, r.dpart.as<double>());
-        fold_all<<<1, 1, 0, h.s>>>(r.dpart.as<double>(), n * ch, (double)n, dst);
+        row_sums<<<(unsigned)((n + 255) / 256), 256, 0, h.s>>>(r.dpart.as<double>(), n, ch,
+                                                                nullptr, rowsum);
+        fold_all<<<1, 1, 0, h.s>>>(rowsum, n, (double)n, dst);
       };
       w_k *= w_growth;
       weight_total += w_k;
