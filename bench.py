@@ -52,6 +52,7 @@ CONFIGS = {
     "C3": (16, 3, 4096, 25_600_000, 0.0, 3),
 }
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_ALL_ACTIVE_GBS = 665.0  # every GPU pulling from its peers at once (profiles/r01/p2p_probe.txt)
 PROTOCOL_SEED = 7
 INIT_SEED = 0x5EED
 
@@ -746,6 +747,11 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
             "combined_frac": round((trl + trc) / t_max, 4) if t_max else None,
             "combined_frac_overlapped_bound": round(
                 max(trl + hbm_cross_ms, nvl_max / (NVLINK_GBS * 1e9) * 1e3) / t_max, 4)
+            if t_max else None,
+            # the same against the all-GPUs-active peer-read figure (every GPU
+            # pulling from its peers at once: 663-667 GB/s, profiles/r01/p2p_probe.txt)
+            "combined_frac_overlapped_bound_all_active": round(
+                max(trl + hbm_cross_ms, nvl_max / (NVLINK_ALL_ACTIVE_GBS * 1e9) * 1e3) / t_max, 4)
             if t_max else None,
             "note": "t_roof = max(HBM bytes / hbm_gbs, NVLink ingress / 770 GB/s) per round, "
                     "busiest GPU, minimal bytes (raw remote member chunks + one copy of each "
