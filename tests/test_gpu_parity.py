@@ -125,7 +125,8 @@ def test_run_moshpit_f64_bit_exact_vs_golden(mb, oracle, golden):
 @pytest.mark.parametrize("M,d,n,p,R,dim", [(3, 2, 9, 0.0, 4, 2), (5, 2, 24, 0.1, 10, 3),
                                            (4, 3, 50, 0.2, 8, 5), (8, 1, 8, 0.3, 3, 4),
                                            (7, 2, 40, 0.5, 6, 3), (2, 5, 32, 0.1, 9, 2),
-                                           (40, 2, 1600, 0.01, 3, 7), (33, 2, 1000, 0.0, 2, 5)])
+                                           (40, 2, 1600, 0.01, 3, 7), (33, 2, 1000, 0.0, 2, 5),
+                                           (16, 2, 256, 0.05, 3, 70001)])
 def test_run_moshpit_f64_equals_reference(mb, ref, M, d, n, p, R, dim):
     x = np.random.default_rng(n * 31 + d).random((n, dim))
     rr, fr = ref.run_moshpit(M, d, x, p, 1000 + n, R)
@@ -187,7 +188,10 @@ def test_all_failed_round_leaves_state(mb):
                                            # column means over the representative map:
                                            # distinct rows within / past the staged budget
                                            (32, 2, 1024, 0.01, 4, 68), (32, 2, 1024, 0.2, 3, 36),
-                                           (8, 2, 64, 0.05, 5, 20)])
+                                           (8, 2, 64, 0.05, 5, 20),
+                                           # wide rows: the EXACT drift chain runs in column
+                                           # segments beside the means
+                                           (16, 2, 256, 0.05, 3, 70001), (8, 2, 64, 0.0, 2, 131072)])
 def test_run_moshpit_f32_bit_exact_vs_oracle(mb, oracle, M, d, n, p, R, dim):
     x = oracle.init_state(INIT_SEED, n, dim, dtype=np.float32)
     ro, fo = oracle.run_moshpit(M, d, x, p, 7, R)
