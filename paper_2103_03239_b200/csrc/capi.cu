@@ -67,6 +67,21 @@ void to_state(const Xoshiro& r, moshpit_rng_state* st) {
 
 using namespace mb200;
 
+namespace {
+// record_round's second stream (column means -> drift, the critical path
+// beside the distortion) at the device's highest stream priority: its CTAs
+// go first when both kernels have CTAs pending (C2 round + FAST record 7.08-
+// 7.18 -> 6.99 ms; profiles/r02/gpu_prio.sh).  MOSHPIT_DIAG_AUX_PRIORITY=0:
+// default priority.
+inline int aux_priority() {
+  const char* e = std::getenv("MOSHPIT_DIAG_AUX_PRIORITY");
+  if (e && std::atoi(e) == 0) return 0;
+  int lo = 0, hi = 0;
+  MB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  return hi;
+}
+}  // namespace
+
 struct moshpit_engine {
   std::unique_ptr<Plane> plane;
   Xoshiro fail, clock;
@@ -437,7 +452,7 @@ int moshpit_run_moshpit(int dtype, std::uint32_t M, std::uint32_t d, std::uint32
                                                 static_cast<std::uint32_t>(dim));
       return;
     }
-    StreamHolder st, aux;
+    StreamHolder st, aux(aux_priority());
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     MB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     MB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
@@ -943,7 +958,7 @@ int moshpit_engine_set_reference(moshpit_engine* e, int dtype, const void* state
     e->log_n = 0;
     if (diag == MOSHPIT_DIAG_NONE) return;
     if (!e->aux) {
-      e->aux = std::make_unique<StreamHolder>();
+      e->aux = std::make_unique<StreamHolder>(aux_priority());
       MB_CUDA(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
       MB_CUDA(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
     }

@@ -60,6 +60,10 @@ inline std::uint64_t padded_ld(std::uint64_t dim, std::size_t elem) {
 struct StreamHolder {
   cudaStream_t s = nullptr;
   StreamHolder() { MB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  // priority: lower numbers are higher priority (cudaDeviceGetStreamPriorityRange)
+  explicit StreamHolder(int priority) {
+    MB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
+  }
   ~StreamHolder() {
     if (s) cudaStreamDestroy(s);
   }
