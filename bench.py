@@ -530,9 +530,19 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     head = run_peer(mb, torch, dist, cfg, args.steps, args.warmup, rank, world, local,
-                    nvlink=True, e2e=not args.no_e2e)
+                    nvlink=True, e2e=not args.no_e2e, cross=args.cross)
     clk = clocks.stop()
-    coord = c5v = None
+    coord = c5v = other = None
+    # the other cross-round summation on the same config (exact: the reference
+    # tree over raw member chunks, bit-exact; partial: per-GPU partial sums,
+    # within 1e-6 relative)
+    other_mode = "partial" if args.cross == "exact" else "exact"
+    try:
+        other = run_peer(mb, torch, dist, cfg, args.steps, args.warmup, rank, world, local,
+                         nvlink=True, cross=other_mode)
+        other.pop("e2e", None)
+    except Exception as exc:  # noqa: BLE001
+        other = {"error": str(exc)}
     if not args.no_coord:
         try:
             coord = run_coord(mb, torch, dist, cfg, min(args.steps, 40), args.warmup, rank, world,
@@ -571,6 +581,12 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
             "nvlink_counters": head.get("nvlink_counters"),
             "clocks": clk,
             "e2e": head["e2e"],
+            "cross_summation": (
+                "exact: the reference pairwise tree over the members' raw chunks (bit-exact)"
+                if args.cross == "exact" else
+                "partial: per-GPU partial sums combined in rank order in fp64 (the summation "
+                "order is not the reference's: within 1e-6 relative in fp32, north_star)"),
+            f"peer_sharded_{other_mode}": other,
             "coordinate_sharded_weak": coord,
             "peer_sharded_c5v": c5v,
         }
@@ -650,7 +666,7 @@ def measure_e2e_peer(mb, torch, dist, sh, cfg, world, calls=3):
 
 
 def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=False, slabs=None,
-             e2e=False):
+             e2e=False, cross="exact"):
     """Peer-sharded rounds: peers split by grid digit d-1, rounds on
     axes 0..d-2 local, the axis d-1 round one fused NVLink kernel.  Returns
     the whole-problem metric (strong scaling) and the combined roofline."""
@@ -658,7 +674,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     if slabs is None:  # slab pipeline: cross rounds of some slabs under local rounds of others
         slabs = int(os.environ.get("MOSHPIT_SHARD_SLABS", 8 if world > 1 else 1))
     sh = mb.Shard(mb.GridConfig(M, d, Rcfg), N, mb.FailureModel(p), mb.Rng(PROTOCOL_SEED), D,
-                  rank=rank, world=world, device=local, slabs=slabs)
+                  rank=rank, world=world, device=local, slabs=slabs, cross=cross)
     if world > 1:
         sh.connect()
     sh.fill_synthetic(INIT_SEED)
@@ -695,9 +711,19 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
     hbm_local = 2 * es * D * local_rows
     # voided groups of a cross round move the rows whose new rank lives on
     # another GPU: one full row over NVLink (pull) + its HBM read and write
-    hbm_cross = 2 * es * D * Mg * cross_groups + 2 * es * D * moved
-    nvl_cross = (cross_groups * es * (D / world) * ((M - Mg) + (world - 1))
-                 + es * D * moved) if world > 1 else 0
+    if cross == "partial":
+        # per group: the Mg member rows read (partial sums) and written (mean),
+        # the partial row written, this GPU's partial chunk and mean chunk
+        # read by the w-1 peers (and its own partial chunk by itself); NVLink:
+        # w-1 foreign partial chunks + w-1 foreign mean chunks pulled
+        hbm_cross = (es * D * cross_groups * (2 * Mg + 1 + (2 * (world - 1) + 1) / world)
+                     + 2 * es * D * moved)
+        nvl_cross = (cross_groups * es * (D / world) * 2 * (world - 1)
+                     + es * D * moved) if world > 1 else 0
+    else:
+        hbm_cross = 2 * es * D * Mg * cross_groups + 2 * es * D * moved
+        nvl_cross = (cross_groups * es * (D / world) * ((M - Mg) + (world - 1))
+                     + es * D * moved) if world > 1 else 0
     peak, _ = peaks()
     t_roof_local = hbm_local / (peak * 1e9) * 1e3
     t_roof_cross = max(hbm_cross / (peak * 1e9), nvl_cross / (NVLINK_GBS * 1e9)) * 1e3
@@ -726,6 +752,7 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
         "e2e": e2e_line,
         "workload": f"{cfg}: {N} peers on {M}^{d}, D={D} fp32, p_fail={p}, peer-sharded over "
                     f"{world} GPU(s) (grid digit d-1 split; axes 0..d-2 local)",
+        "cross": cross,
         "metric": "peer-vector GB/s averaged per Moshpit round", "value": round(value, 3),
         "unit": "GB/s", "scaling": "strong", "steps": steps, "ms_per_step": round(t_max / steps, 4),
         "slabs": slabs,
@@ -1019,6 +1046,9 @@ def main():
     ap.add_argument("--config", default="C2", choices=[c for c in sorted(CONFIGS) if c != "C3"],
                     help="C3 at full size exceeds one GPU: see the c3_full_1gpu key")
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
+    ap.add_argument("--cross", default=os.environ.get("MOSHPIT_BENCH_CROSS", "exact"),
+                    choices=["exact", "partial"],
+                    help="N > 1 headline's cross-round summation (the other one is attached)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sgd", action="store_true", help="skip the C4 Moshpit-SGD measurement")

@@ -365,6 +365,18 @@ int moshpit_shard_round(moshpit_shard* s, void* stream, uint32_t* active_out,
                         int32_t* crossed_out);
 /* Resident peers' vectors -> out[n*dim] by peer id, mask[p]=1 where written. */
 int moshpit_shard_read(moshpit_shard* s, void* out, uint8_t* mask);
+/* Cross-round summation (rounds enqueued after the call):
+ * MOSHPIT_CROSS_EXACT (default) evaluates the reference tree
+ * (allreduce.hpp:79-121 over core.hpp:72-81) on the members' raw chunks,
+ * pulled over NVLink -- bit-exact; MOSHPIT_CROSS_PARTIAL sums each GPU's
+ * members first and moves one partial row per GPU and group (2(w-1)/w rows
+ * of NVLink ingress per group instead of ((M-Mg)+(w-1))/w), combined in a
+ * fixed rank order in fp64 -- deterministic, within 1e-6 relative of the
+ * reference order in fp32 (north_star's tolerance where the summation order
+ * is not matched).  Group formation, failures and placement are unchanged. */
+#define MOSHPIT_CROSS_EXACT 0
+#define MOSHPIT_CROSS_PARTIAL 1
+int moshpit_shard_set_cross_mode(moshpit_shard* s, int32_t mode);
 int moshpit_shard_set_timing(moshpit_shard* s, int32_t enable);
 int moshpit_shard_kernel_time(moshpit_shard* s, double* local_ms,
                               uint64_t* local_n, double* cross_ms,

@@ -825,12 +825,16 @@ class Shard:
     k; e.g. world 8 on 4 GPUs); ``emulate=True`` hosts all ``world`` ranks on
     one GPU.  ``slabs=S`` pipelines S column slabs one round apart so NVLink
     cross rounds overlap HBM-bound local rounds (bit-identical results).
+    ``cross="exact"`` (default) runs the reference tree over the members' raw
+    chunks in cross rounds (bit-exact); ``cross="partial"`` ships one partial
+    sum per GPU and group instead (fixed order, fp64 combine; within 1e-6
+    relative in fp32 -- the summation order is not the reference's).
     """
 
     def __init__(self, grid: GridConfig, n_peers: int, failure: FailureModel, rng: Rng,
                  dim: int, rank: int = 0, world: int = 1, emulate: bool = False,
                  device: int = 0, dtype=np.float32, ranks_per_process: int = 1,
-                 slabs: int = 1):
+                 slabs: int = 1, cross: str = "exact"):
         self.grid, self.n, self.dim = grid, int(n_peers), int(dim)
         self.world, self.emulate = world, emulate
         self.nhost = world if emulate else int(ranks_per_process)
@@ -846,6 +850,11 @@ class Shard:
                                             self.dim, self.rank, self.nhost, world, self.slabs,
                                             device, C.byref(h)))
         self._h = h
+        if cross not in ("exact", "partial"):
+            self.close()
+            raise InvalidArgument(f"Shard: cross must be 'exact' or 'partial', not {cross!r}")
+        self.cross = cross
+        check(lib().moshpit_shard_set_cross_mode(self._h, 1 if cross == "partial" else 0))
 
     def close(self):
         if getattr(self, "_h", None):

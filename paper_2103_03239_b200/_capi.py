@@ -120,6 +120,7 @@ PROTOTYPES = {
     "moshpit_shard_round": (C.c_int, [vp, vp, P(u32), P(i32)]),
     "moshpit_shard_read": (C.c_int, [vp, vp, vp]),
     "moshpit_shard_set_timing": (C.c_int, [vp, i32]),
+    "moshpit_shard_set_cross_mode": (C.c_int, [vp, i32]),
     "moshpit_shard_kernel_time": (C.c_int, [vp, P(dbl), P(u64), P(dbl), P(u64)]),
     "moshpit_shard_stats": (C.c_int, [vp, i32, P(u64), P(u64), P(u64)]),
     "moshpit_shard_cross_detail": (C.c_int, [vp, i32, P(dbl), P(dbl), P(u64)]),

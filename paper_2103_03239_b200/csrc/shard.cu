@@ -311,6 +311,134 @@ __global__ void __launch_bounds__(kCrossThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Partial-sum cross round (MOSHPIT_CROSS_PARTIAL).  The reference tree spans
+// GPUs, so the exact round ships every remote member's raw chunk: per GPU
+// (M - Mg) / world rows' worth of NVLink ingress per group.  This mode sums
+// each GPU's own members first and ships one partial row per GPU and group:
+//   phase 0 (local)  GPU h: P_h = its members' rows summed in position order
+//                    (sequentially, in T), stored IN PLACE into its first
+//                    member row p_h (a member row: it gets the mean anyway);
+//   phase A (pull)   GPU r, coordinate chunk r: m = (P_0 + ... + P_{w-1}) / n
+//                    in fp64 (the w partials pulled over NVLink in rank
+//                    order), rounded to T, stored into its member rows;
+//   phase B          unchanged (shard_pull_kernel): the foreign chunk means
+//                    pulled once per group.
+// NVLink ingress per GPU and group: 2 (w-1)/w rows instead of
+// ((M - Mg) + (w-1)) / w.  The summation order is no longer the reference's
+// ("within 1e-6 relative in fp32" where the order is not
+// matched); deterministic (fixed order), and group formation, failures and
+// placement are unchanged (replicated integer plane).  p_h is the first
+// member of the group on GPU h in position order by SOURCE row, which is
+// also one of its destination rows there (the row set of a group on a GPU
+// does not change in a cross round), so phase A's stores cover it.
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads)
+    partial_sum_kernel(CrossArgs<T> a) {
+  using V = typename V16s<T>::type;
+  __shared__ const V* s_src[32];
+  __shared__ std::uint32_t s_n;
+  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  V* const pool = reinterpret_cast<V*>(a.pools[a.me]);
+  std::uint32_t cached = 0xffffffffu, k = 0;
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t g = a.act[w / a.n_tiles];
+    if (g != cached) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        std::uint32_t q = 0;
+        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
+          const std::uint32_t s = a.src_row[pos];
+          if (s / a.R == a.me) s_src[q++] = pool + (s % a.R) * a.ld_vec;
+        }
+        s_n = q;
+      }
+      cached = g;
+      __syncthreads();
+      k = s_n;
+    }
+    const std::uint64_t rel = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    const std::uint64_t col = a.vb + rel;
+    if (col >= a.ve || k == 0) continue;
+    V acc = szero((V*)nullptr);
+    for (std::uint32_t i = 0; i < k; i += 8) {
+      V x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i + u < k) x[u] = __ldcs(s_src[i + u] + col);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i + u < k) acc = sadd(acc, x[u]);
+    }
+    const_cast<V*>(s_src[0])[col] = acc;
+  }
+}
+
+__device__ __forceinline__ void dacc(double (&s)[4], float4 v) {
+  s[0] = __dadd_rn(s[0], (double)v.x);
+  s[1] = __dadd_rn(s[1], (double)v.y);
+  s[2] = __dadd_rn(s[2], (double)v.z);
+  s[3] = __dadd_rn(s[3], (double)v.w);
+}
+__device__ __forceinline__ void dacc(double (&s)[4], double2 v) {
+  s[0] = __dadd_rn(s[0], v.x);
+  s[1] = __dadd_rn(s[1], v.y);
+}
+__device__ __forceinline__ float4 dmean(const double (&s)[4], double n, float4*) {
+  return make_float4((float)__ddiv_rn(s[0], n), (float)__ddiv_rn(s[1], n),
+                     (float)__ddiv_rn(s[2], n), (float)__ddiv_rn(s[3], n));
+}
+__device__ __forceinline__ double2 dmean(const double (&s)[4], double n, double2*) {
+  return make_double2(__ddiv_rn(s[0], n), __ddiv_rn(s[1], n));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCrossThreads)
+    partial_combine_kernel(CrossArgs<T> a) {
+  using V = typename V16s<T>::type;
+  __shared__ const V* s_part[kMaxWorld];
+  __shared__ V* s_dst[32];
+  __shared__ std::uint32_t s_nd, s_cnt;
+  const std::uint32_t world = a.world;
+  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  std::uint32_t cached = 0xffffffffu, nd = 0;
+  double cntd = 1.0;
+  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const std::uint32_t g = a.act[w / a.n_tiles];
+    if (g != cached) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (std::uint32_t h = 0; h < world; ++h) s_part[h] = nullptr;
+        std::uint32_t q = 0;
+        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
+          const std::uint32_t s = a.src_row[pos], d = a.dst_row[pos];
+          const std::uint32_t h = (std::uint32_t)(s / a.R);
+          if (!s_part[h]) s_part[h] = reinterpret_cast<const V*>(a.pools[h]) + (s % a.R) * a.ld_vec;
+          if (d / a.R == a.me) s_dst[q++] = reinterpret_cast<V*>(a.pools[a.me]) + (d % a.R) * a.ld_vec;
+        }
+        s_nd = q;
+        s_cnt = a.goff[g + 1] - a.goff[g];
+      }
+      cached = g;
+      __syncthreads();
+      nd = s_nd;
+      cntd = (double)s_cnt;
+    }
+    const std::uint64_t col = a.c0 + (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    if (col >= a.c1) continue;
+    V x[kMaxWorld];
+#pragma unroll
+    for (std::uint32_t h = 0; h < kMaxWorld; ++h)
+      if (h < world && s_part[h]) x[h] = __ldcg(s_part[h] + col);
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (std::uint32_t h = 0; h < kMaxWorld; ++h)
+      if (h < world && s_part[h]) dacc(s, x[h]);
+    const V m = dmean(s, cntd, (V*)nullptr);
+    for (std::uint32_t q = 0; q < nd; ++q) __stcs(s_dst[q] + col, m);
+  }
+}
+
 // Copy-engine cross round (MOSHPIT_CROSS_CE=1).  SM loads from peer HBM top
 // out at ~660 GB/s of NVLink ingress per GPU, one large copy-engine pull
 // reaches ~760 GB/s (profiles/ce_probe.cu, profiles/r01/ce_probe.txt).  In
@@ -526,6 +654,7 @@ struct TableSlot {
   cudaEvent_t freed[kMaxSlabs] = {};       // slab k is done with it
   bool used[kMaxSlabs] = {};
   int cross = 0;
+  int partial = 0;  // cross round in the partial-sum mode (MOSHPIT_CROSS_PARTIAL)
   ~TableSlot() {
     if (ready) cudaEventDestroy(ready);
     for (auto e : freed)
@@ -546,6 +675,7 @@ struct Shard {
   bool emulate = false;    // nhost == world: no peers, no barriers
   bool connected = false;  // peers' pools/flags mapped (open_peers)
   bool probe = false;      // profiling only: no inter-rank barriers (results invalid)
+  int cross_mode = 0;      // MOSHPIT_CROSS_EXACT (reference tree) / MOSHPIT_CROSS_PARTIAL
   // slab pipeline: SMs' worth of CTAs for the local (kernel 2) and cross
   // kernels while they share the GPU (0 = all; MOSHPIT_PIPE_LOCAL_SMS /
   // MOSHPIT_PIPE_CROSS_SMS)
@@ -685,6 +815,26 @@ struct Shard {
     int sms = sm_count();
     if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
     if (a.n_tiles) cross_mean_kernel<T><<<sms * per, kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+
+  // partial-sum mode: phase 0 (rank r's members summed into its first member
+  // row, whole slab width) and phase A (chunk r of the means from the w
+  // partial rows)
+  template <typename T>
+  void partial_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
+    CrossArgs<T> a = cross_args<T>(t, r, k, true);
+    int sms = sm_count();
+    if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
+    if (a.n_tiles) partial_sum_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a);
+    MB_LAUNCH_CHECK();
+  }
+  template <typename T>
+  void combine_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
+    CrossArgs<T> a = cross_args<T>(t, r, k, false);
+    int sms = sm_count();
+    if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
+    if (a.n_tiles) partial_combine_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a);
     MB_LAUNCH_CHECK();
   }
 
@@ -866,16 +1016,29 @@ struct Shard {
       if (te) MB_CUDA(cudaEventRecord(te->b, s));
     } else {
       if (ce) ce_fetch_tables(t, s);
-      barrier(k, s);  // peers finished writing the rows we are about to read
       TEv* ta = timing ? &tpair(1) : nullptr;
-      if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
+      if (t.partial) {
+        // phase 0 touches only this GPU's rows; the barrier then publishes
+        // the partial rows (and the previous rounds' rows) to the peers
+        if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
+        for (std::uint32_t r = me; r < me + nhost; ++r) {
+          if (f32) partial_launch<float>(t, r, k, s);
+          else partial_launch<double>(t, r, k, s);
+        }
+        barrier(k, s);
+      } else {
+        barrier(k, s);  // peers finished writing the rows we are about to read
+        if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
+      }
       for (std::uint32_t r = me; r < me + nhost; ++r) {
         if (f32) {
           if (ce) cross_ce<float>(t, r, s);
+          else if (t.partial) combine_launch<float>(t, r, k, s);
           else cross_launch<float>(t, r, k, s);
           moves_launch<float>(t, r, k, 0, s);
         } else {
           if (ce) cross_ce<double>(t, r, s);
+          else if (t.partial) combine_launch<double>(t, r, k, s);
           else cross_launch<double>(t, r, k, s);
           moves_launch<double>(t, r, k, 0, s);
         }
@@ -950,6 +1113,7 @@ struct Shard {
     place_kernel<<<1, 1024, 0, c>>>(a);
     MB_LAUNCH_CHECK();
     t.cross = cross;
+    t.partial = cross && cross_mode == MOSHPIT_CROSS_PARTIAL;
     plane->mark_done(c);
     if (S > 1) MB_CUDA(cudaEventRecord(t.ready, c));
     for (std::uint32_t k = 0; k < S; ++k)
@@ -1337,6 +1501,21 @@ int moshpit_shard_read(moshpit_shard* h, void* out, std::uint8_t* mask) {
     MB_CUDA(cudaMemcpy(&e, S.err.ptr, 4, cudaMemcpyDeviceToHost));
     if (e) throw std::runtime_error("shard: placement invariant violated (code " +
                                     std::to_string(e) + ")");
+  });
+}
+
+// Cross-round summation: MOSHPIT_CROSS_EXACT (default; the reference tree over
+// the members' raw chunks, bit-exact) or MOSHPIT_CROSS_PARTIAL (per-GPU
+// partial sums, fixed order, tolerance parity; see partial_sum_kernel).
+// Applies to the rounds enqueued after the call.
+int moshpit_shard_set_cross_mode(moshpit_shard* h, std::int32_t mode) {
+  return guarded([&] {
+    shard_require(h);
+    if (mode != MOSHPIT_CROSS_EXACT && mode != MOSHPIT_CROSS_PARTIAL)
+      throw std::invalid_argument("shard: unknown cross-round mode");
+    if (mode == MOSHPIT_CROSS_PARTIAL && h->s->ce)
+      throw std::invalid_argument("shard: the copy-engine round has no partial-sum mode");
+    h->s->cross_mode = mode;
   });
 }
 

@@ -2,7 +2,8 @@
 Each process hosts RANKS_PER_PROC consecutive ranks (default 1; world =
 P * RANKS_PER_PROC, e.g. world 8 on 4 GPUs with 2), with SLABS pipelined
 column slabs (default 1).  Every process checks its resident peers' final
-vectors bit-for-bit against the CPU oracle; exits non-zero on mismatch."""
+vectors bit-for-bit against the CPU oracle (CROSS=partial: the partial-sum
+cross round, within 1e-6 relative); exits non-zero on mismatch."""
 import os
 import sys
 
@@ -22,6 +23,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", prank))
     per = int(os.environ.get("RANKS_PER_PROC", "1"))
     slabs = int(os.environ.get("SLABS", "1"))
+    cross = os.environ.get("CROSS", "exact")
     world = procs * per
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
@@ -35,7 +37,7 @@ def main():
         n = M ** d
         sh = mb.Shard(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), dim,
                       rank=prank * per, world=world, device=local, ranks_per_process=per,
-                      slabs=slabs)
+                      slabs=slabs, cross=cross)
         sh.connect()
         sh.fill_synthetic(0x5EED)
         for _ in range(R):
@@ -45,12 +47,17 @@ def main():
         got, mask = sh.read()
         init = o.init_state(0x5EED, n, dim, dtype=np.float32)
         _, want = o.run_moshpit(M, d, init, p, 7, R)
-        good = got[mask].tobytes() == want[mask].tobytes()
+        if cross == "partial":
+            g, w = got[mask].astype(np.float64), want[mask].astype(np.float64)
+            good = bool((np.abs(g - w) <= 1e-6 * np.abs(w)).all())
+        else:
+            good = got[mask].tobytes() == want[mask].tobytes()
         cnt = torch.tensor([int(mask.sum()), int(good)])
         dist.all_reduce(cnt)
         if prank == 0:
             print(f"M={M} d={d} p={p} R={R} dim={dim} world={world} ({procs} processes x {per} "
-                  f"ranks, slabs={slabs}): resident rows {int(cnt[0])}/{n}, processes bit-exact "
+                  f"ranks, slabs={slabs}, cross={cross}): resident rows {int(cnt[0])}/{n}, "
+                  f"processes {'bit-exact' if cross == 'exact' else 'within 1e-6'} "
                   f"{int(cnt[1])}/{procs}", flush=True)
         ok = ok and int(cnt[0]) == n and int(cnt[1]) == procs
         dist.barrier()
