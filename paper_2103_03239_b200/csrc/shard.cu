@@ -270,44 +270,115 @@ __global__ void __launch_bounds__(kCrossThreads, 3) cross_mean_kernel(CrossArgs<
 // group (in group order) -- a remote READ -- and write it into this GPU's
 // member rows of the group (local writes).  Every GPU derives the same rows
 // from the replicated tables, so no metadata travels.
+// Voided groups' row moves riding in the cross-round launches as extra work
+// items (interleaved 1:1 with the group items while both last): phase 0
+// pulls the rows that leave their GPU into staging (partial_sum_kernel),
+// phase 1 writes them into their new rows (shard_pull_kernel).
+struct MoveItems {
+  const std::uint32_t* moves = nullptr;    // [world][R][2] (src, dst) by dst GPU
+  const std::uint32_t* n_moves = nullptr;  // [world]
+  void* staging = nullptr;                 // this rank's staging block
+};
+
+// Item w of a launch with n_grp group items and n_mov move items.
+__device__ __forceinline__ bool pick_item(std::uint64_t w, std::uint64_t n_grp,
+                                          std::uint64_t n_mov, std::uint64_t& i) {
+  const std::uint64_t n_both = 2 * (n_grp < n_mov ? n_grp : n_mov);
+  if (w < n_both) {
+    i = w >> 1;
+    return w & 1;
+  }
+  i = w - n_both / 2;
+  return n_mov > n_grp;
+}
+
+constexpr int kPullU = 2;  // 16-byte vectors per thread and item (loads in flight)
+
+// Phase B of the cross round (after a barrier): for every active group, pull
+// each foreign coordinate chunk c once from GPU c's first member row of the
+// group (in group order) -- a remote READ -- and write it into this GPU's
+// member rows of the group (local writes).  Every GPU derives the same rows
+// from the replicated tables, so no metadata travels.  With `mv`, the
+// voided rows staged in phase 0 are written to their new rows in the same
+// launch.
 template <typename T>
 __global__ void __launch_bounds__(kCrossThreads)
-    shard_pull_kernel(CrossArgs<T> a) {
+    shard_pull_kernel(CrossArgs<T> a, MoveItems mv) {
   using V = typename V16s<T>::type;
   __shared__ V* s_rows[32];
   __shared__ const V* s_rep[kMaxWorld];
   __shared__ std::uint32_t s_n;
   const std::uint32_t world = a.world;
-  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  const std::uint64_t W = a.ve - a.vb;
+  constexpr std::uint64_t kSpan = (std::uint64_t)kPullU * kCrossThreads;
+  const std::uint64_t tiles = (W + kSpan - 1) / kSpan;
+  const std::uint64_t n_grp = (std::uint64_t)a.cnt[1] * tiles;
+  const std::uint64_t n_mov = mv.moves ? (std::uint64_t)mv.n_moves[a.me] * tiles : 0;
   std::uint32_t cached = 0xffffffffu;
-  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const std::uint32_t g = a.act[w / a.n_tiles];
+  // contiguous runs of items per CTA: the group (and its member table) stays
+  // the same for many consecutive items
+  const std::uint64_t run = (n_grp + n_mov + gridDim.x - 1) / gridDim.x;
+  const std::uint64_t w_end = min((std::uint64_t)(blockIdx.x + 1) * run, n_grp + n_mov);
+  for (std::uint64_t w = blockIdx.x * run; w < w_end; ++w) {
+    std::uint64_t i;
+    if (pick_item(w, n_grp, n_mov, i)) {
+      const std::uint64_t mk = i / tiles;
+      const std::uint32_t dst = mv.moves[((std::uint64_t)a.me * a.R + mk) * 2 + 1];
+      V* to = reinterpret_cast<V*>(a.pools[dst / a.R]) + (dst % a.R) * a.ld_vec;
+      const V* from = reinterpret_cast<const V*>(mv.staging) + mk * a.ld_vec;
+      V v[kPullU];
+#pragma unroll
+      for (int u = 0; u < kPullU; ++u) {
+        const std::uint64_t rel = (i % tiles) * kSpan + u * kCrossThreads + threadIdx.x;
+        if (rel < W) v[u] = __ldcs(from + a.vb + rel);
+      }
+#pragma unroll
+      for (int u = 0; u < kPullU; ++u) {
+        const std::uint64_t rel = (i % tiles) * kSpan + u * kCrossThreads + threadIdx.x;
+        if (rel < W) __stcs(to + a.vb + rel, v[u]);
+      }
+      continue;
+    }
+    const std::uint32_t g = a.act[i / tiles];
     if (g != cached) {
       __syncthreads();
-      if (threadIdx.x == 0) {
-        std::uint32_t k = 0;
-        for (std::uint32_t h = 0; h < world; ++h) s_rep[h] = nullptr;
-        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
-          const std::uint32_t d = a.dst_row[pos];
-          const std::uint32_t h = (std::uint32_t)(d / a.R);
-          V* row = reinterpret_cast<V*>(a.pools[h]) + (d % a.R) * a.ld_vec;
-          if (!s_rep[h]) s_rep[h] = row;
-          if (h == a.me) s_rows[k++] = row;
+      if (threadIdx.x < 32) {  // warp 0: one lane per member position
+        const std::uint32_t lane = threadIdx.x, beg = a.goff[g], n = a.goff[g + 1] - beg;
+        const std::uint32_t d = lane < n ? a.dst_row[beg + lane] : 0u;
+        const std::uint32_t h = lane < n ? (std::uint32_t)(d / a.R) : 0xffffffffu;
+        V* row = reinterpret_cast<V*>(a.pools[lane < n ? h : 0]) + (d % a.R) * a.ld_vec;
+        const unsigned mine = __ballot_sync(0xffffffffu, h == a.me);
+        if (h == a.me) s_rows[__popc(mine & ((1u << lane) - 1u))] = row;
+        for (std::uint32_t q = 0; q < world; ++q) {  // first row (position order) on GPU q
+          const unsigned on = __ballot_sync(0xffffffffu, h == q);
+          if (on && lane == (std::uint32_t)(__ffs(on) - 1)) s_rep[q] = row;
+          if (!on && lane == 0) s_rep[q] = nullptr;
         }
-        s_n = k;
+        if (lane == 0) s_n = __popc(mine);
       }
       cached = g;
       __syncthreads();
     }
-    const std::uint64_t rel = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
-    const std::uint64_t W = a.ve - a.vb, col = a.vb + rel;
-    if (rel >= W || (col >= a.c0 && col < a.c1)) continue;
-    // owner of this column: chunk c covers [vb + W*c/world, vb + W*(c+1)/world)
-    std::uint32_t c = (std::uint32_t)((rel * world) / W);
-    while (c + 1 < world && (W * (c + 1)) / world <= rel) ++c;
-    while (c > 0 && (W * c) / world > rel) --c;
-    const V v = *(s_rep[c] + col);
-    for (std::uint32_t k = 0; k < s_n; ++k) s_rows[k][col] = v;
+    V v[kPullU];
+    bool ok[kPullU];
+#pragma unroll
+    for (int u = 0; u < kPullU; ++u) {
+      const std::uint64_t rel = (i % tiles) * kSpan + u * kCrossThreads + threadIdx.x;
+      const std::uint64_t col = a.vb + rel;
+      ok[u] = rel < W && !(col >= a.c0 && col < a.c1);
+      if (!ok[u]) continue;
+      // owner of this column: chunk c covers [vb + W*c/world, vb + W*(c+1)/world)
+      std::uint32_t c = (std::uint32_t)((rel * world) / W);
+      while (c + 1 < world && (W * (c + 1)) / world <= rel) ++c;
+      while (c > 0 && (W * c) / world > rel) --c;
+      v[u] = *(s_rep[c] + col);
+    }
+    const std::uint32_t n = s_n;
+    for (std::uint32_t k = 0; k < n; ++k) {
+#pragma unroll
+      for (int u = 0; u < kPullU; ++u)
+        if (ok[u]) s_rows[k][a.vb + (i % tiles) * kSpan + u * kCrossThreads + threadIdx.x] = v[u];
+    }
   }
 }
 
@@ -332,32 +403,53 @@ __global__ void __launch_bounds__(kCrossThreads)
 // member of the group on GPU h in position order by SOURCE row, which is
 // also one of its destination rows there (the row set of a group on a GPU
 // does not change in a cross round), so phase A's stores cover it.
+//
+// The voided groups' row moves (phase 0: remote rows pulled into staging,
+// NVLink-bound) ride in the same launch as extra work items (MoveItems), so
+// the partial sums (HBM-bound) and the pulls overlap instead of adding up;
+// both need the peers' rows final, hence the barrier before this launch.
+
 template <typename T>
 __global__ void __launch_bounds__(kCrossThreads)
-    partial_sum_kernel(CrossArgs<T> a) {
+    partial_sum_kernel(CrossArgs<T> a, MoveItems mv) {
   using V = typename V16s<T>::type;
   __shared__ const V* s_src[32];
   __shared__ std::uint32_t s_n;
-  const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  const std::uint64_t n_grp = (std::uint64_t)a.cnt[1] * a.n_tiles;
+  const std::uint64_t n_mov = mv.moves ? (std::uint64_t)mv.n_moves[a.me] * a.n_tiles : 0;
+  const std::uint64_t n_items = n_grp + n_mov;
   V* const pool = reinterpret_cast<V*>(a.pools[a.me]);
   std::uint32_t cached = 0xffffffffu, k = 0;
-  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
-    const std::uint32_t g = a.act[w / a.n_tiles];
+  const std::uint64_t run = (n_items + gridDim.x - 1) / gridDim.x;  // contiguous runs
+  const std::uint64_t w_end = min((std::uint64_t)(blockIdx.x + 1) * run, n_items);
+  for (std::uint64_t w = blockIdx.x * run; w < w_end; ++w) {
+    std::uint64_t i;
+    if (pick_item(w, n_grp, n_mov, i)) {
+      const std::uint64_t mk = i / a.n_tiles;
+      const std::uint64_t col = a.vb + (i % a.n_tiles) * kCrossThreads + threadIdx.x;
+      if (col >= a.ve) continue;
+      const std::uint32_t src = mv.moves[((std::uint64_t)a.me * a.R + mk) * 2];
+      const V* from = reinterpret_cast<const V*>(a.pools[src / a.R]) + (src % a.R) * a.ld_vec;
+      reinterpret_cast<V*>(mv.staging)[mk * a.ld_vec + col] = __ldcs(from + col);
+      continue;
+    }
+    const std::uint64_t w2 = i;
+    const std::uint32_t g = a.act[w2 / a.n_tiles];
     if (g != cached) {
       __syncthreads();
-      if (threadIdx.x == 0) {
-        std::uint32_t q = 0;
-        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
-          const std::uint32_t s = a.src_row[pos];
-          if (s / a.R == a.me) s_src[q++] = pool + (s % a.R) * a.ld_vec;
-        }
-        s_n = q;
+      if (threadIdx.x < 32) {  // warp 0: one lane per member position
+        const std::uint32_t lane = threadIdx.x, beg = a.goff[g], n = a.goff[g + 1] - beg;
+        const std::uint32_t sr = lane < n ? a.src_row[beg + lane] : 0u;
+        const bool here = lane < n && sr / a.R == a.me;
+        const unsigned mine = __ballot_sync(0xffffffffu, here);
+        if (here) s_src[__popc(mine & ((1u << lane) - 1u))] = pool + (sr % a.R) * a.ld_vec;
+        if (lane == 0) s_n = __popc(mine);
       }
       cached = g;
       __syncthreads();
       k = s_n;
     }
-    const std::uint64_t rel = (w % a.n_tiles) * kCrossThreads + threadIdx.x;
+    const std::uint64_t rel = (w2 % a.n_tiles) * kCrossThreads + threadIdx.x;
     const std::uint64_t col = a.vb + rel;
     if (col >= a.ve || k == 0) continue;
     V acc = szero((V*)nullptr);
@@ -392,7 +484,9 @@ __device__ __forceinline__ double2 dmean(const double (&s)[4], double n, double2
   return make_double2(__ddiv_rn(s[0], n), __ddiv_rn(s[1], n));
 }
 
-template <typename T>
+// NW: the world size this instance is unrolled for (its partial loads sit in
+// registers), kMaxWorld for any other world.
+template <typename T, int NW>
 __global__ void __launch_bounds__(kCrossThreads)
     partial_combine_kernel(CrossArgs<T> a) {
   using V = typename V16s<T>::type;
@@ -403,39 +497,62 @@ __global__ void __launch_bounds__(kCrossThreads)
   const std::uint64_t n_items = (std::uint64_t)a.cnt[1] * a.n_tiles;
   std::uint32_t cached = 0xffffffffu, nd = 0;
   double cntd = 1.0;
-  for (std::uint64_t w = blockIdx.x; w < n_items; w += gridDim.x) {
+  const std::uint64_t run = (n_items + gridDim.x - 1) / gridDim.x;  // contiguous runs
+  const std::uint64_t w_end = min((std::uint64_t)(blockIdx.x + 1) * run, n_items);
+  for (std::uint64_t w = blockIdx.x * run; w < w_end; ++w) {
     const std::uint32_t g = a.act[w / a.n_tiles];
     if (g != cached) {
       __syncthreads();
-      if (threadIdx.x == 0) {
-        for (std::uint32_t h = 0; h < world; ++h) s_part[h] = nullptr;
-        std::uint32_t q = 0;
-        for (std::uint32_t pos = a.goff[g]; pos < a.goff[g + 1]; ++pos) {
-          const std::uint32_t s = a.src_row[pos], d = a.dst_row[pos];
-          const std::uint32_t h = (std::uint32_t)(s / a.R);
-          if (!s_part[h]) s_part[h] = reinterpret_cast<const V*>(a.pools[h]) + (s % a.R) * a.ld_vec;
-          if (d / a.R == a.me) s_dst[q++] = reinterpret_cast<V*>(a.pools[a.me]) + (d % a.R) * a.ld_vec;
+      if (threadIdx.x < 32) {  // warp 0: one lane per member position
+        const std::uint32_t lane = threadIdx.x, beg = a.goff[g], n = a.goff[g + 1] - beg;
+        const std::uint32_t sr = lane < n ? a.src_row[beg + lane] : 0u;
+        const std::uint32_t d = lane < n ? a.dst_row[beg + lane] : 0u;
+        const std::uint32_t h = lane < n ? (std::uint32_t)(sr / a.R) : 0xffffffffu;
+        const bool here = lane < n && d / a.R == a.me;
+        const unsigned mine = __ballot_sync(0xffffffffu, here);
+        if (here)
+          s_dst[__popc(mine & ((1u << lane) - 1u))] =
+              reinterpret_cast<V*>(a.pools[a.me]) + (d % a.R) * a.ld_vec;
+        for (std::uint32_t q = 0; q < world; ++q) {  // partial row: first source row on GPU q
+          const unsigned on = __ballot_sync(0xffffffffu, h == q);
+          if (on && lane == (std::uint32_t)(__ffs(on) - 1))
+            s_part[q] = reinterpret_cast<const V*>(a.pools[q]) + (sr % a.R) * a.ld_vec;
+          if (!on && lane == 0) s_part[q] = nullptr;
         }
-        s_nd = q;
-        s_cnt = a.goff[g + 1] - a.goff[g];
+        if (lane == 0) {
+          s_nd = __popc(mine);
+          s_cnt = n;
+        }
       }
       cached = g;
       __syncthreads();
       nd = s_nd;
       cntd = (double)s_cnt;
     }
-    const std::uint64_t col = a.c0 + (w % a.n_tiles) * kCrossThreads + threadIdx.x;
-    if (col >= a.c1) continue;
-    V x[kMaxWorld];
+    // kPullU vectors per thread: the remote partial loads of both in flight
+    const std::uint64_t col0 = a.c0 + (w % a.n_tiles) * (kPullU * kCrossThreads) + threadIdx.x;
+    V x[kPullU][NW];
 #pragma unroll
-    for (std::uint32_t h = 0; h < kMaxWorld; ++h)
-      if (h < world && s_part[h]) x[h] = __ldcg(s_part[h] + col);
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int u = 0; u < kPullU; ++u) {
+      const std::uint64_t col = col0 + u * kCrossThreads;
 #pragma unroll
-    for (std::uint32_t h = 0; h < kMaxWorld; ++h)
-      if (h < world && s_part[h]) dacc(s, x[h]);
-    const V m = dmean(s, cntd, (V*)nullptr);
-    for (std::uint32_t q = 0; q < nd; ++q) __stcs(s_dst[q] + col, m);
+      for (std::uint32_t h = 0; h < (std::uint32_t)NW; ++h)
+        if (col < a.c1 && h < world && s_part[h]) x[u][h] = __ldcg(s_part[h] + col);
+    }
+    V m[kPullU];
+#pragma unroll
+    for (int u = 0; u < kPullU; ++u) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (std::uint32_t h = 0; h < (std::uint32_t)NW; ++h)
+        if (h < world && s_part[h]) dacc(s, x[u][h]);
+      m[u] = dmean(s, cntd, (V*)nullptr);
+    }
+    for (std::uint32_t q = 0; q < nd; ++q) {
+#pragma unroll
+      for (int u = 0; u < kPullU; ++u)
+        if (col0 + u * kCrossThreads < a.c1) __stcs(s_dst[q] + col0 + u * kCrossThreads, m[u]);
+    }
   }
 }
 
@@ -824,17 +941,28 @@ struct Shard {
   template <typename T>
   void partial_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
     CrossArgs<T> a = cross_args<T>(t, r, k, true);
+    MoveItems mv;
+    if (p > 0.0) {  // the voided groups' row pulls ride along (phase 0 of the moves)
+      mv.moves = t.moves.as<std::uint32_t>();
+      mv.n_moves = t.n_moves.as<std::uint32_t>();
+      mv.staging = staging->as<T>() + (hosts(r) ? (r - me) : 0) * R * ld;
+    }
     int sms = sm_count();
     if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
-    if (a.n_tiles) partial_sum_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a);
+    if (a.n_tiles) partial_sum_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a, mv);
     MB_LAUNCH_CHECK();
   }
   template <typename T>
   void combine_launch(const TableSlot& t, std::uint32_t r, std::uint32_t k, cudaStream_t s) {
     CrossArgs<T> a = cross_args<T>(t, r, k, false);
+    a.n_tiles = (a.c1 - a.c0 + kPullU * kCrossThreads - 1) / (kPullU * kCrossThreads);
     int sms = sm_count();
     if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
-    if (a.n_tiles) partial_combine_kernel<T><<<sms * 8, kCrossThreads, 0, s>>>(a);
+    if (a.n_tiles) {
+      if (world == 2) partial_combine_kernel<T, 2><<<sms * 8, kCrossThreads, 0, s>>>(a);
+      else if (world == 4) partial_combine_kernel<T, 4><<<sms * 8, kCrossThreads, 0, s>>>(a);
+      else partial_combine_kernel<T, kMaxWorld><<<sms * 8, kCrossThreads, 0, s>>>(a);
+    }
     MB_LAUNCH_CHECK();
   }
 
@@ -847,9 +975,15 @@ struct Shard {
       per = 8;
       if (const char* e = std::getenv("MOSHPIT_PULL_CTAS")) per = std::max(1, std::atoi(e));
     }
+    MoveItems mv;
+    if (p > 0.0) {  // the staged voided rows go to their new rows in the same launch
+      mv.moves = t.moves.as<std::uint32_t>();
+      mv.n_moves = t.n_moves.as<std::uint32_t>();
+      mv.staging = staging->as<T>() + (hosts(r) ? (r - me) : 0) * R * ld;
+    }
     int sms = sm_count();
     if (S > 1 && pipe_cross_sms > 0) sms = std::min(sms, pipe_cross_sms);
-    if (a.n_tiles) shard_pull_kernel<T><<<sms * per, kCrossThreads, 0, s>>>(a);
+    if (a.n_tiles) shard_pull_kernel<T><<<sms * per, kCrossThreads, 0, s>>>(a, mv);
     MB_LAUNCH_CHECK();
   }
 
@@ -1017,30 +1151,28 @@ struct Shard {
     } else {
       if (ce) ce_fetch_tables(t, s);
       TEv* ta = timing ? &tpair(1) : nullptr;
+      barrier(k, s);  // peers finished writing the rows we are about to read
+      if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
       if (t.partial) {
-        // phase 0 touches only this GPU's rows; the barrier then publishes
-        // the partial rows (and the previous rounds' rows) to the peers
-        if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
+        // phase 0: partial rows (local HBM) + the voided rows' pulls (NVLink)
+        // in one launch; the barrier then publishes the partial rows
         for (std::uint32_t r = me; r < me + nhost; ++r) {
           if (f32) partial_launch<float>(t, r, k, s);
           else partial_launch<double>(t, r, k, s);
         }
         barrier(k, s);
-      } else {
-        barrier(k, s);  // peers finished writing the rows we are about to read
-        if (ta) MB_CUDA(cudaEventRecord(ta->a, s));
       }
       for (std::uint32_t r = me; r < me + nhost; ++r) {
         if (f32) {
           if (ce) cross_ce<float>(t, r, s);
           else if (t.partial) combine_launch<float>(t, r, k, s);
           else cross_launch<float>(t, r, k, s);
-          moves_launch<float>(t, r, k, 0, s);
+          if (!t.partial) moves_launch<float>(t, r, k, 0, s);
         } else {
           if (ce) cross_ce<double>(t, r, s);
           else if (t.partial) combine_launch<double>(t, r, k, s);
           else cross_launch<double>(t, r, k, s);
-          moves_launch<double>(t, r, k, 0, s);
+          if (!t.partial) moves_launch<double>(t, r, k, 0, s);
         }
       }
       if (ta) MB_CUDA(cudaEventRecord(ta->b, s));
@@ -1049,13 +1181,19 @@ struct Shard {
       if (tb) MB_CUDA(cudaEventRecord(tb->a, s));
       for (std::uint32_t r = me; r < me + nhost; ++r) {
         if (f32) {
-          if (ce) pull_ce<float>(t, r, s);
-          else pull_launch<float>(t, r, k, s);
-          moves_launch<float>(t, r, k, 1, s);
+          if (ce) {
+            pull_ce<float>(t, r, s);
+            moves_launch<float>(t, r, k, 1, s);
+          } else {
+            pull_launch<float>(t, r, k, s);  // + the voided rows' writes
+          }
         } else {
-          if (ce) pull_ce<double>(t, r, s);
-          else pull_launch<double>(t, r, k, s);
-          moves_launch<double>(t, r, k, 1, s);
+          if (ce) {
+            pull_ce<double>(t, r, s);
+            moves_launch<double>(t, r, k, 1, s);
+          } else {
+            pull_launch<double>(t, r, k, s);
+          }
         }
       }
       if (tb) MB_CUDA(cudaEventRecord(tb->b, s));
