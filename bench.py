@@ -560,7 +560,7 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
         if Mv % world == 0 and fits.item() > 0:
             try:
                 c5v = run_peer(mb, torch, dist, "C5v", max(8, min(args.steps, 24)), 4, rank,
-                               world, local, nvlink=True)
+                               world, local, nvlink=True, cross=args.cross)
             except Exception as exc:  # noqa: BLE001
                 c5v = {"error": str(exc)}
     if rank == 0:
@@ -572,7 +572,8 @@ def run_mine_multi(args, mb, torch, dist, rank, world, local):
             "data": "synthetic (counter-based uniform [0,1) init, exact in fp32)",
             "config": workload_config(cfg),
             "parallelism": (f"peer-sharded x{world}: grid digit d-1 split across GPUs; axis-0 "
-                            f"rounds GPU-local, axis-(d-1) rounds one fused NVLink kernel"),
+                            f"rounds GPU-local, axis-(d-1) rounds over NVLink peer memory "
+                            f"({args.cross} cross-round summation)"),
             "roofline": dict(head["roofline"], bound="hbm+nvlink",
                              frac=head["roofline"]["combined_frac"], peak_hbm=peak,
                              peak_nvlink=NVLINK_GBS, peak_source=peak_src),
@@ -781,7 +782,8 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
                 max(trl + hbm_cross_ms, nvl_max / (NVLINK_ALL_ACTIVE_GBS * 1e9) * 1e3) / t_max, 4)
             if t_max else None,
             "note": "t_roof = max(HBM bytes / hbm_gbs, NVLink ingress / 770 GB/s) per round, "
-                    "busiest GPU, minimal bytes (raw remote member chunks + one copy of each "
+                    "busiest GPU, minimal bytes of the mode (exact: raw remote member chunks; "
+                    "partial: one partial chunk per foreign GPU and group; both: one copy of each "
                     "foreign mean chunk + the voided-group rows whose new rank lives on another "
                     "GPU, all NVLink traffic as pulls); combined_frac = sum of the rounds' t_roof "
                     "/ the measured wall time of all rounds (max over ranks; host draws, kernel 1, "
@@ -1046,7 +1048,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=[c for c in sorted(CONFIGS) if c != "C3"],
                     help="C3 at full size exceeds one GPU: see the c3_full_1gpu key")
     ap.add_argument("--kernel", default="auto", choices=["auto", "register", "bulk"])
-    ap.add_argument("--cross", default=os.environ.get("MOSHPIT_BENCH_CROSS", "exact"),
+    ap.add_argument("--cross", default=os.environ.get("MOSHPIT_BENCH_CROSS", "partial"),
                     choices=["exact", "partial"],
                     help="N > 1 headline's cross-round summation (the other one is attached)")
     ap.add_argument("--no-e2e", action="store_true")
