@@ -10,6 +10,7 @@ nvlrx__bytes.sum -k regex:"partial|shard_pull|move_rows|group_mean|cross_mean" \
         python profiles/partial_probe.py 4 partial
 """
 import ctypes as C
+import json
 import os
 import sys
 
@@ -36,10 +37,24 @@ for r in range(world):
         sh[r].fill_synthetic(0x5EED)
 for r in range(world):
     torch.cuda.synchronize(r)
+models = []
 with torch.cuda.device(0):
+    prev = (0, 0, 0)
     for _ in range(2 * d):
         sh[0].round()
-    torch.cuda.synchronize()
-print("probe done", world, cross, sh[0].stats(), flush=True)
+        torch.cuda.synchronize()
+        c = sh[0].stats()
+        moved = sh[0].cross_detail(0)[2]
+        if c[0] > prev[0]:  # a cross round: modelled NVLink user bytes into rank 0
+            groups, mv = c[1] - prev[1], moved - prev[2]
+            chunk = 4 * D // world
+            if cross == "partial":
+                b = groups * chunk * 2 * (world - 1) + 4 * D * mv
+            else:
+                b = groups * chunk * ((M - M // world) + (world - 1)) + 4 * D * mv
+            models.append({"active_groups": groups, "voided_rows_moved_in": mv,
+                           "modelled_nvlink_user_bytes": b})
+        prev = (c[0], c[1], moved)
+print(json.dumps({"world": world, "cross": cross, "cross_rounds": models}), flush=True)
 for x in sh:
     x.close()
