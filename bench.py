@@ -874,13 +874,22 @@ def measure_sgd_c4(mb, steps=20, sigma=1.0, diagnostics="none"):
         best = r.loop_ms if best is None else min(best, r.loop_ms)
     ms = best / steps
     alg = 2 * 2 * N * D * 4  # two averaging rounds, each one read + one write of the state
+    one = 2 * N * D * 4  # the two-round pass: one read + one write of the state per step
     peak, _ = peaks()
+    two = os.environ.get("MOSHPIT_SGD_TWO_ROUND", "1") != "0"
     return {"workload": f"C4: Moshpit SGD, 1024 peers on 32x32, Quadratic D=2^20, tau=1, "
-                        f"inner=2, sigma={sigma} (device noise), fp32, kernel 3 fused step",
+                        f"inner=2, sigma={sigma} (device noise), fp32, "
+                        + ("the step + both averaging rounds in one pass (two_round_step_kernel)"
+                           if two else "kernel 3 fused step + kernel 2"),
             "ms_per_sgd_step": round(ms, 4),
             "peer_vector_gbs": round(N * D * 4 / (ms / 1e3) / 1e9, 1),
             "algorithmic_bytes_per_step": alg,
             "hbm_frac": round(alg / (ms / 1e3) / 1e9 / peak, 4),
+            "one_pass_bytes_per_step": one,
+            "hbm_frac_one_pass": round(one / (ms / 1e3) / 1e9 / peak, 4),
+            "note": "hbm_frac: against two rounds of one read + one write each (the per-round "
+                    "algorithm); hbm_frac_one_pass: against the one-pass bytes the two-round "
+                    "kernel actually moves",
             "timing": f"CUDA events around the {steps}-step loop (best of 2), incl. host draws; "
                       f"per-step diagnostics: {diagnostics}",
             "final_sigma_hat": round(r.diagnostics.sigma_hat, 6)}

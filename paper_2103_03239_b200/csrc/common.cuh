@@ -311,6 +311,17 @@ template <typename T>
 void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
                          const FusedRound* rounds_dev, std::uint32_t R,
                          const StepPrologue<T>* step, cudaStream_t s);
+// The Moshpit-SGD averaging step with two rounds and no failures in one pass
+// (step_kernel.cu): kernel 3's step + round 1 into shared memory, round 2 from
+// there, one read and one write of the state; bit-identical to kernel 3 +
+// kernel 2.  host_rounds: the two rounds' device tables (host array);
+// g1_max >= round 1's group count, <= two_round_max_groups(); groups of <= 32.
+std::uint32_t two_round_max_groups();
+template <typename T>
+void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
+                           const FusedRound* host_rounds, std::uint32_t g1_max,
+                           std::uint32_t* grp1, std::uint32_t* src1, const StepPrologue<T>& sp,
+                           cudaStream_t s);
 // Kernel-2 grid cap for launches from the calling thread (0 = every SM).
 void set_k2_grid_sms(int sms);
 // fp32 LogisticRegression step on the tensor cores (tc_logit.cu: tcgen05

@@ -290,7 +290,8 @@ struct Plane {
 // The tables of R consecutive rounds of a Plane (kernel 1 each, no data
 // pass) copied aside for the fused-rounds kernel (fused_rounds.cu).
 struct RoundTables {
-  DeviceBuffer members, goff, act, counts, rounds;
+  DeviceBuffer members, goff, act, counts, rounds, scratch;
+  std::vector<FusedRound> host;  // the same tables' device pointers, per round
   void form(Plane& p, std::uint32_t R, Xoshiro* fail, double prob, Xoshiro& clock,
             cudaStream_t s, std::uint32_t* active_out = nullptr) {
     const std::uint64_t n = p.n;
@@ -316,6 +317,7 @@ struct RoundTables {
     // pageable source: staged before the call returns
     MB_CUDA(cudaMemcpyAsync(rounds.ptr, h.data(), R * sizeof(FusedRound),
                             cudaMemcpyHostToDevice, s));
+    host = h;
   }
   const FusedRound* dev() const { return static_cast<const FusedRound*>(rounds.ptr); }
 };

@@ -999,6 +999,18 @@ static int run_sgd(
       const char* e = std::getenv("MOSHPIT_SGD_FUSED_ROUNDS");
       return e && std::atoi(e) != 0;
     }();
+    // Two averaging rounds per sync (d = 2, C4): the step and both rounds in
+    // one pass (two_round_step_kernel, step_kernel.cu; bit-identical to kernel
+    // 3 + kernel 2, half the HBM traffic).  Needs groups of <= 32 (M <= 32)
+    // and at most two_round_max_groups() round-1 groups (<= M^(d-1) lines).
+    // MOSHPIT_SGD_TWO_ROUND=0: kernel 3 + kernel 2.
+    std::uint64_t g1_bound = 1;
+    for (std::uint32_t q = 1; q < d && g1_bound <= two_round_max_groups(); ++q) g1_bound *= M;
+    const bool two_round = [&] {
+      const char* e = std::getenv("MOSHPIT_SGD_TWO_ROUND");
+      if (e && std::atoi(e) == 0) return false;
+      return inner == 2 && M <= 32 && g1_bound <= two_round_max_groups();
+    }();
     // no per-step diagnostics: fused quadratic runs and logistic DIAG_NONE
     const bool skip_diag = fused || (logit && diag == MOSHPIT_DIAG_NONE);
     DeviceBuffer cpad, tpad;
@@ -1072,7 +1084,19 @@ static int run_sgd(
                                    philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
           sd = StepPrologue<double>{cpad.as<double>(), tpad.as<double>(), gamma, coord_std,
                                     philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
-          if (fused_rounds && inner <= fused_rounds_max(n)) {
+          if (two_round) {
+            r.tables.form(*plane, 2, nullptr, 0.0, avg, h.s);
+            r.tables.scratch.resize((std::uint64_t)n * 8 + 16);
+            auto* g1 = r.tables.scratch.as<std::uint32_t>();
+            const auto g1n = (std::uint32_t)std::min<std::uint64_t>(g1_bound, n);
+            if (dtype == MOSHPIT_F32)
+              launch_two_round_step<float>(x.as<float>(), r.ld, dim, (std::uint32_t)n,
+                                           r.tables.host.data(), g1n, g1, g1 + n, sf, h.s);
+            else
+              launch_two_round_step<double>(x.as<double>(), r.ld, dim, (std::uint32_t)n,
+                                            r.tables.host.data(), g1n, g1, g1 + n, sd, h.s);
+            plane->mark_done(h.s);
+          } else if (fused_rounds && inner <= fused_rounds_max(n)) {
             // the step and all `inner` rounds in one pass over the state
             // (temporal blocking): bit-identical to kernel 3 + kernel 2
             r.tables.form(*plane, inner, nullptr, 0.0, avg, h.s);

@@ -24,6 +24,9 @@
 // the joins are the reference's; the step matches sgd_step_kernel (sgd.cu)
 // and the Philox noise per (step, peer, coordinate quad) is the same function,
 // so this kernel, the register form and step-then-average are bit-identical.
+#include <algorithm>
+#include <stdexcept>
+
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -327,6 +330,185 @@ void launch_leaf(const LArgs<T>& a, cudaStream_t s) {
   group_mean_step_leaf<T, NOISY><<<leaf_grid<T, NOISY>(), kLThreads, 0, s>>>(a);
 }
 
+// ---------------------------------------------------------------------------
+// Two-round pass for the Moshpit-SGD averaging step (moshpit_average with two
+// rounds and no failures, optimizer.hpp:249-284; C4): the local step, round
+// 1 and round 2 in ONE read and ONE write of the state.  Coordinates are
+// independent and a thread owns one 16-byte column vector of a tile, so it
+// can finish both rounds for its column before storing anything:
+//   round 1  every group g1 (kernel 3's leaf-streamed tree with the step and
+//            the Philox normals): its mean m1[g1] goes to shared memory
+//            (this thread's column slot), nothing is written to HBM;
+//   round 2  every group g2: the reference tree over its members' values,
+//            member k's value being m1[group of k in round 1] (without
+//            failures every peer was in an averaged round-1 group, so its
+//            row would hold exactly that mean), then the mean is stored to
+//            every member row.
+// Bit-identical to kernel 3 + kernel 2 (same step, same noise per (step,
+// peer, quad), the same trees, the same division); HBM traffic 2 * n * D *
+// sizeof(T) per SGD step instead of twice that.  Shared memory: G1 slots of
+// 16 bytes per thread (64-thread CTAs: 32 KB at G1 = 32, 7 CTAs per SM).
+constexpr int kTwoThreads = 64;
+constexpr std::uint32_t kTwoMaxG1 = 96;
+
+template <typename T>
+struct TwoArgs {
+  T* state;
+  std::uint64_t ld_vec, nvec, n_tiles;
+  const std::uint32_t* members1;
+  const std::uint32_t* goff1;
+  const std::uint32_t* counts1;
+  const std::uint32_t* members2;
+  const std::uint32_t* goff2;
+  const std::uint32_t* counts2;
+  const std::uint32_t* src1;  // [n] round-1 group of the member at round-2 position pos
+  const T* curv;
+  const T* tgt;
+  T gamma;
+  double coord_std;
+  std::uint64_t step_no, dim;
+  std::uint32_t* nonfinite;
+  double* noise_partial;
+  PhiloxKeys pk;
+};
+
+// round-2 source table: src1[pos2] = round-1 group of members2[pos2]
+__global__ void __launch_bounds__(1024) two_round_src_kernel(
+    const std::uint32_t* members1, const std::uint32_t* goff1, const std::uint32_t* counts1,
+    const std::uint32_t* members2, std::uint32_t n, std::uint32_t* grp1,
+    std::uint32_t* src1) {
+  const std::uint32_t g1n = counts1[0];
+  for (std::uint32_t g = threadIdx.x; g < g1n; g += blockDim.x)
+    for (std::uint32_t pos = goff1[g]; pos < goff1[g + 1]; ++pos) grp1[members1[pos]] = g;
+  __syncthreads();
+  for (std::uint32_t pos = threadIdx.x; pos < n; pos += blockDim.x) src1[pos] = grp1[members2[pos]];
+}
+
+template <typename T, bool NOISY>
+__global__ void __launch_bounds__(kTwoThreads, 6)
+    two_round_step_kernel(TwoArgs<T> a) {
+  using V = typename LVec<T>::V;
+  constexpr int kV = LVec<T>::kN;
+  extern __shared__ uint4 two_smem[];
+  V* const m1 = reinterpret_cast<V*>(two_smem);  // [G1][kTwoThreads]
+  const T gamma = a.gamma;
+  const T cst = (T)a.coord_std;
+  const std::uint64_t step_no = a.step_no, dim = a.dim, ld_vec = a.ld_vec;
+  const PhiloxKeys& seed = a.pk;
+  V* const base = reinterpret_cast<V*>(a.state);
+  const std::uint32_t G1 = a.counts1[0], G2 = a.counts2[0];
+  T chk = T(0);
+  double nsq = 0.0;
+  for (std::uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+    const std::uint64_t col = tile * kTwoThreads + threadIdx.x;
+    if (col >= a.nvec) continue;  // no barriers below: each thread owns its column
+    const std::uint64_t j0 = col * kV;
+    const bool full = j0 + kV <= dim;
+    const V c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
+    const V t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
+    V* const colp = base + col;
+    // round 1: the step + the tree of every group; means to shared memory
+#pragma unroll 1
+    for (std::uint32_t g = 0; g < G1; ++g) {
+      const std::uint32_t beg = __ldg(a.goff1 + g);
+      const std::uint32_t cnt = __ldg(a.goff1 + g + 1) - beg;
+      const std::uint32_t* ids = a.members1 + beg;
+      std::uint32_t b[5] = {0, 0, 0, 0, 0};
+      const std::uint32_t nl = (std::uint32_t)leaf_bounds(cnt, b);
+      const std::uint32_t b1 = b[1], b2 = b[2], b3 = b[3], b4 = b[4];
+      const std::uint32_t r = nl == 4 ? 2u : 1u;
+      V P = vz<V>(), Q = vz<V>();
+      std::uint32_t lb = 0;  // leaf l = [lb, le), in registers (no local-memory array)
+#pragma unroll 1
+      for (std::uint32_t l = 0; l < nl; ++l) {
+        const std::uint32_t le = l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4;
+        // a leaf has <= 8 members (groups of <= 32): all its loads in flight
+        // at once (the CTA count per SM is capped by the shared-memory means,
+        // so each thread needs the memory parallelism), then the step in two
+        // batches of 4 interleaved Philox chains, then the sequential sum
+        V sl = vz<V>();
+        std::uint32_t id[8];
+        V X[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) id[k] = (lb + k < le) ? __ldg(ids + lb + k) : 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          X[k] = (lb + k < le) ? colp[(std::uint64_t)id[k] * ld_vec] : vz<V>();
+#pragma unroll
+        for (int h = 0; h < 8; h += 4) {
+          if (lb + h + 4 <= le) {
+            float z[4][4] = {};
+            if constexpr (NOISY) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                philox_normals4(seed, step_no, id[h + e], j0 / 4, z[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              step_lanes<T, NOISY>(X[h + e], c, t, gamma, cst, z[e], j0, full, dim, chk, nsq);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (lb + h + e < le)
+                step_vec<T, NOISY>(X[h + e], c, t, gamma, cst, seed, step_no, id[h + e], j0,
+                                   full, dim, chk, nsq);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (lb + k < le) sl = vsum(sl, X[k]);
+        if (l < r) P = l == 0 ? sl : vsum(P, sl);
+        else Q = l == r ? sl : vsum(Q, sl);
+        lb = le;
+      }
+      const V sum = nl == 1 ? P : vsum(P, Q);
+      m1[g * kTwoThreads + threadIdx.x] = vdivn(sum, cnt);
+    }
+    // round 2: member k of group g2 holds m1[src1[pos]]
+#pragma unroll 1
+    for (std::uint32_t g = 0; g < G2; ++g) {
+      const std::uint32_t beg = __ldg(a.goff2 + g);
+      const std::uint32_t cnt = __ldg(a.goff2 + g + 1) - beg;
+      std::uint32_t b[5] = {0, 0, 0, 0, 0};
+      const std::uint32_t nl = (std::uint32_t)leaf_bounds(cnt, b);
+      const std::uint32_t b1 = b[1], b2 = b[2], b3 = b[3], b4 = b[4];
+      const std::uint32_t r = nl == 4 ? 2u : 1u;
+      V P = vz<V>(), Q = vz<V>();
+      std::uint32_t lb = 0;
+#pragma unroll 1
+      for (std::uint32_t l = 0; l < nl; ++l) {
+        const std::uint32_t le = l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4;
+        V sl = vz<V>();
+#pragma unroll 4
+        for (std::uint32_t k = lb; k < le; ++k)
+          sl = vsum(sl, m1[__ldg(a.src1 + beg + k) * kTwoThreads + threadIdx.x]);
+        if (l < r) P = l == 0 ? sl : vsum(P, sl);
+        else Q = l == r ? sl : vsum(Q, sl);
+        lb = le;
+      }
+      const V m = vdivn(nl == 1 ? P : vsum(P, Q), cnt);
+#pragma unroll 4
+      for (std::uint32_t k = 0; k < cnt; ++k)
+        __stcs(colp + (std::uint64_t)__ldg(a.members2 + beg + k) * ld_vec, m);
+    }
+  }
+  if constexpr (NOISY) {
+    __shared__ double red[kTwoThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nsq;
+    __syncthreads();
+    if (threadIdx.x == 0 && a.noise_partial) {
+      double s = 0.0;
+      for (int i = 0; i < kTwoThreads / 32; ++i) s += red[i];
+      a.noise_partial[blockIdx.x] = s;
+    }
+  } else if (threadIdx.x == 0 && a.noise_partial) {
+    a.noise_partial[blockIdx.x] = 0.0;
+  }
+  if (chk != T(0)) atomicOr(a.nonfinite, 1u);
+}
+
 }  // namespace
 
 template <typename T>
@@ -364,6 +546,79 @@ int group_mean_step_grid(bool f64, bool noisy) {
   if (f64) return noisy ? leaf_grid<double, true>() : leaf_grid<double, false>();
   return noisy ? leaf_grid<float, true>() : leaf_grid<float, false>();
 }
+
+// Step + two averaging rounds in one pass (see two_round_step_kernel).  The
+// caller guarantees: no voided groups (p = 0), groups of <= 32 members, at
+// most two_round_max_groups() groups in round 1.  grp1 / src1: n u32 each
+// (scratch).  Grid: at most 148 * 16 CTAs (the noise-partial slots).
+std::uint32_t two_round_max_groups() { return kTwoMaxG1; }
+
+template <typename T>
+void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
+                           const FusedRound* host_rounds, std::uint32_t g1_max,
+                           std::uint32_t* grp1, std::uint32_t* src1, const StepPrologue<T>& sp,
+                           cudaStream_t s) {
+  if (dim == 0) return;
+  if (g1_max > kTwoMaxG1) throw std::invalid_argument("two-round pass: too many round-1 groups");
+  constexpr int kV = LVec<T>::kN;
+  const FusedRound& r1 = host_rounds[0];
+  const FusedRound& r2 = host_rounds[1];
+  two_round_src_kernel<<<1, 1024, 0, s>>>(r1.members, r1.goff, r1.counts, r2.members, n, grp1,
+                                          src1);
+  MB_LAUNCH_CHECK();
+  TwoArgs<T> a;
+  a.state = state;
+  a.ld_vec = ld / kV;
+  a.nvec = (dim + kV - 1) / kV;
+  a.n_tiles = (a.nvec + kTwoThreads - 1) / kTwoThreads;
+  a.members1 = r1.members;
+  a.goff1 = r1.goff;
+  a.counts1 = r1.counts;
+  a.members2 = r2.members;
+  a.goff2 = r2.goff;
+  a.counts2 = r2.counts;
+  a.src1 = src1;
+  a.curv = sp.curv;
+  a.tgt = sp.tgt;
+  a.gamma = sp.gamma;
+  a.coord_std = sp.coord_std;
+  a.step_no = sp.step_no;
+  a.dim = sp.dim;
+  a.nonfinite = sp.nonfinite;
+  a.noise_partial = sp.noise_partial;
+  a.pk = philox_keys(sp.seed);
+  const std::size_t smem = (std::size_t)g1_max * kTwoThreads * 16;
+  auto run = [&](auto kern) {
+    static thread_local int dev_cached = -1;
+    static thread_local std::size_t smem_set = 0;
+    int dev = 0;
+    MB_CUDA(cudaGetDevice(&dev));
+    if (dev != dev_cached || smem > smem_set) {
+      MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<std::size_t>(smem, 48 * 1024)));
+      dev_cached = dev;
+      smem_set = std::max<std::size_t>(smem, 48 * 1024);
+    }
+    int sms = 0, per = 0;
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTwoThreads, smem));
+    std::uint64_t grid = (std::uint64_t)sms * std::max(per, 1);
+    grid = std::min<std::uint64_t>(grid, std::min<std::uint64_t>(a.n_tiles, 148ull * 16));
+    kern<<<(unsigned)grid, kTwoThreads, smem, s>>>(a);
+  };
+  if (sp.philox) run(two_round_step_kernel<T, true>);
+  else run(two_round_step_kernel<T, false>);
+  MB_LAUNCH_CHECK();
+}
+
+template void launch_two_round_step<float>(float*, std::uint64_t, std::uint64_t, std::uint32_t,
+                                           const FusedRound*, std::uint32_t, std::uint32_t*,
+                                           std::uint32_t*, const StepPrologue<float>&,
+                                           cudaStream_t);
+template void launch_two_round_step<double>(double*, std::uint64_t, std::uint64_t, std::uint32_t,
+                                            const FusedRound*, std::uint32_t, std::uint32_t*,
+                                            std::uint32_t*, const StepPrologue<double>&,
+                                            cudaStream_t);
 
 template void launch_group_mean_step<float>(float*, std::uint64_t, std::uint64_t,
                                             const std::uint32_t*, const std::uint32_t*,

@@ -219,3 +219,36 @@ def test_fused_kernel3_equals_unfused(mb, f64, sigma, tau, M, d, n):
     assert np.isnan(a.f_gap).all()
     if sigma > 0:
         assert abs(a.diagnostics.sigma_hat - b.diagnostics.sigma_hat) <= 1e-9 * b.diagnostics.sigma_hat
+
+
+@pytest.mark.parametrize("f64", [False, True])
+@pytest.mark.parametrize("sigma,tau,M,n,dim,sched", [
+    (1.0, 1, 32, 1024, 1029, []),                  # C4-shaped: 32 groups of 32
+    (0.0, 1, 32, 1024, 64, []),
+    (1.0, 2, 8, 64, 45, [(3, -5), (7, 2)]),        # partial grids after membership events
+    (0.7, 1, 13, 150, 37, [(4, 9)]),               # groups of 13 / ragged lines
+    (1.0, 1, 31, 900, 18, [(2, -100), (9, 61)]),   # leaves of 7-8 members, 4-member batches
+    (1.0, 3, 5, 25, 9, []),
+])
+def test_two_round_pass_equals_kernel3_plus_kernel2(mb, monkeypatch, f64, sigma, tau, M, n,
+                                                    dim, sched):
+    """The SGD averaging step with two rounds in ONE pass over the state
+    (step + round 1 into shared memory, round 2 from there; the default for
+    d = 2, M <= 32) is bit-identical to kernel 3 + kernel 2
+    (MOSHPIT_SGD_TWO_ROUND=0), device noise included."""
+    tgt = mb.Rng(3).stream("objective").normals(dim)
+    cfg = mb.OptimizerConfig(gamma=0.05, tau=tau, steps=9, grid=mb.GridConfig(M, 2, 1),
+                             sigma=sigma, n_peers=n)
+    quad = mb.Quadratic(dim, 2.0, 0.2, tgt)
+    dt = np.float64 if f64 else np.float32
+    ev = [mb.MembershipEvent(*e) for e in sched]
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MOSHPIT_SGD_TWO_ROUND", flag)
+        outs.append(mb.run_moshpit_sgd(cfg, quad, np.zeros(dim), ev, mb.Rng(5), dtype=dt,
+                                       noise="device", diagnostics="none", return_thetas=True))
+    a, b = outs
+    assert bits_equal(a.final_thetas, b.final_thetas)
+    assert bits_equal(a.final_mean, b.final_mean)
+    if sigma > 0:
+        assert abs(a.diagnostics.sigma_hat - b.diagnostics.sigma_hat) <= 1e-9 * b.diagnostics.sigma_hat
