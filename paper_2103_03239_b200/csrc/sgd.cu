@@ -1086,7 +1086,7 @@ static int run_sgd(
                                     philox, seed, k, dim, r.flag.as<std::uint32_t>(), np_slot};
           if (two_round) {
             r.tables.form(*plane, 2, nullptr, 0.0, avg, h.s);
-            r.tables.scratch.resize((std::uint64_t)n * 8 + 16);
+            r.tables.scratch.resize(((std::uint64_t)n * 2 + 8 * two_round_max_groups() + 4) * 4);
             auto* g1 = r.tables.scratch.as<std::uint32_t>();
             const auto g1n = (std::uint32_t)std::min<std::uint64_t>(g1_bound, n);
             if (dtype == MOSHPIT_F32)

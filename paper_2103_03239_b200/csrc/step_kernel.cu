@@ -362,6 +362,9 @@ struct TwoArgs {
   const std::uint32_t* goff2;
   const std::uint32_t* counts2;
   const std::uint32_t* src1;  // [n] round-1 group of the member at round-2 position pos
+  const std::uint32_t* leaf_pos;   // round-1 leaves in order: first position in members1
+  const std::uint32_t* leaf_meta;  // len | l << 4 | nl << 6 | cnt << 9 | g << 15
+  const std::uint32_t* n_leaves;
   const T* curv;
   const T* tgt;
   T gamma;
@@ -373,14 +376,36 @@ struct TwoArgs {
 };
 
 // round-2 source table: src1[pos2] = round-1 group of members2[pos2]
+// ... and round 1's leaf schedule (group order, <= 4 leaves of <= 8 per group)
 __global__ void __launch_bounds__(1024) two_round_src_kernel(
     const std::uint32_t* members1, const std::uint32_t* goff1, const std::uint32_t* counts1,
     const std::uint32_t* members2, std::uint32_t n, std::uint32_t* grp1,
-    std::uint32_t* src1) {
+    std::uint32_t* src1, std::uint32_t* leaf_pos, std::uint32_t* leaf_meta,
+    std::uint32_t* n_leaves) {
   const std::uint32_t g1n = counts1[0];
+  __shared__ std::uint32_t s_first[kTwoMaxG1 + 1];
   for (std::uint32_t g = threadIdx.x; g < g1n; g += blockDim.x)
     for (std::uint32_t pos = goff1[g]; pos < goff1[g + 1]; ++pos) grp1[members1[pos]] = g;
+  if (threadIdx.x == 0) {  // leaves before group g (g1n <= kTwoMaxG1)
+    std::uint32_t acc = 0;
+    for (std::uint32_t g = 0; g < g1n; ++g) {
+      s_first[g] = acc;
+      const std::uint32_t cnt = goff1[g + 1] - goff1[g];
+      acc += cnt <= 8 ? 1u : cnt <= 16 ? 2u : cnt == 17 ? 3u : 4u;
+    }
+    s_first[g1n] = acc;
+    *n_leaves = acc;
+  }
   __syncthreads();
+  for (std::uint32_t g = threadIdx.x; g < g1n; g += blockDim.x) {
+    const std::uint32_t beg = goff1[g], cnt = goff1[g + 1] - beg;
+    std::uint32_t b[5] = {0, 0, 0, 0, 0};
+    const std::uint32_t nl = (std::uint32_t)leaf_bounds(cnt, b);
+    for (std::uint32_t l = 0; l < nl; ++l) {
+      leaf_pos[s_first[g] + l] = beg + b[l];
+      leaf_meta[s_first[g] + l] = (b[l + 1] - b[l]) | (l << 4) | (nl << 6) | (cnt << 9) | (g << 15);
+    }
+  }
   for (std::uint32_t pos = threadIdx.x; pos < n; pos += blockDim.x) src1[pos] = grp1[members2[pos]];
 }
 
@@ -407,36 +432,47 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
     const V c = __ldg(reinterpret_cast<const V*>(a.curv) + col);
     const V t = __ldg(reinterpret_cast<const V*>(a.tgt) + col);
     V* const colp = base + col;
-    // round 1: the step + the tree of every group; means to shared memory
-#pragma unroll 1
-    for (std::uint32_t g = 0; g < G1; ++g) {
-      const std::uint32_t beg = __ldg(a.goff1 + g);
-      const std::uint32_t cnt = __ldg(a.goff1 + g + 1) - beg;
-      const std::uint32_t* ids = a.members1 + beg;
-      std::uint32_t b[5] = {0, 0, 0, 0, 0};
-      const std::uint32_t nl = (std::uint32_t)leaf_bounds(cnt, b);
-      const std::uint32_t b1 = b[1], b2 = b[2], b3 = b[3], b4 = b[4];
-      const std::uint32_t r = nl == 4 ? 2u : 1u;
-      V P = vz<V>(), Q = vz<V>();
-      std::uint32_t lb = 0;  // leaf l = [lb, le), in registers (no local-memory array)
-#pragma unroll 1
-      for (std::uint32_t l = 0; l < nl; ++l) {
-        const std::uint32_t le = l == 0 ? b1 : l == 1 ? b2 : l == 2 ? b3 : b4;
-        // a leaf has <= 8 members (groups of <= 32): all its loads in flight
-        // at once (the CTA count per SM is capped by the shared-memory means,
-        // so each thread needs the memory parallelism), then the step in two
-        // batches of 4 interleaved Philox chains, then the sequential sum
-        V sl = vz<V>();
-        std::uint32_t id[8];
-        V X[8];
+    // round 1: the step + the tree of every group; means to shared memory.
+    // Software-pipelined over the flat leaf schedule: the NEXT leaf's member
+    // loads (<= 8 rows) are in flight while this leaf's Philox normals, step
+    // and sum run (the shared-memory means cap the CTAs per SM, so each
+    // thread carries the memory parallelism).
+    {
+      const std::uint32_t NL = __ldg(a.n_leaves);
+      std::uint32_t meta = __ldg(a.leaf_meta), pos = __ldg(a.leaf_pos);
+      std::uint32_t id[8];
+      V X[8];
+      {
+        const std::uint32_t len = meta & 15u;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) id[k] = (lb + k < le) ? __ldg(ids + lb + k) : 0u;
+        for (int k = 0; k < 8; ++k) id[k] = (k < (int)len) ? __ldg(a.members1 + pos + k) : 0u;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          X[k] = (lb + k < le) ? colp[(std::uint64_t)id[k] * ld_vec] : vz<V>();
+          X[k] = (k < (int)len) ? colp[(std::uint64_t)id[k] * ld_vec] : vz<V>();
+      }
+      V P = vz<V>(), Q = vz<V>();
+#pragma unroll 1
+      for (std::uint32_t L = 0; L < NL; ++L) {
+        // next leaf's loads first
+        std::uint32_t meta_n = 0, id_n[8];
+        V X_n[8];
+        {
+          const bool more = L + 1 < NL;
+          const std::uint32_t pos_n = more ? __ldg(a.leaf_pos + L + 1) : 0u;
+          meta_n = more ? __ldg(a.leaf_meta + L + 1) : 0u;
+          const std::uint32_t len_n = meta_n & 15u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            id_n[k] = (k < (int)len_n) ? __ldg(a.members1 + pos_n + k) : 0u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            X_n[k] = (k < (int)len_n) ? colp[(std::uint64_t)id_n[k] * ld_vec] : vz<V>();
+        }
+        const std::uint32_t len = meta & 15u, l = (meta >> 4) & 3u, nl = (meta >> 6) & 7u;
+        const std::uint32_t cnt = (meta >> 9) & 63u, g = meta >> 15;
 #pragma unroll
         for (int h = 0; h < 8; h += 4) {
-          if (lb + h + 4 <= le) {
+          if ((std::uint32_t)h + 4 <= len) {
             float z[4][4] = {};
             if constexpr (NOISY) {
 #pragma unroll
@@ -449,20 +485,27 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              if (lb + h + e < le)
+              if ((std::uint32_t)(h + e) < len)
                 step_vec<T, NOISY>(X[h + e], c, t, gamma, cst, seed, step_no, id[h + e], j0,
                                    full, dim, chk, nsq);
           }
         }
+        V sl = vz<V>();
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (lb + k < le) sl = vsum(sl, X[k]);
+          if ((std::uint32_t)k < len) sl = vsum(sl, X[k]);
+        // joins: L0 | L0+L1 | L0+(L1+L2) | (L0+L1)+(L2+L3)
+        const std::uint32_t r = nl == 4 ? 2u : 1u;
         if (l < r) P = l == 0 ? sl : vsum(P, sl);
         else Q = l == r ? sl : vsum(Q, sl);
-        lb = le;
+        if (l + 1 == nl) m1[g * kTwoThreads + threadIdx.x] = vdivn(nl == 1 ? P : vsum(P, Q), cnt);
+        meta = meta_n;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          id[k] = id_n[k];
+          X[k] = X_n[k];
+        }
       }
-      const V sum = nl == 1 ? P : vsum(P, Q);
-      m1[g * kTwoThreads + threadIdx.x] = vdivn(sum, cnt);
     }
     // round 2: member k of group g2 holds m1[src1[pos]]
 #pragma unroll 1
@@ -549,8 +592,9 @@ int group_mean_step_grid(bool f64, bool noisy) {
 
 // Step + two averaging rounds in one pass (see two_round_step_kernel).  The
 // caller guarantees: no voided groups (p = 0), groups of <= 32 members, at
-// most two_round_max_groups() groups in round 1.  grp1 / src1: n u32 each
-// (scratch).  Grid: at most 148 * 16 CTAs (the noise-partial slots).
+// most two_round_max_groups() groups in round 1.  grp1: n u32, src1: n +
+// 8 * two_round_max_groups() + 1 u32 (scratch: the round-2 sources, then
+// round 1's leaf schedule).  Grid: at most 148 * 16 CTAs (the noise-partial slots).
 std::uint32_t two_round_max_groups() { return kTwoMaxG1; }
 
 template <typename T>
@@ -563,8 +607,11 @@ void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::u
   constexpr int kV = LVec<T>::kN;
   const FusedRound& r1 = host_rounds[0];
   const FusedRound& r2 = host_rounds[1];
+  std::uint32_t* leaf_pos = src1 + n;
+  std::uint32_t* leaf_meta = leaf_pos + 4 * kTwoMaxG1;
+  std::uint32_t* n_leaves = leaf_meta + 4 * kTwoMaxG1;
   two_round_src_kernel<<<1, 1024, 0, s>>>(r1.members, r1.goff, r1.counts, r2.members, n, grp1,
-                                          src1);
+                                          src1, leaf_pos, leaf_meta, n_leaves);
   MB_LAUNCH_CHECK();
   TwoArgs<T> a;
   a.state = state;
@@ -578,6 +625,9 @@ void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::u
   a.goff2 = r2.goff;
   a.counts2 = r2.counts;
   a.src1 = src1;
+  a.leaf_pos = leaf_pos;
+  a.leaf_meta = leaf_meta;
+  a.n_leaves = n_leaves;
   a.curv = sp.curv;
   a.tgt = sp.tgt;
   a.gamma = sp.gamma;
