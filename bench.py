@@ -758,7 +758,12 @@ def run_peer(mb, torch, dist, cfg, steps, warmup, rank, world, local, nvlink=Fal
         "unit": "GB/s", "scaling": "strong", "steps": steps, "ms_per_step": round(t_max / steps, 4),
         "slabs": slabs,
         "rounds_local": ln, "rounds_cross": cross_rounds,
-        "gpu_launches": ln * 3 + cross_rounds * (7 + (2 if p > 0 else 0)),
+        # per round: kernel 1 + the placement kernel (control stream); per slab
+        # and local round: kernel 2; per slab and cross round: the barriers and
+        # the mode's kernels (exact: cross_mean + pull [+ the voided rows'
+        # staging pull]; partial: partial_sum + combine + pull)
+        "gpu_launches": steps * 2 + ln + (cn // 2) * (
+            (4 + 3) if cross == "partial" else (3 + 2 + (1 if p > 0 else 0))),
         "nvlink_counters": nvl_meas,
         "local_kernel_ms": round(lmax, 3), "cross_kernel_ms": round(cmax, 3),
         "roofline": {
