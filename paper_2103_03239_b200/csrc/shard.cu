@@ -1657,12 +1657,16 @@ int moshpit_shard_set_cross_mode(moshpit_shard* h, std::int32_t mode) {
     S.cross_mode = mode;
     // the slab pipeline's SM split: the exact round's cross kernels are
     // NVLink-bound (~30 % of the SMs), the partial round's carry HBM-bound
-    // partial sums too (an even split: C2 2 GPUs 5378 -> 5758 GB/s, 4 GPUs
-    // 8384 -> 8563 against 104 / 44; profiles/r02/partial/p7_sweep_*.txt)
+    // partial sums too: the local kernels get the local rounds' share,
+    // (d-1)/d of the SMs (d = 2: an even split, C2 2 GPUs 5378 -> 5758 GB/s,
+    // 4 GPUs 8384 -> 8563 against 104 / 44; profiles/r02/partial/p7_sweep_*.txt)
     if (S.S > 1 && !std::getenv("MOSHPIT_PIPE_LOCAL_SMS") &&
         !std::getenv("MOSHPIT_PIPE_CROSS_SMS")) {
       const int sms = S.sm_count();
-      S.pipe_local_sms = mode == MOSHPIT_CROSS_PARTIAL ? sms / 2 : (sms * 104 + 74) / 148;
+      S.pipe_local_sms = mode == MOSHPIT_CROSS_PARTIAL
+                             ? (int)((std::uint64_t)sms * (S.d - 1) / std::max<std::uint32_t>(S.d, 2))
+                             : (sms * 104 + 74) / 148;
+      if (S.pipe_local_sms < 1) S.pipe_local_sms = sms / 2;
       S.pipe_cross_sms = sms - S.pipe_local_sms;
     }
   });
