@@ -365,6 +365,7 @@ struct TwoArgs {
   const std::uint32_t* leaf_pos;   // round-1 leaves in order: first position in members1
   const std::uint32_t* leaf_meta;  // len | l << 4 | nl << 6 | cnt << 9 | g << 15
   const std::uint32_t* n_leaves;
+  std::uint32_t n, g1_max;
   const T* curv;
   const T* tgt;
   T gamma;
@@ -415,13 +416,23 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
   using V = typename LVec<T>::V;
   constexpr int kV = LVec<T>::kN;
   extern __shared__ uint4 two_smem[];
-  V* const m1 = reinterpret_cast<V*>(two_smem);  // [G1][kTwoThreads]
+  V* const m1 = reinterpret_cast<V*>(two_smem);  // [g1_max][kTwoThreads]
   const T gamma = a.gamma;
   const T cst = (T)a.coord_std;
   const std::uint64_t step_no = a.step_no, dim = a.dim, ld_vec = a.ld_vec;
   const PhiloxKeys& seed = a.pk;
   V* const base = reinterpret_cast<V*>(a.state);
   const std::uint32_t G1 = a.counts1[0], G2 = a.counts2[0];
+  // round 2's tables in shared memory (its loop is a chain of table look-ups:
+  // position -> round-1 slot / member row): packed (src1 << 16 | member) per
+  // position, then the group offsets
+  std::uint32_t* const s_tab = reinterpret_cast<std::uint32_t*>(m1 + a.g1_max * kTwoThreads);
+  std::uint32_t* const s_goff2 = s_tab + a.n;
+  for (std::uint32_t q = threadIdx.x; q < a.n; q += kTwoThreads)
+    s_tab[q] = (__ldg(a.src1 + q) << 16) | __ldg(a.members2 + q);
+  if (G1 > a.g1_max || G2 > a.g1_max) __trap();  // the host's bound (grid lines) broke
+  for (std::uint32_t q = threadIdx.x; q <= G2; q += kTwoThreads) s_goff2[q] = __ldg(a.goff2 + q);
+  __syncthreads();
   T chk = T(0);
   double nsq = 0.0;
   for (std::uint64_t tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
@@ -510,8 +521,8 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
     // round 2: member k of group g2 holds m1[src1[pos]]
 #pragma unroll 1
     for (std::uint32_t g = 0; g < G2; ++g) {
-      const std::uint32_t beg = __ldg(a.goff2 + g);
-      const std::uint32_t cnt = __ldg(a.goff2 + g + 1) - beg;
+      const std::uint32_t beg = s_goff2[g];
+      const std::uint32_t cnt = s_goff2[g + 1] - beg;
       std::uint32_t b[5] = {0, 0, 0, 0, 0};
       const std::uint32_t nl = (std::uint32_t)leaf_bounds(cnt, b);
       const std::uint32_t b1 = b[1], b2 = b[2], b3 = b[3], b4 = b[4];
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
         V sl = vz<V>();
 #pragma unroll 4
         for (std::uint32_t k = lb; k < le; ++k)
-          sl = vsum(sl, m1[__ldg(a.src1 + beg + k) * kTwoThreads + threadIdx.x]);
+          sl = vsum(sl, m1[(s_tab[beg + k] >> 16) * kTwoThreads + threadIdx.x]);
         if (l < r) P = l == 0 ? sl : vsum(P, sl);
         else Q = l == r ? sl : vsum(Q, sl);
         lb = le;
@@ -532,7 +543,7 @@ __global__ void __launch_bounds__(kTwoThreads, 6)
       const V m = vdivn(nl == 1 ? P : vsum(P, Q), cnt);
 #pragma unroll 4
       for (std::uint32_t k = 0; k < cnt; ++k)
-        __stcs(colp + (std::uint64_t)__ldg(a.members2 + beg + k) * ld_vec, m);
+        __stcs(colp + (std::uint64_t)(s_tab[beg + k] & 0xffffu) * ld_vec, m);
     }
   }
   if constexpr (NOISY) {
@@ -628,6 +639,8 @@ void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::u
   a.leaf_pos = leaf_pos;
   a.leaf_meta = leaf_meta;
   a.n_leaves = n_leaves;
+  a.n = n;
+  a.g1_max = g1_max;
   a.curv = sp.curv;
   a.tgt = sp.tgt;
   a.gamma = sp.gamma;
@@ -637,7 +650,11 @@ void launch_two_round_step(T* state, std::uint64_t ld, std::uint64_t dim, std::u
   a.nonfinite = sp.nonfinite;
   a.noise_partial = sp.noise_partial;
   a.pk = philox_keys(sp.seed);
-  const std::size_t smem = (std::size_t)g1_max * kTwoThreads * 16;
+  if (n > 0xffffu) throw std::invalid_argument("two-round pass: more than 65535 peers");
+  // round-1 means + round 2's packed table (n) and group offsets (round 2 has
+  // at most as many groups as round 1's bound: both are lines of the grid)
+  const std::size_t smem =
+      (std::size_t)g1_max * kTwoThreads * 16 + ((std::size_t)n + g1_max + 1) * 4;
   auto run = [&](auto kern) {
     static thread_local int dev_cached = -1;
     static thread_local std::size_t smem_set = 0;
