@@ -724,7 +724,11 @@ __global__ void broadcast_rows_kernel(T* __restrict__ dst, std::uint64_t ld,
 // then the block tree of block_sum_fixed per row.  The rows of a block share
 // every reference load (the fp64 reference is twice the bytes of an fp32
 // row: one row per block read 12 bytes per fp32 coordinate through L2).
-constexpr int kFastRows = 4;
+#ifndef MB_FAST_ROWS
+#define MB_FAST_ROWS 4
+#endif
+constexpr int kFastRows = MB_FAST_ROWS;  // rows per block (bits do not depend on it;
+// C2 round + FAST record 6.97 ms at 4, 7.60 at 16, 8.24 at 8: profiles/r02/diag/fast_rows.txt)
 
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)

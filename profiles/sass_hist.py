@@ -1,7 +1,8 @@
 """SASS instruction histogram per kernel of the built library (cuobjdump
 -sass), for the hot kernels: kernel 1 (form_groups_kernel), kernel 2
 (group_mean_register, group_mean_bulk), kernel 3 (group_mean_step_leaf), the
-cross-round kernels and the EXACT diagnostics.  Writes a text table.
+two-round SGD pass, the cross-round kernels (exact and partial-sum) and the
+EXACT diagnostics.  Writes a text table.
 
     python profiles/sass_hist.py > profiles/r02/sass_hist.txt
 """
@@ -14,7 +15,8 @@ import sys
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                    "paper_2103_03239_b200", "libmoshpit_b200.so")
 PATTERNS = ["form_groups_kernel", "group_mean_register", "group_mean_bulk",
-            "group_mean_step_leaf", "cross_mean_kernel", "shard_pull_kernel",
+            "group_mean_step_leaf", "two_round_step_kernel", "cross_mean_kernel",
+            "partial_sum_kernel", "partial_combine_kernel", "shard_pull_kernel",
             "dist_exact_tiled", "colmean_kernel"]
 
 
