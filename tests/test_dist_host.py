@@ -74,7 +74,10 @@ def test_two_rank_handle_exchange_and_validation():
 
 
 @pytest.mark.gpu
-def test_real_multi_gpu_shards():
+@pytest.mark.parametrize("cross", ["exact", "partial"])
+def test_real_multi_gpu_shards(cross):
+    """One process per GPU over real NVLink: exact cross rounds bit-exact,
+    partial-sum cross rounds within 1e-6 relative of the oracle."""
     import subprocess
     import sys
 
@@ -87,6 +90,7 @@ def test_real_multi_gpu_shards():
                         f"--nproc-per-node={min(g, 8)}", "--master-addr", "127.0.0.1",
                         "--master-port", str(_free_port()),
                         os.path.join(root, "tests", "mgpu", "shard_check.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, CROSS=cross))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SHARD CHECK PASS" in r.stdout
