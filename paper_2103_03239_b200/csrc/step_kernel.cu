@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(1024) two_round_src_kernel(
     std::uint32_t* n_leaves) {
   const std::uint32_t g1n = counts1[0];
   __shared__ std::uint32_t s_first[kTwoMaxG1 + 1];
+  if (g1n > kTwoMaxG1) __trap();  // the host's bound (grid lines) broke
   for (std::uint32_t g = threadIdx.x; g < g1n; g += blockDim.x)
     for (std::uint32_t pos = goff1[g]; pos < goff1[g + 1]; ++pos) grp1[members1[pos]] = g;
   if (threadIdx.x == 0) {  // leaves before group g (g1n <= kTwoMaxG1)
