@@ -312,6 +312,16 @@ int moshpit_engine_record(moshpit_engine* e, int dtype, const void* state,
 int moshpit_engine_round_record(moshpit_engine* e, int dtype, void* state,
                                 uint64_t dim, uint64_t ld, void* stream,
                                 uint32_t* active_out);
+/* `rounds` x (round + record_round) in one call on device-resident state
+ * (the protocols::run_moshpit loop, protocols.hpp:142-173).  Nothing else
+ * touches the state between the rounds of one call, so with
+ * MOSHPIT_DIAG_FAST the voided groups' rows keep their cached FAST row
+ * partials and only the averaged groups' representative rows are re-read;
+ * the TrialReport bits equal `rounds` moshpit_engine_round_record calls.
+ * active_out: [rounds] non-failed peers per round (optional). */
+int moshpit_engine_rounds_record(moshpit_engine* e, int dtype, void* state,
+                                 uint64_t dim, uint64_t ld, uint32_t rounds,
+                                 void* stream, uint32_t* active_out);
 int moshpit_engine_report(moshpit_engine* e, double* initial_distortion,
                           double* distortion, double* mean_drift, uint64_t cap,
                           uint64_t* count);

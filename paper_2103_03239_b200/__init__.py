@@ -753,6 +753,21 @@ class Engine:
                                                 s.cuda_stream, C.byref(act)))
         return act.value
 
+    def rounds_record(self, state, rounds: int, dim: Optional[int] = None,
+                      stream=None) -> List[int]:
+        """``rounds`` x (round + record_round) in one call (the run_moshpit
+        loop on the device): with FAST diagnostics the voided rows' cached row
+        partials are reused, only the averaged groups' representatives are
+        re-read; same bits as ``rounds`` round_record() calls."""
+        import torch
+        code, ptr, ld = _tensor_args(state)
+        s = stream if stream is not None else torch.cuda.current_stream(state.device)
+        act = (C.c_uint32 * max(int(rounds), 1))()
+        check(lib().moshpit_engine_rounds_record(self._h, code, ptr,
+                                                 state.shape[1] if dim is None else dim, ld,
+                                                 int(rounds), s.cuda_stream, act))
+        return list(act)[:int(rounds)]
+
     def record(self, state, dim: Optional[int] = None, stream=None):
         """Append this round's (distortion, mean_drift) to the device log."""
         import torch

@@ -106,6 +106,7 @@ PROTOTYPES = {
     "moshpit_engine_set_reference": (C.c_int, [vp, C.c_int, vp, u64, u64, C.c_int, vp]),
     "moshpit_engine_record": (C.c_int, [vp, C.c_int, vp, u64, u64, vp]),
     "moshpit_engine_round_record": (C.c_int, [vp, C.c_int, vp, u64, u64, vp, P(u32)]),
+    "moshpit_engine_rounds_record": (C.c_int, [vp, C.c_int, vp, u64, u64, u32, vp, P(u32)]),
     "moshpit_engine_report": (C.c_int, [vp, P(dbl), vp, vp, u64, P(u64)]),
     "moshpit_shard_create": (C.c_int, [C.c_int, u32, u32, u64, dbl, u64, u64, i32, i32, i32,
                                        i32, P(vp)]),

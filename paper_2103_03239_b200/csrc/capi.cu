@@ -916,18 +916,24 @@ int moshpit_engine_tables(moshpit_engine* e, std::uint32_t* members, std::uint32
 // ---------------------------------------------------------------------------
 namespace {
 
+// cached: FAST with representatives, the row-partial cache kept warm
+// (launch_distortion_fast_cached; reps lists only what changed)
 template <typename T>
 void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t dim,
                  double* dist_slot, double* drift_slot, cudaStream_t s,
-                 const RepRows* reps = nullptr) {
+                 const RepRows* reps = nullptr, bool cached = false) {
   const std::uint64_t n = e->plane->n;
   const int exact = e->diag == MOSHPIT_DIAG_EXACT;
   if (drift_slot) {
     MB_CUDA(cudaEventRecord(e->ev_fork, s));
     MB_CUDA(cudaStreamWaitEvent(e->aux->s, e->ev_fork, 0));
   }
-  launch_distortion<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
-                       e->part.as<double>(), dist_slot, exact, s, reps);
+  if (cached && reps && !exact)
+    launch_distortion_fast_cached<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
+                                     e->part.as<double>(), dist_slot, s, *reps);
+  else
+    launch_distortion<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
+                         e->part.as<double>(), dist_slot, exact, s, reps);
   if (drift_slot) {
     launch_colmean<T, double>(x, n, ld, dim, reps ? reps->rep : nullptr, e->mean.as<double>(),
                               e->aux->s, true);
@@ -992,8 +998,12 @@ namespace {
 // record_round after the state's latest change; with `after_round` the
 // state is exactly the output of the engine's last round, so its averaged
 // groups' rows are identical and only representative rows are read.
+// cache_warm (FAST, after_round, within one moshpit_engine_rounds_record
+// call): every row's FAST partials are in its slot from the previous round's
+// record, so only the averaged groups' representatives are re-read.
 void engine_record_impl(moshpit_engine* e, int dtype, const void* state, std::uint64_t dim,
-                        std::uint64_t ld, cudaStream_t s, bool after_round) {
+                        std::uint64_t ld, cudaStream_t s, bool after_round,
+                        bool use_cache = false, bool cache_warm = false) {
   if (e->diag == MOSHPIT_DIAG_NONE)
     throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
   if (dim != e->diag_dim) throw std::invalid_argument("engine_record: dim changed");
@@ -1017,17 +1027,18 @@ void engine_record_impl(moshpit_engine* e, int dtype, const void* state, std::ui
     launch_build_reps(p.members.as<std::uint32_t>(), p.goff.as<std::uint32_t>(),
                       p.gvoid.as<std::uint8_t>(), p.counts.as<std::uint32_t>(), n,
                       e->rep.as<std::uint32_t>(), e->rlist.as<std::uint32_t>(),
-                      e->rcount.as<std::uint32_t>(), s);
+                      e->rcount.as<std::uint32_t>(), s, use_cache && cache_warm ? 0 : 1);
     reps = RepRows{e->rep.as<std::uint32_t>(), e->rlist.as<std::uint32_t>(),
                    e->rcount.as<std::uint32_t>()};
   }
   double* slot = e->log.as<double>() + 1 + 2 * e->log_n;
+  const bool cached = use_cache && after_round;
   if (dtype == MOSHPIT_F32)
     engine_diag<float>(e, static_cast<const float*>(state), ld, dim, slot, slot + 1, s,
-                       after_round ? &reps : nullptr);
+                       after_round ? &reps : nullptr, cached);
   else
     engine_diag<double>(e, static_cast<const double*>(state), ld, dim, slot, slot + 1, s,
-                        after_round ? &reps : nullptr);
+                        after_round ? &reps : nullptr, cached);
   ++e->log_n;
   e->plane->mark_done(s);
 }
@@ -1060,6 +1071,35 @@ int moshpit_engine_round_record(moshpit_engine* e, int dtype, void* state, std::
         e->plane->round(&e->fail, e->p, e->clock, dtype, state, dim, ld, s, e->variant);
     if (active_out) *active_out = a;
     engine_record_impl(e, dtype, state, dim, ld, s, true);
+  });
+}
+
+// `rounds` rounds, each followed by its record_round, in one call (the
+// protocols.hpp:142-173 loop on device-resident state).  Between the rounds
+// of one call nothing else touches the state, so with FAST diagnostics the
+// rows of voided groups -- unchanged by their round -- keep their FAST row
+// partials from the previous record and only the averaged groups'
+// representatives are re-read (the first round of the call reads every
+// representative).  TrialReport bits are those of `rounds` round_record
+// calls.  active_out: [rounds] (optional).
+int moshpit_engine_rounds_record(moshpit_engine* e, int dtype, void* state, std::uint64_t dim,
+                                 std::uint64_t ld, std::uint32_t rounds, void* stream,
+                                 std::uint32_t* active_out) {
+  return guarded([&] {
+    if (!e) throw std::invalid_argument("null engine");
+    if (!state) throw std::invalid_argument("engine_rounds_record: null state");
+    check_state(dtype, state, dim, ld);
+    if (e->diag == MOSHPIT_DIAG_NONE)
+      throw std::invalid_argument("engine_record: set_reference with a diagnostics mode first");
+    DeviceGuard g(e->plane->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const bool fast = e->diag == MOSHPIT_DIAG_FAST;
+    for (std::uint32_t r = 0; r < rounds; ++r) {
+      const std::uint32_t a =
+          e->plane->round(&e->fail, e->p, e->clock, dtype, state, dim, ld, s, e->variant);
+      if (active_out) active_out[r] = a;
+      engine_record_impl(e, dtype, state, dim, ld, s, true, fast, r > 0);
+    }
   });
 }
 

@@ -357,10 +357,12 @@ bool launch_step_colmean(T* x, std::uint64_t n, std::uint64_t ld, std::uint64_t 
                          std::uint64_t seed, std::uint64_t step_no, std::uint32_t* nonfinite,
                          double* noise_partial, std::uint64_t partial_slots, double* hat,
                          cudaStream_t s);
+// list_voided = 0: only the averaged groups' representatives are listed
+// (the voided rows are unchanged; see launch_distortion_fast_cached)
 void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint8_t* gvoid, const std::uint32_t* counts, std::uint64_t n,
                        std::uint32_t* rep, std::uint32_t* list, std::uint32_t* count,
-                       cudaStream_t s);
+                       cudaStream_t s, int list_voided = 1);
 template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
@@ -370,6 +372,11 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq_scratch,
                        double* partial_scratch, double* out, int exact,
                        cudaStream_t s, const RepRows* reps = nullptr);
+template <typename T>
+void launch_distortion_fast_cached(const T* x, std::uint64_t n, std::uint64_t ld,
+                                   std::uint64_t dim, const double* ref, double* sq,
+                                   double* partial, double* out, cudaStream_t s,
+                                   const RepRows& reps);
 void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
                   double* partial_scratch, double* out, int exact,
                   cudaStream_t s);

@@ -607,7 +607,7 @@ __global__ void build_reps_kernel(const std::uint32_t* __restrict__ members,
                                   const std::uint8_t* __restrict__ gvoid,
                                   const std::uint32_t* __restrict__ counts,
                                   std::uint32_t* __restrict__ rep, std::uint32_t* __restrict__ list,
-                                  std::uint32_t* __restrict__ count) {
+                                  std::uint32_t* __restrict__ count, int list_voided) {
   const std::uint32_t ng = counts[0];
   for (std::uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng;
        g += gridDim.x * blockDim.x) {
@@ -619,9 +619,25 @@ __global__ void build_reps_kernel(const std::uint32_t* __restrict__ members,
     } else {  // voided: the members keep their own rows
       for (std::uint32_t k = b; k < e; ++k) {
         rep[members[k]] = members[k];
-        list[atomicAdd(count, 1u)] = members[k];
+        if (list_voided) list[atomicAdd(count, 1u)] = members[k];
       }
     }
+  }
+}
+
+// FAST row partials of every member of an averaged group from its
+// representative's (the rows are identical): afterwards every row's slot
+// holds its own partials, so a later record can skip the rows it knows are
+// unchanged (the voided rows of the next round).
+__global__ void scatter_rep_partials(double* __restrict__ partial,
+                                     const std::uint32_t* __restrict__ rep, std::uint64_t n,
+                                     std::uint64_t nch) {
+  const std::uint64_t total = n * nch;
+  for (std::uint64_t e = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t i = e / nch, c = e % nch;
+    const std::uint32_t r = rep[i];
+    if (r != i) partial[i * nch + c] = partial[(std::uint64_t)r * nch + c];
   }
 }
 
@@ -675,15 +691,29 @@ __global__ void drift_fast_partial(const double* __restrict__ mean,
   }
 }
 
-__global__ void drift_fast_finish(const double* __restrict__ partial,
-                                  std::uint64_t nch, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The two chunk folds in chunk order by one thread, the partials staged in
+// shared memory by the whole CTA first (a lone thread's global loads were
+// ~80 us of latency per record on the drift stream, its critical path).
+constexpr int kDriftFinThreads = 256, kDriftFinBatch = 1024;
+__global__ void __launch_bounds__(kDriftFinThreads)
+    drift_fast_finish(const double* __restrict__ partial, std::uint64_t nch,
+                      double* __restrict__ out) {
+  __shared__ double buf[2 * kDriftFinBatch];
   double a = 0.0, b = 0.0;
-  for (std::uint64_t c = 0; c < nch; ++c) {
-    a = __dadd_rn(a, partial[2 * c]);
-    b = __dadd_rn(b, partial[2 * c + 1]);
+  for (std::uint64_t c0 = 0; c0 < nch; c0 += kDriftFinBatch) {
+    const std::uint64_t m = nch - c0 < (std::uint64_t)kDriftFinBatch ? nch - c0 : kDriftFinBatch;
+    for (std::uint64_t q = threadIdx.x; q < 2 * m; q += kDriftFinThreads)
+      buf[q] = partial[2 * c0 + q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (std::uint64_t c = 0; c < m; ++c) {
+        a = __dadd_rn(a, buf[2 * c]);
+        b = __dadd_rn(b, buf[2 * c + 1]);
+      }
+    }
+    __syncthreads();
   }
-  *out = __ddiv_rn(__dsqrt_rn(a), fmax(__dsqrt_rn(b), 1e-300));
+  if (threadIdx.x == 0) *out = __ddiv_rn(__dsqrt_rn(a), fmax(__dsqrt_rn(b), 1e-300));
 }
 
 __device__ __forceinline__ std::uint64_t splitmix64_dev(std::uint64_t s) {
@@ -882,10 +912,10 @@ void launch_dist_slab(const T* x, std::uint64_t n, std::uint64_t ld, std::uint64
 void launch_build_reps(const std::uint32_t* members, const std::uint32_t* goff,
                        const std::uint8_t* gvoid, const std::uint32_t* counts, std::uint64_t n,
                        std::uint32_t* rep, std::uint32_t* list, std::uint32_t* count,
-                       cudaStream_t s) {
+                       cudaStream_t s, int list_voided) {
   MB_CUDA(cudaMemsetAsync(count, 0, 4, s));
   build_reps_kernel<<<(unsigned)std::max<std::uint64_t>(1, (n + 255) / 256), 256, 0, s>>>(
-      members, goff, gvoid, counts, rep, list, count);
+      members, goff, gvoid, counts, rep, list, count, list_voided);
   MB_LAUNCH_CHECK();
 }
 
@@ -920,7 +950,7 @@ void launch_diag_finish(std::uint64_t n, std::uint64_t nch_total, int exact, dou
     if (exact)
       drift_finish_acc<<<1, 1, 0, s>>>(acc2, drift_out);
     else
-      drift_fast_finish<<<1, 1, 0, s>>>(drift_partial, nch_total, drift_out);
+      drift_fast_finish<<<1, kDriftFinThreads, 0, s>>>(drift_partial, nch_total, drift_out);
     MB_LAUNCH_CHECK();
   }
 }
@@ -1068,6 +1098,42 @@ void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
   MB_LAUNCH_CHECK();
 }
 
+// FAST distortion after a round from the representative rows listed in
+// `reps` -- every row when the caller's partial cache is cold, only the
+// averaged groups' representatives when every other row is known to be
+// unchanged since the previous call (its partials are still in its slot) --
+// then the representatives' partials scattered into their members' slots.
+// The per-row partials and their fold are the uncached path's: bit-identical.
+template <typename T>
+void launch_distortion_fast_cached(const T* x, std::uint64_t n, std::uint64_t ld,
+                                   std::uint64_t dim, const double* ref, double* sq,
+                                   double* partial, double* out, cudaStream_t s,
+                                   const RepRows& reps) {
+  if (n == 0 || dim == 0) {
+    launch_distortion<T>(x, n, ld, dim, ref, sq, partial, out, 0, s, &reps);
+    return;
+  }
+  const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
+  const unsigned gy = fast_rows_grid(n, nch, true);
+  dist_rows_fast_off<T><<<dim3((unsigned)nch, gy), kRedThreads, 0, s>>>(
+      x, ld, dim, ref, nch, 0, partial, n, reps.list, reps.count);
+  MB_LAUNCH_CHECK();
+  fold_rows<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(partial, n, nch, sq, reps.rep);
+  MB_LAUNCH_CHECK();
+  scatter_rep_partials<<<grid_for(n * nch, 256), 256, 0, s>>>(partial, reps.rep, n, nch);
+  MB_LAUNCH_CHECK();
+  finish_distortion<<<1, kFinThreads, 0, s>>>(sq, n, out);
+  MB_LAUNCH_CHECK();
+}
+template void launch_distortion_fast_cached<float>(const float*, std::uint64_t, std::uint64_t,
+                                                   std::uint64_t, const double*, double*,
+                                                   double*, double*, cudaStream_t,
+                                                   const RepRows&);
+template void launch_distortion_fast_cached<double>(const double*, std::uint64_t, std::uint64_t,
+                                                    std::uint64_t, const double*, double*,
+                                                    double*, double*, cudaStream_t,
+                                                    const RepRows&);
+
 void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
                   double* partial, double* out, int exact, cudaStream_t s) {
   if (exact || dim == 0) {
@@ -1077,7 +1143,7 @@ void launch_drift(const double* mean, const double* ref, std::uint64_t dim,
     const std::uint64_t nch = (dim + kChunk - 1) / kChunk;
     drift_fast_partial<<<(unsigned)nch, kRedThreads, 0, s>>>(mean, ref, dim, partial);
     MB_LAUNCH_CHECK();
-    drift_fast_finish<<<1, 1, 0, s>>>(partial, nch, out);
+    drift_fast_finish<<<1, kDriftFinThreads, 0, s>>>(partial, nch, out);
   }
   MB_LAUNCH_CHECK();
 }

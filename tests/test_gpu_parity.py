@@ -627,3 +627,47 @@ def test_engine_round_record_equals_round_then_record(mb, torch, diag):
     assert bits_equal(np.array([i0]), np.array([i1]))
     assert bits_equal(np.array(d0), np.array(d1))
     assert bits_equal(np.array(f0), np.array(f1))
+
+
+@pytest.mark.parametrize("f64,diag,M,d,n,p,R,dim", [
+    (False, "fast", 16, 2, 256, 0.05, 7, 70_001),
+    (False, "fast", 32, 2, 1024, 0.01, 6, 8_195),
+    (True, "fast", 8, 3, 400, 0.2, 5, 4_099),
+    (False, "fast", 5, 2, 25, 0.3, 9, 37),
+    (False, "exact", 16, 2, 256, 0.05, 4, 1_000),
+])
+def test_engine_rounds_record_equals_run_moshpit(mb, torch, f64, diag, M, d, n, p, R, dim):
+    """Engine.rounds_record (R rounds + record_round in one call; FAST reuses
+    the voided rows' cached row partials and re-reads only the averaged
+    groups' representatives) gives the TrialReport bits and vectors of
+    run_moshpit on host buffers, and of R round_record calls."""
+    tdt = torch.float64 if f64 else torch.float32
+    pad = (dim + 3) // 4 * 4
+    x = torch.zeros((n, pad), dtype=tdt, device="cuda")
+    mb.fill_synthetic(x, INIT_SEED, dim=dim)
+    host = np.ascontiguousarray(x[:, :dim].cpu().numpy())
+    y = x.clone()
+    outs = []
+    for mode in ("rounds", "each"):
+        z = x if mode == "rounds" else y
+        eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+        eng.set_reference(z, diagnostics=diag, dim=dim)
+        if mode == "rounds":
+            act = eng.rounds_record(z, R, dim=dim)
+        else:
+            act = [eng.round_record(z, dim=dim) for _ in range(R)]
+        outs.append((eng.report(), act))
+        eng.close()
+    torch.cuda.synchronize()
+    (init_a, dist_a, drift_a), act_a = outs[0]
+    (init_b, dist_b, drift_b), act_b = outs[1]
+    assert act_a == act_b
+    assert bits_equal(np.array(dist_a), np.array(dist_b))
+    assert bits_equal(np.array(drift_a), np.array(drift_b))
+    assert torch.equal(x, y)
+    want = mb.run_moshpit(mb.GridConfig(M, d, 1), host, mb.FailureModel(p), mb.Rng(7), R,
+                          diagnostics=diag, return_vectors=True)
+    assert bits_equal(np.array([init_a]), np.array([want.initial_distortion]))
+    assert bits_equal(np.array(dist_a), np.array(want.distortion))
+    assert bits_equal(np.array(drift_a), np.array(want.mean_drift))
+    assert bits_equal(np.ascontiguousarray(x[:, :dim].cpu().numpy()), want.vectors)
