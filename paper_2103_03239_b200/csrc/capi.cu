@@ -817,7 +817,7 @@ int moshpit_engine_round(moshpit_engine* e, int dtype, void* state, std::uint64_
 
 // Several rounds in one pass over the state (temporal blocking, a separate
 // mode from the per-round path): kernel 1 for each round, then one fused
-// kernel per chunk of at most fused_rounds_max(n) rounds.  Bit-identical to
+// kernel per chunk of at most fused_rounds_max(n, M^(d-1)) rounds.  Bit-identical to
 // `rounds` calls of moshpit_engine_round.
 int moshpit_engine_rounds_fused(moshpit_engine* e, int dtype, void* state, std::uint64_t dim,
                                 std::uint64_t ld, std::uint32_t rounds, void* stream,
@@ -827,7 +827,8 @@ int moshpit_engine_rounds_fused(moshpit_engine* e, int dtype, void* state, std::
     if (!state) throw std::invalid_argument("fused rounds: null state");
     check_state(dtype, state, dim, ld);
     Plane& p = *e->plane;
-    const std::uint32_t cap = fused_rounds_max(p.n);
+    const auto gcap = (std::uint32_t)std::min<std::uint64_t>(p.grid.lines(), p.n);
+    const std::uint32_t cap = fused_rounds_max(p.n, gcap);
     if (cap == 0) throw std::invalid_argument("fused rounds: too many peers for one pass");
     DeviceGuard g(p.device);
     auto s = static_cast<cudaStream_t>(stream);
@@ -835,10 +836,10 @@ int moshpit_engine_rounds_fused(moshpit_engine* e, int dtype, void* state, std::
       const std::uint32_t R = std::min(cap, rounds - done);
       e->fused.form(p, R, &e->fail, e->p, e->clock, s, active_out ? active_out + done : nullptr);
       if (dtype == MOSHPIT_F32)
-        launch_rounds_fused<float>(static_cast<float*>(state), ld, dim, (std::uint32_t)p.n,
+        launch_rounds_fused<float>(static_cast<float*>(state), ld, dim, (std::uint32_t)p.n, gcap,
                                    e->fused.dev(), R, nullptr, s);
       else
-        launch_rounds_fused<double>(static_cast<double*>(state), ld, dim, (std::uint32_t)p.n,
+        launch_rounds_fused<double>(static_cast<double*>(state), ld, dim, (std::uint32_t)p.n, gcap,
                                     e->fused.dev(), R, nullptr, s);
       p.mark_done(s);
       done += R;

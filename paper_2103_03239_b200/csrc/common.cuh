@@ -122,6 +122,8 @@ struct Grid {
     pow_drop = 1;
     for (std::uint32_t j = 0; j + 2 < d; ++j) pow_drop *= M;
   }
+  // distinct (d-1)-digit group keys, M^(d-1): a bound on any round's groups
+  std::uint64_t lines() const { return capacity / M; }
   // matchmaking.hpp:46-59, packed
   std::uint64_t initial_key(std::uint64_t cell) const {
     std::uint64_t rest = cell / M, key = 0;
@@ -303,13 +305,14 @@ struct FusedRound {
   const std::uint32_t* act = nullptr;
   const std::uint32_t* counts = nullptr;
 };
-// ... the most rounds one pass can hold for n peers (0: n too large, > ~1800) ...
-std::uint32_t fused_rounds_max(std::uint64_t n);
+// ... the most rounds one pass can hold for n peers in at most gcap groups a
+// round (0: n too large, > ~1800) ...
+std::uint32_t fused_rounds_max(std::uint64_t n, std::uint64_t gcap);
 // ... and the pass: optional kernel-3 step, then R rounds (rounds_dev: [R]
 // tables in device memory), bit-identical to kernel 3 + R - 1 kernel-2 rounds.
 template <typename T>
 void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
-                         const FusedRound* rounds_dev, std::uint32_t R,
+                         std::uint32_t gcap, const FusedRound* rounds_dev, std::uint32_t R,
                          const StepPrologue<T>* step, cudaStream_t s);
 // The Moshpit-SGD averaging step with two rounds and no failures in one pass
 // (step_kernel.cu): kernel 3's step + round 1 into shared memory, round 2 from

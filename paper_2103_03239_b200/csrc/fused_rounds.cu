@@ -33,9 +33,16 @@
 namespace mb200 {
 namespace {
 
-constexpr int kFrThreads = 512;
-constexpr int kFrTeams = 2, kFrTeamThreads = kFrThreads / kFrTeams;
-constexpr int kFrTV = 4;  // 16-byte vectors per row in a tile (64 bytes)
+#ifndef MB_FR_TV
+#define MB_FR_TV 4
+#endif
+// 2 or 3 teams of 256 threads, each with its own tile: 3 when their tiles
+// and the tables fit in shared memory (C2: 10 rounds in 21.3 ms with 3 teams
+// vs 27.1 with 2; profiles/r02/fused_rounds.md)
+constexpr int kFrTeamsMax = 3, kFrTeamThreads = 256;
+constexpr int kFrThreads = kFrTeamsMax * kFrTeamThreads;
+constexpr int kFrTV = MB_FR_TV;  // 16-byte vectors per row in a tile
+static_assert(kFrTV == 1 || kFrTV == 2 || kFrTV == 4, "tile row = 1, 2 or 4 vectors");
 constexpr std::size_t kFrSmemMax = 226 * 1024;  // 227 KB opt-in less the static reduction buffer
 
 template <typename T>
@@ -56,6 +63,7 @@ struct FrArgs {
   T* state;
   std::uint64_t ld_vec, nvec, n_tiles, dim;
   std::uint32_t n, R;
+  std::uint32_t gcap;  // >= active groups of any round (<= min(n, M^(d-1)))
   const FusedRound* rounds;  // [R] device tables
   // optional local step before round 0 (kernel 3's prologue)
   const T* curv;
@@ -117,11 +125,13 @@ __device__ __forceinline__ double2 fr_shfl_xor(unsigned mask, double2 v, int o) 
   return make_double2(__shfl_xor_sync(mask, v.x, o), __shfl_xor_sync(mask, v.y, o));
 }
 
-// Tile position of (row, vector): the 4 vectors of a row are XOR-swizzled by
-// row bits 1-2, so the 8 lanes of an LDS.128 phase reading one vector index
-// of 8 random rows spread over 8 bank groups instead of 2 (row parity).
+// Tile position of (row, vector): the kFrTV vectors of a row are XOR-swizzled
+// by the row bits above those that pick its 16-byte slot in a 128-byte bank
+// line, so the 8 lanes of an LDS.128 phase reading one vector index of 8
+// random rows spread over 8 bank groups (4 vectors: row bits 1-2; 2: bit 2).
 __device__ __forceinline__ std::uint32_t fr_pos(std::uint32_t row, std::uint32_t v) {
-  return row * kFrTV + (v ^ ((row >> 1) & 3u));
+  constexpr int sh = kFrTV == 4 ? 1 : 2;
+  return row * kFrTV + (v ^ ((row >> sh) & (std::uint32_t)(kFrTV - 1)));
 }
 __device__ __forceinline__ float4 fr_shfl(unsigned mask, float4 v, int src) {
   return make_float4(__shfl_sync(mask, v.x, src), __shfl_sync(mask, v.y, src),
@@ -162,9 +172,10 @@ __global__ void __launch_bounds__(kFrThreads, 1)
   constexpr int TC = kFrTV * W;  // columns per tile row
   extern __shared__ __align__(16) unsigned char fr_raw[];
   const std::uint32_t n = a.n, R = a.R;
-  V* const tiles = reinterpret_cast<V*>(fr_raw);  // [2][n][kFrTV]
-  std::uint32_t* const s_grp = reinterpret_cast<std::uint32_t*>(tiles + 2 * n * kFrTV);  // [R][n]: beg << 16 | count
-  std::uint32_t* const s_cnt = s_grp + (std::size_t)R * n;  // [R] active groups
+  const int teams = (int)blockDim.x / kFrTeamThreads;
+  V* const tiles = reinterpret_cast<V*>(fr_raw);  // [teams][n][kFrTV]
+  std::uint32_t* const s_grp = reinterpret_cast<std::uint32_t*>(tiles + teams * n * kFrTV);  // [R][gcap]: beg << 16 | count
+  std::uint32_t* const s_cnt = s_grp + (std::size_t)R * a.gcap;  // [R] active groups
   std::uint16_t* const s_mem = reinterpret_cast<std::uint16_t*>(s_cnt + R);  // [R][n] member rows
   const int tid = threadIdx.x;
 
@@ -172,12 +183,13 @@ __global__ void __launch_bounds__(kFrThreads, 1)
   for (std::uint32_t r = 0; r < R; ++r) {
     const FusedRound rt = a.rounds[r];
     const std::uint32_t A = rt.counts[1];
-    for (std::uint32_t i = tid; i < n; i += kFrThreads)
+    if (A > a.gcap) __trap();  // more groups than the grid has lines: a caller bug
+    for (std::uint32_t i = tid; i < n; i += blockDim.x)
       s_mem[r * n + i] = (std::uint16_t)rt.members[i];
-    for (std::uint32_t i = tid; i < A; i += kFrThreads) {
+    for (std::uint32_t i = tid; i < A; i += blockDim.x) {
       const std::uint32_t g = rt.act[i];
       const std::uint32_t beg = rt.goff[g];
-      s_grp[r * n + i] = beg << 16 | (rt.goff[g + 1] - beg);
+      s_grp[r * a.gcap + i] = beg << 16 | (rt.goff[g + 1] - beg);
     }
     if (tid == 0) s_cnt[r] = A;
   }
@@ -193,12 +205,12 @@ __global__ void __launch_bounds__(kFrThreads, 1)
   };
   V* const gvec = reinterpret_cast<V*>(a.state);
   V* const tile = tiles + (std::size_t)team * n * kFrTV;
-  __shared__ V s_ct[kFrTeams][2][kFrTV];
+  __shared__ V s_ct[kFrTeamsMax][2][kFrTV];
 
   T chk = T(0);
   double nsq = 0.0;
-  const std::uint64_t stride = (std::uint64_t)gridDim.x * kFrTeams;
-  for (std::uint64_t t = (std::uint64_t)blockIdx.x * kFrTeams + team; t < a.n_tiles; t += stride) {
+  const std::uint64_t stride = (std::uint64_t)gridDim.x * teams;
+  for (std::uint64_t t = (std::uint64_t)blockIdx.x * teams + team; t < a.n_tiles; t += stride) {
     const std::uint64_t v0 = t * kFrTV;
     for (std::uint32_t idx = ttid; idx < n * kFrTV; idx += kFrTeamThreads) {
       const std::uint32_t row = idx / kFrTV, v = idx % kFrTV;
@@ -253,21 +265,25 @@ __global__ void __launch_bounds__(kFrThreads, 1)
       team_sync();
     }
 
-    // R rounds on the tile: a quad of lanes per (active group, 16-byte
-    // vector); lane l sums leaf l of the group's tree (<= 8 members, loads
-    // independent of the adds), the quad swaps its leaf sums with shuffles,
-    // every lane joins them in the tree's order (identical ops, identical
-    // bits) and writes the mean to its own leaf's members.  Groups of more
-    // than 32: lane 0 of the quad walks the runtime tree.
+    // R rounds on the tile: 4 x kFrTV lanes per active group, lane (l, v)
+    // summing leaf l of the group's tree (<= 8 members, loads independent of
+    // the adds) over 16-byte vector v.  The kFrTV lanes of one leaf read the
+    // same member row, i.e. one contiguous row of the tile per leaf step (a
+    // phase of 8 lanes touches 2 rows instead of 8 random (row, vector) slots:
+    // fewer shared-memory bank conflicts).  The lanes of a vector swap their
+    // leaf sums with shuffles, every lane joins them in the tree's order
+    // (identical ops, identical bits) and writes the mean to its own leaf's
+    // members.  Groups of more than 32: the leaf-0 lanes walk the runtime tree.
+    constexpr std::uint32_t GL = 4 * kFrTV;  // lanes per group
     for (std::uint32_t r = 0; r < R; ++r) {
       const std::uint32_t A = s_cnt[r];
       const std::uint16_t* mem = s_mem + (std::size_t)r * n;
-      const std::uint32_t lane4 = (std::uint32_t)tid & 3u;
-      const int qbase = tid & 28;
-      const unsigned qmask = 0xfu << qbase;
-      for (std::uint32_t item = ttid; item < A * kFrTV * 4; item += kFrTeamThreads) {
-        const std::uint32_t gi = item / (kFrTV * 4), v = (item / 4) % kFrTV;
-        const std::uint32_t pk = s_grp[(std::size_t)r * n + gi];
+      const std::uint32_t leaf = ((std::uint32_t)tid / kFrTV) & 3u;
+      const int gbase = tid & (int)(32 - GL);
+      const unsigned gmask = (GL == 32 ? 0xffffffffu : ((1u << GL) - 1u)) << gbase;
+      for (std::uint32_t item = ttid; item < A * GL; item += kFrTeamThreads) {
+        const std::uint32_t gi = item / GL, v = item % kFrTV;
+        const std::uint32_t pk = s_grp[(std::size_t)r * a.gcap + gi];
         const std::uint32_t beg = pk >> 16, cnt = pk & 0xffffu;
         const std::uint16_t* m = mem + beg;
         if (cnt <= 32) {
@@ -276,7 +292,7 @@ __global__ void __launch_bounds__(kFrThreads, 1)
           std::uint32_t lb = 0, le = 0;
 #pragma unroll
           for (int l = 0; l < 4; ++l)
-            if ((std::uint32_t)l == lane4 && l < nl) {
+            if ((std::uint32_t)l == leaf && l < nl) {
               lb = b[l];
               le = b[l + 1];
             }
@@ -287,20 +303,20 @@ __global__ void __launch_bounds__(kFrThreads, 1)
             pos[k] = lb + k < le ? fr_pos(m[lb + k], v) : 0u;
             if (lb + k < le) sl = fr_vadd(sl, tile[pos[k]]);
           }
-          // leaf j's sum lives on quad lane j; every lane joins all of them
-          // in the tree's order (identical ops: identical bits on each lane)
-          const V L0 = fr_shfl(qmask, sl, qbase);
+          // leaf j's sum for vector v lives on lane gbase + j * kFrTV + v
+          const int src = gbase + (int)v;
+          const V L0 = fr_shfl(gmask, sl, src);
           V sum = L0;
           if (nl >= 2) {
-            const V L1 = fr_shfl(qmask, sl, qbase + 1);
+            const V L1 = fr_shfl(gmask, sl, src + kFrTV);
             if (nl == 2) {
               sum = fr_vadd(L0, L1);
             } else {
-              const V L2 = fr_shfl(qmask, sl, qbase + 2);
+              const V L2 = fr_shfl(gmask, sl, src + 2 * kFrTV);
               if (nl == 3) {
                 sum = fr_vadd(L0, fr_vadd(L1, L2));
               } else {
-                const V L3 = fr_shfl(qmask, sl, qbase + 3);
+                const V L3 = fr_shfl(gmask, sl, src + 3 * kFrTV);
                 sum = fr_vadd(fr_vadd(L0, L1), fr_vadd(L2, L3));
               }
             }
@@ -309,7 +325,7 @@ __global__ void __launch_bounds__(kFrThreads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             if (lb + k < le) tile[pos[k]] = mean;
-        } else if (lane4 == 0) {
+        } else if (leaf == 0) {
           auto ld = [&](std::uint32_t k) { return tile[fr_pos(m[k], v)]; };
           const V sum = pairwise_rt<V>(ld, cnt, [](V x, V y) { return fr_vadd(x, y); },
                                        fr_zero<V>());
@@ -338,20 +354,19 @@ __global__ void __launch_bounds__(kFrThreads, 1)
       __syncthreads();
       if (tid == 0 && a.noise_partial) {
         double s = 0.0;
-        for (int i = 0; i < kFrThreads / 32; ++i) s += red[i];
+        for (int i = 0; i < (int)blockDim.x / 32; ++i) s += red[i];
         a.noise_partial[blockIdx.x] = s;
       }
     }
   }
 }
 
-std::size_t fr_smem(std::uint32_t n, std::uint32_t R, std::size_t es) {
-  (void)es;
-  return (std::size_t)2 * n * kFrTV * 16 + (std::size_t)R * n * 6 + (std::size_t)R * 4 + 16;
+std::size_t fr_smem(int teams, std::uint32_t n, std::uint32_t gcap, std::uint32_t R) {
+  return (std::size_t)teams * n * kFrTV * 16 + (std::size_t)R * ((std::size_t)n * 2 + (std::size_t)gcap * 4 + 4) + 16;
 }
 
 template <typename T, bool STEP, bool NOISY>
-void launch_fr(const FrArgs<T>& a, std::size_t smem, cudaStream_t s) {
+void launch_fr(const FrArgs<T>& a, int teams, std::size_t smem, cudaStream_t s) {
   static thread_local int attr_dev = -1;
   int dev = 0;
   MB_CUDA(cudaGetDevice(&dev));
@@ -363,27 +378,29 @@ void launch_fr(const FrArgs<T>& a, std::size_t smem, cudaStream_t s) {
   int sms = 0;
   MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const unsigned grid = (unsigned)std::min<std::uint64_t>((std::uint64_t)sms, a.n_tiles);
-  rounds_fused_kernel<T, STEP, NOISY><<<grid, kFrThreads, smem, s>>>(a);
+  rounds_fused_kernel<T, STEP, NOISY><<<grid, teams * kFrTeamThreads, smem, s>>>(a);
   MB_LAUNCH_CHECK();
 }
 
 }  // namespace
 
-std::uint32_t fused_rounds_max(std::uint64_t n) {
+std::uint32_t fused_rounds_max(std::uint64_t n, std::uint64_t gcap) {
   if (n == 0 || n > 4096) return 0;
-  const std::size_t tiles = (std::size_t)2 * n * kFrTV * 16;
+  gcap = std::min(gcap, n);
+  const std::size_t tiles = (std::size_t)2 * n * kFrTV * 16;  // two teams at least
   if (tiles + 64 >= kFrSmemMax) return 0;
-  const std::size_t per = (std::size_t)n * 6 + 4;
+  const std::size_t per = (std::size_t)n * 2 + (std::size_t)gcap * 4 + 4;
   return (std::uint32_t)std::min<std::size_t>((kFrSmemMax - tiles - 16) / per, 64);
 }
 
 template <typename T>
 void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uint32_t n,
-                         const FusedRound* rounds_dev, std::uint32_t R,
+                         std::uint32_t gcap, const FusedRound* rounds_dev, std::uint32_t R,
                          const StepPrologue<T>* step, cudaStream_t s) {
   constexpr int W = FrVec<T>::W;
   if (dim == 0 || n == 0 || (R == 0 && !step)) return;
-  if (R > fused_rounds_max(n)) throw std::invalid_argument("fused rounds: tables exceed shared memory");
+  gcap = std::min(gcap, n);
+  if (R > fused_rounds_max(n, gcap)) throw std::invalid_argument("fused rounds: tables exceed shared memory");
   FrArgs<T> a{};
   a.state = state;
   a.ld_vec = ld / W;
@@ -392,8 +409,10 @@ void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uin
   a.dim = dim;
   a.n = n;
   a.R = R;
+  a.gcap = gcap;
   a.rounds = rounds_dev;
-  const std::size_t smem = fr_smem(n, R, sizeof(T));
+  const int teams = fr_smem(3, n, gcap, R) <= kFrSmemMax ? 3 : 2;
+  const std::size_t smem = fr_smem(teams, n, gcap, R);
   if (step) {
     a.curv = step->curv;
     a.tgt = step->tgt;
@@ -403,17 +422,17 @@ void launch_rounds_fused(T* state, std::uint64_t ld, std::uint64_t dim, std::uin
     a.pk = philox_keys(step->seed);
     a.nonfinite = step->nonfinite;
     a.noise_partial = step->noise_partial;
-    if (step->philox) launch_fr<T, true, true>(a, smem, s);
-    else launch_fr<T, true, false>(a, smem, s);
+    if (step->philox) launch_fr<T, true, true>(a, teams, smem, s);
+    else launch_fr<T, true, false>(a, teams, smem, s);
   } else {
-    launch_fr<T, false, false>(a, smem, s);
+    launch_fr<T, false, false>(a, teams, smem, s);
   }
 }
 
-template void launch_rounds_fused<float>(float*, std::uint64_t, std::uint64_t, std::uint32_t,
+template void launch_rounds_fused<float>(float*, std::uint64_t, std::uint64_t, std::uint32_t, std::uint32_t,
                                          const FusedRound*, std::uint32_t,
                                          const StepPrologue<float>*, cudaStream_t);
-template void launch_rounds_fused<double>(double*, std::uint64_t, std::uint64_t, std::uint32_t,
+template void launch_rounds_fused<double>(double*, std::uint64_t, std::uint64_t, std::uint32_t, std::uint32_t,
                                           const FusedRound*, std::uint32_t,
                                           const StepPrologue<double>*, cudaStream_t);
 

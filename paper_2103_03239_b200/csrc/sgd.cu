@@ -1096,15 +1096,17 @@ static int run_sgd(
               launch_two_round_step<double>(x.as<double>(), r.ld, dim, (std::uint32_t)n,
                                             r.tables.host.data(), g1n, g1, g1 + n, sd, h.s);
             plane->mark_done(h.s);
-          } else if (fused_rounds && inner <= fused_rounds_max(n)) {
+          } else if (fused_rounds &&
+                     inner <= fused_rounds_max(n, std::min<std::uint64_t>(plane->grid.lines(), n))) {
+            const auto gcap = (std::uint32_t)std::min<std::uint64_t>(plane->grid.lines(), n);
             // the step and all `inner` rounds in one pass over the state
             // (temporal blocking): bit-identical to kernel 3 + kernel 2
             r.tables.form(*plane, inner, nullptr, 0.0, avg, h.s);
             if (dtype == MOSHPIT_F32)
-              launch_rounds_fused<float>(x.as<float>(), r.ld, dim, (std::uint32_t)n,
+              launch_rounds_fused<float>(x.as<float>(), r.ld, dim, (std::uint32_t)n, gcap,
                                          r.tables.dev(), inner, &sf, h.s);
             else
-              launch_rounds_fused<double>(x.as<double>(), r.ld, dim, (std::uint32_t)n,
+              launch_rounds_fused<double>(x.as<double>(), r.ld, dim, (std::uint32_t)n, gcap,
                                           r.tables.dev(), inner, &sd, h.s);
             plane->mark_done(h.s);
           } else {
