@@ -92,6 +92,7 @@ struct moshpit_engine {
   std::uint64_t diag_dim = 0;
   DeviceBuffer ref, mean, sq, part, part2, log;  // log: [0] initial, then (dist, drift) pairs
   DeviceBuffer rep, rlist, rcount;               // representatives of the last round
+  DeviceBuffer colsum;                          // launch_colmean_exactsum scratch
   RoundTables fused;                             // tables of moshpit_engine_rounds_fused
   std::uint64_t log_cap = 0, log_n = 0;
   std::unique_ptr<StreamHolder> aux;
@@ -936,8 +937,17 @@ void engine_diag(moshpit_engine* e, const T* x, std::uint64_t ld, std::uint64_t 
     launch_distortion<T>(x, n, ld, dim, e->ref.as<double>(), e->sq.as<double>(),
                          e->part.as<double>(), dist_slot, exact, s, reps);
   if (drift_slot) {
-    launch_colmean<T, double>(x, n, ld, dim, reps ? reps->rep : nullptr, e->mean.as<double>(),
-                              e->aux->s, true);
+    bool done = false;
+    if constexpr (std::is_same<T, float>::value) {
+      if (reps && reps->rep) {
+        e->colsum.resize(colsum_scratch_bytes(n, dim));
+        done = launch_colmean_exactsum(x, n, ld, dim, reps->rep, e->mean.as<double>(),
+                                       e->colsum.ptr, e->aux->s);
+      }
+    }
+    if (!done)
+      launch_colmean<T, double>(x, n, ld, dim, reps ? reps->rep : nullptr, e->mean.as<double>(),
+                                e->aux->s, true);
     launch_drift(e->mean.as<double>(), e->ref.as<double>(), dim, e->part2.as<double>(),
                  drift_slot, exact, e->aux->s);
     MB_CUDA(cudaEventRecord(e->ev_join, e->aux->s));

@@ -370,6 +370,13 @@ template <typename T, typename Acc>
 void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
                     std::uint64_t dim, const std::uint32_t* rows, Acc* out,
                     cudaStream_t s, bool rows_optional = false);
+// fp32 column means over the representative map by exact sums of the distinct
+// rows (bit-identical to the tree when the column's exponent range allows,
+// the tree for the other columns); false = not applicable, nothing launched.
+std::size_t colsum_scratch_bytes(std::uint64_t n, std::uint64_t dim);
+bool launch_colmean_exactsum(const float* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                             const std::uint32_t* rep, double* out, void* scratch,
+                             cudaStream_t s);
 template <typename T>
 void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq_scratch,

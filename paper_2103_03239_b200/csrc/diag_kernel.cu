@@ -1066,6 +1066,161 @@ void launch_colmean(const T* x, std::uint64_t n, std::uint64_t ld,
   MB_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------------------
+// fp32 column means over the representative map by EXACT sums.  The tree's
+// leaves are fp32 values widened to fp64; every partial sum of them (any
+// subset, any order) is an integer multiple of 2^lo (lo: the smallest ulp
+// exponent among the column's nonzero values) bounded by n * 2^hi (hi: the
+// largest |value| < 2^hi), so when hi + ceil(log2 n) - lo <= 53 every add of
+// the reference tree (core.hpp:72-81) is exact and the tree's result equals
+// the exact sum -- which the sum over the DISTINCT rows with their
+// multiplicities (count * value is exact in fp64) also computes.  Same bits,
+// but each distinct row is read once (C2 after a round: ~300 of 1024) instead
+// of a tree leaf per row.  Columns that fail the bound (or hold Inf/NaN) are
+// listed and run the tree itself.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void cs_mult(const std::uint32_t* __restrict__ rep, std::uint64_t n,
+                        std::uint32_t* __restrict__ mult) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&mult[rep[i]], 1u);
+}
+__global__ void cs_compact(const std::uint32_t* __restrict__ mult, std::uint64_t n,
+                           std::uint32_t* __restrict__ dl, std::uint32_t* __restrict__ dm,
+                           std::uint32_t* __restrict__ cnt) {
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (std::uint64_t)gridDim.x * blockDim.x)
+    if (mult[i]) {
+      const std::uint32_t k = atomicAdd(cnt, 1u);
+      dl[k] = (std::uint32_t)i;
+      dm[k] = mult[i];
+    }
+}
+__device__ __forceinline__ void cs_range(float f, int& lo, int& hi, bool& bad) {
+  const std::uint32_t u = __float_as_uint(f);
+  const int E = (int)((u >> 23) & 0xffu);
+  if (E == 255) bad = true;
+  else if (E != 0) { lo = min(lo, E - 150); hi = max(hi, E - 126); }
+  else if (u & 0x7fffffu) { lo = min(lo, -149); hi = max(hi, -126); }
+}
+__global__ void __launch_bounds__(256)
+    cs_sum(const float4* __restrict__ x, std::uint64_t ldv, std::uint64_t nv, std::uint64_t dim,
+           std::uint64_t n, int lgn, const std::uint32_t* __restrict__ dl,
+           const std::uint32_t* __restrict__ dm, const std::uint32_t* __restrict__ cnt,
+           double* __restrict__ out, std::uint32_t* __restrict__ flagged,
+           std::uint32_t* __restrict__ fcnt) {
+  const std::uint64_t cv = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x;
+  if (cv >= nv) return;
+  const std::uint32_t L = *cnt;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int lo = 1 << 20, hi = -(1 << 20);
+  bool bad = false;
+#pragma unroll 8
+  for (std::uint32_t k = 0; k < L; ++k) {
+    const float4 v = __ldg(x + (std::uint64_t)dl[k] * ldv + cv);
+    const double m = (double)dm[k];
+    cs_range(v.x, lo, hi, bad);
+    cs_range(v.y, lo, hi, bad);
+    cs_range(v.z, lo, hi, bad);
+    cs_range(v.w, lo, hi, bad);
+    a0 = __dadd_rn(a0, __dmul_rn(m, (double)v.x));
+    a1 = __dadd_rn(a1, __dmul_rn(m, (double)v.y));
+    a2 = __dadd_rn(a2, __dmul_rn(m, (double)v.z));
+    a3 = __dadd_rn(a3, __dmul_rn(m, (double)v.w));
+  }
+  if (bad || hi + lgn - lo > 53) {
+    flagged[atomicAdd(fcnt, 1u)] = (std::uint32_t)cv;
+    return;
+  }
+  const double a[4] = {a0, a1, a2, a3};
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+    if (cv * 4 + w < dim) out[cv * 4 + w] = __ddiv_rn(a[w], (double)n);
+}
+// the listed column vectors: the reference tree over the rows (colmean_kernel's)
+__global__ void cs_fix(const float* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                       std::uint64_t dim, const std::uint32_t* __restrict__ rep,
+                       const std::uint32_t* __restrict__ flagged,
+                       const std::uint32_t* __restrict__ fcnt, double* __restrict__ out) {
+  const std::uint64_t items = (std::uint64_t)*fcnt * 4;
+  for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < items;
+       i += (std::uint64_t)gridDim.x * blockDim.x) {
+    const std::uint64_t j = (std::uint64_t)flagged[i / 4] * 4 + i % 4;
+    if (j >= dim) continue;
+    auto ld_fn = [&](std::uint32_t r) -> double { return (double)x[(std::uint64_t)rep[r] * ld + j]; };
+    const double t = pairwise_rt<double>(ld_fn, (std::uint32_t)n,
+                                         [](double a, double b) { return __dadd_rn(a, b); }, 0.0);
+    out[j] = __ddiv_rn(t, (double)n);
+  }
+}
+
+// n = 8 * 2^K >= 256: a warp per listed column -- lane l evaluates the
+// aligned subtree over rows [l n/32, (l+1) n/32) (the reference tree splits
+// at n/2 down to 8-row blocks, so these are its subtrees), then five xor
+// shuffle levels join them pairwise: the tree's own adds, 32 lanes deep.
+__global__ void cs_fix_warp(const float* __restrict__ x, std::uint64_t n, std::uint64_t ld,
+                            std::uint64_t dim, const std::uint32_t* __restrict__ rep,
+                            const std::uint32_t* __restrict__ flagged,
+                            const std::uint32_t* __restrict__ fcnt, double* __restrict__ out) {
+  const std::uint64_t items = (std::uint64_t)*fcnt * 4;
+  const std::uint32_t lane = threadIdx.x & 31u, c = (std::uint32_t)(n / 32);
+  const std::uint64_t warps = (std::uint64_t)gridDim.x * (blockDim.x / 32);
+  for (std::uint64_t i = (blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x) / 32; i < items;
+       i += warps) {
+    const std::uint64_t j = (std::uint64_t)flagged[i / 4] * 4 + i % 4;
+    if (j >= dim) continue;  // warp-uniform
+    const std::uint32_t base = lane * c;
+    auto ld_fn = [&](std::uint32_t r) -> double {
+      return (double)x[(std::uint64_t)rep[base + r] * ld + j];
+    };
+    double v = pairwise_rt<double>(ld_fn, c, [](double a, double b) { return __dadd_rn(a, b); },
+                                   0.0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) out[j] = __ddiv_rn(v, (double)n);
+  }
+}
+
+}  // namespace
+
+std::size_t colsum_scratch_bytes(std::uint64_t n, std::uint64_t dim) {
+  return (3 * n + 4 + (dim + 3) / 4) * 4 + 64;
+}
+
+bool launch_colmean_exactsum(const float* x, std::uint64_t n, std::uint64_t ld, std::uint64_t dim,
+                             const std::uint32_t* rep, double* out, void* scratch,
+                             cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("MOSHPIT_COLSUM_EXACT");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || !rep || !scratch || n == 0 || dim == 0 || ld % 4 != 0 ||
+      reinterpret_cast<std::uintptr_t>(x) % 16 != 0 || n > (1u << 24))
+    return false;
+  int lgn = 0;
+  while ((1ull << lgn) < n) ++lgn;
+  auto* u = static_cast<std::uint32_t*>(scratch);
+  std::uint32_t *mult = u, *dl = u + n, *dm = u + 2 * n, *cnt = u + 3 * n, *fcnt = cnt + 1,
+                *flagged = cnt + 4;
+  MB_CUDA(cudaMemsetAsync(mult, 0, n * 4, s));
+  MB_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
+  const unsigned gb = (unsigned)std::min<std::uint64_t>((n + 255) / 256, 1184);
+  cs_mult<<<gb, 256, 0, s>>>(rep, n, mult);
+  cs_compact<<<gb, 256, 0, s>>>(mult, n, dl, dm, cnt);
+  const std::uint64_t nv = (dim + 3) / 4;
+  cs_sum<<<(unsigned)((nv + 255) / 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x), ld / 4,
+                                                     nv, dim, n, lgn, dl, dm, cnt, out, flagged,
+                                                     fcnt);
+  if (n >= 256 && n % 8 == 0 && (((n / 8) & (n / 8 - 1)) == 0))
+    cs_fix_warp<<<1184, 128, 0, s>>>(x, n, ld, dim, rep, flagged, fcnt, out);
+  else
+    cs_fix<<<1184, 128, 0, s>>>(x, n, ld, dim, rep, flagged, fcnt, out);
+  MB_LAUNCH_CHECK();
+  return true;
+}
+
 template <typename T>
 void launch_distortion(const T* x, std::uint64_t n, std::uint64_t ld,
                        std::uint64_t dim, const double* ref, double* sq,

@@ -671,3 +671,32 @@ def test_engine_rounds_record_equals_run_moshpit(mb, torch, f64, diag, M, d, n, 
     assert bits_equal(np.array(dist_a), np.array(want.distortion))
     assert bits_equal(np.array(drift_a), np.array(want.mean_drift))
     assert bits_equal(np.ascontiguousarray(x[:, :dim].cpu().numpy()), want.vectors)
+
+
+@pytest.mark.parametrize("diag", ["fast", "exact"])
+def test_engine_record_exact_column_sums_fallback(mb, torch, diag):
+    """fp32 column means by exact sums of the distinct rows (launch_colmean_
+    exactsum) equal the reference tree's bits: columns whose exponent range
+    fits take the exact sum, columns spanning 40 binades, tiny/huge mixes and
+    subnormals take the tree (the fallback list) -- all against run_moshpit's
+    tree on host buffers."""
+    M, d, n, p, R, dim = 32, 2, 1024, 0.01, 3, 1000
+    x = torch.zeros((n, dim), dtype=torch.float32, device="cuda")
+    mb.fill_synthetic(x, INIT_SEED, dim=dim)
+    i = torch.arange(n, device="cuda", dtype=torch.float32)
+    x[:, 5] *= torch.pow(2.0, (i % 40) - 20)          # 40 binades: tree
+    x[:, 6] = torch.where(i % 97 == 0, x[:, 6] * 1e-30, x[:, 6])  # tiny among O(1): tree
+    x[:, 7] = torch.where(i % 13 == 0, x[:, 7] * 1e-40, x[:, 7])  # subnormals: tree
+    x[:, 8] *= torch.pow(2.0, (i % 8) - 4)            # 8 binades: exact sum
+    host = np.ascontiguousarray(x.cpu().numpy())
+    eng = mb.Engine(mb.GridConfig(M, d, R), n, mb.FailureModel(p), mb.Rng(7), device=0)
+    eng.set_reference(x, diagnostics=diag, dim=dim)
+    eng.rounds_record(x, R, dim=dim)
+    init_a, dist_a, drift_a = eng.report()
+    eng.close()
+    torch.cuda.synchronize()
+    want = mb.run_moshpit(mb.GridConfig(M, d, 1), host, mb.FailureModel(p), mb.Rng(7), R,
+                          diagnostics=diag, return_vectors=True)
+    assert bits_equal(np.array(dist_a), np.array(want.distortion))
+    assert bits_equal(np.array(drift_a), np.array(want.mean_drift))
+    assert bits_equal(np.ascontiguousarray(x.cpu().numpy()), want.vectors)
